@@ -1,0 +1,110 @@
+/* condmpc_cuda.h — C ABI of the B200 condensed-space IPM hot path.
+ *
+ * Drop-in boundary for the per-iteration body of condmpc::ipm::solve
+ * (/root/reference/proj/src/ipm.cpp:160-268). All matrices are FP64, column-major
+ * with leading dimension = rows (Eigen::MatrixXd layout,
+ * proj/include/condmpc/types.hpp:10-11). Pointers are borrowed for the call.
+ * Return codes: 0 ok, 1 not positive definite (pivot reported), <0 error (message in
+ * cmpc_last_error(), thread-local). One context = one QP = one CUDA stream; contexts
+ * are independent, so concurrent solves on different threads are safe
+ * (proj/src/verify.cpp:104-111 runs ipm::solve concurrently).
+ */
+#ifndef CONDMPC_CUDA_H
+#define CONDMPC_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CMPC_OK 0
+#define CMPC_NOT_PD 1
+#define CMPC_ERR_DIM (-1)
+#define CMPC_ERR_ARG (-2)
+#define CMPC_ERR_CUDA (-3)
+
+typedef struct cmpc_ctx cmpc_ctx;
+
+int cmpc_abi_version(void);
+const char* cmpc_last_error(void);
+/* kernels launched by this thread so far (all entry points) */
+long long cmpc_launch_count(void);
+
+/* context = the device-resident DenseQp + IpmState of one solve */
+int cmpc_ctx_create(cmpc_ctx** out, int device);
+void cmpc_ctx_destroy(cmpc_ctx* ctx);
+
+/* Load DenseQp{H, h, h0, J, d} (proj/include/condmpc/reduction.hpp:25-33).
+ * on_device = 0: host pointers (copied H2D); 1: device pointers (copied D2D).
+ * Runs the exact structure analysis of J (distinct rows up to sign, prefix widths). */
+int cmpc_load_qp(cmpc_ctx* ctx, int64_t n, int64_t m, const double* H, const double* h, double h0,
+                 const double* J, const double* d, int on_device);
+/* out[6] = n, m, prototypes, SYRK prototypes, singleton prototypes, SYRK work units */
+int cmpc_qp_info(cmpc_ctx* ctx, int64_t* out);
+/* Replace h, h0, d of a loaded QP (refresh_initial_state, proj/src/reduction.cpp:270-280) */
+int cmpc_update_qp_affine(cmpc_ctx* ctx, const double* h, double h0, const double* d, int on_device);
+
+/* IpmState (proj/include/condmpc/ipm.hpp:18-25); host pointers, any may be NULL on get */
+int cmpc_set_state(cmpc_ctx* ctx, const double* v, const double* s, const double* lambda,
+                   const double* z, double mu);
+int cmpc_get_state(cmpc_ctx* ctx, double* v, double* s, double* lambda, double* z);
+
+/* compute_residuals (ipm.cpp:46-70): r1 (n), r2, r3 (m), kkt error; outputs nullable */
+int cmpc_compute_residuals(cmpc_ctx* ctx, double* r1, double* r2, double* r3, double* kkt);
+int cmpc_set_residuals(cmpc_ctx* ctx, const double* r1, const double* r2, const double* r3);
+/* assemble_condensed (ipm.cpp:72-77): M = H + J' diag(sigma) J (full symmetric, n x n).
+ * sigma NULL = z./s of the current state. M may be NULL (keeps it on the device). */
+int cmpc_assemble_condensed(cmpc_ctx* ctx, const double* sigma, double* M);
+/* factorize the device M + delta I (ReferenceBackend::factorize, dense_linalg.cpp:59-77);
+ * returns CMPC_NOT_PD with *pivot = first failing pivot (0-based) */
+int cmpc_factorize_condensed(cmpc_ctx* ctx, double delta, int64_t* pivot);
+int cmpc_get_factor(cmpc_ctx* ctx, double* L);
+int cmpc_set_factor(cmpc_ctx* ctx, const double* L);
+/* step_directions (ipm.cpp:79-103) with the current factor, then fraction_to_boundary
+ * (ipm.cpp:105-116): alpha[2] = {alpha_max, alpha_z}. Outputs nullable. */
+int cmpc_step_directions(cmpc_ctx* ctx, double tau, double* pv, double* ps, double* plambda,
+                         double* pz, double* alpha);
+int cmpc_set_directions(cmpc_ctx* ctx, const double* pv, const double* ps, const double* plambda,
+                        const double* pz);
+/* line_search (ipm.cpp:118-144) on the current directions; *trial = accepted j or -1 */
+int cmpc_line_search(cmpc_ctx* ctx, double alpha_max, double armijo_eta, double* alpha, int* trial);
+/* merit (ipm.cpp:25-32) at (v + alpha pv, s + alpha ps) */
+int cmpc_merit(cmpc_ctx* ctx, double alpha, double rho, double* phi);
+/* v, s, lambda += alpha p; z += alpha_z pz (ipm.cpp:240-243) */
+int cmpc_apply_step(cmpc_ctx* ctx, double alpha, double alpha_z);
+int cmpc_dense_objective(cmpc_ctx* ctx, double* obj);
+
+/* ipm::solve (ipm.cpp:160-268) on the loaded QP.
+ * opts[5] = tol, mu_init, kappa_mu, tau, armijo_eta.
+ * out_scalars[10] = status (0 converged, 1 max_iter, 2 factorization_failure,
+ *   3 line_search_failure), iter, kkt_error, objective, total_seconds, linalg_seconds,
+ *   device_seconds, launches, syncs, trials.
+ * log(user, rec[8]) per accepted step: iter, mu, alpha, alpha_z, kkt_error, objective,
+ *   delta, trial (IterationRecord, ipm.hpp:41-49, plus the shift and trial index).
+ * inspect(...) per iteration before the line search (IterationInspection, ipm.hpp:53-58);
+ *   pointers valid only during the callback. */
+typedef void (*cmpc_log_fn)(void* user, const double* rec);
+typedef void (*cmpc_inspect_fn)(void* user, const double* v, const double* s, const double* lambda,
+                                const double* z, double mu, const double* r1, const double* r2,
+                                const double* r3, double kkt, const double* pv, const double* ps,
+                                const double* plambda, const double* pz, double delta);
+int cmpc_solve(cmpc_ctx* ctx, const double* opts, int64_t max_iter, double* v, double* s,
+               double* lambda, double* z, double* out_scalars, cmpc_log_fn log,
+               cmpc_inspect_fn inspect, void* user);
+
+/* Stand-alone dense linear algebra (the reference's linalg plug point,
+ * proj/include/condmpc/dense_linalg.hpp:37-59), host buffers in and out. */
+int cmpc_gram_weighted(int device, int64_t m, int64_t n, const double* J, const double* sigma,
+                       double* G);
+int cmpc_cholesky(int device, int64_t n, const double* M, double* L, int64_t* pivot);
+int cmpc_cholesky_solve(int device, int64_t n, const double* L, const double* b, double* x);
+/* fraction_to_boundary (ipm.cpp:105-116) on host vectors: out[2] = {alpha, alpha_z} */
+int cmpc_fraction_to_boundary(int device, int64_t m, const double* s, const double* ps,
+                              const double* z, const double* pz, double tau, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CONDMPC_CUDA_H */

@@ -1,0 +1,447 @@
+// C ABI (include/condmpc_cuda.h): context lifecycle, QP upload, per-step entry points and
+// the stand-alone linear algebra of the reference's plug point.
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/condmpc_cuda.h"
+#include "internal.cuh"
+
+namespace cmpc {
+thread_local long long g_launches = 0;
+thread_local std::string g_error;
+
+// host loop (ipm_host.cpp)
+int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v, double* s, double* lam,
+               double* z, double* out, cmpc_log_fn log, cmpc_inspect_fn inspect, void* user);
+int line_search_host(Ctx& c, double alpha_max, double eta, double* alpha, int* ntrials);
+double merit_host(const Packet& A, double vhv, double hv, double sum_log, double sum_abs,
+                  double mu, double rho, bool has_rows);
+}  // namespace cmpc
+
+using namespace cmpc;
+
+struct cmpc_ctx {
+  Ctx c;
+};
+
+namespace {
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    return f();
+  } catch (const DimError& e) {
+    g_error = e.what();
+    return CMPC_ERR_DIM;
+  } catch (const CudaError& e) {
+    g_error = e.what();
+    return CMPC_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return CMPC_ERR_ARG;
+  }
+}
+
+void sync(Ctx& c) { CMPC_CUDA(cudaStreamSynchronize(c.stream)); }
+
+void d2h(Ctx& c, double* dst, const double* src, int64_t count) {
+  if (dst && count > 0)
+    CMPC_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * count, cudaMemcpyDeviceToHost, c.stream));
+}
+void h2d(Ctx& c, double* dst, const double* src, int64_t count) {
+  if (src && count > 0)
+    CMPC_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * count, cudaMemcpyHostToDevice, c.stream));
+}
+
+void read_packet(Ctx& c) {
+  CMPC_CUDA(cudaMemcpyAsync(c.pk_host, c.pk, sizeof(Packet), cudaMemcpyDeviceToHost, c.stream));
+  sync(c);
+}
+
+void release_qp(Ctx& c) {
+  vec_free(c);
+  syrk_free(c);
+  free_structure(c);
+  for (double* p : {c.H, c.h, c.d}) if (p) cudaFree(p);
+  if (c.J && c.owns_J) cudaFree(c.J);
+  c.H = c.h = c.J = c.d = nullptr;
+  c.n = c.m = 0;
+}
+
+void require_loaded(Ctx& c) {
+  if (!c.pk) throw DimError("no QP loaded on this context");
+}
+
+}  // namespace
+
+extern "C" {
+
+int cmpc_abi_version(void) { return 1; }
+const char* cmpc_last_error(void) { return g_error.c_str(); }
+long long cmpc_launch_count(void) { return g_launches; }
+
+int cmpc_ctx_create(cmpc_ctx** out, int device) {
+  return guard([&] {
+    auto* x = new cmpc_ctx;
+    x->c.device = device;
+    CMPC_CUDA(cudaSetDevice(device));
+    CMPC_CUDA(cudaStreamCreateWithFlags(&x->c.stream, cudaStreamNonBlocking));
+    CMPC_CUDA(cudaEventCreate(&x->c.ev0));
+    CMPC_CUDA(cudaEventCreate(&x->c.ev1));
+    *out = x;
+    return CMPC_OK;
+  });
+}
+
+void cmpc_ctx_destroy(cmpc_ctx* x) {
+  if (!x) return;
+  cudaSetDevice(x->c.device);
+  cudaStreamSynchronize(x->c.stream);
+  release_qp(x->c);
+  cudaEventDestroy(x->c.ev0);
+  cudaEventDestroy(x->c.ev1);
+  cudaStreamDestroy(x->c.stream);
+  delete x;
+}
+
+int cmpc_load_qp(cmpc_ctx* x, int64_t n, int64_t m, const double* H, const double* h, double h0,
+                 const double* J, const double* d, int on_device) {
+  return guard([&] {
+    Ctx& c = x->c;
+    if (n < 0 || m < 0) throw DimError("negative dimensions");
+    if (m > (int64_t(1) << 29) || n > (int64_t(1) << 24)) throw DimError("QP too large");
+    CMPC_CUDA(cudaSetDevice(c.device));
+    release_qp(c);
+    c.n = n;
+    c.m = m;
+    c.h0 = h0;
+    const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CMPC_CUDA(cudaMalloc(&c.H, sizeof(double) * std::max<int64_t>(1, n * n)));
+    CMPC_CUDA(cudaMalloc(&c.h, sizeof(double) * std::max<int64_t>(1, n)));
+    CMPC_CUDA(cudaMalloc(&c.J, sizeof(double) * std::max<int64_t>(1, m * n)));
+    CMPC_CUDA(cudaMalloc(&c.d, sizeof(double) * std::max<int64_t>(1, m)));
+    c.owns_J = true;
+    if (n * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.H, H, sizeof(double) * n * n, kind, c.stream));
+    if (n > 0) CMPC_CUDA(cudaMemcpyAsync(c.h, h, sizeof(double) * n, kind, c.stream));
+    if (m * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.J, J, sizeof(double) * m * n, kind, c.stream));
+    if (m > 0) CMPC_CUDA(cudaMemcpyAsync(c.d, d, sizeof(double) * m, kind, c.stream));
+    analyze_structure(c);
+    // the dense J is not read again: every product goes through P
+    cudaFree(c.J);
+    c.J = nullptr;
+    syrk_plan(c);
+    vec_alloc(c);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_qp_info(cmpc_ctx* x, int64_t* out) {
+  const Ctx& c = x->c;
+  out[0] = c.n;
+  out[1] = c.m;
+  out[2] = c.p;
+  out[3] = c.ps;
+  out[4] = c.pz;
+  out[5] = c.nunits;
+  return CMPC_OK;
+}
+
+int cmpc_update_qp_affine(cmpc_ctx* x, const double* h, double h0, const double* d, int on_device) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (h && c.n > 0) CMPC_CUDA(cudaMemcpyAsync(c.h, h, sizeof(double) * c.n, kind, c.stream));
+    if (d && c.m > 0) CMPC_CUDA(cudaMemcpyAsync(c.d, d, sizeof(double) * c.m, kind, c.stream));
+    c.h0 = h0;
+    CMPC_CUDA(cudaMemsetAsync(c.hmax, 0, sizeof(double), c.stream));
+    vec_free(c);
+    vec_alloc(c);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_set_state(cmpc_ctx* x, const double* v, const double* s, const double* lam,
+                   const double* z, double mu) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    h2d(c, c.v, v, c.n);
+    h2d(c, c.s, s, c.m);
+    h2d(c, c.lam, lam, c.m);
+    h2d(c, c.z, z, c.m);
+    c.mu = mu;
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_get_state(cmpc_ctx* x, double* v, double* s, double* lam, double* z) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    d2h(c, v, c.v, c.n);
+    d2h(c, s, c.s, c.m);
+    d2h(c, lam, c.lam, c.m);
+    d2h(c, z, c.z, c.m);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_compute_residuals(cmpc_ctx* x, double* r1, double* r2, double* r3, double* kkt) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    launch_residuals(c);
+    d2h(c, r1, c.r1, c.n);
+    d2h(c, r2, c.r2, c.m);
+    d2h(c, r3, c.r3, c.m);
+    read_packet(c);
+    if (kkt) *kkt = c.pk_host->kkt;
+    return CMPC_OK;
+  });
+}
+
+int cmpc_set_residuals(cmpc_ctx* x, const double* r1, const double* r2, const double* r3) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    h2d(c, c.r1, r1, c.n);
+    h2d(c, c.r2, r2, c.m);
+    h2d(c, c.r3, r3, c.m);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_assemble_condensed(cmpc_ctx* x, const double* sigma, double* M) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    if (sigma && c.m > 0) h2d(c, c.sigma, sigma, c.m);
+    launch_prepare_step(c, sigma ? c.sigma : nullptr);
+    launch_condense(c, true);
+    d2h(c, M, c.M, c.n * c.n);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_factorize_condensed(cmpc_ctx* x, double delta, int64_t* pivot) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    launch_cholesky(c, c.M, c.L, delta);
+    read_packet(c);
+    if (c.pk_host->info != 0) {
+      if (pivot) *pivot = c.pk_host->info - 1;
+      g_error = "cholesky failed: matrix not positive definite at pivot " +
+                std::to_string(c.pk_host->info - 1);
+      return CMPC_NOT_PD;
+    }
+    return CMPC_OK;
+  });
+}
+
+int cmpc_get_factor(cmpc_ctx* x, double* L) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    d2h(c, L, c.L, c.n * c.n);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_set_factor(cmpc_ctx* x, const double* L) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    h2d(c, c.L, L, c.n * c.n);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_step_directions(cmpc_ctx* x, double tau, double* pv, double* ps, double* pl, double* pz,
+                         double* alpha) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    if (!(tau > 0.0 && tau < 1.0)) throw DimError("tau must lie in (0,1)");
+    launch_prepare_step(c, nullptr);
+    launch_rhs(c);
+    launch_chol_solve(c, c.L, c.rhs, c.pv);
+    launch_recover(c, tau);
+    d2h(c, pv, c.pv, c.n);
+    d2h(c, ps, c.ps_, c.m);
+    d2h(c, pl, c.pl, c.m);
+    d2h(c, pz, c.pzd, c.m);
+    read_packet(c);
+    if (alpha) {
+      alpha[0] = std::min(1.0, c.pk_host->alpha_s_min);
+      alpha[1] = std::min(1.0, c.pk_host->alpha_z_min);
+    }
+    return CMPC_OK;
+  });
+}
+
+int cmpc_set_directions(cmpc_ctx* x, const double* pv, const double* ps, const double* pl,
+                        const double* pz) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    h2d(c, c.pv, pv, c.n);
+    h2d(c, c.ps_, ps, c.m);
+    h2d(c, c.pl, pl, c.m);
+    h2d(c, c.pzd, pz, c.m);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_line_search(cmpc_ctx* x, double alpha_max, double eta, double* alpha, int* trial) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    if (!(alpha_max > 0.0 && alpha_max <= 1.0)) throw DimError("alpha_max must lie in (0,1]");
+    launch_residuals(c);
+    launch_ls_pieces(c);
+    read_packet(c);
+    int nt = 0;
+    const int j = line_search_host(c, alpha_max, eta, alpha, &nt);
+    if (trial) *trial = j;
+    return CMPC_OK;
+  });
+}
+
+int cmpc_merit(cmpc_ctx* x, double alpha, double rho, double* phi) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    launch_trial(c, alpha, false);
+    read_packet(c);
+    const Packet& T = *c.pk_host;
+    *phi = merit_host(T, T.t_vHv, T.t_hv, T.t_sum_log, T.t_sum_abs, c.mu, rho, c.m > 0);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_apply_step(cmpc_ctx* x, double alpha, double alpha_z) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    launch_update(c, alpha, alpha_z);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_dense_objective(cmpc_ctx* x, double* obj) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    launch_residuals(c);
+    read_packet(c);
+    *obj = c.pk_host->objective;
+    return CMPC_OK;
+  });
+}
+
+int cmpc_solve(cmpc_ctx* x, const double* opts, int64_t max_iter, double* v, double* s,
+               double* lam, double* z, double* out, cmpc_log_fn log, cmpc_inspect_fn inspect,
+               void* user) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    CMPC_CUDA(cudaSetDevice(c.device));
+    return solve_loop(c, opts, max_iter, v, s, lam, z, out, log, inspect, user);
+  });
+}
+
+// ---------------------------------------------------------------- stand-alone linalg
+int cmpc_gram_weighted(int device, int64_t m, int64_t n, const double* J, const double* sigma,
+                       double* G) {
+  cmpc_ctx* x = nullptr;
+  int rc = cmpc_ctx_create(&x, device);
+  if (rc) return rc;
+  rc = guard([&] {
+    std::vector<double> zeros(size_t(std::max<int64_t>(1, n * n)), 0.0), d(size_t(std::max<int64_t>(1, m)), 0.0);
+    int r = cmpc_load_qp(x, n, m, zeros.data(), zeros.data(), 0.0, J, d.data(), 0);
+    if (r) return r;
+    return cmpc_assemble_condensed(x, sigma, G);
+  });
+  cmpc_ctx_destroy(x);
+  return rc;
+}
+
+int cmpc_cholesky(int device, int64_t n, const double* M, double* L, int64_t* pivot) {
+  cmpc_ctx* x = nullptr;
+  int rc = cmpc_ctx_create(&x, device);
+  if (rc) return rc;
+  rc = guard([&] {
+    std::vector<double> zeros(size_t(std::max<int64_t>(1, n)), 0.0);
+    int r = cmpc_load_qp(x, n, 0, M, zeros.data(), 0.0, nullptr, nullptr, 0);
+    if (r) return r;
+    Ctx& c = x->c;
+    CMPC_CUDA(cudaMemcpyAsync(c.M, M, sizeof(double) * n * n, cudaMemcpyHostToDevice, c.stream));
+    r = cmpc_factorize_condensed(x, 0.0, pivot);
+    if (r == CMPC_OK) r = cmpc_get_factor(x, L);
+    return r;
+  });
+  cmpc_ctx_destroy(x);
+  return rc;
+}
+
+int cmpc_fraction_to_boundary(int device, int64_t m, const double* s, const double* ps,
+                              const double* z, const double* pz, double tau, double* out) {
+  return guard([&] {
+    if (!(tau > 0.0 && tau < 1.0)) throw DimError("tau must lie in (0,1)");
+    CMPC_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    CMPC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    double* buf = nullptr;
+    const int64_t mm = std::max<int64_t>(m, 1);
+    CMPC_CUDA(cudaMalloc(&buf, sizeof(double) * (4 * mm + 2)));
+    const double* src[4] = {s, ps, z, pz};
+    for (int k = 0; k < 4; ++k)
+      if (m > 0)
+        CMPC_CUDA(cudaMemcpyAsync(buf + k * mm, src[k], sizeof(double) * m, cudaMemcpyHostToDevice, st));
+    launch_fraction_to_boundary(st, m, buf, buf + mm, buf + 2 * mm, buf + 3 * mm, tau, buf + 4 * mm);
+    double r[2];
+    CMPC_CUDA(cudaMemcpyAsync(r, buf + 4 * mm, sizeof(r), cudaMemcpyDeviceToHost, st));
+    CMPC_CUDA(cudaStreamSynchronize(st));
+    cudaFree(buf);
+    cudaStreamDestroy(st);
+    out[0] = std::min(1.0, r[0]);
+    out[1] = std::min(1.0, r[1]);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_cholesky_solve(int device, int64_t n, const double* L, const double* b, double* xout) {
+  cmpc_ctx* x = nullptr;
+  int rc = cmpc_ctx_create(&x, device);
+  if (rc) return rc;
+  rc = guard([&] {
+    std::vector<double> zeros(size_t(std::max<int64_t>(1, n * n)), 0.0);
+    int r = cmpc_load_qp(x, n, 0, zeros.data(), zeros.data(), 0.0, nullptr, nullptr, 0);
+    if (r) return r;
+    Ctx& c = x->c;
+    h2d(c, c.L, L, n * n);
+    h2d(c, c.rhs, b, n);
+    launch_chol_solve(c, c.L, c.rhs, c.pv);
+    d2h(c, xout, c.pv, n);
+    sync(c);
+    return CMPC_OK;
+  });
+  cmpc_ctx_destroy(x);
+  return rc;
+}
+
+}  // extern "C"

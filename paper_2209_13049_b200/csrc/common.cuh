@@ -1,0 +1,84 @@
+// Shared device/host helpers for the B200 condensed-space IPM path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace cmpc {
+
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+// shape/option precondition failures (the reference's DimensionError, types.hpp:17-19)
+struct DimError : std::runtime_error {
+  explicit DimError(const std::string& m) : std::runtime_error(m) {}
+};
+
+#define CMPC_CUDA(x)                                                                        \
+  do {                                                                                      \
+    cudaError_t e__ = (x);                                                                  \
+    if (e__ != cudaSuccess)                                                                 \
+      throw ::cmpc::CudaError(std::string("CUDA error ") + cudaGetErrorString(e__) + " at " + \
+                              __FILE__ + ":" + std::to_string(__LINE__));                    \
+  } while (0)
+
+// every kernel launch goes through this so the launch count is observable
+extern thread_local long long g_launches;
+#define CMPC_LAUNCHED()                 \
+  do {                                  \
+    ++::cmpc::g_launches;               \
+    CMPC_CUDA(cudaPeekAtLastError());   \
+  } while (0)
+
+#ifdef __CUDACC__
+// IEEE operations without FMA contraction: elementwise updates follow the
+// reference's separate multiply/add rounding (Eigen, SSE2, no -march).
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dv(double a, double b) { return __ddiv_rn(a, b); }
+
+// max/min of non-negative doubles through their ordered bit patterns
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+__device__ __forceinline__ void atomic_min_nonneg(double* addr, double v) {
+  atomicMin(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// fixed-order block sum (result valid in thread 0); blockDim.x multiple of 32, <= 1024
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = (l < NT / 32) ? sh[l] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+#endif  // __CUDACC__
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+inline int64_t ceil_div(int64_t x, int64_t a) { return (x + a - 1) / a; }
+
+}  // namespace cmpc

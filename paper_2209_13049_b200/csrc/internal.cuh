@@ -1,0 +1,148 @@
+// Device-resident condensed-space IPM context and the launcher interface between
+// the kernel files (structure.cu, syrk.cu, chol.cu, vec.cu) and the C ABI (capi.cu)
+// plus the host loop (ipm_host.cpp).
+//
+// Data layout in HBM (all FP64, column-major like Eigen::MatrixXd):
+//   H   n x n (ld n)          J   m x n (ld m, the caller's dense constraint Jacobian)
+//   P   ldp x n               the distinct rows of J ("prototypes"), K-major: J = Pi P
+//                             with Pi an m x p signed selection (each row of J is +-1 x one
+//                             prototype). SYRK prototypes (>=2 nonzeros) come first, sorted
+//                             by their nonzero prefix width hi ascending; singleton rows
+//                             (one nonzero, e.g. input bounds) are diagonal terms.
+//   M   n x n lower           H + J' diag(z/s) J (+ shift); L n x n lower Cholesky factor
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cmpc {
+
+constexpr int kTile = 64;      // SYRK / Cholesky output tile
+constexpr int kBK = 32;        // SYRK k rows per pipeline stage
+constexpr int kPartBlocks = 592;  // fixed grid for m-length reductions (4 x 148 SMs)
+
+// small scalar packet read back at the two sync points of an iteration
+struct Packet {
+  // residual pass (packet A)
+  double kkt, max_r1, max_r3, max_comp, max_lam, max_s, max_z, max_h;
+  double obj_vHv, obj_hv, sum_log_s, sum_abs_r3, objective;
+  // step (packet B)
+  double alpha_s_min, alpha_z_min;  // tau-ratio minima (1.0 when no blocking entry)
+  double d_gpv, d_ps_s;             // (Hv+h).pv, sum ps/s
+  long long info;                   // Cholesky failing pivot + 1 (0 = ok)
+  long long any_nonpos;             // trial slack positivity violated
+  // trial merit pieces
+  double t_vHv, t_hv, t_sum_log, t_sum_abs;
+  double pad[8];
+};
+
+struct Workspace;
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool owns_stream = true;
+
+  int64_t n = 0, m = 0;
+  double h0 = 0.0;
+  // problem (device)
+  double *H = nullptr, *h = nullptr, *J = nullptr, *d = nullptr;
+  bool owns_J = true;
+
+  // structure of J
+  int64_t ps = 0;   // SYRK prototypes
+  int64_t pz = 0;   // singleton prototypes (incl. all-zero rows)
+  int64_t p = 0;    // ps + pz
+  int64_t ldp = 0;  // padded leading dimension of P (multiple of kBK, >= ps)
+  double* P = nullptr;           // ldp x n
+  int32_t* hi = nullptr;         // ps: nonzero prefix width
+  int32_t* start_col = nullptr;  // n+1: first SYRK prototype with hi > c
+  int32_t* row_map = nullptr;    // m: proto << 1 | (sign < 0)
+  int32_t* mem_ptr = nullptr;    // p+1
+  int32_t* mem_rows = nullptr;   // m: row << 1 | (sign < 0)
+  int32_t* sing_col = nullptr;   // pz (ascending)
+  double* sing_val = nullptr;    // pz
+  std::vector<int32_t> h_start_col;
+
+  // SYRK work decomposition
+  int nunits = 0, ntiles = 0;
+  int4* units = nullptr;          // {tile_i, tile_j, k0, k1} in execution (k-major) order
+  int32_t* tile_ptr = nullptr;    // ntiles+1 into tile_units
+  int32_t* tile_units = nullptr;  // unit ids per tile in k order
+  int2* tiles = nullptr;          // ntiles {ti, tj}
+  double* partial = nullptr;      // nunits x 64 x 64
+  void* tmap_P = nullptr;         // CUtensorMap (128 B), host copy passed by value
+
+  // iterate and per-iteration buffers (device)
+  double *v = nullptr, *s = nullptr, *lam = nullptr, *z = nullptr, *r1 = nullptr, *r2 = nullptr,
+         *r3 = nullptr;
+  double *Hv = nullptr, *Jtl = nullptr, *y = nullptr, *sigma = nullptr, *omega = nullptr,
+         *q = nullptr, *dsing = nullptr, *rhs = nullptr, *M = nullptr, *L = nullptr;
+  double *pv = nullptr, *ps_ = nullptr, *pl = nullptr, *pzd = nullptr, *Jpv = nullptr,
+         *vt = nullptr, *yt = nullptr, *Hvt = nullptr;
+  double* part = nullptr;     // kPartBlocks x 16 partial sums
+  double* colpart = nullptr;  // Pt q partial: nchunks x n
+  int colchunks = 0;
+  double* hmax = nullptr;
+  Packet* pk = nullptr;      // device packet
+  Packet* pk_host = nullptr; // pinned mirror
+  double mu = 0.0;
+
+  // events for per-phase timing
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+// ---- structure.cu
+void analyze_structure(Ctx& c);
+void free_structure(Ctx& c);
+
+// ---- syrk.cu
+void syrk_plan(Ctx& c);
+// M(lower) = H + P' diag(omega) P + diag(dsing); writes full symmetric M when mirror
+void launch_condense(Ctx& c, bool mirror);
+void syrk_free(Ctx& c);
+
+// ---- chol.cu
+// L = chol(M + delta I) (lower, upper zeroed); failing pivot+1 in c.pk->info
+void launch_cholesky(Ctx& c, const double* M, double* L, double delta);
+// x = L^{-T} L^{-1} b (in place on x allowed)
+void launch_chol_solve(Ctx& c, const double* L, const double* b, double* x);
+
+// ---- vec.cu
+void launch_zero_packet(Ctx& c);
+// residuals at the current state (r1, r2, r3, kkt, objective pieces) -> packet A
+void launch_residuals(Ctx& c);
+// r2 and complementarity only (after a barrier change) -> packet A kkt updated
+void launch_residuals_mu(Ctx& c);
+// sigma = z/s, omega, dsing, q = Pi'(r2 - sigma r3)
+void launch_prepare_step(Ctx& c, const double* sigma_override);
+// rhs = -r1 + (P' q + singletons)
+void launch_rhs(Ctx& c);
+// Jpv, ps, plambda, pz, fraction-to-boundary minima, line-search derivative pieces
+void launch_recover(Ctx& c, double tau);
+// merit pieces of trial (alpha): v_t = v + alpha pv, s_t = s + alpha ps; with
+// alpha_from_device the step is alpha_max = min(1, packet tau-ratio minimum)
+void launch_trial(Ctx& c, double alpha, bool alpha_from_device);
+// line-search derivative pieces for externally set directions: (Hv+h).pv, sum ps/s
+void launch_ls_pieces(Ctx& c);
+// v = 0, s = max(1, d), z = mu / s, lambda = z (ipm.cpp:170-177)
+void launch_init_state(Ctx& c, double mu);
+// iterate update v,s,lambda += alpha p; z += alpha_z pz
+void launch_update(Ctx& c, double alpha, double alpha_z);
+// y = P x (+ singletons), Jx_r = sign y[proto]; optional
+void launch_Jx(Ctx& c, const double* x, double* y, double* Jx);
+// out = P' q + singleton scatter
+void launch_Jtq(Ctx& c, const double* q, double* out);
+// Hx
+void launch_Hx(Ctx& c, const double* x, double* out);
+// stand-alone fraction_to_boundary minima into out[2] (device)
+void launch_fraction_to_boundary(cudaStream_t st, int64_t m, const double* s, const double* ps,
+                                 const double* z, const double* pz, double tau, double* out);
+void vec_alloc(Ctx& c);
+void vec_free(Ctx& c);
+
+}  // namespace cmpc

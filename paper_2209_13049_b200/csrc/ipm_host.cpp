@@ -1,0 +1,252 @@
+// The IPM outer loop on the host (C++), driving the device kernels through the launchers
+// of internal.cuh. Restates condmpc::ipm::solve (proj/src/ipm.cpp:160-268) decision for
+// decision: termination (:153-158), monotone barrier (:146-151), the shift ladder
+// (:205-221), fraction to boundary (:105-116), backtracking Armijo with the roundoff band
+// (:118-144). The device returns small scalar packets; every branch is evaluated here with
+// the reference's rule on the same scalars.
+//
+// Two host syncs per iteration in the common case:
+//   A: after the residual pass (kkt -> termination and barrier decisions)
+//   B: after condense + Cholesky + solve + recovery + trial 0 (info, alpha_max, merit)
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/condmpc_cuda.h"
+#include "internal.cuh"
+
+namespace cmpc {
+
+namespace {
+double now_seconds() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+void require(bool c, const char* m) {
+  if (!c) throw DimError(m);
+}
+void sync_packet(Ctx& c, long long* syncs) {
+  CMPC_CUDA(cudaMemcpyAsync(c.pk_host, c.pk, sizeof(Packet), cudaMemcpyDeviceToHost, c.stream));
+  CMPC_CUDA(cudaStreamSynchronize(c.stream));
+  if (syncs) ++*syncs;
+}
+}  // namespace
+
+// merit phi(v, s) = 0.5 v'Hv + h'v - mu sum log s + rho |Jv - d + s|_1 (ipm.cpp:25-32)
+double merit_host(const Packet&, double vhv, double hv, double sum_log, double sum_abs, double mu,
+                  double rho, bool has_rows) {
+  double phi = 0.5 * vhv + hv;
+  if (has_rows) {
+    phi -= mu * sum_log;
+    phi += rho * sum_abs;
+  }
+  return phi;
+}
+
+namespace {
+
+// the accept loop of line_search (ipm.cpp:129-143). `A` holds the residual packet at the
+// current state, `dg`/`dps` the derivative pieces; trial 0 may already be evaluated.
+int run_line_search(Ctx& c, const Packet& A, double dg, double dps, double alpha_max, double eta,
+                    const Packet* trial0, double* alpha_out, int* ntrials, long long* syncs) {
+  const bool rows = c.m > 0;
+  const double rho = 10.0 * A.max_lam + 1.0;
+  const double phi0 = merit_host(A, A.obj_vHv, A.obj_hv, A.sum_log_s, A.sum_abs_r3, c.mu, rho, rows);
+  double derivative = dg;
+  if (rows) {
+    derivative -= c.mu * dps;
+    derivative -= rho * A.sum_abs_r3;
+  }
+  constexpr double band = 10.0 * std::numeric_limits<double>::epsilon();
+  double alpha = alpha_max;
+  for (int j = 0; j <= 30; ++j, alpha *= 0.5) {
+    Packet T;
+    if (j == 0 && trial0) {
+      T = *trial0;
+    } else {
+      launch_trial(c, alpha, false);
+      sync_packet(c, syncs);
+      T = *c.pk_host;
+    }
+    ++*ntrials;
+    if (rows && T.any_nonpos) continue;
+    const double phi = merit_host(T, T.t_vHv, T.t_hv, T.t_sum_log, T.t_sum_abs, c.mu, rho, rows);
+    if (derivative <= 0.0 && phi <= phi0 + eta * alpha * derivative) {
+      *alpha_out = alpha;
+      return j;
+    }
+    if (std::abs(phi - phi0) <= band * (1.0 + std::abs(phi0))) {
+      *alpha_out = alpha;
+      return j;
+    }
+  }
+  return -1;
+}
+
+}  // namespace
+
+int line_search_host(Ctx& c, double alpha_max, double eta, double* alpha, int* ntrials) {
+  const Packet A = *c.pk_host;  // residuals + derivative pieces already in the packet
+  return run_line_search(c, A, A.d_gpv, A.d_ps_s, alpha_max, eta, nullptr, alpha, ntrials, nullptr);
+}
+
+int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, double* s_out,
+               double* lam_out, double* z_out, double* out, cmpc_log_fn log,
+               cmpc_inspect_fn inspect, void* user) {
+  const double tol = opts[0], mu_init = opts[1], kappa_mu = opts[2], tau = opts[3],
+               eta = opts[4];
+  // check_options (ipm.cpp:17-23)
+  require(tol > 0.0, "tol must be positive");
+  require(kappa_mu > 0.0 && kappa_mu < 1.0, "kappa_mu must lie in (0,1)");
+  require(tau > 0.0 && tau < 1.0, "tau must lie in (0,1)");
+  require(mu_init > 0.0, "mu_init must be positive");
+  require(max_iter >= 1, "max_iter must be at least 1");
+
+  const long long launches0 = g_launches;
+  long long syncs = 0, trials = 0;
+  const int64_t n = c.n, m = c.m;
+  const double start = now_seconds();
+  double linalg = 0.0, device_s = 0.0;
+  cudaEvent_t e_start, e_end;
+  CMPC_CUDA(cudaEventCreate(&e_start));
+  CMPC_CUDA(cudaEventCreate(&e_end));
+  CMPC_CUDA(cudaEventRecord(e_start, c.stream));
+
+  // init (ipm.cpp:170-177)
+  c.mu = mu_init;
+  launch_init_state(c, c.mu);
+  launch_residuals(c);
+  sync_packet(c, &syncs);
+  Packet A = *c.pk_host;
+  int64_t iter = 0;
+  int status = 1;
+  static constexpr std::array<double, 7> kShifts = {0.0, 1e-8, 1e-6, 1e-4, 1e-2, 1.0, 1e2};
+
+  std::vector<double> hv, hs, hl, hz, h1, h2, h3, hpv, hps, hpl, hpz;
+  if (inspect) {
+    hv.resize(size_t(n)); h1.resize(size_t(n)); hpv.resize(size_t(n));
+    for (auto* x : {&hs, &hl, &hz, &h2, &h3, &hps, &hpl, &hpz}) x->resize(size_t(m));
+  }
+
+  while (true) {
+    // check_termination (ipm.cpp:153-158)
+    if (A.kkt <= tol && c.mu <= tol) {
+      status = 0;
+      break;
+    }
+    if (iter >= max_iter) {
+      status = 1;
+      break;
+    }
+    // update_barrier (ipm.cpp:146-151)
+    const double mu_next = (A.kkt <= 10.0 * c.mu) ? std::max(tol / 10.0, kappa_mu * c.mu) : c.mu;
+    if (mu_next != c.mu) {
+      c.mu = mu_next;
+      launch_residuals_mu(c);
+    }
+    // sigma, condensed matrix, factorization with the shift ladder (ipm.cpp:200-226)
+    CMPC_CUDA(cudaEventRecord(c.ev0, c.stream));
+    launch_prepare_step(c, nullptr);
+    launch_condense(c, false);
+    size_t shift = 0;
+    launch_cholesky(c, c.M, c.L, kShifts[shift]);
+    CMPC_CUDA(cudaEventRecord(c.ev1, c.stream));
+    // speculative: directions, recovery, fraction to boundary, line-search trial 0
+    launch_rhs(c);
+    launch_chol_solve(c, c.L, c.rhs, c.pv);
+    launch_recover(c, tau);
+    launch_trial(c, 0.0, true);
+    sync_packet(c, &syncs);
+    float ms = 0.f;
+    CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+    linalg += ms * 1e-3;
+    while (c.pk_host->info != 0) {
+      if (++shift == kShifts.size()) break;
+      CMPC_CUDA(cudaEventRecord(c.ev0, c.stream));
+      launch_cholesky(c, c.M, c.L, kShifts[shift]);
+      CMPC_CUDA(cudaEventRecord(c.ev1, c.stream));
+      launch_chol_solve(c, c.L, c.rhs, c.pv);
+      launch_recover(c, tau);
+      launch_trial(c, 0.0, true);
+      sync_packet(c, &syncs);
+      CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+      linalg += ms * 1e-3;
+    }
+    const Packet B = *c.pk_host;
+    A.kkt = B.kkt;  // kkt at the (possibly new) barrier value, as the reference's res
+    A.max_comp = B.max_comp;
+    if (shift == kShifts.size()) {
+      status = 2;
+      break;
+    }
+    const double delta = kShifts[shift];
+
+    if (inspect) {
+      const std::pair<double*, const double*> cp[] = {
+          {hv.data(), c.v}, {h1.data(), c.r1}, {hpv.data(), c.pv}};
+      for (auto& pr : cp)
+        if (n > 0) CMPC_CUDA(cudaMemcpyAsync(pr.first, pr.second, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+      const std::pair<double*, const double*> cm[] = {{hs.data(), c.s},   {hl.data(), c.lam},
+                                                      {hz.data(), c.z},   {h2.data(), c.r2},
+                                                      {h3.data(), c.r3},  {hps.data(), c.ps_},
+                                                      {hpl.data(), c.pl}, {hpz.data(), c.pzd}};
+      for (auto& pr : cm)
+        if (m > 0) CMPC_CUDA(cudaMemcpyAsync(pr.first, pr.second, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
+      CMPC_CUDA(cudaStreamSynchronize(c.stream));
+      ++syncs;
+      inspect(user, hv.data(), hs.data(), hl.data(), hz.data(), c.mu, h1.data(), h2.data(),
+              h3.data(), B.kkt, hpv.data(), hps.data(), hpl.data(), hpz.data(), delta);
+    }
+
+    const double alpha_max = std::min(1.0, B.alpha_s_min);
+    const double alpha_z = std::min(1.0, B.alpha_z_min);
+    double alpha = 0.0;
+    int nt = 0;
+    const int j = run_line_search(c, A, B.d_gpv, B.d_ps_s, alpha_max, eta, &B, &alpha, &nt, &syncs);
+    trials += nt;
+    if (j < 0) {
+      status = 3;
+      break;
+    }
+    const double mu_used = c.mu;
+    launch_update(c, alpha, alpha_z);
+    iter += 1;
+    launch_residuals(c);
+    sync_packet(c, &syncs);
+    A = *c.pk_host;
+    if (log) {
+      const double rec[8] = {double(iter), mu_used, alpha, alpha_z, A.kkt, A.objective, delta, double(j)};
+      log(user, rec);
+    }
+  }
+
+  if (v_out && n > 0) CMPC_CUDA(cudaMemcpyAsync(v_out, c.v, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+  if (m > 0) {
+    if (s_out) CMPC_CUDA(cudaMemcpyAsync(s_out, c.s, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
+    if (lam_out) CMPC_CUDA(cudaMemcpyAsync(lam_out, c.lam, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
+    if (z_out) CMPC_CUDA(cudaMemcpyAsync(z_out, c.z, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
+  }
+  CMPC_CUDA(cudaEventRecord(e_end, c.stream));
+  CMPC_CUDA(cudaStreamSynchronize(c.stream));
+  float dms = 0.f;
+  CMPC_CUDA(cudaEventElapsedTime(&dms, e_start, e_end));
+  device_s = dms * 1e-3;
+  cudaEventDestroy(e_start);
+  cudaEventDestroy(e_end);
+  out[0] = status;
+  out[1] = double(iter);
+  out[2] = A.kkt;
+  out[3] = A.objective;
+  out[4] = now_seconds() - start;
+  out[5] = linalg;
+  out[6] = device_s;
+  out[7] = double(g_launches - launches0);
+  out[8] = double(syncs);
+  out[9] = double(trials);
+  return CMPC_OK;
+}
+
+}  // namespace cmpc

@@ -1,0 +1,345 @@
+// Exact structure analysis of the constraint Jacobian J (once per loaded QP).
+//
+// The reference multiplies the dense J in every pass (proj/src/ipm.cpp:53-56, :88,
+// :93, :126, :129; proj/src/dense_linalg.cpp:133-134). Its rows repeat with a sign
+// flip (upper/lower bounds: proj/src/reduction.cpp:205-248) and most of each row is
+// a zero suffix (state row at stage t spans t*n_u columns). This pass finds, bit
+// exactly, the distinct rows of J up to sign ("prototypes") so that
+//   J v      = Pi (P v),        J' y = P' (Pi' y),        J' S J = P' diag(Pi' sigma) P
+// with Pi the signed row->prototype selection. Nothing is assumed about the layout:
+// rows are hashed after sign normalisation, grouped by a stable radix sort and every
+// group member is verified element by element against its leader; a hash run with any
+// mismatch falls back to one prototype per row.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace cmpc {
+
+namespace {
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+
+// per row: first/last nonzero, count, sign of the first nonzero, hash of the
+// sign-normalised row
+__global__ void k_row_summary(const double* __restrict__ J, int64_t m, int64_t n, int64_t ldj,
+                              unsigned long long* key, int32_t* lo, int32_t* hi, int32_t* nnz,
+                              int8_t* sg, int32_t* idx) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  unsigned long long h = 0x84222325cbf29ce4ull;
+  int first = -1, last = -1, cnt = 0;
+  double sign = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    const double a = J[r + j * ldj];
+    if (a != 0.0) {
+      if (first < 0) {
+        first = (int)j;
+        sign = a > 0.0 ? 1.0 : -1.0;
+      }
+      last = (int)j;
+      ++cnt;
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(a * sign);
+      h = mix64(h ^ (bits + 0x9e3779b97f4a7c15ull * (unsigned long long)(j + 1)));
+    }
+  }
+  key[r] = mix64(h ^ ((unsigned long long)cnt << 32));
+  lo[r] = first;
+  hi[r] = last + 1;
+  nnz[r] = cnt;
+  sg[r] = sign < 0.0 ? -1 : 1;
+  idx[r] = (int32_t)r;
+}
+
+__global__ void k_head0(const unsigned long long* key, int64_t m, int32_t* head_pos) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  head_pos[i] = (i == 0 || key[i] != key[i - 1]) ? (int32_t)i : 0;
+}
+
+// leader row of every row (in original row order) for coalesced verification
+__global__ void k_leader_of_row(const int32_t* srow, const int32_t* lead_pos, int64_t m,
+                                int32_t* leader_row, int32_t* run_of_row) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int32_t r = srow[i];
+  leader_row[r] = srow[lead_pos[i]];
+  run_of_row[r] = lead_pos[i];
+}
+
+__global__ void k_verify(const double* __restrict__ J, int64_t m, int64_t n, int64_t ldj,
+                         const int32_t* leader_row, const int32_t* run_of_row, const int8_t* sg,
+                         int32_t* collide) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const int32_t l = leader_row[r];
+  if (l == r) return;
+  const double s = (sg[r] == sg[l]) ? 1.0 : -1.0;
+  bool eq = true;
+  for (int64_t j = 0; j < n && eq; ++j) eq = (J[r + j * ldj] == s * J[l + j * ldj]);
+  if (!eq) collide[run_of_row[r]] = 1;
+}
+
+__global__ void k_heads(const int32_t* lead_pos, const int32_t* collide, int64_t m,
+                        int32_t* head) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  head[i] = (lead_pos[i] == i || collide[lead_pos[i]]) ? 1 : 0;
+}
+
+// group info at head positions
+__global__ void k_group_info(const int32_t* head, const int32_t* gid, const int32_t* srow,
+                             const int32_t* hi, const int32_t* nnz, int64_t m,
+                             int32_t* first_pos, unsigned long long* key2, int32_t* gidx) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m || !head[i]) return;
+  const int32_t g = gid[i] - 1;
+  const int32_t r = srow[i];
+  first_pos[g] = (int32_t)i;
+  const unsigned long long single = nnz[r] <= 1 ? 1ull : 0ull;
+  // SYRK prototypes by prefix width, singletons by their column; ties by leader row
+  const unsigned long long w = single ? (unsigned long long)(hi[r] > 0 ? hi[r] : 0)
+                                      : (unsigned long long)hi[r];
+  key2[g] = (single << 62) | (w << 32) | (unsigned long long)r;
+  gidx[g] = g;
+}
+
+__global__ void k_proto_of_group(const int32_t* gorder, int64_t G, int32_t* proto_of_group) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= G) return;
+  proto_of_group[gorder[k]] = (int32_t)k;
+}
+
+__global__ void k_group_size(const int32_t* first_pos, int64_t G, int64_t m,
+                             const int32_t* proto_of_group, int32_t* size_by_proto) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  const int32_t end = (g + 1 < G) ? first_pos[g + 1] : (int32_t)m;
+  size_by_proto[proto_of_group[g]] = end - first_pos[g];
+}
+
+// row_map addresses prototype-indexed vectors: SYRK prototypes at [0, ps), singletons
+// at [ldp, ldp + pz)
+__global__ void k_row_map(const int32_t* srow, const int32_t* gid, const int32_t* first_pos,
+                          const int32_t* proto_of_group, const int32_t* mem_ptr,
+                          const int8_t* sg, int64_t m, int64_t ps, int64_t ldp, int32_t* row_map,
+                          int32_t* mem_rows) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int32_t g = gid[i] - 1;
+  const int32_t r = srow[i];
+  const int32_t lead = srow[first_pos[g]];
+  const int32_t pr = proto_of_group[g];
+  const int32_t neg = sg[r] != sg[lead] ? 1 : 0;
+  const int32_t yi = pr < ps ? pr : (int32_t)(ldp + (pr - ps));
+  row_map[r] = (yi << 1) | neg;
+  mem_rows[mem_ptr[pr] + (int32_t)(i - first_pos[g])] = (r << 1) | neg;
+}
+
+__global__ void k_proto_leader(const int32_t* gorder, const int32_t* first_pos,
+                               const int32_t* srow, int64_t G, int32_t* proto_leader) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= G) return;
+  proto_leader[k] = srow[first_pos[gorder[k]]];
+}
+
+// P[k, j] = J[leader_k, j] for j < hi_k (P pre-zeroed); singletons separately
+__global__ void k_gather_P(const double* __restrict__ J, int64_t ldj, const int32_t* leader,
+                           const int32_t* hi_row, int64_t ps, int64_t n, int64_t ldp,
+                           double* P, int32_t* hi) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= ps) return;
+  const int32_t l = leader[k];
+  const int32_t w = hi_row[l];
+  hi[k] = w;
+  const int64_t j0 = blockIdx.y;
+  for (int64_t j = j0; j < w; j += gridDim.y) P[k + j * ldp] = J[l + j * ldj];
+}
+
+__global__ void k_singletons(const double* __restrict__ J, int64_t ldj, const int32_t* leader,
+                             const int32_t* lo_row, int64_t ps, int64_t pz, int32_t* sing_col,
+                             double* sing_val) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= pz) return;
+  const int32_t l = leader[ps + k];
+  const int32_t c = lo_row[l];
+  sing_col[k] = c < 0 ? 0 : c;
+  sing_val[k] = c < 0 ? 0.0 : J[l + (int64_t)c * ldj];
+}
+
+__global__ void k_start_col(const int32_t* hi, int64_t ps, int64_t n, int32_t* start_col) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > n) return;
+  int64_t lo = 0, up = ps;  // first k with hi[k] > c
+  while (lo < up) {
+    const int64_t mid = (lo + up) / 2;
+    if (hi[mid] > c) up = mid;
+    else lo = mid + 1;
+  }
+  start_col[c] = (int32_t)lo;
+}
+
+template <typename T>
+T* dalloc(size_t count) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  CMPC_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+}  // namespace
+
+void free_structure(Ctx& c) {
+  for (void* p : {(void*)c.P, (void*)c.hi, (void*)c.start_col, (void*)c.row_map,
+                  (void*)c.mem_ptr, (void*)c.mem_rows, (void*)c.sing_col, (void*)c.sing_val})
+    if (p) cudaFree(p);
+  c.P = nullptr;
+  c.hi = c.start_col = c.row_map = c.mem_ptr = c.mem_rows = c.sing_col = nullptr;
+  c.sing_val = nullptr;
+}
+
+void analyze_structure(Ctx& c) {
+  free_structure(c);
+  const int64_t m = c.m, n = c.n;
+  cudaStream_t st = c.stream;
+  c.start_col = dalloc<int32_t>(size_t(n + 1));
+  if (m == 0) {
+    c.ps = c.pz = c.p = 0;
+    c.ldp = kBK;
+    c.P = dalloc<double>(size_t(c.ldp * std::max<int64_t>(n, 1)));
+    CMPC_CUDA(cudaMemsetAsync(c.P, 0, sizeof(double) * c.ldp * std::max<int64_t>(n, 1), st));
+    CMPC_CUDA(cudaMemsetAsync(c.start_col, 0, sizeof(int32_t) * (n + 1), st));
+    c.h_start_col.assign(size_t(n + 1), 0);
+    c.mem_ptr = dalloc<int32_t>(1);
+    CMPC_CUDA(cudaMemsetAsync(c.mem_ptr, 0, sizeof(int32_t), st));
+    return;
+  }
+  const int T = 256;
+  const unsigned gm = unsigned((m + T - 1) / T);
+
+  auto* key = dalloc<unsigned long long>(m);
+  auto* key_s = dalloc<unsigned long long>(m);
+  auto* lo = dalloc<int32_t>(m);
+  auto* hi_row = dalloc<int32_t>(m);
+  auto* nnz = dalloc<int32_t>(m);
+  auto* sg = dalloc<int8_t>(m);
+  auto* idx = dalloc<int32_t>(m);
+  auto* srow = dalloc<int32_t>(m);
+  auto* head_pos = dalloc<int32_t>(m);
+  auto* lead_pos = dalloc<int32_t>(m);
+  auto* leader_row = dalloc<int32_t>(m);
+  auto* run_of_row = dalloc<int32_t>(m);
+  auto* collide = dalloc<int32_t>(m);
+  auto* head = dalloc<int32_t>(m);
+  auto* gid = dalloc<int32_t>(m);
+
+  k_row_summary<<<gm, T, 0, st>>>(c.J, m, n, m, key, lo, hi_row, nnz, sg, idx);
+  CMPC_LAUNCHED();
+
+  size_t tmp_bytes = 0, need = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, need, key, key_s, idx, srow, (int)m, 0, 64, st);
+  tmp_bytes = std::max(tmp_bytes, need);
+  cub::DeviceScan::InclusiveScan(nullptr, need, head_pos, lead_pos, cub::Max(), (int)m, st);
+  tmp_bytes = std::max(tmp_bytes, need);
+  cub::DeviceScan::InclusiveSum(nullptr, need, head, gid, (int)m, st);
+  tmp_bytes = std::max(tmp_bytes, need);
+  cub::DeviceScan::ExclusiveSum(nullptr, need, head, gid, (int)m + 1, st);
+  tmp_bytes = std::max(tmp_bytes, need);
+  // group sort and member pointer scan use at most m items as well
+  auto* tmp = dalloc<unsigned char>(tmp_bytes + 256);
+
+  CMPC_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_s, idx, srow, (int)m, 0, 64, st));
+  k_head0<<<gm, T, 0, st>>>(key_s, m, head_pos);
+  CMPC_LAUNCHED();
+  CMPC_CUDA(cub::DeviceScan::InclusiveScan(tmp, tmp_bytes, head_pos, lead_pos, cub::Max(), (int)m, st));
+  k_leader_of_row<<<gm, T, 0, st>>>(srow, lead_pos, m, leader_row, run_of_row);
+  CMPC_LAUNCHED();
+  CMPC_CUDA(cudaMemsetAsync(collide, 0, sizeof(int32_t) * m, st));
+  k_verify<<<gm, T, 0, st>>>(c.J, m, n, m, leader_row, run_of_row, sg, collide);
+  CMPC_LAUNCHED();
+  k_heads<<<gm, T, 0, st>>>(lead_pos, collide, m, head);
+  CMPC_LAUNCHED();
+  CMPC_CUDA(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, head, gid, (int)m, st));
+  int32_t G = 0;
+  CMPC_CUDA(cudaMemcpyAsync(&G, gid + m - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CMPC_CUDA(cudaStreamSynchronize(st));
+
+  auto* first_pos = dalloc<int32_t>(G);
+  auto* key2 = dalloc<unsigned long long>(G);
+  auto* key2_s = dalloc<unsigned long long>(G);
+  auto* gidx = dalloc<int32_t>(G);
+  auto* gorder = dalloc<int32_t>(G);
+  auto* proto_of_group = dalloc<int32_t>(G);
+  auto* size_by_proto = dalloc<int32_t>(G + 1);
+  auto* leader = dalloc<int32_t>(G);
+  const unsigned gg = unsigned((G + T - 1) / T);
+  k_group_info<<<gm, T, 0, st>>>(head, gid, srow, hi_row, nnz, m, first_pos, key2, gidx);
+  CMPC_LAUNCHED();
+  CMPC_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key2, key2_s, gidx, gorder, G, 0, 64, st));
+  k_proto_of_group<<<gg, T, 0, st>>>(gorder, G, proto_of_group);
+  CMPC_LAUNCHED();
+  CMPC_CUDA(cudaMemsetAsync(size_by_proto, 0, sizeof(int32_t) * (G + 1), st));
+  k_group_size<<<gg, T, 0, st>>>(first_pos, G, m, proto_of_group, size_by_proto);
+  CMPC_LAUNCHED();
+  c.mem_ptr = dalloc<int32_t>(G + 1);
+  CMPC_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, size_by_proto, c.mem_ptr, G + 1, st));
+  k_proto_leader<<<gg, T, 0, st>>>(gorder, first_pos, srow, G, leader);
+  CMPC_LAUNCHED();
+
+  // split point between SYRK prototypes and singletons
+  std::vector<unsigned long long> hk(static_cast<size_t>(G));
+  CMPC_CUDA(cudaMemcpyAsync(hk.data(), key2_s, sizeof(unsigned long long) * G,
+                            cudaMemcpyDeviceToHost, st));
+  CMPC_CUDA(cudaStreamSynchronize(st));
+  int64_t ps = std::lower_bound(hk.begin(), hk.end(), 1ull << 62) - hk.begin();
+  c.ps = ps;
+  c.p = G;
+  c.pz = G - ps;
+  c.ldp = round_up(std::max<int64_t>(ps, 1), kBK);
+  c.row_map = dalloc<int32_t>(m);
+  c.mem_rows = dalloc<int32_t>(m);
+  k_row_map<<<gm, T, 0, st>>>(srow, gid, first_pos, proto_of_group, c.mem_ptr, sg, m, ps, c.ldp,
+                              c.row_map, c.mem_rows);
+  CMPC_LAUNCHED();
+
+  c.P = dalloc<double>(size_t(c.ldp * n));
+  CMPC_CUDA(cudaMemsetAsync(c.P, 0, sizeof(double) * c.ldp * n, st));
+  c.hi = dalloc<int32_t>(ps);
+  if (ps > 0) {
+    dim3 grid(unsigned((ps + T - 1) / T), unsigned(std::min<int64_t>(n, 64)));
+    k_gather_P<<<grid, T, 0, st>>>(c.J, m, leader, hi_row, ps, n, c.ldp, c.P, c.hi);
+    CMPC_LAUNCHED();
+  }
+  c.sing_col = dalloc<int32_t>(c.pz);
+  c.sing_val = dalloc<double>(c.pz);
+  if (c.pz > 0) {
+    k_singletons<<<unsigned((c.pz + T - 1) / T), T, 0, st>>>(c.J, m, leader, lo, ps, c.pz,
+                                                             c.sing_col, c.sing_val);
+    CMPC_LAUNCHED();
+  }
+  k_start_col<<<unsigned((n + 1 + T - 1) / T), T, 0, st>>>(c.hi, ps, n, c.start_col);
+  CMPC_LAUNCHED();
+  c.h_start_col.resize(size_t(n + 1));
+  CMPC_CUDA(cudaMemcpyAsync(c.h_start_col.data(), c.start_col, sizeof(int32_t) * (n + 1),
+                            cudaMemcpyDeviceToHost, st));
+  CMPC_CUDA(cudaStreamSynchronize(st));
+
+  for (void* p : {(void*)key, (void*)key_s, (void*)lo, (void*)hi_row, (void*)nnz, (void*)sg,
+                  (void*)idx, (void*)srow, (void*)head_pos, (void*)lead_pos, (void*)leader_row,
+                  (void*)run_of_row, (void*)collide, (void*)head, (void*)gid, (void*)tmp,
+                  (void*)first_pos, (void*)key2, (void*)key2_s, (void*)gidx, (void*)gorder,
+                  (void*)proto_of_group, (void*)size_by_proto, (void*)leader})
+    cudaFree(p);
+}
+
+}  // namespace cmpc

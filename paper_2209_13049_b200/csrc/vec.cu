@@ -1,0 +1,730 @@
+// K5-K9: the bandwidth-bound passes of one IPM iteration.
+//
+// Reference (proj/src/ipm.cpp): compute_residuals :46-70, step_directions :79-103,
+// fraction_to_boundary :105-116, line_search + merit :118-144 / :25-32, the iterate
+// update :240-243. Every J product goes through the prototype matrix P (structure.cu):
+//   (J x)_r = sign_r (P x)_{proto(r)}    J' y = P' (Pi' y)
+// Elementwise formulas keep the reference's separate multiply/add rounding (no FMA);
+// every sum is a fixed-order two-stage reduction, every max/min an order-free atomic,
+// so two runs are bitwise identical (proj/tests/test_ipm.cpp:432-457).
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace cmpc {
+
+namespace {
+
+constexpr int kRowT = 256;
+enum Slot { kSumAbs = 0, kSumLog = 1, kSumPsS = 2, kSlots = 16 };
+
+inline unsigned part_blocks(int64_t m) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(kPartBlocks, ceil_div(m, kRowT)));
+}
+
+// y[k] = sum_{j < hi_k} A[k + j*lda] x[j]; 32 rows x 8 column slices per block
+__global__ void __launch_bounds__(256) k_rows_gemv(const double* __restrict__ A, int64_t lda,
+                                                   int64_t rows, int64_t ncols,
+                                                   const int32_t* __restrict__ hi,
+                                                   const double* __restrict__ x, double* __restrict__ y) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r = blockIdx.x * 32ll + lane;
+  const int width = (r < rows) ? (hi ? hi[r] : (int)ncols) : 0;
+  int wmax = width;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+  double s0 = 0.0, s1 = 0.0;
+  int64_t j = w;
+  for (; j + 8 < wmax; j += 16) {
+    const double a0 = (j < width) ? A[r + j * lda] : 0.0;
+    const double a1 = (j + 8 < width) ? A[r + (j + 8) * lda] : 0.0;
+    s0 += a0 * x[j];
+    s1 += a1 * x[j + 8];
+  }
+  if (j < wmax) s0 += ((j < width) ? A[r + j * lda] : 0.0) * x[j];
+  red[w][lane] = s0 + s1;
+  __syncthreads();
+  if (w == 0 && r < rows) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += red[q][lane];
+    y[r] = s;
+  }
+}
+
+__global__ void k_sing_x(const int32_t* __restrict__ col, const double* __restrict__ val, int64_t pz,
+                         const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < pz) y[k] = val[k] * x[col[k]];
+}
+
+__device__ __forceinline__ double jrow(const double* y, int32_t rm) {
+  const double v = y[rm >> 1];
+  return (rm & 1) ? -v : v;
+}
+
+// out[j] partial over a chunk of P rows: colpart[chunk*n + j]
+__global__ void __launch_bounds__(256) k_ptq_partial(const double* __restrict__ P, int64_t ldp,
+                                                     int64_t ps, int64_t n,
+                                                     const int32_t* __restrict__ start_col,
+                                                     const double* __restrict__ q, int rc,
+                                                     double* __restrict__ colpart) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j = blockIdx.y * 8ll + w;
+  if (j >= n) return;
+  const int64_t k0 = (int64_t)blockIdx.x * rc, k1 = (ps < k0 + rc ? ps : k0 + rc);
+  const int64_t kb = (k0 > (int64_t)start_col[j] ? k0 : (int64_t)start_col[j]);
+  double s = 0.0;
+  const double* col = P + j * ldp;
+  for (int64_t k = kb + lane; k < k1; k += 32) s += col[k] * q[k];
+  s = warp_sum(s);
+  if (lane == 0) colpart[blockIdx.x * n + j] = s;
+}
+
+// out[j] = sum_chunks colpart + singleton scatter (singletons sorted by column)
+__global__ void k_ptq_final(const double* __restrict__ colpart, int nchunks, int64_t n,
+                            const int32_t* __restrict__ sing_col, const double* __restrict__ sing_val,
+                            int64_t pz, const double* __restrict__ qs, double* __restrict__ out) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += colpart[(int64_t)c * n + j];
+  int64_t lo = 0, hi = pz;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (sing_col[mid] < j) lo = mid + 1;
+    else hi = mid;
+  }
+  for (int64_t k = lo; k < pz && sing_col[k] == j; ++k) s += sing_val[k] * qs[k];
+  out[j] = s;
+}
+
+// ---------------------------------------------------------------- residuals
+__global__ void __launch_bounds__(kRowT) k_res_rows(int64_t m, const int32_t* __restrict__ row_map,
+                                                    const double* __restrict__ y,
+                                                    const double* __restrict__ d,
+                                                    const double* __restrict__ s,
+                                                    const double* __restrict__ lam,
+                                                    const double* __restrict__ z, double mu,
+                                                    double* __restrict__ r2, double* __restrict__ r3,
+                                                    double* __restrict__ part, Packet* pk) {
+  __shared__ double sh[32];
+  double sabs = 0.0, slog = 0.0, ml = 0.0, mss = 0.0, mz = 0.0, mr3 = 0.0, mc = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double jv = jrow(y, row_map[r]);
+    const double sr = s[r], lr = lam[r], zr = z[r];
+    r2[r] = sub(lr, mul(mu, dv(1.0, sr)));
+    const double t3 = add(sub(jv, d[r]), sr);
+    r3[r] = t3;
+    sabs += fabs(t3);
+    slog += log(sr);
+    ml = fmax(ml, fabs(lr));
+    mss = fmax(mss, fabs(sr));
+    mz = fmax(mz, fabs(zr));
+    mr3 = fmax(mr3, fabs(t3));
+    mc = fmax(mc, fabs(sub(mul(sr, zr), mu)));
+  }
+  double t = block_sum<kRowT>(sabs, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumAbs] = t;
+  t = block_sum<kRowT>(slog, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumLog] = t;
+  ml = warp_max(ml);
+  mss = warp_max(mss);
+  mz = warp_max(mz);
+  mr3 = warp_max(mr3);
+  mc = warp_max(mc);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(&pk->max_lam, ml);
+    atomic_max_nonneg(&pk->max_s, mss);
+    atomic_max_nonneg(&pk->max_z, mz);
+    atomic_max_nonneg(&pk->max_r3, mr3);
+    atomic_max_nonneg(&pk->max_comp, mc);
+  }
+}
+
+// r2 and complementarity at a new barrier value (r1, r3 unchanged)
+__global__ void __launch_bounds__(kRowT) k_mu_rows(int64_t m, const double* __restrict__ s,
+                                                   const double* __restrict__ lam,
+                                                   const double* __restrict__ z, double mu,
+                                                   double* __restrict__ r2, Packet* pk) {
+  double mc = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double sr = s[r];
+    r2[r] = sub(lam[r], mul(mu, dv(1.0, sr)));
+    mc = fmax(mc, fabs(sub(mul(sr, z[r]), mu)));
+  }
+  mc = warp_max(mc);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(&pk->max_comp, mc);
+}
+
+// q[proto] = sum over member rows of sign * x[row] (rows ascending)
+__global__ void k_proto_sum(int64_t p, const int32_t* __restrict__ mem_ptr,
+                            const int32_t* __restrict__ mem_rows, const double* __restrict__ x,
+                            double* __restrict__ q, int64_t ps, int64_t ldp) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= p) return;
+  double s = 0.0;
+  for (int32_t e = mem_ptr[k]; e < mem_ptr[k + 1]; ++e) {
+    const int32_t rm = mem_rows[e];
+    const double v = x[rm >> 1];
+    s += (rm & 1) ? -v : v;
+  }
+  q[k < ps ? k : ldp + (k - ps)] = s;
+}
+
+constexpr int kFinT = 1024;
+
+// finalize packet A: r1 = (Hv + h) + J'lambda, max|r1|, kkt, dots for objective and merit
+__global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m, int nparts,
+                                                     const double* __restrict__ Hv,
+                                                     const double* __restrict__ h,
+                                                     const double* __restrict__ Jtl,
+                                                     const double* __restrict__ v,
+                                                     double* __restrict__ r1,
+                                                     const double* __restrict__ part, double h0,
+                                                     const double* __restrict__ hmax, Packet* pk) {
+  __shared__ double sh[32];
+  double mr1 = 0.0, vhv = 0.0, hv = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double g = add(Hv[i], h[i]);
+    const double r = m > 0 ? add(g, Jtl[i]) : g;
+    r1[i] = r;
+    mr1 = fmax(mr1, fabs(r));
+    vhv += v[i] * Hv[i];
+    hv += h[i] * v[i];
+  }
+  vhv = block_sum<kFinT>(vhv, sh);
+  __syncthreads();
+  hv = block_sum<kFinT>(hv, sh);
+  __syncthreads();
+  double sabs = 0.0, slog = 0.0;
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+    sabs += part[b * kSlots + kSumAbs];
+    slog += part[b * kSlots + kSumLog];
+  }
+  sabs = block_sum<kFinT>(sabs, sh);
+  __syncthreads();
+  slog = block_sum<kFinT>(slog, sh);
+  __syncthreads();
+  mr1 = warp_max(mr1);
+  __shared__ double mx[32];
+  if ((threadIdx.x & 31) == 0) mx[threadIdx.x >> 5] = mr1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int q = 0; q < kFinT / 32; ++q) a = fmax(a, mx[q]);
+    pk->max_r1 = a;
+    pk->obj_vHv = vhv;
+    pk->obj_hv = hv;
+    pk->sum_abs_r3 = m > 0 ? sabs : 0.0;
+    pk->sum_log_s = m > 0 ? slog : 0.0;
+    pk->max_h = *hmax;
+    pk->objective = 0.5 * vhv + hv + h0;
+    const double ds = fmax(1.0, fmax(*hmax, pk->max_lam) / (double)(n + m));
+    double kkt = a / ds;
+    if (m > 0) {
+      const double cs = fmax(1.0, fmax(pk->max_s, pk->max_z) / (double)(2 * m));
+      kkt = fmax(kkt, pk->max_r3);
+      kkt = fmax(kkt, pk->max_comp / cs);
+    }
+    pk->kkt = kkt;
+  }
+}
+
+__global__ void k_kkt_only(int64_t n, int64_t m, const double* __restrict__ hmax, Packet* pk) {
+  const double ds = fmax(1.0, fmax(*hmax, pk->max_lam) / (double)(n + m));
+  double kkt = pk->max_r1 / ds;
+  if (m > 0) {
+    const double cs = fmax(1.0, fmax(pk->max_s, pk->max_z) / (double)(2 * m));
+    kkt = fmax(kkt, pk->max_r3);
+    kkt = fmax(kkt, pk->max_comp / cs);
+  }
+  pk->kkt = kkt;
+}
+
+__global__ void k_absmax(const double* __restrict__ x, int64_t n, double* out) {
+  double a = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a = fmax(a, fabs(x[i]));
+  a = warp_max(a);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, a);
+}
+
+// ---------------------------------------------------------------- step
+// sigma = z/s, w = r2 - sigma r3
+__global__ void k_sigma_rows(int64_t m, const double* __restrict__ s, const double* __restrict__ z,
+                             const double* __restrict__ r2, const double* __restrict__ r3,
+                             const double* __restrict__ sig_in, double* __restrict__ sigma,
+                             double* __restrict__ w) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const double sg = sig_in ? sig_in[r] : dv(z[r], s[r]);
+  sigma[r] = sg;
+  if (w) w[r] = sub(r2[r], mul(sg, r3[r]));
+}
+
+// omega[proto] = sum of member sigma; rhs q[proto] = sum of signed member w
+__global__ void k_proto_step(int64_t p, const int32_t* __restrict__ mem_ptr,
+                             const int32_t* __restrict__ mem_rows, const double* __restrict__ sigma,
+                             const double* __restrict__ w, double* __restrict__ omega,
+                             double* __restrict__ q, int64_t ps, int64_t ldp) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= p) return;
+  double so = 0.0, sq = 0.0;
+  for (int32_t e = mem_ptr[k]; e < mem_ptr[k + 1]; ++e) {
+    const int32_t rm = mem_rows[e];
+    const int32_t r = rm >> 1;
+    so += sigma[r];
+    if (w) {
+      const double v = w[r];
+      sq += (rm & 1) ? -v : v;
+    }
+  }
+  const int64_t o = k < ps ? k : ldp + (k - ps);
+  omega[o] = so;
+  if (w) q[o] = sq;
+}
+
+// dsing[c] = sum over singleton prototypes at column c of omega * a^2
+__global__ void k_dsing(int64_t n, const int32_t* __restrict__ sing_col,
+                        const double* __restrict__ sing_val, int64_t pz,
+                        const double* __restrict__ omega_s, double* __restrict__ dsing) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int64_t lo = 0, hi = pz;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (sing_col[mid] < j) lo = mid + 1;
+    else hi = mid;
+  }
+  double s = 0.0;
+  for (int64_t k = lo; k < pz && sing_col[k] == j; ++k) s += omega_s[k] * (sing_val[k] * sing_val[k]);
+  dsing[j] = s;
+}
+
+__global__ void k_rhs(int64_t n, const double* __restrict__ r1, const double* __restrict__ t,
+                      int64_t m, double* __restrict__ rhs) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  rhs[i] = m > 0 ? add(-r1[i], t[i]) : -r1[i];
+}
+
+// ps, plambda, pz, fraction-to-boundary minima, sum ps/s
+__global__ void __launch_bounds__(kRowT) k_recover_rows(
+    int64_t m, const int32_t* __restrict__ row_map, const double* __restrict__ y,
+    const double* __restrict__ s, const double* __restrict__ z, const double* __restrict__ sigma,
+    const double* __restrict__ r2, const double* __restrict__ r3, double mu, double tau,
+    double* __restrict__ Jpv, double* __restrict__ ps, double* __restrict__ pl,
+    double* __restrict__ pz, double* __restrict__ part, Packet* pk) {
+  __shared__ double sh[32];
+  double q = 0.0, as = 1e308, az = 1e308;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double jp = jrow(y, row_map[r]);
+    const double sr = s[r], zr = z[r], sg = sigma[r], t3 = r3[r];
+    Jpv[r] = jp;
+    const double p_s = sub(-t3, jp);
+    const double p_l = add(-r2[r], mul(sg, add(t3, jp)));
+    const double p_z = sub(sub(mul(mu, dv(1.0, sr)), zr), mul(sg, p_s));
+    ps[r] = p_s;
+    pl[r] = p_l;
+    pz[r] = p_z;
+    q += dv(p_s, sr);
+    if (p_s < 0.0) as = fmin(as, mul(tau, dv(-sr, p_s)));
+    if (p_z < 0.0) az = fmin(az, mul(tau, dv(-zr, p_z)));
+  }
+  const double t = block_sum<kRowT>(q, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumPsS] = t;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    as = fmin(as, __shfl_xor_sync(0xffffffffu, as, o));
+    az = fmin(az, __shfl_xor_sync(0xffffffffu, az, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (as < 1e308) atomic_min_nonneg(&pk->alpha_s_min, as);
+    if (az < 1e308) atomic_min_nonneg(&pk->alpha_z_min, az);
+  }
+}
+
+__global__ void __launch_bounds__(kFinT) k_recover_final(int64_t n, int nparts,
+                                                         const double* __restrict__ Hv,
+                                                         const double* __restrict__ h,
+                                                         const double* __restrict__ pv,
+                                                         const double* __restrict__ part, Packet* pk) {
+  __shared__ double sh[32];
+  double g = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) g += add(Hv[i], h[i]) * pv[i];
+  g = block_sum<kFinT>(g, sh);
+  __syncthreads();
+  double q = 0.0;
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x) q += part[b * kSlots + kSumPsS];
+  q = block_sum<kFinT>(q, sh);
+  if (threadIdx.x == 0) {
+    pk->d_gpv = g;
+    pk->d_ps_s = q;
+  }
+}
+
+__global__ void __launch_bounds__(kRowT) k_pss_rows(int64_t m, const double* __restrict__ s,
+                                                    const double* __restrict__ ps,
+                                                    double* __restrict__ part) {
+  __shared__ double sh[32];
+  double q = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x)
+    q += dv(ps[r], s[r]);
+  const double t = block_sum<kRowT>(q, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumPsS] = t;
+}
+
+__global__ void k_init_state(int64_t m, const double* __restrict__ d, double mu,
+                             double* __restrict__ s, double* __restrict__ lam,
+                             double* __restrict__ z) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const double sr = fmax(1.0, d[r]);
+  const double zr = mul(mu, dv(1.0, sr));
+  s[r] = sr;
+  z[r] = zr;
+  lam[r] = zr;
+}
+
+// ---------------------------------------------------------------- line-search trial
+// trial step length: host value, or alpha_max = min(1, tau-ratio minimum) from the device
+__device__ __forceinline__ double trial_alpha(double a, const Packet* pk) {
+  return pk ? fmin(1.0, pk->alpha_s_min) : a;
+}
+
+__global__ void k_axpy_n(int64_t n, const double* __restrict__ x, double a, const Packet* apk,
+                         const double* __restrict__ p, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const double al = trial_alpha(a, apk);
+  if (i < n) out[i] = add(x[i], mul(al, p[i]));
+}
+
+__global__ void __launch_bounds__(kRowT) k_trial_rows(int64_t m, const int32_t* __restrict__ row_map,
+                                                      const double* __restrict__ yt,
+                                                      const double* __restrict__ d,
+                                                      const double* __restrict__ s,
+                                                      const double* __restrict__ ps, double alpha_h,
+                                                      const Packet* apk, double* __restrict__ part,
+                                                      Packet* pk) {
+  __shared__ double sh[32];
+  double sabs = 0.0, slog = 0.0;
+  const double alpha = trial_alpha(alpha_h, apk);
+  int bad = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double st = add(s[r], mul(alpha, ps[r]));
+    if (st <= 0.0) bad = 1;
+    slog += log(st);
+    sabs += fabs(add(sub(jrow(yt, row_map[r]), d[r]), st));
+  }
+  double t = block_sum<kRowT>(sabs, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumAbs] = t;
+  t = block_sum<kRowT>(slog, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumLog] = t;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) pk->any_nonpos = 1;
+}
+
+__global__ void __launch_bounds__(kFinT) k_trial_final(int64_t n, int64_t m, int nparts,
+                                                       const double* __restrict__ vt,
+                                                       const double* __restrict__ Hvt,
+                                                       const double* __restrict__ h,
+                                                       const double* __restrict__ part, Packet* pk) {
+  __shared__ double sh[32];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    a += vt[i] * Hvt[i];
+    b += h[i] * vt[i];
+  }
+  a = block_sum<kFinT>(a, sh);
+  __syncthreads();
+  b = block_sum<kFinT>(b, sh);
+  __syncthreads();
+  double sabs = 0.0, slog = 0.0;
+  for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
+    sabs += part[q * kSlots + kSumAbs];
+    slog += part[q * kSlots + kSumLog];
+  }
+  sabs = block_sum<kFinT>(sabs, sh);
+  __syncthreads();
+  slog = block_sum<kFinT>(slog, sh);
+  if (threadIdx.x == 0) {
+    pk->t_vHv = a;
+    pk->t_hv = b;
+    pk->t_sum_abs = m > 0 ? sabs : 0.0;
+    pk->t_sum_log = m > 0 ? slog : 0.0;
+  }
+}
+
+__global__ void k_update(int64_t n, int64_t m, double alpha, double alpha_z, double* __restrict__ v,
+                         const double* __restrict__ pv, double* __restrict__ s,
+                         const double* __restrict__ ps, double* __restrict__ lam,
+                         const double* __restrict__ pl, double* __restrict__ z,
+                         const double* __restrict__ pz) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = add(v[i], mul(alpha, pv[i]));
+  if (i < m) {
+    s[i] = add(s[i], mul(alpha, ps[i]));
+    lam[i] = add(lam[i], mul(alpha, pl[i]));
+    z[i] = add(z[i], mul(alpha_z, pz[i]));
+  }
+}
+
+// stand-alone fraction_to_boundary minima (out[0..1] pre-set to +inf)
+__global__ void k_ftb(int64_t m, const double* __restrict__ s, const double* __restrict__ ps,
+                      const double* __restrict__ z, const double* __restrict__ pz, double tau,
+                      double* out) {
+  double as = 1e308, az = 1e308;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (ps[r] < 0.0) as = fmin(as, mul(tau, dv(-s[r], ps[r])));
+    if (pz[r] < 0.0) az = fmin(az, mul(tau, dv(-z[r], pz[r])));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    as = fmin(as, __shfl_xor_sync(0xffffffffu, as, o));
+    az = fmin(az, __shfl_xor_sync(0xffffffffu, az, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (as < 1e308) atomic_min_nonneg(&out[0], as);
+    if (az < 1e308) atomic_min_nonneg(&out[1], az);
+  }
+}
+
+__global__ void k_reset_packet(Packet* pk, int which) {
+  if (which == 0) {  // residual maxima
+    pk->max_r1 = pk->max_r3 = pk->max_comp = pk->max_lam = pk->max_s = pk->max_z = 0.0;
+  } else if (which == 1) {  // recovery minima
+    pk->alpha_s_min = __longlong_as_double(0x7ff0000000000000ll);
+    pk->alpha_z_min = __longlong_as_double(0x7ff0000000000000ll);
+  } else if (which == 2) {
+    pk->any_nonpos = 0;
+  } else if (which == 3) {
+    pk->max_comp = 0.0;
+  }
+}
+
+template <typename T>
+T* dz(size_t count) {
+  T* p = nullptr;
+  CMPC_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  CMPC_CUDA(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)));
+  return p;
+}
+
+}  // namespace
+
+void vec_alloc(Ctx& c) {
+  const size_t n = (size_t)c.n, m = (size_t)c.m;
+  const size_t py = (size_t)(c.ldp + c.pz);  // prototype-indexed arrays
+  c.v = dz<double>(n); c.s = dz<double>(m); c.lam = dz<double>(m); c.z = dz<double>(m);
+  c.r1 = dz<double>(n); c.r2 = dz<double>(m); c.r3 = dz<double>(m);
+  c.Hv = dz<double>(n); c.Jtl = dz<double>(n); c.y = dz<double>(py); c.sigma = dz<double>(m);
+  c.omega = dz<double>(py); c.q = dz<double>(py); c.dsing = dz<double>(n); c.rhs = dz<double>(n);
+  c.M = dz<double>(n * n); c.L = dz<double>(n * n);
+  c.pv = dz<double>(n); c.ps_ = dz<double>(m); c.pl = dz<double>(m); c.pzd = dz<double>(m);
+  c.Jpv = dz<double>(m); c.vt = dz<double>(n); c.yt = dz<double>(py); c.Hvt = dz<double>(n);
+  c.part = dz<double>((size_t)kPartBlocks * kSlots);
+  const int rc = 2048;
+  c.colchunks = (int)std::max<int64_t>(1, ceil_div(c.ps, rc));
+  c.colpart = dz<double>((size_t)c.colchunks * n);
+  c.hmax = dz<double>(1);
+  CMPC_CUDA(cudaMalloc(&c.pk, sizeof(Packet)));
+  CMPC_CUDA(cudaMemset(c.pk, 0, sizeof(Packet)));
+  CMPC_CUDA(cudaMallocHost(&c.pk_host, sizeof(Packet)));
+  if (c.n > 0) {
+    k_absmax<<<(unsigned)std::min<int64_t>(64, ceil_div(c.n, 256)), 256, 0, c.stream>>>(c.h, c.n, c.hmax);
+    CMPC_LAUNCHED();
+  }
+}
+
+void vec_free(Ctx& c) {
+  for (void* p : {(void*)c.v, (void*)c.s, (void*)c.lam, (void*)c.z, (void*)c.r1, (void*)c.r2,
+                  (void*)c.r3, (void*)c.Hv, (void*)c.Jtl, (void*)c.y, (void*)c.sigma,
+                  (void*)c.omega, (void*)c.q, (void*)c.dsing, (void*)c.rhs, (void*)c.M,
+                  (void*)c.L, (void*)c.pv, (void*)c.ps_, (void*)c.pl, (void*)c.pzd, (void*)c.Jpv,
+                  (void*)c.vt, (void*)c.yt, (void*)c.Hvt, (void*)c.part, (void*)c.colpart,
+                  (void*)c.hmax, (void*)c.pk})
+    if (p) cudaFree(p);
+  if (c.pk_host) cudaFreeHost(c.pk_host);
+  c.v = c.s = c.lam = c.z = c.r1 = c.r2 = c.r3 = c.Hv = c.Jtl = c.y = c.sigma = nullptr;
+  c.omega = c.q = c.dsing = c.rhs = c.M = c.L = c.pv = c.ps_ = c.pl = c.pzd = nullptr;
+  c.Jpv = c.vt = c.yt = c.Hvt = c.part = c.colpart = c.hmax = nullptr;
+  c.pk = nullptr;
+  c.pk_host = nullptr;
+}
+
+void launch_zero_packet(Ctx& c) {
+  CMPC_CUDA(cudaMemsetAsync(c.pk, 0, sizeof(Packet), c.stream));
+}
+
+void launch_Hx(Ctx& c, const double* x, double* out) {
+  if (c.n == 0) return;
+  k_rows_gemv<<<(unsigned)ceil_div(c.n, 32), 256, 0, c.stream>>>(c.H, c.n, c.n, c.n, nullptr, x, out);
+  CMPC_LAUNCHED();
+}
+
+void launch_Jx(Ctx& c, const double* x, double* y, double* Jx) {
+  if (c.ps > 0) {
+    k_rows_gemv<<<(unsigned)ceil_div(c.ps, 32), 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.n, c.hi, x, y);
+    CMPC_LAUNCHED();
+  }
+  if (c.pz > 0) {
+    k_sing_x<<<(unsigned)ceil_div(c.pz, 256), 256, 0, c.stream>>>(c.sing_col, c.sing_val, c.pz, x,
+                                                                  y + c.ldp);
+    CMPC_LAUNCHED();
+  }
+  (void)Jx;
+}
+
+// prototype-indexed y (SYRK part at [0,ldp), singletons at [ldp, ldp+pz)) -> row values:
+// the row kernels address y with proto index k < ps directly and singletons at ldp + (k - ps);
+// to keep one index space the row_map stores the compact index (see compact_row_map).
+
+void launch_Jtq(Ctx& c, const double* q, double* out) {
+  if (c.n == 0) return;
+  if (c.ps > 0) {
+    const int rc = 2048;
+    dim3 g((unsigned)c.colchunks, (unsigned)ceil_div(c.n, 8));
+    k_ptq_partial<<<g, 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.n, c.start_col, q, rc, c.colpart);
+    CMPC_LAUNCHED();
+  }
+  k_ptq_final<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(
+      c.colpart, c.ps > 0 ? c.colchunks : 0, c.n, c.sing_col, c.sing_val, c.pz, q + c.ldp, out);
+  CMPC_LAUNCHED();
+}
+
+void launch_residuals(Ctx& c) {
+  const unsigned pb = part_blocks(c.m);
+  k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 0);
+  CMPC_LAUNCHED();
+  launch_Hx(c, c.v, c.Hv);
+  if (c.m > 0) {
+    launch_Jx(c, c.v, c.y, nullptr);
+    k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.d, c.s, c.lam, c.z, c.mu, c.r2,
+                                           c.r3, c.part, c.pk);
+    CMPC_LAUNCHED();
+    k_proto_sum<<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(c.p, c.mem_ptr, c.mem_rows,
+                                                                    c.lam, c.q, c.ps, c.ldp);
+    CMPC_LAUNCHED();
+    launch_Jtq(c, c.q, c.Jtl);
+  }
+  k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m, c.m > 0 ? (int)pb : 0, c.Hv, c.h, c.Jtl, c.v,
+                                         c.r1, c.part, c.h0, c.hmax, c.pk);
+  CMPC_LAUNCHED();
+}
+
+void launch_residuals_mu(Ctx& c) {
+  if (c.m > 0) {
+    k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 3);
+    CMPC_LAUNCHED();
+    k_mu_rows<<<part_blocks(c.m), kRowT, 0, c.stream>>>(c.m, c.s, c.lam, c.z, c.mu, c.r2, c.pk);
+    CMPC_LAUNCHED();
+  }
+  k_kkt_only<<<1, 1, 0, c.stream>>>(c.n, c.m, c.hmax, c.pk);
+  CMPC_LAUNCHED();
+}
+
+void launch_prepare_step(Ctx& c, const double* sigma_override) {
+  if (c.m == 0) {
+    CMPC_CUDA(cudaMemsetAsync(c.dsing, 0, sizeof(double) * std::max<int64_t>(c.n, 1), c.stream));
+    return;
+  }
+  k_sigma_rows<<<(unsigned)ceil_div(c.m, 256), 256, 0, c.stream>>>(
+      c.m, c.s, c.z, c.r2, c.r3, sigma_override, c.sigma, sigma_override ? nullptr : c.Jpv);
+  CMPC_LAUNCHED();
+  k_proto_step<<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
+      c.p, c.mem_ptr, c.mem_rows, c.sigma, sigma_override ? nullptr : c.Jpv, c.omega, c.q, c.ps,
+      c.ldp);
+  CMPC_LAUNCHED();
+  k_dsing<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.sing_col, c.sing_val, c.pz,
+                                                              c.omega + c.ldp, c.dsing);
+  CMPC_LAUNCHED();
+}
+
+void launch_rhs(Ctx& c) {
+  if (c.m > 0) launch_Jtq(c, c.q, c.rhs);
+  k_rhs<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.r1, c.rhs, c.m, c.rhs);
+  CMPC_LAUNCHED();
+}
+
+void launch_recover(Ctx& c, double tau) {
+  k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 1);
+  CMPC_LAUNCHED();
+  const unsigned pb = part_blocks(c.m);
+  if (c.m > 0) {
+    launch_Jx(c, c.pv, c.y, nullptr);
+    k_recover_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.s, c.z, c.sigma, c.r2, c.r3,
+                                               c.mu, tau, c.Jpv, c.ps_, c.pl, c.pzd, c.part, c.pk);
+    CMPC_LAUNCHED();
+  }
+  k_recover_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m > 0 ? (int)pb : 0, c.Hv, c.h, c.pv, c.part,
+                                             c.pk);
+  CMPC_LAUNCHED();
+}
+
+void launch_trial(Ctx& c, double alpha, bool alpha_from_device) {
+  const Packet* apk = alpha_from_device ? c.pk : nullptr;
+  k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 2);
+  CMPC_LAUNCHED();
+  if (c.n > 0) {
+    k_axpy_n<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.v, alpha, apk, c.pv, c.vt);
+    CMPC_LAUNCHED();
+  }
+  launch_Hx(c, c.vt, c.Hvt);
+  const unsigned pb = part_blocks(c.m);
+  if (c.m > 0) {
+    launch_Jx(c, c.vt, c.yt, nullptr);
+    k_trial_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.yt, c.d, c.s, c.ps_, alpha, apk,
+                                             c.part, c.pk);
+    CMPC_LAUNCHED();
+  }
+  k_trial_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m, c.m > 0 ? (int)pb : 0, c.vt, c.Hvt, c.h,
+                                           c.part, c.pk);
+  CMPC_LAUNCHED();
+}
+
+void launch_fraction_to_boundary(cudaStream_t st, int64_t m, const double* s, const double* ps,
+                                 const double* z, const double* pz, double tau, double* out) {
+  const double inf = __builtin_huge_val();
+  const double init[2] = {inf, inf};
+  CMPC_CUDA(cudaMemcpyAsync(out, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  if (m > 0) {
+    k_ftb<<<part_blocks(m), kRowT, 0, st>>>(m, s, ps, z, pz, tau, out);
+    CMPC_LAUNCHED();
+  }
+}
+
+void launch_ls_pieces(Ctx& c) {
+  const unsigned pb = part_blocks(c.m);
+  if (c.m > 0) {
+    k_pss_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.s, c.ps_, c.part);
+    CMPC_LAUNCHED();
+  }
+  k_recover_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m > 0 ? (int)pb : 0, c.Hv, c.h, c.pv, c.part,
+                                             c.pk);
+  CMPC_LAUNCHED();
+}
+
+void launch_init_state(Ctx& c, double mu) {
+  if (c.n > 0) CMPC_CUDA(cudaMemsetAsync(c.v, 0, sizeof(double) * c.n, c.stream));
+  if (c.m > 0) {
+    k_init_state<<<(unsigned)ceil_div(c.m, 256), 256, 0, c.stream>>>(c.m, c.d, mu, c.s, c.lam, c.z);
+    CMPC_LAUNCHED();
+  }
+}
+
+void launch_update(Ctx& c, double alpha, double alpha_z) {
+  const int64_t k = std::max(c.n, c.m);
+  if (k == 0) return;
+  k_update<<<(unsigned)ceil_div(k, 256), 256, 0, c.stream>>>(c.n, c.m, alpha, alpha_z, c.v, c.pv,
+                                                             c.s, c.ps_, c.lam, c.pl, c.z, c.pzd);
+  CMPC_LAUNCHED();
+}
+
+}  // namespace cmpc

@@ -1,0 +1,320 @@
+"""condmpc::ipm on the B200 (proj/include/condmpc/ipm.hpp, proj/src/ipm.cpp).
+
+Same names, argument meaning and error behaviour as the reference: ``solve(qp, opts)``
+runs the C++ host loop of csrc/ipm_host.cpp over the device kernels; the per-step
+functions (``compute_residuals``, ``assemble_condensed``, ``step_directions``,
+``line_search`` ...) run the same kernels on the QP's device context so they can be
+unit-tested like proj/tests/test_ipm.cpp. ``update_barrier`` and ``check_termination``
+are the host-side scalar rules (identical to the C++ loop's).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import DimensionError, check, f64, ptr
+from .linalg import DEVICE, Factor, NotPositiveDefinite
+from .problem import DenseQp, Trajectory, recover_trajectory
+
+
+class IpmStatus(enum.Enum):
+    converged = 0
+    max_iter = 1
+    factorization_failure = 2
+    line_search_failure = 3
+
+
+def to_string(status: IpmStatus) -> str:
+    return status.name
+
+
+class Termination(enum.Enum):
+    converged = 0
+    max_iter = 1
+    keep_going = 2
+
+
+@dataclass
+class IpmState:
+    v: np.ndarray
+    s: np.ndarray
+    lambda_: np.ndarray
+    z: np.ndarray
+    mu: float = 0.0
+    iter: int = 0
+
+
+@dataclass
+class Residuals:
+    r1: np.ndarray
+    r2: np.ndarray
+    r3: np.ndarray
+    kkt_error: float = 0.0
+
+
+@dataclass
+class StepDirections:
+    pv: np.ndarray
+    ps: np.ndarray
+    plambda: np.ndarray
+    pz: np.ndarray
+
+
+@dataclass
+class IterationRecord:
+    iter: int
+    mu: float
+    alpha: float
+    alpha_z: float
+    kkt_error: float
+    objective: float
+    delta: float = 0.0  # extension: shift used by the factorization
+    trial: int = 0      # extension: accepted line-search trial j
+
+
+@dataclass
+class IterationInspection:
+    state: IpmState
+    residuals: Residuals
+    dirs: StepDirections
+    delta: float
+
+
+@dataclass
+class IpmOptions:
+    tol: float = 1e-8
+    mu_init: float = 1e-1
+    kappa_mu: float = 0.2
+    tau: float = 0.995
+    max_iter: int = 200
+    armijo_eta: float = 1e-4
+    backend: str = "cuda"
+    log: Optional[Callable[[IterationRecord], None]] = None
+    inspect: Optional[Callable[[IterationInspection], None]] = None
+
+
+@dataclass
+class IpmResult:
+    status: IpmStatus = IpmStatus.max_iter
+    solution: Trajectory = field(default_factory=Trajectory)
+    v: np.ndarray = None
+    s: np.ndarray = None
+    lambda_: np.ndarray = None
+    z: np.ndarray = None
+    iter: int = 0
+    kkt_error: float = 0.0
+    objective: float = 0.0
+    total_seconds: float = 0.0
+    linalg_seconds: float = 0.0
+    device_seconds: float = 0.0
+    launches: int = 0
+    syncs: int = 0
+    trials: int = 0
+
+
+class DeviceQp:
+    """One device context (stream + HBM buffers) holding a loaded DenseQp."""
+
+    def __init__(self, qp: DenseQp, device: int = DEVICE, on_device_ptrs=None):
+        L = _lib.lib()
+        h = C.c_void_p()
+        check(L.cmpc_ctx_create(C.byref(h), device))
+        self.h = h
+        self.n, self.m = qp.n, qp.m
+        if on_device_ptrs is not None:
+            H, hv, J, d = on_device_ptrs
+            check(L.cmpc_load_qp(self.h, qp.n, qp.m, C.cast(H, _lib.D), C.cast(hv, _lib.D),
+                                 qp.h0, C.cast(J, _lib.D), C.cast(d, _lib.D), 1))
+        else:
+            check(L.cmpc_load_qp(self.h, qp.n, qp.m, ptr(qp.H), ptr(qp.h), qp.h0, ptr(qp.J),
+                                 ptr(qp.d), 0))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().cmpc_ctx_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def info(self):
+        out = (C.c_int64 * 6)()
+        _lib.lib().cmpc_qp_info(self.h, out)
+        return dict(n=out[0], m=out[1], prototypes=out[2], syrk_prototypes=out[3],
+                    singletons=out[4], syrk_units=out[5])
+
+    def update_affine(self, h, h0, d):
+        h, d = f64(h), f64(d)
+        check(_lib.lib().cmpc_update_qp_affine(self.h, ptr(h), float(h0), ptr(d), 0))
+
+    def set_state(self, st: IpmState):
+        v, s, l, z = _state_arrays(st, self.n, self.m)
+        check(_lib.lib().cmpc_set_state(self.h, ptr(v), ptr(s), ptr(l), ptr(z), float(st.mu)))
+
+
+def device_qp(qp: DenseQp) -> DeviceQp:
+    if qp._device is None:
+        qp._device = DeviceQp(qp)
+    return qp._device
+
+
+def _state_arrays(st: IpmState, n, m):
+    v, s, l, z = (f64(x).reshape(-1) for x in (st.v, st.s, st.lambda_, st.z))
+    if v.size != n:
+        raise DimensionError("state.v does not match the QP")
+    if s.size != m or l.size != m or z.size != m:
+        raise DimensionError("state slack/dual lengths do not match the QP row count")
+    return v, s, l, z
+
+
+def _check_options(opts: IpmOptions):
+    """ipm.cpp:17-23."""
+    if not opts.tol > 0.0:
+        raise DimensionError("tol must be positive")
+    if not (0.0 < opts.kappa_mu < 1.0):
+        raise DimensionError("kappa_mu must lie in (0,1)")
+    if not (0.0 < opts.tau < 1.0):
+        raise DimensionError("tau must lie in (0,1)")
+    if not opts.mu_init > 0.0:
+        raise DimensionError("mu_init must be positive")
+    if not opts.max_iter >= 1:
+        raise DimensionError("max_iter must be at least 1")
+
+
+# ------------------------------------------------------------------ per-step API
+def compute_residuals(qp: DenseQp, state: IpmState) -> Residuals:
+    """ipm.cpp:46-70."""
+    dq = device_qp(qp)
+    dq.set_state(state)
+    r1, r2, r3 = np.zeros(qp.n), np.zeros(qp.m), np.zeros(qp.m)
+    kkt = C.c_double()
+    check(_lib.lib().cmpc_compute_residuals(dq.h, ptr(r1), ptr(r2), ptr(r3), C.byref(kkt)))
+    return Residuals(r1, r2, r3, kkt.value)
+
+
+def assemble_condensed(qp: DenseQp, sigma) -> np.ndarray:
+    """ipm.cpp:72-77: H + J' diag(sigma) J (full symmetric)."""
+    sigma = f64(sigma).reshape(-1)
+    if sigma.size != qp.m:
+        raise DimensionError("sigma length does not match the QP row count")
+    dq = device_qp(qp)
+    M = np.zeros((qp.n, qp.n), order="F")
+    check(_lib.lib().cmpc_assemble_condensed(dq.h, ptr(sigma) if qp.m > 0 else None, ptr(M)))
+    return M
+
+
+def step_directions(qp: DenseQp, state: IpmState, res: Residuals, factor: Factor) -> StepDirections:
+    """ipm.cpp:79-103 with the given factor of the condensed matrix."""
+    dq = device_qp(qp)
+    dq.set_state(state)
+    L = _lib.lib()
+    r1, r2, r3 = (f64(x).reshape(-1) for x in (res.r1, res.r2, res.r3))
+    check(L.cmpc_set_residuals(dq.h, ptr(r1), ptr(r2), ptr(r3)))
+    Lf = f64(factor.lower())
+    if Lf.shape != (qp.n, qp.n):
+        raise DimensionError("factor dimension does not match the QP")
+    check(L.cmpc_set_factor(dq.h, ptr(Lf)))
+    pv, ps, pl, pz = np.zeros(qp.n), np.zeros(qp.m), np.zeros(qp.m), np.zeros(qp.m)
+    alpha = np.zeros(2)
+    check(L.cmpc_step_directions(dq.h, 0.5, ptr(pv), ptr(ps), ptr(pl), ptr(pz), ptr(alpha)))
+    return StepDirections(pv, ps, pl, pz)
+
+
+def fraction_to_boundary(s, ps, z, pz, tau):
+    """ipm.cpp:105-116: (alpha_max, alpha_z)."""
+    if not (0.0 < tau < 1.0):
+        raise DimensionError("tau must lie in (0,1)")
+    s, ps, z, pz = (f64(x).reshape(-1) for x in (s, ps, z, pz))
+    out = np.zeros(2)
+    check(_lib.lib().cmpc_fraction_to_boundary(DEVICE, s.size, ptr(s), ptr(ps), ptr(z), ptr(pz),
+                                                float(tau), ptr(out)))
+    return float(out[0]), float(out[1])
+
+
+def line_search(qp: DenseQp, state: IpmState, dirs: StepDirections, alpha_max: float,
+                opts: IpmOptions = IpmOptions()) -> Optional[float]:
+    """ipm.cpp:118-144: first accepted alpha_max * 2^-j, or None."""
+    if not (0.0 < alpha_max <= 1.0):
+        raise DimensionError("alpha_max must lie in (0,1]")
+    dq = device_qp(qp)
+    dq.set_state(state)
+    L = _lib.lib()
+    pv, ps, pl, pz = (f64(x).reshape(-1) for x in (dirs.pv, dirs.ps, dirs.plambda, dirs.pz))
+    check(L.cmpc_set_directions(dq.h, ptr(pv), ptr(ps) if qp.m else None, ptr(pl) if qp.m else None,
+                                ptr(pz) if qp.m else None))
+    a = C.c_double()
+    j = C.c_int()
+    check(L.cmpc_line_search(dq.h, float(alpha_max), float(opts.armijo_eta), C.byref(a), C.byref(j)))
+    return a.value if j.value >= 0 else None
+
+
+def update_barrier(state: IpmState, res: Residuals, opts: IpmOptions) -> float:
+    """ipm.cpp:146-151."""
+    if res.kkt_error <= 10.0 * state.mu:
+        return max(opts.tol / 10.0, opts.kappa_mu * state.mu)
+    return state.mu
+
+
+def check_termination(res: Residuals, state: IpmState, opts: IpmOptions) -> Termination:
+    """ipm.cpp:153-158."""
+    if res.kkt_error <= opts.tol and state.mu <= opts.tol:
+        return Termination.converged
+    if state.iter >= opts.max_iter:
+        return Termination.max_iter
+    return Termination.keep_going
+
+
+# ------------------------------------------------------------------ solve
+def solve(qp: DenseQp, opts: IpmOptions = None) -> IpmResult:
+    """ipm.cpp:160-268: the whole solve on the device, host loop in C++."""
+    opts = opts or IpmOptions()
+    _check_options(opts)
+    if qp.h.size != qp.n:
+        raise DimensionError("qp.h length does not match qp.H")
+    if qp.d.size != qp.m:
+        raise DimensionError("qp.d length does not match qp.J")
+    if opts.backend != "cuda":
+        raise ValueError(f"unknown factorization backend: {opts.backend}")
+    t0 = time.perf_counter()
+    dq = device_qp(qp)
+    return solve_loaded(dq, qp, opts, t0)
+
+
+def solve_loaded(dq: DeviceQp, qp: DenseQp, opts: IpmOptions, t0=None) -> IpmResult:
+    t0 = time.perf_counter() if t0 is None else t0
+    n, m = qp.n, qp.m
+    v, s, l, z = np.zeros(n), np.zeros(m), np.zeros(m), np.zeros(m)
+    out = np.zeros(10)
+    L = _lib.lib()
+
+    def _log(user, rec):
+        opts.log(IterationRecord(int(rec[0]), rec[1], rec[2], rec[3], rec[4], rec[5], rec[6],
+                                 int(rec[7])))
+
+    def _insp(user, v_, s_, l_, z_, mu, r1, r2, r3, kkt, pv, ps, pl, pz, delta):
+        vec = lambda p, k: np.ctypeslib.as_array(p, shape=(k,)).copy() if k else np.zeros(0)
+        st = IpmState(vec(v_, n), vec(s_, m), vec(l_, m), vec(z_, m), mu)
+        opts.inspect(IterationInspection(st, Residuals(vec(r1, n), vec(r2, m), vec(r3, m), kkt),
+                                         StepDirections(vec(pv, n), vec(ps, m), vec(pl, m),
+                                                        vec(pz, m)), delta))
+
+    lf = _lib.LOG_FN(_log) if opts.log else _lib.LOG_FN()
+    inf_ = _lib.INSPECT_FN(_insp) if opts.inspect else _lib.INSPECT_FN()
+    od = (C.c_double * 5)(opts.tol, opts.mu_init, opts.kappa_mu, opts.tau, opts.armijo_eta)
+    check(L.cmpc_solve(dq.h, od, int(opts.max_iter), ptr(v), ptr(s), ptr(l), ptr(z), ptr(out), lf,
+                       inf_, None))
+    res = IpmResult(status=IpmStatus(int(out[0])), v=v, s=s, lambda_=l, z=z, iter=int(out[1]),
+                    kkt_error=float(out[2]), objective=float(out[3]), linalg_seconds=float(out[5]),
+                    device_seconds=float(out[6]), launches=int(out[7]), syncs=int(out[8]),
+                    trials=int(out[9]))
+    if qp.source is not None:
+        res.solution = recover_trajectory(qp, v)
+    else:
+        res.solution = Trajectory(objective=res.objective)
+    res.total_seconds = time.perf_counter() - t0
+    return res
