@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark: ms per MPC solve (and per IPM iteration) of the condensed-space IPM.
+
+Workload (N=1 default): BASELINE.json config 3, the 2-D heat-equation MPC (50 x 50 copper
+plate, n_x = 2500, n_u = 10, T = 50 -> n = 500 controls, m = 251,000 inequality rows).
+A "step" is one complete ipm::solve (proj/src/ipm.cpp:160-268) of that QP, tol 1e-8.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c3]
+
+value: device time of K solves with the QP resident in HBM (CUDA events on the solve's
+stream, max over ranks). e2e: the same metric through the public API
+(paper_2209_13049_b200.ipm.solve on a fresh DenseQp whose arrays sit in pinned host
+memory): H2D upload + structure analysis + solve + D2H of the iterate + trajectory recovery,
+wall clock. N > 1 (torchrun): every rank solves its own instance (initial temperature
+varied per rank, config-5 style batch), no collective in the loop -> weak scaling.
+--impl reference: the oracle (CPU restatement of the reference solver) on the box's host
+cores, bounded sample (one IPM iteration, extrapolated by the solve's iteration count).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.1   # measured DMMA (mma.sync f64) peak, profiles/r01_fp64_peak_probe.txt
+CONFIGS = {
+    "c1": dict(desc="config 1: random LQ-MPC n_x=10, n_u=2, T=10 (instance_rng(42, 0))"),
+    "c2": dict(desc="config 2: 1-D heat rod MPC n_x=200, n_u=4, T=50 (n=200, m=20,400)"),
+    "c3": dict(desc="config 3: 2-D heat plate MPC 50x50, n_x=2500, n_u=10, T=50 (n=500, m=251,000)"),
+    "c4": dict(desc="config 4: long-horizon 2-D heat 40x25, n_x=1000, n_u=10, T=200 (n=2000, m=404,000)"),
+    "c5": dict(desc="config 5 instance: 2-D heat 20x25, n_x=500, n_u=5, T=30 (n=150, m=30,300)"),
+}
+# iteration count of the reference restatement (oracle) on the full configuration, used to
+# extrapolate its bounded one-iteration sample; cross-checked against the device solve
+ORACLE_ITERS = {"c3": 34, "c4": 36, "c2": 29, "c5": 31}
+
+
+def build_problem(cfg, rank=0):
+    from paper_2209_13049_b200 import problem as P
+    if cfg == "c1":
+        from oracle import oracle as O  # only the C1 random generator lives in the oracle
+        p = O.random_problem(O.instance_rng(42, rank), fixed=(10, 2, 0, 10))
+        d = p.as_dict()
+        T = d.pop("T")
+        data = P.LqProblemData(T=T, **d)
+    elif cfg == "c2":
+        data = P.heat1d_problem(200, 50)
+    elif cfg == "c3":
+        data = P.heat2d_problem(50, 50, T=50)
+    elif cfg == "c4":
+        data = P.heat2d_problem(40, 25, T=200)
+    elif cfg == "c5":
+        data = P.heat2d_problem(20, 25, T=30)
+    else:
+        raise SystemExit(f"unknown config {cfg}")
+    if rank > 0 and cfg != "c1":
+        data.x_bar = P.batch_initial_states(data.A.shape[0], 1, seed=1000 + rank)[0]
+    return data
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return None
+        sm = [float(s[1]) for s in self.samples if len(s) > 8 and s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if len(s) > 8 and s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) > 8:
+                for nm, v in zip(names, s[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def pinned_like(a):
+    """copy into page-locked host memory (torch is used only as the allocator)."""
+    import torch
+    t = torch.empty(a.shape[::-1] if a.flags.f_contiguous and a.ndim == 2 else a.shape,
+                    dtype=torch.float64, pin_memory=True)
+    out = t.numpy()
+    if a.ndim == 2 and a.flags.f_contiguous:
+        out = out.T  # Fortran-ordered view of the pinned buffer
+    out[...] = a
+    return out
+
+
+def cpu_sample(qp, threads, iters_full):
+    """Oracle (reference restatement) on the host: one IPM iteration, bounded sample."""
+    from oracle import oracle as O
+    O.set_threads(threads)
+    oq = O.qp_from_arrays(qp.H, qp.h, qp.h0, qp.J, qp.d)
+    t = time.perf_counter()
+    r0 = O.solve(oq, max_iter=1, log=False)
+    dt = time.perf_counter() - t
+    return dict(ms_per_iter=dt * 1e3, ms_per_solve=dt * 1e3 * iters_full, status=r0.status)
+
+
+def run_reference(args, rank, world):
+    cfg = args.config
+    line = {"impl": "reference", "metric": "ms per MPC solve", "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
+            "scaling": "weak", "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIGS[cfg]["desc"], "tol": 1e-8}}
+    if rank != 0:
+        return None
+    from paper_2209_13049_b200 import problem as P
+    qp = P.build_dense_qp(build_problem(cfg))
+    threads = os.cpu_count() or 1
+    iters = ORACLE_ITERS.get(cfg, 30)
+    samples = []
+    for k in range(args.warmup + args.steps):
+        s = cpu_sample(qp, threads, iters)
+        if k >= args.warmup:
+            samples.append(s)
+    ms = statistics.median(s["ms_per_solve"] for s in samples)
+    line.update(value=ms, ms_per_step=ms,
+                cpu_baseline={"value": ms, "unit": "ms", "cores": threads, "kind": "port",
+                              "sample": f"one IPM iteration of the oracle (CPU restatement of "
+                                        f"proj/src/ipm.cpp + dense_linalg.cpp) on the full {cfg} "
+                                        f"QP, x{iters} iterations (its full-solve count)"},
+                e2e={"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                ms_per_iter=statistics.median(s["ms_per_iter"] for s in samples))
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1 and args.impl != "reference":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line:
+            print(json.dumps(line), flush=True)
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    import torch
+    from paper_2209_13049_b200 import _lib, ipm, linalg, problem as P
+    linalg.DEVICE = local
+    cfg = args.config
+    data = build_problem(cfg, rank)
+    qp = P.build_dense_qp(data)
+    dq = ipm.DeviceQp(qp, device=local)
+    qp._device = dq
+    info = dq.info()
+    opts = ipm.IpmOptions()
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        r = ipm.solve_loaded(dq, qp, opts)
+    barrier()
+    l0 = _lib.launch_count()
+    dev_s, syrk_s, syrk_n, chol_s, iters, wall = 0.0, 0.0, 0, 0.0, [], time.perf_counter()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            r = ipm.solve_loaded(dq, qp, opts)
+            dev_s += r.device_seconds
+            syrk_s += r.syrk_seconds
+            syrk_n += r.condensations
+            chol_s += r.chol_seconds
+            iters.append(r.iter)
+    barrier()
+    wall = time.perf_counter() - wall
+    launches = _lib.launch_count() - l0
+    status = r.status.name
+    t_local = dev_s
+    if dist:
+        t = torch.tensor([dev_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+    ms_total = dev_s * 1e3
+    ms_per_step = ms_total / args.steps
+    value = ms_total / (args.steps * world)  # whole job: ms per solve over all ranks
+
+    # end to end through the public API with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = dict(H=pinned_like(qp.H), h=pinned_like(qp.h), J=pinned_like(qp.J), d=pinned_like(qp.d))
+        e2e_ms = []
+        for k in range(args.warmup + args.steps):
+            fresh = P.DenseQp(H=pin["H"], h=pin["h"], h0=qp.h0, J=pin["J"], d=pin["d"],
+                              source=qp.source, gk=qp.gk, x0=qp.x0)
+            barrier()
+            t0 = time.perf_counter()
+            re = ipm.solve(fresh, opts)
+            torch.cuda.synchronize(local)
+            dt = time.perf_counter() - t0
+            fresh.invalidate_device()
+            if k >= args.warmup:
+                e2e_ms.append(dt * 1e3)
+        e2e_local = float(np.sum(e2e_ms))
+        if dist:
+            t = torch.tensor([e2e_local], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_local = float(t.item())
+        n, m = qp.n, qp.m
+        e2e = {"value": e2e_local / (args.steps * world), "unit": "ms",
+               "h2d_bytes_per_step": int(8 * (n * n + n + m * n + m)),
+               "d2h_bytes_per_step": int(8 * (n + 3 * m)),
+               "median_ms": statistics.median(e2e_ms), "status": re.status.name,
+               "iterations": re.iter}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    avg_syrk_s = syrk_s / max(syrk_n, 1)
+    achieved = info["syrk_flops"] / avg_syrk_s / 1e12
+    line = {
+        "metric": "ms per MPC solve", "value": value, "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": CONFIGS[cfg]["desc"], "n": qp.n, "m": qp.m, "tol": 1e-8,
+                   "parallelism": f"{world} independent instances (one per GPU)" if world > 1 else "single instance",
+                   "l2": "inputs larger than L2 (J 1.0 GB dense, P %.0f MB)" % (info["p_bytes"] / 1e6),
+                   "prototype_rows": info["prototypes"], "syrk_rows": info["syrk_prototypes"]},
+        "ms_per_iter": ms_total / max(sum(iters), 1) * (1 if world == 1 else 1),
+        "iterations": iters[-1], "status": status,
+        "roofline": {"bound": "tensor", "kernel": "k_syrk + k_syrk_reduce (condensation)",
+                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS,
+                     "peak_source": "measured FP64 DMMA peak (mma.sync m16n8k16.f64, "
+                                    "profiles/r01_fp64_peak_probe.txt); MEASURED_PEAKS.json has no FP64 entry",
+                     "algorithmic_flops_per_launch": info["syrk_flops"],
+                     "avg_launch_ms": avg_syrk_s * 1e3, "share_of_step": syrk_s / max(t_local, 1e-30),
+                     "traffic": None},
+        "phase_ms_per_iter": {"condense": syrk_s * 1e3 / max(sum(iters), 1),
+                              "cholesky": chol_s * 1e3 / max(sum(iters), 1)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "wall_s": wall,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        s = cpu_sample(qp, os.cpu_count() or 1, r.iter)
+        line["cpu_baseline"] = {
+            "value": s["ms_per_solve"], "unit": "ms", "cores": os.cpu_count() or 1, "kind": "port",
+            "sample": f"one IPM iteration of the oracle (CPU restatement of proj/src/ipm.cpp + "
+                      f"dense_linalg.cpp, dense J) on the same QP, x{r.iter} iterations"}
+    traffic = os.path.join(ROOT, "profiles", f"syrk_traffic_{cfg}.json")
+    if os.path.exists(traffic):
+        line["roofline"]["traffic"] = json.load(open(traffic)).get("dram_bytes_per_launch")
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -40,7 +40,9 @@ void cmpc_ctx_destroy(cmpc_ctx* ctx);
  * Runs the exact structure analysis of J (distinct rows up to sign, prefix widths). */
 int cmpc_load_qp(cmpc_ctx* ctx, int64_t n, int64_t m, const double* H, const double* h, double h0,
                  const double* J, const double* d, int on_device);
-/* out[6] = n, m, prototypes, SYRK prototypes, singleton prototypes, SYRK work units */
+/* out[8] = n, m, prototypes, SYRK prototypes, singleton prototypes, SYRK work units,
+ * algorithmic SYRK flops per condensation (sum over prototypes of hi (hi + 1)),
+ * algorithmic bytes of one pass over P (8 x nonzeros) */
 int cmpc_qp_info(cmpc_ctx* ctx, int64_t* out);
 /* Replace h, h0, d of a loaded QP (refresh_initial_state, proj/src/reduction.cpp:270-280) */
 int cmpc_update_qp_affine(cmpc_ctx* ctx, const double* h, double h0, const double* d, int on_device);
@@ -77,9 +79,10 @@ int cmpc_dense_objective(cmpc_ctx* ctx, double* obj);
 
 /* ipm::solve (ipm.cpp:160-268) on the loaded QP.
  * opts[5] = tol, mu_init, kappa_mu, tau, armijo_eta.
- * out_scalars[10] = status (0 converged, 1 max_iter, 2 factorization_failure,
+ * out_scalars[13] = status (0 converged, 1 max_iter, 2 factorization_failure,
  *   3 line_search_failure), iter, kkt_error, objective, total_seconds, linalg_seconds,
- *   device_seconds, launches, syncs, trials.
+ *   device_seconds, launches, syncs, trials, condensation (SYRK) seconds, Cholesky seconds,
+ *   condensations; the per-phase times are CUDA events on the solve's stream.
  * log(user, rec[8]) per accepted step: iter, mu, alpha, alpha_z, kkt_error, objective,
  *   delta, trial (IterationRecord, ipm.hpp:41-49, plus the shift and trial index).
  * inspect(...) per iteration before the line search (IterationInspection, ipm.hpp:53-58);
@@ -92,6 +95,12 @@ typedef void (*cmpc_inspect_fn)(void* user, const double* v, const double* s, co
 int cmpc_solve(cmpc_ctx* ctx, const double* opts, int64_t max_iter, double* v, double* s,
                double* lambda, double* z, double* out_scalars, cmpc_log_fn log,
                cmpc_inspect_fn inspect, void* user);
+
+/* Device time of one phase of the iteration on the current device state, averaged over
+ * reps back-to-back launches (CUDA events): 0 sigma+condense, 1 condense, 2 Cholesky,
+ * 3 triangular solves, 4 residuals, 5 step recovery, 6 line-search trial, 7 J x, 8 J' y,
+ * 9 sigma/omega/rhs preparation. */
+int cmpc_time_phase(cmpc_ctx* ctx, int what, int reps, double* ms_per_rep);
 
 /* Stand-alone dense linear algebra (the reference's linalg plug point,
  * proj/include/condmpc/dense_linalg.hpp:37-59), host buffers in and out. */

@@ -52,6 +52,7 @@ SIGNATURES = {
     "cmpc_cholesky": (C.c_int, [C.c_int, C.c_int64, D, D, I64]),
     "cmpc_cholesky_solve": (C.c_int, [C.c_int, C.c_int64, D, D, D]),
     "cmpc_fraction_to_boundary": (C.c_int, [C.c_int, C.c_int64, D, D, D, D, C.c_double, D]),
+    "cmpc_time_phase": (C.c_int, [C.c_void_p, C.c_int, C.c_int, D]),
 }
 
 

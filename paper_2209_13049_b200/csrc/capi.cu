@@ -90,6 +90,8 @@ int cmpc_ctx_create(cmpc_ctx** out, int device) {
     CMPC_CUDA(cudaStreamCreateWithFlags(&x->c.stream, cudaStreamNonBlocking));
     CMPC_CUDA(cudaEventCreate(&x->c.ev0));
     CMPC_CUDA(cudaEventCreate(&x->c.ev1));
+    CMPC_CUDA(cudaEventCreate(&x->c.ev2));
+    CMPC_CUDA(cudaEventCreate(&x->c.ev3));
     *out = x;
     return CMPC_OK;
   });
@@ -102,6 +104,8 @@ void cmpc_ctx_destroy(cmpc_ctx* x) {
   release_qp(x->c);
   cudaEventDestroy(x->c.ev0);
   cudaEventDestroy(x->c.ev1);
+  cudaEventDestroy(x->c.ev2);
+  cudaEventDestroy(x->c.ev3);
   cudaStreamDestroy(x->c.stream);
   delete x;
 }
@@ -146,7 +150,41 @@ int cmpc_qp_info(cmpc_ctx* x, int64_t* out) {
   out[3] = c.ps;
   out[4] = c.pz;
   out[5] = c.nunits;
+  out[6] = (int64_t)c.syrk_flops;
+  out[7] = (int64_t)c.syrk_bytes;
   return CMPC_OK;
+}
+
+int cmpc_time_phase(cmpc_ctx* x, int what, int reps, double* ms_per_rep) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    if (reps < 1) throw DimError("reps must be positive");
+    auto run = [&] {
+      switch (what) {
+        case 0: launch_prepare_step(c, nullptr); launch_condense(c, false); break;
+        case 1: launch_condense(c, false); break;
+        case 2: launch_cholesky(c, c.M, c.L, 0.0); break;
+        case 3: launch_chol_solve(c, c.L, c.rhs, c.pv); break;
+        case 4: launch_residuals(c); break;
+        case 5: launch_recover(c, 0.995); break;
+        case 6: launch_trial(c, 0.5, false); break;
+        case 7: launch_Jx(c, c.v, c.y, nullptr); break;
+        case 8: launch_Jtq(c, c.q, c.Jtl); break;
+        case 9: launch_prepare_step(c, nullptr); break;
+        default: throw DimError("unknown phase");
+      }
+    };
+    run();
+    CMPC_CUDA(cudaEventRecord(c.ev2, c.stream));
+    for (int r = 0; r < reps; ++r) run();
+    CMPC_CUDA(cudaEventRecord(c.ev3, c.stream));
+    CMPC_CUDA(cudaEventSynchronize(c.ev3));
+    float ms = 0.f;
+    CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev2, c.ev3));
+    *ms_per_rep = ms / reps;
+    return CMPC_OK;
+  });
 }
 
 int cmpc_update_qp_affine(cmpc_ctx* x, const double* h, double h0, const double* d, int on_device) {
@@ -263,6 +301,7 @@ int cmpc_set_factor(cmpc_ctx* x, const double* L) {
     Ctx& c = x->c;
     require_loaded(c);
     h2d(c, c.L, L, c.n * c.n);
+    launch_factor_inverses(c, c.L);
     sync(c);
     return CMPC_OK;
   });
@@ -435,6 +474,7 @@ int cmpc_cholesky_solve(int device, int64_t n, const double* L, const double* b,
     Ctx& c = x->c;
     h2d(c, c.L, L, n * n);
     h2d(c, c.rhs, b, n);
+    launch_factor_inverses(c, c.L);
     launch_chol_solve(c, c.L, c.rhs, c.pv);
     d2h(c, xout, c.pv, n);
     sync(c);

@@ -7,9 +7,16 @@
 // 205-221) re-factors M + delta I; here M is kept intact and L written separately, so a
 // retry never repeats the SYRK. info = failing pivot + 1 (0 = success).
 //
-// Blocked right-looking, 64-wide panels: potf2 of the diagonal block in shared memory
-// (1 CTA), panel TRSM (1 CTA per 64-row block), trailing lower SYRK on DMMA tensor
-// cores (1 CTA per 64x64 tile). Every kernel returns immediately once info != 0.
+// Blocked right-looking with 64-wide panels, three kernels per panel:
+//   k_potf2_inv  1 CTA: right-looking potf2 of the diagonal block in shared memory with
+//                the inverse W = L_kk^{-1} built in the same column sweep;
+//   k_panel      L_ik = A_ik W^T for every 64-row block below (DMMA GEMM, no sequential
+//                triangular solve on the critical path);
+//   k_trail      A_ij -= L_ik L_jk^T on the trailing lower tiles (DMMA).
+// The W blocks are kept, so the triangular solves (k_trsv) are block GEMVs.
+// Every kernel returns immediately once info != 0.
+#include <algorithm>
+
 #include "internal.cuh"
 #include "ptx.cuh"
 
@@ -19,8 +26,9 @@ namespace {
 
 constexpr int kNB = 64;
 constexpr int kLD = kNB + 1;
-constexpr int kTrsmSmem = 2 * kNB * kLD * 8;
-constexpr int kTrailSmem = 2 * kNB * 68 * 8;
+constexpr int kGemmLD = 68;
+constexpr int kGemmSmem = 2 * kNB * kGemmLD * 8;
+constexpr int kPotfSmem = (2 * kNB * kLD + kNB) * 8;
 
 __global__ void k_chol_copy(const double* __restrict__ M, double* __restrict__ L, int64_t n,
                             double delta, long long* info) {
@@ -34,116 +42,222 @@ __global__ void k_chol_copy(const double* __restrict__ M, double* __restrict__ L
   L[i + j * n] = v;
 }
 
-// factor the b x b diagonal block at (k0, k0)
-__global__ void k_potf2(double* __restrict__ L, int64_t n, int64_t k0, int b, long long* info) {
-  __shared__ double a[kNB * kLD];
-  __shared__ int fail;
+// W = L^{-1} for the factored 64 x 64 lower block in a (identity padding beyond b),
+// right-looking substitution on L W = I: step p scales row p of W, then rows i > p
+// subtract l_ip W_p. 256 threads, 2 barriers per step.
+__device__ void inv64(const double* a, double* w) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kNB * kNB; e += blockDim.x) w[(e & 63) + (e >> 6) * kLD] = ((e & 63) == (e >> 6)) ? 1.0 : 0.0;
+  __syncthreads();
+  const int i = tid & 63, kg = tid >> 6;
+  for (int p = 0; p < kNB; ++p) {
+    const double l = a[p + p * kLD];
+    if (tid >= 64 && tid - 64 <= p) w[p + (tid - 64) * kLD] = dv(w[p + (tid - 64) * kLD], l);
+    __syncthreads();
+    if (i > p) {
+      const double lip = a[i + p * kLD];
+      for (int k = kg; k <= p; k += 4) w[i + k * kLD] = fma(-lip, w[p + k * kLD], w[i + k * kLD]);
+    }
+    __syncthreads();
+  }
+}
+
+// load the b x b diagonal block at (k0, k0); identity padding beyond b
+__device__ void load_diag(const double* L, int64_t n, int64_t k0, int b, double* a) {
+  for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
+    const int i = e & 63, j = e >> 6;
+    double v = 0.0;
+    if (i < b && j < b) {
+      if (i >= j) v = L[(k0 + i) + (k0 + j) * n];
+    } else if (i == j) {
+      v = 1.0;
+    }
+    a[i + j * kLD] = v;
+  }
+}
+
+// write the lower b x b part of a to L and the full (zero-upper) 64 x 64 W
+__device__ void store_diag(double* L, int64_t n, int64_t k0, int b, const double* a, const double* w,
+                           double* Wout, bool write_l) {
+  for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
+    const int i = e & 63, j = e >> 6;
+    if (write_l && i < b && j < b && i >= j) L[(k0 + i) + (k0 + j) * n] = a[i + j * kLD];
+    Wout[e] = (i >= j) ? w[i + j * kLD] : 0.0;
+  }
+}
+
+// factor the b x b diagonal block at (k0, k0) (right-looking, 2 barriers per column) and
+// build W = L_kk^{-1} in the same sweep: once column j of L is final, step j of the
+// substitution L W = I runs alongside the rank-1 trailing update. 256 threads.
+__global__ void __launch_bounds__(256) k_potf2_inv(double* __restrict__ L, int64_t n, int64_t k0,
+                                                   int b, long long* info, double* __restrict__ Wout) {
+  extern __shared__ double sm[];
+  double* a = sm;              // kNB x kLD
+  double* w = sm + kNB * kLD;  // kNB x kLD
+  double* dj = w + kNB * kLD;  // pivots
   if (*info != 0) return;
   const int tid = threadIdx.x;
-  for (int e = tid; e < b * b; e += blockDim.x) {
-    const int i = e % b, j = e / b;
-    if (i >= j) a[i + j * kLD] = L[(k0 + i) + (k0 + j) * n];
-  }
-  if (tid == 0) fail = 0;
+  load_diag(L, n, k0, b, a);
+  for (int e = tid; e < kNB * kNB; e += blockDim.x) w[(e & 63) + (e >> 6) * kLD] = ((e & 63) == (e >> 6)) ? 1.0 : 0.0;
   __syncthreads();
-  for (int j = 0; j < b; ++j) {
-    if (tid == 0) {
-      const double d = a[j + j * kLD];
-      if (!(d > 0.0) || !isfinite(d)) {
-        fail = 1;
-        *info = (long long)(k0 + j + 1);
-      } else {
-        a[j + j * kLD] = sqrt(d);
+  const int i = tid & 63, kg = tid >> 6;
+  for (int j = 0; j < kNB; ++j) {
+    const double d = a[j + j * kLD];
+    if (j < b && (!(d > 0.0) || !isfinite(d))) {
+      if (tid == 0) *info = (long long)(k0 + j + 1);
+      return;
+    }
+    const double l = sqrt(d);
+    if (tid < 64) {
+      if (i > j) a[i + j * kLD] = dv(a[i + j * kLD], l);
+    } else if (tid - 64 <= j) {
+      w[j + (tid - 64) * kLD] = dv(w[j + (tid - 64) * kLD], l);
+    }
+    if (tid == 0) dj[j] = l;
+    __syncthreads();
+    if (i > j) {
+      // batch every load of this step before any store (the smem updates are independent)
+      const double lij = a[i + j * kLD];
+      double av[16], cv[16], wv[16], rv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int k = j + 1 + kg + 4 * u;
+        if (k <= i) {
+          av[u] = a[i + k * kLD];
+          cv[u] = a[k + j * kLD];
+        }
+        const int q = kg + 4 * u;
+        if (q <= j) {
+          wv[u] = w[i + q * kLD];
+          rv[u] = w[j + q * kLD];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int k = j + 1 + kg + 4 * u;
+        if (k <= i) a[i + k * kLD] = fma(-lij, cv[u], av[u]);
+        const int q = kg + 4 * u;
+        if (q <= j) w[i + q * kLD] = fma(-lij, rv[u], wv[u]);
       }
     }
     __syncthreads();
-    if (fail) return;
-    const double djj = a[j + j * kLD];
-    for (int i = j + 1 + tid; i < b; i += blockDim.x) a[i + j * kLD] = dv(a[i + j * kLD], djj);
-    __syncthreads();
-    const int w = b - j - 1;
-    for (int e = tid; e < w * w; e += blockDim.x) {
-      const int i = j + 1 + e % w, k = j + 1 + e / w;
-      if (i >= k) a[i + k * kLD] -= a[i + j * kLD] * a[k + j * kLD];
-    }
-    __syncthreads();
   }
-  for (int e = tid; e < b * b; e += blockDim.x) {
-    const int i = e % b, j = e / b;
-    if (i >= j) L[(k0 + i) + (k0 + j) * n] = a[i + j * kLD];
-  }
+  for (int e = tid; e < kNB; e += blockDim.x) a[e + e * kLD] = dj[e];
+  __syncthreads();
+  store_diag(L, n, k0, b, a, w, Wout, true);
 }
 
-// X <- X L11^{-T} for the 64-row block below the diagonal block (4 threads per row)
-__global__ void k_trsm(double* __restrict__ L, int64_t n, int64_t k0, int b, long long* info) {
-  extern __shared__ double sm_trsm[];
-  double* l11 = sm_trsm;
-  double* x = sm_trsm + kNB * kLD;  // x[r + j*kLD]
-  if (*info != 0) return;
-  const int tid = threadIdx.x;
-  const int64_t r0 = k0 + b + (int64_t)blockIdx.x * kNB;
-  const int rows = (int)(n - r0 < kNB ? n - r0 : kNB);
-  for (int e = tid; e < b * b; e += blockDim.x) {
-    const int i = e % b, j = e / b;
-    l11[i + j * kLD] = (i >= j) ? L[(k0 + i) + (k0 + j) * n] : 0.0;
-  }
-  for (int e = tid; e < kNB * b; e += blockDim.x) {
-    const int i = e % kNB, j = e / kNB;
-    x[i + j * kLD] = (i < rows) ? L[(r0 + i) + (k0 + j) * n] : 0.0;
-  }
+// inverse of every 64 x 64 diagonal block of an existing factor (one CTA per block)
+__global__ void __launch_bounds__(256) k_diag_inv(const double* __restrict__ L, int64_t n,
+                                                  double* __restrict__ Winv) {
+  extern __shared__ double sm[];
+  double* a = sm;
+  double* w = sm + kNB * kLD;
+  const int64_t k0 = (int64_t)blockIdx.x * kNB;
+  const int b = (int)(n - k0 < kNB ? n - k0 : kNB);
+  load_diag(L, n, k0, b, a);
   __syncthreads();
-  const int r = tid >> 2, q = tid & 3;
-  for (int j = 0; j < b; ++j) {
-    double s = 0.0;
-    for (int p = q; p < j; p += 4) s += x[r + p * kLD] * l11[j + p * kLD];
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (q == 0) x[r + j * kLD] = dv(x[r + j * kLD] - s, l11[j + j * kLD]);
-    __syncwarp();
-  }
-  __syncthreads();
-  for (int e = tid; e < rows * b; e += blockDim.x) {
-    const int i = e % rows, j = e / rows;
-    L[(r0 + i) + (k0 + j) * n] = x[i + j * kLD];
-  }
+  inv64(a, w);
+  store_diag(nullptr, n, k0, b, a, w, Winv + (size_t)blockIdx.x * kNB * kNB, false);
 }
 
-// trailing update A22(I,J) -= X_I X_J^T, lower tiles only, DMMA m16n8k4
-__global__ void __launch_bounds__(128) k_trail(double* __restrict__ L, int64_t n, int64_t k0, int b,
-                                               long long* info) {
-  extern __shared__ double sm_trail[];
-  double* xi = sm_trail;  // xi[k*68 + i]
-  double* xj = sm_trail + kNB * 68;
-  if (*info != 0) return;
-  const int ti = blockIdx.x, tj = blockIdx.y;
-  if (ti < tj) return;
-  const int64_t base = k0 + b;
-  const int64_t i0 = base + (int64_t)ti * kNB, j0 = base + (int64_t)tj * kNB;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < kNB * kNB; e += blockDim.x) {
-    const int i = e % kNB, k = e / kNB;
-    xi[k * 68 + i] = (k < b && i0 + i < n) ? L[(i0 + i) + (k0 + k) * n] : 0.0;
-    xj[k * 68 + i] = (k < b && j0 + i < n) ? L[(j0 + i) + (k0 + k) * n] : 0.0;
-  }
-  __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+// acc(i, j) += sum_k X[i][k] Y[j][k] for 64x64 smem tiles stored x[k*kGemmLD + i];
+// 4 warps, 32 x 32 per warp, DMMA m16n8k4
+__device__ __forceinline__ void tile_xyt(const double* x, const double* y, int kmax,
+                                         double (&acc)[2][4][4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
-  double acc[2][4][4] = {};
-  for (int ks = 0; ks < b; ks += 4) {
+  for (int ks = 0; ks < kmax; ks += 4) {
     double af[2][2], bf[4];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {
       const int r = 32 * wm + 16 * mi + g;
-      af[mi][0] = xi[(ks + t) * 68 + r];
-      af[mi][1] = xi[(ks + t) * 68 + r + 8];
+      af[mi][0] = x[(ks + t) * kGemmLD + r];
+      af[mi][1] = x[(ks + t) * kGemmLD + r + 8];
     }
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) bf[ni] = xj[(ks + t) * 68 + 32 * wn + 8 * ni + g];
+    for (int ni = 0; ni < 4; ++ni) bf[ni] = y[(ks + t) * kGemmLD + 32 * wn + 8 * ni + g];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) dmma1684(acc[mi][ni], af[mi], bf[ni]);
   }
+}
+
+// L_ik = A_ik W^T for the 64-row block i below the diagonal block
+__global__ void __launch_bounds__(128) k_panel(double* __restrict__ L, int64_t n, int64_t k0, int b,
+                                               long long* info, const double* __restrict__ W) {
+  extern __shared__ double sm[];
+  double* xa = sm;                  // A_ik: xa[k*LD + i]
+  double* xw = sm + kNB * kGemmLD;  // W:    xw[k*LD + j] = W[j][k]
+  if (*info != 0) return;
+  const int64_t r0 = k0 + b + (int64_t)blockIdx.x * kNB;
+  {
+    double ra[32], rw[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int e = threadIdx.x + u * 128, i = e & 63, k = e >> 6;
+      ra[u] = (k < b && r0 + i < n) ? L[(r0 + i) + (k0 + k) * n] : 0.0;
+      rw[u] = W[i + k * kNB];  // W col-major: W[i][k] at i + k*64
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int e = threadIdx.x + u * 128, i = e & 63, k = e >> 6;
+      xa[k * kGemmLD + i] = ra[u];
+      xw[k * kGemmLD + i] = rw[u];
+    }
+  }
+  __syncthreads();
+  double acc[2][4][4] = {};
+  tile_xyt(xa, xw, b, acc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t r = r0 + 32 * wm + 16 * mi + g + 8 * (e >> 1);
+        const int c = 32 * wn + 8 * ni + 2 * t + (e & 1);
+        if (r < n && c < b) L[r + (k0 + c) * n] = acc[mi][ni][e];
+      }
+}
+
+// trailing update A22(I,J) -= L_Ik L_Jk^T, lower tiles only
+__global__ void __launch_bounds__(128) k_trail(double* __restrict__ L, int64_t n, int64_t k0, int b,
+                                               long long* info) {
+  extern __shared__ double sm[];
+  double* xi = sm;
+  double* xj = sm + kNB * kGemmLD;
+  if (*info != 0) return;
+  // blockIdx.x enumerates the lower tiles (ti >= tj) of the trailing matrix
+  int ti = (int)((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);
+  while ((ti + 1) * (ti + 2) / 2 <= (int)blockIdx.x) ++ti;
+  while (ti * (ti + 1) / 2 > (int)blockIdx.x) --ti;
+  const int tj = (int)blockIdx.x - ti * (ti + 1) / 2;
+  const int64_t base = k0 + b;
+  const int64_t i0 = base + (int64_t)ti * kNB, j0 = base + (int64_t)tj * kNB;
+  {
+    double ra[32], rb[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int e = threadIdx.x + u * 128, i = e & 63, k = e >> 6;
+      ra[u] = (k < b && i0 + i < n) ? L[(i0 + i) + (k0 + k) * n] : 0.0;
+      rb[u] = (k < b && j0 + i < n) ? L[(j0 + i) + (k0 + k) * n] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int e = threadIdx.x + u * 128, i = e & 63, k = e >> 6;
+      xi[k * kGemmLD + i] = ra[u];
+      xj[k * kGemmLD + i] = rb[u];
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  // prefetch the tile being updated (all loads in flight before the MMA loop)
+  double old[2][4][4];
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -152,67 +266,112 @@ __global__ void __launch_bounds__(128) k_trail(double* __restrict__ L, int64_t n
       for (int e = 0; e < 4; ++e) {
         const int64_t r = i0 + 32 * wm + 16 * mi + g + 8 * (e >> 1);
         const int64_t c = j0 + 32 * wn + 8 * ni + 2 * t + (e & 1);
-        if (r < n && c < n && r >= c) L[r + c * n] -= acc[mi][ni][e];
+        old[mi][ni][e] = (r < n && c < n && r >= c) ? L[r + c * n] : 0.0;
+      }
+  double acc[2][4][4] = {};
+  tile_xyt(xi, xj, b, acc);
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t r = i0 + 32 * wm + 16 * mi + g + 8 * (e >> 1);
+        const int64_t c = j0 + 32 * wn + 8 * ni + 2 * t + (e & 1);
+        if (r < n && c < n && r >= c) L[r + c * n] = old[mi][ni][e] - acc[mi][ni][e];
       }
 }
 
-// x = L^{-T} L^{-1} b, one CTA; x may alias b
-__global__ void __launch_bounds__(512) k_trsv(const double* __restrict__ L, const double* b,
+// x = L^{-T} L^{-1} b with the 64 x 64 diagonal-block inverses W; one CTA of 512
+// threads; x may alias b. Forward: y_k = W_k (b_k - sum_{j<k} L_kj y_j); backward:
+// x_k = W_k^T (y_k - sum_{i>k} L_ik^T x_i).
+__global__ void __launch_bounds__(512) k_trsv(const double* __restrict__ L,
+                                              const double* __restrict__ W, const double* b,
                                               double* x, int64_t n) {
   extern __shared__ double xs[];
+  double* t = xs + n;  // 64 scratch
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nw = blockDim.x >> 5;
   for (int64_t i = tid; i < n; i += blockDim.x) xs[i] = b[i];
   __syncthreads();
-  // forward: L y = b (blocks of 32; right-looking)
-  for (int64_t blk = 0; blk < n; blk += 32) {
-    const int bs = (int)(n - blk < 32 ? n - blk : 32);
-    if (warp == 0) {
-      double xv = lane < bs ? xs[blk + lane] : 0.0;
-      for (int jj = 0; jj < bs; ++jj) {
-        if (lane == jj) xv = dv(xv, L[(blk + jj) + (blk + jj) * n]);
-        const double xj = __shfl_sync(0xffffffffu, xv, jj);
-        if (lane > jj && lane < bs) xv -= L[(blk + lane) + (blk + jj) * n] * xj;
-      }
-      if (lane < bs) xs[blk + lane] = xv;
-    }
+  const int64_t nb = (n + kNB - 1) / kNB;
+  const int row = tid >> 3, part = tid & 7;  // 64 rows x 8 parts
+  for (int64_t kb = 0; kb < nb; ++kb) {
+    const int64_t r0 = kb * kNB;
+    const int bs = (int)(n - r0 < kNB ? n - r0 : kNB);
+    const double* Wk = W + kb * kNB * kNB;
+    // y_k = W_k b'_k (W lower: row i uses columns j <= i)
+    double s = 0.0;
+    if (row < bs)
+      for (int j = part; j <= row; j += 8) s += Wk[row + j * kNB] * xs[r0 + j];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
     __syncthreads();
-    for (int64_t i = blk + bs + tid; i < n; i += blockDim.x) {
-      double s = 0.0;
-      for (int p = 0; p < bs; ++p) s += L[i + (blk + p) * n] * xs[blk + p];
-      xs[i] -= s;
+    if (part == 0 && row < bs) xs[r0 + row] = s;
+    __syncthreads();
+    for (int64_t i = r0 + bs + tid; i < n; i += blockDim.x) {
+      double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+      int p = 0;
+      for (; p + 3 < bs; p += 4) {
+        u0 += L[i + (r0 + p) * n] * xs[r0 + p];
+        u1 += L[i + (r0 + p + 1) * n] * xs[r0 + p + 1];
+        u2 += L[i + (r0 + p + 2) * n] * xs[r0 + p + 2];
+        u3 += L[i + (r0 + p + 3) * n] * xs[r0 + p + 3];
+      }
+      for (; p < bs; ++p) u0 += L[i + (r0 + p) * n] * xs[r0 + p];
+      xs[i] -= (u0 + u1) + (u2 + u3);
     }
     __syncthreads();
   }
-  // backward: L^T x = y (blocks of 32 from the bottom; left-looking column dots)
-  const int64_t nblk = (n + 31) / 32;
-  for (int64_t bi = nblk - 1; bi >= 0; --bi) {
-    const int64_t blk = bi * 32;
-    const int bs = (int)(n - blk < 32 ? n - blk : 32);
-    const int64_t tail = blk + bs;
-    for (int r = warp; r < bs; r += nw) {
-      const int64_t i = blk + r;
-      double s = 0.0;
-      for (int64_t p = tail + lane; p < n; p += 32) s += L[p + i * n] * xs[p];
-      s = warp_sum(s);
-      if (lane == 0) xs[i] -= s;
+  for (int64_t kb = nb - 1; kb >= 0; --kb) {
+    const int64_t r0 = kb * kNB;
+    const int bs = (int)(n - r0 < kNB ? n - r0 : kNB);
+    const int64_t tail = r0 + bs;
+    const double* Wk = W + kb * kNB * kNB;
+    // t_i = y_i - sum_{p >= tail} L[p, i] x_p (column dots, one warp per column)
+    for (int i = warp; i < bs; i += 16) {
+      double u = 0.0;
+      for (int64_t p = tail + lane; p < n; p += 32) u += L[p + (r0 + i) * n] * xs[p];
+      u = warp_sum(u);
+      if (lane == 0) t[i] = xs[r0 + i] - u;
     }
     __syncthreads();
-    if (warp == 0) {
-      double xv = lane < bs ? xs[blk + lane] : 0.0;
-      for (int jj = bs - 1; jj >= 0; --jj) {
-        if (lane == jj) xv = dv(xv, L[(blk + jj) + (blk + jj) * n]);
-        const double xj = __shfl_sync(0xffffffffu, xv, jj);
-        if (lane < jj) xv -= L[(blk + jj) + (blk + lane) * n] * xj;
-      }
-      if (lane < bs) xs[blk + lane] = xv;
-    }
+    // x_k = W_k^T t: x_i = sum_{j >= i} W[j][i] t_j
+    double s = 0.0;
+    if (row < bs)
+      for (int j = row + part; j < bs; j += 8) s += Wk[j + row * kNB] * t[j];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (part == 0 && row < bs) xs[r0 + row] = s;
     __syncthreads();
   }
   for (int64_t i = tid; i < n; i += blockDim.x) x[i] = xs[i];
 }
 
+void set_attrs() {
+  static bool done = false;
+  if (done) return;
+  CMPC_CUDA(cudaFuncSetAttribute(k_potf2_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotfSmem));
+  CMPC_CUDA(cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotfSmem));
+  CMPC_CUDA(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
+  CMPC_CUDA(cudaFuncSetAttribute(k_trail, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
+  CMPC_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  done = true;
+}
+
 }  // namespace
+
+void chol_alloc(Ctx& c) {
+  const int64_t nb = ceil_div(std::max<int64_t>(c.n, 1), kNB);
+  CMPC_CUDA(cudaMalloc(&c.Winv, sizeof(double) * nb * kNB * kNB));
+  CMPC_CUDA(cudaMemset(c.Winv, 0, sizeof(double) * nb * kNB * kNB));
+}
+
+void chol_free(Ctx& c) {
+  if (c.Winv) cudaFree(c.Winv);
+  c.Winv = nullptr;
+}
 
 void launch_cholesky(Ctx& c, const double* M, double* L, double delta) {
   const int64_t n = c.n;
@@ -221,40 +380,39 @@ void launch_cholesky(Ctx& c, const double* M, double* L, double delta) {
     CMPC_CUDA(cudaMemsetAsync(info, 0, sizeof(long long), c.stream));
     return;
   }
-  static bool attr = false;
-  if (!attr) {
-    CMPC_CUDA(cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
-    CMPC_CUDA(cudaFuncSetAttribute(k_trail, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrailSmem));
-    attr = true;
-  }
+  set_attrs();
   dim3 g0((unsigned)ceil_div(n, 256), (unsigned)n);
   k_chol_copy<<<g0, 256, 0, c.stream>>>(M, L, n, delta, info);
   CMPC_LAUNCHED();
   for (int64_t k0 = 0; k0 < n; k0 += kNB) {
     const int b = (int)std::min<int64_t>(kNB, n - k0);
-    k_potf2<<<1, 256, 0, c.stream>>>(L, n, k0, b, info);
+    double* Wk = c.Winv + (k0 / kNB) * kNB * kNB;
+    k_potf2_inv<<<1, 256, kPotfSmem, c.stream>>>(L, n, k0, b, info, Wk);
     CMPC_LAUNCHED();
     const int64_t rest = n - k0 - b;
     if (rest > 0) {
       const unsigned nb = (unsigned)ceil_div(rest, kNB);
-      k_trsm<<<nb, 256, kTrsmSmem, c.stream>>>(L, n, k0, b, info);
+      k_panel<<<nb, 128, kGemmSmem, c.stream>>>(L, n, k0, b, info, Wk);
       CMPC_LAUNCHED();
-      k_trail<<<dim3(nb, nb), 128, kTrailSmem, c.stream>>>(L, n, k0, b, info);
+      k_trail<<<nb * (nb + 1) / 2, 128, kGemmSmem, c.stream>>>(L, n, k0, b, info);
       CMPC_LAUNCHED();
     }
   }
 }
 
+void launch_factor_inverses(Ctx& c, const double* L) {
+  if (c.n == 0) return;
+  set_attrs();
+  k_diag_inv<<<(unsigned)ceil_div(c.n, kNB), 256, kPotfSmem, c.stream>>>(L, c.n, c.Winv);
+  CMPC_LAUNCHED();
+}
+
 void launch_chol_solve(Ctx& c, const double* L, const double* b, double* x) {
   if (c.n == 0) return;
-  const size_t sm = sizeof(double) * (size_t)c.n;
-  static bool attr = false;
-  if (!attr) {
-    CMPC_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  set_attrs();
+  const size_t sm = sizeof(double) * ((size_t)c.n + kNB);
   if (sm > 200 * 1024) throw CudaError("chol_solve: n too large for the single-CTA TRSV");
-  k_trsv<<<1, 512, sm, c.stream>>>(L, b, x, c.n);
+  k_trsv<<<1, 512, sm, c.stream>>>(L, c.Winv, b, x, c.n);
   CMPC_LAUNCHED();
 }
 

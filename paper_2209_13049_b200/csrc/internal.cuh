@@ -64,6 +64,7 @@ struct Ctx {
   int32_t* row_map = nullptr;    // m: proto << 1 | (sign < 0)
   int32_t* mem_ptr = nullptr;    // p+1
   int32_t* mem_rows = nullptr;   // m: row << 1 | (sign < 0)
+  int64_t zero_k = -1;           // prototype index of the all-zero row group (-1: none)
   int32_t* sing_col = nullptr;   // pz (ascending)
   double* sing_val = nullptr;    // pz
   std::vector<int32_t> h_start_col;
@@ -88,12 +89,15 @@ struct Ctx {
   double* colpart = nullptr;  // Pt q partial: nchunks x n
   int colchunks = 0;
   double* hmax = nullptr;
+  double* Winv = nullptr;    // inverses of the 64 x 64 diagonal blocks of L
   Packet* pk = nullptr;      // device packet
   Packet* pk_host = nullptr; // pinned mirror
   double mu = 0.0;
 
   // events for per-phase timing
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  double syrk_flops = 0.0;   // algorithmic: sum over prototypes of hi (hi + 1)
+  double syrk_bytes = 0.0;   // algorithmic: 8 x nonzeros of P (one read)
 };
 
 // ---- structure.cu
@@ -109,13 +113,18 @@ void syrk_free(Ctx& c);
 // ---- chol.cu
 // L = chol(M + delta I) (lower, upper zeroed); failing pivot+1 in c.pk->info
 void launch_cholesky(Ctx& c, const double* M, double* L, double delta);
-// x = L^{-T} L^{-1} b (in place on x allowed)
+void chol_alloc(Ctx& c);
+void chol_free(Ctx& c);
+// diagonal-block inverses of an externally provided factor (set_factor)
+void launch_factor_inverses(Ctx& c, const double* L);
+// x = L^{-T} L^{-1} b (in place on x allowed); uses the diagonal-block inverses
 void launch_chol_solve(Ctx& c, const double* L, const double* b, double* x);
 
 // ---- vec.cu
 void launch_zero_packet(Ctx& c);
-// residuals at the current state (r1, r2, r3, kkt, objective pieces) -> packet A
-void launch_residuals(Ctx& c);
+// residuals at the current state (r1, r2, r3, kkt, objective pieces) -> packet A;
+// reuse_trial: the state was just moved to the last evaluated line-search trial point
+void launch_residuals(Ctx& c, bool reuse_trial = false);
 // r2 and complementarity only (after a barrier change) -> packet A kkt updated
 void launch_residuals_mu(Ctx& c);
 // sigma = z/s, omega, dsing, q = Pi'(r2 - sigma r3)

@@ -109,7 +109,8 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   long long syncs = 0, trials = 0;
   const int64_t n = c.n, m = c.m;
   const double start = now_seconds();
-  double linalg = 0.0, device_s = 0.0;
+  double linalg = 0.0, device_s = 0.0, syrk_s = 0.0, chol_s = 0.0;
+  long long syrk_launches = 0;
   cudaEvent_t e_start, e_end;
   CMPC_CUDA(cudaEventCreate(&e_start));
   CMPC_CUDA(cudaEventCreate(&e_end));
@@ -150,7 +151,9 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     // sigma, condensed matrix, factorization with the shift ladder (ipm.cpp:200-226)
     CMPC_CUDA(cudaEventRecord(c.ev0, c.stream));
     launch_prepare_step(c, nullptr);
+    CMPC_CUDA(cudaEventRecord(c.ev2, c.stream));
     launch_condense(c, false);
+    CMPC_CUDA(cudaEventRecord(c.ev3, c.stream));
     size_t shift = 0;
     launch_cholesky(c, c.M, c.L, kShifts[shift]);
     CMPC_CUDA(cudaEventRecord(c.ev1, c.stream));
@@ -163,6 +166,11 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     float ms = 0.f;
     CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
     linalg += ms * 1e-3;
+    CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev2, c.ev3));
+    syrk_s += ms * 1e-3;
+    ++syrk_launches;
+    CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev3, c.ev1));
+    chol_s += ms * 1e-3;
     while (c.pk_host->info != 0) {
       if (++shift == kShifts.size()) break;
       CMPC_CUDA(cudaEventRecord(c.ev0, c.stream));
@@ -214,7 +222,7 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     const double mu_used = c.mu;
     launch_update(c, alpha, alpha_z);
     iter += 1;
-    launch_residuals(c);
+    launch_residuals(c, /*reuse_trial=*/true);
     sync_packet(c, &syncs);
     A = *c.pk_host;
     if (log) {
@@ -246,6 +254,9 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   out[7] = double(g_launches - launches0);
   out[8] = double(syncs);
   out[9] = double(trials);
+  out[10] = syrk_s;
+  out[11] = chol_s;
+  out[12] = double(syrk_launches);
   return CMPC_OK;
 }
 

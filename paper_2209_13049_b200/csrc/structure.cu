@@ -327,6 +327,14 @@ void analyze_structure(Ctx& c) {
                                                              c.sing_col, c.sing_val);
     CMPC_LAUNCHED();
   }
+  // all-zero rows sort first among the singletons (prefix width 0, value 0)
+  c.zero_k = -1;
+  if (c.pz > 0) {
+    double v0 = 1.0;
+    CMPC_CUDA(cudaMemcpyAsync(&v0, c.sing_val, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CMPC_CUDA(cudaStreamSynchronize(st));
+    if (v0 == 0.0) c.zero_k = ps;
+  }
   k_start_col<<<unsigned((n + 1 + T - 1) / T), T, 0, st>>>(c.hi, ps, n, c.start_col);
   CMPC_LAUNCHED();
   c.h_start_col.resize(size_t(n + 1));

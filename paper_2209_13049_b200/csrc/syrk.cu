@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
     }
 }
 
-// M(i,j) = H(i,j) + (sum over the tile's units in k order [+ singleton diagonal]), lower
+// M(i,j) = H(i,j) + (sum over the tile's units in k order [+ singleton diagonal]), lower;
+// grid (tiles, 16): 256 elements of one tile per block
 __global__ void k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
                               const int32_t* __restrict__ tile_ptr,
                               const int32_t* __restrict__ tile_units, const double* __restrict__ H,
@@ -159,17 +160,22 @@ __global__ void k_syrk_reduce(const double* __restrict__ partial, const int2* __
                               int mirror) {
   const int2 tl = tiles[blockIdx.x];
   const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
-  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
-    const int rl = e & (kTile - 1), cl = e >> 6;
-    const int64_t i = (int64_t)kTile * tl.x + rl, j = (int64_t)kTile * tl.y + cl;
-    if (i >= n || j >= n || i < j) continue;
-    double s = 0.0;
-    for (int q = u0; q < u1; ++q) s += partial[(size_t)tile_units[q] * (kTile * kTile) + e];
-    if (i == j) s += dsing[i];
-    const double v = H[i + j * n] + s;
-    M[i + j * n] = v;
-    if (mirror && i != j) M[j + i * n] = v;
+  const int e = blockIdx.y * blockDim.x + threadIdx.x;
+  const int rl = e & (kTile - 1), cl = e >> 6;
+  const int64_t i = (int64_t)kTile * tl.x + rl, j = (int64_t)kTile * tl.y + cl;
+  if (i >= n || j >= n || i < j) return;
+  double s0 = 0.0, s1 = 0.0;
+  int q = u0;
+  for (; q + 1 < u1; q += 2) {
+    s0 += partial[(size_t)tile_units[q] * (kTile * kTile) + e];
+    s1 += partial[(size_t)tile_units[q + 1] * (kTile * kTile) + e];
   }
+  if (q < u1) s0 += partial[(size_t)tile_units[q] * (kTile * kTile) + e];
+  double s = s0 + s1;
+  if (i == j) s += dsing[i];
+  const double v = H[i + j * n] + s;
+  M[i + j * n] = v;
+  if (mirror && i != j) M[j + i * n] = v;
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -257,6 +263,19 @@ void syrk_plan(Ctx& c) {
     CMPC_CUDA(cudaMemcpy(c.tile_units, tunits.data(), sizeof(int32_t) * tunits.size(),
                          cudaMemcpyHostToDevice));
 
+  // algorithmic work of one condensation: lower triangle of P' diag(omega) P
+  {
+    std::vector<int32_t> hh(size_t(std::max<int64_t>(c.ps, 1)));
+    if (c.ps > 0)
+      CMPC_CUDA(cudaMemcpy(hh.data(), c.hi, sizeof(int32_t) * c.ps, cudaMemcpyDeviceToHost));
+    double f = 0.0, b = 0.0;
+    for (int64_t k = 0; k < c.ps; ++k) {
+      f += double(hh[size_t(k)]) * double(hh[size_t(k)] + 1);
+      b += 8.0 * hh[size_t(k)];
+    }
+    c.syrk_flops = f;
+    c.syrk_bytes = b;
+  }
   // TMA descriptor over P (ldp rows x n cols, column-major), box {16 rows, 64 cols}
   auto* tm = new unsigned char[sizeof(CUtensorMap)];
   c.tmap_P = tm;
@@ -282,7 +301,7 @@ void launch_condense(Ctx& c, bool mirror) {
     k_syrk<<<c.nunits, kSyrkThreads, kSyrkSmem, c.stream>>>(*tm, c.omega, c.units, c.partial);
     CMPC_LAUNCHED();
   }
-  k_syrk_reduce<<<c.ntiles, 256, 0, c.stream>>>(c.partial, c.tiles, c.tile_ptr, c.tile_units, c.H,
+  k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 256), 256, 0, c.stream>>>(c.partial, c.tiles, c.tile_ptr, c.tile_units, c.H,
                                                  c.dsing, c.n, c.M, mirror ? 1 : 0);
   CMPC_LAUNCHED();
 }

@@ -160,19 +160,69 @@ __global__ void __launch_bounds__(kRowT) k_mu_rows(int64_t m, const double* __re
   if ((threadIdx.x & 31) == 0) atomic_max_nonneg(&pk->max_comp, mc);
 }
 
-// q[proto] = sum over member rows of sign * x[row] (rows ascending)
-__global__ void k_proto_sum(int64_t p, const int32_t* __restrict__ mem_ptr,
-                            const int32_t* __restrict__ mem_rows, const double* __restrict__ x,
-                            double* __restrict__ q, int64_t ps, int64_t ldp) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= p) return;
-  double s = 0.0;
-  for (int32_t e = mem_ptr[k]; e < mem_ptr[k + 1]; ++e) {
-    const int32_t rm = mem_rows[e];
-    const double v = x[rm >> 1];
-    s += (rm & 1) ? -v : v;
+// Per prototype k (rows of J that equal +-P_k): out1[k] = sum of x1 over the member rows
+// (signed when SIGNED1), out2[k] = signed sum of x2; members in ascending row order.
+// One warp per 32 prototypes: small groups are summed by their own lane, large groups
+// (repeated rows) cooperatively by the whole warp; fixed order either way. The all-zero
+// row group (if any) contributes nothing and is skipped.
+template <bool SIGNED1, bool HAS2>
+__global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* __restrict__ mem_ptr,
+                                                      const int32_t* __restrict__ mem_rows,
+                                                      const double* __restrict__ x1,
+                                                      const double* __restrict__ x2,
+                                                      double* __restrict__ out1,
+                                                      double* __restrict__ out2, int64_t ps,
+                                                      int64_t ldp, int64_t zero_k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t base = (blockIdx.x * 8ll + (threadIdx.x >> 5)) * 32;
+  const int64_t k = base + lane;
+  int32_t b0 = 0, b1 = 0;
+  if (k < p && k != zero_k) {
+    b0 = mem_ptr[k];
+    b1 = mem_ptr[k + 1];
   }
-  q[k < ps ? k : ldp + (k - ps)] = s;
+  constexpr int kSmall = 8;
+  double s1 = 0.0, s2 = 0.0;
+  if (b1 - b0 <= kSmall) {
+    for (int32_t e = b0; e < b1; ++e) {
+      const int32_t rm = mem_rows[e];
+      const int32_t r = rm >> 1;
+      const double a = x1[r];
+      s1 += (SIGNED1 && (rm & 1)) ? -a : a;
+      if (HAS2) {
+        const double b = x2[r];
+        s2 += (rm & 1) ? -b : b;
+      }
+    }
+  }
+  unsigned big = __ballot_sync(0xffffffffu, b1 - b0 > kSmall);
+  while (big) {
+    const int src = __ffs(big) - 1;
+    big &= big - 1;
+    const int32_t e0 = __shfl_sync(0xffffffffu, b0, src), e1 = __shfl_sync(0xffffffffu, b1, src);
+    double t1 = 0.0, t2 = 0.0;
+    for (int32_t e = e0 + lane; e < e1; e += 32) {
+      const int32_t rm = mem_rows[e];
+      const int32_t r = rm >> 1;
+      const double a = x1[r];
+      t1 += (SIGNED1 && (rm & 1)) ? -a : a;
+      if (HAS2) {
+        const double b = x2[r];
+        t2 += (rm & 1) ? -b : b;
+      }
+    }
+    t1 = warp_sum(t1);
+    if (HAS2) t2 = warp_sum(t2);
+    if (lane == src) {
+      s1 = t1;
+      s2 = t2;
+    }
+  }
+  if (k < p) {
+    const int64_t o = k < ps ? k : ldp + (k - ps);
+    out1[o] = s1;
+    if (HAS2) out2[o] = s2;
+  }
 }
 
 constexpr int kFinT = 1024;
@@ -264,28 +314,6 @@ __global__ void k_sigma_rows(int64_t m, const double* __restrict__ s, const doub
   const double sg = sig_in ? sig_in[r] : dv(z[r], s[r]);
   sigma[r] = sg;
   if (w) w[r] = sub(r2[r], mul(sg, r3[r]));
-}
-
-// omega[proto] = sum of member sigma; rhs q[proto] = sum of signed member w
-__global__ void k_proto_step(int64_t p, const int32_t* __restrict__ mem_ptr,
-                             const int32_t* __restrict__ mem_rows, const double* __restrict__ sigma,
-                             const double* __restrict__ w, double* __restrict__ omega,
-                             double* __restrict__ q, int64_t ps, int64_t ldp) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= p) return;
-  double so = 0.0, sq = 0.0;
-  for (int32_t e = mem_ptr[k]; e < mem_ptr[k + 1]; ++e) {
-    const int32_t rm = mem_rows[e];
-    const int32_t r = rm >> 1;
-    so += sigma[r];
-    if (w) {
-      const double v = w[r];
-      sq += (rm & 1) ? -v : v;
-    }
-  }
-  const int64_t o = k < ps ? k : ldp + (k - ps);
-  omega[o] = so;
-  if (w) q[o] = sq;
 }
 
 // dsing[c] = sum over singleton prototypes at column c of omega * a^2
@@ -537,6 +565,7 @@ void vec_alloc(Ctx& c) {
   CMPC_CUDA(cudaMalloc(&c.pk, sizeof(Packet)));
   CMPC_CUDA(cudaMemset(c.pk, 0, sizeof(Packet)));
   CMPC_CUDA(cudaMallocHost(&c.pk_host, sizeof(Packet)));
+  chol_alloc(c);
   if (c.n > 0) {
     k_absmax<<<(unsigned)std::min<int64_t>(64, ceil_div(c.n, 256)), 256, 0, c.stream>>>(c.h, c.n, c.hmax);
     CMPC_LAUNCHED();
@@ -552,6 +581,7 @@ void vec_free(Ctx& c) {
                   (void*)c.hmax, (void*)c.pk})
     if (p) cudaFree(p);
   if (c.pk_host) cudaFreeHost(c.pk_host);
+  chol_free(c);
   c.v = c.s = c.lam = c.z = c.r1 = c.r2 = c.r3 = c.Hv = c.Jtl = c.y = c.sigma = nullptr;
   c.omega = c.q = c.dsing = c.rhs = c.M = c.L = c.pv = c.ps_ = c.pl = c.pzd = nullptr;
   c.Jpv = c.vt = c.yt = c.Hvt = c.part = c.colpart = c.hmax = nullptr;
@@ -599,18 +629,25 @@ void launch_Jtq(Ctx& c, const double* q, double* out) {
   CMPC_LAUNCHED();
 }
 
-void launch_residuals(Ctx& c) {
+void launch_residuals(Ctx& c, bool reuse_trial) {
   const unsigned pb = part_blocks(c.m);
   k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 0);
   CMPC_LAUNCHED();
-  launch_Hx(c, c.v, c.Hv);
+  if (reuse_trial) {
+    // v was just set to the accepted trial point v + alpha pv, computed with the same
+    // kernel and inputs as the trial: H v and P v are the trial's, bit for bit
+    std::swap(c.Hv, c.Hvt);
+    std::swap(c.y, c.yt);
+  } else {
+    launch_Hx(c, c.v, c.Hv);
+  }
   if (c.m > 0) {
-    launch_Jx(c, c.v, c.y, nullptr);
+    if (!reuse_trial) launch_Jx(c, c.v, c.y, nullptr);
     k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.d, c.s, c.lam, c.z, c.mu, c.r2,
                                            c.r3, c.part, c.pk);
     CMPC_LAUNCHED();
-    k_proto_sum<<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(c.p, c.mem_ptr, c.mem_rows,
-                                                                    c.lam, c.q, c.ps, c.ldp);
+    k_proto_reduce<true, false><<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
+        c.p, c.mem_ptr, c.mem_rows, c.lam, nullptr, c.q, nullptr, c.ps, c.ldp, c.zero_k);
     CMPC_LAUNCHED();
     launch_Jtq(c, c.q, c.Jtl);
   }
@@ -638,9 +675,12 @@ void launch_prepare_step(Ctx& c, const double* sigma_override) {
   k_sigma_rows<<<(unsigned)ceil_div(c.m, 256), 256, 0, c.stream>>>(
       c.m, c.s, c.z, c.r2, c.r3, sigma_override, c.sigma, sigma_override ? nullptr : c.Jpv);
   CMPC_LAUNCHED();
-  k_proto_step<<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
-      c.p, c.mem_ptr, c.mem_rows, c.sigma, sigma_override ? nullptr : c.Jpv, c.omega, c.q, c.ps,
-      c.ldp);
+  if (sigma_override)
+    k_proto_reduce<false, false><<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
+        c.p, c.mem_ptr, c.mem_rows, c.sigma, nullptr, c.omega, nullptr, c.ps, c.ldp, c.zero_k);
+  else
+    k_proto_reduce<false, true><<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
+        c.p, c.mem_ptr, c.mem_rows, c.sigma, c.Jpv, c.omega, c.q, c.ps, c.ldp, c.zero_k);
   CMPC_LAUNCHED();
   k_dsing<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.sing_col, c.sing_val, c.pz,
                                                               c.omega + c.ldp, c.dsing);

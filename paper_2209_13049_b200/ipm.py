@@ -19,7 +19,8 @@ import numpy as np
 
 from . import _lib
 from ._lib import DimensionError, check, f64, ptr
-from .linalg import DEVICE, Factor, NotPositiveDefinite
+from . import linalg as _linalg
+from .linalg import Factor, NotPositiveDefinite
 from .problem import DenseQp, Trajectory, recover_trajectory
 
 
@@ -116,13 +117,17 @@ class IpmResult:
     launches: int = 0
     syncs: int = 0
     trials: int = 0
+    syrk_seconds: float = 0.0     # device time of the condensation (SYRK + reduce)
+    chol_seconds: float = 0.0     # device time of the first factorization attempts
+    condensations: int = 0
 
 
 class DeviceQp:
     """One device context (stream + HBM buffers) holding a loaded DenseQp."""
 
-    def __init__(self, qp: DenseQp, device: int = DEVICE, on_device_ptrs=None):
+    def __init__(self, qp: DenseQp, device: int | None = None, on_device_ptrs=None):
         L = _lib.lib()
+        device = _linalg.DEVICE if device is None else device
         h = C.c_void_p()
         check(L.cmpc_ctx_create(C.byref(h), device))
         self.h = h
@@ -143,10 +148,19 @@ class DeviceQp:
     __del__ = close
 
     def info(self):
-        out = (C.c_int64 * 6)()
+        out = (C.c_int64 * 8)()
         _lib.lib().cmpc_qp_info(self.h, out)
         return dict(n=out[0], m=out[1], prototypes=out[2], syrk_prototypes=out[3],
-                    singletons=out[4], syrk_units=out[5])
+                    singletons=out[4], syrk_units=out[5], syrk_flops=out[6], p_bytes=out[7])
+
+    PHASES = dict(condense_all=0, condense=1, cholesky=2, chol_solve=3, residuals=4, recover=5,
+                  trial=6, Jx=7, Jty=8, prepare=9)
+
+    def time_phase(self, name: str, reps: int = 10) -> float:
+        """Device milliseconds of one phase (CUDA events, back-to-back launches)."""
+        ms = C.c_double()
+        check(_lib.lib().cmpc_time_phase(self.h, self.PHASES[name], int(reps), C.byref(ms)))
+        return ms.value
 
     def update_affine(self, h, h0, d):
         h, d = f64(h), f64(d)
@@ -231,7 +245,7 @@ def fraction_to_boundary(s, ps, z, pz, tau):
         raise DimensionError("tau must lie in (0,1)")
     s, ps, z, pz = (f64(x).reshape(-1) for x in (s, ps, z, pz))
     out = np.zeros(2)
-    check(_lib.lib().cmpc_fraction_to_boundary(DEVICE, s.size, ptr(s), ptr(ps), ptr(z), ptr(pz),
+    check(_lib.lib().cmpc_fraction_to_boundary(_linalg.DEVICE, s.size, ptr(s), ptr(ps), ptr(z), ptr(pz),
                                                 float(tau), ptr(out)))
     return float(out[0]), float(out[1])
 
@@ -289,7 +303,7 @@ def solve_loaded(dq: DeviceQp, qp: DenseQp, opts: IpmOptions, t0=None) -> IpmRes
     t0 = time.perf_counter() if t0 is None else t0
     n, m = qp.n, qp.m
     v, s, l, z = np.zeros(n), np.zeros(m), np.zeros(m), np.zeros(m)
-    out = np.zeros(10)
+    out = np.zeros(13)
     L = _lib.lib()
 
     def _log(user, rec):
@@ -311,7 +325,8 @@ def solve_loaded(dq: DeviceQp, qp: DenseQp, opts: IpmOptions, t0=None) -> IpmRes
     res = IpmResult(status=IpmStatus(int(out[0])), v=v, s=s, lambda_=l, z=z, iter=int(out[1]),
                     kkt_error=float(out[2]), objective=float(out[3]), linalg_seconds=float(out[5]),
                     device_seconds=float(out[6]), launches=int(out[7]), syncs=int(out[8]),
-                    trials=int(out[9]))
+                    trials=int(out[9]), syrk_seconds=float(out[10]), chol_seconds=float(out[11]),
+                    condensations=int(out[12]))
     if qp.source is not None:
         res.solution = recover_trajectory(qp, v)
     else:

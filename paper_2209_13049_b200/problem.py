@@ -328,23 +328,35 @@ def refresh_initial_state(qp: DenseQp, x_bar) -> None:
 
 
 def recover_trajectory(qp: DenseQp, v) -> Trajectory:
-    """reduction.cpp:282-314 by the recursion x_{t+1} = A x_t + B u_t + w_t, u_t = K x_t + v_t."""
+    """reduction.cpp:282-314: x = (bigA x_bar + bigAtilde w) + bigB v, u_t = K x_t + v_t, and
+    the Eq. (1a) objective. Uses the cached free response x0 and bigB's first block column
+    (x_t = x0_t + sum_{j<t} A_K^{t-1-j} B v_j), never the stacked matrices."""
     data = qp.source
     dm = dims(data)
     v = np.asarray(v, dtype=np.float64)
     if v.size != dm.T * dm.n_u:
         raise DimensionError(f"recover_trajectory: v has length {v.size}, expected {dm.T * dm.n_u}")
     vt = v.reshape(dm.T, dm.n_u)
-    x = np.zeros((dm.T + 1, dm.n_x))
-    u = np.zeros((dm.T, dm.n_u))
-    x[0] = data.x_bar
-    A_K = data.A + data.B @ data.K
-    for t in range(dm.T):
-        u[t] = data.K @ x[t] + vt[t]
-        x[t + 1] = A_K @ x[t] + data.B @ vt[t] + data.w[t]
-    obj = float(x[-1] @ data.Qf @ x[-1])
-    for t in range(dm.T):
-        obj += float(x[t] @ data.Q @ x[t] + 2.0 * x[t] @ data.S @ u[t] + u[t] @ data.R @ u[t])
+    if qp.gk is None or qp.x0 is None:
+        A_K = data.A + data.B @ data.K
+        qp.gk = np.zeros((dm.T, dm.n_x, dm.n_u))
+        qp.gk[0] = data.B
+        for k in range(1, dm.T):
+            qp.gk[k] = A_K @ qp.gk[k - 1]
+        qp.x0 = free_response(A_K, data.x_bar, data.w)
+    x = qp.x0.copy()
+    for t in range(1, dm.T + 1):
+        # sum_{j<t} G_{t-1-j} v_j
+        x[t] += np.einsum("kij,kj->i", qp.gk[t - 1::-1], vt[:t])
+    u = x[:-1] @ data.K.T + vt
+
+    def quad(X, Mx):
+        d = _diag_or_none(Mx)
+        return (X * X) @ d if d is not None else np.einsum("ti,ti->t", X @ Mx, X)
+
+    obj = float(quad(x[-1:], data.Qf)[0])
+    per_t = quad(x[:-1], data.Q) + 2.0 * np.einsum("ti,ti->t", x[:-1] @ data.S, u) + quad(u, data.R)
+    obj += float(per_t.sum())
     return Trajectory(x=x, u=u, v=vt.copy(), objective=obj)
 
 
