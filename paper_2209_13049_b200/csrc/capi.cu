@@ -1,6 +1,8 @@
 // C ABI (include/condmpc_cuda.h): context lifecycle, QP upload, per-step entry points and
 // the stand-alone linear algebra of the reference's plug point.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -10,6 +12,16 @@
 
 namespace cmpc {
 thread_local long long g_launches = 0;
+
+void pool_init(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  CMPC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  unsigned long long keep = ~0ull;  // never hand cached pages back to the OS
+  CMPC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done[device] = true;
+}
 thread_local std::string g_error;
 
 // host loop (ipm_host.cpp)
@@ -64,8 +76,8 @@ void release_qp(Ctx& c) {
   vec_free(c);
   syrk_free(c);
   free_structure(c);
-  for (double* p : {c.H, c.h, c.d}) if (p) cudaFree(p);
-  if (c.J && c.owns_J) cudaFree(c.J);
+  for (double* p : {c.H, c.h, c.d}) dev_free(p, c.stream);
+  if (c.J && c.owns_J) dev_free(c.J, c.stream);
   c.H = c.h = c.J = c.d = nullptr;
   c.n = c.m = 0;
 }
@@ -87,6 +99,7 @@ int cmpc_ctx_create(cmpc_ctx** out, int device) {
     auto* x = new cmpc_ctx;
     x->c.device = device;
     CMPC_CUDA(cudaSetDevice(device));
+    pool_init(device);
     CMPC_CUDA(cudaStreamCreateWithFlags(&x->c.stream, cudaStreamNonBlocking));
     CMPC_CUDA(cudaEventCreate(&x->c.ev0));
     CMPC_CUDA(cudaEventCreate(&x->c.ev1));
@@ -102,6 +115,7 @@ void cmpc_ctx_destroy(cmpc_ctx* x) {
   cudaSetDevice(x->c.device);
   cudaStreamSynchronize(x->c.stream);
   release_qp(x->c);
+  cudaStreamSynchronize(x->c.stream);
   cudaEventDestroy(x->c.ev0);
   cudaEventDestroy(x->c.ev1);
   cudaEventDestroy(x->c.ev2);
@@ -117,27 +131,44 @@ int cmpc_load_qp(cmpc_ctx* x, int64_t n, int64_t m, const double* H, const doubl
     if (n < 0 || m < 0) throw DimError("negative dimensions");
     if (m > (int64_t(1) << 29) || n > (int64_t(1) << 24)) throw DimError("QP too large");
     CMPC_CUDA(cudaSetDevice(c.device));
+    const double t_in = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     release_qp(c);
+    if (getenv("CMPC_VERBOSE"))
+      fprintf(stderr, "[cmpc load] release    %8.2f ms\n",
+              (std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count() - t_in) * 1e3);
     c.n = n;
     c.m = m;
     c.h0 = h0;
     const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    CMPC_CUDA(cudaMalloc(&c.H, sizeof(double) * std::max<int64_t>(1, n * n)));
-    CMPC_CUDA(cudaMalloc(&c.h, sizeof(double) * std::max<int64_t>(1, n)));
-    CMPC_CUDA(cudaMalloc(&c.J, sizeof(double) * std::max<int64_t>(1, m * n)));
-    CMPC_CUDA(cudaMalloc(&c.d, sizeof(double) * std::max<int64_t>(1, m)));
+    c.H = dev_alloc<double>((size_t)(n * n), c.stream);
+    c.h = dev_alloc<double>((size_t)n, c.stream);
+    c.J = dev_alloc<double>((size_t)(m * n), c.stream);
+    c.d = dev_alloc<double>((size_t)m, c.stream);
     c.owns_J = true;
     if (n * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.H, H, sizeof(double) * n * n, kind, c.stream));
     if (n > 0) CMPC_CUDA(cudaMemcpyAsync(c.h, h, sizeof(double) * n, kind, c.stream));
     if (m * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.J, J, sizeof(double) * m * n, kind, c.stream));
     if (m > 0) CMPC_CUDA(cudaMemcpyAsync(c.d, d, sizeof(double) * m, kind, c.stream));
+    const bool verbose = getenv("CMPC_VERBOSE") != nullptr;
+    auto tick = [&](const char* what) {
+      static double last = 0.0;
+      if (!verbose) return;
+      sync(c);
+      const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+      if (what) fprintf(stderr, "[cmpc load] %-10s %8.2f ms\n", what, (now - last) * 1e3);
+      last = now;
+    };
+    tick(nullptr);
     analyze_structure(c);
+    tick("analyze");
     // the dense J is not read again: every product goes through P
-    cudaFree(c.J);
+    dev_free(c.J, c.stream);
     c.J = nullptr;
     syrk_plan(c);
+    tick("plan");
     vec_alloc(c);
     sync(c);
+    tick("alloc");
     return CMPC_OK;
   });
 }
@@ -444,9 +475,8 @@ int cmpc_fraction_to_boundary(int device, int64_t m, const double* s, const doub
     CMPC_CUDA(cudaSetDevice(device));
     cudaStream_t st;
     CMPC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    double* buf = nullptr;
     const int64_t mm = std::max<int64_t>(m, 1);
-    CMPC_CUDA(cudaMalloc(&buf, sizeof(double) * (4 * mm + 2)));
+    double* buf = dev_alloc<double>((size_t)(4 * mm + 2), st);
     const double* src[4] = {s, ps, z, pz};
     for (int k = 0; k < 4; ++k)
       if (m > 0)
@@ -454,8 +484,8 @@ int cmpc_fraction_to_boundary(int device, int64_t m, const double* s, const doub
     launch_fraction_to_boundary(st, m, buf, buf + mm, buf + 2 * mm, buf + 3 * mm, tau, buf + 4 * mm);
     double r[2];
     CMPC_CUDA(cudaMemcpyAsync(r, buf + 4 * mm, sizeof(r), cudaMemcpyDeviceToHost, st));
+    dev_free(buf, st);
     CMPC_CUDA(cudaStreamSynchronize(st));
-    cudaFree(buf);
     cudaStreamDestroy(st);
     out[0] = std::min(1.0, r[0]);
     out[1] = std::min(1.0, r[1]);

@@ -28,7 +28,7 @@ constexpr int kNB = 64;
 constexpr int kLD = kNB + 1;
 constexpr int kGemmLD = 68;
 constexpr int kGemmSmem = 2 * kNB * kGemmLD * 8;
-constexpr int kPotfSmem = (2 * kNB * kLD + kNB) * 8;
+constexpr int kPotfSmem = (2 * kNB * kLD + 16 * 65 + 64) * 8;
 
 __global__ void k_chol_copy(const double* __restrict__ M, double* __restrict__ L, int64_t n,
                             double delta, long long* info) {
@@ -86,64 +86,172 @@ __device__ void store_diag(double* L, int64_t n, int64_t k0, int b, const double
   }
 }
 
-// factor the b x b diagonal block at (k0, k0) (right-looking, 2 barriers per column) and
-// build W = L_kk^{-1} in the same sweep: once column j of L is final, step j of the
-// substitution L W = I runs alongside the rank-1 trailing update. 256 threads.
+// 1/sqrt(x) from a float seed and two Newton steps in FP64 (the FP64 sqrt and divide
+// sequences cost several hundred cycles each on the pivot's critical path); exact
+// fallback outside the float range
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  if (x > 1e-30 && x < 1e30) {
+    double y = (double)rsqrtf((float)x);
+    const double hx = 0.5 * x;
+    y = y * fma(-hx * y, y, 1.5);
+    y = y * fma(-hx * y, y, 1.5);
+    return y;
+  }
+  return 1.0 / sqrt(x);
+}
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// One warp factors the 16 x 16 lower block of a at (o, o) in registers (lane & 15 = row;
+// lanes 16..31 mirror 0..15 so every shuffle is warp-uniform) and writes L and L^{-1}
+// (into w) back to shared memory. Returns the first failing local pivot or -1.
+// The step loops are deliberately not unrolled (the register row is rotated instead of
+// indexed): a fully unrolled body is ~30 KB of straight-line SASS whose instruction fetch,
+// not the arithmetic, set the pace (27k cycles measured vs ~4k for this form).
+__device__ int warp_potf2_inv16(double* a, double* w, int o, int bvalid, double* bc) {
+  // bc: 2 x 32 doubles of shared scratch, double-buffered by step parity:
+  // [0,16) column j of L, [16,32) row j of W
+  const int lane = threadIdx.x & 31, row = lane & 15;
+  double r[16], wr[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    r[k] = (k <= row) ? a[(o + row) + (o + k) * kLD] : 0.0;
+    wr[k] = (k == row) ? 1.0 : 0.0;
+  }
+  int fail = -1;
+  // step j: factor column j of L and, interleaved, step j of the substitution L W = I
+  // (row j of W is final once scaled by 1/l_jj; rows below subtract l_ij W_j). The column
+  // and the row are broadcast through shared memory: a 64-bit shuffle costs ~10 issue
+  // cycles per lane-pair on one warp, a broadcast LDS far less.
+#pragma unroll 1
+  for (int j = 0; j < 16; ++j) {
+    double* cb = bc + 32 * (j & 1);
+    // r[0] holds column j of this row (rotated)
+    const double pj = __shfl_sync(kFull, r[0], j);
+    if (fail < 0 && j < bvalid && (!(pj > 0.0) || !isfinite(pj))) fail = j;
+    const double y = rsqrt_fast(pj);
+    double lij = r[0];
+    if (row == j) {
+      lij = pj * y;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) wr[k] *= y;
+      if (lane == j) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) cb[16 + k] = wr[k];
+      }
+    } else if (row > j) {
+      lij = r[0] * y;
+    }
+    if (lane < 16) {
+      cb[row] = lij;
+      if (row >= j) a[(o + row) + (o + j) * kLD] = lij;
+    }
+    __syncwarp();
+    if (row > j) {
+#pragma unroll
+      for (int k = 1; k < 16; ++k) {
+        if (row >= j + k) r[k] = fma(-lij, cb[(j + k) & 15], r[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) wr[k] = fma(-lij, cb[16 + k], wr[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 15; ++k) r[k] = r[k + 1];
+    r[15] = 0.0;
+  }
+  if (fail >= 0) return fail;
+  if (lane < 16) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) w[(o + row) + (o + k) * kLD] = (k <= row) ? wr[k] : 0.0;
+  }
+  return -1;
+}
+
+// Factor the b x b diagonal block at (k0, k0) and build W = L_kk^{-1}: four 16-wide
+// column blocks, each factored (with its inverse) inside one warp's registers, then the
+// panel below (A_ik <- A_ik W16^T) and the trailing update by all 8 warps; W's off-diagonal
+// blocks follow from W_ij = -W_ii sum_{k=j}^{i-1} L_ik W_kj (three dependent stages).
 __global__ void __launch_bounds__(256) k_potf2_inv(double* __restrict__ L, int64_t n, int64_t k0,
                                                    int b, long long* info, double* __restrict__ Wout) {
   extern __shared__ double sm[];
   double* a = sm;              // kNB x kLD
   double* w = sm + kNB * kLD;  // kNB x kLD
-  double* dj = w + kNB * kLD;  // pivots
+  double* tt = w + kNB * kLD;  // 64 x 17 scratch (panel / W stages)
+  __shared__ int fail;
   if (*info != 0) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5;
   load_diag(L, n, k0, b, a);
-  for (int e = tid; e < kNB * kNB; e += blockDim.x) w[(e & 63) + (e >> 6) * kLD] = ((e & 63) == (e >> 6)) ? 1.0 : 0.0;
+  for (int e = tid; e < kNB * kNB; e += blockDim.x) w[(e & 63) + (e >> 6) * kLD] = 0.0;
+  if (tid == 0) fail = -1;
   __syncthreads();
-  const int i = tid & 63, kg = tid >> 6;
-  for (int j = 0; j < kNB; ++j) {
-    const double d = a[j + j * kLD];
-    if (j < b && (!(d > 0.0) || !isfinite(d))) {
-      if (tid == 0) *info = (long long)(k0 + j + 1);
+  for (int kb = 0; kb < 4; ++kb) {
+    const int o = 16 * kb;
+    if (warp == 0) {
+      const int bv = b - o < 0 ? 0 : (b - o > 16 ? 16 : b - o);
+      const int f = warp_potf2_inv16(a, w, o, bv, tt + 16 * 65);
+      if (f >= 0 && tid == 0) fail = o + f;
+    }
+    __syncthreads();
+    if (fail >= 0) {
+      if (tid == 0) *info = (long long)(k0 + fail + 1);
       return;
     }
-    const double l = sqrt(d);
-    if (tid < 64) {
-      if (i > j) a[i + j * kLD] = dv(a[i + j * kLD], l);
-    } else if (tid - 64 <= j) {
-      w[j + (tid - 64) * kLD] = dv(w[j + (tid - 64) * kLD], l);
+    const int rows = kNB - o - 16;  // panel rows below the block
+    if (rows > 0) {
+      // panel: X(i, c) = sum_{p <= c} A(i, o+p) W16(c, p), rows i = o+16.., 16 columns
+      for (int e = tid; e < rows * 16; e += blockDim.x) {
+        const int i = o + 16 + e % rows, c = e / rows;
+        double s = 0.0;
+#pragma unroll 4
+        for (int q = 0; q <= c; ++q) s = fma(a[i + (o + q) * kLD], w[(o + c) + (o + q) * kLD], s);
+        tt[(i - o - 16) + c * 65] = s;
+      }
+      __syncthreads();
+      for (int e = tid; e < rows * 16; e += blockDim.x) {
+        const int i = e % rows, c = e / rows;
+        a[(o + 16 + i) + (o + c) * kLD] = tt[i + c * 65];
+      }
+      __syncthreads();
+      // trailing: A(i, j) -= sum_p X(i, p) X(j, p) for o+16 <= j <= i < 64
+      const int cnt = rows * rows;
+      for (int e = tid; e < cnt; e += blockDim.x) {
+        const int ii = e % rows, jj = e / rows;
+        if (ii < jj) continue;
+        const int i = o + 16 + ii, j = o + 16 + jj;
+        double s = 0.0;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) s = fma(a[i + (o + p) * kLD], a[j + (o + p) * kLD], s);
+        a[i + j * kLD] -= s;
+      }
+      __syncthreads();
     }
-    if (tid == 0) dj[j] = l;
+  }
+  // off-diagonal blocks of W, by block distance d = i - j
+  for (int d = 1; d < 4; ++d) {
+    const int nblk = 4 - d;  // blocks (j + d, j), j = 0 .. nblk-1
+    // T(j) = sum_{k=j}^{j+d-1} L(j+d, k) W(k, j)   (16 x 16 each)
+    for (int e = tid; e < nblk * 256; e += blockDim.x) {
+      const int jb = e >> 8, r = (e >> 4) & 15, c = e & 15;
+      const int ib = jb + d;
+      double s = 0.0;
+      for (int kb2 = jb; kb2 < ib; ++kb2)
+#pragma unroll 4
+        for (int q = 0; q < 16; ++q)
+          s = fma(a[(16 * ib + r) + (16 * kb2 + q) * kLD], w[(16 * kb2 + q) + (16 * jb + c) * kLD], s);
+      tt[(e & 255) + jb * 256] = s;
+    }
     __syncthreads();
-    if (i > j) {
-      // batch every load of this step before any store (the smem updates are independent)
-      const double lij = a[i + j * kLD];
-      double av[16], cv[16], wv[16], rv[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int k = j + 1 + kg + 4 * u;
-        if (k <= i) {
-          av[u] = a[i + k * kLD];
-          cv[u] = a[k + j * kLD];
-        }
-        const int q = kg + 4 * u;
-        if (q <= j) {
-          wv[u] = w[i + q * kLD];
-          rv[u] = w[j + q * kLD];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int k = j + 1 + kg + 4 * u;
-        if (k <= i) a[i + k * kLD] = fma(-lij, cv[u], av[u]);
-        const int q = kg + 4 * u;
-        if (q <= j) w[i + q * kLD] = fma(-lij, rv[u], wv[u]);
-      }
+    // W(j+d, j) = -W(j+d, j+d) T(j)
+    for (int e = tid; e < nblk * 256; e += blockDim.x) {
+      const int jb = e >> 8, r = (e >> 4) & 15, c = e & 15;
+      const int ib = jb + d;
+      double s = 0.0;
+#pragma unroll 4
+      for (int q = 0; q <= r; ++q) s = fma(w[(16 * ib + r) + (16 * ib + q) * kLD], tt[(q << 4 | c) + jb * 256], s);
+      w[(16 * ib + r) + (16 * jb + c) * kLD] = -s;
     }
     __syncthreads();
   }
-  for (int e = tid; e < kNB; e += blockDim.x) a[e + e * kLD] = dj[e];
-  __syncthreads();
   store_diag(L, n, k0, b, a, w, Wout, true);
 }
 
@@ -364,12 +472,11 @@ void set_attrs() {
 
 void chol_alloc(Ctx& c) {
   const int64_t nb = ceil_div(std::max<int64_t>(c.n, 1), kNB);
-  CMPC_CUDA(cudaMalloc(&c.Winv, sizeof(double) * nb * kNB * kNB));
-  CMPC_CUDA(cudaMemset(c.Winv, 0, sizeof(double) * nb * kNB * kNB));
+  c.Winv = dev_zeros<double>((size_t)nb * kNB * kNB, c.stream);
 }
 
 void chol_free(Ctx& c) {
-  if (c.Winv) cudaFree(c.Winv);
+  dev_free(c.Winv, c.stream);
   c.Winv = nullptr;
 }
 

@@ -33,6 +33,28 @@ extern thread_local long long g_launches;
     CMPC_CUDA(cudaPeekAtLastError());   \
   } while (0)
 
+// Stream-ordered device allocations from the device's memory pool (kept cached: a
+// reloaded QP of similar size reuses the pages instead of re-mapping gigabytes).
+void pool_init(int device);
+template <typename T>
+inline T* dev_alloc(size_t count, cudaStream_t st) {
+  void* p = nullptr;
+  const size_t bytes = (count == 0 ? 1 : count) * sizeof(T);
+  cudaError_t e = cudaMallocAsync(&p, bytes, st);
+  if (e != cudaSuccess)
+    throw CudaError(std::string("cudaMallocAsync(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  return static_cast<T*>(p);
+}
+template <typename T>
+inline T* dev_zeros(size_t count, cudaStream_t st) {
+  T* p = dev_alloc<T>(count, st);
+  CMPC_CUDA(cudaMemsetAsync(p, 0, (count == 0 ? 1 : count) * sizeof(T), st));
+  return p;
+}
+inline void dev_free(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
 #ifdef __CUDACC__
 // IEEE operations without FMA contraction: elementwise updates follow the
 // reference's separate multiply/add rounding (Eigen, SSE2, no -march).

@@ -189,20 +189,13 @@ __global__ void k_start_col(const int32_t* hi, int64_t ps, int64_t n, int32_t* s
   start_col[c] = (int32_t)lo;
 }
 
-template <typename T>
-T* dalloc(size_t count) {
-  T* p = nullptr;
-  if (count == 0) count = 1;
-  CMPC_CUDA(cudaMalloc(&p, count * sizeof(T)));
-  return p;
-}
 
 }  // namespace
 
 void free_structure(Ctx& c) {
   for (void* p : {(void*)c.P, (void*)c.hi, (void*)c.start_col, (void*)c.row_map,
                   (void*)c.mem_ptr, (void*)c.mem_rows, (void*)c.sing_col, (void*)c.sing_val})
-    if (p) cudaFree(p);
+    dev_free(p, c.stream);
   c.P = nullptr;
   c.hi = c.start_col = c.row_map = c.mem_ptr = c.mem_rows = c.sing_col = nullptr;
   c.sing_val = nullptr;
@@ -212,36 +205,37 @@ void analyze_structure(Ctx& c) {
   free_structure(c);
   const int64_t m = c.m, n = c.n;
   cudaStream_t st = c.stream;
-  c.start_col = dalloc<int32_t>(size_t(n + 1));
+  (void)0;
+  c.start_col = dev_alloc<int32_t>(size_t(n + 1), st);
   if (m == 0) {
     c.ps = c.pz = c.p = 0;
     c.ldp = kBK;
-    c.P = dalloc<double>(size_t(c.ldp * std::max<int64_t>(n, 1)));
+    c.P = dev_alloc<double>(size_t(c.ldp * std::max<int64_t>(n, 1)), st);
     CMPC_CUDA(cudaMemsetAsync(c.P, 0, sizeof(double) * c.ldp * std::max<int64_t>(n, 1), st));
     CMPC_CUDA(cudaMemsetAsync(c.start_col, 0, sizeof(int32_t) * (n + 1), st));
     c.h_start_col.assign(size_t(n + 1), 0);
-    c.mem_ptr = dalloc<int32_t>(1);
+    c.mem_ptr = dev_alloc<int32_t>(1, st);
     CMPC_CUDA(cudaMemsetAsync(c.mem_ptr, 0, sizeof(int32_t), st));
     return;
   }
   const int T = 256;
   const unsigned gm = unsigned((m + T - 1) / T);
 
-  auto* key = dalloc<unsigned long long>(m);
-  auto* key_s = dalloc<unsigned long long>(m);
-  auto* lo = dalloc<int32_t>(m);
-  auto* hi_row = dalloc<int32_t>(m);
-  auto* nnz = dalloc<int32_t>(m);
-  auto* sg = dalloc<int8_t>(m);
-  auto* idx = dalloc<int32_t>(m);
-  auto* srow = dalloc<int32_t>(m);
-  auto* head_pos = dalloc<int32_t>(m);
-  auto* lead_pos = dalloc<int32_t>(m);
-  auto* leader_row = dalloc<int32_t>(m);
-  auto* run_of_row = dalloc<int32_t>(m);
-  auto* collide = dalloc<int32_t>(m);
-  auto* head = dalloc<int32_t>(m);
-  auto* gid = dalloc<int32_t>(m);
+  auto* key = dev_alloc<unsigned long long>(m, st);
+  auto* key_s = dev_alloc<unsigned long long>(m, st);
+  auto* lo = dev_alloc<int32_t>(m, st);
+  auto* hi_row = dev_alloc<int32_t>(m, st);
+  auto* nnz = dev_alloc<int32_t>(m, st);
+  auto* sg = dev_alloc<int8_t>(m, st);
+  auto* idx = dev_alloc<int32_t>(m, st);
+  auto* srow = dev_alloc<int32_t>(m, st);
+  auto* head_pos = dev_alloc<int32_t>(m, st);
+  auto* lead_pos = dev_alloc<int32_t>(m, st);
+  auto* leader_row = dev_alloc<int32_t>(m, st);
+  auto* run_of_row = dev_alloc<int32_t>(m, st);
+  auto* collide = dev_alloc<int32_t>(m, st);
+  auto* head = dev_alloc<int32_t>(m, st);
+  auto* gid = dev_alloc<int32_t>(m, st);
 
   k_row_summary<<<gm, T, 0, st>>>(c.J, m, n, m, key, lo, hi_row, nnz, sg, idx);
   CMPC_LAUNCHED();
@@ -256,7 +250,7 @@ void analyze_structure(Ctx& c) {
   cub::DeviceScan::ExclusiveSum(nullptr, need, head, gid, (int)m + 1, st);
   tmp_bytes = std::max(tmp_bytes, need);
   // group sort and member pointer scan use at most m items as well
-  auto* tmp = dalloc<unsigned char>(tmp_bytes + 256);
+  auto* tmp = dev_alloc<unsigned char>(tmp_bytes + 256, st);
 
   CMPC_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_s, idx, srow, (int)m, 0, 64, st));
   k_head0<<<gm, T, 0, st>>>(key_s, m, head_pos);
@@ -274,14 +268,14 @@ void analyze_structure(Ctx& c) {
   CMPC_CUDA(cudaMemcpyAsync(&G, gid + m - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CMPC_CUDA(cudaStreamSynchronize(st));
 
-  auto* first_pos = dalloc<int32_t>(G);
-  auto* key2 = dalloc<unsigned long long>(G);
-  auto* key2_s = dalloc<unsigned long long>(G);
-  auto* gidx = dalloc<int32_t>(G);
-  auto* gorder = dalloc<int32_t>(G);
-  auto* proto_of_group = dalloc<int32_t>(G);
-  auto* size_by_proto = dalloc<int32_t>(G + 1);
-  auto* leader = dalloc<int32_t>(G);
+  auto* first_pos = dev_alloc<int32_t>(G, st);
+  auto* key2 = dev_alloc<unsigned long long>(G, st);
+  auto* key2_s = dev_alloc<unsigned long long>(G, st);
+  auto* gidx = dev_alloc<int32_t>(G, st);
+  auto* gorder = dev_alloc<int32_t>(G, st);
+  auto* proto_of_group = dev_alloc<int32_t>(G, st);
+  auto* size_by_proto = dev_alloc<int32_t>(G + 1, st);
+  auto* leader = dev_alloc<int32_t>(G, st);
   const unsigned gg = unsigned((G + T - 1) / T);
   k_group_info<<<gm, T, 0, st>>>(head, gid, srow, hi_row, nnz, m, first_pos, key2, gidx);
   CMPC_LAUNCHED();
@@ -291,7 +285,7 @@ void analyze_structure(Ctx& c) {
   CMPC_CUDA(cudaMemsetAsync(size_by_proto, 0, sizeof(int32_t) * (G + 1), st));
   k_group_size<<<gg, T, 0, st>>>(first_pos, G, m, proto_of_group, size_by_proto);
   CMPC_LAUNCHED();
-  c.mem_ptr = dalloc<int32_t>(G + 1);
+  c.mem_ptr = dev_alloc<int32_t>(G + 1, st);
   CMPC_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, size_by_proto, c.mem_ptr, G + 1, st));
   k_proto_leader<<<gg, T, 0, st>>>(gorder, first_pos, srow, G, leader);
   CMPC_LAUNCHED();
@@ -306,22 +300,22 @@ void analyze_structure(Ctx& c) {
   c.p = G;
   c.pz = G - ps;
   c.ldp = round_up(std::max<int64_t>(ps, 1), kBK);
-  c.row_map = dalloc<int32_t>(m);
-  c.mem_rows = dalloc<int32_t>(m);
+  c.row_map = dev_alloc<int32_t>(m, st);
+  c.mem_rows = dev_alloc<int32_t>(m, st);
   k_row_map<<<gm, T, 0, st>>>(srow, gid, first_pos, proto_of_group, c.mem_ptr, sg, m, ps, c.ldp,
                               c.row_map, c.mem_rows);
   CMPC_LAUNCHED();
 
-  c.P = dalloc<double>(size_t(c.ldp * n));
+  c.P = dev_alloc<double>(size_t(c.ldp * n), st);
   CMPC_CUDA(cudaMemsetAsync(c.P, 0, sizeof(double) * c.ldp * n, st));
-  c.hi = dalloc<int32_t>(ps);
+  c.hi = dev_alloc<int32_t>(ps, st);
   if (ps > 0) {
     dim3 grid(unsigned((ps + T - 1) / T), unsigned(std::min<int64_t>(n, 64)));
     k_gather_P<<<grid, T, 0, st>>>(c.J, m, leader, hi_row, ps, n, c.ldp, c.P, c.hi);
     CMPC_LAUNCHED();
   }
-  c.sing_col = dalloc<int32_t>(c.pz);
-  c.sing_val = dalloc<double>(c.pz);
+  c.sing_col = dev_alloc<int32_t>(c.pz, st);
+  c.sing_val = dev_alloc<double>(c.pz, st);
   if (c.pz > 0) {
     k_singletons<<<unsigned((c.pz + T - 1) / T), T, 0, st>>>(c.J, m, leader, lo, ps, c.pz,
                                                              c.sing_col, c.sing_val);
@@ -347,7 +341,7 @@ void analyze_structure(Ctx& c) {
                   (void*)run_of_row, (void*)collide, (void*)head, (void*)gid, (void*)tmp,
                   (void*)first_pos, (void*)key2, (void*)key2_s, (void*)gidx, (void*)gorder,
                   (void*)proto_of_group, (void*)size_by_proto, (void*)leader})
-    cudaFree(p);
+    dev_free(p, st);
 }
 
 }  // namespace cmpc

@@ -200,7 +200,7 @@ PFN_encodeTiled get_encode() {
 void syrk_free(Ctx& c) {
   for (void* p : {(void*)c.units, (void*)c.tile_ptr, (void*)c.tile_units, (void*)c.tiles,
                   (void*)c.partial})
-    if (p) cudaFree(p);
+    dev_free(p, c.stream);
   c.units = nullptr;
   c.tile_ptr = c.tile_units = nullptr;
   c.tiles = nullptr;
@@ -250,24 +250,28 @@ void syrk_plan(Ctx& c) {
   }
   c.nunits = (int)units.size();
   c.ntiles = (int)tiles.size();
-  CMPC_CUDA(cudaMalloc(&c.units, sizeof(int4) * std::max<size_t>(1, units.size())));
-  CMPC_CUDA(cudaMalloc(&c.tiles, sizeof(int2) * tiles.size()));
-  CMPC_CUDA(cudaMalloc(&c.tile_ptr, sizeof(int32_t) * tptr.size()));
-  CMPC_CUDA(cudaMalloc(&c.tile_units, sizeof(int32_t) * std::max<size_t>(1, tunits.size())));
-  CMPC_CUDA(cudaMalloc(&c.partial, sizeof(double) * kTile * kTile * std::max(1, c.nunits)));
+  cudaStream_t st = c.stream;
+  c.units = dev_alloc<int4>(units.size(), st);
+  c.tiles = dev_alloc<int2>(tiles.size(), st);
+  c.tile_ptr = dev_alloc<int32_t>(tptr.size(), st);
+  c.tile_units = dev_alloc<int32_t>(tunits.size(), st);
+  c.partial = dev_alloc<double>((size_t)kTile * kTile * std::max(1, c.nunits), st);
   if (!units.empty())
-    CMPC_CUDA(cudaMemcpy(c.units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice));
-  CMPC_CUDA(cudaMemcpy(c.tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice));
-  CMPC_CUDA(cudaMemcpy(c.tile_ptr, tptr.data(), sizeof(int32_t) * tptr.size(), cudaMemcpyHostToDevice));
+    CMPC_CUDA(cudaMemcpyAsync(c.units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaMemcpyAsync(c.tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaMemcpyAsync(c.tile_ptr, tptr.data(), sizeof(int32_t) * tptr.size(), cudaMemcpyHostToDevice, st));
   if (!tunits.empty())
-    CMPC_CUDA(cudaMemcpy(c.tile_units, tunits.data(), sizeof(int32_t) * tunits.size(),
-                         cudaMemcpyHostToDevice));
+    CMPC_CUDA(cudaMemcpyAsync(c.tile_units, tunits.data(), sizeof(int32_t) * tunits.size(),
+                              cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
 
   // algorithmic work of one condensation: lower triangle of P' diag(omega) P
   {
     std::vector<int32_t> hh(size_t(std::max<int64_t>(c.ps, 1)));
-    if (c.ps > 0)
-      CMPC_CUDA(cudaMemcpy(hh.data(), c.hi, sizeof(int32_t) * c.ps, cudaMemcpyDeviceToHost));
+    if (c.ps > 0) {
+      CMPC_CUDA(cudaMemcpyAsync(hh.data(), c.hi, sizeof(int32_t) * c.ps, cudaMemcpyDeviceToHost, c.stream));
+      CMPC_CUDA(cudaStreamSynchronize(c.stream));
+    }
     double f = 0.0, b = 0.0;
     for (int64_t k = 0; k < c.ps; ++k) {
       f += double(hh[size_t(k)]) * double(hh[size_t(k)] + 1);

@@ -537,33 +537,26 @@ __global__ void k_reset_packet(Packet* pk, int which) {
   }
 }
 
-template <typename T>
-T* dz(size_t count) {
-  T* p = nullptr;
-  CMPC_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
-  CMPC_CUDA(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)));
-  return p;
-}
+
 
 }  // namespace
 
 void vec_alloc(Ctx& c) {
   const size_t n = (size_t)c.n, m = (size_t)c.m;
   const size_t py = (size_t)(c.ldp + c.pz);  // prototype-indexed arrays
-  c.v = dz<double>(n); c.s = dz<double>(m); c.lam = dz<double>(m); c.z = dz<double>(m);
-  c.r1 = dz<double>(n); c.r2 = dz<double>(m); c.r3 = dz<double>(m);
-  c.Hv = dz<double>(n); c.Jtl = dz<double>(n); c.y = dz<double>(py); c.sigma = dz<double>(m);
-  c.omega = dz<double>(py); c.q = dz<double>(py); c.dsing = dz<double>(n); c.rhs = dz<double>(n);
-  c.M = dz<double>(n * n); c.L = dz<double>(n * n);
-  c.pv = dz<double>(n); c.ps_ = dz<double>(m); c.pl = dz<double>(m); c.pzd = dz<double>(m);
-  c.Jpv = dz<double>(m); c.vt = dz<double>(n); c.yt = dz<double>(py); c.Hvt = dz<double>(n);
-  c.part = dz<double>((size_t)kPartBlocks * kSlots);
+  c.v = dev_zeros<double>(n, c.stream); c.s = dev_zeros<double>(m, c.stream); c.lam = dev_zeros<double>(m, c.stream); c.z = dev_zeros<double>(m, c.stream);
+  c.r1 = dev_zeros<double>(n, c.stream); c.r2 = dev_zeros<double>(m, c.stream); c.r3 = dev_zeros<double>(m, c.stream);
+  c.Hv = dev_zeros<double>(n, c.stream); c.Jtl = dev_zeros<double>(n, c.stream); c.y = dev_zeros<double>(py, c.stream); c.sigma = dev_zeros<double>(m, c.stream);
+  c.omega = dev_zeros<double>(py, c.stream); c.q = dev_zeros<double>(py, c.stream); c.dsing = dev_zeros<double>(n, c.stream); c.rhs = dev_zeros<double>(n, c.stream);
+  c.M = dev_zeros<double>(n * n, c.stream); c.L = dev_zeros<double>(n * n, c.stream);
+  c.pv = dev_zeros<double>(n, c.stream); c.ps_ = dev_zeros<double>(m, c.stream); c.pl = dev_zeros<double>(m, c.stream); c.pzd = dev_zeros<double>(m, c.stream);
+  c.Jpv = dev_zeros<double>(m, c.stream); c.vt = dev_zeros<double>(n, c.stream); c.yt = dev_zeros<double>(py, c.stream); c.Hvt = dev_zeros<double>(n, c.stream);
+  c.part = dev_zeros<double>((size_t)kPartBlocks * kSlots, c.stream);
   const int rc = 2048;
   c.colchunks = (int)std::max<int64_t>(1, ceil_div(c.ps, rc));
-  c.colpart = dz<double>((size_t)c.colchunks * n);
-  c.hmax = dz<double>(1);
-  CMPC_CUDA(cudaMalloc(&c.pk, sizeof(Packet)));
-  CMPC_CUDA(cudaMemset(c.pk, 0, sizeof(Packet)));
+  c.colpart = dev_zeros<double>((size_t)c.colchunks * n, c.stream);
+  c.hmax = dev_zeros<double>(1, c.stream);
+  c.pk = dev_zeros<Packet>(1, c.stream);
   CMPC_CUDA(cudaMallocHost(&c.pk_host, sizeof(Packet)));
   chol_alloc(c);
   if (c.n > 0) {
@@ -579,7 +572,7 @@ void vec_free(Ctx& c) {
                   (void*)c.L, (void*)c.pv, (void*)c.ps_, (void*)c.pl, (void*)c.pzd, (void*)c.Jpv,
                   (void*)c.vt, (void*)c.yt, (void*)c.Hvt, (void*)c.part, (void*)c.colpart,
                   (void*)c.hmax, (void*)c.pk})
-    if (p) cudaFree(p);
+    dev_free(p, c.stream);
   if (c.pk_host) cudaFreeHost(c.pk_host);
   chol_free(c);
   c.v = c.s = c.lam = c.z = c.r1 = c.r2 = c.r3 = c.Hv = c.Jtl = c.y = c.sigma = nullptr;

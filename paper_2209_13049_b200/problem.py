@@ -174,7 +174,7 @@ def _apply_Q(Qt, X, diag):
 
 def _diag_or_none(Mx):
     d = np.diag(Mx).copy()
-    return d if np.count_nonzero(Mx - np.diag(d)) == 0 else None
+    return d if np.count_nonzero(Mx) == np.count_nonzero(d) else None
 
 
 def free_response(A_K, x_bar, w):
@@ -345,17 +345,22 @@ def recover_trajectory(qp: DenseQp, v) -> Trajectory:
             qp.gk[k] = A_K @ qp.gk[k - 1]
         qp.x0 = free_response(A_K, data.x_bar, data.w)
     x = qp.x0.copy()
-    for t in range(1, dm.T + 1):
-        # sum_{j<t} G_{t-1-j} v_j
-        x[t] += np.einsum("kij,kj->i", qp.gk[t - 1::-1], vt[:t])
+    # x_t += sum_{j<t} G_{t-1-j} v_j, one GEMM per lag k = t-1-j
+    for k in range(dm.T):
+        x[k + 1:] += vt[:dm.T - k] @ qp.gk[k].T
     u = x[:-1] @ data.K.T + vt
+    cache = qp.__dict__.setdefault("_quad_cache", {})
+    if cache.get("src") is not data:
+        cache.clear()
+        cache.update(src=data, Q=_diag_or_none(data.Q), Qf=_diag_or_none(data.Qf),
+                     R=_diag_or_none(data.R), S0=not np.any(data.S))
 
-    def quad(X, Mx):
-        d = _diag_or_none(Mx)
+    def quad(X, Mx, d):
         return (X * X) @ d if d is not None else np.einsum("ti,ti->t", X @ Mx, X)
 
-    obj = float(quad(x[-1:], data.Qf)[0])
-    per_t = quad(x[:-1], data.Q) + 2.0 * np.einsum("ti,ti->t", x[:-1] @ data.S, u) + quad(u, data.R)
+    obj = float(quad(x[-1:], data.Qf, cache["Qf"])[0])
+    cross = 0.0 if cache["S0"] else 2.0 * np.einsum("ti,ti->t", x[:-1] @ data.S, u)
+    per_t = quad(x[:-1], data.Q, cache["Q"]) + cross + quad(u, data.R, cache["R"])
     obj += float(per_t.sum())
     return Trajectory(x=x, u=u, v=vt.copy(), objective=obj)
 
