@@ -40,6 +40,16 @@ void cmpc_ctx_destroy(cmpc_ctx* ctx);
  * Runs the exact structure analysis of J (distinct rows up to sign, prefix widths). */
 int cmpc_load_qp(cmpc_ctx* ctx, int64_t n, int64_t m, const double* H, const double* h, double h0,
                  const double* J, const double* d, int on_device);
+/* A new context (own stream and iterate buffers) holding a device copy of ctx's loaded QP
+ * and its structure: instances that share H and J and differ in h, h0, d (the
+ * refresh_initial_state case, config 5's batch) are cloned and then updated with
+ * cmpc_update_qp_affine instead of re-uploading and re-analysing J. */
+int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out);
+/* Solve `count` loaded contexts concurrently: a pool of `threads` host threads, each driving
+ * its contexts' own streams (the GPU overlaps the instances). v_out: count x n (nullable),
+ * scal_out: count x 13 (cmpc_solve's out_scalars per instance). */
+int cmpc_solve_batch(cmpc_ctx** ctxs, int64_t count, const double* opts, int64_t max_iter,
+                     double* v_out, double* scal_out, int threads);
 /* out[8] = n, m, prototypes, SYRK prototypes, singleton prototypes, SYRK work units,
  * algorithmic SYRK flops per condensation (sum over prototypes of hi (hi + 1)),
  * algorithmic bytes of one pass over P (8 x nonzeros) */

@@ -53,6 +53,8 @@ SIGNATURES = {
     "cmpc_cholesky_solve": (C.c_int, [C.c_int, C.c_int64, D, D, D]),
     "cmpc_fraction_to_boundary": (C.c_int, [C.c_int, C.c_int64, D, D, D, D, C.c_double, D]),
     "cmpc_time_phase": (C.c_int, [C.c_void_p, C.c_int, C.c_int, D]),
+    "cmpc_ctx_clone": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "cmpc_solve_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int64, D, C.c_int64, D, D, C.c_int]),
 }
 
 

@@ -1,10 +1,13 @@
 // C ABI (include/condmpc_cuda.h): context lifecycle, QP upload, per-step entry points and
 // the stand-alone linear algebra of the reference's plug point.
+#include <atomic>
 #include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/condmpc_cuda.h"
@@ -171,6 +174,91 @@ int cmpc_load_qp(cmpc_ctx* x, int64_t n, int64_t m, const double* H, const doubl
     tick("alloc");
     return CMPC_OK;
   });
+}
+
+int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
+  cmpc_ctx* x = nullptr;
+  int rc = cmpc_ctx_create(&x, src->c.device);
+  if (rc) return rc;
+  rc = guard([&] {
+    const Ctx& s = src->c;
+    Ctx& c = x->c;
+    require_loaded(const_cast<Ctx&>(s));
+    CMPC_CUDA(cudaStreamSynchronize(s.stream));
+    c.n = s.n;
+    c.m = s.m;
+    c.h0 = s.h0;
+    c.ps = s.ps;
+    c.pz = s.pz;
+    c.p = s.p;
+    c.ldp = s.ldp;
+    c.zero_k = s.zero_k;
+    c.h_start_col = s.h_start_col;
+    cudaStream_t st = c.stream;
+    auto dup = [&](auto* src_ptr, size_t count) {
+      using T = std::remove_const_t<std::remove_pointer_t<decltype(src_ptr)>>;
+      T* dst = dev_alloc<T>(count, st);
+      if (count > 0 && src_ptr)
+        CMPC_CUDA(cudaMemcpyAsync(dst, src_ptr, sizeof(T) * count, cudaMemcpyDeviceToDevice, st));
+      return dst;
+    };
+    c.H = dup(s.H, size_t(s.n * s.n));
+    c.h = dup(s.h, size_t(s.n));
+    c.d = dup(s.d, size_t(s.m));
+    c.J = nullptr;
+    c.P = dup(s.P, size_t(s.ldp * s.n));
+    c.hi = dup(s.hi, size_t(s.ps));
+    c.start_col = dup(s.start_col, size_t(s.n + 1));
+    c.row_map = dup(s.row_map, size_t(s.m));
+    c.mem_ptr = dup(s.mem_ptr, size_t(s.p + 1));
+    c.mem_rows = dup(s.mem_rows, size_t(s.m));
+    c.sing_col = dup(s.sing_col, size_t(s.pz));
+    c.sing_val = dup(s.sing_val, size_t(s.pz));
+    syrk_plan(c);
+    vec_alloc(c);
+    sync(c);
+    return CMPC_OK;
+  });
+  if (rc) {
+    cmpc_ctx_destroy(x);
+    return rc;
+  }
+  *out = x;
+  return CMPC_OK;
+}
+
+int cmpc_solve_batch(cmpc_ctx** ctxs, int64_t count, const double* opts, int64_t max_iter,
+                     double* v_out, double* scal_out, int threads) {
+  if (count <= 0) return CMPC_OK;
+  if (threads < 1) threads = 1;
+  if (threads > count) threads = (int)count;
+  std::atomic<int64_t> next{0};
+  std::atomic<int> err{0};
+  std::string first_error;
+  std::atomic<bool> have_error{false};
+  auto worker = [&] {
+    for (;;) {
+      const int64_t i = next.fetch_add(1);
+      if (i >= count || err.load() != 0) break;
+      Ctx& c = ctxs[i]->c;
+      const int rc = guard([&] {
+        CMPC_CUDA(cudaSetDevice(c.device));
+        require_loaded(c);
+        return solve_loop(c, opts, max_iter, v_out ? v_out + i * c.n : nullptr, nullptr, nullptr,
+                          nullptr, scal_out + i * 13, nullptr, nullptr, nullptr);
+      });
+      if (rc < 0 && !have_error.exchange(true)) {
+        first_error = g_error;
+        err.store(rc);
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+  if (err.load() != 0) g_error = first_error;
+  return err.load();
 }
 
 int cmpc_qp_info(cmpc_ctx* x, int64_t* out) {

@@ -28,7 +28,7 @@ constexpr int kNB = 64;
 constexpr int kLD = kNB + 1;
 constexpr int kGemmLD = 68;
 constexpr int kGemmSmem = 2 * kNB * kGemmLD * 8;
-constexpr int kPotfSmem = (2 * kNB * kLD + 16 * 65 + 64) * 8;
+constexpr int kPotfSmem = (2 * kNB * kLD + 8 * 64) * 8;
 
 __global__ void k_chol_copy(const double* __restrict__ M, double* __restrict__ L, int64_t n,
                             double delta, long long* info) {
@@ -62,27 +62,43 @@ __device__ void inv64(const double* a, double* w) {
   }
 }
 
-// load the b x b diagonal block at (k0, k0); identity padding beyond b
+// load the b x b diagonal block at (k0, k0); identity padding beyond b. All 16 loads of a
+// thread are issued before any shared store (generic pointers would otherwise serialise them).
 __device__ void load_diag(const double* L, int64_t n, int64_t k0, int b, double* a) {
-  for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
-    const int i = e & 63, j = e >> 6;
-    double v = 0.0;
+  double v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int e = threadIdx.x + 256 * u, i = e & 63, j = e >> 6;
+    double x = 0.0;
     if (i < b && j < b) {
-      if (i >= j) v = L[(k0 + i) + (k0 + j) * n];
+      if (i >= j) x = L[(k0 + i) + (k0 + j) * n];
     } else if (i == j) {
-      v = 1.0;
+      x = 1.0;
     }
-    a[i + j * kLD] = v;
+    v[u] = x;
+  }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int e = threadIdx.x + 256 * u;
+    a[(e & 63) + (e >> 6) * kLD] = v[u];
   }
 }
 
 // write the lower b x b part of a to L and the full (zero-upper) 64 x 64 W
 __device__ void store_diag(double* L, int64_t n, int64_t k0, int b, const double* a, const double* w,
                            double* Wout, bool write_l) {
-  for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
-    const int i = e & 63, j = e >> 6;
-    if (write_l && i < b && j < b && i >= j) L[(k0 + i) + (k0 + j) * n] = a[i + j * kLD];
-    Wout[e] = (i >= j) ? w[i + j * kLD] : 0.0;
+  double va[16], vw[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int e = threadIdx.x + 256 * u, i = e & 63, j = e >> 6;
+    va[u] = a[i + j * kLD];
+    vw[u] = (i >= j) ? w[i + j * kLD] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int e = threadIdx.x + 256 * u, i = e & 63, j = e >> 6;
+    if (write_l && i < b && j < b && i >= j) L[(k0 + i) + (k0 + j) * n] = va[u];
+    Wout[e] = vw[u];
   }
 }
 
@@ -102,153 +118,157 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// One warp factors the 16 x 16 lower block of a at (o, o) in registers (lane & 15 = row;
-// lanes 16..31 mirror 0..15 so every shuffle is warp-uniform) and writes L and L^{-1}
-// (into w) back to shared memory. Returns the first failing local pivot or -1.
-// The step loops are deliberately not unrolled (the register row is rotated instead of
-// indexed): a fully unrolled body is ~30 KB of straight-line SASS whose instruction fetch,
-// not the arithmetic, set the pace (27k cycles measured vs ~4k for this form).
-__device__ int warp_potf2_inv16(double* a, double* w, int o, int bvalid, double* bc) {
-  // bc: 2 x 32 doubles of shared scratch, double-buffered by step parity:
-  // [0,16) column j of L, [16,32) row j of W
-  const int lane = threadIdx.x & 31, row = lane & 15;
-  double r[16], wr[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    r[k] = (k <= row) ? a[(o + row) + (o + k) * kLD] : 0.0;
-    wr[k] = (k == row) ? 1.0 : 0.0;
+// 1/x for x > 0 from a float seed and two Newton steps (exact fallback outside float range)
+__device__ __forceinline__ double rcp_fast(double x) {
+  if (x > 1e-30 && x < 1e30) {
+    double y = (double)__frcp_rn((float)x);
+    y = y * fma(-x, y, 2.0);
+    y = y * fma(-x, y, 2.0);
+    return y;
   }
-  int fail = -1;
-  // step j: factor column j of L and, interleaved, step j of the substitution L W = I
-  // (row j of W is final once scaled by 1/l_jj; rows below subtract l_ij W_j). The column
-  // and the row are broadcast through shared memory: a 64-bit shuffle costs ~10 issue
-  // cycles per lane-pair on one warp, a broadcast LDS far less.
-#pragma unroll 1
-  for (int j = 0; j < 16; ++j) {
-    double* cb = bc + 32 * (j & 1);
-    // r[0] holds column j of this row (rotated)
-    const double pj = __shfl_sync(kFull, r[0], j);
-    if (fail < 0 && j < bvalid && (!(pj > 0.0) || !isfinite(pj))) fail = j;
-    const double y = rsqrt_fast(pj);
-    double lij = r[0];
-    if (row == j) {
-      lij = pj * y;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) wr[k] *= y;
-      if (lane == j) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) cb[16 + k] = wr[k];
-      }
-    } else if (row > j) {
-      lij = r[0] * y;
-    }
-    if (lane < 16) {
-      cb[row] = lij;
-      if (row >= j) a[(o + row) + (o + j) * kLD] = lij;
-    }
-    __syncwarp();
-    if (row > j) {
-#pragma unroll
-      for (int k = 1; k < 16; ++k) {
-        if (row >= j + k) r[k] = fma(-lij, cb[(j + k) & 15], r[k]);
-      }
-#pragma unroll
-      for (int k = 0; k < 16; ++k) wr[k] = fma(-lij, cb[16 + k], wr[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < 15; ++k) r[k] = r[k + 1];
-    r[15] = 0.0;
-  }
-  if (fail >= 0) return fail;
-  if (lane < 16) {
-#pragma unroll
-    for (int k = 0; k < 16; ++k) w[(o + row) + (o + k) * kLD] = (k <= row) ? wr[k] : 0.0;
-  }
-  return -1;
+  return 1.0 / x;
 }
 
-// Factor the b x b diagonal block at (k0, k0) and build W = L_kk^{-1}: four 16-wide
-// column blocks, each factored (with its inverse) inside one warp's registers, then the
-// panel below (A_ik <- A_ik W16^T) and the trailing update by all 8 warps; W's off-diagonal
-// blocks follow from W_ij = -W_ii sum_{k=j}^{i-1} L_ik W_kj (three dependent stages).
+// Every thread factors the same 8 x 8 diagonal block in its own registers (redundantly:
+// no shuffles, no barriers on the pivot chain) and forms its inverse. Returns the first
+// failing local pivot (< bvalid) or -1. l, wi: lower triangles, row-major packed by hand.
+__device__ __forceinline__ int potf2_inv8(const double* a, int o, int bvalid, double (&l)[8][8],
+                                          double (&wi)[8][8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) l[i][j] = a[(o + i) + (o + j) * kLD];
+  int fail = -1;
+  double rl[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double d = l[j][j];
+    if (fail < 0 && j < bvalid && (!(d > 0.0) || !isfinite(d))) fail = j;
+    const double y = rsqrt_fast(d);
+    rl[j] = y;
+    l[j][j] = d * y;
+#pragma unroll
+    for (int i = j + 1; i < 8; ++i) l[i][j] *= y;
+#pragma unroll
+    for (int k = j + 1; k < 8; ++k)
+#pragma unroll
+      for (int i = k; i < 8; ++i) l[i][k] = fma(-l[i][j], l[k][j], l[i][k]);
+  }
+  // W = L^{-1}: W_pp = 1/l_pp, W_pk = -(1/l_pp) sum_{q=k}^{p-1} l_pq W_qk
+#pragma unroll
+  for (int p2 = 0; p2 < 8; ++p2) {
+    wi[p2][p2] = rl[p2];
+#pragma unroll
+    for (int k = 0; k < p2; ++k) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int q = k; q < p2; ++q) sacc = fma(l[p2][q], wi[q][k], sacc);
+      wi[p2][k] = -rl[p2] * sacc;
+    }
+  }
+  return fail;
+}
+
+// Factor the b x b diagonal block at (k0, k0) and build W = L_kk^{-1}. Eight 8-wide column
+// blocks: each 8 x 8 diagonal block is factored (with its inverse) redundantly in every
+// thread's registers, so the sequential pivot chain runs without any communication; the rows
+// below become X = A W8^T (each thread its row, W8 in registers) and all threads apply the
+// rank-8 trailing update. W's off-diagonal 8 x 8 blocks follow from
+// W_ij = -W_ii sum_{k=j}^{i-1} L_ik W_kj (seven dependent stages).
 __global__ void __launch_bounds__(256) k_potf2_inv(double* __restrict__ L, int64_t n, int64_t k0,
                                                    int b, long long* info, double* __restrict__ Wout) {
   extern __shared__ double sm[];
-  double* a = sm;              // kNB x kLD
-  double* w = sm + kNB * kLD;  // kNB x kLD
-  double* tt = w + kNB * kLD;  // 64 x 17 scratch (panel / W stages)
+  double* a = sm;               // kNB x kLD
+  double* w = sm + kNB * kLD;   // kNB x kLD
+  double* tt = w + kNB * kLD;   // 8 x 64 scratch (W stages)
   __shared__ int fail;
   if (*info != 0) return;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x;
   load_diag(L, n, k0, b, a);
   for (int e = tid; e < kNB * kNB; e += blockDim.x) w[(e & 63) + (e >> 6) * kLD] = 0.0;
   if (tid == 0) fail = -1;
   __syncthreads();
-  for (int kb = 0; kb < 4; ++kb) {
-    const int o = 16 * kb;
-    if (warp == 0) {
-      const int bv = b - o < 0 ? 0 : (b - o > 16 ? 16 : b - o);
-      const int f = warp_potf2_inv16(a, w, o, bv, tt + 16 * 65);
-      if (f >= 0 && tid == 0) fail = o + f;
+  for (int kb = 0; kb < 8; ++kb) {
+    const int o = 8 * kb;
+    const int bv = b - o < 0 ? 0 : (b - o > 8 ? 8 : b - o);
+    double l[8][8], wi[8][8];
+    const int f = potf2_inv8(a, o, bv, l, wi);
+    if (f >= 0) {
+      if (tid == 0) *info = (long long)(k0 + o + f + 1);
+      return;  // uniform: every thread computed the same block
     }
-    __syncthreads();
-    if (fail >= 0) {
-      if (tid == 0) *info = (long long)(k0 + fail + 1);
-      return;
-    }
-    const int rows = kNB - o - 16;  // panel rows below the block
-    if (rows > 0) {
-      // panel: X(i, c) = sum_{p <= c} A(i, o+p) W16(c, p), rows i = o+16.., 16 columns
-      for (int e = tid; e < rows * 16; e += blockDim.x) {
-        const int i = o + 16 + e % rows, c = e / rows;
-        double s = 0.0;
-#pragma unroll 4
-        for (int q = 0; q <= c; ++q) s = fma(a[i + (o + q) * kLD], w[(o + c) + (o + q) * kLD], s);
-        tt[(i - o - 16) + c * 65] = s;
-      }
-      __syncthreads();
-      for (int e = tid; e < rows * 16; e += blockDim.x) {
-        const int i = e % rows, c = e / rows;
-        a[(o + 16 + i) + (o + c) * kLD] = tt[i + c * 65];
-      }
-      __syncthreads();
-      // trailing: A(i, j) -= sum_p X(i, p) X(j, p) for o+16 <= j <= i < 64
-      const int cnt = rows * rows;
-      for (int e = tid; e < cnt; e += blockDim.x) {
-        const int ii = e % rows, jj = e / rows;
-        if (ii < jj) continue;
-        const int i = o + 16 + ii, j = o + 16 + jj;
-        double s = 0.0;
+    __syncthreads();  // all threads have read the block before it is overwritten
+    if (tid < 64) {
+      const int i = tid & 7, j = tid >> 3;
+      if (j <= i) {
 #pragma unroll
-        for (int p = 0; p < 16; ++p) s = fma(a[i + (o + p) * kLD], a[j + (o + p) * kLD], s);
-        a[i + j * kLD] -= s;
+        for (int ii = 0; ii < 8; ++ii)
+#pragma unroll
+          for (int jj = 0; jj <= ii; ++jj)
+            if (ii == i && jj == j) {
+              a[(o + i) + (o + j) * kLD] = l[ii][jj];
+              w[(o + i) + (o + j) * kLD] = wi[ii][jj];
+            }
+      }
+    }
+    const int rows = kNB - o - 8;
+    if (rows > 0) {
+      // panel: X(i, :) = A(i, o:o+8) W8^T, one thread per row
+      if (tid < rows) {
+        const int i = o + 8 + tid;
+        double x[8], y[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = a[i + (o + c) * kLD];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int q = 0; q <= c; ++q) sacc = fma(x[q], wi[c][q], sacc);
+          y[c] = sacc;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) a[i + (o + c) * kLD] = y[c];
       }
       __syncthreads();
-    }
-  }
-  // off-diagonal blocks of W, by block distance d = i - j
-  for (int d = 1; d < 4; ++d) {
-    const int nblk = 4 - d;  // blocks (j + d, j), j = 0 .. nblk-1
-    // T(j) = sum_{k=j}^{j+d-1} L(j+d, k) W(k, j)   (16 x 16 each)
-    for (int e = tid; e < nblk * 256; e += blockDim.x) {
-      const int jb = e >> 8, r = (e >> 4) & 15, c = e & 15;
-      const int ib = jb + d;
-      double s = 0.0;
-      for (int kb2 = jb; kb2 < ib; ++kb2)
-#pragma unroll 4
-        for (int q = 0; q < 16; ++q)
-          s = fma(a[(16 * ib + r) + (16 * kb2 + q) * kLD], w[(16 * kb2 + q) + (16 * jb + c) * kLD], s);
-      tt[(e & 255) + jb * 256] = s;
+      // trailing: A(i, j) -= sum_p X(i, p) X(j, p) for o+8 <= j <= i < 64
+      const int cnt = rows * (rows + 1) / 2;
+      for (int e = tid; e < cnt; e += blockDim.x) {
+        // e -> (ii, jj) with jj <= ii, row-major over the lower triangle
+        int ii = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+        while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
+        while (ii * (ii + 1) / 2 > e) --ii;
+        const int jj = e - ii * (ii + 1) / 2;
+        const int i = o + 8 + ii, j = o + 8 + jj;
+        double sacc = 0.0;
+#pragma unroll
+        for (int p2 = 0; p2 < 8; ++p2) sacc = fma(a[i + (o + p2) * kLD], a[j + (o + p2) * kLD], sacc);
+        a[i + j * kLD] -= sacc;
+      }
     }
     __syncthreads();
-    // W(j+d, j) = -W(j+d, j+d) T(j)
-    for (int e = tid; e < nblk * 256; e += blockDim.x) {
-      const int jb = e >> 8, r = (e >> 4) & 15, c = e & 15;
+  }
+  // off-diagonal 8 x 8 blocks of W by block distance d = i - j
+  for (int d = 1; d < 8; ++d) {
+    const int nblk = 8 - d;  // blocks (j + d, j)
+    for (int e = tid; e < nblk * 64; e += blockDim.x) {
+      const int jb = e >> 6, r = (e >> 3) & 7, c = e & 7;
       const int ib = jb + d;
-      double s = 0.0;
-#pragma unroll 4
-      for (int q = 0; q <= r; ++q) s = fma(w[(16 * ib + r) + (16 * ib + q) * kLD], tt[(q << 4 | c) + jb * 256], s);
-      w[(16 * ib + r) + (16 * jb + c) * kLD] = -s;
+      double sacc = 0.0;
+      for (int kb2 = jb; kb2 < ib; ++kb2)
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          sacc = fma(a[(8 * ib + r) + (8 * kb2 + q) * kLD], w[(8 * kb2 + q) + (8 * jb + c) * kLD], sacc);
+      tt[e] = sacc;
+    }
+    __syncthreads();
+    for (int e = tid; e < nblk * 64; e += blockDim.x) {
+      const int jb = e >> 6, r = (e >> 3) & 7, c = e & 7;
+      const int ib = jb + d;
+      double sacc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q <= r) sacc = fma(w[(8 * ib + r) + (8 * ib + q) * kLD], tt[(jb << 6) | (q << 3) | c], sacc);
+      w[(8 * ib + r) + (8 * jb + c) * kLD] = -sacc;
     }
     __syncthreads();
   }
@@ -438,9 +458,17 @@ __global__ void __launch_bounds__(512) k_trsv(const double* __restrict__ L,
     const double* Wk = W + kb * kNB * kNB;
     // t_i = y_i - sum_{p >= tail} L[p, i] x_p (column dots, one warp per column)
     for (int i = warp; i < bs; i += 16) {
-      double u = 0.0;
-      for (int64_t p = tail + lane; p < n; p += 32) u += L[p + (r0 + i) * n] * xs[p];
-      u = warp_sum(u);
+      double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+      const double* Lc = L + (r0 + i) * n;
+      int64_t p = tail + lane;
+      for (; p + 96 < n; p += 128) {
+        u0 += Lc[p] * xs[p];
+        u1 += Lc[p + 32] * xs[p + 32];
+        u2 += Lc[p + 64] * xs[p + 64];
+        u3 += Lc[p + 96] * xs[p + 96];
+      }
+      for (; p < n; p += 32) u0 += Lc[p] * xs[p];
+      const double u = warp_sum((u0 + u1) + (u2 + u3));
       if (lane == 0) t[i] = xs[r0 + i] - u;
     }
     __syncthreads();

@@ -162,9 +162,8 @@ __global__ void __launch_bounds__(kRowT) k_mu_rows(int64_t m, const double* __re
 
 // Per prototype k (rows of J that equal +-P_k): out1[k] = sum of x1 over the member rows
 // (signed when SIGNED1), out2[k] = signed sum of x2; members in ascending row order.
-// One warp per 32 prototypes: small groups are summed by their own lane, large groups
-// (repeated rows) cooperatively by the whole warp; fixed order either way. The all-zero
-// row group (if any) contributes nothing and is skipped.
+// One lane per prototype, members in fixed (ascending) order; the all-zero row group
+// (if any) contributes nothing and is skipped.
 template <bool SIGNED1, bool HAS2>
 __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* __restrict__ mem_ptr,
                                                       const int32_t* __restrict__ mem_rows,
@@ -181,41 +180,32 @@ __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* 
     b0 = mem_ptr[k];
     b1 = mem_ptr[k + 1];
   }
-  constexpr int kSmall = 8;
+  // every lane sums its own prototype: member loads are independent, so they are issued
+  // in batches of 8 ahead of the (ordered) accumulation
   double s1 = 0.0, s2 = 0.0;
-  if (b1 - b0 <= kSmall) {
-    for (int32_t e = b0; e < b1; ++e) {
-      const int32_t rm = mem_rows[e];
-      const int32_t r = rm >> 1;
-      const double a = x1[r];
-      s1 += (SIGNED1 && (rm & 1)) ? -a : a;
-      if (HAS2) {
-        const double b = x2[r];
-        s2 += (rm & 1) ? -b : b;
+  for (int32_t e = b0; e < b1; e += 8) {
+    double v1[8], v2[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      v1[u] = 0.0;
+      v2[u] = 0.0;
+      if (e + u < b1) {
+        const int32_t rm = mem_rows[e + u];
+        const int32_t r = rm >> 1;
+        const double a = x1[r];
+        v1[u] = (SIGNED1 && (rm & 1)) ? -a : a;
+        if (HAS2) {
+          const double bb = x2[r];
+          v2[u] = (rm & 1) ? -bb : bb;
+        }
       }
     }
-  }
-  unsigned big = __ballot_sync(0xffffffffu, b1 - b0 > kSmall);
-  while (big) {
-    const int src = __ffs(big) - 1;
-    big &= big - 1;
-    const int32_t e0 = __shfl_sync(0xffffffffu, b0, src), e1 = __shfl_sync(0xffffffffu, b1, src);
-    double t1 = 0.0, t2 = 0.0;
-    for (int32_t e = e0 + lane; e < e1; e += 32) {
-      const int32_t rm = mem_rows[e];
-      const int32_t r = rm >> 1;
-      const double a = x1[r];
-      t1 += (SIGNED1 && (rm & 1)) ? -a : a;
-      if (HAS2) {
-        const double b = x2[r];
-        t2 += (rm & 1) ? -b : b;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (e + u < b1) {
+        s1 += v1[u];
+        if (HAS2) s2 += v2[u];
       }
-    }
-    t1 = warp_sum(t1);
-    if (HAS2) t2 = warp_sum(t2);
-    if (lane == src) {
-      s1 = t1;
-      s2 = t2;
     }
   }
   if (k < p) {

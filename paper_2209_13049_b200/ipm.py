@@ -162,6 +162,14 @@ class DeviceQp:
         check(_lib.lib().cmpc_time_phase(self.h, self.PHASES[name], int(reps), C.byref(ms)))
         return ms.value
 
+    def clone(self) -> "DeviceQp":
+        """A new context with a device copy of this QP and its J structure."""
+        out = DeviceQp.__new__(DeviceQp)
+        h = C.c_void_p()
+        check(_lib.lib().cmpc_ctx_clone(self.h, C.byref(h)))
+        out.h, out.n, out.m = h, self.n, self.m
+        return out
+
     def update_affine(self, h, h0, d):
         h, d = f64(h), f64(d)
         check(_lib.lib().cmpc_update_qp_affine(self.h, ptr(h), float(h0), ptr(d), 0))
@@ -333,3 +341,54 @@ def solve_loaded(dq: DeviceQp, qp: DenseQp, opts: IpmOptions, t0=None) -> IpmRes
         res.solution = Trajectory(objective=res.objective)
     res.total_seconds = time.perf_counter() - t0
     return res
+
+
+@dataclass
+class BatchResult:
+    status: list
+    iter: np.ndarray
+    objective: np.ndarray
+    kkt_error: np.ndarray
+    v: np.ndarray            # count x n
+    device_seconds: np.ndarray
+    launches: int
+    wall_seconds: float
+
+
+class BatchSolver:
+    """Independent instances that share H and J and differ in (h, h0, d) — the
+    receding-horizon / config-5 case (refresh_initial_state, reduction.cpp:270-280).
+    One device context per instance (cloned from the base QP's analysed structure), solved
+    concurrently by a pool of host threads inside the library, one CUDA stream each."""
+
+    def __init__(self, base: DenseQp, count: int):
+        self.base = base
+        root = device_qp(base)
+        self.ctxs = [root.clone() for _ in range(count)]
+        self.count = count
+
+    def set_instance(self, i: int, h, h0: float, d):
+        self.ctxs[i].update_affine(h, h0, d)
+
+    def solve(self, opts: IpmOptions = None, threads: int | None = None) -> BatchResult:
+        import os
+        opts = opts or IpmOptions()
+        _check_options(opts)
+        n, cnt = self.base.n, self.count
+        v = np.zeros((cnt, n))
+        scal = np.zeros((cnt, 13))
+        arr = (C.c_void_p * cnt)(*[c.h.value if isinstance(c.h, C.c_void_p) else c.h for c in self.ctxs])
+        od = (C.c_double * 5)(opts.tol, opts.mu_init, opts.kappa_mu, opts.tau, opts.armijo_eta)
+        t0 = time.perf_counter()
+        check(_lib.lib().cmpc_solve_batch(arr, cnt, od, int(opts.max_iter), ptr(v), ptr(scal),
+                                          int(threads or min(cnt, os.cpu_count() or 1))))
+        wall = time.perf_counter() - t0
+        return BatchResult(status=[IpmStatus(int(x)).name for x in scal[:, 0]], iter=scal[:, 1].astype(int),
+                           objective=scal[:, 3].copy(), kkt_error=scal[:, 2].copy(), v=v,
+                           device_seconds=scal[:, 6].copy(), launches=int(scal[:, 7].sum()),
+                           wall_seconds=wall)
+
+    def close(self):
+        for c in self.ctxs:
+            c.close()
+        self.ctxs = []
