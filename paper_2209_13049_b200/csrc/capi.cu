@@ -30,6 +30,7 @@ thread_local std::string g_error;
 // host loop (ipm_host.cpp)
 int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v, double* s, double* lam,
                double* z, double* out, cmpc_log_fn log, cmpc_inspect_fn inspect, void* user);
+void drop_graphs(Ctx& c);
 int line_search_host(Ctx& c, double alpha_max, double eta, double* alpha, int* ntrials);
 double merit_host(const Packet& A, double vhv, double hv, double sum_log, double sum_abs,
                   double mu, double rho, bool has_rows);
@@ -76,6 +77,7 @@ void read_packet(Ctx& c) {
 }
 
 void release_qp(Ctx& c) {
+  drop_graphs(c);
   vec_free(c);
   syrk_free(c);
   free_structure(c);
@@ -108,6 +110,9 @@ int cmpc_ctx_create(cmpc_ctx** out, int device) {
     CMPC_CUDA(cudaEventCreate(&x->c.ev1));
     CMPC_CUDA(cudaEventCreate(&x->c.ev2));
     CMPC_CUDA(cudaEventCreate(&x->c.ev3));
+    CMPC_CUDA(cudaStreamCreateWithFlags(&x->c.stream2, cudaStreamNonBlocking));
+    CMPC_CUDA(cudaEventCreateWithFlags(&x->c.fork, cudaEventDisableTiming));
+    CMPC_CUDA(cudaEventCreateWithFlags(&x->c.join, cudaEventDisableTiming));
     *out = x;
     return CMPC_OK;
   });
@@ -123,6 +128,9 @@ void cmpc_ctx_destroy(cmpc_ctx* x) {
   cudaEventDestroy(x->c.ev1);
   cudaEventDestroy(x->c.ev2);
   cudaEventDestroy(x->c.ev3);
+  cudaEventDestroy(x->c.fork);
+  cudaEventDestroy(x->c.join);
+  cudaStreamDestroy(x->c.stream2);
   cudaStreamDestroy(x->c.stream);
   delete x;
 }
@@ -314,9 +322,7 @@ int cmpc_update_qp_affine(cmpc_ctx* x, const double* h, double h0, const double*
     if (h && c.n > 0) CMPC_CUDA(cudaMemcpyAsync(c.h, h, sizeof(double) * c.n, kind, c.stream));
     if (d && c.m > 0) CMPC_CUDA(cudaMemcpyAsync(c.d, d, sizeof(double) * c.m, kind, c.stream));
     c.h0 = h0;
-    CMPC_CUDA(cudaMemsetAsync(c.hmax, 0, sizeof(double), c.stream));
-    vec_free(c);
-    vec_alloc(c);
+    launch_hmax(c);
     sync(c);
     return CMPC_OK;
   });
@@ -331,7 +337,7 @@ int cmpc_set_state(cmpc_ctx* x, const double* v, const double* s, const double* 
     h2d(c, c.s, s, c.m);
     h2d(c, c.lam, lam, c.m);
     h2d(c, c.z, z, c.m);
-    c.mu = mu;
+    set_mu(c, mu);
     sync(c);
     return CMPC_OK;
   });

@@ -89,6 +89,15 @@ struct Ctx {
   double* colpart = nullptr;  // Pt q partial: nchunks x n
   int colchunks = 0;
   double* hmax = nullptr;
+  double* d_mu = nullptr;    // barrier value on the device (kernels read it: graph-safe)
+  double* d_alpha = nullptr; // accepted step lengths {alpha, alpha_z} on the device
+  double h_alpha[2] = {0.0, 0.0};
+  // CUDA graphs of the two per-iteration segments (captured on the second iteration)
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaGraphExec_t g_step = nullptr, g_next = nullptr;
+  long long g_step_nodes = 0, g_next_nodes = 0;
+  double g_tau = 0.0;
   double* Winv = nullptr;    // inverses of the 64 x 64 diagonal blocks of L
   Packet* pk = nullptr;      // device packet
   Packet* pk_host = nullptr; // pinned mirror
@@ -122,6 +131,10 @@ void launch_chol_solve(Ctx& c, const double* L, const double* b, double* x);
 
 // ---- vec.cu
 void launch_zero_packet(Ctx& c);
+// max |h| (after h changed)
+void launch_hmax(Ctx& c);
+// set the barrier value (host copy and the device scalar the kernels read)
+void set_mu(Ctx& c, double mu);
 // residuals at the current state (r1, r2, r3, kkt, objective pieces) -> packet A;
 // reuse_trial: the state was just moved to the last evaluated line-search trial point
 void launch_residuals(Ctx& c, bool reuse_trial = false);
@@ -142,6 +155,9 @@ void launch_ls_pieces(Ctx& c);
 void launch_init_state(Ctx& c, double mu);
 // iterate update v,s,lambda += alpha p; z += alpha_z pz
 void launch_update(Ctx& c, double alpha, double alpha_z);
+// the same with the step lengths already on the device (set_alpha)
+void set_alpha(Ctx& c, double alpha, double alpha_z);
+void launch_update_dev(Ctx& c);
 // y = P x (+ singletons), Jx_r = sign y[proto]; optional
 void launch_Jx(Ctx& c, const double* x, double* y, double* Jx);
 // out = P' q + singleton scatter

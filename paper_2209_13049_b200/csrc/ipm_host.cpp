@@ -12,6 +12,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 #include <stdexcept>
 #include <vector>
@@ -33,6 +34,89 @@ void sync_packet(Ctx& c, long long* syncs) {
   CMPC_CUDA(cudaStreamSynchronize(c.stream));
   if (syncs) ++*syncs;
 }
+}  // namespace
+
+void drop_graphs(Ctx& c) {
+  if (c.g_step) cudaGraphExecDestroy(c.g_step);
+  if (c.g_next) cudaGraphExecDestroy(c.g_next);
+  c.g_step = c.g_next = nullptr;
+  c.g_step_nodes = c.g_next_nodes = 0;
+}
+
+namespace {
+
+// timing event: a plain record, or an external event-record node while capturing
+void rec(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  CMPC_CUDA(cudaStreamIsCapturing(s, &st));
+  if (st == cudaStreamCaptureStatusActive)
+    CMPC_CUDA(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+  else
+    CMPC_CUDA(cudaEventRecord(e, s));
+}
+
+// segment A: sigma/omega/q, condensation, Cholesky (delta = 0) with the right-hand side
+// J'(r2 - sigma r3) on a parallel branch, solve, recovery + fraction to boundary, trial 0
+void seg_step(Ctx& c, double tau) {
+  rec(c.ev0, c.stream);
+  launch_prepare_step(c, nullptr);
+  CMPC_CUDA(cudaEventRecord(c.fork, c.stream));
+  CMPC_CUDA(cudaStreamWaitEvent(c.stream2, c.fork, 0));
+  {
+    cudaStream_t s0 = c.stream;
+    c.stream = c.stream2;
+    launch_rhs(c);  // memory-bound pass, overlaps the tensor-core SYRK
+    c.stream = s0;
+  }
+  CMPC_CUDA(cudaEventRecord(c.join, c.stream2));
+  rec(c.ev2, c.stream);
+  launch_condense(c, false);
+  rec(c.ev3, c.stream);
+  launch_cholesky(c, c.M, c.L, 0.0);
+  rec(c.ev1, c.stream);
+  CMPC_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
+  launch_chol_solve(c, c.L, c.rhs, c.pv);
+  launch_recover(c, tau);
+  launch_trial(c, 0.0, true);
+}
+
+// segment B: the accepted step (alpha, alpha_z on the device) and the residuals after it
+void seg_next(Ctx& c) {
+  launch_update_dev(c);
+  launch_residuals(c, /*reuse_trial=*/true);
+}
+
+// run a segment eagerly, or capture it once into a CUDA graph and replay it
+template <typename F>
+void run_segment(Ctx& c, cudaGraphExec_t& exec, long long& nodes, bool allow_capture, F&& seg) {
+  if (exec) {
+    CMPC_CUDA(cudaGraphLaunch(exec, c.stream));
+    g_launches += nodes;
+    return;
+  }
+  if (!allow_capture || getenv("CMPC_NO_GRAPHS")) {
+    seg();
+    return;
+  }
+  cudaGraph_t graph = nullptr;
+  const long long l0 = g_launches;
+  CMPC_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    seg();
+  } catch (...) {
+    cudaStreamEndCapture(c.stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  CMPC_CUDA(cudaStreamEndCapture(c.stream, &graph));
+  nodes = g_launches - l0;
+  g_launches = l0;
+  CMPC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  CMPC_CUDA(cudaGraphLaunch(exec, c.stream));
+  g_launches += nodes;
+}
+
 }  // namespace
 
 // merit phi(v, s) = 0.5 v'Hv + h'v - mu sum log s + rho |Jv - d + s|_1 (ipm.cpp:25-32)
@@ -117,8 +201,10 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   CMPC_CUDA(cudaEventRecord(e_start, c.stream));
 
   // init (ipm.cpp:170-177)
-  c.mu = mu_init;
+  set_mu(c, mu_init);
   launch_init_state(c, c.mu);
+  if (c.g_tau != tau) drop_graphs(c);
+  c.g_tau = tau;
   launch_residuals(c);
   sync_packet(c, &syncs);
   Packet A = *c.pk_host;
@@ -145,23 +231,13 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     // update_barrier (ipm.cpp:146-151)
     const double mu_next = (A.kkt <= 10.0 * c.mu) ? std::max(tol / 10.0, kappa_mu * c.mu) : c.mu;
     if (mu_next != c.mu) {
-      c.mu = mu_next;
+      set_mu(c, mu_next);
       launch_residuals_mu(c);
     }
-    // sigma, condensed matrix, factorization with the shift ladder (ipm.cpp:200-226)
-    CMPC_CUDA(cudaEventRecord(c.ev0, c.stream));
-    launch_prepare_step(c, nullptr);
-    CMPC_CUDA(cudaEventRecord(c.ev2, c.stream));
-    launch_condense(c, false);
-    CMPC_CUDA(cudaEventRecord(c.ev3, c.stream));
+    // sigma, condensed matrix, factorization with the shift ladder (ipm.cpp:200-226), then
+    // speculatively: directions, recovery, fraction to boundary, line-search trial 0
     size_t shift = 0;
-    launch_cholesky(c, c.M, c.L, kShifts[shift]);
-    CMPC_CUDA(cudaEventRecord(c.ev1, c.stream));
-    // speculative: directions, recovery, fraction to boundary, line-search trial 0
-    launch_rhs(c);
-    launch_chol_solve(c, c.L, c.rhs, c.pv);
-    launch_recover(c, tau);
-    launch_trial(c, 0.0, true);
+    run_segment(c, c.g_step, c.g_step_nodes, iter >= 1, [&] { seg_step(c, tau); });
     sync_packet(c, &syncs);
     float ms = 0.f;
     CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
@@ -220,9 +296,9 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
       break;
     }
     const double mu_used = c.mu;
-    launch_update(c, alpha, alpha_z);
+    set_alpha(c, alpha, alpha_z);
     iter += 1;
-    launch_residuals(c, /*reuse_trial=*/true);
+    run_segment(c, c.g_next, c.g_next_nodes, iter >= 2, [&] { seg_next(c); });
     sync_packet(c, &syncs);
     A = *c.pk_host;
     if (log) {

@@ -106,10 +106,12 @@ __global__ void __launch_bounds__(kRowT) k_res_rows(int64_t m, const int32_t* __
                                                     const double* __restrict__ d,
                                                     const double* __restrict__ s,
                                                     const double* __restrict__ lam,
-                                                    const double* __restrict__ z, double mu,
+                                                    const double* __restrict__ z,
+                                                    const double* __restrict__ mu_p,
                                                     double* __restrict__ r2, double* __restrict__ r3,
                                                     double* __restrict__ part, Packet* pk) {
   __shared__ double sh[32];
+  const double mu = *mu_p;
   double sabs = 0.0, slog = 0.0, ml = 0.0, mss = 0.0, mz = 0.0, mr3 = 0.0, mc = 0.0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
        r += (int64_t)gridDim.x * blockDim.x) {
@@ -147,8 +149,10 @@ __global__ void __launch_bounds__(kRowT) k_res_rows(int64_t m, const int32_t* __
 // r2 and complementarity at a new barrier value (r1, r3 unchanged)
 __global__ void __launch_bounds__(kRowT) k_mu_rows(int64_t m, const double* __restrict__ s,
                                                    const double* __restrict__ lam,
-                                                   const double* __restrict__ z, double mu,
+                                                   const double* __restrict__ z,
+                                                   const double* __restrict__ mu_p,
                                                    double* __restrict__ r2, Packet* pk) {
+  const double mu = *mu_p;
   double mc = 0.0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
        r += (int64_t)gridDim.x * blockDim.x) {
@@ -334,10 +338,11 @@ __global__ void k_rhs(int64_t n, const double* __restrict__ r1, const double* __
 __global__ void __launch_bounds__(kRowT) k_recover_rows(
     int64_t m, const int32_t* __restrict__ row_map, const double* __restrict__ y,
     const double* __restrict__ s, const double* __restrict__ z, const double* __restrict__ sigma,
-    const double* __restrict__ r2, const double* __restrict__ r3, double mu, double tau,
-    double* __restrict__ Jpv, double* __restrict__ ps, double* __restrict__ pl,
+    const double* __restrict__ r2, const double* __restrict__ r3, const double* __restrict__ mu_p,
+    double tau, double* __restrict__ Jpv, double* __restrict__ ps, double* __restrict__ pl,
     double* __restrict__ pz, double* __restrict__ part, Packet* pk) {
   __shared__ double sh[32];
+  const double mu = *mu_p;
   double q = 0.0, as = 1e308, az = 1e308;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
        r += (int64_t)gridDim.x * blockDim.x) {
@@ -479,11 +484,12 @@ __global__ void __launch_bounds__(kFinT) k_trial_final(int64_t n, int64_t m, int
   }
 }
 
-__global__ void k_update(int64_t n, int64_t m, double alpha, double alpha_z, double* __restrict__ v,
+__global__ void k_update(int64_t n, int64_t m, const double* __restrict__ ap, double* __restrict__ v,
                          const double* __restrict__ pv, double* __restrict__ s,
                          const double* __restrict__ ps, double* __restrict__ lam,
                          const double* __restrict__ pl, double* __restrict__ z,
                          const double* __restrict__ pz) {
+  const double alpha = ap[0], alpha_z = ap[1];
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) v[i] = add(v[i], mul(alpha, pv[i]));
   if (i < m) {
@@ -546,6 +552,8 @@ void vec_alloc(Ctx& c) {
   c.colchunks = (int)std::max<int64_t>(1, ceil_div(c.ps, rc));
   c.colpart = dev_zeros<double>((size_t)c.colchunks * n, c.stream);
   c.hmax = dev_zeros<double>(1, c.stream);
+  c.d_mu = dev_zeros<double>(1, c.stream);
+  c.d_alpha = dev_zeros<double>(2, c.stream);
   c.pk = dev_zeros<Packet>(1, c.stream);
   CMPC_CUDA(cudaMallocHost(&c.pk_host, sizeof(Packet)));
   chol_alloc(c);
@@ -561,13 +569,13 @@ void vec_free(Ctx& c) {
                   (void*)c.omega, (void*)c.q, (void*)c.dsing, (void*)c.rhs, (void*)c.M,
                   (void*)c.L, (void*)c.pv, (void*)c.ps_, (void*)c.pl, (void*)c.pzd, (void*)c.Jpv,
                   (void*)c.vt, (void*)c.yt, (void*)c.Hvt, (void*)c.part, (void*)c.colpart,
-                  (void*)c.hmax, (void*)c.pk})
+                  (void*)c.hmax, (void*)c.pk, (void*)c.d_mu})
     dev_free(p, c.stream);
   if (c.pk_host) cudaFreeHost(c.pk_host);
   chol_free(c);
   c.v = c.s = c.lam = c.z = c.r1 = c.r2 = c.r3 = c.Hv = c.Jtl = c.y = c.sigma = nullptr;
   c.omega = c.q = c.dsing = c.rhs = c.M = c.L = c.pv = c.ps_ = c.pl = c.pzd = nullptr;
-  c.Jpv = c.vt = c.yt = c.Hvt = c.part = c.colpart = c.hmax = nullptr;
+  c.Jpv = c.vt = c.yt = c.Hvt = c.part = c.colpart = c.hmax = c.d_mu = c.d_alpha = nullptr;
   c.pk = nullptr;
   c.pk_host = nullptr;
 }
@@ -619,14 +627,16 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
   if (reuse_trial) {
     // v was just set to the accepted trial point v + alpha pv, computed with the same
     // kernel and inputs as the trial: H v and P v are the trial's, bit for bit
-    std::swap(c.Hv, c.Hvt);
-    std::swap(c.y, c.yt);
+    if (c.n > 0) CMPC_CUDA(cudaMemcpyAsync(c.Hv, c.Hvt, sizeof(double) * c.n, cudaMemcpyDeviceToDevice, c.stream));
+    const int64_t py = c.ldp + c.pz;
+    if (c.m > 0 && py > 0)
+      CMPC_CUDA(cudaMemcpyAsync(c.y, c.yt, sizeof(double) * py, cudaMemcpyDeviceToDevice, c.stream));
   } else {
     launch_Hx(c, c.v, c.Hv);
   }
   if (c.m > 0) {
     if (!reuse_trial) launch_Jx(c, c.v, c.y, nullptr);
-    k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.d, c.s, c.lam, c.z, c.mu, c.r2,
+    k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.d, c.s, c.lam, c.z, c.d_mu, c.r2,
                                            c.r3, c.part, c.pk);
     CMPC_LAUNCHED();
     k_proto_reduce<true, false><<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
@@ -643,7 +653,7 @@ void launch_residuals_mu(Ctx& c) {
   if (c.m > 0) {
     k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 3);
     CMPC_LAUNCHED();
-    k_mu_rows<<<part_blocks(c.m), kRowT, 0, c.stream>>>(c.m, c.s, c.lam, c.z, c.mu, c.r2, c.pk);
+    k_mu_rows<<<part_blocks(c.m), kRowT, 0, c.stream>>>(c.m, c.s, c.lam, c.z, c.d_mu, c.r2, c.pk);
     CMPC_LAUNCHED();
   }
   k_kkt_only<<<1, 1, 0, c.stream>>>(c.n, c.m, c.hmax, c.pk);
@@ -676,6 +686,19 @@ void launch_rhs(Ctx& c) {
   CMPC_LAUNCHED();
 }
 
+void launch_hmax(Ctx& c) {
+  CMPC_CUDA(cudaMemsetAsync(c.hmax, 0, sizeof(double), c.stream));
+  if (c.n > 0) {
+    k_absmax<<<(unsigned)std::min<int64_t>(64, ceil_div(c.n, 256)), 256, 0, c.stream>>>(c.h, c.n, c.hmax);
+    CMPC_LAUNCHED();
+  }
+}
+
+void set_mu(Ctx& c, double mu) {
+  c.mu = mu;
+  CMPC_CUDA(cudaMemcpyAsync(c.d_mu, &c.mu, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+}
+
 void launch_recover(Ctx& c, double tau) {
   k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 1);
   CMPC_LAUNCHED();
@@ -683,7 +706,7 @@ void launch_recover(Ctx& c, double tau) {
   if (c.m > 0) {
     launch_Jx(c, c.pv, c.y, nullptr);
     k_recover_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.s, c.z, c.sigma, c.r2, c.r3,
-                                               c.mu, tau, c.Jpv, c.ps_, c.pl, c.pzd, c.part, c.pk);
+                                               c.d_mu, tau, c.Jpv, c.ps_, c.pl, c.pzd, c.part, c.pk);
     CMPC_LAUNCHED();
   }
   k_recover_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m > 0 ? (int)pb : 0, c.Hv, c.h, c.pv, c.part,
@@ -742,12 +765,23 @@ void launch_init_state(Ctx& c, double mu) {
   }
 }
 
-void launch_update(Ctx& c, double alpha, double alpha_z) {
+void set_alpha(Ctx& c, double alpha, double alpha_z) {
+  c.h_alpha[0] = alpha;
+  c.h_alpha[1] = alpha_z;
+  CMPC_CUDA(cudaMemcpyAsync(c.d_alpha, c.h_alpha, 2 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+}
+
+void launch_update_dev(Ctx& c) {
   const int64_t k = std::max(c.n, c.m);
   if (k == 0) return;
-  k_update<<<(unsigned)ceil_div(k, 256), 256, 0, c.stream>>>(c.n, c.m, alpha, alpha_z, c.v, c.pv,
+  k_update<<<(unsigned)ceil_div(k, 256), 256, 0, c.stream>>>(c.n, c.m, c.d_alpha, c.v, c.pv,
                                                              c.s, c.ps_, c.lam, c.pl, c.z, c.pzd);
   CMPC_LAUNCHED();
+}
+
+void launch_update(Ctx& c, double alpha, double alpha_z) {
+  set_alpha(c, alpha, alpha_z);
+  launch_update_dev(c);
 }
 
 }  // namespace cmpc
