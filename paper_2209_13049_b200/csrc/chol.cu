@@ -7,14 +7,17 @@
 // 205-221) re-factors M + delta I; here M is kept intact and L written separately, so a
 // retry never repeats the SYRK. info = failing pivot + 1 (0 = success).
 //
-// Blocked right-looking with 64-wide panels, three kernels per panel:
-//   k_potf2_inv  1 CTA: right-looking potf2 of the diagonal block in shared memory with
-//                the inverse W = L_kk^{-1} built in the same column sweep;
-//   k_panel      L_ik = A_ik W^T for every 64-row block below (DMMA GEMM, no sequential
-//                triangular solve on the critical path);
-//   k_trail      A_ij -= L_ik L_jk^T on the trailing lower tiles (DMMA).
-// The W blocks are kept, so the triangular solves (k_trsv) are block GEMVs.
-// Every kernel returns immediately once info != 0.
+// One persistent dataflow kernel (k_chol_df) factors the whole matrix, tile by tile
+// (64 x 64, lower tiles only), left-looking:
+//   tile (i, j):  A_ij <- M_ij - sum_{k<j} L_ik L_jk^T        (DMMA, accumulator in registers)
+//                 i == j: L_jj = potf2(A_jj) and W_j = L_jj^{-1} (register-blocked, in smem)
+//                 i >  j: L_ij = A_ij W_j^T                   (DMMA, no sequential TRSM)
+// Every finished tile publishes a per-tile flag (release/acquire at GPU scope) stamped with
+// the launch's generation number, so flags never need resetting. CTAs grab tiles from an
+// atomic counter in column-major (topological) order, and a tile only waits for tiles
+// earlier in that order, which were grabbed by CTAs that are already running: the kernel
+// cannot deadlock whatever the residency. The last CTA out publishes info and advances the
+// generation. The W blocks are kept, so the triangular solves (k_trsv) are block GEMVs.
 #include <algorithm>
 
 #include "internal.cuh"
@@ -24,23 +27,30 @@ namespace cmpc {
 
 namespace {
 
+#ifdef CMPC_TRACE
+__device__ unsigned long long g_trace[256];
+#define TRACE(i)                                                   \
+  do {                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_trace[(i)] = clock64(); \
+  } while (0)
+#define TRACEW(i)                                                   \
+  do {                                                              \
+    if (blockIdx.x == 0 && threadIdx.x == 32) g_trace[(i)] = clock64(); \
+  } while (0)
+#else
+#define TRACE(i) \
+  do {           \
+  } while (0)
+#define TRACEW(i) \
+  do {            \
+  } while (0)
+#endif
+
 constexpr int kNB = 64;
 constexpr int kLD = kNB + 1;
 constexpr int kGemmLD = 68;
-constexpr int kGemmSmem = 2 * kNB * kGemmLD * 8;
 constexpr int kPotfSmem = (2 * kNB * kLD + 8 * 64) * 8;
-
-__global__ void k_chol_copy(const double* __restrict__ M, double* __restrict__ L, int64_t n,
-                            double delta, long long* info) {
-  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) *info = 0;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t j = blockIdx.y;
-  if (i >= n) return;
-  double v = 0.0;
-  if (i > j) v = M[i + j * n];
-  else if (i == j) v = delta == 0.0 ? M[i + j * n] : add(M[i + j * n], delta);
-  L[i + j * n] = v;
-}
+constexpr int kDfThreads = 256;
 
 // W = L^{-1} for the factored 64 x 64 lower block in a (identity padding beyond b),
 // right-looking substitution on L W = I: step p scales row p of W, then rows i > p
@@ -129,22 +139,44 @@ __device__ __forceinline__ double rcp_fast(double x) {
   return 1.0 / x;
 }
 
-// Every thread factors the same 8 x 8 diagonal block in its own registers (redundantly:
-// no shuffles, no barriers on the pivot chain) and forms its inverse. Returns the first
-// failing local pivot (< bvalid) or -1. l, wi: lower triangles, row-major packed by hand.
-__device__ __forceinline__ int potf2_inv8(const double* a, int o, int bvalid, double (&l)[8][8],
-                                          double (&wi)[8][8]) {
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// 1/sqrt(x): MUFU.RSQ64H seed + two Newton steps (~1/3 the latency of the float-seed
+// path with its range branch, measured in tools/exp/p1_bench.cu); flushes subnormals, so
+// the caller re-factors exactly when a pivot leaves [1e-300, 1e300]
+__device__ __forceinline__ double rsqrt_mufu(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
+// 8 x 8 Cholesky + inverse in registers (every lane redundantly) from the lower block at
+// a + o * (kLD + 1). Returns the first failing pivot (< bv) or -1; *odd flags a pivot out of
+// the fast reciprocal square root's range.
+template <bool EXACT>
+__device__ __forceinline__ int factor8(const double* a, int o, int bv, double (&l)[8][8], double (&wi)[8][8],
+                                       bool* odd) {
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j <= i; ++j) l[i][j] = a[(o + i) + (o + j) * kLD];
   int fail = -1;
+  bool bad = false;
   double rl[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const double d = l[j][j];
-    if (fail < 0 && j < bvalid && (!(d > 0.0) || !isfinite(d))) fail = j;
-    const double y = rsqrt_fast(d);
+    if (fail < 0 && j < bv && (!(d > 0.0) || !isfinite(d))) fail = j;
+    bad |= !(d >= 1e-300 && d <= 1e300);
+    const double y = EXACT ? 1.0 / sqrt(d) : rsqrt_mufu(d);
     rl[j] = y;
     l[j][j] = d * y;
 #pragma unroll
@@ -154,125 +186,235 @@ __device__ __forceinline__ int potf2_inv8(const double* a, int o, int bvalid, do
 #pragma unroll
       for (int i = k; i < 8; ++i) l[i][k] = fma(-l[i][j], l[k][j], l[i][k]);
   }
-  // W = L^{-1}: W_pp = 1/l_pp, W_pk = -(1/l_pp) sum_{q=k}^{p-1} l_pq W_qk
 #pragma unroll
-  for (int p2 = 0; p2 < 8; ++p2) {
-    wi[p2][p2] = rl[p2];
+  for (int p = 0; p < 8; ++p) {
+    wi[p][p] = rl[p];
 #pragma unroll
-    for (int k = 0; k < p2; ++k) {
-      double sacc = 0.0;
+    for (int k = 0; k < p; ++k) {
+      double s = 0.0;
 #pragma unroll
-      for (int q = k; q < p2; ++q) sacc = fma(l[p2][q], wi[q][k], sacc);
-      wi[p2][k] = -rl[p2] * sacc;
+      for (int q = k; q < p; ++q) s = fma(l[p][q], wi[q][k], s);
+      wi[p][k] = -rl[p] * s;
     }
   }
+  *odd = bad;
   return fail;
 }
 
-// Factor the b x b diagonal block at (k0, k0) and build W = L_kk^{-1}. Eight 8-wide column
-// blocks: each 8 x 8 diagonal block is factored (with its inverse) redundantly in every
-// thread's registers, so the sequential pivot chain runs without any communication; the rows
-// below become X = A W8^T (each thread its row, W8 in registers) and all threads apply the
-// rank-8 trailing update. W's off-diagonal 8 x 8 blocks follow from
-// W_ij = -W_ii sum_{k=j}^{i-1} L_ik W_kj (seven dependent stages).
-__global__ void __launch_bounds__(256) k_potf2_inv(double* __restrict__ L, int64_t n, int64_t k0,
-                                                   int b, long long* info, double* __restrict__ Wout) {
-  extern __shared__ double sm[];
-  double* a = sm;               // kNB x kLD
-  double* w = sm + kNB * kLD;   // kNB x kLD
-  double* tt = w + kNB * kLD;   // 8 x 64 scratch (W stages)
-  __shared__ int fail;
-  if (*info != 0) return;
-  const int tid = threadIdx.x;
-  load_diag(L, n, k0, b, a);
-  for (int e = tid; e < kNB * kNB; e += blockDim.x) w[(e & 63) + (e >> 6) * kLD] = 0.0;
-  if (tid == 0) fail = -1;
-  __syncthreads();
-  for (int kb = 0; kb < 8; ++kb) {
-    const int o = 8 * kb;
-    const int bv = b - o < 0 ? 0 : (b - o > 8 ? 8 : b - o);
-    double l[8][8], wi[8][8];
-    const int f = potf2_inv8(a, o, bv, l, wi);
-    if (f >= 0) {
-      if (tid == 0) *info = (long long)(k0 + o + f + 1);
-      return;  // uniform: every thread computed the same block
-    }
-    __syncthreads();  // all threads have read the block before it is overwritten
-    if (tid < 64) {
-      const int i = tid & 7, j = tid >> 3;
-      if (j <= i) {
+__device__ __forceinline__ double dot8(const double* x, const double* y) {  // 16-byte aligned
+  const double2* a = reinterpret_cast<const double2*>(x);
+  const double2* b = reinterpret_cast<const double2*>(y);
+  double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int ii = 0; ii < 8; ++ii)
-#pragma unroll
-          for (int jj = 0; jj <= ii; ++jj)
-            if (ii == i && jj == j) {
-              a[(o + i) + (o + j) * kLD] = l[ii][jj];
-              w[(o + i) + (o + j) * kLD] = wi[ii][jj];
-            }
-      }
-    }
-    const int rows = kNB - o - 8;
-    if (rows > 0) {
-      // panel: X(i, :) = A(i, o:o+8) W8^T, one thread per row
-      if (tid < rows) {
-        const int i = o + 8 + tid;
-        double x[8], y[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) x[c] = a[i + (o + c) * kLD];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          double sacc = 0.0;
-#pragma unroll
-          for (int q = 0; q <= c; ++q) sacc = fma(x[q], wi[c][q], sacc);
-          y[c] = sacc;
-        }
-#pragma unroll
-        for (int c = 0; c < 8; ++c) a[i + (o + c) * kLD] = y[c];
-      }
-      __syncthreads();
-      // trailing: A(i, j) -= sum_p X(i, p) X(j, p) for o+8 <= j <= i < 64
-      const int cnt = rows * (rows + 1) / 2;
-      for (int e = tid; e < cnt; e += blockDim.x) {
-        // e -> (ii, jj) with jj <= ii, row-major over the lower triangle
-        int ii = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-        while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
-        while (ii * (ii + 1) / 2 > e) --ii;
-        const int jj = e - ii * (ii + 1) / 2;
-        const int i = o + 8 + ii, j = o + 8 + jj;
-        double sacc = 0.0;
-#pragma unroll
-        for (int p2 = 0; p2 < 8; ++p2) sacc = fma(a[i + (o + p2) * kLD], a[j + (o + p2) * kLD], sacc);
-        a[i + j * kLD] -= sacc;
-      }
-    }
-    __syncthreads();
+  for (int k = 0; k < 4; ++k) {
+    const double2 u = a[k], v = b[k];
+    s0 = fma(u.x, v.x, s0);
+    s1 = fma(u.y, v.y, s1);
   }
-  // off-diagonal 8 x 8 blocks of W by block distance d = i - j
-  for (int d = 1; d < 8; ++d) {
-    const int nblk = 8 - d;  // blocks (j + d, j)
-    for (int e = tid; e < nblk * 64; e += blockDim.x) {
-      const int jb = e >> 6, r = (e >> 3) & 7, c = e & 7;
-      const int ib = jb + d;
-      double sacc = 0.0;
-      for (int kb2 = jb; kb2 < ib; ++kb2)
+  return s0 + s1;
+}
+
+// x (registers) . y[0:8] (shared, 16-byte aligned)
+__device__ __forceinline__ double dot8r(const double (&x)[8], const double* y) {
+  const double2* b = reinterpret_cast<const double2*>(y);
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double2 v = b[k];
+    s0 = fma(x[2 * k], v.x, s0);
+    s1 = fma(x[2 * k + 1], v.y, s1);
+  }
+  return s0 + s1;
+}
+
+// Factor the 64 x 64 block a (LD kLD; lower, zero upper part, identity padding beyond b)
+// in place and build W = L^{-1} in w (LD kLD, lower). Right-looking over eight 8-wide
+// column blocks with one block of lookahead:
+//   warp 0 (pivot warp)  P1 factor the 8 x 8 diagonal block kb and its inverse W8 in
+//                        registers (the pivot chain), then, once the workers have finished
+//                        step kb-1, P3 the panel rows X of block kb+1 (W8 from registers)
+//                        and P4 the update of diagonal block kb+1, so P1(kb+1) starts
+//                        without waiting for the rest of step kb;
+//   warps 1-3, 5-7       W2 the W rows of block kb, W(o+i, :o) = -W8(i,:) B(o:o+8, :o)
+//   (workers)            (B = sum L W accumulates in w), the panel rows X below block kb+1,
+//                        then S3: A(r, c) -= X(r,:) X(c,:)' below block kb+1, L(r, o:o+8) =
+//                        X(r,:), B(r, c) += X(r,:) W(o:o+8, c);
+//   warp 4               parked, so the pivot warp owns its scheduler's instruction cache.
+// X and the W rows are kept 8-contiguous (16-byte vector loads, broadcast across a warp).
+// Named barriers: 1 = step published (pivot -> workers), 3 = workers done with a step
+// (workers -> pivot), 4 = worker-only. The loops stay rolled: a fully unrolled body
+// overflows the instruction cache. Returns the first failing pivot (uniform) or -1.
+__device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, double* __restrict__ sc, int b) {
+  constexpr int kW = 192;  // worker threads
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* xs = sc;          // 2 x [64 x 8]: X(r, p) at xs[buf][r * 8 + p]
+  double* ws = xs + 1024;   // [64 x 8]: W(o + p, c) at ws[c * 8 + p] for the current block
+  double* l8s = ws + 512;   // 2 x [8 x 8] factor (row-major)
+  double* w8s = l8s + 128;  // 2 x [8 x 8] inverse
+  volatile int* fls = reinterpret_cast<volatile int*>(w8s + 128);
+  for (int e = tid; e < kNB * kLD; e += kDfThreads) w[e] = 0.0;
+  l8s[tid] = 0.0;  // l8s and w8s (256 doubles): strictly upper parts stay zero
+  if (tid == 0) *fls = -1;
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll 1
+    for (int kb = 0; kb < 8; ++kb) {
+      const int o = 8 * kb, buf = kb & 1;
+      TRACE(10 + 4 * kb);
+      const int bv = b - o < 0 ? 0 : (b - o > 8 ? 8 : b - o);
+      double l[8][8], wi[8][8];
+      bool odd;
+      int fail = factor8<false>(a, o, bv, l, wi, &odd);
+      if (odd) fail = factor8<true>(a, o, bv, l, wi, &odd);
+      double* l8 = l8s + 64 * buf;
+      double* w8 = w8s + 64 * buf;
+      if (lane == 0) {  // straight-line stores (a lane-indexed store compiles to a jump table)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j <= i; ++j) {
+            l8[i * 8 + j] = l[i][j];
+            w8[i * 8 + j] = wi[i][j];
+          }
+        if (fail >= 0) *fls = o + fail;
+      }
+      TRACE(11 + 4 * kb);
+      if (kb < 7) {
+        bar_sync_n(3, 224);  // workers are done with step kb-1
+#ifdef CMPC_TRACE
+        if (*fls > 1000) break;  // never: a shared read that waits for the barrier (trace)
+#endif
+        TRACE(12 + 4 * kb);
+        if (fail < 0) {
+          double* x = xs + 512 * buf;
+          // P3: X rows of block kb+1, lane i < 8 takes row o+8+i: X(r, p) = sum_{q<=p} A(r, o+q) W8(p, q)
+          if (lane < 8) {
+            const int r = o + 8 + lane;
+            double ar[8], xr[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ar[q] = a[r + (o + q) * kLD];
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+              double s = 0.0;
+#pragma unroll
+              for (int q = 0; q <= p; ++q) s = fma(ar[q], wi[p][q], s);
+              xr[p] = s;
+            }
+            double2* xv = reinterpret_cast<double2*>(x + r * 8);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) xv[k] = make_double2(xr[2 * k], xr[2 * k + 1]);
+#pragma unroll
+            for (int p = 0; p < 8; ++p) a[r + (o + p) * kLD] = xr[p];
+          }
+          __syncwarp();
+          // P4: diagonal block kb+1 -= X X' (36 lower entries)
+          for (int e = lane; e < 36; e += 32) {
+            int i = 0;
+            while ((i + 1) * (i + 2) / 2 <= e) ++i;
+            const int j = e - i * (i + 1) / 2;
+            const int ri = o + 8 + i, rj = o + 8 + j;
+            a[ri + rj * kLD] -= dot8(x + ri * 8, x + rj * 8);
+          }
+          __syncwarp();
+        }
+      }
+      TRACE(13 + 4 * kb);
+      bar_arrive_n(1, 224);  // step kb published
+      if (fail >= 0) break;
+    }
+  } else if (warp != 4) {
+    const int wt = (warp < 4 ? warp - 1 : warp - 2) * 32 + lane;  // 0..191
+    bar_arrive_n(3, 224);
+#pragma unroll 1
+    for (int kb = 0; kb < 8; ++kb) {
+      const int o = 8 * kb, buf = kb & 1;
+      bar_sync_n(1, 224);
+      if (*fls >= 0) break;
+      TRACEW(100 + 4 * kb);
+      const double* l8 = l8s + 64 * buf;
+      const double* w8 = w8s + 64 * buf;
+      double* x = xs + 512 * buf;
+      // W2: W rows of block kb into ws (the B rows they read stay in w until S3)
+      for (int e = wt; e < 8 * o; e += kW) {
+        const int i = e & 7, c = e >> 3;
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int p = 0; p < 8; p += 2) {
+          s0 = fma(w8[i * 8 + p], w[(o + p) + c * kLD], s0);
+          s1 = fma(w8[i * 8 + p + 1], w[(o + p + 1) + c * kLD], s1);
+        }
+        ws[c * 8 + i] = -(s0 + s1);
+      }
+      if (wt < 64) {
+        const int i = wt >> 3, j = wt & 7;
+        ws[(o + j) * 8 + i] = w8[i * 8 + j];
+        a[(o + i) + (o + j) * kLD] = l8[i * 8 + j];
+      }
+      // panel rows X below block kb+1
+      const int nx = kNB - 16 - o;
+      for (int e = wt; e < 8 * (nx > 0 ? nx : 0); e += kW) {
+        const int r = o + 16 + (e >> 3), p = e & 7;
+        double s = 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          sacc = fma(a[(8 * ib + r) + (8 * kb2 + q) * kLD], w[(8 * kb2 + q) + (8 * jb + c) * kLD], sacc);
-      tt[e] = sacc;
-    }
-    __syncthreads();
-    for (int e = tid; e < nblk * 64; e += blockDim.x) {
-      const int jb = e >> 6, r = (e >> 3) & 7, c = e & 7;
-      const int ib = jb + d;
-      double sacc = 0.0;
+          if (q <= p) s = fma(a[r + (o + q) * kLD], w8[p * 8 + q], s);
+        x[r * 8 + p] = s;
+      }
+      TRACEW(101 + 4 * kb);
+      bar_sync_n(4, kW);
+#ifdef CMPC_TRACE
+      if (*fls > 1000) break;  // never: waits for the barrier (trace)
+#endif
+      TRACEW(102 + 4 * kb);
+      // S3 over rows o..63: thread (row, g) takes columns c = g (mod ng)
+      const int nr = kNB - o, ng = kW / nr;
+      if (wt < ng * nr) {
+        const int r = o + wt % nr, g = wt / nr;
+        if (r < o + 8) {
+          for (int c = g; c < o + 8; c += ng) w[r + c * kLD] = ws[c * 8 + (r - o)];
+        } else {
+          double xr[8];
+          {
+            const double2* xv = reinterpret_cast<const double2*>(x + r * 8);
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q <= r) sacc = fma(w[(8 * ib + r) + (8 * ib + q) * kLD], tt[(jb << 6) | (q << 3) | c], sacc);
-      w[(8 * ib + r) + (8 * jb + c) * kLD] = -sacc;
+            for (int k = 0; k < 4; ++k) {
+              const double2 t = xv[k];
+              xr[2 * k] = t.x;
+              xr[2 * k + 1] = t.y;
+            }
+          }
+          // B update, columns c < o + 8; trailing update, columns o + 8 .. r. Four
+          // independent columns per iteration: one column is a latency-bound chain.
+          int c = g;
+          for (; c + 3 * ng < o + 8; c += 4 * ng) {
+            const double s0 = dot8r(xr, ws + c * 8), s1 = dot8r(xr, ws + (c + ng) * 8);
+            const double s2 = dot8r(xr, ws + (c + 2 * ng) * 8), s3 = dot8r(xr, ws + (c + 3 * ng) * 8);
+            w[r + c * kLD] += s0;
+            w[r + (c + ng) * kLD] += s1;
+            w[r + (c + 2 * ng) * kLD] += s2;
+            w[r + (c + 3 * ng) * kLD] += s3;
+          }
+          for (; c < o + 8; c += ng) w[r + c * kLD] += dot8r(xr, ws + c * 8);
+          if (r >= o + 16) {
+            for (c = o + g; c < o + 8; c += ng) a[r + c * kLD] = x[r * 8 + (c - o)];
+            for (c = o + 8 + g; c + 3 * ng <= r; c += 4 * ng) {
+              const double s0 = dot8r(xr, x + c * 8), s1 = dot8r(xr, x + (c + ng) * 8);
+              const double s2 = dot8r(xr, x + (c + 2 * ng) * 8), s3 = dot8r(xr, x + (c + 3 * ng) * 8);
+              a[r + c * kLD] -= s0;
+              a[r + (c + ng) * kLD] -= s1;
+              a[r + (c + 2 * ng) * kLD] -= s2;
+              a[r + (c + 3 * ng) * kLD] -= s3;
+            }
+            for (; c <= r; c += ng) a[r + c * kLD] -= dot8r(xr, x + c * 8);
+          }
+        }
+      }
+      TRACEW(103 + 4 * kb);
+      if (kb < 6) bar_arrive_n(3, 224);
     }
-    __syncthreads();
   }
-  store_diag(L, n, k0, b, a, w, Wout, true);
+  __syncthreads();
+  return *fls;
 }
 
 // inverse of every 64 x 64 diagonal block of an existing factor (one CTA per block)
@@ -289,125 +431,269 @@ __global__ void __launch_bounds__(256) k_diag_inv(const double* __restrict__ L, 
   store_diag(nullptr, n, k0, b, a, w, Winv + (size_t)blockIdx.x * kNB * kNB, false);
 }
 
-// acc(i, j) += sum_k X[i][k] Y[j][k] for 64x64 smem tiles stored x[k*kGemmLD + i];
-// 4 warps, 32 x 32 per warp, DMMA m16n8k4
-__device__ __forceinline__ void tile_xyt(const double* x, const double* y, int kmax,
-                                         double (&acc)[2][4][4]) {
+constexpr int kTB = kNB * kGemmLD;    // doubles per staged 64 x 64 tile
+constexpr int kDfSmem = 4 * kTB * 8;  // two stages of (X, Y); the potf2 scratch aliases stage 0
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// stage a packed 64 x 64 tile (column-major, 64 contiguous doubles per column) into
+// x[k * kGemmLD + i] with 16-byte cp.async (L2 only: tiles written by other CTAs)
+__device__ __forceinline__ void stage_tile(double* x, const double* src) {
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int ch = threadIdx.x + kDfThreads * u;
+    const int k = ch >> 5, i2 = (ch & 31) * 2;
+    cp_async16(x + k * kGemmLD + i2, src + k * kNB + i2);
+  }
+}
+
+// acc += X Y^T (k = 0..63) for this warp's 32 x 16 block; 8 warps cover the 64 x 64 tile.
+// acc[mi][ni][e] holds element (32 wm + 16 mi + g + 8 (e >> 1), 16 wn + 8 ni + 2 t + (e & 1)).
+__device__ __forceinline__ void gemm_xyt(const double* x, const double* y, double (&acc)[2][2][4]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
-  for (int ks = 0; ks < kmax; ks += 4) {
-    double af[2][2], bf[4];
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-      const int r = 32 * wm + 16 * mi + g;
-      af[mi][0] = x[(ks + t) * kGemmLD + r];
-      af[mi][1] = x[(ks + t) * kGemmLD + r + 8];
-    }
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) bf[ni] = y[(ks + t) * kGemmLD + 32 * wn + 8 * ni + g];
+  const double* xa = x + t * kGemmLD + 32 * (warp & 1) + g;
+  const double* yb = y + t * kGemmLD + 16 * (warp >> 1) + g;
+#pragma unroll 4
+  for (int ks = 0; ks < kNB; ks += 4) {
+    const int o = ks * kGemmLD;
+    double af[2][2], bf[2];
+    af[0][0] = xa[o];
+    af[0][1] = xa[o + 8];
+    af[1][0] = xa[o + 16];
+    af[1][1] = xa[o + 24];
+    bf[0] = yb[o];
+    bf[1] = yb[o + 8];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) dmma1684(acc[mi][ni], af[mi], bf[ni]);
+      for (int ni = 0; ni < 2; ++ni) dmma1684(acc[mi][ni], af[mi], bf[ni]);
   }
 }
 
-// L_ik = A_ik W^T for the 64-row block i below the diagonal block
-__global__ void __launch_bounds__(128) k_panel(double* __restrict__ L, int64_t n, int64_t k0, int b,
-                                               long long* info, const double* __restrict__ W) {
-  extern __shared__ double sm[];
-  double* xa = sm;                  // A_ik: xa[k*LD + i]
-  double* xw = sm + kNB * kGemmLD;  // W:    xw[k*LD + j] = W[j][k]
-  if (*info != 0) return;
-  const int64_t r0 = k0 + b + (int64_t)blockIdx.x * kNB;
-  {
-    double ra[32], rw[32];
-#pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int e = threadIdx.x + u * 128, i = e & 63, k = e >> 6;
-      ra[u] = (k < b && r0 + i < n) ? L[(r0 + i) + (k0 + k) * n] : 0.0;
-      rw[u] = W[i + k * kNB];  // W col-major: W[i][k] at i + k*64
-    }
-#pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int e = threadIdx.x + u * 128, i = e & 63, k = e >> 6;
-      xa[k * kGemmLD + i] = ra[u];
-      xw[k * kGemmLD + i] = rw[u];
-    }
+struct DfArgs {
+  const double* M;  // n x n, lower part read
+  double* L;        // n x n column-major factor (lower tiles and diagonal tiles written)
+  double* Lt;       // nt x nt packed 64 x 64 tiles of L (off-diagonal tiles), read by other CTAs
+  double* W;        // nt packed 64 x 64 inverses of the diagonal tiles
+  int64_t n;
+  double delta;
+  int nt, ntiles;
+  unsigned* flags;  // nt x nt per-tile done flags (== generation when done)
+  unsigned* ctl;    // [0] generation, [1] exit count, [2] failure generation, [3] pivot + 1, [4] tile counter
+  long long* info;
+};
+
+// thread 0: spin until both tile flags carry the generation; false on a published failure
+__device__ __forceinline__ bool wait_flags(const unsigned* f1, const unsigned* f2, const unsigned* fail,
+                                           unsigned target) {
+  while (true) {
+    if (ld_acquire(f1) == target && ld_acquire(f2) == target) return true;
+    if (ld_acquire(fail) == target) return false;
   }
-  __syncthreads();
-  double acc[2][4][4] = {};
-  tile_xyt(xa, xw, b, acc);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t r = r0 + 32 * wm + 16 * mi + g + 8 * (e >> 1);
-        const int c = 32 * wn + 8 * ni + 2 * t + (e & 1);
-        if (r < n && c < b) L[r + (k0 + c) * n] = acc[mi][ni][e];
-      }
 }
 
-// trailing update A22(I,J) -= L_Ik L_Jk^T, lower tiles only
-__global__ void __launch_bounds__(128) k_trail(double* __restrict__ L, int64_t n, int64_t k0, int b,
-                                               long long* info) {
-  extern __shared__ double sm[];
-  double* xi = sm;
-  double* xj = sm + kNB * kGemmLD;
-  if (*info != 0) return;
-  // blockIdx.x enumerates the lower tiles (ti >= tj) of the trailing matrix
-  int ti = (int)((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);
-  while ((ti + 1) * (ti + 2) / 2 <= (int)blockIdx.x) ++ti;
-  while (ti * (ti + 1) / 2 > (int)blockIdx.x) --ti;
-  const int tj = (int)blockIdx.x - ti * (ti + 1) / 2;
-  const int64_t base = k0 + b;
-  const int64_t i0 = base + (int64_t)ti * kNB, j0 = base + (int64_t)tj * kNB;
-  {
-    double ra[32], rb[32];
+// one lower tile (i, j): left-looking updates, then potf2 + inverse (i == j) or the panel
+// product with W_j (i > j). Returns false when the factorization failed somewhere.
+__device__ bool df_tile(const DfArgs& A, int i, int j, unsigned target, double* sm, volatile unsigned* s_flag) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int nt = A.nt;
+  const int64_t n = A.n, r0 = (int64_t)kNB * i, c0 = (int64_t)kNB * j;
+  const bool diag = i == j;
+  const bool idle = diag && wm == 0 && wn >= 2;  // strictly upper 32 x 16 blocks of a diagonal tile
+  const unsigned* fl = A.flags;
+  const unsigned* failw = A.ctl + 2;
+
+  // acc = -(M_ij) (+ -delta on the diagonal), so the updates accumulate with DMMA's "+"
+  double acc[2][2][4];
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int e = threadIdx.x + u * 128, i = e & 63, k = e >> 6;
-      ra[u] = (k < b && i0 + i < n) ? L[(i0 + i) + (k0 + k) * n] : 0.0;
-      rb[u] = (k < b && j0 + i < n) ? L[(j0 + i) + (k0 + k) * n] : 0.0;
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = 32 * wm + 16 * mi + g + 8 * (e >> 1), cl = 16 * wn + 8 * ni + 2 * t + (e & 1);
+        double v = 0.0;
+        if (r0 + r < n && c0 + cl < n && (!diag || r >= cl)) {
+          v = A.M[(r0 + r) + (c0 + cl) * n];
+          if (diag && r == cl && A.delta != 0.0) v = add(v, A.delta);
+        }
+        acc[mi][ni][e] = -v;
+      }
+
+  // A_ij -= sum_k L_ik L_jk^T, double-buffered: tile k+1 is prefetched when already published
+  if (j > 0) {
+    if (tid == 0) *s_flag = wait_flags(fl + i * nt, fl + j * nt, failw, target) ? 1u : 2u;
+    __syncthreads();
+    if (*s_flag == 2u) return false;
+    stage_tile(sm, A.Lt + ((size_t)i * nt) * (kNB * kNB));
+    if (!diag) stage_tile(sm + kTB, A.Lt + ((size_t)j * nt) * (kNB * kNB));
+    cp_commit();
+    for (int k = 0; k < j; ++k) {
+      const int s = k & 1;
+      double* xs = sm + 2 * s * kTB;
+      double* xo = sm + 2 * (s ^ 1) * kTB;
+      const bool more = k + 1 < j;
+      if (tid == 0)
+        *s_flag = (more && ld_acquire(fl + i * nt + k + 1) == target && ld_acquire(fl + j * nt + k + 1) == target)
+                      ? 1u : 0u;
+      __syncthreads();  // buffer s^1 is free (gemm k-1 done); s_flag visible
+      const bool pre = *s_flag == 1u;
+      if (pre) {
+        stage_tile(xo, A.Lt + ((size_t)i * nt + k + 1) * (kNB * kNB));
+        if (!diag) stage_tile(xo + kTB, A.Lt + ((size_t)j * nt + k + 1) * (kNB * kNB));
+      }
+      cp_commit();
+      cp_wait1();
+      __syncthreads();  // tile k visible to every warp
+      if (!idle) gemm_xyt(xs, diag ? xs : xs + kTB, acc);
+      if (more && !pre) {
+        if (tid == 0) *s_flag = wait_flags(fl + i * nt + k + 1, fl + j * nt + k + 1, failw, target) ? 1u : 2u;
+        __syncthreads();
+        if (*s_flag == 2u) return false;
+        stage_tile(xo, A.Lt + ((size_t)i * nt + k + 1) * (kNB * kNB));
+        if (!diag) stage_tile(xo + kTB, A.Lt + ((size_t)j * nt + k + 1) * (kNB * kNB));
+        cp_commit();
+      }
     }
+  }
+  __syncthreads();  // staging buffers free
+
+  if (diag) {
+    double* a = sm;
+    const int b = (int)(n - c0 < kNB ? n - c0 : kNB);
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int e = threadIdx.x + u * 128, i = e & 63, k = e >> 6;
-      xi[k * kGemmLD + i] = ra[u];
-      xj[k * kGemmLD + i] = rb[u];
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = 32 * wm + 16 * mi + g + 8 * (e >> 1), cl = 16 * wn + 8 * ni + 2 * t + (e & 1);
+          double v;
+          if (r >= b || cl >= b) v = (r == cl) ? 1.0 : 0.0;
+          else v = (r >= cl) ? -acc[mi][ni][e] : 0.0;
+          a[r + cl * kLD] = v;
+        }
+    __syncthreads();
+    TRACE(2);
+    double* w = sm + kNB * kLD;
+    const int f = diag_factor(a, w, w + kNB * kLD, b);
+    if (f >= 0) {
+      if (tid == 0) {
+        A.ctl[3] = (unsigned)(c0 + f + 1);
+        __threadfence();
+        st_release(A.ctl + 2, target);
+      }
+      return false;
+    }
+    double* Wj = A.W + (size_t)j * (kNB * kNB);
+    for (int e = tid; e < kNB * kNB; e += kDfThreads) {
+      const int r = e & 63, cl = e >> 6;
+      if (r < b && cl < b) A.L[(c0 + r) + (c0 + cl) * n] = (r >= cl) ? a[r + cl * kLD] : 0.0;
+      Wj[e] = (r >= cl) ? w[r + cl * kLD] : 0.0;
+    }
+  } else {
+    double* x = sm;
+    double* y = sm + kTB;
+    if (tid == 0) *s_flag = wait_flags(fl + j * nt + j, fl + j * nt + j, failw, target) ? 1u : 2u;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = 32 * wm + 16 * mi + g + 8 * (e >> 1), cl = 16 * wn + 8 * ni + 2 * t + (e & 1);
+          x[cl * kGemmLD + r] = -acc[mi][ni][e];
+        }
+    __syncthreads();
+    if (*s_flag == 2u) return false;
+    stage_tile(y, A.W + (size_t)j * (kNB * kNB));
+    cp_commit();
+    cp_wait0();
+    __syncthreads();
+    double out[2][2][4];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) out[mi][ni][e] = 0.0;
+    gemm_xyt(x, y, out);  // L_ij = A_ij W_j^T
+    __syncthreads();
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = 32 * wm + 16 * mi + g + 8 * (e >> 1), cl = 16 * wn + 8 * ni + 2 * t + (e & 1);
+          x[cl * kGemmLD + r] = out[mi][ni][e];
+        }
+    __syncthreads();
+    double* Lt = A.Lt + ((size_t)i * nt + j) * (kNB * kNB);
+    for (int e = tid; e < kNB * kNB; e += kDfThreads) {
+      const int r = e & 63, cl = e >> 6;
+      const double v = x[cl * kGemmLD + r];
+      Lt[e] = v;
+      if (r0 + r < n) A.L[(r0 + r) + (c0 + cl) * n] = v;
     }
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
-  // prefetch the tile being updated (all loads in flight before the MMA loop)
-  double old[2][4][4];
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t r = i0 + 32 * wm + 16 * mi + g + 8 * (e >> 1);
-        const int64_t c = j0 + 32 * wn + 8 * ni + 2 * t + (e & 1);
-        old[mi][ni][e] = (r < n && c < n && r >= c) ? L[r + c * n] : 0.0;
-      }
-  double acc[2][4][4] = {};
-  tile_xyt(xi, xj, b, acc);
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t r = i0 + 32 * wm + 16 * mi + g + 8 * (e >> 1);
-        const int64_t c = j0 + 32 * wn + 8 * ni + 2 * t + (e & 1);
-        if (r < n && c < n && r >= c) L[r + c * n] = old[mi][ni][e] - acc[mi][ni][e];
-      }
+  if (tid == 0) {
+    __threadfence();
+    st_release(A.flags + i * nt + j, target);
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(kDfThreads, 1) k_chol_df(const DfArgs A) {
+  extern __shared__ __align__(16) double sm_df[];
+  __shared__ unsigned s_target, s_q, s_flag;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_target = *reinterpret_cast<volatile unsigned*>(A.ctl) + 1u;
+  __syncthreads();
+  const unsigned target = s_target;
+  TRACE(0);
+  while (true) {
+    if (tid == 0) s_q = atomicAdd(A.ctl + 4, 1u);
+    __syncthreads();
+    const int q = (int)s_q;
+    if (q >= A.ntiles) break;
+    int j = 0, rem = q;  // column-major enumeration of the lower tiles
+    while (rem >= A.nt - j) {
+      rem -= A.nt - j;
+      ++j;
+    }
+    if (!df_tile(A, j + rem, j, target, sm_df, &s_flag)) break;
+  }
+  TRACE(3);
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(A.ctl + 1, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      const bool failed = ld_acquire(A.ctl + 2) == target;
+      *A.info = failed ? (long long)*reinterpret_cast<volatile unsigned*>(A.ctl + 3) : 0;
+      A.ctl[1] = 0;
+      A.ctl[4] = 0;
+      __threadfence();
+      st_release(A.ctl, target);
+    }
+  }
 }
 
 // x = L^{-T} L^{-1} b with the 64 x 64 diagonal-block inverses W; one CTA of 512
@@ -488,10 +774,8 @@ __global__ void __launch_bounds__(512) k_trsv(const double* __restrict__ L,
 void set_attrs() {
   static bool done = false;
   if (done) return;
-  CMPC_CUDA(cudaFuncSetAttribute(k_potf2_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotfSmem));
+  CMPC_CUDA(cudaFuncSetAttribute(k_chol_df, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
   CMPC_CUDA(cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotfSmem));
-  CMPC_CUDA(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
-  CMPC_CUDA(cudaFuncSetAttribute(k_trail, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
   CMPC_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   done = true;
 }
@@ -501,11 +785,18 @@ void set_attrs() {
 void chol_alloc(Ctx& c) {
   const int64_t nb = ceil_div(std::max<int64_t>(c.n, 1), kNB);
   c.Winv = dev_zeros<double>((size_t)nb * kNB * kNB, c.stream);
+  c.Lt = dev_zeros<double>((size_t)nb * nb * kNB * kNB, c.stream);
+  c.df_flags = dev_zeros<unsigned>((size_t)nb * nb, c.stream);
+  c.df_ctl = dev_zeros<unsigned>(8, c.stream);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+  c.df_grid = sms;
 }
 
 void chol_free(Ctx& c) {
-  dev_free(c.Winv, c.stream);
-  c.Winv = nullptr;
+  for (void* p : {(void*)c.Winv, (void*)c.Lt, (void*)c.df_flags, (void*)c.df_ctl}) dev_free(p, c.stream);
+  c.Winv = c.Lt = nullptr;
+  c.df_flags = c.df_ctl = nullptr;
 }
 
 void launch_cholesky(Ctx& c, const double* M, double* L, double delta) {
@@ -516,23 +807,22 @@ void launch_cholesky(Ctx& c, const double* M, double* L, double delta) {
     return;
   }
   set_attrs();
-  dim3 g0((unsigned)ceil_div(n, 256), (unsigned)n);
-  k_chol_copy<<<g0, 256, 0, c.stream>>>(M, L, n, delta, info);
+  const int nt = (int)ceil_div(n, kNB);
+  DfArgs a;
+  a.M = M;
+  a.L = L;
+  a.Lt = c.Lt;
+  a.W = c.Winv;
+  a.n = n;
+  a.delta = delta;
+  a.nt = nt;
+  a.ntiles = nt * (nt + 1) / 2;
+  a.flags = c.df_flags;
+  a.ctl = c.df_ctl;
+  a.info = info;
+  const int grid = std::min(a.ntiles, c.df_grid);
+  k_chol_df<<<grid, kDfThreads, kDfSmem, c.stream>>>(a);
   CMPC_LAUNCHED();
-  for (int64_t k0 = 0; k0 < n; k0 += kNB) {
-    const int b = (int)std::min<int64_t>(kNB, n - k0);
-    double* Wk = c.Winv + (k0 / kNB) * kNB * kNB;
-    k_potf2_inv<<<1, 256, kPotfSmem, c.stream>>>(L, n, k0, b, info, Wk);
-    CMPC_LAUNCHED();
-    const int64_t rest = n - k0 - b;
-    if (rest > 0) {
-      const unsigned nb = (unsigned)ceil_div(rest, kNB);
-      k_panel<<<nb, 128, kGemmSmem, c.stream>>>(L, n, k0, b, info, Wk);
-      CMPC_LAUNCHED();
-      k_trail<<<nb * (nb + 1) / 2, 128, kGemmSmem, c.stream>>>(L, n, k0, b, info);
-      CMPC_LAUNCHED();
-    }
-  }
 }
 
 void launch_factor_inverses(Ctx& c, const double* L) {

@@ -99,6 +99,10 @@ struct Ctx {
   long long g_step_nodes = 0, g_next_nodes = 0;
   double g_tau = 0.0;
   double* Winv = nullptr;    // inverses of the 64 x 64 diagonal blocks of L
+  double* Lt = nullptr;      // packed 64 x 64 off-diagonal tiles of L (dataflow Cholesky)
+  unsigned* df_flags = nullptr;  // per-tile done flags (generation stamped)
+  unsigned* df_ctl = nullptr;    // generation, exit count, failure, pivot, tile counter
+  int df_grid = 148;
   Packet* pk = nullptr;      // device packet
   Packet* pk_host = nullptr; // pinned mirror
   double mu = 0.0;

@@ -569,7 +569,7 @@ void vec_free(Ctx& c) {
                   (void*)c.omega, (void*)c.q, (void*)c.dsing, (void*)c.rhs, (void*)c.M,
                   (void*)c.L, (void*)c.pv, (void*)c.ps_, (void*)c.pl, (void*)c.pzd, (void*)c.Jpv,
                   (void*)c.vt, (void*)c.yt, (void*)c.Hvt, (void*)c.part, (void*)c.colpart,
-                  (void*)c.hmax, (void*)c.pk, (void*)c.d_mu})
+                  (void*)c.hmax, (void*)c.pk, (void*)c.d_mu, (void*)c.d_alpha})
     dev_free(p, c.stream);
   if (c.pk_host) cudaFreeHost(c.pk_host);
   chol_free(c);

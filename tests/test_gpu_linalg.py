@@ -56,7 +56,7 @@ def test_cholesky_factorize_rejects_asymmetric_input():  # :72-78
         linalg.cholesky_factorize(be, np.zeros((2, 3)))
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 17, 40, 63, 64, 65, 127, 150, 200, 500, 1000])
+@pytest.mark.parametrize("n", [1, 2, 5, 17, 40, 63, 64, 65, 127, 150, 200, 333, 500, 1000, 2000])
 def test_factor_reconstructs_and_solves(n):  # :80-116, :118-132
     rng = np.random.default_rng(n)
     M = spd(rng, n, 1.0)

@@ -9,4 +9,4 @@ qp = P.DenseQp(H=G.T @ G + n * np.eye(n), h=np.zeros(n), h0=0.0, J=np.zeros((0, 
 dq = ipm.device_qp(qp)
 ipm.assemble_condensed(qp, np.zeros(0))
 for ph in ["cholesky", "chol_solve"]:
-    print(ph, dq.time_phase(ph, 20) * 1e3, "us")
+    print(n, ph, dq.time_phase(ph, 20) * 1e3, "us")
