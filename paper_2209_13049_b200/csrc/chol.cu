@@ -201,31 +201,7 @@ __device__ __forceinline__ int factor8(const double* a, int o, int bv, double (&
   return fail;
 }
 
-__device__ __forceinline__ double dot8(const double* x, const double* y) {  // 16-byte aligned
-  const double2* a = reinterpret_cast<const double2*>(x);
-  const double2* b = reinterpret_cast<const double2*>(y);
-  double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const double2 u = a[k], v = b[k];
-    s0 = fma(u.x, v.x, s0);
-    s1 = fma(u.y, v.y, s1);
-  }
-  return s0 + s1;
-}
 
-// x (registers) . y[0:8] (shared, 16-byte aligned)
-__device__ __forceinline__ double dot8r(const double (&x)[8], const double* y) {
-  const double2* b = reinterpret_cast<const double2*>(y);
-  double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const double2 v = b[k];
-    s0 = fma(x[2 * k], v.x, s0);
-    s1 = fma(x[2 * k + 1], v.y, s1);
-  }
-  return s0 + s1;
-}
 
 // Factor the 64 x 64 block a (LD kLD; lower, zero upper part, identity padding beyond b)
 // in place and build W = L^{-1} in w (LD kLD, lower). Right-looking over eight 8-wide
@@ -235,22 +211,25 @@ __device__ __forceinline__ double dot8r(const double (&x)[8], const double* y) {
 //                        step kb-1, P3 the panel rows X of block kb+1 (W8 from registers)
 //                        and P4 the update of diagonal block kb+1, so P1(kb+1) starts
 //                        without waiting for the rest of step kb;
-//   warps 1-3, 5-7       W2 the W rows of block kb, W(o+i, :o) = -W8(i,:) B(o:o+8, :o)
-//   (workers)            (B = sum L W accumulates in w), the panel rows X below block kb+1,
-//                        then S3: A(r, c) -= X(r,:) X(c,:)' below block kb+1, L(r, o:o+8) =
-//                        X(r,:), B(r, c) += X(r,:) W(o:o+8, c);
+//   warps 1-3, 5-7       every other product of the step, as DMMA m16n8k4 fragments
+//   (workers)            (K = 8) spread warp-uniformly over the six warps: W2 the W rows of
+//                        block kb, W(o+i, :o) = -W8(i,:) B(o:o+8, :o) (B = sum L W
+//                        accumulates in w), the panel rows X(r,:) = A(r, o:o+8) W8' below
+//                        block kb+1, then S3 A(r, c) -= X(r,:) X(c,:)' below block kb+1 and
+//                        B(r, c) += X(r,:) W(o:o+8, c);
 //   warp 4               parked, so the pivot warp owns its scheduler's instruction cache.
-// X and the W rows are kept 8-contiguous (16-byte vector loads, broadcast across a warp).
+// X and the block's W rows are stored p-major with stride kXLD (conflict-free fragments).
 // Named barriers: 1 = step published (pivot -> workers), 3 = workers done with a step
 // (workers -> pivot), 4 = worker-only. The loops stay rolled: a fully unrolled body
 // overflows the instruction cache. Returns the first failing pivot (uniform) or -1.
+constexpr int kXLD = 68;
 __device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, double* __restrict__ sc, int b) {
-  constexpr int kW = 192;  // worker threads
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* xs = sc;          // 2 x [64 x 8]: X(r, p) at xs[buf][r * 8 + p]
-  double* ws = xs + 1024;   // [64 x 8]: W(o + p, c) at ws[c * 8 + p] for the current block
-  double* l8s = ws + 512;   // 2 x [8 x 8] factor (row-major)
-  double* w8s = l8s + 128;  // 2 x [8 x 8] inverse
+  constexpr int kW = 192, kWarps = 6;  // worker threads / warps
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  double* xs = sc;                  // 2 x [8 x kXLD]: X(r, p) at xs[buf][p * kXLD + r]
+  double* wsb = xs + 2 * 8 * kXLD;  // [8 x kXLD]: W(o + p, c) at wsb[p * kXLD + c]
+  double* l8s = wsb + 8 * kXLD;     // 2 x [8 x 8] factor (row-major)
+  double* w8s = l8s + 128;          // 2 x [8 x 8] inverse
   volatile int* fls = reinterpret_cast<volatile int*>(w8s + 128);
   for (int e = tid; e < kNB * kLD; e += kDfThreads) w[e] = 0.0;
   l8s[tid] = 0.0;  // l8s and w8s (256 doubles): strictly upper parts stay zero
@@ -286,11 +265,11 @@ __device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, doubl
 #endif
         TRACE(12 + 4 * kb);
         if (fail < 0) {
-          double* x = xs + 512 * buf;
+          double* x = xs + 8 * kXLD * buf;
           // P3: X rows of block kb+1, lane i < 8 takes row o+8+i: X(r, p) = sum_{q<=p} A(r, o+q) W8(p, q)
           if (lane < 8) {
             const int r = o + 8 + lane;
-            double ar[8], xr[8];
+            double ar[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) ar[q] = a[r + (o + q) * kLD];
 #pragma unroll
@@ -298,22 +277,24 @@ __device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, doubl
               double s = 0.0;
 #pragma unroll
               for (int q = 0; q <= p; ++q) s = fma(ar[q], wi[p][q], s);
-              xr[p] = s;
+              x[p * kXLD + r] = s;
+              a[r + (o + p) * kLD] = s;
             }
-            double2* xv = reinterpret_cast<double2*>(x + r * 8);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) xv[k] = make_double2(xr[2 * k], xr[2 * k + 1]);
-#pragma unroll
-            for (int p = 0; p < 8; ++p) a[r + (o + p) * kLD] = xr[p];
           }
           __syncwarp();
-          // P4: diagonal block kb+1 -= X X' (36 lower entries)
-          for (int e = lane; e < 36; e += 32) {
-            int i = 0;
-            while ((i + 1) * (i + 2) / 2 <= e) ++i;
-            const int j = e - i * (i + 1) / 2;
-            const int ri = o + 8 + i, rj = o + 8 + j;
-            a[ri + rj * kLD] -= dot8(x + ri * 8, x + rj * 8);
+          TRACE(60 + kb);
+          // P4: diagonal block kb+1 -= X X', lane (i, j0) takes entries (i, j0) and (i, j0 + 4)
+          {
+            const int ri = o + 8 + g, r0 = o + 8 + t, r1 = r0 + 4;
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+              const double xi = x[p * kXLD + ri];
+              s0 = fma(xi, x[p * kXLD + r0], s0);
+              s1 = fma(xi, x[p * kXLD + r1], s1);
+            }
+            if (t <= g) a[ri + r0 * kLD] -= s0;
+            if (t + 4 <= g) a[ri + r1 * kLD] -= s1;
           }
           __syncwarp();
         }
@@ -323,7 +304,8 @@ __device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, doubl
       if (fail >= 0) break;
     }
   } else if (warp != 4) {
-    const int wt = (warp < 4 ? warp - 1 : warp - 2) * 32 + lane;  // 0..191
+    const int wid = warp < 4 ? warp - 1 : warp - 2;  // 0..5
+    const int wt = wid * 32 + lane;                   // 0..191
     bar_arrive_n(3, 224);
 #pragma unroll 1
     for (int kb = 0; kb < 8; ++kb) {
@@ -333,32 +315,48 @@ __device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, doubl
       TRACEW(100 + 4 * kb);
       const double* l8 = l8s + 64 * buf;
       const double* w8 = w8s + 64 * buf;
-      double* x = xs + 512 * buf;
-      // W2: W rows of block kb into ws (the B rows they read stay in w until S3)
-      for (int e = wt; e < 8 * o; e += kW) {
-        const int i = e & 7, c = e >> 3;
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int p = 0; p < 8; p += 2) {
-          s0 = fma(w8[i * 8 + p], w[(o + p) + c * kLD], s0);
-          s1 = fma(w8[i * 8 + p + 1], w[(o + p + 1) + c * kLD], s1);
-        }
-        ws[c * 8 + i] = -(s0 + s1);
-      }
+      double* x = xs + 8 * kXLD * buf;
+      // the block's L entries and its diagonal W entries
       if (wt < 64) {
         const int i = wt >> 3, j = wt & 7;
-        ws[(o + j) * 8 + i] = w8[i * 8 + j];
+        wsb[i * kXLD + o + j] = w8[i * 8 + j];
         a[(o + i) + (o + j) * kLD] = l8[i * 8 + j];
       }
-      // panel rows X below block kb+1
-      const int nx = kNB - 16 - o;
-      for (int e = wt; e < 8 * (nx > 0 ? nx : 0); e += kW) {
-        const int r = o + 16 + (e >> 3), p = e & 7;
-        double s = 0.0;
+      // W2: D(c, i) = sum_p B(o+p, c) W8(i, p), c < o; W(o+i, c) = -D
+      for (int f = wid; f < (o + 15) / 16; f += kWarps) {
+        const int m0 = 16 * f;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q <= p) s = fma(a[r + (o + q) * kLD], w8[p * 8 + q], s);
-        x[r * 8 + p] = s;
+        for (int k0 = 0; k0 < 8; k0 += 4) {
+          const int p = k0 + t;
+          double af[2];
+          af[0] = m0 + g < o ? w[(o + p) + (m0 + g) * kLD] : 0.0;
+          af[1] = m0 + g + 8 < o ? w[(o + p) + (m0 + g + 8) * kLD] : 0.0;
+          dmma1684(acc, af, w8[g * 8 + p]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = m0 + g + 8 * (e >> 1), i = 2 * t + (e & 1);
+          if (c < o) wsb[i * kXLD + c] = -acc[e];
+        }
+      }
+      // X rows below block kb+1: D(r, p) = sum_q A(r, o+q) W8(p, q), r >= o+16
+      for (int f = wid; f < (kNB - 1 - o) / 16; f += kWarps) {
+        const int m0 = o + 16 + 16 * f;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k0 = 0; k0 < 8; k0 += 4) {
+          const int q = k0 + t;
+          double af[2];
+          af[0] = m0 + g < kNB ? a[(m0 + g) + (o + q) * kLD] : 0.0;
+          af[1] = m0 + g + 8 < kNB ? a[(m0 + g + 8) + (o + q) * kLD] : 0.0;
+          dmma1684(acc, af, w8[g * 8 + q]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = m0 + g + 8 * (e >> 1), p = 2 * t + (e & 1);
+          if (r < kNB) x[p * kXLD + r] = acc[e];
+        }
       }
       TRACEW(101 + 4 * kb);
       bar_sync_n(4, kW);
@@ -366,48 +364,109 @@ __device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, doubl
       if (*fls > 1000) break;  // never: waits for the barrier (trace)
 #endif
       TRACEW(102 + 4 * kb);
-      // S3 over rows o..63: thread (row, g) takes columns c = g (mod ng)
-      const int nr = kNB - o, ng = kW / nr;
-      if (wt < ng * nr) {
-        const int r = o + wt % nr, g = wt / nr;
-        if (r < o + 8) {
-          for (int c = g; c < o + 8; c += ng) w[r + c * kLD] = ws[c * 8 + (r - o)];
-        } else {
-          double xr[8];
-          {
-            const double2* xv = reinterpret_cast<const double2*>(x + r * 8);
+      // S3a: A(r, c) -= X(r,:) X(c,:)' for r >= o+16, o+8 <= c <= r, in 16 x 8 fragments
+      // (row group rg holds min(2 rg + 3, ncg) of them); two fragments in flight per warp
+      {
+        const int nrg = (kNB - 1 - o) / 16, ncg = (kNB - 8 - o) / 8;
+        int total = 0;
+        for (int rg = 0; rg < nrg; ++rg) total += min(2 * rg + 3, ncg);
+        for (int f = wid; f < total; f += 2 * kWarps) {
+          const bool two = f + kWarps < total;
+          int m0[2], n0[2];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const double2 t = xv[k];
-              xr[2 * k] = t.x;
-              xr[2 * k + 1] = t.y;
+          for (int u = 0; u < 2; ++u) {
+            int ff = (u == 0 || !two) ? f : f + kWarps, rg = 0, cnt = min(3, ncg);
+            while (ff >= cnt) {
+              ff -= cnt;
+              ++rg;
+              cnt = min(2 * rg + 3, ncg);
+            }
+            m0[u] = o + 16 + 16 * rg;
+            n0[u] = o + 8 + 8 * ff;
+          }
+          double acc[2][4], af[2][2][2], bf[2][2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              const int r = m0[u] + g + 8 * (e2 >> 1), c = n0[u] + 2 * t + (e2 & 1);
+              acc[u][e2] = (r < kNB && c <= r) ? a[r + c * kLD] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int p = 4 * k + t;
+              af[u][k][0] = m0[u] + g < kNB ? -x[p * kXLD + m0[u] + g] : 0.0;
+              af[u][k][1] = m0[u] + g + 8 < kNB ? -x[p * kXLD + m0[u] + g + 8] : 0.0;
+              bf[u][k] = x[p * kXLD + n0[u] + g];
             }
           }
-          // B update, columns c < o + 8; trailing update, columns o + 8 .. r. Four
-          // independent columns per iteration: one column is a latency-bound chain.
-          int c = g;
-          for (; c + 3 * ng < o + 8; c += 4 * ng) {
-            const double s0 = dot8r(xr, ws + c * 8), s1 = dot8r(xr, ws + (c + ng) * 8);
-            const double s2 = dot8r(xr, ws + (c + 2 * ng) * 8), s3 = dot8r(xr, ws + (c + 3 * ng) * 8);
-            w[r + c * kLD] += s0;
-            w[r + (c + ng) * kLD] += s1;
-            w[r + (c + 2 * ng) * kLD] += s2;
-            w[r + (c + 3 * ng) * kLD] += s3;
-          }
-          for (; c < o + 8; c += ng) w[r + c * kLD] += dot8r(xr, ws + c * 8);
-          if (r >= o + 16) {
-            for (c = o + g; c < o + 8; c += ng) a[r + c * kLD] = x[r * 8 + (c - o)];
-            for (c = o + 8 + g; c + 3 * ng <= r; c += 4 * ng) {
-              const double s0 = dot8r(xr, x + c * 8), s1 = dot8r(xr, x + (c + ng) * 8);
-              const double s2 = dot8r(xr, x + (c + 2 * ng) * 8), s3 = dot8r(xr, x + (c + 3 * ng) * 8);
-              a[r + c * kLD] -= s0;
-              a[r + (c + ng) * kLD] -= s1;
-              a[r + (c + 2 * ng) * kLD] -= s2;
-              a[r + (c + 3 * ng) * kLD] -= s3;
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) dmma1684(acc[u], af[u][k], bf[u][k]);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !two) break;
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              const int r = m0[u] + g + 8 * (e2 >> 1), c = n0[u] + 2 * t + (e2 & 1);
+              if (r < kNB && c <= r) a[r + c * kLD] = acc[u][e2];
             }
-            for (; c <= r; c += ng) a[r + c * kLD] -= dot8r(xr, x + c * 8);
           }
         }
+      }
+      // S3b: B(r, c) += X(r,:) W(o:o+8, c) for r >= o+8, c < o+8; two fragments in flight
+      {
+        const int nrg = (kNB - 8 - o + 15) / 16, ncg = kb + 1, total = nrg * ncg;
+        for (int f = wid; f < total; f += 2 * kWarps) {
+          const bool two = f + kWarps < total;
+          int m0[2], n0[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int ff = (u == 0 || !two) ? f : f + kWarps;
+            const int rg = ff / ncg;
+            m0[u] = o + 8 + 16 * rg;
+            n0[u] = 8 * (ff - rg * ncg);
+          }
+          double acc[2][4], af[2][2][2], bf[2][2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              const int r = m0[u] + g + 8 * (e2 >> 1), c = n0[u] + 2 * t + (e2 & 1);
+              acc[u][e2] = r < kNB ? w[r + c * kLD] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int p = 4 * k + t;
+              af[u][k][0] = m0[u] + g < kNB ? x[p * kXLD + m0[u] + g] : 0.0;
+              af[u][k][1] = m0[u] + g + 8 < kNB ? x[p * kXLD + m0[u] + g + 8] : 0.0;
+              bf[u][k] = wsb[p * kXLD + n0[u] + g];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) dmma1684(acc[u], af[u][k], bf[u][k]);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !two) break;
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              const int r = m0[u] + g + 8 * (e2 >> 1), c = n0[u] + 2 * t + (e2 & 1);
+              if (r < kNB) w[r + c * kLD] = acc[u][e2];
+            }
+          }
+        }
+      }
+      // finished W rows of block kb; the panel L(r, o:o+8) = X below block kb+1
+      for (int e = wt; e < 8 * (o + 8); e += kW) {
+        const int i = e & 7, c = e >> 3;
+        w[(o + i) + c * kLD] = wsb[i * kXLD + c];
+      }
+      for (int e = wt; e < 8 * (kNB - 16 - o); e += kW) {
+        const int r = o + 16 + (e >> 3), p = e & 7;
+        a[r + (o + p) * kLD] = x[p * kXLD + r];
       }
       TRACEW(103 + 4 * kb);
       if (kb < 6) bar_arrive_n(3, 224);

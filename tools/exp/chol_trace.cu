@@ -8,6 +8,23 @@
 
 namespace cmpc {
 thread_local long long g_launches = 0;
+namespace {
+// the diagonal factor alone (one CTA, the first 64 x 64 block of M)
+__global__ void __launch_bounds__(kDfThreads, 1) k_diag_only(const double* M, int64_t n, double* out) {
+  extern __shared__ __align__(16) double sm_do[];
+  double* a = sm_do;
+  double* w = sm_do + kNB * kLD;
+  for (int e = threadIdx.x; e < kNB * kNB; e += kDfThreads) {
+    const int r = e & 63, c = e >> 6;
+    a[r + c * kLD] = (r >= c && r < n && c < n) ? M[r + c * n] : (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  TRACE(0);
+  const int f = diag_factor(a, w, w + kNB * kLD, (int)(n < 64 ? n : 64));
+  TRACE(3);
+  for (int e = threadIdx.x; e < kNB * kNB; e += kDfThreads) out[e] = a[(e & 63) + (e >> 6) * kLD] + f;
+}
+}  // namespace
 }
 
 int main(int argc, char** argv) {
@@ -61,6 +78,18 @@ int main(int argc, char** argv) {
     printf("kb %d: P1 %6llu  wait-B3 %6llu  P3+P4 %6llu  ->next %6llu\n", kb, tr[11 + 4 * kb] - tr[10 + 4 * kb],
            tr[12 + 4 * kb] - tr[11 + 4 * kb], tr[13 + 4 * kb] - tr[12 + 4 * kb],
            (kb < 7 ? tr[14 + 4 * kb] : tr[3]) - tr[13 + 4 * kb]);
+  {
+    CMPC_CUDA(cudaFuncSetAttribute(k_diag_only, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
+    double* dout = dev_alloc<double>(4096, c.stream);
+    for (int it = 0; it < 5; ++it) k_diag_only<<<1, kDfThreads, kDfSmem, c.stream>>>(dM, n, dout);
+    CMPC_CUDA(cudaStreamSynchronize(c.stream));
+    unsigned long long t2[256];
+    CMPC_CUDA(cudaMemcpyFromSymbol(t2, g_trace, sizeof(t2)));
+    printf("k_diag_only: %llu cycles; per step:\n", t2[3] - t2[0]);
+    for (int kb = 0; kb < 7; ++kb)
+      printf("  kb %d: P1 %6llu  B3-wait %6llu  P3 %6llu  P4 %6llu\n", kb, t2[11 + 4 * kb] - t2[10 + 4 * kb],
+             t2[12 + 4 * kb] - t2[11 + 4 * kb], t2[60 + kb] - t2[12 + 4 * kb], t2[13 + 4 * kb] - t2[60 + kb]);
+  }
   printf("worker lane (tid 32), relative to warp-0 P1 start of the same step:\n");
   for (int kb = 0; kb < 8; ++kb)
     printf("kb %d: B1 passed %6lld  W2+X done %6lld  B4 passed %6lld  S3 done %6lld\n", kb,
