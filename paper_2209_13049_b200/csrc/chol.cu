@@ -491,7 +491,8 @@ __global__ void __launch_bounds__(256) k_diag_inv(const double* __restrict__ L, 
 }
 
 constexpr int kTB = kNB * kGemmLD;    // doubles per staged 64 x 64 tile
-constexpr int kDfSmem = 4 * kTB * 8;  // two stages of (X, Y); the potf2 scratch aliases stage 0
+constexpr int kDfExt = 512;           // solve scratch after the staging buffers (doubles)
+constexpr int kDfSmem = (4 * kTB + kDfExt) * 8;  // two stages of (X, Y); the potf2 scratch aliases stage 0
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -553,6 +554,15 @@ struct DfArgs {
   unsigned* flags;  // nt x nt per-tile done flags (== generation when done)
   unsigned* ctl;    // [0] generation, [1] exit count, [2] failure generation, [3] pivot + 1, [4] tile counter
   long long* info;
+  // fused triangular solves (rhs == nullptr: factor only). The diagonal tile i also forms
+  // y_i = W_i (b_i - sum_k L_ik y_k) while it streams L_ik; nt backward tasks follow the
+  // tiles: x_i = W_i' (y_i - sum_{j>i} L_ji' x_j), published through xflags.
+  const double* rhs;  // n
+  double* x;          // n (may alias rhs only if rhs is not read after the forward pass: it is not)
+  double* ybuf;       // nt * 64
+  double* xbuf;       // nt * 64
+  unsigned* xflags;   // nt
+  int nback;          // nt when solving, else 0
 };
 
 // thread 0: spin until both tile flags carry the generation; false on a published failure
@@ -575,6 +585,10 @@ __device__ bool df_tile(const DfArgs& A, int i, int j, unsigned target, double* 
   const bool idle = diag && wm == 0 && wn >= 2;  // strictly upper 32 x 16 blocks of a diagonal tile
   const unsigned* fl = A.flags;
   const unsigned* failw = A.ctl + 2;
+  const bool fwd = diag && A.rhs != nullptr;
+  double* ext = sm + 4 * kTB;  // [0,128) y_k stages, [128,192) t_i, [192,448) quarter partials
+  const int fr = tid & 63, qd = tid >> 6;
+  double fpart = 0.0;
 
   // acc = -(M_ij) (+ -delta on the diagonal), so the updates accumulate with DMMA's "+"
   double acc[2][2][4];
@@ -600,6 +614,7 @@ __device__ bool df_tile(const DfArgs& A, int i, int j, unsigned target, double* 
     if (*s_flag == 2u) return false;
     stage_tile(sm, A.Lt + ((size_t)i * nt) * (kNB * kNB));
     if (!diag) stage_tile(sm + kTB, A.Lt + ((size_t)j * nt) * (kNB * kNB));
+    if (fwd && tid < 32) cp_async16(ext + 2 * tid, A.ybuf + 2 * tid);
     cp_commit();
     for (int k = 0; k < j; ++k) {
       const int s = k & 1;
@@ -614,22 +629,38 @@ __device__ bool df_tile(const DfArgs& A, int i, int j, unsigned target, double* 
       if (pre) {
         stage_tile(xo, A.Lt + ((size_t)i * nt + k + 1) * (kNB * kNB));
         if (!diag) stage_tile(xo + kTB, A.Lt + ((size_t)j * nt + k + 1) * (kNB * kNB));
+        if (fwd && tid < 32) cp_async16(ext + 64 * (s ^ 1) + 2 * tid, A.ybuf + 64 * (k + 1) + 2 * tid);
       }
       cp_commit();
       cp_wait1();
       __syncthreads();  // tile k visible to every warp
       if (!idle) gemm_xyt(xs, diag ? xs : xs + kTB, acc);
+      if (fwd) {  // forward substitution partial: sum_k L_ik y_k, quarter qd of the columns
+        const double* yk = ext + 64 * s;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) fpart = fma(xs[(16 * qd + kk) * kGemmLD + fr], yk[16 * qd + kk], fpart);
+      }
       if (more && !pre) {
         if (tid == 0) *s_flag = wait_flags(fl + i * nt + k + 1, fl + j * nt + k + 1, failw, target) ? 1u : 2u;
         __syncthreads();
         if (*s_flag == 2u) return false;
         stage_tile(xo, A.Lt + ((size_t)i * nt + k + 1) * (kNB * kNB));
         if (!diag) stage_tile(xo + kTB, A.Lt + ((size_t)j * nt + k + 1) * (kNB * kNB));
+        if (fwd && tid < 32) cp_async16(ext + 64 * (s ^ 1) + 2 * tid, A.ybuf + 64 * (k + 1) + 2 * tid);
         cp_commit();
       }
     }
   }
   __syncthreads();  // staging buffers free
+  if (fwd) {  // t_i = b_i - sum_k L_ik y_k (fixed-order quarter sums)
+    double* red = ext + 192;
+    red[qd * 64 + fr] = fpart;
+    __syncthreads();
+    if (tid < 64) {
+      const double bi = c0 + tid < n ? A.rhs[c0 + tid] : 0.0;
+      ext[128 + tid] = bi - ((red[tid] + red[64 + tid]) + (red[128 + tid] + red[192 + tid]));
+    }
+  }
 
   if (diag) {
     double* a = sm;
@@ -663,6 +694,19 @@ __device__ bool df_tile(const DfArgs& A, int i, int j, unsigned target, double* 
       const int r = e & 63, cl = e >> 6;
       if (r < b && cl < b) A.L[(c0 + r) + (c0 + cl) * n] = (r >= cl) ? a[r + cl * kLD] : 0.0;
       Wj[e] = (r >= cl) ? w[r + cl * kLD] : 0.0;
+    }
+    if (fwd) {  // y_i = W_i t_i (W lower), published with the tile flag
+      double* red = ext + 192;
+      const double* tv = ext + 128;
+      double s = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        const int c = 16 * qd + cc;
+        if (c <= fr) s = fma(w[fr + c * kLD], tv[c], s);
+      }
+      red[qd * 64 + fr] = s;
+      __syncthreads();
+      if (tid < 64) A.ybuf[c0 + tid] = (red[tid] + red[64 + tid]) + (red[128 + tid] + red[192 + tid]);
     }
   } else {
     double* x = sm;
@@ -718,6 +762,74 @@ __device__ bool df_tile(const DfArgs& A, int i, int j, unsigned target, double* 
   return true;
 }
 
+// backward block i: x_i = W_i' (y_i - sum_{j>i} L_ji' x_j), j from the last block down (the
+// tile L_ji is staged before x_j is awaited). Warp w owns columns 8w..8w+7; lanes split the
+// 64 rows, fixed-order warp sums.
+__device__ bool df_back(const DfArgs& A, int i, unsigned target, double* sm, volatile unsigned* s_flag) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nt = A.nt;
+  const unsigned* fl = A.flags;
+  const unsigned* failw = A.ctl + 2;
+  // W_i and y_i are final once the diagonal tile is
+  if (tid == 0) *s_flag = wait_flags(fl + i * nt + i, fl + i * nt + i, failw, target) ? 1u : 2u;
+  __syncthreads();
+  if (*s_flag == 2u) return false;
+  const double* Wi = A.W + (size_t)i * (kNB * kNB);
+  double wv0[8], wv1[8];
+#pragma unroll
+  for (int cl = 0; cl < 8; ++cl) {
+    wv0[cl] = __ldcg(Wi + (8 * warp + cl) * kNB + lane);
+    wv1[cl] = __ldcg(Wi + (8 * warp + cl) * kNB + lane + 32);
+  }
+  double part[8];
+#pragma unroll
+  for (int cl = 0; cl < 8; ++cl) part[cl] = 0.0;
+  for (int j = nt - 1; j > i; --j) {
+    if (tid == 0) *s_flag = wait_flags(fl + j * nt + i, fl + j * nt + i, failw, target) ? 1u : 2u;
+    __syncthreads();
+    if (*s_flag == 2u) return false;
+    stage_tile(sm, A.Lt + ((size_t)j * nt + i) * (kNB * kNB));
+    cp_commit();
+    if (tid == 0) *s_flag = wait_flags(A.xflags + j, A.xflags + j, failw, target) ? 1u : 2u;
+    cp_wait0();
+    __syncthreads();
+    if (*s_flag == 2u) return false;
+    const double x0 = __ldcg(A.xbuf + 64 * j + lane), x1 = __ldcg(A.xbuf + 64 * j + lane + 32);
+#pragma unroll
+    for (int cl = 0; cl < 8; ++cl) {
+      const int c = 8 * warp + cl;
+      part[cl] = fma(sm[c * kGemmLD + lane], x0, part[cl]);
+      part[cl] = fma(sm[c * kGemmLD + lane + 32], x1, part[cl]);
+    }
+    __syncthreads();  // staging buffer reused by the next j
+  }
+  double* accv = sm + 4 * kTB;  // 64
+  const double* yi = A.ybuf + 64 * i;
+#pragma unroll
+  for (int cl = 0; cl < 8; ++cl) {
+    const double s = warp_sum(part[cl]);
+    if (lane == 0) accv[8 * warp + cl] = __ldcg(yi + 8 * warp + cl) - s;
+  }
+  __syncthreads();
+  const double a0 = accv[lane], a1 = accv[lane + 32];
+  const int64_t r0 = (int64_t)kNB * i;
+#pragma unroll
+  for (int cl = 0; cl < 8; ++cl) {
+    const int c = 8 * warp + cl;  // x(c) = sum_{r >= c} W(r, c) acc(r)
+    const double s = warp_sum(fma(wv0[cl], a0, wv1[cl] * a1));
+    if (lane == 0) {
+      A.xbuf[64 * i + c] = s;
+      if (r0 + c < A.n) A.x[r0 + c] = s;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(A.xflags + i, target);
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(kDfThreads, 1) k_chol_df(const DfArgs A) {
   extern __shared__ __align__(16) double sm_df[];
   __shared__ unsigned s_target, s_q, s_flag;
@@ -730,7 +842,11 @@ __global__ void __launch_bounds__(kDfThreads, 1) k_chol_df(const DfArgs A) {
     if (tid == 0) s_q = atomicAdd(A.ctl + 4, 1u);
     __syncthreads();
     const int q = (int)s_q;
-    if (q >= A.ntiles) break;
+    if (q >= A.ntiles + A.nback) break;
+    if (q >= A.ntiles) {  // backward solve tasks, last block first
+      if (!df_back(A, A.nt - 1 - (q - A.ntiles), target, sm_df, &s_flag)) break;
+      continue;
+    }
     int j = 0, rem = q;  // column-major enumeration of the lower tiles
     while (rem >= A.nt - j) {
       rem -= A.nt - j;
@@ -847,18 +963,23 @@ void chol_alloc(Ctx& c) {
   c.Lt = dev_zeros<double>((size_t)nb * nb * kNB * kNB, c.stream);
   c.df_flags = dev_zeros<unsigned>((size_t)nb * nb, c.stream);
   c.df_ctl = dev_zeros<unsigned>(8, c.stream);
+  c.df_y = dev_zeros<double>((size_t)nb * kNB, c.stream);
+  c.df_x = dev_zeros<double>((size_t)nb * kNB, c.stream);
+  c.df_xflags = dev_zeros<unsigned>((size_t)nb, c.stream);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
   c.df_grid = sms;
 }
 
 void chol_free(Ctx& c) {
-  for (void* p : {(void*)c.Winv, (void*)c.Lt, (void*)c.df_flags, (void*)c.df_ctl}) dev_free(p, c.stream);
-  c.Winv = c.Lt = nullptr;
-  c.df_flags = c.df_ctl = nullptr;
+  for (void* p : {(void*)c.Winv, (void*)c.Lt, (void*)c.df_flags, (void*)c.df_ctl, (void*)c.df_y,
+                  (void*)c.df_x, (void*)c.df_xflags})
+    dev_free(p, c.stream);
+  c.Winv = c.Lt = c.df_y = c.df_x = nullptr;
+  c.df_flags = c.df_ctl = c.df_xflags = nullptr;
 }
 
-void launch_cholesky(Ctx& c, const double* M, double* L, double delta) {
+void launch_cholesky(Ctx& c, const double* M, double* L, double delta, const double* rhs, double* x) {
   const int64_t n = c.n;
   long long* info = &c.pk->info;
   if (n == 0) {
@@ -879,7 +1000,13 @@ void launch_cholesky(Ctx& c, const double* M, double* L, double delta) {
   a.flags = c.df_flags;
   a.ctl = c.df_ctl;
   a.info = info;
-  const int grid = std::min(a.ntiles, c.df_grid);
+  a.rhs = rhs;
+  a.x = x;
+  a.ybuf = c.df_y;
+  a.xbuf = c.df_x;
+  a.xflags = c.df_xflags;
+  a.nback = rhs ? nt : 0;
+  const int grid = std::min(a.ntiles + a.nback, c.df_grid);
   k_chol_df<<<grid, kDfThreads, kDfSmem, c.stream>>>(a);
   CMPC_LAUNCHED();
 }

@@ -102,6 +102,9 @@ struct Ctx {
   double* Lt = nullptr;      // packed 64 x 64 off-diagonal tiles of L (dataflow Cholesky)
   unsigned* df_flags = nullptr;  // per-tile done flags (generation stamped)
   unsigned* df_ctl = nullptr;    // generation, exit count, failure, pivot, tile counter
+  double* df_y = nullptr;        // fused forward-solve blocks (nt x 64)
+  double* df_x = nullptr;        // fused backward-solve blocks (nt x 64)
+  unsigned* df_xflags = nullptr; // backward block done flags
   int df_grid = 148;
   Packet* pk = nullptr;      // device packet
   Packet* pk_host = nullptr; // pinned mirror
@@ -124,8 +127,10 @@ void launch_condense(Ctx& c, bool mirror);
 void syrk_free(Ctx& c);
 
 // ---- chol.cu
-// L = chol(M + delta I) (lower, upper zeroed); failing pivot+1 in c.pk->info
-void launch_cholesky(Ctx& c, const double* M, double* L, double delta);
+// L = chol(M + delta I) (lower, upper zeroed); failing pivot+1 in c.pk->info; with rhs,
+// the same kernel also solves L L' x = rhs (x written only when the factorization succeeds)
+void launch_cholesky(Ctx& c, const double* M, double* L, double delta, const double* rhs = nullptr,
+                     double* x = nullptr);
 void chol_alloc(Ctx& c);
 void chol_free(Ctx& c);
 // diagonal-block inverses of an externally provided factor (set_factor)

@@ -55,8 +55,9 @@ void rec(cudaEvent_t e, cudaStream_t s) {
     CMPC_CUDA(cudaEventRecord(e, s));
 }
 
-// segment A: sigma/omega/q, condensation, Cholesky (delta = 0) with the right-hand side
-// J'(r2 - sigma r3) on a parallel branch, solve, recovery + fraction to boundary, trial 0
+// segment A: sigma/omega/q, condensation with the right-hand side J'(r2 - sigma r3) on a
+// parallel branch, Cholesky (delta = 0) fused with the solve, recovery + fraction to
+// boundary, trial 0
 void seg_step(Ctx& c, double tau) {
   rec(c.ev0, c.stream);
   launch_prepare_step(c, nullptr);
@@ -72,10 +73,9 @@ void seg_step(Ctx& c, double tau) {
   rec(c.ev2, c.stream);
   launch_condense(c, false);
   rec(c.ev3, c.stream);
-  launch_cholesky(c, c.M, c.L, 0.0);
-  rec(c.ev1, c.stream);
   CMPC_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
-  launch_chol_solve(c, c.L, c.rhs, c.pv);
+  launch_cholesky(c, c.M, c.L, 0.0, c.rhs, c.pv);  // factor + both triangular solves
+  rec(c.ev1, c.stream);
   launch_recover(c, tau);
   launch_trial(c, 0.0, true);
 }
@@ -250,9 +250,8 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     while (c.pk_host->info != 0) {
       if (++shift == kShifts.size()) break;
       CMPC_CUDA(cudaEventRecord(c.ev0, c.stream));
-      launch_cholesky(c, c.M, c.L, kShifts[shift]);
+      launch_cholesky(c, c.M, c.L, kShifts[shift], c.rhs, c.pv);
       CMPC_CUDA(cudaEventRecord(c.ev1, c.stream));
-      launch_chol_solve(c, c.L, c.rhs, c.pv);
       launch_recover(c, tau);
       launch_trial(c, 0.0, true);
       sync_packet(c, &syncs);

@@ -53,6 +53,65 @@ __global__ void __launch_bounds__(256) k_rows_gemv(const double* __restrict__ A,
   }
 }
 
+// y[k] = sum_{j < hi_k} P[k + j*ldp] x[j] for the SYRK prototypes: 64 rows per block (two
+// per lane, 16-byte loads), the eight warps take interleaved column slices with four loads
+// in flight each, then a fixed-order reduction of the slices. ldp is even (a multiple of
+// kBK), so every row pair is 16-byte aligned. HBM-bound: P is read once.
+__global__ void __launch_bounds__(256) k_proto_gemv(const double* __restrict__ P, int64_t ldp, int64_t rows,
+                                                    const int32_t* __restrict__ hi,
+                                                    const double* __restrict__ x, double* __restrict__ y) {
+  __shared__ double2 red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // widest rows first (rows are sorted by width): the heavy blocks start in the first wave
+  const int64_t r = (int64_t)(gridDim.x - 1 - blockIdx.x) * 64 + 2 * lane;
+  const int w0 = r < rows ? hi[r] : 0, w1 = r + 1 < rows ? hi[r + 1] : 0;
+  int wmax = max(w0, w1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  const double2* col = reinterpret_cast<const double2*>(P + r);
+  const int64_t ld2 = ldp / 2;
+  int j = w;
+  for (; j + 24 < wmax; j += 32) {
+    double2 v[4];
+    double xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v[u] = r < rows ? __ldcs(col + (j + 8 * u) * ld2) : make_double2(0.0, 0.0);
+      xv[u] = x[j + 8 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jj = j + 8 * u;
+      const double p0 = jj < w0 ? v[u].x : 0.0, p1 = jj < w1 ? v[u].y : 0.0;
+      if (u & 1) {
+        b0 += p0 * xv[u];
+        b1 += p1 * xv[u];
+      } else {
+        a0 += p0 * xv[u];
+        a1 += p1 * xv[u];
+      }
+    }
+  }
+  for (; j < wmax; j += 8) {
+    const double2 v = r < rows ? __ldcs(col + j * ld2) : make_double2(0.0, 0.0);
+    a0 += (j < w0 ? v.x : 0.0) * x[j];
+    a1 += (j < w1 ? v.y : 0.0) * x[j];
+  }
+  red[w][lane] = make_double2(a0 + b0, a1 + b1);
+  __syncthreads();
+  if (w == 0 && r < rows) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      s0 += red[q][lane].x;
+      s1 += red[q][lane].y;
+    }
+    y[r] = s0;
+    if (r + 1 < rows) y[r + 1] = s1;
+  }
+}
+
 __global__ void k_sing_x(const int32_t* __restrict__ col, const double* __restrict__ val, int64_t pz,
                          const double* __restrict__ x, double* __restrict__ y) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -64,7 +123,9 @@ __device__ __forceinline__ double jrow(const double* y, int32_t rm) {
   return (rm & 1) ? -v : v;
 }
 
-// out[j] partial over a chunk of P rows: colpart[chunk*n + j]
+// out[j] partial over a chunk of rc P rows: colpart[chunk*n + j]; one warp per (chunk,
+// column), 16-byte loads (two rows per lane) with four in flight. Column j's nonzeros are
+// the rows >= start_col[j]; the pair containing start_col[j] is read whole and masked.
 __global__ void __launch_bounds__(256) k_ptq_partial(const double* __restrict__ P, int64_t ldp,
                                                      int64_t ps, int64_t n,
                                                      const int32_t* __restrict__ start_col,
@@ -75,29 +136,63 @@ __global__ void __launch_bounds__(256) k_ptq_partial(const double* __restrict__ 
   if (j >= n) return;
   const int64_t k0 = (int64_t)blockIdx.x * rc, k1 = (ps < k0 + rc ? ps : k0 + rc);
   const int64_t kb = (k0 > (int64_t)start_col[j] ? k0 : (int64_t)start_col[j]);
-  double s = 0.0;
+  const int64_t ka = kb & ~int64_t(1);
   const double* col = P + j * ldp;
-  for (int64_t k = kb + lane; k < k1; k += 32) s += col[k] * q[k];
-  s = warp_sum(s);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t k = ka + 2 * lane;
+  for (; k + 192 < k1; k += 256) {
+    double2 v[4], qq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v[u] = __ldcs(reinterpret_cast<const double2*>(col + k + 64 * u));
+      qq[u] = *reinterpret_cast<const double2*>(q + k + 64 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t kk = k + 64 * u;
+      const double e0 = kk >= kb ? v[u].x * qq[u].x : 0.0;
+      const double e1 = (kk + 1 >= kb && kk + 1 < k1) ? v[u].y * qq[u].y : 0.0;
+      if (u & 1) {
+        s2 += e0;
+        s3 += e1;
+      } else {
+        s0 += e0;
+        s1 += e1;
+      }
+    }
+  }
+  for (; k < k1; k += 64) {
+    const double2 v = __ldcs(reinterpret_cast<const double2*>(col + k));
+    const double2 qq = *reinterpret_cast<const double2*>(q + k);
+    if (k >= kb) s0 += v.x * qq.x;
+    if (k + 1 >= kb && k + 1 < k1) s1 += v.y * qq.y;
+  }
+  const double s = warp_sum((s0 + s1) + (s2 + s3));
   if (lane == 0) colpart[blockIdx.x * n + j] = s;
 }
 
-// out[j] = sum_chunks colpart + singleton scatter (singletons sorted by column)
-__global__ void k_ptq_final(const double* __restrict__ colpart, int nchunks, int64_t n,
-                            const int32_t* __restrict__ sing_col, const double* __restrict__ sing_val,
-                            int64_t pz, const double* __restrict__ qs, double* __restrict__ out) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// out[j] = sum_chunks colpart + singleton scatter (singletons sorted by column); one warp
+// per column, lanes stride the chunks, fixed-order warp sum
+__global__ void __launch_bounds__(256) k_ptq_final(const double* __restrict__ colpart, int nchunks, int64_t n,
+                                                   const int32_t* __restrict__ sing_col,
+                                                   const double* __restrict__ sing_val, int64_t pz,
+                                                   const double* __restrict__ qs, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x * 8ll + (threadIdx.x >> 5);
   if (j >= n) return;
   double s = 0.0;
-  for (int c = 0; c < nchunks; ++c) s += colpart[(int64_t)c * n + j];
-  int64_t lo = 0, hi = pz;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) / 2;
-    if (sing_col[mid] < j) lo = mid + 1;
-    else hi = mid;
+  for (int c = lane; c < nchunks; c += 32) s += colpart[(int64_t)c * n + j];
+  s = warp_sum(s);
+  if (lane == 0) {
+    int64_t lo = 0, hi = pz;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (sing_col[mid] < j) lo = mid + 1;
+      else hi = mid;
+    }
+    for (int64_t k = lo; k < pz && sing_col[k] == j; ++k) s += sing_val[k] * qs[k];
+    out[j] = s;
   }
-  for (int64_t k = lo; k < pz && sing_col[k] == j; ++k) s += sing_val[k] * qs[k];
-  out[j] = s;
 }
 
 // ---------------------------------------------------------------- residuals
@@ -592,7 +687,7 @@ void launch_Hx(Ctx& c, const double* x, double* out) {
 
 void launch_Jx(Ctx& c, const double* x, double* y, double* Jx) {
   if (c.ps > 0) {
-    k_rows_gemv<<<(unsigned)ceil_div(c.ps, 32), 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.n, c.hi, x, y);
+    k_proto_gemv<<<(unsigned)ceil_div(c.ps, 64), 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.hi, x, y);
     CMPC_LAUNCHED();
   }
   if (c.pz > 0) {
@@ -615,7 +710,7 @@ void launch_Jtq(Ctx& c, const double* q, double* out) {
     k_ptq_partial<<<g, 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.n, c.start_col, q, rc, c.colpart);
     CMPC_LAUNCHED();
   }
-  k_ptq_final<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(
+  k_ptq_final<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(
       c.colpart, c.ps > 0 ? c.colchunks : 0, c.n, c.sing_col, c.sing_val, c.pz, q + c.ldp, out);
   CMPC_LAUNCHED();
 }

@@ -24,7 +24,7 @@ for cfg in cfgs:
     print(f"   solve: {r.status.name} iter={r.iter} total={r.total_seconds*1e3:.2f}ms device={r.device_seconds*1e3:.2f}ms "
           f"syrk={r.syrk_seconds*1e3:.2f}ms chol={r.chol_seconds*1e3:.2f}ms launches={r.launches} syncs={r.syncs}")
     per = {}
-    for ph in ["prepare", "condense", "cholesky", "chol_solve", "residuals", "recover", "trial", "Jx", "Jty"]:
+    for ph in ["prepare", "condense", "cholesky", "chol_solve", "chol_fused", "residuals", "recover", "trial", "Jx", "Jty"]:
         per[ph] = dq.time_phase(ph, 20)
     for k, v in per.items():
         extra = ""
