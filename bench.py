@@ -330,7 +330,8 @@ def main():
         e2e = {"value": e2e_local / (args.steps * world), "unit": "ms",
                "h2d_bytes_per_step": int(8 * (n * n + n + m * n + m)),
                "d2h_bytes_per_step": int(8 * (n + 3 * m)),
-               "median_ms": statistics.median(e2e_ms), "status": re.status.name,
+               "median_ms": statistics.median(e2e_ms), "samples_ms": [round(x, 2) for x in e2e_ms],
+               "status": re.status.name,
                "iterations": re.iter}
 
     if rank != 0:

@@ -161,15 +161,15 @@ int cmpc_load_qp(cmpc_ctx* x, int64_t n, int64_t m, const double* H, const doubl
     if (m * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.J, J, sizeof(double) * m * n, kind, c.stream));
     if (m > 0) CMPC_CUDA(cudaMemcpyAsync(c.d, d, sizeof(double) * m, kind, c.stream));
     const bool verbose = getenv("CMPC_VERBOSE") != nullptr;
+    double last = t_in;
     auto tick = [&](const char* what) {
-      static double last = 0.0;
       if (!verbose) return;
       sync(c);
       const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
       if (what) fprintf(stderr, "[cmpc load] %-10s %8.2f ms\n", what, (now - last) * 1e3);
       last = now;
     };
-    tick(nullptr);
+    tick("h2d");
     analyze_structure(c);
     tick("analyze");
     // the dense J is not read again: every product goes through P

@@ -55,6 +55,15 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// 64-bit shared-memory load from a 32-bit shared address (a pointer that went through
+// integer alignment arithmetic would otherwise compile to a generic LD with global-load
+// scoreboard latency)
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 // D(16x8) += A(16x16, row) B(16x8, col), FP64 (lowers to DMMA.8x8x4 on sm_100a)
 __device__ __forceinline__ void dmma16816(double* d, const double* a, const double* b) {
   asm volatile(

@@ -18,6 +18,8 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <functional>
+#include <queue>
 #include <vector>
 
 #include "internal.cuh"
@@ -103,9 +105,11 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
     const int s = it % kStages;
     mbar_wait(&full[s], (it / kStages) & 1);
     if (!skip) {
-      const unsigned char* sA = smem + s * kStageBytes;
-      const unsigned char* sB = diag ? sA : sA + kOpBytes;
-      const double* sW = reinterpret_cast<const double*>(smem + s * kStageBytes + 2 * kOpBytes);
+      // explicit 32-bit shared addresses: the aligned generic pointer would compile to LD
+      // (global-load scoreboard latency) instead of LDS
+      const uint32_t sA = smem_u32(smem + s * kStageBytes);
+      const uint32_t sB = diag ? sA : sA + kOpBytes;
+      const uint32_t sW = sA + 2 * kOpBytes;
 #pragma unroll
       for (int ks = 0; ks < kBK; ks += 16) {
         double af[2][8], bf[4][4];
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
           for (int x = 0; x < 8; ++x) {
             const int c = 32 * wm + 16 * mi + g + 8 * (x & 1);
             const int k = ks + t + 4 * (x >> 1);
-            af[mi][x] = *reinterpret_cast<const double*>(sA + op_off(c, k));
+            af[mi][x] = lds64(sA + op_off(c, k));
           }
         }
 #pragma unroll
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
           for (int x = 0; x < 4; ++x) {
             const int c = 32 * wn + 8 * ni + g;
             const int k = ks + t + 4 * x;
-            bf[ni][x] = sW[k] * *reinterpret_cast<const double*>(sB + op_off(c, k));
+            bf[ni][x] = lds64(sW + 8 * k) * lds64(sB + op_off(c, k));
           }
         }
 #pragma unroll
@@ -226,23 +230,60 @@ void syrk_plan(Ctx& c) {
       range.push_back({kb, k_end});
       total += std::max(0, k_end - kb);
     }
-  // chunk so that there are ~4 waves of 2 CTAs per SM
+  // split-K chunk: the (tile, chunk) units run in k-major order (concurrent units share P
+  // rows in L2) and the hardware dispatches them in order onto 2 CTAs per SM. Pick the chunk
+  // by simulating that list schedule (cost = k-steps + a fixed per-unit overhead for the
+  // pipeline fill and the partial-tile store) and keeping the shortest makespan: a chunk
+  // that leaves a sliver of a last wave idles most of the chip.
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  int64_t kc = round_up(std::max<int64_t>(1, total / (int64_t(sms) * 2 * 4)), kBK);
+  const int slots = sms * 2;
+  auto build = [&](int64_t kc, std::vector<int4>* out, std::vector<std::vector<int>>* pt) {
+    const int64_t nchunks = ceil_div(k_end, kc);
+    for (int64_t q = 0; q < nchunks; ++q) {
+      const int64_t c0 = q * kc, c1 = std::min<int64_t>(k_end, c0 + kc);
+      for (size_t t = 0; t < tiles.size(); ++t) {
+        const int64_t a = std::max<int64_t>(c0, range[t].first), b = std::min<int64_t>(c1, range[t].second);
+        if (a >= b) continue;
+        if (pt) (*pt)[t].push_back((int)out->size());
+        out->push_back({tiles[t].x, tiles[t].y, (int)a, (int)b});
+      }
+    }
+  };
+  auto makespan = [&](const std::vector<int4>& us) {
+    std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+    for (int s = 0; s < slots; ++s) q.push(0.0);
+    double end = 0.0;
+    for (const int4& u : us) {
+      const double t0 = q.top();
+      q.pop();
+      // a diagonal tile loads one operand instead of two: ~3/4 of the time per step
+      const double steps = double(u.w - u.z) / kBK * (u.x == u.y ? 0.75 : 1.0);
+      const double t1 = t0 + steps + 1.5;
+      end = std::max(end, t1);
+      q.push(t1);
+    }
+    return end;
+  };
+  int64_t kc = round_up(std::max<int64_t>(1, total / (int64_t(slots) * 4)), kBK);
   kc = std::max<int64_t>(kc, 8 * kBK);
-  std::vector<int4> units;
-  std::vector<std::vector<int>> per_tile(tiles.size());
-  const int64_t nchunks = ceil_div(k_end, kc);
-  for (int64_t q = 0; q < nchunks; ++q) {
-    const int64_t c0 = q * kc, c1 = std::min<int64_t>(k_end, c0 + kc);
-    for (size_t t = 0; t < tiles.size(); ++t) {
-      const int64_t a = std::max<int64_t>(c0, range[t].first), b = std::min<int64_t>(c1, range[t].second);
-      if (a >= b) continue;
-      per_tile[t].push_back((int)units.size());
-      units.push_back({tiles[t].x, tiles[t].y, (int)a, (int)b});
+  {
+    double best = 1e300;
+    const int64_t hi_kc = std::max<int64_t>(8 * kBK, round_up(std::max<int64_t>(1, total / slots), kBK));
+    const int64_t step = std::max<int64_t>(kBK, round_up((hi_kc - 8 * kBK) / 40, kBK));
+    for (int64_t cand = 8 * kBK; cand <= hi_kc; cand += step) {
+      std::vector<int4> us;
+      build(cand, &us, nullptr);
+      const double ms = makespan(us);
+      if (ms < best * 0.999) {
+        best = ms;
+        kc = cand;
+      }
     }
   }
+  std::vector<int4> units;
+  std::vector<std::vector<int>> per_tile(tiles.size());
+  build(kc, &units, &per_tile);
   std::vector<int32_t> tptr(tiles.size() + 1, 0), tunits;
   for (size_t t = 0; t < tiles.size(); ++t) {
     tptr[t + 1] = tptr[t] + (int32_t)per_tile[t].size();
@@ -295,6 +336,8 @@ void syrk_plan(Ctx& c) {
   static bool attr = false;
   if (!attr) {
     CMPC_CUDA(cudaFuncSetAttribute(k_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
+    // two 99 KB CTAs per SM need the largest shared-memory carveout
+    CMPC_CUDA(cudaFuncSetAttribute(k_syrk, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
 }

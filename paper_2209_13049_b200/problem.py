@@ -349,10 +349,14 @@ def recover_trajectory(qp: DenseQp, v) -> Trajectory:
     for k in range(dm.T):
         x[k + 1:] += vt[:dm.T - k] @ qp.gk[k].T
     u = x[:-1] @ data.K.T + vt
-    cache = qp.__dict__.setdefault("_quad_cache", {})
-    if cache.get("src") is not data:
+    # the diagonal-weight check scans n_x^2 entries: cache it on the problem data, which
+    # every DenseQp built from it (e.g. a fresh upload per solve) shares
+    cache = data.__dict__.setdefault("_quad_cache", {})
+    key = (id(data.Q), id(data.Qf), id(data.R), id(data.S))
+    if cache.get("key") != key:
         cache.clear()
-        cache.update(src=data, Q=_diag_or_none(data.Q), Qf=_diag_or_none(data.Qf),
+        cache["key"] = key
+        cache.update(Q=_diag_or_none(data.Q), Qf=_diag_or_none(data.Qf),
                      R=_diag_or_none(data.R), S0=not np.any(data.S))
 
     def quad(X, Mx, d):
