@@ -173,6 +173,116 @@ def run_reference(args, rank, world):
     return line
 
 
+def run_shard(args, rank, world, local, dist):
+    """Configs 3/4 at N GPUs: the rows of J split across the ranks by whole stages
+    (problem.shard_rows), one solve per step: every rank condenses its rows, the partial
+    condensed matrices and the row reductions are allreduced over NVLink (NCCL, captured in
+    the iteration's CUDA graphs), and the Cholesky + solve run redundantly. value = ms per
+    solve (strong scaling: the whole QP is fixed), max over ranks."""
+    import torch
+    from paper_2209_13049_b200 import _lib, ipm, problem as P
+    cfg = args.config
+    qp = P.build_dense_qp(build_problem(cfg, 0))  # the same QP on every rank
+    uid = ipm.nccl_unique_id() if rank == 0 else None
+    if dist:
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    rows = P.shard_rows(qp, world)[rank]
+    sh = ipm.ShardedQp(qp, rows, uid, world, rank)
+    info = sh.dq.info()
+    opts = ipm.IpmOptions()
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        r = sh.solve(opts)
+    barrier()
+    l0 = _lib.launch_count()
+    dev_s, syrk_s, syrk_n, chol_s, iters = 0.0, 0.0, 0, 0.0, []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            r = sh.solve(opts)
+            dev_s += r.device_seconds
+            syrk_s += r.syrk_seconds
+            syrk_n += r.condensations
+            chol_s += r.chol_seconds
+            iters.append(r.iter)
+    barrier()
+    launches = _lib.launch_count() - l0
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms_total = max_over_ranks(dev_s) * 1e3
+    e2e = None
+    if not args.no_e2e:
+        loc = sh.local
+        pin = P.DenseQp(H=pinned_like(loc.H), h=pinned_like(loc.h), h0=loc.h0,
+                        J=pinned_like(loc.J), d=pinned_like(loc.d))
+        e2e_ms = []
+        for k in range(args.warmup + args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            sh.reload(P.DenseQp(H=pin.H, h=pin.h, h0=pin.h0, J=pin.J, d=pin.d))
+            re = sh.solve(opts)
+            if rank == 0:
+                P.recover_trajectory(qp, re.v)
+            torch.cuda.synchronize(local)
+            dt = time.perf_counter() - t0
+            if k >= args.warmup:
+                e2e_ms.append(dt * 1e3)
+        e2e_tot = max_over_ranks(float(np.sum(e2e_ms)))
+        n, m = loc.n, loc.m
+        e2e = {"value": e2e_tot / args.steps, "unit": "ms",
+               "h2d_bytes_per_step": int(8 * (n * n + n + m * n + m)),
+               "d2h_bytes_per_step": int(8 * (n + 3 * m)),
+               "median_ms": statistics.median(e2e_ms), "samples_ms": [round(x, 2) for x in e2e_ms],
+               "status": re.status.name, "iterations": re.iter,
+               "note": "per rank: its rows of J, d (pinned host) + H, h; max over ranks"}
+    syrk_max = max_over_ranks(syrk_s)
+    if rank != 0:
+        sh.close()
+        if dist:
+            dist.destroy_process_group()
+        return
+    flops_rank0 = info["syrk_flops"]
+    line = {
+        "metric": "ms per MPC solve", "value": ms_total / args.steps, "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": CONFIGS[cfg]["desc"], "n": qp.n, "m": qp.m, "tol": 1e-8,
+                   "parallelism": f"rows of J sharded across {world} GPU(s) by whole stages; "
+                                  f"partial J_g' Sigma_g J_g + row reductions allreduced (NCCL)",
+                   "rows_rank0": int(len(rows)), "prototype_rows_rank0": info["prototypes"],
+                   "l2": "inputs larger than L2 (J 1.0 GB dense)"},
+        "ms_per_iter": ms_total / max(sum(iters), 1), "iterations": iters[-1], "status": r.status.name,
+        "roofline": {"bound": "tensor", "kernel": "k_syrk + k_syrk_reduce (rank 0's rows)",
+                     "achieved": flops_rank0 / (syrk_s / max(syrk_n, 1)) / 1e12,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": flops_rank0 / (syrk_s / max(syrk_n, 1)) / 1e12 / FP64_PEAK_TFLOPS,
+                     "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak_probe.txt",
+                     "algorithmic_flops_per_launch": flops_rank0,
+                     "avg_launch_ms": syrk_s / max(syrk_n, 1) * 1e3,
+                     "share_of_step": syrk_max / max(dev_s, 1e-30), "traffic": None},
+        "phase_ms_per_iter": {"condense": syrk_s * 1e3 / max(sum(iters), 1),
+                              "cholesky": chol_s * 1e3 / max(sum(iters), 1)},
+        "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
+    }
+    print(json.dumps(line), flush=True)
+    sh.close()
+    if dist:
+        dist.destroy_process_group()
+
+
 def run_batch(args, rank, world, local, dist):
     """config 5: 1024 instances split across the ranks; each rank solves its share as one
     concurrent batch (shared H/J structure, per-instance h, h0, d). A step = the whole batch."""
@@ -242,6 +352,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "shard", "replica"],
+                    help="N > 1: shard = rows of J split across the GPUs, one solve (configs 3/4, "
+                         "the default there); replica = an independent instance per GPU")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -267,6 +380,9 @@ def main():
     cfg = args.config
     if cfg == "c5":
         return run_batch(args, rank, world, local, dist)
+    mode = args.mode if args.mode != "auto" else ("shard" if cfg in ("c3", "c4") and world > 1 else "replica")
+    if mode == "shard":
+        return run_shard(args, rank, world, local, dist)
     data = build_problem(cfg, rank)
     qp = P.build_dense_qp(data)
     dq = ipm.DeviceQp(qp, device=local)

@@ -106,10 +106,22 @@ int cmpc_solve(cmpc_ctx* ctx, const double* opts, int64_t max_iter, double* v, d
                double* lambda, double* z, double* out_scalars, cmpc_log_fn log,
                cmpc_inspect_fn inspect, void* user);
 
+/* Row-sharded solve, one process per GPU: each rank loads its own rows of
+ * J and d (cmpc_load_qp with m = its row count) and the full H, h, h0; rank 0 creates the
+ * NCCL unique id (128 bytes) and the host broadcasts it; every rank attaches with the total
+ * row count. cmpc_solve then runs the same host loop on every rank: the per-row partial
+ * sums (J_g' Sigma_g J_g, J_g' y_g, residual/merit sums and maxima, step-length minima) are
+ * allreduced over NVLink on the solve's stream and the Cholesky + solve run redundantly on
+ * the identical condensed matrix, so every rank takes identical decisions and returns the
+ * same v (its own rows of s, lambda, z). Needs libnccl.so.2 at run time (dlopen). */
+int cmpc_comm_unique_id(void* id128);
+int cmpc_ctx_attach_comm(cmpc_ctx* ctx, const void* id128, int nranks, int rank, int64_t m_total);
+int cmpc_ctx_detach_comm(cmpc_ctx* ctx);
+
 /* Device time of one phase of the iteration on the current device state, averaged over
  * reps back-to-back launches (CUDA events): 0 sigma+condense, 1 condense, 2 Cholesky,
  * 3 triangular solves, 4 residuals, 5 step recovery, 6 line-search trial, 7 J x, 8 J' y,
- * 9 sigma/omega/rhs preparation. */
+ * 9 sigma/omega/rhs preparation, 10 Cholesky fused with both triangular solves. */
 int cmpc_time_phase(cmpc_ctx* ctx, int what, int reps, double* ms_per_rep);
 
 /* Stand-alone dense linear algebra (the reference's linalg plug point,

@@ -55,6 +55,9 @@ SIGNATURES = {
     "cmpc_time_phase": (C.c_int, [C.c_void_p, C.c_int, C.c_int, D]),
     "cmpc_ctx_clone": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "cmpc_solve_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int64, D, C.c_int64, D, D, C.c_int]),
+    "cmpc_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "cmpc_ctx_attach_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int64]),
+    "cmpc_ctx_detach_comm": (C.c_int, [C.c_void_p]),
 }
 
 

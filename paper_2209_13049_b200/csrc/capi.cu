@@ -122,6 +122,11 @@ void cmpc_ctx_destroy(cmpc_ctx* x) {
   if (!x) return;
   cudaSetDevice(x->c.device);
   cudaStreamSynchronize(x->c.stream);
+  drop_graphs(x->c);
+  try {
+    comm_detach(x->c);
+  } catch (...) {
+  }
   release_qp(x->c);
   cudaStreamSynchronize(x->c.stream);
   cudaEventDestroy(x->c.ev0);
@@ -282,6 +287,38 @@ int cmpc_qp_info(cmpc_ctx* x, int64_t* out) {
   return CMPC_OK;
 }
 
+int cmpc_comm_unique_id(void* id128) {
+  return guard([&] {
+    if (!id128) throw DimError("id buffer is NULL");
+    comm_unique_id(id128);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_ctx_attach_comm(cmpc_ctx* x, const void* id128, int nranks, int rank, int64_t m_total) {
+  return guard([&] {
+    Ctx& c = x->c;
+    require_loaded(c);
+    if (!id128 || nranks < 1 || rank < 0 || rank >= nranks) throw DimError("bad communicator arguments");
+    if (m_total < c.m) throw DimError("m_total is smaller than this shard's rows");
+    CMPC_CUDA(cudaStreamSynchronize(c.stream));
+    drop_graphs(c);
+    comm_attach(c, id128, nranks, rank);
+    c.m_all = m_total;
+    return CMPC_OK;
+  });
+}
+
+int cmpc_ctx_detach_comm(cmpc_ctx* x) {
+  return guard([&] {
+    Ctx& c = x->c;
+    drop_graphs(c);
+    comm_detach(c);
+    c.m_all = -1;
+    return CMPC_OK;
+  });
+}
+
 int cmpc_time_phase(cmpc_ctx* x, int what, int reps, double* ms_per_rep) {
   return guard([&] {
     Ctx& c = x->c;
@@ -390,6 +427,7 @@ int cmpc_assemble_condensed(cmpc_ctx* x, const double* sigma, double* M) {
     if (sigma && c.m > 0) h2d(c, c.sigma, sigma, c.m);
     launch_prepare_step(c, sigma ? c.sigma : nullptr);
     launch_condense(c, true);
+    comm_allreduce(c, c.M, (size_t)(c.n * c.n), CommType::f64, CommOp::sum);  // sharded
     d2h(c, M, c.M, c.n * c.n);
     sync(c);
     return CMPC_OK;
@@ -440,7 +478,9 @@ int cmpc_step_directions(cmpc_ctx* x, double tau, double* pv, double* ps, double
     require_loaded(c);
     if (!(tau > 0.0 && tau < 1.0)) throw DimError("tau must lie in (0,1)");
     launch_prepare_step(c, nullptr);
-    launch_rhs(c);
+    launch_rhs_partial(c);
+    comm_allreduce(c, c.rhs, (size_t)c.n, CommType::f64, CommOp::sum);  // sharded
+    launch_rhs_final(c);
     launch_chol_solve(c, c.L, c.rhs, c.pv);
     launch_recover(c, tau);
     d2h(c, pv, c.pv, c.n);

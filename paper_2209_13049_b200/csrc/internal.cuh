@@ -14,6 +14,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <vector>
 
@@ -40,10 +41,20 @@ struct Packet {
   double pad[8];
 };
 
+// the allreduced groups of the sharded solve are contiguous
+static_assert(offsetof(Packet, sum_abs_r3) == offsetof(Packet, sum_log_s) + 8, "packet layout");
+static_assert(offsetof(Packet, max_z) == offsetof(Packet, max_r3) + 32, "packet layout");
+static_assert(offsetof(Packet, alpha_z_min) == offsetof(Packet, alpha_s_min) + 8, "packet layout");
+static_assert(offsetof(Packet, t_sum_abs) == offsetof(Packet, t_sum_log) + 8, "packet layout");
+
 struct Workspace;
 
 struct Ctx {
   int device = 0;
+  // row-sharded solve (comm.cpp): this context holds rows of J; partial sums are allreduced
+  void* comm = nullptr;  // ncclComm_t
+  int nranks = 1, rank = 0;
+  int64_t m_all = -1;    // rows of the whole QP (kkt scaling); -1 = m
   cudaStream_t stream = nullptr;
   bool owns_stream = true;
 
@@ -138,6 +149,17 @@ void launch_factor_inverses(Ctx& c, const double* L);
 // x = L^{-T} L^{-1} b (in place on x allowed); uses the diagonal-block inverses
 void launch_chol_solve(Ctx& c, const double* L, const double* b, double* x);
 
+// ---- comm.cpp (NCCL, opened at run time)
+enum class CommType { f64, i64 };
+enum class CommOp { sum, max, min };
+void comm_unique_id(void* out128);
+void comm_attach(Ctx& c, const void* id128, int nranks, int rank);
+void comm_detach(Ctx& c);
+// in-place allreduce on c.stream (no-op without a communicator)
+void comm_allreduce(Ctx& c, void* buf, size_t count, CommType type, CommOp op);
+void comm_group(bool start);
+inline int64_t rows_all(const Ctx& c) { return c.m_all >= 0 ? c.m_all : c.m; }
+
 // ---- vec.cu
 void launch_zero_packet(Ctx& c);
 // max |h| (after h changed)
@@ -151,7 +173,10 @@ void launch_residuals(Ctx& c, bool reuse_trial = false);
 void launch_residuals_mu(Ctx& c);
 // sigma = z/s, omega, dsing, q = Pi'(r2 - sigma r3)
 void launch_prepare_step(Ctx& c, const double* sigma_override);
-// rhs = -r1 + (P' q + singletons)
+// rhs = -r1 + (P' q + singletons): the partial product (this context's rows) and the final
+// combination; launch_rhs does both (unsharded)
+void launch_rhs_partial(Ctx& c);
+void launch_rhs_final(Ctx& c);
 void launch_rhs(Ctx& c);
 // Jpv, ps, plambda, pz, fraction-to-boundary minima, line-search derivative pieces
 void launch_recover(Ctx& c, double tau);

@@ -66,7 +66,10 @@ void seg_step(Ctx& c, double tau) {
   {
     cudaStream_t s0 = c.stream;
     c.stream = c.stream2;
-    launch_rhs(c);  // memory-bound pass, overlaps the tensor-core SYRK
+    // memory-bound pass, overlaps the tensor-core SYRK (sharded: the partial only; the
+    // collectives stay on the main stream, one communicator, one issue order)
+    if (c.comm) launch_rhs_partial(c);
+    else launch_rhs(c);
     c.stream = s0;
   }
   CMPC_CUDA(cudaEventRecord(c.join, c.stream2));
@@ -74,6 +77,13 @@ void seg_step(Ctx& c, double tau) {
   launch_condense(c, false);
   rec(c.ev3, c.stream);
   CMPC_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
+  if (c.comm) {  // M = H + sum_g J_g' Sigma_g J_g and J' (r2 - sigma r3) over all ranks
+    comm_group(true);
+    comm_allreduce(c, c.M, (size_t)(c.n * c.n), CommType::f64, CommOp::sum);
+    comm_allreduce(c, c.rhs, (size_t)c.n, CommType::f64, CommOp::sum);
+    comm_group(false);
+    launch_rhs_final(c);
+  }
   launch_cholesky(c, c.M, c.L, 0.0, c.rhs, c.pv);  // factor + both triangular solves
   rec(c.ev1, c.stream);
   launch_recover(c, tau);
@@ -136,7 +146,7 @@ namespace {
 // current state, `dg`/`dps` the derivative pieces; trial 0 may already be evaluated.
 int run_line_search(Ctx& c, const Packet& A, double dg, double dps, double alpha_max, double eta,
                     const Packet* trial0, double* alpha_out, int* ntrials, long long* syncs) {
-  const bool rows = c.m > 0;
+  const bool rows = rows_all(c) > 0;
   const double rho = 10.0 * A.max_lam + 1.0;
   const double phi0 = merit_host(A, A.obj_vHv, A.obj_hv, A.sum_log_s, A.sum_abs_r3, c.mu, rho, rows);
   double derivative = dg;

@@ -177,7 +177,7 @@ __global__ void k_syrk_reduce(const double* __restrict__ partial, const int2* __
   if (q < u1) s0 += partial[(size_t)tile_units[q] * (kTile * kTile) + e];
   double s = s0 + s1;
   if (i == j) s += dsing[i];
-  const double v = H[i + j * n] + s;
+  const double v = H ? H[i + j * n] + s : s;  // H on one rank only when sharded
   M[i + j * n] = v;
   if (mirror && i != j) M[j + i * n] = v;
 }
@@ -348,8 +348,9 @@ void launch_condense(Ctx& c, bool mirror) {
     k_syrk<<<c.nunits, kSyrkThreads, kSyrkSmem, c.stream>>>(*tm, c.omega, c.units, c.partial);
     CMPC_LAUNCHED();
   }
-  k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 256), 256, 0, c.stream>>>(c.partial, c.tiles, c.tile_ptr, c.tile_units, c.H,
+  k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 256), 256, 0, c.stream>>>(c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr,
                                                  c.dsing, c.n, c.M, mirror ? 1 : 0);
+  // (sharded: every rank's partial J_g' Sigma_g J_g, H added by rank 0; the caller allreduces)
   CMPC_LAUNCHED();
 }
 

@@ -316,20 +316,42 @@ __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* 
 
 constexpr int kFinT = 1024;
 
-// finalize packet A: r1 = (Hv + h) + J'lambda, max|r1|, kkt, dots for objective and merit
-__global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m, int nparts,
+// finalize packet A: r1 = (Hv + h) + J'lambda, max|r1|, kkt, dots for objective and merit.
+// mode 0: everything; 1: only this context's row sums into the packet (sharded: they are
+// allreduced next); 2: everything, with the (allreduced) row sums taken from the packet.
+// m_all = rows of the whole QP (the kkt scaling), nparts = 0 when this context has no rows.
+__global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, int nparts,
                                                      const double* __restrict__ Hv,
                                                      const double* __restrict__ h,
                                                      const double* __restrict__ Jtl,
                                                      const double* __restrict__ v,
                                                      double* __restrict__ r1,
                                                      const double* __restrict__ part, double h0,
-                                                     const double* __restrict__ hmax, Packet* pk) {
+                                                     const double* __restrict__ hmax, Packet* pk,
+                                                     int mode) {
   __shared__ double sh[32];
+  double sabs = 0.0, slog = 0.0;
+  if (mode != 2) {
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+      sabs += part[b * kSlots + kSumAbs];
+      slog += part[b * kSlots + kSumLog];
+    }
+    sabs = block_sum<kFinT>(sabs, sh);
+    __syncthreads();
+    slog = block_sum<kFinT>(slog, sh);
+    __syncthreads();
+    if (mode == 1) {
+      if (threadIdx.x == 0) {
+        pk->sum_abs_r3 = sabs;
+        pk->sum_log_s = slog;
+      }
+      return;
+    }
+  }
   double mr1 = 0.0, vhv = 0.0, hv = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const double g = add(Hv[i], h[i]);
-    const double r = m > 0 ? add(g, Jtl[i]) : g;
+    const double r = m_all > 0 ? add(g, Jtl[i]) : g;
     r1[i] = r;
     mr1 = fmax(mr1, fabs(r));
     vhv += v[i] * Hv[i];
@@ -339,33 +361,28 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m, int n
   __syncthreads();
   hv = block_sum<kFinT>(hv, sh);
   __syncthreads();
-  double sabs = 0.0, slog = 0.0;
-  for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
-    sabs += part[b * kSlots + kSumAbs];
-    slog += part[b * kSlots + kSumLog];
-  }
-  sabs = block_sum<kFinT>(sabs, sh);
-  __syncthreads();
-  slog = block_sum<kFinT>(slog, sh);
-  __syncthreads();
   mr1 = warp_max(mr1);
   __shared__ double mx[32];
   if ((threadIdx.x & 31) == 0) mx[threadIdx.x >> 5] = mr1;
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (mode == 2) {
+      sabs = pk->sum_abs_r3;
+      slog = pk->sum_log_s;
+    }
     double a = 0.0;
     for (int q = 0; q < kFinT / 32; ++q) a = fmax(a, mx[q]);
     pk->max_r1 = a;
     pk->obj_vHv = vhv;
     pk->obj_hv = hv;
-    pk->sum_abs_r3 = m > 0 ? sabs : 0.0;
-    pk->sum_log_s = m > 0 ? slog : 0.0;
+    pk->sum_abs_r3 = m_all > 0 ? sabs : 0.0;
+    pk->sum_log_s = m_all > 0 ? slog : 0.0;
     pk->max_h = *hmax;
     pk->objective = 0.5 * vhv + hv + h0;
-    const double ds = fmax(1.0, fmax(*hmax, pk->max_lam) / (double)(n + m));
+    const double ds = fmax(1.0, fmax(*hmax, pk->max_lam) / (double)(n + m_all));
     double kkt = a / ds;
-    if (m > 0) {
-      const double cs = fmax(1.0, fmax(pk->max_s, pk->max_z) / (double)(2 * m));
+    if (m_all > 0) {
+      const double cs = fmax(1.0, fmax(pk->max_s, pk->max_z) / (double)(2 * m_all));
       kkt = fmax(kkt, pk->max_r3);
       kkt = fmax(kkt, pk->max_comp / cs);
     }
@@ -717,6 +734,7 @@ void launch_Jtq(Ctx& c, const double* q, double* out) {
 
 void launch_residuals(Ctx& c, bool reuse_trial) {
   const unsigned pb = part_blocks(c.m);
+  const int64_t m_all = rows_all(c);
   k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 0);
   CMPC_LAUNCHED();
   if (reuse_trial) {
@@ -738,20 +756,37 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
         c.p, c.mem_ptr, c.mem_rows, c.lam, nullptr, c.q, nullptr, c.ps, c.ldp, c.zero_k);
     CMPC_LAUNCHED();
     launch_Jtq(c, c.q, c.Jtl);
+  } else if (c.comm && c.n > 0) {
+    CMPC_CUDA(cudaMemsetAsync(c.Jtl, 0, sizeof(double) * c.n, c.stream));
   }
-  k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m, c.m > 0 ? (int)pb : 0, c.Hv, c.h, c.Jtl, c.v,
-                                         c.r1, c.part, c.h0, c.hmax, c.pk);
+  const int np = c.m > 0 ? (int)pb : 0;
+  if (c.comm) {
+    // this rank's rows: J_g' lambda_g, the row sums and maxima -> allreduce -> finalize
+    k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part,
+                                           c.h0, c.hmax, c.pk, 1);
+    CMPC_LAUNCHED();
+    comm_group(true);
+    comm_allreduce(c, c.Jtl, (size_t)c.n, CommType::f64, CommOp::sum);
+    comm_allreduce(c, &c.pk->sum_log_s, 2, CommType::f64, CommOp::sum);  // sum_log_s, sum_abs_r3
+    comm_allreduce(c, &c.pk->max_r3, 5, CommType::f64, CommOp::max);     // max_r3 .. max_z
+    comm_group(false);
+  }
+  k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part, c.h0,
+                                         c.hmax, c.pk, c.comm ? 2 : 0);
   CMPC_LAUNCHED();
 }
 
 void launch_residuals_mu(Ctx& c) {
-  if (c.m > 0) {
+  if (c.m > 0 || c.comm) {
     k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 3);
     CMPC_LAUNCHED();
+  }
+  if (c.m > 0) {
     k_mu_rows<<<part_blocks(c.m), kRowT, 0, c.stream>>>(c.m, c.s, c.lam, c.z, c.d_mu, c.r2, c.pk);
     CMPC_LAUNCHED();
   }
-  k_kkt_only<<<1, 1, 0, c.stream>>>(c.n, c.m, c.hmax, c.pk);
+  comm_allreduce(c, &c.pk->max_comp, 1, CommType::f64, CommOp::max);
+  k_kkt_only<<<1, 1, 0, c.stream>>>(c.n, rows_all(c), c.hmax, c.pk);
   CMPC_LAUNCHED();
 }
 
@@ -775,10 +810,20 @@ void launch_prepare_step(Ctx& c, const double* sigma_override) {
   CMPC_LAUNCHED();
 }
 
-void launch_rhs(Ctx& c) {
+void launch_rhs_partial(Ctx& c) {
   if (c.m > 0) launch_Jtq(c, c.q, c.rhs);
-  k_rhs<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.r1, c.rhs, c.m, c.rhs);
+  else if (c.n > 0) CMPC_CUDA(cudaMemsetAsync(c.rhs, 0, sizeof(double) * c.n, c.stream));
+}
+
+void launch_rhs_final(Ctx& c) {
+  if (c.n == 0) return;
+  k_rhs<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.r1, c.rhs, rows_all(c), c.rhs);
   CMPC_LAUNCHED();
+}
+
+void launch_rhs(Ctx& c) {
+  launch_rhs_partial(c);
+  launch_rhs_final(c);
 }
 
 void launch_hmax(Ctx& c) {
@@ -807,6 +852,12 @@ void launch_recover(Ctx& c, double tau) {
   k_recover_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m > 0 ? (int)pb : 0, c.Hv, c.h, c.pv, c.part,
                                              c.pk);
   CMPC_LAUNCHED();
+  if (c.comm) {  // step-length minima and sum ps/s over every rank's rows
+    comm_group(true);
+    comm_allreduce(c, &c.pk->alpha_s_min, 2, CommType::f64, CommOp::min);
+    comm_allreduce(c, &c.pk->d_ps_s, 1, CommType::f64, CommOp::sum);
+    comm_group(false);
+  }
 }
 
 void launch_trial(Ctx& c, double alpha, bool alpha_from_device) {
@@ -828,6 +879,12 @@ void launch_trial(Ctx& c, double alpha, bool alpha_from_device) {
   k_trial_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m, c.m > 0 ? (int)pb : 0, c.vt, c.Hvt, c.h,
                                            c.part, c.pk);
   CMPC_LAUNCHED();
+  if (c.comm) {  // merit row sums and the slack-positivity flag over every rank's rows
+    comm_group(true);
+    comm_allreduce(c, &c.pk->t_sum_log, 2, CommType::f64, CommOp::sum);
+    comm_allreduce(c, &c.pk->any_nonpos, 1, CommType::i64, CommOp::max);
+    comm_group(false);
+  }
 }
 
 void launch_fraction_to_boundary(cudaStream_t st, int64_t m, const double* s, const double* ps,
@@ -850,6 +907,7 @@ void launch_ls_pieces(Ctx& c) {
   k_recover_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m > 0 ? (int)pb : 0, c.Hv, c.h, c.pv, c.part,
                                              c.pk);
   CMPC_LAUNCHED();
+  comm_allreduce(c, &c.pk->d_ps_s, 1, CommType::f64, CommOp::sum);
 }
 
 void launch_init_state(Ctx& c, double mu) {

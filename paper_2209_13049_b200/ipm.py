@@ -179,6 +179,53 @@ class DeviceQp:
         check(_lib.lib().cmpc_set_state(self.h, ptr(v), ptr(s), ptr(l), ptr(z), float(st.mu)))
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for a row-sharded solve; create it on rank 0 and
+    broadcast it to the other ranks (any host channel: torch.distributed, MPI, a file)."""
+    buf = C.create_string_buffer(128)
+    check(_lib.lib().cmpc_comm_unique_id(buf))
+    return buf.raw
+
+
+class ShardedQp:
+    """This rank's part of a row-sharded QP: rows `rows` of J and d (from
+    problem.shard_rows) on this process's GPU, attached to an NCCL communicator over all
+    ranks. solve() runs ipm::solve cooperatively — every rank must call it with the same
+    options — and returns the same v, kkt, objective, iteration count and status on every
+    rank, with s, lambda, z for this rank's rows."""
+
+    def __init__(self, qp: DenseQp, rows, uid: bytes, nranks: int, rank: int):
+        from .problem import shard_qp
+        self.rows = np.asarray(rows, dtype=np.int64)
+        self.m_total = qp.m
+        self.local = shard_qp(qp, self.rows)
+        self.dq = DeviceQp(self.local)
+        if len(uid) != 128:
+            raise DimensionError("the NCCL unique id is 128 bytes")
+        check(_lib.lib().cmpc_ctx_attach_comm(self.dq.h, uid, int(nranks), int(rank),
+                                              int(self.m_total)))
+        self.nranks, self.rank = nranks, rank
+
+    def solve(self, opts: IpmOptions = None) -> IpmResult:
+        opts = opts or IpmOptions()
+        _check_options(opts)
+        return solve_loaded(self.dq, self.local, opts)
+
+    def reload(self, local: DenseQp):
+        """Upload a new copy of this rank's rows (same shape) into the same context: the
+        communicator and the total row count stay attached (end-to-end timing)."""
+        if local.m != self.local.m or local.n != self.local.n:
+            raise DimensionError("reload: the shard's shape changed")
+        check(_lib.lib().cmpc_load_qp(self.dq.h, local.n, local.m, ptr(local.H), ptr(local.h),
+                                      local.h0, ptr(local.J), ptr(local.d), 0))
+        self.local = local
+
+    def close(self):
+        if getattr(self, "dq", None) is not None:
+            self.dq.close()
+            self.dq = None
+
+
 def device_qp(qp: DenseQp) -> DeviceQp:
     if qp._device is None:
         qp._device = DeviceQp(qp)

@@ -140,6 +140,10 @@ class DenseQp:
     source: LqProblemData | None = None
     gk: np.ndarray | None = None     # T x n_x x n_u: A_K^k B
     x0: np.ndarray | None = None     # (T+1) x n_x free response
+    # per row of J: (stage t, nonzero prefix width) from the builder (None for a bare QP);
+    # used to shard rows across GPUs by whole stages
+    row_stage: np.ndarray | None = None
+    row_width: np.ndarray | None = None
     _device: object = field(default=None, repr=False, compare=False)
 
     def __post_init__(self):
@@ -268,6 +272,8 @@ def build_dense_qp(data: LqProblemData) -> DenseQp:
     cnt = lambda lo, hi: int(np.isfinite(lo).sum() + np.isfinite(hi).sum()) * T
     m = cnt(data.gl, data.gu) + cnt(data.xl, data.xu) + cnt(data.ul, data.uu)
     J = np.zeros((m, n), order="F")
+    row_stage = np.zeros(m, dtype=np.int64)
+    row_width = np.zeros(m, dtype=np.int64)
     r = 0
 
     def brow(t):  # bigB block row t (nx x t*nu)
@@ -284,6 +290,7 @@ def build_dense_qp(data: LqProblemData) -> DenseQp:
                 if t > 0:
                     J[r, :t * nu] = sign * (EFK[i] @ Bt)
                 J[r, t * nu:(t + 1) * nu] += sign * data.F[i]
+                row_stage[r], row_width[r] = t, (t + 1) * nu
                 r += 1
     for upper in (1, 0):
         sign = 1.0 if upper else -1.0
@@ -293,6 +300,7 @@ def build_dense_qp(data: LqProblemData) -> DenseQp:
             Bt = brow(t)
             k = fin.size
             J[r:r + k, :t * nu] = sign * Bt[fin]
+            row_stage[r:r + k], row_width[r:r + k] = t, t * nu
             r += k
     for upper in (1, 0):
         sign = 1.0 if upper else -1.0
@@ -305,9 +313,51 @@ def build_dense_qp(data: LqProblemData) -> DenseQp:
                 if t > 0:
                     J[r, :t * nu] = sign * (data.K[i] @ Bt)
                 J[r, t * nu + i] += sign
+                row_stage[r] = t
+                row_width[r] = t * nu + i + 1 if np.any(data.K) else 1
                 r += 1
     assert r == m, "inequality assembly row count mismatch"
-    return DenseQp(H=H, h=h, h0=h0, J=J, d=d, source=data, gk=gk, x0=x0)
+    return DenseQp(H=H, h=h, h0=h0, J=J, d=d, source=data, gk=gk, x0=x0, row_stage=row_stage,
+                   row_width=row_width)
+
+
+# ------------------------------------------------------------------ row sharding (§8(e))
+def shard_rows(qp: DenseQp, nranks: int) -> list:
+    """Partition the rows of J for the row-sharded solve (one GPU per part).
+
+    J' Sigma J = sum_g J_g' Sigma_g J_g holds for any partition; this one cuts at whole
+    stages (every row of a stage — upper and lower bound of the same quantity, the mirror
+    rows of the plate — lands in one shard, so each shard's exact-duplicate analysis finds
+    the same merges as the whole) and balances the condensation work, which grows with the
+    square of a row's nonzero prefix width. A bare QP (no builder metadata) is cut into
+    contiguous blocks of equal row count. Returns ascending row-index arrays."""
+    m = qp.m
+    if nranks < 1:
+        raise DimensionError("nranks must be positive")
+    if qp.row_stage is None or qp.row_width is None or m == 0:
+        edges = np.linspace(0, m, nranks + 1).round().astype(np.int64)
+        return [np.arange(edges[g], edges[g + 1], dtype=np.int64) for g in range(nranks)]
+    stage = np.asarray(qp.row_stage)
+    work = np.asarray(qp.row_width, dtype=np.float64) ** 2 + 1.0
+    nst = int(stage.max()) + 1
+    per_stage = np.bincount(stage, weights=work, minlength=nst)
+    cum = np.cumsum(per_stage)
+    total = cum[-1]
+    # stage boundaries: the first stage whose cumulative work reaches g / nranks of the total
+    bounds = [0]
+    for g in range(1, nranks):
+        b = int(np.searchsorted(cum, total * g / nranks, side="left")) + 1
+        bounds.append(min(max(b, bounds[-1]), nst))
+    bounds.append(nst)
+    return [np.flatnonzero((stage >= bounds[g]) & (stage < bounds[g + 1])) for g in range(nranks)]
+
+
+def shard_qp(qp: DenseQp, rows) -> DenseQp:
+    """The QP restricted to `rows` of J and d (H, h, h0 are replicated on every shard)."""
+    rows = np.asarray(rows, dtype=np.int64)
+    return DenseQp(H=qp.H, h=qp.h, h0=qp.h0, J=qp.J[rows], d=qp.d[rows],
+                   row_stage=None if qp.row_stage is None else qp.row_stage[rows],
+                   row_width=None if qp.row_width is None else qp.row_width[rows])
 
 
 def refresh_initial_state(qp: DenseQp, x_bar) -> None:
