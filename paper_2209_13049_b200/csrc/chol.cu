@@ -415,6 +415,7 @@ __device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, doubl
           }
         }
       }
+      TRACEW(140 + 2 * kb);
       // S3b: B(r, c) += X(r,:) W(o:o+8, c) for r >= o+8, c < o+8; two fragments in flight
       {
         const int nrg = (kNB - 8 - o + 15) / 16, ncg = kb + 1, total = nrg * ncg;
@@ -459,6 +460,7 @@ __device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, doubl
           }
         }
       }
+      TRACEW(141 + 2 * kb);
       // finished W rows of block kb; the panel L(r, o:o+8) = X below block kb+1
       for (int e = wt; e < 8 * (o + 8); e += kW) {
         const int i = e & 7, c = e >> 3;

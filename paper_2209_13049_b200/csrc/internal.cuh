@@ -118,7 +118,12 @@ struct Ctx {
   unsigned* df_xflags = nullptr; // backward block done flags
   int df_grid = 148;
   Packet* pk = nullptr;      // device packet
-  Packet* pk_host = nullptr; // pinned mirror
+  Packet* pk_host = nullptr; // pinned, device-mapped mirror
+  Packet* pk_map = nullptr;  // device address of pk_host (k_publish writes it directly)
+  volatile unsigned long long* pub_host = nullptr;  // mapped publish sequence number
+  unsigned long long* pub_map = nullptr;            // its device address
+  unsigned long long* pub_dev = nullptr;            // device-side publish counter
+  unsigned long long pub_expect = 0;                // publishes enqueued so far
   double mu = 0.0;
 
   // events for per-phase timing
@@ -162,6 +167,9 @@ inline int64_t rows_all(const Ctx& c) { return c.m_all >= 0 ? c.m_all : c.m; }
 
 // ---- vec.cu
 void launch_zero_packet(Ctx& c);
+// copy the packet into the mapped host mirror and bump the publish sequence (the host spins
+// on it instead of a stream synchronize + D2H copy); returns the sequence value to wait for
+unsigned long long launch_publish(Ctx& c);
 // max |h| (after h changed)
 void launch_hmax(Ctx& c);
 // set the barrier value (host copy and the device scalar the kernels read)

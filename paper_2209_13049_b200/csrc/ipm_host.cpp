@@ -10,6 +10,7 @@
 //   B: after condense + Cholesky + solve + recovery + trial 0 (info, alpha_max, merit)
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -29,11 +30,23 @@ double now_seconds() {
 void require(bool c, const char* m) {
   if (!c) throw DimError(m);
 }
-void sync_packet(Ctx& c, long long* syncs) {
-  CMPC_CUDA(cudaMemcpyAsync(c.pk_host, c.pk, sizeof(Packet), cudaMemcpyDeviceToHost, c.stream));
-  CMPC_CUDA(cudaStreamSynchronize(c.stream));
+// wait for publish number `seq` (k_publish wrote the packet into mapped host memory first):
+// a spin on the mapped word instead of a stream synchronize plus a D2H copy; the stream is
+// polled now and then so a device error surfaces instead of hanging
+void wait_published(Ctx& c, unsigned long long seq, long long* syncs) {
+  for (long spins = 0;; ++spins) {
+    if (*c.pub_host >= seq) break;
+    if ((spins & 0xfff) == 0xfff) {
+      const cudaError_t e = cudaStreamQuery(c.stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady) CMPC_CUDA(e);
+      if (e == cudaSuccess && *c.pub_host < seq)
+        throw CudaError("packet publish lost (stream idle, sequence not reached)");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   if (syncs) ++*syncs;
 }
+void sync_packet(Ctx& c, long long* syncs) { wait_published(c, launch_publish(c), syncs); }
 }  // namespace
 
 void drop_graphs(Ctx& c) {
@@ -88,12 +101,14 @@ void seg_step(Ctx& c, double tau) {
   rec(c.ev1, c.stream);
   launch_recover(c, tau);
   launch_trial(c, 0.0, true);
+  launch_publish(c);
 }
 
 // segment B: the accepted step (alpha, alpha_z on the device) and the residuals after it
 void seg_next(Ctx& c) {
   launch_update_dev(c);
   launch_residuals(c, /*reuse_trial=*/true);
+  launch_publish(c);
 }
 
 // run a segment eagerly, or capture it once into a CUDA graph and replay it
@@ -102,6 +117,7 @@ void run_segment(Ctx& c, cudaGraphExec_t& exec, long long& nodes, bool allow_cap
   if (exec) {
     CMPC_CUDA(cudaGraphLaunch(exec, c.stream));
     g_launches += nodes;
+    ++c.pub_expect;  // every segment graph ends with one k_publish
     return;
   }
   if (!allow_capture || getenv("CMPC_NO_GRAPHS")) {
@@ -248,7 +264,7 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     // speculatively: directions, recovery, fraction to boundary, line-search trial 0
     size_t shift = 0;
     run_segment(c, c.g_step, c.g_step_nodes, iter >= 1, [&] { seg_step(c, tau); });
-    sync_packet(c, &syncs);
+    wait_published(c, c.pub_expect, &syncs);
     float ms = 0.f;
     CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
     linalg += ms * 1e-3;
@@ -308,7 +324,7 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     set_alpha(c, alpha, alpha_z);
     iter += 1;
     run_segment(c, c.g_next, c.g_next_nodes, iter >= 2, [&] { seg_next(c); });
-    sync_packet(c, &syncs);
+    wait_published(c, c.pub_expect, &syncs);
     A = *c.pk_host;
     if (log) {
       const double rec[8] = {double(iter), mu_used, alpha, alpha_z, A.kkt, A.objective, delta, double(j)};

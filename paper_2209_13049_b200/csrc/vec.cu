@@ -667,7 +667,13 @@ void vec_alloc(Ctx& c) {
   c.d_mu = dev_zeros<double>(1, c.stream);
   c.d_alpha = dev_zeros<double>(2, c.stream);
   c.pk = dev_zeros<Packet>(1, c.stream);
-  CMPC_CUDA(cudaMallocHost(&c.pk_host, sizeof(Packet)));
+  CMPC_CUDA(cudaHostAlloc(&c.pk_host, sizeof(Packet) + 64, cudaHostAllocMapped));
+  CMPC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.pk_map), c.pk_host, 0));
+  c.pub_host = reinterpret_cast<volatile unsigned long long*>(reinterpret_cast<char*>(c.pk_host) + sizeof(Packet));
+  c.pub_map = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(c.pk_map) + sizeof(Packet));
+  *c.pub_host = 0;
+  c.pub_dev = dev_zeros<unsigned long long>(1, c.stream);
+  c.pub_expect = 0;
   chol_alloc(c);
   if (c.n > 0) {
     k_absmax<<<(unsigned)std::min<int64_t>(64, ceil_div(c.n, 256)), 256, 0, c.stream>>>(c.h, c.n, c.hmax);
@@ -684,12 +690,40 @@ void vec_free(Ctx& c) {
                   (void*)c.hmax, (void*)c.pk, (void*)c.d_mu, (void*)c.d_alpha})
     dev_free(p, c.stream);
   if (c.pk_host) cudaFreeHost(c.pk_host);
+  dev_free(c.pub_dev, c.stream);
+  c.pub_dev = nullptr;
+  c.pk_map = nullptr;
+  c.pub_host = nullptr;
+  c.pub_map = nullptr;
   chol_free(c);
   c.v = c.s = c.lam = c.z = c.r1 = c.r2 = c.r3 = c.Hv = c.Jtl = c.y = c.sigma = nullptr;
   c.omega = c.q = c.dsing = c.rhs = c.M = c.L = c.pv = c.ps_ = c.pl = c.pzd = nullptr;
   c.Jpv = c.vt = c.yt = c.Hvt = c.part = c.colpart = c.hmax = c.d_mu = c.d_alpha = nullptr;
   c.pk = nullptr;
   c.pk_host = nullptr;
+}
+
+// one warp: packet -> mapped host memory, then the sequence number (system-scope fence
+// between them, so a host that sees the new sequence sees the packet)
+__global__ void k_publish(const Packet* __restrict__ pk, Packet* out, unsigned long long* dev_seq,
+                          unsigned long long* host_seq) {
+  constexpr int kWords = sizeof(Packet) / 8;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(pk);
+  volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(out);
+  for (int i = threadIdx.x; i < kWords; i += 32) dst[i] = src[i];
+  __threadfence_system();
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    const unsigned long long q = *dev_seq + 1;
+    *dev_seq = q;
+    *reinterpret_cast<volatile unsigned long long*>(host_seq) = q;
+  }
+}
+
+unsigned long long launch_publish(Ctx& c) {
+  k_publish<<<1, 32, 0, c.stream>>>(c.pk, c.pk_map, c.pub_dev, c.pub_map);
+  CMPC_LAUNCHED();
+  return ++c.pub_expect;
 }
 
 void launch_zero_packet(Ctx& c) {

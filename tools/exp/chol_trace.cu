@@ -92,7 +92,9 @@ int main(int argc, char** argv) {
   }
   printf("worker lane (tid 32), relative to warp-0 P1 start of the same step:\n");
   for (int kb = 0; kb < 8; ++kb)
-    printf("kb %d: B1 passed %6lld  W2+X done %6lld  B4 passed %6lld  S3 done %6lld\n", kb,
+    printf("kb %d: S3a %5lld S3b %5lld copies %5lld | B1 passed %6lld  W2+X done %6lld  B4 passed %6lld  S3 done %6lld\n", kb,
+           (long long)(tr[140 + 2 * kb] - tr[102 + 4 * kb]), (long long)(tr[141 + 2 * kb] - tr[140 + 2 * kb]),
+           (long long)(tr[103 + 4 * kb] - tr[141 + 2 * kb]),
            (long long)(tr[100 + 4 * kb] - tr[10 + 4 * kb]), (long long)(tr[101 + 4 * kb] - tr[10 + 4 * kb]),
            (long long)(tr[102 + 4 * kb] - tr[10 + 4 * kb]), (long long)(tr[103 + 4 * kb] - tr[10 + 4 * kb]));
   return 0;
