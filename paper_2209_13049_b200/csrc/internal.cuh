@@ -78,6 +78,8 @@ struct Ctx {
   int64_t zero_k = -1;           // prototype index of the all-zero row group (-1: none)
   int32_t* sing_col = nullptr;   // pz (ascending)
   double* sing_val = nullptr;    // pz
+  int32_t* sing_ptr = nullptr;   // n+1: singleton prototypes of column j are [sing_ptr[j], sing_ptr[j+1])
+  bool h_symmetric = false;      // H == H' bitwise: H x as column dots
   std::vector<int32_t> h_start_col;
 
   // SYRK work decomposition

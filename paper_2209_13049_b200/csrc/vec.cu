@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(256) k_ptq_partial(const double* __restrict__ 
 // out[j] = sum_chunks colpart + singleton scatter (singletons sorted by column); one warp
 // per column, lanes stride the chunks, fixed-order warp sum
 __global__ void __launch_bounds__(256) k_ptq_final(const double* __restrict__ colpart, int nchunks, int64_t n,
-                                                   const int32_t* __restrict__ sing_col,
-                                                   const double* __restrict__ sing_val, int64_t pz,
+                                                   const int32_t* __restrict__ sing_ptr,
+                                                   const double* __restrict__ sing_val,
                                                    const double* __restrict__ qs, double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x * 8ll + (threadIdx.x >> 5);
@@ -184,13 +184,7 @@ __global__ void __launch_bounds__(256) k_ptq_final(const double* __restrict__ co
   for (int c = lane; c < nchunks; c += 32) s += colpart[(int64_t)c * n + j];
   s = warp_sum(s);
   if (lane == 0) {
-    int64_t lo = 0, hi = pz;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) / 2;
-      if (sing_col[mid] < j) lo = mid + 1;
-      else hi = mid;
-    }
-    for (int64_t k = lo; k < pz && sing_col[k] == j; ++k) s += sing_val[k] * qs[k];
+    for (int32_t k = sing_ptr[j]; k < sing_ptr[j + 1]; ++k) s += sing_val[k] * qs[k];
     out[j] = s;
   }
 }
@@ -423,19 +417,13 @@ __global__ void k_sigma_rows(int64_t m, const double* __restrict__ s, const doub
 }
 
 // dsing[c] = sum over singleton prototypes at column c of omega * a^2
-__global__ void k_dsing(int64_t n, const int32_t* __restrict__ sing_col,
-                        const double* __restrict__ sing_val, int64_t pz,
-                        const double* __restrict__ omega_s, double* __restrict__ dsing) {
+__global__ void k_dsing(int64_t n, const int32_t* __restrict__ sing_ptr,
+                        const double* __restrict__ sing_val, const double* __restrict__ omega_s,
+                        double* __restrict__ dsing) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
-  int64_t lo = 0, hi = pz;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) / 2;
-    if (sing_col[mid] < j) lo = mid + 1;
-    else hi = mid;
-  }
   double s = 0.0;
-  for (int64_t k = lo; k < pz && sing_col[k] == j; ++k) s += omega_s[k] * (sing_val[k] * sing_val[k]);
+  for (int32_t k = sing_ptr[j]; k < sing_ptr[j + 1]; ++k) s += omega_s[k] * (sing_val[k] * sing_val[k]);
   dsing[j] = s;
 }
 
@@ -647,6 +635,53 @@ __global__ void k_reset_packet(Packet* pk, int which) {
 
 
 
+// sing_ptr[j] = first singleton prototype with column >= j (singletons sorted by column)
+__global__ void k_sing_ptr(const int32_t* __restrict__ sing_col, int64_t pz, int64_t n,
+                           int32_t* __restrict__ ptr) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j > n) return;
+  int64_t lo = 0, hi = pz;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (sing_col[mid] < j) lo = mid + 1;
+    else hi = mid;
+  }
+  ptr[j] = (int32_t)lo;
+}
+
+// any H(i, j) != H(j, i) -> *bad = 1 (once per load: picks the column-dot form of H x)
+__global__ void k_sym_check(const double* __restrict__ H, int64_t n, unsigned* bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    if (i > j && H[i + j * n] != H[j + i * n]) atomicOr(bad, 1u);
+  }
+}
+
+// y = H x for a symmetric H as column dots (H' x): one warp per column, contiguous 16-byte
+// loads when n is even, fixed-order warp sum
+__global__ void __launch_bounds__(256) k_hcol_gemv(const double* __restrict__ H, int64_t n,
+                                                   const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x * 8ll + (threadIdx.x >> 5);
+  if (j >= n) return;
+  const double* col = H + j * n;
+  double s0 = 0.0, s1 = 0.0;
+  if ((n & 1) == 0) {
+    const double2* c2 = reinterpret_cast<const double2*>(col);
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    for (int64_t i = lane; i < n / 2; i += 32) {
+      const double2 a = c2[i], b = x2[i];
+      s0 = fma(a.x, b.x, s0);
+      s1 = fma(a.y, b.y, s1);
+    }
+  } else {
+    for (int64_t i = lane; i < n; i += 32) s0 = fma(col[i], x[i], s0);
+  }
+  const double s = warp_sum(s0 + s1);
+  if (lane == 0) y[j] = s;
+}
+
 }  // namespace
 
 void vec_alloc(Ctx& c) {
@@ -679,6 +714,20 @@ void vec_alloc(Ctx& c) {
     k_absmax<<<(unsigned)std::min<int64_t>(64, ceil_div(c.n, 256)), 256, 0, c.stream>>>(c.h, c.n, c.hmax);
     CMPC_LAUNCHED();
   }
+  c.sing_ptr = dev_alloc<int32_t>((size_t)n + 1, c.stream);
+  k_sing_ptr<<<(unsigned)ceil_div((int64_t)n + 1, 256), 256, 0, c.stream>>>(c.sing_col, c.pz, c.n, c.sing_ptr);
+  CMPC_LAUNCHED();
+  c.h_symmetric = false;
+  if (c.n > 0) {
+    unsigned* bad = dev_zeros<unsigned>(1, c.stream);
+    k_sym_check<<<(unsigned)std::min<int64_t>(592, ceil_div(c.n * c.n, 256)), 256, 0, c.stream>>>(c.H, c.n, bad);
+    CMPC_LAUNCHED();
+    unsigned hb = 1;
+    CMPC_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, c.stream));
+    CMPC_CUDA(cudaStreamSynchronize(c.stream));
+    dev_free(bad, c.stream);
+    c.h_symmetric = hb == 0;
+  }
 }
 
 void vec_free(Ctx& c) {
@@ -690,6 +739,8 @@ void vec_free(Ctx& c) {
                   (void*)c.hmax, (void*)c.pk, (void*)c.d_mu, (void*)c.d_alpha})
     dev_free(p, c.stream);
   if (c.pk_host) cudaFreeHost(c.pk_host);
+  dev_free(c.sing_ptr, c.stream);
+  c.sing_ptr = nullptr;
   dev_free(c.pub_dev, c.stream);
   c.pub_dev = nullptr;
   c.pk_map = nullptr;
@@ -732,7 +783,11 @@ void launch_zero_packet(Ctx& c) {
 
 void launch_Hx(Ctx& c, const double* x, double* out) {
   if (c.n == 0) return;
-  k_rows_gemv<<<(unsigned)ceil_div(c.n, 32), 256, 0, c.stream>>>(c.H, c.n, c.n, c.n, nullptr, x, out);
+  if (c.h_symmetric) {
+    k_hcol_gemv<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(c.H, c.n, x, out);
+  } else {
+    k_rows_gemv<<<(unsigned)ceil_div(c.n, 32), 256, 0, c.stream>>>(c.H, c.n, c.n, c.n, nullptr, x, out);
+  }
   CMPC_LAUNCHED();
 }
 
@@ -762,7 +817,7 @@ void launch_Jtq(Ctx& c, const double* q, double* out) {
     CMPC_LAUNCHED();
   }
   k_ptq_final<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(
-      c.colpart, c.ps > 0 ? c.colchunks : 0, c.n, c.sing_col, c.sing_val, c.pz, q + c.ldp, out);
+      c.colpart, c.ps > 0 ? c.colchunks : 0, c.n, c.sing_ptr, c.sing_val, q + c.ldp, out);
   CMPC_LAUNCHED();
 }
 
@@ -839,7 +894,7 @@ void launch_prepare_step(Ctx& c, const double* sigma_override) {
     k_proto_reduce<false, true><<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
         c.p, c.mem_ptr, c.mem_rows, c.sigma, c.Jpv, c.omega, c.q, c.ps, c.ldp, c.zero_k);
   CMPC_LAUNCHED();
-  k_dsing<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.sing_col, c.sing_val, c.pz,
+  k_dsing<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.sing_ptr, c.sing_val,
                                                               c.omega + c.ldp, c.dsing);
   CMPC_LAUNCHED();
 }
