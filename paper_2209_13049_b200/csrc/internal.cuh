@@ -104,7 +104,8 @@ struct Ctx {
   double* hmax = nullptr;
   double* d_mu = nullptr;    // barrier value on the device (kernels read it: graph-safe)
   double* d_alpha = nullptr; // accepted step lengths {alpha, alpha_z} on the device
-  double h_alpha[2] = {0.0, 0.0};
+  double* stage = nullptr;   // pinned ring for the host -> device scalars (mu, alpha): a copy from
+  int stage_i = 0;           // pageable memory is staged and synchronous, from pinned a plain DMA
   // CUDA graphs of the two per-iteration segments (captured on the second iteration)
   cudaStream_t stream2 = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;

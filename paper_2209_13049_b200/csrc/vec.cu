@@ -703,6 +703,8 @@ void vec_alloc(Ctx& c) {
   c.d_alpha = dev_zeros<double>(2, c.stream);
   c.pk = dev_zeros<Packet>(1, c.stream);
   CMPC_CUDA(cudaHostAlloc(&c.pk_host, sizeof(Packet) + 64, cudaHostAllocMapped));
+  CMPC_CUDA(cudaMallocHost(&c.stage, 64 * sizeof(double)));
+  c.stage_i = 0;
   CMPC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.pk_map), c.pk_host, 0));
   c.pub_host = reinterpret_cast<volatile unsigned long long*>(reinterpret_cast<char*>(c.pk_host) + sizeof(Packet));
   c.pub_map = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(c.pk_map) + sizeof(Packet));
@@ -739,6 +741,8 @@ void vec_free(Ctx& c) {
                   (void*)c.hmax, (void*)c.pk, (void*)c.d_mu, (void*)c.d_alpha})
     dev_free(p, c.stream);
   if (c.pk_host) cudaFreeHost(c.pk_host);
+  if (c.stage) cudaFreeHost(c.stage);
+  c.stage = nullptr;
   dev_free(c.sing_ptr, c.stream);
   c.sing_ptr = nullptr;
   dev_free(c.pub_dev, c.stream);
@@ -923,9 +927,19 @@ void launch_hmax(Ctx& c) {
   }
 }
 
+// a slot of the pinned staging ring (64 doubles, 2 per slot): the host loop synchronises
+// with the stream between segments, so a slot is never reused while its copy is pending
+double* stage_slot(Ctx& c, int) {
+  double* p = c.stage + 2 * (c.stage_i & 31);
+  ++c.stage_i;
+  return p;
+}
+
 void set_mu(Ctx& c, double mu) {
   c.mu = mu;
-  CMPC_CUDA(cudaMemcpyAsync(c.d_mu, &c.mu, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  double* st = stage_slot(c, 1);
+  st[0] = mu;
+  CMPC_CUDA(cudaMemcpyAsync(c.d_mu, st, sizeof(double), cudaMemcpyHostToDevice, c.stream));
 }
 
 void launch_recover(Ctx& c, double tau) {
@@ -1008,9 +1022,10 @@ void launch_init_state(Ctx& c, double mu) {
 }
 
 void set_alpha(Ctx& c, double alpha, double alpha_z) {
-  c.h_alpha[0] = alpha;
-  c.h_alpha[1] = alpha_z;
-  CMPC_CUDA(cudaMemcpyAsync(c.d_alpha, c.h_alpha, 2 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  double* st = stage_slot(c, 2);
+  st[0] = alpha;
+  st[1] = alpha_z;
+  CMPC_CUDA(cudaMemcpyAsync(c.d_alpha, st, 2 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
 }
 
 void launch_update_dev(Ctx& c) {
