@@ -13,6 +13,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <limits>
 #include <stdexcept>
@@ -244,6 +245,28 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     for (auto* x : {&hs, &hl, &hz, &h2, &h3, &hps, &hpl, &hpz}) x->resize(size_t(m));
   }
 
+  // CMPC_GAP_TRACE: device-timeline gaps between a segment's end and the next enqueue
+  const bool gap_trace = getenv("CMPC_GAP_TRACE") != nullptr;
+  cudaEvent_t g_end = nullptr, g_beg = nullptr;
+  double gap_ms = 0.0;
+  long gap_n = 0;
+  if (gap_trace) {
+    CMPC_CUDA(cudaEventCreate(&g_end));
+    CMPC_CUDA(cudaEventCreate(&g_beg));
+  }
+  auto gap_mark_end = [&] {
+    if (gap_trace) CMPC_CUDA(cudaEventRecord(g_end, c.stream));
+  };
+  auto gap_mark_begin = [&] {
+    if (!gap_trace) return;
+    CMPC_CUDA(cudaEventRecord(g_beg, c.stream));
+    CMPC_CUDA(cudaEventSynchronize(g_beg));
+    float ms = 0.f;
+    CMPC_CUDA(cudaEventElapsedTime(&ms, g_end, g_beg));
+    gap_ms += ms;
+    ++gap_n;
+  };
+  gap_mark_end();
   while (true) {
     // check_termination (ipm.cpp:153-158)
     if (A.kkt <= tol && c.mu <= tol) {
@@ -263,7 +286,9 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     // sigma, condensed matrix, factorization with the shift ladder (ipm.cpp:200-226), then
     // speculatively: directions, recovery, fraction to boundary, line-search trial 0
     size_t shift = 0;
+    gap_mark_begin();
     run_segment(c, c.g_step, c.g_step_nodes, iter >= 1, [&] { seg_step(c, tau); });
+    gap_mark_end();
     wait_published(c, c.pub_expect, &syncs);
     float ms = 0.f;
     CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
@@ -323,7 +348,9 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     const double mu_used = c.mu;
     set_alpha(c, alpha, alpha_z);
     iter += 1;
+    gap_mark_begin();
     run_segment(c, c.g_next, c.g_next_nodes, iter >= 2, [&] { seg_next(c); });
+    gap_mark_end();
     wait_published(c, c.pub_expect, &syncs);
     A = *c.pk_host;
     if (log) {
@@ -332,6 +359,12 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     }
   }
 
+  if (gap_trace) {
+    fprintf(stderr, "[cmpc gaps] %ld host turnarounds, %.1f us average\n", gap_n,
+            gap_n ? gap_ms * 1e3 / gap_n : 0.0);
+    cudaEventDestroy(g_end);
+    cudaEventDestroy(g_beg);
+  }
   if (v_out && n > 0) CMPC_CUDA(cudaMemcpyAsync(v_out, c.v, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
   if (m > 0) {
     if (s_out) CMPC_CUDA(cudaMemcpyAsync(s_out, c.s, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
