@@ -50,10 +50,22 @@ int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out);
  * scal_out: count x 13 (cmpc_solve's out_scalars per instance). */
 int cmpc_solve_batch(cmpc_ctx** ctxs, int64_t count, const double* opts, int64_t max_iter,
                      double* v_out, double* scal_out, int threads);
+/* Solve `count` instances sharing H and J (config 5): h_all count x n, h0_all count,
+ * d_all count x m (host, row per instance); `nctx` loaded worker contexts (clones of one
+ * analysed QP), one host thread each, take instances in turn. v_out / scal_out as above. */
+int cmpc_solve_batch_affine(cmpc_ctx** ctxs, int nctx, int64_t count, const double* h_all,
+                            const double* h0_all, const double* d_all, const double* opts,
+                            int64_t max_iter, double* v_out, double* scal_out);
+/* Page-lock / release a host buffer (cudaHostRegister) used for repeated uploads */
+int cmpc_host_register(void* p, int64_t bytes);
+int cmpc_host_unregister(void* p);
 /* out[8] = n, m, prototypes, SYRK prototypes, singleton prototypes, SYRK work units,
  * algorithmic SYRK flops per condensation (sum over prototypes of hi (hi + 1)),
  * algorithmic bytes of one pass over P (8 x nonzeros) */
 int cmpc_qp_info(cmpc_ctx* ctx, int64_t* out);
+/* Diagnostics: run the condensation once and record a per-CTA timeline; out (cap x 4):
+ * {start us, end us, SM id, planned weighted k-steps}; *nctas = CTAs of the launch */
+int cmpc_debug_syrk_timeline(cmpc_ctx* ctx, double* out, int64_t cap, int64_t* nctas);
 /* Replace h, h0, d of a loaded QP (refresh_initial_state, proj/src/reduction.cpp:270-280) */
 int cmpc_update_qp_affine(cmpc_ctx* ctx, const double* h, double h0, const double* d, int on_device);
 

@@ -31,6 +31,7 @@ SIGNATURES = {
     "cmpc_ctx_destroy": (None, [C.c_void_p]),
     "cmpc_load_qp": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, D, D, C.c_double, D, D, C.c_int]),
     "cmpc_qp_info": (C.c_int, [C.c_void_p, I64]),
+    "cmpc_debug_syrk_timeline": (C.c_int, [C.c_void_p, D, C.c_int64, I64]),
     "cmpc_update_qp_affine": (C.c_int, [C.c_void_p, D, C.c_double, D, C.c_int]),
     "cmpc_set_state": (C.c_int, [C.c_void_p, D, D, D, D, C.c_double]),
     "cmpc_get_state": (C.c_int, [C.c_void_p, D, D, D, D]),
@@ -55,6 +56,10 @@ SIGNATURES = {
     "cmpc_time_phase": (C.c_int, [C.c_void_p, C.c_int, C.c_int, D]),
     "cmpc_ctx_clone": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "cmpc_solve_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int64, D, C.c_int64, D, D, C.c_int]),
+    "cmpc_host_register": (C.c_int, [C.c_void_p, C.c_int64]),
+    "cmpc_host_unregister": (C.c_int, [C.c_void_p]),
+    "cmpc_solve_batch_affine": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, D, D, D, D,
+                                          C.c_int64, D, D]),
     "cmpc_comm_unique_id": (C.c_int, [C.c_void_p]),
     "cmpc_ctx_attach_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int64]),
     "cmpc_ctx_detach_comm": (C.c_int, [C.c_void_p]),

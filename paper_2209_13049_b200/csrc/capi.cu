@@ -1,6 +1,9 @@
 // C ABI (include/condmpc_cuda.h): context lifecycle, QP upload, per-step entry points and
 // the stand-alone linear algebra of the reference's plug point.
 #include <atomic>
+#include <csignal>
+#include <execinfo.h>
+#include <unistd.h>
 #include <chrono>
 #include <thread>
 #include <cstdio>
@@ -93,6 +96,22 @@ void require_loaded(Ctx& c) {
 
 }  // namespace
 
+// Diagnostics: CMPC_SEGV_TRACE=1 prints the native stack on SIGSEGV (addr2line-able offsets)
+namespace {
+void segv_trace(int sig) {
+  void* frames[64];
+  const int k = backtrace(frames, 64);
+  backtrace_symbols_fd(frames, k, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+struct SegvInstall {
+  SegvInstall() {
+    if (getenv("CMPC_SEGV_TRACE")) signal(SIGSEGV, segv_trace);
+  }
+} g_segv_install;
+}  // namespace
+
 extern "C" {
 
 int cmpc_abi_version(void) { return 1; }
@@ -143,6 +162,7 @@ void cmpc_ctx_destroy(cmpc_ctx* x) {
 int cmpc_load_qp(cmpc_ctx* x, int64_t n, int64_t m, const double* H, const double* h, double h0,
                  const double* J, const double* d, int on_device) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     if (n < 0 || m < 0) throw DimError("negative dimensions");
     if (m > (int64_t(1) << 29) || n > (int64_t(1) << 24)) throw DimError("QP too large");
@@ -190,6 +210,10 @@ int cmpc_load_qp(cmpc_ctx* x, int64_t n, int64_t m, const double* H, const doubl
 }
 
 int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
+  if (!src || !out) {
+    g_error = "cmpc_ctx_clone: null context";
+    return CMPC_ERR_ARG;
+  }
   cmpc_ctx* x = nullptr;
   int rc = cmpc_ctx_create(&x, src->c.device);
   if (rc) return rc;
@@ -274,6 +298,65 @@ int cmpc_solve_batch(cmpc_ctx** ctxs, int64_t count, const double* opts, int64_t
   return err.load();
 }
 
+// A batch of `count` instances that share H and J and differ in (h, h0, d) (config 5,
+// refresh_initial_state), solved by `nctx` worker contexts cloned from one analysed QP:
+// worker w drives ctxs[w] on its own host thread and takes instances from a shared counter;
+// per instance it uploads (h, h0, d) into its context (the captured iteration graphs keep
+// pointing at the same buffers) and runs the host loop. Memory and setup cost scale with
+// the number of workers, not with the batch.
+int cmpc_solve_batch_affine(cmpc_ctx** ctxs, int nctx, int64_t count, const double* h_all,
+                            const double* h0_all, const double* d_all, const double* opts,
+                            int64_t max_iter, double* v_out, double* scal_out) {
+  if (count <= 0 || nctx <= 0) return CMPC_OK;
+  std::atomic<int64_t> next{0};
+  std::atomic<int> err{0};
+  std::string first_error;
+  std::atomic<bool> have_error{false};
+  auto worker = [&](int w) {
+    Ctx& c = ctxs[w]->c;
+    for (;;) {
+      const int64_t i = next.fetch_add(1);
+      if (i >= count || err.load() != 0) break;
+      const int rc = guard([&] {
+        CMPC_CUDA(cudaSetDevice(c.device));
+        require_loaded(c);
+        if (c.n > 0)
+          CMPC_CUDA(cudaMemcpyAsync(c.h, h_all + i * c.n, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
+        if (c.m > 0)
+          CMPC_CUDA(cudaMemcpyAsync(c.d, d_all + i * c.m, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
+        c.h0 = h0_all[i];
+        launch_hmax(c);
+        return solve_loop(c, opts, max_iter, v_out ? v_out + i * c.n : nullptr, nullptr, nullptr,
+                          nullptr, scal_out + i * 13, nullptr, nullptr, nullptr);
+      });
+      if (rc < 0 && !have_error.exchange(true)) {
+        first_error = g_error;
+        err.store(rc);
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nctx; ++t) pool.emplace_back(worker, t);
+  worker(0);
+  for (auto& th : pool) th.join();
+  if (err.load() != 0) g_error = first_error;
+  return err.load();
+}
+
+// Page-lock a host buffer for the batch uploads (plain DMA instead of staged copies)
+int cmpc_host_register(void* p, int64_t bytes) {
+  return guard([&] {
+    if (p && bytes > 0) CMPC_CUDA(cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault));
+    return CMPC_OK;
+  });
+}
+int cmpc_host_unregister(void* p) {
+  return guard([&] {
+    if (p) CMPC_CUDA(cudaHostUnregister(p));
+    return CMPC_OK;
+  });
+}
+
 int cmpc_qp_info(cmpc_ctx* x, int64_t* out) {
   const Ctx& c = x->c;
   out[0] = c.n;
@@ -297,6 +380,7 @@ int cmpc_comm_unique_id(void* id128) {
 
 int cmpc_ctx_attach_comm(cmpc_ctx* x, const void* id128, int nranks, int rank, int64_t m_total) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     if (!id128 || nranks < 1 || rank < 0 || rank >= nranks) throw DimError("bad communicator arguments");
@@ -311,6 +395,7 @@ int cmpc_ctx_attach_comm(cmpc_ctx* x, const void* id128, int nranks, int rank, i
 
 int cmpc_ctx_detach_comm(cmpc_ctx* x) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     drop_graphs(c);
     comm_detach(c);
@@ -321,6 +406,7 @@ int cmpc_ctx_detach_comm(cmpc_ctx* x) {
 
 int cmpc_time_phase(cmpc_ctx* x, int what, int reps, double* ms_per_rep) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     if (reps < 1) throw DimError("reps must be positive");
@@ -352,8 +438,39 @@ int cmpc_time_phase(cmpc_ctx* x, int what, int reps, double* ms_per_rep) {
   });
 }
 
+// Debug: run the condensation once with a per-piece timeline. out: 8 doubles per piece
+// {start us, end us (from the first start), smid, segments, k-steps of the full off-diagonal,
+// thin off-diagonal, full diagonal and thin diagonal segments}
+int cmpc_debug_syrk_timeline(cmpc_ctx* x, double* out, int64_t cap, int64_t* nctas) {
+  return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
+    Ctx& c = x->c;
+    require_loaded(c);
+    const int nb = c.npieces;
+    long long* buf = dev_alloc<long long>(size_t(3 * std::max(nb, 1)), c.stream);
+    c.syrk_prof = buf;
+    launch_condense(c, false);
+    c.syrk_prof = nullptr;
+    std::vector<long long> h(size_t(3 * std::max(nb, 1)));
+    CMPC_CUDA(cudaMemcpyAsync(h.data(), buf, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, c.stream));
+    CMPC_CUDA(cudaStreamSynchronize(c.stream));
+    dev_free(buf, c.stream);
+    long long t0 = h.empty() ? 0 : h[0];
+    for (int b = 0; b < nb; ++b) t0 = std::min(t0, h[size_t(3 * b)]);
+    for (int b = 0; b < nb && b < cap; ++b) {
+      out[8 * b] = (h[size_t(3 * b)] - t0) * 1e-3;
+      out[8 * b + 1] = (h[size_t(3 * b + 1)] - t0) * 1e-3;
+      out[8 * b + 2] = double(h[size_t(3 * b + 2)]);
+      for (int q = 0; q < 5; ++q) out[8 * b + 3 + q] = c.syrk_cta_cost[size_t(5 * b + q)];
+    }
+    *nctas = nb;
+    return CMPC_OK;
+  });
+}
+
 int cmpc_update_qp_affine(cmpc_ctx* x, const double* h, double h0, const double* d, int on_device) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -369,6 +486,7 @@ int cmpc_update_qp_affine(cmpc_ctx* x, const double* h, double h0, const double*
 int cmpc_set_state(cmpc_ctx* x, const double* v, const double* s, const double* lam,
                    const double* z, double mu) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     h2d(c, c.v, v, c.n);
@@ -383,6 +501,7 @@ int cmpc_set_state(cmpc_ctx* x, const double* v, const double* s, const double* 
 
 int cmpc_get_state(cmpc_ctx* x, double* v, double* s, double* lam, double* z) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     d2h(c, v, c.v, c.n);
@@ -396,6 +515,7 @@ int cmpc_get_state(cmpc_ctx* x, double* v, double* s, double* lam, double* z) {
 
 int cmpc_compute_residuals(cmpc_ctx* x, double* r1, double* r2, double* r3, double* kkt) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     launch_residuals(c);
@@ -410,6 +530,7 @@ int cmpc_compute_residuals(cmpc_ctx* x, double* r1, double* r2, double* r3, doub
 
 int cmpc_set_residuals(cmpc_ctx* x, const double* r1, const double* r2, const double* r3) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     h2d(c, c.r1, r1, c.n);
@@ -422,6 +543,7 @@ int cmpc_set_residuals(cmpc_ctx* x, const double* r1, const double* r2, const do
 
 int cmpc_assemble_condensed(cmpc_ctx* x, const double* sigma, double* M) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     if (sigma && c.m > 0) h2d(c, c.sigma, sigma, c.m);
@@ -436,6 +558,7 @@ int cmpc_assemble_condensed(cmpc_ctx* x, const double* sigma, double* M) {
 
 int cmpc_factorize_condensed(cmpc_ctx* x, double delta, int64_t* pivot) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     launch_cholesky(c, c.M, c.L, delta);
@@ -452,6 +575,7 @@ int cmpc_factorize_condensed(cmpc_ctx* x, double delta, int64_t* pivot) {
 
 int cmpc_get_factor(cmpc_ctx* x, double* L) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     d2h(c, L, c.L, c.n * c.n);
@@ -462,6 +586,7 @@ int cmpc_get_factor(cmpc_ctx* x, double* L) {
 
 int cmpc_set_factor(cmpc_ctx* x, const double* L) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     h2d(c, c.L, L, c.n * c.n);
@@ -474,6 +599,7 @@ int cmpc_set_factor(cmpc_ctx* x, const double* L) {
 int cmpc_step_directions(cmpc_ctx* x, double tau, double* pv, double* ps, double* pl, double* pz,
                          double* alpha) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     if (!(tau > 0.0 && tau < 1.0)) throw DimError("tau must lie in (0,1)");
@@ -499,6 +625,7 @@ int cmpc_step_directions(cmpc_ctx* x, double tau, double* pv, double* ps, double
 int cmpc_set_directions(cmpc_ctx* x, const double* pv, const double* ps, const double* pl,
                         const double* pz) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     h2d(c, c.pv, pv, c.n);
@@ -512,6 +639,7 @@ int cmpc_set_directions(cmpc_ctx* x, const double* pv, const double* ps, const d
 
 int cmpc_line_search(cmpc_ctx* x, double alpha_max, double eta, double* alpha, int* trial) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     if (!(alpha_max > 0.0 && alpha_max <= 1.0)) throw DimError("alpha_max must lie in (0,1]");
@@ -527,6 +655,7 @@ int cmpc_line_search(cmpc_ctx* x, double alpha_max, double eta, double* alpha, i
 
 int cmpc_merit(cmpc_ctx* x, double alpha, double rho, double* phi) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     launch_trial(c, alpha, false);
@@ -539,6 +668,7 @@ int cmpc_merit(cmpc_ctx* x, double alpha, double rho, double* phi) {
 
 int cmpc_apply_step(cmpc_ctx* x, double alpha, double alpha_z) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     launch_update(c, alpha, alpha_z);
@@ -549,6 +679,7 @@ int cmpc_apply_step(cmpc_ctx* x, double alpha, double alpha_z) {
 
 int cmpc_dense_objective(cmpc_ctx* x, double* obj) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     launch_residuals(c);
@@ -562,6 +693,7 @@ int cmpc_solve(cmpc_ctx* x, const double* opts, int64_t max_iter, double* v, dou
                double* lam, double* z, double* out, cmpc_log_fn log, cmpc_inspect_fn inspect,
                void* user) {
   return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
     require_loaded(c);
     CMPC_CUDA(cudaSetDevice(c.device));

@@ -82,14 +82,19 @@ struct Ctx {
   bool h_symmetric = false;      // H == H' bitwise: H x as column dots
   std::vector<int32_t> h_start_col;
 
-  // SYRK work decomposition
-  int nunits = 0, ntiles = 0;
-  int4* units = nullptr;          // {tile_i, tile_j, k0, k1} in execution (k-major) order
-  int32_t* tile_ptr = nullptr;    // ntiles+1 into tile_units
-  int32_t* tile_units = nullptr;  // unit ids per tile in k order
+  // SYRK work decomposition (syrk.cu): segments (a k range of one tile) grouped in pieces
+  int nunits = 0, ntiles = 0, nctas = 0, npieces = 0;
+  int4* units = nullptr;          // segments {tile_i | tile_j << 10 | thin << 20, k0, k1, tile}
+  int32_t* cta_ptr = nullptr;     // npieces+1 into units
+  unsigned* syrk_ctl = nullptr;   // piece counter, retired CTAs, reduction item counter, per-tile done counts
   int2* tiles = nullptr;          // ntiles {ti, tj}
+  int32_t* tile_ptr = nullptr;    // ntiles+1 into tile_units
+  int32_t* tile_units = nullptr;  // segment ids per tile in k order (| 1 << 31: thin, rows 0..31 only)
   double* partial = nullptr;      // nunits x 64 x 64
-  void* tmap_P = nullptr;         // CUtensorMap (128 B), host copy passed by value
+  long long* syrk_prof = nullptr; // debug timeline: {start ns, end ns, smid} per piece (null: off)
+  std::vector<double> syrk_cta_cost;  // per piece: segments, k steps per shape (debug timeline)
+  void* tmap_P = nullptr;         // CUtensorMap (128 B), host copy passed by value: box {16, 64}
+  void* tmap_P32 = nullptr;       // the same over box {16, 32} (thin units' A operand)
 
   // iterate and per-iteration buffers (device)
   double *v = nullptr, *s = nullptr, *lam = nullptr, *z = nullptr, *r1 = nullptr, *r2 = nullptr,

@@ -12,6 +12,7 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -37,6 +38,9 @@ void require(bool c, const char* m) {
 void wait_published(Ctx& c, unsigned long long seq, long long* syncs) {
   for (long spins = 0;; ++spins) {
     if (*c.pub_host >= seq) break;
+    // after the first microseconds, give the core back now and then: with as many solving
+    // threads as cores (batch mode) a pure spin starves the driver's own threads
+    if (spins > 4096) std::this_thread::yield();
     if ((spins & 0xfff) == 0xfff) {
       const cudaError_t e = cudaStreamQuery(c.stream);
       if (e != cudaSuccess && e != cudaErrorNotReady) CMPC_CUDA(e);

@@ -9,17 +9,22 @@
 //   3-stage mbarrier pipeline fed by one producer warp; omega rides the same barrier as a
 //   1-D bulk copy; the diagonal weight is applied to the B fragment in registers, so a
 //   diagonal tile loads its operand once.
-// * math: mma.sync m16n8k16 f64 (DMMA.8x8x4), 4 consumer warps x (32x32) per 64x64 tile.
+// * math: mma.sync m16n8k16 f64 (DMMA.8x8x4), 4 consumer warps per 64x64 tile, each owning
+//   an equal share of the tile's useful 16x8 fragments.
 // * zero-block skipping: rows are sorted by nonzero prefix width; tile (I,J) (I>=J) only
-//   visits the rows whose prefix reaches column 64*I.
-// * split-K: (tile, k-chunk) work units with globally aligned chunks so concurrently
-//   running units share P rows in L2; partial tiles are summed in a fixed order by
-//   k_syrk_reduce (bitwise deterministic run to run).
+//   visits the rows whose prefix reaches column 64*I, and the rows whose prefix ends in the
+//   first half of block I run as THIN segments (output rows 0..31 only, A operand 32
+//   columns): the executed DMMA work is 1.22x the algorithmic count at config 3, not 1.35x.
+// * scheduling: one persistent CTA pair per SM grabs PIECES from an atomic counter: first one
+//   equal-cost body piece each, then tail pieces of decreasing cost so the CTAs finish
+//   together; a piece holds one or more SEGMENTS (a k range of one tile).
+// * reduction: every segment stores a partial tile; k_syrk_reduce sums a tile's partials in
+//   the plan's k order and adds H and the singleton diagonal (M bitwise reproducible).
 #include <cuda.h>
 
 #include <algorithm>
-#include <functional>
-#include <queue>
+#include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -33,9 +38,22 @@ constexpr int kStages = 3;
 constexpr int kBoxBytes = 16 * 64 * 8;          // {16 k, 64 cols} FP64 box
 constexpr int kOpBytes = 2 * kBoxBytes;         // 32 k x 64 cols
 constexpr int kStageBytes = 2 * kOpBytes + 1024;  // A, B, omega (256 B, padded to 1 KB)
-constexpr int kSyrkSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kSyrkSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers, ring*/;
 constexpr int kConsumerWarps = 4;
-constexpr int kSyrkThreads = (kConsumerWarps + 1) * 32;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kSyrkThreads = kConsumers + 32;
+// relative cost of one k step per segment shape (measured: tools/syrk_timeline.py, C3)
+constexpr double kCostFull = 1.0, kCostThin = 0.6, kCostDiag = 0.85, kCostDiagThin = 0.35;
+
+struct SyrkArgs {
+  const double* omega;
+  const int4* segs;          // {ti | tj << 10 | thin << 20, k0, k1, tile index}
+  const int32_t* piece_ptr;  // npieces + 1 into segs
+  int npieces;
+  unsigned* ctl;             // [0] next piece, [1] retired CTAs (both 0 between launches)
+  double* partial;           // per segment: 64 x 64 column-major partial tile
+  long long* prof;           // debug: per piece {start ns, end ns, smid}
+};
 
 // byte offset of element (col c, k) inside a 32 x 64 operand tile (two swizzled boxes)
 __device__ __forceinline__ uint32_t op_off(int c, int k) {
@@ -43,19 +61,123 @@ __device__ __forceinline__ uint32_t op_off(int c, int k) {
   return (uint32_t)((k >> 4) * kBoxBytes + c * 128 + ((((kk >> 1) ^ (c & 7)) << 4) | ((kk & 1) << 3)));
 }
 
+// Segment epilogue: store the accumulators as the segment's partial tile.
+template <int NF>
+__device__ __forceinline__ void store_partial(const SyrkArgs& a, int sg,
+                                              const double (&acc)[NF][2][4], const int* fr,
+                                              const int* fn, int lane) {
+  double* out = a.partial + (size_t)sg * (kTile * kTile);
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int r = 32 * fr[f] + 16 * mi + g;
+      const int c = 8 * fn[f] + 2 * t;
+      __stcg(out + c * kTile + r, acc[f][mi][0]);
+      __stcg(out + (c + 1) * kTile + r, acc[f][mi][1]);
+      __stcg(out + c * kTile + r + 8, acc[f][mi][2]);
+      __stcg(out + (c + 1) * kTile + r + 8, acc[f][mi][3]);
+    }
+}
+
+// Consumer work of one segment. Each segment covers a k range of one 64x64 output tile in
+// one of four shapes; the 4 consumer warps split the useful 8-column fragments evenly:
+//   FULL (off-diagonal): 2 x 8 fragments (row halves r = 0,1) -> 4 per warp
+//   THIN (off-diagonal): rows 0..31 only                      -> 2 per warp
+//   FULL (diagonal):     the 12 fragments on or below the diagonal 32x32 blocks -> 3 per warp
+//   THIN (diagonal):     the lower-left 32x32 block           -> 1 per warp
+template <int NF, bool DIAG, bool THIN>
+__device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* smem, uint64_t* full,
+                                             uint64_t* empty, int it0, int sg, const int4 u,
+                                             int warp, int lane) {
+  const int nsteps = (u.z - u.y) / kBK;
+  const int g = lane >> 2, t = lane & 3;
+  // fragment i covers output rows 32*r(i).. and columns 8*fn(i)..; MIXED: the one diagonal
+  // warp whose fragments straddle both row halves (fragment 0 in half 0, the rest in half 1)
+  const bool mixed = DIAG && !THIN && warp == 1;
+  int r0, fn0;
+  if (DIAG && !THIN) {
+    r0 = warp >= 2 ? 1 : 0;
+    fn0 = warp == 0 ? 0 : warp == 1 ? 3 : warp == 2 ? 2 : 5;
+  } else if (THIN) {
+    r0 = 0;
+    fn0 = NF * warp;
+  } else {
+    r0 = warp & 1;
+    fn0 = 4 * (warp >> 1);
+  }
+  int fr[NF], fn[NF];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) {
+    fr[i] = mixed ? (i == 0 ? 0 : 1) : r0;
+    fn[i] = mixed ? (i == 0 ? 3 : i - 1) : fn0 + i;
+  }
+
+  double acc[NF][2][4];
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[f][b][c] = 0.0;
+
+  for (int it = it0; it < it0 + nsteps; ++it) {
+    const int s = it % kStages;
+    mbar_wait(&full[s], (it / kStages) & 1);
+    // explicit 32-bit shared addresses: the aligned generic pointer would compile to LD
+    // (global-load scoreboard latency) instead of LDS
+    const uint32_t sA = smem_u32(smem + s * kStageBytes);
+    const uint32_t sB = DIAG ? sA : sA + kOpBytes;
+    const uint32_t sW = sA + 2 * kOpBytes;
+#pragma unroll
+    for (int ks = 0; ks < kBK; ks += 16) {
+      double af[2][8], ax[2][8];  // A fragments of half r0 (ax: half 0 for the mixed warp)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const int c = 16 * mi + g + 8 * (x & 1);
+          const int k = ks + t + 4 * (x >> 1);
+          af[mi][x] = lds64(sA + op_off(32 * (mixed ? 1 : r0) + c, k));
+          if (DIAG && !THIN) {
+            if (mixed) ax[mi][x] = lds64(sA + op_off(c, k));
+          }
+        }
+      double w[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) w[x] = lds64(sW + 8 * (ks + t + 4 * x));
+#pragma unroll
+      for (int i = 0; i < NF; ++i) {
+        double bf[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) bf[x] = w[x] * lds64(sB + op_off(8 * fn[i] + g, ks + t + 4 * x));
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          if (DIAG && !THIN && i == 0 && mixed) dmma16816(acc[i][mi], ax[mi], bf);
+          else dmma16816(acc[i][mi], af[mi], bf);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  store_partial<NF>(a, sg, acc, fr, fn, lane);
+}
+
+// 2 CTAs per SM: 168 registers (each SM sub-partition holds 3 warps of 168 x 32; the few
+// spilled values live outside the k loops)
 __global__ void __launch_bounds__(kSyrkThreads, 2)
-    k_syrk(const __grid_constant__ CUtensorMap tmP, const double* __restrict__ omega,
-           const int4* __restrict__ units, double* __restrict__ partial) {
+    k_syrk(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP32,
+           const SyrkArgs a) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-
-  const int4 u = units[blockIdx.x];
-  const int ti = u.x, tj = u.y, k0 = u.z, k1 = u.w;
-  const bool diag = ti == tj;
-  const int nsteps = (k1 - k0) / kBK;
+  uint64_t* pfull = empty + kStages;  // piece ring: producer -> consumers
+  uint64_t* pempty = pfull + 2;
+  volatile int* ring = reinterpret_cast<volatile int*>(pempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -63,119 +185,128 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&pfull[s], 1);
+      mbar_init(&pempty[s], kConsumerWarps);
+    }
     fence_barrier_init();
   }
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    // ---------------- producer
+    // ---------------- producer: grab pieces, stream their segments' stages
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(diag ? kOpBytes : 2 * kOpBytes) + kBK * 8;
-      for (int it = 0; it < nsteps; ++it) {
-        const int s = it % kStages;
-        if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-        unsigned char* st = smem + s * kStageBytes;
-        const int kk = k0 + it * kBK;
-        mbar_expect_tx(&full[s], bytes);
-        tma_load_2d(st, &tmP, kk, 64 * ti, &full[s]);
-        tma_load_2d(st + kBoxBytes, &tmP, kk + 16, 64 * ti, &full[s]);
-        if (!diag) {
-          tma_load_2d(st + kOpBytes, &tmP, kk, 64 * tj, &full[s]);
-          tma_load_2d(st + kOpBytes + kBoxBytes, &tmP, kk + 16, 64 * tj, &full[s]);
+      int it = 0;
+      for (int i = 0;; ++i) {
+        const int slot = i & 1;
+        if (i >= 2) mbar_wait(&pempty[slot], ((i >> 1) & 1) ^ 1);
+        int p = (int)atomicAdd(a.ctl, 1u);
+        if (p >= a.npieces) p = -1;
+        ring[slot] = p;
+        mbar_arrive(&pfull[slot]);
+        if (p < 0) break;
+        for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
+          const int4 u = a.segs[sg];
+          const int ti = u.x & 1023, tj = (u.x >> 10) & 1023;
+          const bool thin = (u.x >> 20) & 1, diag = ti == tj;
+          const uint32_t abytes = thin ? kOpBytes / 2 : kOpBytes;
+          const uint32_t bytes = abytes + (diag ? 0u : (uint32_t)kOpBytes) + kBK * 8;
+          const void* tmA = thin ? (const void*)&tmP32 : (const void*)&tmP;
+          for (int kk = u.y; kk < u.z; kk += kBK, ++it) {
+            const int s = it % kStages;
+            if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+            unsigned char* st = smem + s * kStageBytes;
+            mbar_expect_tx(&full[s], bytes);
+            // a 32-column box lands exactly where the first 32 columns of a 64-column box would
+            tma_load_2d(st, tmA, kk, 64 * ti, &full[s]);
+            tma_load_2d(st + kBoxBytes, tmA, kk + 16, 64 * ti, &full[s]);
+            if (!diag) {
+              tma_load_2d(st + kOpBytes, &tmP, kk, 64 * tj, &full[s]);
+              tma_load_2d(st + kOpBytes + kBoxBytes, &tmP, kk + 16, 64 * tj, &full[s]);
+            }
+            bulk_load(st + 2 * kOpBytes, a.omega + kk, kBK * 8, &full[s]);
+          }
         }
-        bulk_load(st + 2 * kOpBytes, omega + kk, kBK * 8, &full[s]);
       }
     }
     return;
   }
 
-  // ---------------- consumers: warp (wm, wn) owns rows 32*wm.., cols 32*wn.. of the tile
-  const int wm = warp & 1, wn = warp >> 1;
-  const bool skip = diag && wm == 0 && wn == 1;  // strictly upper block of a diagonal tile
-  const int g = lane >> 2, t = lane & 3;
-  double acc[2][4][4];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
-
-  for (int it = 0; it < nsteps; ++it) {
-    const int s = it % kStages;
-    mbar_wait(&full[s], (it / kStages) & 1);
-    if (!skip) {
-      // explicit 32-bit shared addresses: the aligned generic pointer would compile to LD
-      // (global-load scoreboard latency) instead of LDS
-      const uint32_t sA = smem_u32(smem + s * kStageBytes);
-      const uint32_t sB = diag ? sA : sA + kOpBytes;
-      const uint32_t sW = sA + 2 * kOpBytes;
-#pragma unroll
-      for (int ks = 0; ks < kBK; ks += 16) {
-        double af[2][8], bf[4][4];
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-#pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            const int c = 32 * wm + 16 * mi + g + 8 * (x & 1);
-            const int k = ks + t + 4 * (x >> 1);
-            af[mi][x] = lds64(sA + op_off(c, k));
-          }
-        }
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            const int c = 32 * wn + 8 * ni + g;
-            const int k = ks + t + 4 * x;
-            bf[ni][x] = lds64(sW + 8 * k) * lds64(sB + op_off(c, k));
-          }
-        }
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma16816(acc[mi][ni], af[mi], bf[ni]);
-      }
-    }
+  // ---------------- consumers
+  int it0 = 0;
+  for (int i = 0;; ++i) {
+    const int slot = i & 1;
+    mbar_wait(&pfull[slot], (i >> 1) & 1);
+    const int p = ring[slot];
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-  if (skip) return;
-  double* out = partial + (size_t)blockIdx.x * (kTile * kTile);
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int r = 32 * wm + 16 * mi + g;
-      const int c = 32 * wn + 8 * ni + 2 * t;
-      out[c * kTile + r] = acc[mi][ni][0];
-      out[(c + 1) * kTile + r] = acc[mi][ni][1];
-      out[c * kTile + r + 8] = acc[mi][ni][2];
-      out[(c + 1) * kTile + r + 8] = acc[mi][ni][3];
+    if (lane == 0) mbar_arrive(&pempty[slot]);
+    if (p < 0) break;
+    long long t_start = 0;
+    if (a.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
+      const int4 u = a.segs[sg];
+      const bool thin = (u.x >> 20) & 1, diag = (u.x & 1023) == ((u.x >> 10) & 1023);
+      if (diag) {
+        if (thin) syrk_segment<1, true, true>(a, smem, full, empty, it0, sg, u, warp, lane);
+        else syrk_segment<3, true, false>(a, smem, full, empty, it0, sg, u, warp, lane);
+      } else {
+        if (thin) syrk_segment<2, false, true>(a, smem, full, empty, it0, sg, u, warp, lane);
+        else syrk_segment<4, false, false>(a, smem, full, empty, it0, sg, u, warp, lane);
+      }
+      it0 += (u.z - u.y) / kBK;
     }
+    if (a.prof && threadIdx.x == 0) {  // debug timeline (cmpc_debug_syrk_timeline)
+      long long t_end;
+      unsigned smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      a.prof[3 * p] = t_start;
+      a.prof[3 * p + 1] = t_end;
+      a.prof[3 * p + 2] = smid;
+    }
+  }
+  // the last CTA out resets the piece counter for the next launch (every producer has made
+  // its final grab before its consumers saw the end marker)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.ctl + 1, 1u) == gridDim.x - 1) {
+      a.ctl[0] = 0;
+      a.ctl[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
-// M(i,j) = H(i,j) + (sum over the tile's units in k order [+ singleton diagonal]), lower;
-// grid (tiles, 16): 256 elements of one tile per block
-__global__ void k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
-                              const int32_t* __restrict__ tile_ptr,
-                              const int32_t* __restrict__ tile_units, const double* __restrict__ H,
-                              const double* __restrict__ dsing, int64_t n, double* __restrict__ M,
-                              int mirror) {
+// M(i,j) = H(i,j) + (sum of the tile's partials in k order [+ singleton diagonal]), lower
+// (+ mirrored upper); grid (tiles, 16): 256 elements of one tile per block. Thin partials
+// hold rows 0..31 only (flag bit 31 of their id); a warp's 32 elements share one row half,
+// so the skip is warp-uniform. Eight loads in flight, summed in order (deterministic).
+__global__ void __launch_bounds__(256)
+    k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
+                  const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ tile_segs,
+                  const double* __restrict__ H, const double* __restrict__ dsing, int64_t n,
+                  double* __restrict__ M, int mirror) {
   const int2 tl = tiles[blockIdx.x];
   const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
   const int e = blockIdx.y * blockDim.x + threadIdx.x;
   const int rl = e & (kTile - 1), cl = e >> 6;
   const int64_t i = (int64_t)kTile * tl.x + rl, j = (int64_t)kTile * tl.y + cl;
   if (i >= n || j >= n || i < j) return;
-  double s0 = 0.0, s1 = 0.0;
-  int q = u0;
-  for (; q + 1 < u1; q += 2) {
-    s0 += partial[(size_t)tile_units[q] * (kTile * kTile) + e];
-    s1 += partial[(size_t)tile_units[q + 1] * (kTile * kTile) + e];
+  const bool lower_half = rl >= 32;
+  double s = 0.0;
+  for (int q = u0; q < u1; q += 8) {
+    double x[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      x[b] = 0.0;
+      if (q + b < u1) {
+        const int32_t id = __ldg(tile_segs + q + b);
+        if (!(id < 0 && lower_half)) x[b] = __ldcg(partial + (size_t)(id & 0x7fffffff) * (kTile * kTile) + e);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) s += x[b];
   }
-  if (q < u1) s0 += partial[(size_t)tile_units[q] * (kTile * kTile) + e];
-  double s = s0 + s1;
   if (i == j) s += dsing[i];
   const double v = H ? H[i + j * n] + s : s;  // H on one rank only when sharded
   M[i + j * n] = v;
@@ -202,110 +333,25 @@ PFN_encodeTiled get_encode() {
 }  // namespace
 
 void syrk_free(Ctx& c) {
-  for (void* p : {(void*)c.units, (void*)c.tile_ptr, (void*)c.tile_units, (void*)c.tiles,
-                  (void*)c.partial})
+  for (void* p : {(void*)c.units, (void*)c.cta_ptr, (void*)c.syrk_ctl, (void*)c.tiles,
+                  (void*)c.tile_ptr, (void*)c.tile_units, (void*)c.partial})
     dev_free(p, c.stream);
   c.units = nullptr;
-  c.tile_ptr = c.tile_units = nullptr;
+  c.cta_ptr = nullptr;
+  c.syrk_ctl = nullptr;
   c.tiles = nullptr;
+  c.tile_ptr = c.tile_units = nullptr;
   c.partial = nullptr;
   delete[] reinterpret_cast<unsigned char*>(c.tmap_P);
-  c.tmap_P = nullptr;
+  delete[] reinterpret_cast<unsigned char*>(c.tmap_P32);
+  c.tmap_P = c.tmap_P32 = nullptr;
 }
 
 void syrk_plan(Ctx& c) {
   syrk_free(c);
   const int64_t n = c.n;
   const int nt = (int)ceil_div(n, kTile);
-  std::vector<int2> tiles;
-  std::vector<std::pair<int, int>> range;  // per tile [k_begin, k_end)
   const int k_end = (int)c.ldp;
-  int64_t total = 0;
-  for (int tj = 0; tj < nt; ++tj)
-    for (int ti = tj; ti < nt; ++ti) {
-      tiles.push_back({ti, tj});
-      int kb = c.ps > 0 ? c.h_start_col[size_t(std::min<int64_t>(n, (int64_t)kTile * ti))] : k_end;
-      kb = kb / kBK * kBK;
-      if (c.ps == 0) kb = k_end;
-      range.push_back({kb, k_end});
-      total += std::max(0, k_end - kb);
-    }
-  // split-K chunk: the (tile, chunk) units run in k-major order (concurrent units share P
-  // rows in L2) and the hardware dispatches them in order onto 2 CTAs per SM. Pick the chunk
-  // by simulating that list schedule (cost = k-steps + a fixed per-unit overhead for the
-  // pipeline fill and the partial-tile store) and keeping the shortest makespan: a chunk
-  // that leaves a sliver of a last wave idles most of the chip.
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  const int slots = sms * 2;
-  auto build = [&](int64_t kc, std::vector<int4>* out, std::vector<std::vector<int>>* pt) {
-    const int64_t nchunks = ceil_div(k_end, kc);
-    for (int64_t q = 0; q < nchunks; ++q) {
-      const int64_t c0 = q * kc, c1 = std::min<int64_t>(k_end, c0 + kc);
-      for (size_t t = 0; t < tiles.size(); ++t) {
-        const int64_t a = std::max<int64_t>(c0, range[t].first), b = std::min<int64_t>(c1, range[t].second);
-        if (a >= b) continue;
-        if (pt) (*pt)[t].push_back((int)out->size());
-        out->push_back({tiles[t].x, tiles[t].y, (int)a, (int)b});
-      }
-    }
-  };
-  auto makespan = [&](const std::vector<int4>& us) {
-    std::priority_queue<double, std::vector<double>, std::greater<double>> q;
-    for (int s = 0; s < slots; ++s) q.push(0.0);
-    double end = 0.0;
-    for (const int4& u : us) {
-      const double t0 = q.top();
-      q.pop();
-      // a diagonal tile loads one operand instead of two: ~3/4 of the time per step
-      const double steps = double(u.w - u.z) / kBK * (u.x == u.y ? 0.75 : 1.0);
-      const double t1 = t0 + steps + 1.5;
-      end = std::max(end, t1);
-      q.push(t1);
-    }
-    return end;
-  };
-  int64_t kc = round_up(std::max<int64_t>(1, total / (int64_t(slots) * 4)), kBK);
-  kc = std::max<int64_t>(kc, 8 * kBK);
-  {
-    double best = 1e300;
-    const int64_t hi_kc = std::max<int64_t>(8 * kBK, round_up(std::max<int64_t>(1, total / slots), kBK));
-    const int64_t step = std::max<int64_t>(kBK, round_up((hi_kc - 8 * kBK) / 40, kBK));
-    for (int64_t cand = 8 * kBK; cand <= hi_kc; cand += step) {
-      std::vector<int4> us;
-      build(cand, &us, nullptr);
-      const double ms = makespan(us);
-      if (ms < best * 0.999) {
-        best = ms;
-        kc = cand;
-      }
-    }
-  }
-  std::vector<int4> units;
-  std::vector<std::vector<int>> per_tile(tiles.size());
-  build(kc, &units, &per_tile);
-  std::vector<int32_t> tptr(tiles.size() + 1, 0), tunits;
-  for (size_t t = 0; t < tiles.size(); ++t) {
-    tptr[t + 1] = tptr[t] + (int32_t)per_tile[t].size();
-    for (int u : per_tile[t]) tunits.push_back(u);
-  }
-  c.nunits = (int)units.size();
-  c.ntiles = (int)tiles.size();
-  cudaStream_t st = c.stream;
-  c.units = dev_alloc<int4>(units.size(), st);
-  c.tiles = dev_alloc<int2>(tiles.size(), st);
-  c.tile_ptr = dev_alloc<int32_t>(tptr.size(), st);
-  c.tile_units = dev_alloc<int32_t>(tunits.size(), st);
-  c.partial = dev_alloc<double>((size_t)kTile * kTile * std::max(1, c.nunits), st);
-  if (!units.empty())
-    CMPC_CUDA(cudaMemcpyAsync(c.units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice, st));
-  CMPC_CUDA(cudaMemcpyAsync(c.tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, st));
-  CMPC_CUDA(cudaMemcpyAsync(c.tile_ptr, tptr.data(), sizeof(int32_t) * tptr.size(), cudaMemcpyHostToDevice, st));
-  if (!tunits.empty())
-    CMPC_CUDA(cudaMemcpyAsync(c.tile_units, tunits.data(), sizeof(int32_t) * tunits.size(),
-                              cudaMemcpyHostToDevice, st));
-  CMPC_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
-
   // algorithmic work of one condensation: lower triangle of P' diag(omega) P
   {
     std::vector<int32_t> hh(size_t(std::max<int64_t>(c.ps, 1)));
@@ -321,18 +367,163 @@ void syrk_plan(Ctx& c) {
     c.syrk_flops = f;
     c.syrk_bytes = b;
   }
-  // TMA descriptor over P (ldp rows x n cols, column-major), box {16 rows, 64 cols}
-  auto* tm = new unsigned char[sizeof(CUtensorMap)];
-  c.tmap_P = tm;
-  const cuuint64_t dims[2] = {(cuuint64_t)c.ldp, (cuuint64_t)n};
-  const cuuint64_t strides[1] = {(cuuint64_t)c.ldp * sizeof(double)};
-  const cuuint32_t box[2] = {16, 64};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult r = get_encode()(reinterpret_cast<CUtensorMap*>(tm), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
-                            c.P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  // first P row (kBK-aligned down) whose prefix reaches column col
+  auto kstart = [&](int64_t col) {
+    if (c.ps == 0) return k_end;
+    return c.h_start_col[size_t(std::min<int64_t>(n, col))] / kBK * kBK;
+  };
+  // jobs: per lower tile (I,J), the rows whose prefix ends in the first half of column block I
+  // (THIN: only output rows 0..31 are nonzero) and the rest (FULL)
+  struct Job { int tile, ti, tj, thin, kb, ke; double w; };
+  std::vector<Job> jobs;
+  std::vector<int2> tiles;
+  for (int tj = 0; tj < nt; ++tj)
+    for (int ti = tj; ti < nt; ++ti) {
+      const int tile = (int)tiles.size();
+      tiles.push_back({ti, tj});
+      const int a0 = kstart((int64_t)kTile * ti), a1 = std::max(a0, kstart((int64_t)kTile * ti + 32));
+      const bool dg = ti == tj;
+      if (a1 > a0) jobs.push_back({tile, ti, tj, 1, a0, a1, dg ? kCostDiagThin : kCostThin});
+      if (k_end > a1) jobs.push_back({tile, ti, tj, 0, a1, k_end, dg ? kCostDiag : kCostFull});
+    }
+  // Pieces. The k axis is split where the cumulative weighted work reaches (1 - tail_frac).
+  // The body [0, K) is laid out job after job and cut into one equal-cost piece per CTA slot
+  // (every CTA starts with one; few segments, so few partial tiles). The tail [K, end) is laid
+  // out the same way and cut into pieces of decreasing cost (remaining / slots, at least
+  // min_piece steps) that the CTAs grab as they finish: the dynamic tail absorbs the run-time
+  // spread of the body pieces so the CTAs finish together.
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+  const int slots = sms * 2;
+  const int nsteps_all = k_end / kBK;
+  std::vector<double> dens(size_t(std::max(nsteps_all, 1)), 0.0);  // weighted cost per k step
+  for (const Job& jb : jobs)
+    for (int q = jb.kb / kBK; q < jb.ke / kBK; ++q) dens[size_t(q)] += jb.w;
+  double work = 0.0;
+  for (double x : dens) work += x;
+  // small problems (C2, C5: ~2 steps per slot) run fewer, longer pieces: fewer partial tiles
+  // to reduce, and no dynamic tail
+  double tail_frac = work >= 16.0 * slots ? 0.1 : 0.0, min_piece = 3.0, min_body = 8.0;
+  if (const char* e = getenv("CMPC_SYRK_TAILFRAC")) tail_frac = std::min(1.0, std::max(0.0, atof(e)));
+  if (const char* e = getenv("CMPC_SYRK_MINBODY")) min_body = std::max(1.0, atof(e));
+  if (const char* e = getenv("CMPC_SYRK_MINPIECE")) min_piece = std::max(0.5, atof(e));
+  int ksplit = nsteps_all;  // body = steps [0, ksplit)
+  {
+    double acc = 0.0;
+    for (int q = 0; q < nsteps_all; ++q) {
+      if (acc >= work * (1.0 - tail_frac)) {
+        ksplit = q;
+        break;
+      }
+      acc += dens[size_t(q)];
+    }
+  }
+  std::vector<int4> segs;
+  std::vector<int32_t> pptr{0};
+  std::vector<std::vector<int32_t>> per_tile(tiles.size());
+  auto emit = [&](const Job& jb, int a, int b) {
+    const int id = (int)segs.size();
+    per_tile[size_t(jb.tile)].push_back(jb.thin ? (id | int(0x80000000u)) : id);
+    segs.push_back({jb.ti | jb.tj << 10 | jb.thin << 20, a * kBK, b * kBK, jb.tile});
+  };
+  auto close_piece = [&]() {
+    if (pptr.back() != (int32_t)segs.size()) pptr.push_back((int32_t)segs.size());
+  };
+  for (int region = 0; region < 2; ++region) {
+    const int q0 = region == 0 ? 0 : ksplit, q1 = region == 0 ? ksplit : nsteps_all;
+    double cw = 0.0;
+    int64_t steps = 0;
+    for (const Job& jb : jobs) {
+      const int a = std::max(q0, jb.kb / kBK), b = std::min(q1, jb.ke / kBK);
+      if (a < b) {
+        cw += (b - a) * jb.w;
+        steps += b - a;
+      }
+    }
+    if (steps == 0) continue;
+    double remaining = cw, in_piece = 0.0;
+    auto target = [&] {
+      return region == 0 ? std::max(std::min(min_body, cw), cw / double(std::min<int64_t>(slots, steps)))
+                         : std::max(min_piece, remaining / slots);
+    };
+    double tgt = target();
+    for (const Job& jb : jobs) {
+      const double w = jb.w;
+      int a = std::max(q0, jb.kb / kBK);
+      const int b = std::min(q1, jb.ke / kBK);
+      while (a < b) {
+        const int need = std::max(1, (int)std::ceil((tgt - in_piece) / w - 1e-9));
+        const int take = std::min(b - a, need);
+        emit(jb, a, a + take);
+        in_piece += take * w;
+        remaining -= take * w;
+        a += take;
+        if (in_piece >= tgt - 1e-9) {
+          close_piece();
+          in_piece = 0.0;
+          tgt = target();
+        }
+      }
+    }
+    close_piece();
+  }
+  const int npieces = (int)pptr.size() - 1;
+  c.syrk_cta_cost.assign(size_t(5 * npieces), 0.0);  // per piece: segments, steps per shape
+  for (int p = 0; p < npieces; ++p)
+    for (int q = pptr[size_t(p)]; q < pptr[size_t(p) + 1]; ++q) {
+      const int4 u = segs[size_t(q)];
+      const int thin = (u.x >> 20) & 1, dg = (u.x & 1023) == ((u.x >> 10) & 1023);
+      c.syrk_cta_cost[size_t(5 * p)] += 1.0;
+      c.syrk_cta_cost[size_t(5 * p + 1 + thin + 2 * dg)] += double(u.z - u.y) / kBK;
+    }
+  if (getenv("CMPC_SYRK_PLAN"))
+    fprintf(stderr, "[syrk plan] jobs %zu tail from step %d of %d, pieces %d segments %zu weighted steps %.0f (%.1f per slot)\n",
+            jobs.size(), ksplit, nsteps_all, npieces, segs.size(), work, work / slots);
+  std::vector<int32_t> tptr(tiles.size() + 1, 0), tsegs;
+  for (size_t t = 0; t < tiles.size(); ++t) {
+    tptr[t + 1] = tptr[t] + (int32_t)per_tile[t].size();
+    for (int32_t u : per_tile[t]) tsegs.push_back(u);
+  }
+  c.nunits = (int)segs.size();
+  c.npieces = npieces;
+  c.nctas = std::min(npieces, slots);
+  c.ntiles = (int)tiles.size();
+  cudaStream_t st = c.stream;
+  c.units = dev_alloc<int4>(segs.size(), st);
+  c.cta_ptr = dev_alloc<int32_t>(pptr.size(), st);
+  c.syrk_ctl = dev_zeros<unsigned>(2, st);
+  c.tiles = dev_alloc<int2>(tiles.size(), st);
+  c.tile_ptr = dev_alloc<int32_t>(tptr.size(), st);
+  c.tile_units = dev_alloc<int32_t>(std::max<size_t>(1, tsegs.size()), st);
+  c.partial = dev_alloc<double>((size_t)kTile * kTile * std::max<size_t>(1, segs.size()), st);
+  if (!segs.empty())
+    CMPC_CUDA(cudaMemcpyAsync(c.units, segs.data(), sizeof(int4) * segs.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaMemcpyAsync(c.cta_ptr, pptr.data(), sizeof(int32_t) * pptr.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaMemcpyAsync(c.tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaMemcpyAsync(c.tile_ptr, tptr.data(), sizeof(int32_t) * tptr.size(), cudaMemcpyHostToDevice, st));
+  if (!tsegs.empty())
+    CMPC_CUDA(cudaMemcpyAsync(c.tile_units, tsegs.data(), sizeof(int32_t) * tsegs.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+
+  // TMA descriptors over P (ldp rows x n cols, column-major), boxes {16 rows, 64 | 32 cols}
+  auto encode = [&](int cols) {
+    auto* tm = new unsigned char[sizeof(CUtensorMap)];
+    const cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(c.ldp, 1), (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)std::max<int64_t>(c.ldp, 1) * sizeof(double)};
+    const cuuint32_t box[2] = {16, (cuuint32_t)cols};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(reinterpret_cast<CUtensorMap*>(tm), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                              c.P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      delete[] tm;
+      throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    }
+    return tm;
+  };
+  c.tmap_P = encode(64);
+  c.tmap_P32 = encode(32);
   static bool attr = false;
   if (!attr) {
     CMPC_CUDA(cudaFuncSetAttribute(k_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
@@ -343,14 +534,24 @@ void syrk_plan(Ctx& c) {
 }
 
 void launch_condense(Ctx& c, bool mirror) {
-  if (c.nunits > 0) {
+  SyrkArgs a;
+  a.omega = c.omega;
+  a.segs = c.units;
+  a.piece_ptr = c.cta_ptr;
+  a.npieces = c.npieces;
+  a.ctl = c.syrk_ctl;
+  a.partial = c.partial;
+  a.prof = c.syrk_prof;
+  if (c.npieces > 0) {
     const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(c.tmap_P);
-    k_syrk<<<c.nunits, kSyrkThreads, kSyrkSmem, c.stream>>>(*tm, c.omega, c.units, c.partial);
+    const CUtensorMap* tm32 = reinterpret_cast<const CUtensorMap*>(c.tmap_P32);
+    k_syrk<<<c.nctas, kSyrkThreads, kSyrkSmem, c.stream>>>(*tm, *tm32, a);
     CMPC_LAUNCHED();
   }
-  k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 256), 256, 0, c.stream>>>(c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr,
-                                                 c.dsing, c.n, c.M, mirror ? 1 : 0);
-  // (sharded: every rank's partial J_g' Sigma_g J_g, H added by rank 0; the caller allreduces)
+  // sharded: every rank's partial J_g' Sigma_g J_g, H added by rank 0; the caller allreduces
+  k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 256), 256, 0, c.stream>>>(
+      c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr, c.dsing, c.n, c.M,
+      mirror ? 1 : 0);
   CMPC_LAUNCHED();
 }
 

@@ -227,7 +227,8 @@ class ShardedQp:
 
 
 def device_qp(qp: DenseQp) -> DeviceQp:
-    if qp._device is None:
+    """The QP's cached device context (re-created when it was closed)."""
+    if qp._device is None or getattr(qp._device, "h", None) is None:
         qp._device = DeviceQp(qp)
     return qp._device
 
@@ -405,30 +406,44 @@ class BatchResult:
 class BatchSolver:
     """Independent instances that share H and J and differ in (h, h0, d) — the
     receding-horizon / config-5 case (refresh_initial_state, reduction.cpp:270-280).
-    One device context per instance (cloned from the base QP's analysed structure), solved
-    concurrently by a pool of host threads inside the library, one CUDA stream each."""
+    A few worker device contexts (cloned from the base QP's analysed structure, one host
+    thread and one CUDA stream each) take the instances in turn inside the library; each
+    instance's (h, h0, d) is uploaded into the worker's context before its solve."""
 
-    def __init__(self, base: DenseQp, count: int):
+    def __init__(self, base: DenseQp, count: int, workers: int | None = None):
+        import os
         self.base = base
-        root = device_qp(base)
-        self.ctxs = [root.clone() for _ in range(count)]
         self.count = count
+        # one core stays free for the driver and the interpreter
+        self.workers = max(1, min(count, workers or max(1, (os.cpu_count() or 2) - 1)))
+        root = device_qp(base)
+        self.ctxs = [root.clone() for _ in range(self.workers)]
+        root.close()
+        self.h_all = np.repeat(f64(base.h).reshape(1, -1), count, axis=0)
+        self.h0_all = np.full(count, float(base.h0))
+        self.d_all = np.repeat(f64(base.d).reshape(1, -1), count, axis=0)
+        self._pinned = []
+        for a in (self.h_all, self.d_all):  # page-locked: the per-instance uploads are plain DMA
+            if a.nbytes and _lib.lib().cmpc_host_register(a.ctypes.data, a.nbytes) == 0:
+                self._pinned.append(a)
 
     def set_instance(self, i: int, h, h0: float, d):
-        self.ctxs[i].update_affine(h, h0, d)
+        self.h_all[i] = np.asarray(h, dtype=np.float64)
+        self.h0_all[i] = float(h0)
+        self.d_all[i] = np.asarray(d, dtype=np.float64)
 
     def solve(self, opts: IpmOptions = None, threads: int | None = None) -> BatchResult:
-        import os
         opts = opts or IpmOptions()
         _check_options(opts)
         n, cnt = self.base.n, self.count
+        nw = max(1, min(self.workers, threads or self.workers))
         v = np.zeros((cnt, n))
         scal = np.zeros((cnt, 13))
-        arr = (C.c_void_p * cnt)(*[c.h.value if isinstance(c.h, C.c_void_p) else c.h for c in self.ctxs])
+        arr = (C.c_void_p * nw)(*[c.h.value if isinstance(c.h, C.c_void_p) else c.h for c in self.ctxs[:nw]])
         od = (C.c_double * 5)(opts.tol, opts.mu_init, opts.kappa_mu, opts.tau, opts.armijo_eta)
         t0 = time.perf_counter()
-        check(_lib.lib().cmpc_solve_batch(arr, cnt, od, int(opts.max_iter), ptr(v), ptr(scal),
-                                          int(threads or min(cnt, os.cpu_count() or 1))))
+        check(_lib.lib().cmpc_solve_batch_affine(arr, nw, cnt, ptr(self.h_all), ptr(self.h0_all),
+                                                 ptr(self.d_all), od, int(opts.max_iter), ptr(v), ptr(scal)))
         wall = time.perf_counter() - t0
         return BatchResult(status=[IpmStatus(int(x)).name for x in scal[:, 0]], iter=scal[:, 1].astype(int),
                            objective=scal[:, 3].copy(), kkt_error=scal[:, 2].copy(), v=v,
@@ -439,3 +454,8 @@ class BatchSolver:
         for c in self.ctxs:
             c.close()
         self.ctxs = []
+        for a in getattr(self, "_pinned", []):
+            _lib.lib().cmpc_host_unregister(a.ctypes.data)
+        self._pinned = []
+
+    __del__ = close

@@ -100,3 +100,14 @@ def test_backend_registry():  # test_dense_linalg.cpp:162-169 with the B200 regi
     for unknown in ("reference-cpu", "eigen", "nonexistent"):
         with pytest.raises(ValueError):
             linalg.make_backend(unknown)
+
+
+def test_null_context_is_an_error_not_a_crash():
+    """A closed (null) context handle is rejected with an error code (no dereference)."""
+    from paper_2209_13049_b200 import _lib
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    assert L.cmpc_ctx_clone(None, ctypes.byref(h)) == _lib.CMPC_ERR_ARG
+    assert "null context" in _lib.last_error()
+    out = (ctypes.c_int64 * 8)()
+    assert L.cmpc_update_qp_affine(None, None, 0.0, None, 0) == _lib.CMPC_ERR_DIM

@@ -48,3 +48,21 @@ def test_config5_batch_slice():
     for i in (0, 7):
         single = ipm.solve(insts[i])
         assert res.iter[i] == single.iter and rel(res.v[i], single.v) <= 1e-14
+
+
+def test_batch_solvers_can_be_created_again_on_the_same_base():
+    """Closing a batch solver closes its root context; the QP's cached device context is
+    re-created for the next one (regression: the second construction dereferenced a closed
+    context)."""
+    data = P.heat2d_problem(10, 8, T=12, splits=([5], [5], [4], [4]))
+    base, insts = instances(data, 6)
+    iters = []
+    for _ in range(3):
+        bs = ipm.BatchSolver(base, len(insts), workers=3)
+        for i, q in enumerate(insts):
+            bs.set_instance(i, q.h, q.h0, q.d)
+        res = bs.solve()
+        assert all(s == "converged" for s in res.status)
+        iters.append(list(res.iter))
+        bs.close()
+    assert iters[0] == iters[1] == iters[2]
