@@ -103,6 +103,7 @@ struct Ctx {
          *q = nullptr, *dsing = nullptr, *rhs = nullptr, *M = nullptr, *L = nullptr;
   double *pv = nullptr, *ps_ = nullptr, *pl = nullptr, *pzd = nullptr, *Jpv = nullptr,
          *vt = nullptr, *yt = nullptr, *Hvt = nullptr;
+  double* yv = nullptr;  // P v of the current point (prototype-indexed, like y = P pv)
   double* part = nullptr;     // kPartBlocks x 16 partial sums
   double* colpart = nullptr;  // Pt q partial: nchunks x n
   int colchunks = 0;
@@ -198,7 +199,9 @@ void launch_rhs(Ctx& c);
 void launch_recover(Ctx& c, double tau);
 // merit pieces of trial (alpha): v_t = v + alpha pv, s_t = s + alpha ps; with
 // alpha_from_device the step is alpha_max = min(1, packet tau-ratio minimum)
-void launch_trial(Ctx& c, double alpha, bool alpha_from_device);
+// linear: J v_t from the current point's and the direction's prototype values (yv + alpha y,
+// valid inside the host loop after launch_residuals and launch_recover) instead of a P pass
+void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear = false);
 // line-search derivative pieces for externally set directions: (Hv+h).pv, sum ps/s
 void launch_ls_pieces(Ctx& c);
 // v = 0, s = max(1, d), z = mu / s, lambda = z (ipm.cpp:170-177)

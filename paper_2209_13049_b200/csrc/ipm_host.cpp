@@ -105,7 +105,7 @@ void seg_step(Ctx& c, double tau) {
   launch_cholesky(c, c.M, c.L, 0.0, c.rhs, c.pv);  // factor + both triangular solves
   rec(c.ev1, c.stream);
   launch_recover(c, tau);
-  launch_trial(c, 0.0, true);
+  launch_trial(c, 0.0, true, /*linear=*/true);
   launch_publish(c);
 }
 
@@ -182,7 +182,7 @@ int run_line_search(Ctx& c, const Packet& A, double dg, double dps, double alpha
     if (j == 0 && trial0) {
       T = *trial0;
     } else {
-      launch_trial(c, alpha, false);
+      launch_trial(c, alpha, false, /*linear=*/true);
       sync_packet(c, syncs);
       T = *c.pk_host;
     }
@@ -205,6 +205,9 @@ int run_line_search(Ctx& c, const Packet& A, double dg, double dps, double alpha
 
 int line_search_host(Ctx& c, double alpha_max, double eta, double* alpha, int* ntrials) {
   const Packet A = *c.pk_host;  // residuals + derivative pieces already in the packet
+  // the trials use P v (from the residual pass) and P pv: the direction may have been set
+  // from the host, so form P pv here
+  launch_Jx(c, c.pv, c.y, nullptr);
   return run_line_search(c, A, A.d_gpv, A.d_ps_s, alpha_max, eta, nullptr, alpha, ntrials, nullptr);
 }
 
@@ -308,7 +311,7 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
       launch_cholesky(c, c.M, c.L, kShifts[shift], c.rhs, c.pv);
       CMPC_CUDA(cudaEventRecord(c.ev1, c.stream));
       launch_recover(c, tau);
-      launch_trial(c, 0.0, true);
+      launch_trial(c, 0.0, true, /*linear=*/true);
       sync_packet(c, &syncs);
       CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
       linalg += ms * 1e-3;

@@ -528,8 +528,13 @@ __global__ void k_axpy_n(int64_t n, const double* __restrict__ x, double a, cons
   if (i < n) out[i] = add(x[i], mul(al, p[i]));
 }
 
+// J v_t rows: from yt = P v_t (exact pass), or, when yt is null, from the prototype values of
+// the current point and the direction, yv + alpha y (J is linear; the accepted trial's
+// values are carried into yv by k_update with the same rounding, so no P pass is needed)
 __global__ void __launch_bounds__(kRowT) k_trial_rows(int64_t m, const int32_t* __restrict__ row_map,
                                                       const double* __restrict__ yt,
+                                                      const double* __restrict__ yv,
+                                                      const double* __restrict__ y,
                                                       const double* __restrict__ d,
                                                       const double* __restrict__ s,
                                                       const double* __restrict__ ps, double alpha_h,
@@ -544,7 +549,15 @@ __global__ void __launch_bounds__(kRowT) k_trial_rows(int64_t m, const int32_t* 
     const double st = add(s[r], mul(alpha, ps[r]));
     if (st <= 0.0) bad = 1;
     slog += log(st);
-    sabs += fabs(add(sub(jrow(yt, row_map[r]), d[r]), st));
+    const int32_t rm = row_map[r];
+    double jv;
+    if (yt) {
+      jv = jrow(yt, rm);
+    } else {
+      const double u = add(yv[rm >> 1], mul(alpha, y[rm >> 1]));
+      jv = (rm & 1) ? -u : u;
+    }
+    sabs += fabs(add(sub(jv, d[r]), st));
   }
   double t = block_sum<kRowT>(sabs, sh);
   if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumAbs] = t;
@@ -588,10 +601,12 @@ __global__ void k_update(int64_t n, int64_t m, const double* __restrict__ ap, do
                          const double* __restrict__ pv, double* __restrict__ s,
                          const double* __restrict__ ps, double* __restrict__ lam,
                          const double* __restrict__ pl, double* __restrict__ z,
-                         const double* __restrict__ pz) {
+                         const double* __restrict__ pz, int64_t py, double* __restrict__ yv,
+                         const double* __restrict__ y) {
   const double alpha = ap[0], alpha_z = ap[1];
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) v[i] = add(v[i], mul(alpha, pv[i]));
+  if (i < py) yv[i] = add(yv[i], mul(alpha, y[i]));  // P v of the new point (see k_trial_rows)
   if (i < m) {
     s[i] = add(s[i], mul(alpha, ps[i]));
     lam[i] = add(lam[i], mul(alpha, pl[i]));
@@ -693,7 +708,7 @@ void vec_alloc(Ctx& c) {
   c.omega = dev_zeros<double>(py, c.stream); c.q = dev_zeros<double>(py, c.stream); c.dsing = dev_zeros<double>(n, c.stream); c.rhs = dev_zeros<double>(n, c.stream);
   c.M = dev_zeros<double>(n * n, c.stream); c.L = dev_zeros<double>(n * n, c.stream);
   c.pv = dev_zeros<double>(n, c.stream); c.ps_ = dev_zeros<double>(m, c.stream); c.pl = dev_zeros<double>(m, c.stream); c.pzd = dev_zeros<double>(m, c.stream);
-  c.Jpv = dev_zeros<double>(m, c.stream); c.vt = dev_zeros<double>(n, c.stream); c.yt = dev_zeros<double>(py, c.stream); c.Hvt = dev_zeros<double>(n, c.stream);
+  c.Jpv = dev_zeros<double>(m, c.stream); c.vt = dev_zeros<double>(n, c.stream); c.yt = dev_zeros<double>(py, c.stream); c.yv = dev_zeros<double>(py, c.stream); c.Hvt = dev_zeros<double>(n, c.stream);
   c.part = dev_zeros<double>((size_t)kPartBlocks * kSlots, c.stream);
   const int rc = 2048;
   c.colchunks = (int)std::max<int64_t>(1, ceil_div(c.ps, rc));
@@ -737,7 +752,7 @@ void vec_free(Ctx& c) {
                   (void*)c.r3, (void*)c.Hv, (void*)c.Jtl, (void*)c.y, (void*)c.sigma,
                   (void*)c.omega, (void*)c.q, (void*)c.dsing, (void*)c.rhs, (void*)c.M,
                   (void*)c.L, (void*)c.pv, (void*)c.ps_, (void*)c.pl, (void*)c.pzd, (void*)c.Jpv,
-                  (void*)c.vt, (void*)c.yt, (void*)c.Hvt, (void*)c.part, (void*)c.colpart,
+                  (void*)c.vt, (void*)c.yt, (void*)c.yv, (void*)c.Hvt, (void*)c.part, (void*)c.colpart,
                   (void*)c.hmax, (void*)c.pk, (void*)c.d_mu, (void*)c.d_alpha})
     dev_free(p, c.stream);
   if (c.pk_host) cudaFreeHost(c.pk_host);
@@ -753,7 +768,7 @@ void vec_free(Ctx& c) {
   chol_free(c);
   c.v = c.s = c.lam = c.z = c.r1 = c.r2 = c.r3 = c.Hv = c.Jtl = c.y = c.sigma = nullptr;
   c.omega = c.q = c.dsing = c.rhs = c.M = c.L = c.pv = c.ps_ = c.pl = c.pzd = nullptr;
-  c.Jpv = c.vt = c.yt = c.Hvt = c.part = c.colpart = c.hmax = c.d_mu = c.d_alpha = nullptr;
+  c.Jpv = c.vt = c.yt = c.yv = c.Hvt = c.part = c.colpart = c.hmax = c.d_mu = c.d_alpha = nullptr;
   c.pk = nullptr;
   c.pk_host = nullptr;
 }
@@ -831,18 +846,16 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
   k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 0);
   CMPC_LAUNCHED();
   if (reuse_trial) {
-    // v was just set to the accepted trial point v + alpha pv, computed with the same
-    // kernel and inputs as the trial: H v and P v are the trial's, bit for bit
+    // v was just set to the accepted trial point v + alpha pv: H v is the trial's (same
+    // kernel, same inputs, bit for bit) and k_update carried P v along as yv + alpha P pv,
+    // the values the trial's merit used
     if (c.n > 0) CMPC_CUDA(cudaMemcpyAsync(c.Hv, c.Hvt, sizeof(double) * c.n, cudaMemcpyDeviceToDevice, c.stream));
-    const int64_t py = c.ldp + c.pz;
-    if (c.m > 0 && py > 0)
-      CMPC_CUDA(cudaMemcpyAsync(c.y, c.yt, sizeof(double) * py, cudaMemcpyDeviceToDevice, c.stream));
   } else {
     launch_Hx(c, c.v, c.Hv);
   }
   if (c.m > 0) {
-    if (!reuse_trial) launch_Jx(c, c.v, c.y, nullptr);
-    k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.d, c.s, c.lam, c.z, c.d_mu, c.r2,
+    if (!reuse_trial) launch_Jx(c, c.v, c.yv, nullptr);
+    k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.yv, c.d, c.s, c.lam, c.z, c.d_mu, c.r2,
                                            c.r3, c.part, c.pk);
     CMPC_LAUNCHED();
     k_proto_reduce<true, false><<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
@@ -963,7 +976,7 @@ void launch_recover(Ctx& c, double tau) {
   }
 }
 
-void launch_trial(Ctx& c, double alpha, bool alpha_from_device) {
+void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear) {
   const Packet* apk = alpha_from_device ? c.pk : nullptr;
   k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 2);
   CMPC_LAUNCHED();
@@ -974,9 +987,9 @@ void launch_trial(Ctx& c, double alpha, bool alpha_from_device) {
   launch_Hx(c, c.vt, c.Hvt);
   const unsigned pb = part_blocks(c.m);
   if (c.m > 0) {
-    launch_Jx(c, c.vt, c.yt, nullptr);
-    k_trial_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.yt, c.d, c.s, c.ps_, alpha, apk,
-                                             c.part, c.pk);
+    if (!linear) launch_Jx(c, c.vt, c.yt, nullptr);
+    k_trial_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, linear ? nullptr : c.yt, c.yv, c.y,
+                                             c.d, c.s, c.ps_, alpha, apk, c.part, c.pk);
     CMPC_LAUNCHED();
   }
   k_trial_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m, c.m > 0 ? (int)pb : 0, c.vt, c.Hvt, c.h,
@@ -1029,10 +1042,12 @@ void set_alpha(Ctx& c, double alpha, double alpha_z) {
 }
 
 void launch_update_dev(Ctx& c) {
-  const int64_t k = std::max(c.n, c.m);
+  const int64_t py = c.m > 0 ? c.ldp + c.pz : 0;
+  const int64_t k = std::max(std::max(c.n, c.m), py);
   if (k == 0) return;
   k_update<<<(unsigned)ceil_div(k, 256), 256, 0, c.stream>>>(c.n, c.m, c.d_alpha, c.v, c.pv,
-                                                             c.s, c.ps_, c.lam, c.pl, c.z, c.pzd);
+                                                             c.s, c.ps_, c.lam, c.pl, c.z, c.pzd,
+                                                             py, c.yv, c.y);
   CMPC_LAUNCHED();
 }
 
