@@ -98,6 +98,35 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return r;
 }
 
+// block max / min (result valid in thread 0): one atomic per block instead of one per warp
+template <int NT>
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = v;
+  if (threadIdx.x < 32) r = warp_max((l < NT / 32) ? sh[l] : v);
+  return r;
+}
+template <int NT>
+__device__ __forceinline__ double block_min(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = v;
+  if (threadIdx.x < 32) {
+    r = (l < NT / 32) ? sh[l] : v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r = fmin(r, __shfl_xor_sync(0xffffffffu, r, o));
+  }
+  return r;
+}
+
 #endif  // __CUDACC__
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }

@@ -24,7 +24,7 @@ namespace cmpc {
 
 constexpr int kTile = 64;      // SYRK / Cholesky output tile
 constexpr int kBK = 32;        // SYRK k rows per pipeline stage
-constexpr int kPartBlocks = 592;  // fixed grid for m-length reductions (4 x 148 SMs)
+constexpr int kPartBlocks = 2048;  // max grid of the m-length row passes: one row per thread up to 524k rows
 
 // small scalar packet read back at the two sync points of an iteration
 struct Packet {
@@ -79,6 +79,8 @@ struct Ctx {
   int32_t* sing_col = nullptr;   // pz (ascending)
   double* sing_val = nullptr;    // pz
   int32_t* sing_ptr = nullptr;   // n+1: singleton prototypes of column j are [sing_ptr[j], sing_ptr[j+1])
+  int32_t* proto_big = nullptr;  // prototypes with more than 8 member rows (k_proto_reduce warp path)
+  int nbig = 0;
   bool h_symmetric = false;      // H == H' bitwise: H x as column dots
   std::vector<int32_t> h_start_col;
 

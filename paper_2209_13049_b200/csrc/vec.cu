@@ -16,6 +16,7 @@ namespace cmpc {
 namespace {
 
 constexpr int kRowT = 256;
+constexpr int kLaneMembers = 8;  // prototypes with more member rows take the warp path of k_proto_reduce
 enum Slot { kSumAbs = 0, kSumLog = 1, kSumPsS = 2, kSlots = 16 };
 
 inline unsigned part_blocks(int64_t m) {
@@ -221,12 +222,12 @@ __global__ void __launch_bounds__(kRowT) k_res_rows(int64_t m, const int32_t* __
   if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumAbs] = t;
   t = block_sum<kRowT>(slog, sh);
   if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumLog] = t;
-  ml = warp_max(ml);
-  mss = warp_max(mss);
-  mz = warp_max(mz);
-  mr3 = warp_max(mr3);
-  mc = warp_max(mc);
-  if ((threadIdx.x & 31) == 0) {
+  ml = block_max<kRowT>(ml, sh);
+  mss = block_max<kRowT>(mss, sh);
+  mz = block_max<kRowT>(mz, sh);
+  mr3 = block_max<kRowT>(mr3, sh);
+  mc = block_max<kRowT>(mc, sh);
+  if (threadIdx.x == 0) {
     atomic_max_nonneg(&pk->max_lam, ml);
     atomic_max_nonneg(&pk->max_s, mss);
     atomic_max_nonneg(&pk->max_z, mz);
@@ -264,8 +265,37 @@ __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* 
                                                       const double* __restrict__ x2,
                                                       double* __restrict__ out1,
                                                       double* __restrict__ out2, int64_t ps,
-                                                      int64_t ldp, int64_t zero_k) {
+                                                      int64_t ldp, int64_t zero_k,
+                                                      const int32_t* __restrict__ big, int nbig,
+                                                      int lane_blocks) {
   const int lane = threadIdx.x & 31;
+  if ((int)blockIdx.x >= lane_blocks) {
+    // a prototype with more than kLaneMembers members: one warp, lanes stride the members
+    // (ascending per lane), fixed butterfly sum across the lanes
+    const int wi = ((int)blockIdx.x - lane_blocks) * 8 + (threadIdx.x >> 5);
+    if (wi >= nbig) return;
+    const int64_t k = big[wi];
+    const int32_t b0 = mem_ptr[k], b1 = mem_ptr[k + 1];
+    double s1 = 0.0, s2 = 0.0;
+    for (int32_t e = b0 + lane; e < b1; e += 32) {
+      const int32_t rm = mem_rows[e];
+      const int32_t r = rm >> 1;
+      const double a = x1[r];
+      s1 += (SIGNED1 && (rm & 1)) ? -a : a;
+      if (HAS2) {
+        const double bb = x2[r];
+        s2 += (rm & 1) ? -bb : bb;
+      }
+    }
+    s1 = warp_sum(s1);
+    if (HAS2) s2 = warp_sum(s2);
+    if (lane == 0) {
+      const int64_t o = k < ps ? k : ldp + (k - ps);
+      out1[o] = s1;
+      if (HAS2) out2[o] = s2;
+    }
+    return;
+  }
   const int64_t base = (blockIdx.x * 8ll + (threadIdx.x >> 5)) * 32;
   const int64_t k = base + lane;
   int32_t b0 = 0, b1 = 0;
@@ -273,17 +303,18 @@ __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* 
     b0 = mem_ptr[k];
     b1 = mem_ptr[k + 1];
   }
+  if (b1 - b0 > kLaneMembers) return;  // the warp path above owns it
   // every lane sums its own prototype: member loads are independent, so they are issued
-  // in batches of 8 ahead of the (ordered) accumulation
+  // together ahead of the (ordered) accumulation
   double s1 = 0.0, s2 = 0.0;
-  for (int32_t e = b0; e < b1; e += 8) {
-    double v1[8], v2[8];
+  {
+    double v1[kLaneMembers], v2[kLaneMembers];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < kLaneMembers; ++u) {
       v1[u] = 0.0;
       v2[u] = 0.0;
-      if (e + u < b1) {
-        const int32_t rm = mem_rows[e + u];
+      if (b0 + u < b1) {
+        const int32_t rm = mem_rows[b0 + u];
         const int32_t r = rm >> 1;
         const double a = x1[r];
         v1[u] = (SIGNED1 && (rm & 1)) ? -a : a;
@@ -294,8 +325,8 @@ __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* 
       }
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (e + u < b1) {
+    for (int u = 0; u < kLaneMembers; ++u) {
+      if (b0 + u < b1) {
         s1 += v1[u];
         if (HAS2) s2 += v2[u];
       }
@@ -461,12 +492,9 @@ __global__ void __launch_bounds__(kRowT) k_recover_rows(
   }
   const double t = block_sum<kRowT>(q, sh);
   if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumPsS] = t;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    as = fmin(as, __shfl_xor_sync(0xffffffffu, as, o));
-    az = fmin(az, __shfl_xor_sync(0xffffffffu, az, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
+  as = block_min<kRowT>(as, sh);
+  az = block_min<kRowT>(az, sh);
+  if (threadIdx.x == 0) {
     if (as < 1e308) atomic_min_nonneg(&pk->alpha_s_min, as);
     if (az < 1e308) atomic_min_nonneg(&pk->alpha_z_min, az);
   }
@@ -731,6 +759,20 @@ void vec_alloc(Ctx& c) {
     k_absmax<<<(unsigned)std::min<int64_t>(64, ceil_div(c.n, 256)), 256, 0, c.stream>>>(c.h, c.n, c.hmax);
     CMPC_LAUNCHED();
   }
+  {  // prototypes with many member rows (duplicates of symmetric segments): warp path
+    std::vector<int32_t> mp(size_t(c.p + 1), 0), big;
+    if (c.p > 0) {
+      CMPC_CUDA(cudaMemcpyAsync(mp.data(), c.mem_ptr, sizeof(int32_t) * (c.p + 1), cudaMemcpyDeviceToHost, c.stream));
+      CMPC_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    for (int64_t k = 0; k < c.p; ++k)
+      if (k != c.zero_k && mp[size_t(k + 1)] - mp[size_t(k)] > kLaneMembers) big.push_back((int32_t)k);
+    c.nbig = (int)big.size();
+    c.proto_big = dev_alloc<int32_t>(std::max<size_t>(1, big.size()), c.stream);
+    if (!big.empty())
+      CMPC_CUDA(cudaMemcpyAsync(c.proto_big, big.data(), sizeof(int32_t) * big.size(), cudaMemcpyHostToDevice, c.stream));
+    CMPC_CUDA(cudaStreamSynchronize(c.stream));
+  }
   c.sing_ptr = dev_alloc<int32_t>((size_t)n + 1, c.stream);
   k_sing_ptr<<<(unsigned)ceil_div((int64_t)n + 1, 256), 256, 0, c.stream>>>(c.sing_col, c.pz, c.n, c.sing_ptr);
   CMPC_LAUNCHED();
@@ -760,6 +802,9 @@ void vec_free(Ctx& c) {
   c.stage = nullptr;
   dev_free(c.sing_ptr, c.stream);
   c.sing_ptr = nullptr;
+  dev_free(c.proto_big, c.stream);
+  c.proto_big = nullptr;
+  c.nbig = 0;
   dev_free(c.pub_dev, c.stream);
   c.pub_dev = nullptr;
   c.pk_map = nullptr;
@@ -794,6 +839,16 @@ unsigned long long launch_publish(Ctx& c) {
   k_publish<<<1, 32, 0, c.stream>>>(c.pk, c.pk_map, c.pub_dev, c.pub_map);
   CMPC_LAUNCHED();
   return ++c.pub_expect;
+}
+
+template <bool SIGNED1, bool HAS2>
+void launch_proto_reduce(Ctx& c, const double* x1, const double* x2, double* out1, double* out2) {
+  const int lane_blocks = (int)ceil_div(c.p, 256);
+  const int grid = lane_blocks + (int)ceil_div(c.nbig, 8);
+  k_proto_reduce<SIGNED1, HAS2><<<(unsigned)grid, 256, 0, c.stream>>>(
+      c.p, c.mem_ptr, c.mem_rows, x1, x2, out1, out2, c.ps, c.ldp, c.zero_k, c.proto_big, c.nbig,
+      lane_blocks);
+  CMPC_LAUNCHED();
 }
 
 void launch_zero_packet(Ctx& c) {
@@ -858,9 +913,7 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
     k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.yv, c.d, c.s, c.lam, c.z, c.d_mu, c.r2,
                                            c.r3, c.part, c.pk);
     CMPC_LAUNCHED();
-    k_proto_reduce<true, false><<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
-        c.p, c.mem_ptr, c.mem_rows, c.lam, nullptr, c.q, nullptr, c.ps, c.ldp, c.zero_k);
-    CMPC_LAUNCHED();
+    launch_proto_reduce<true, false>(c, c.lam, nullptr, c.q, nullptr);
     launch_Jtq(c, c.q, c.Jtl);
   } else if (c.comm && c.n > 0) {
     CMPC_CUDA(cudaMemsetAsync(c.Jtl, 0, sizeof(double) * c.n, c.stream));
@@ -905,12 +958,9 @@ void launch_prepare_step(Ctx& c, const double* sigma_override) {
       c.m, c.s, c.z, c.r2, c.r3, sigma_override, c.sigma, sigma_override ? nullptr : c.Jpv);
   CMPC_LAUNCHED();
   if (sigma_override)
-    k_proto_reduce<false, false><<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
-        c.p, c.mem_ptr, c.mem_rows, c.sigma, nullptr, c.omega, nullptr, c.ps, c.ldp, c.zero_k);
+    launch_proto_reduce<false, false>(c, c.sigma, nullptr, c.omega, nullptr);
   else
-    k_proto_reduce<false, true><<<(unsigned)ceil_div(c.p, 256), 256, 0, c.stream>>>(
-        c.p, c.mem_ptr, c.mem_rows, c.sigma, c.Jpv, c.omega, c.q, c.ps, c.ldp, c.zero_k);
-  CMPC_LAUNCHED();
+    launch_proto_reduce<false, true>(c, c.sigma, c.Jpv, c.omega, c.q);
   k_dsing<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.sing_ptr, c.sing_val,
                                                               c.omega + c.ldp, c.dsing);
   CMPC_LAUNCHED();
