@@ -450,6 +450,28 @@ def main():
                "status": re.status.name,
                "iterations": re.iter}
 
+    # end to end from the structured problem: host LqProblemData ->
+    # dense QP built and analysed on the device -> solve -> trajectory recovered on the device
+    e2e_problem = None
+    if not args.no_e2e:
+        pb_ms = []
+        for k in range(1 + min(args.steps, 5)):
+            barrier()
+            t0 = time.perf_counter()
+            rp = ipm.solve_problem(data, opts)
+            torch.cuda.synchronize(local)
+            if k >= 1:
+                pb_ms.append((time.perf_counter() - t0) * 1e3)
+        nbytes = sum(int(np.asarray(getattr(data, f)).nbytes) for f in
+                     ("A", "B", "Q", "Qf", "R", "S", "E", "F", "gl", "gu", "xl", "xu", "ul", "uu",
+                      "w", "x_bar", "K"))
+        e2e_problem = {"value": statistics.median(pb_ms), "unit": "ms", "h2d_bytes_per_step": nbytes,
+                       "d2h_bytes_per_step": int(8 * (rp.solution.x.size + rp.solution.u.size + qp.n + 3 * qp.m)),
+                       "samples_ms": [round(x, 2) for x in pb_ms], "iterations": rp.iter,
+                       "status": rp.status.name,
+                       "note": "build_dense_qp + solve + recover_trajectory on the device (median); "
+                               "the reference cannot build this QP (bigAtilde alone is 127 GB at config 3)"}
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -481,6 +503,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,
+        "e2e_from_problem": e2e_problem,
         "wall_s": wall,
     }
     if not args.no_cpu_baseline and world == 1:

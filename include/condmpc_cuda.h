@@ -40,6 +40,29 @@ void cmpc_ctx_destroy(cmpc_ctx* ctx);
  * Runs the exact structure analysis of J (distinct rows up to sign, prefix widths). */
 int cmpc_load_qp(cmpc_ctx* ctx, int64_t n, int64_t m, const double* H, const double* h, double h0,
                  const double* J, const double* d, int on_device);
+
+/* The structured LQ-MPC problem (LqProblemData, proj/include/condmpc/problem.hpp:22-45).
+ * Matrices column-major (Eigen's layout); w is T x n_x stage-major (w[t * n_x + i]); bounds
+ * may hold +-inf (rows of infinite bounds are skipped, as in reduction.cpp:191-251); S, K,
+ * E, F, w may be NULL when zero / n_c == 0. */
+typedef struct cmpc_lq_problem {
+  int64_t nx, nu, nc, T;
+  const double *A, *B, *Q, *Qf, *R, *S, *E, *F;
+  const double *gl, *gu, *xl, *xu, *ul, *uu;
+  const double *w, *x_bar, *K;
+} cmpc_lq_problem;
+/* build_dense_qp (proj/src/reduction.cpp:255-268) on the device, then load it like
+ * cmpc_load_qp without the dense J ever crossing PCIe; the problem stays resident for the
+ * two calls below. Replaces the reference's host build + upload. */
+int cmpc_build_qp(cmpc_ctx* ctx, const cmpc_lq_problem* problem);
+/* refresh_initial_state (reduction.cpp:270-280) on a device-built QP: new x_bar -> free
+ * response, h, h0, d recomputed on the device; H, J and the analysed structure are kept. */
+int cmpc_refresh_initial_state(cmpc_ctx* ctx, const double* x_bar);
+/* The loaded QP's H (n x n), h, h0, d (host pointers, each nullable; tests and hooks) */
+int cmpc_get_qp(cmpc_ctx* ctx, double* H, double* h, double* h0, double* d);
+/* recover_trajectory (reduction.cpp:282-314) on the device: x ((T+1) x n_x stage-major),
+ * u (T x n_u), Eq. (1a) objective; v NULL = the last solve's iterate on the device. */
+int cmpc_recover_trajectory(cmpc_ctx* ctx, const double* v, double* x, double* u, double* objective);
 /* A new context (own stream and iterate buffers) holding a device copy of ctx's loaded QP
  * and its structure: instances that share H and J and differ in h, h0, d (the
  * refresh_initial_state case, config 5's batch) are cloned and then updated with

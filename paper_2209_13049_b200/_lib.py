@@ -15,6 +15,15 @@ LIB_PATH = os.path.join(HERE, "libcondmpc_cuda.so")
 D = C.POINTER(C.c_double)
 I64 = C.POINTER(C.c_int64)
 LOG_FN = C.CFUNCTYPE(None, C.c_void_p, D)
+
+
+class LqProblem(C.Structure):
+    """cmpc_lq_problem (include/condmpc_cuda.h): LqProblemData for the device builder."""
+    _fields_ = [("nx", C.c_int64), ("nu", C.c_int64), ("nc", C.c_int64), ("T", C.c_int64)] + [
+        (f, D) for f in ("A", "B", "Q", "Qf", "R", "S", "E", "F", "gl", "gu", "xl", "xu", "ul", "uu",
+                         "w", "x_bar", "K")]
+
+
 INSPECT_FN = C.CFUNCTYPE(None, C.c_void_p, D, D, D, D, C.c_double, D, D, D, C.c_double, D, D, D,
                          D, C.c_double)
 
@@ -31,6 +40,10 @@ SIGNATURES = {
     "cmpc_ctx_destroy": (None, [C.c_void_p]),
     "cmpc_load_qp": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, D, D, C.c_double, D, D, C.c_int]),
     "cmpc_qp_info": (C.c_int, [C.c_void_p, I64]),
+    "cmpc_build_qp": (C.c_int, [C.c_void_p, C.POINTER(LqProblem)]),
+    "cmpc_refresh_initial_state": (C.c_int, [C.c_void_p, D]),
+    "cmpc_get_qp": (C.c_int, [C.c_void_p, D, D, D, D]),
+    "cmpc_recover_trajectory": (C.c_int, [C.c_void_p, D, D, D, D]),
     "cmpc_debug_syrk_timeline": (C.c_int, [C.c_void_p, D, C.c_int64, I64]),
     "cmpc_update_qp_affine": (C.c_int, [C.c_void_p, D, C.c_double, D, C.c_int]),
     "cmpc_set_state": (C.c_int, [C.c_void_p, D, D, D, D, C.c_double]),

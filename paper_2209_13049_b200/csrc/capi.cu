@@ -112,6 +112,66 @@ struct SegvInstall {
 } g_segv_install;
 }  // namespace
 
+namespace {
+// load a QP into the context; adopt = take ownership of the device buffers H, h, J, d
+// (the device builder) instead of copying them
+int load_impl(Ctx& c, int64_t n, int64_t m, const double* H, const double* h, double h0,
+              const double* J, const double* d, int on_device, bool adopt) {
+  return guard([&] {
+    if (n < 0 || m < 0) throw DimError("negative dimensions");
+    if (m > (int64_t(1) << 29) || n > (int64_t(1) << 24)) throw DimError("QP too large");
+    CMPC_CUDA(cudaSetDevice(c.device));
+    const double t_in = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    release_qp(c);
+    if (getenv("CMPC_VERBOSE"))
+      fprintf(stderr, "[cmpc load] release    %8.2f ms\n",
+              (std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count() - t_in) * 1e3);
+    c.n = n;
+    c.m = m;
+    c.h0 = h0;
+    const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    c.owns_J = true;
+    if (adopt) {
+      c.H = const_cast<double*>(H);
+      c.h = const_cast<double*>(h);
+      c.J = const_cast<double*>(J);
+      c.d = const_cast<double*>(d);
+    } else {
+      c.H = dev_alloc<double>((size_t)(n * n), c.stream);
+      c.h = dev_alloc<double>((size_t)n, c.stream);
+      c.J = dev_alloc<double>((size_t)(m * n), c.stream);
+      c.d = dev_alloc<double>((size_t)m, c.stream);
+      if (n * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.H, H, sizeof(double) * n * n, kind, c.stream));
+      if (n > 0) CMPC_CUDA(cudaMemcpyAsync(c.h, h, sizeof(double) * n, kind, c.stream));
+      if (m * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.J, J, sizeof(double) * m * n, kind, c.stream));
+      if (m > 0) CMPC_CUDA(cudaMemcpyAsync(c.d, d, sizeof(double) * m, kind, c.stream));
+    }
+    const bool verbose = getenv("CMPC_VERBOSE") != nullptr;
+    double last = t_in;
+    auto tick = [&](const char* what) {
+      if (!verbose) return;
+      sync(c);
+      const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+      if (what) fprintf(stderr, "[cmpc load] %-10s %8.2f ms\n", what, (now - last) * 1e3);
+      last = now;
+    };
+    tick("h2d");
+    analyze_structure(c);
+    tick("analyze");
+    // the dense J is not read again: every product goes through P
+    dev_free(c.J, c.stream);
+    c.J = nullptr;
+    syrk_plan(c);
+    tick("plan");
+    vec_alloc(c);
+    sync(c);
+    tick("alloc");
+    return CMPC_OK;
+  });
+}
+
+}  // namespace
+
 extern "C" {
 
 int cmpc_abi_version(void) { return 1; }
@@ -147,6 +207,7 @@ void cmpc_ctx_destroy(cmpc_ctx* x) {
   } catch (...) {
   }
   release_qp(x->c);
+  prob_free(x->c);
   cudaStreamSynchronize(x->c.stream);
   cudaEventDestroy(x->c.ev0);
   cudaEventDestroy(x->c.ev1);
@@ -161,50 +222,71 @@ void cmpc_ctx_destroy(cmpc_ctx* x) {
 
 int cmpc_load_qp(cmpc_ctx* x, int64_t n, int64_t m, const double* H, const double* h, double h0,
                  const double* J, const double* d, int on_device) {
+  if (!x) {
+    g_error = "null context (closed?)";
+    return CMPC_ERR_DIM;
+  }
+  prob_free(x->c);  // a bare QP: no structured problem behind it
+  return load_impl(x->c, n, m, H, h, h0, J, d, on_device, false);
+}
+
+int cmpc_build_qp(cmpc_ctx* x, const cmpc_lq_problem* p) {
+  if (!x || !p) {
+    g_error = "null context or problem";
+    return CMPC_ERR_DIM;
+  }
+  double *H = nullptr, *h = nullptr, *J = nullptr, *d = nullptr;
+  double h0 = 0.0;
+  int64_t m = 0;
+  const int rc = guard([&] {
+    CMPC_CUDA(cudaSetDevice(x->c.device));
+    prob_build(x->c, *p, &H, &h, &h0, &J, &d, &m);
+    return CMPC_OK;
+  });
+  if (rc) return rc;
+  return load_impl(x->c, p->T * p->nu, m, H, h, h0, J, d, 1, true);
+}
+
+int cmpc_get_qp(cmpc_ctx* x, double* H, double* h, double* h0, double* d) {
   return guard([&] {
     if (!x) throw DimError("null context (closed?)");
     Ctx& c = x->c;
-    if (n < 0 || m < 0) throw DimError("negative dimensions");
-    if (m > (int64_t(1) << 29) || n > (int64_t(1) << 24)) throw DimError("QP too large");
-    CMPC_CUDA(cudaSetDevice(c.device));
-    const double t_in = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-    release_qp(c);
-    if (getenv("CMPC_VERBOSE"))
-      fprintf(stderr, "[cmpc load] release    %8.2f ms\n",
-              (std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count() - t_in) * 1e3);
-    c.n = n;
-    c.m = m;
-    c.h0 = h0;
-    const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    c.H = dev_alloc<double>((size_t)(n * n), c.stream);
-    c.h = dev_alloc<double>((size_t)n, c.stream);
-    c.J = dev_alloc<double>((size_t)(m * n), c.stream);
-    c.d = dev_alloc<double>((size_t)m, c.stream);
-    c.owns_J = true;
-    if (n * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.H, H, sizeof(double) * n * n, kind, c.stream));
-    if (n > 0) CMPC_CUDA(cudaMemcpyAsync(c.h, h, sizeof(double) * n, kind, c.stream));
-    if (m * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.J, J, sizeof(double) * m * n, kind, c.stream));
-    if (m > 0) CMPC_CUDA(cudaMemcpyAsync(c.d, d, sizeof(double) * m, kind, c.stream));
-    const bool verbose = getenv("CMPC_VERBOSE") != nullptr;
-    double last = t_in;
-    auto tick = [&](const char* what) {
-      if (!verbose) return;
-      sync(c);
-      const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-      if (what) fprintf(stderr, "[cmpc load] %-10s %8.2f ms\n", what, (now - last) * 1e3);
-      last = now;
-    };
-    tick("h2d");
-    analyze_structure(c);
-    tick("analyze");
-    // the dense J is not read again: every product goes through P
-    dev_free(c.J, c.stream);
-    c.J = nullptr;
-    syrk_plan(c);
-    tick("plan");
-    vec_alloc(c);
+    require_loaded(c);
+    d2h(c, H, c.H, c.n * c.n);
+    d2h(c, h, c.h, c.n);
+    d2h(c, d, c.d, c.m);
+    if (h0) *h0 = c.h0;
     sync(c);
-    tick("alloc");
+    return CMPC_OK;
+  });
+}
+
+int cmpc_refresh_initial_state(cmpc_ctx* x, const double* x_bar) {
+  return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
+    Ctx& c = x->c;
+    require_loaded(c);
+    prob_refresh(c, x_bar);
+    launch_hmax(c);
+    sync(c);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_recover_trajectory(cmpc_ctx* x, const double* v, double* xs, double* us, double* objective) {
+  return guard([&] {
+    if (!x) throw DimError("null context (closed?)");
+    Ctx& c = x->c;
+    require_loaded(c);
+    const double* vd = c.v;
+    double* tmp = nullptr;
+    if (v) {
+      tmp = dev_alloc<double>(size_t(std::max<int64_t>(c.n, 1)), c.stream);
+      if (c.n > 0) CMPC_CUDA(cudaMemcpyAsync(tmp, v, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
+      vd = tmp;
+    }
+    prob_recover(c, vd, xs, us, objective);
+    dev_free(tmp, c.stream);
     return CMPC_OK;
   });
 }

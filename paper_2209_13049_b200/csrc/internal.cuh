@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "../../include/condmpc_cuda.h"
 
 namespace cmpc {
 
@@ -48,6 +49,7 @@ static_assert(offsetof(Packet, alpha_z_min) == offsetof(Packet, alpha_s_min) + 8
 static_assert(offsetof(Packet, t_sum_abs) == offsetof(Packet, t_sum_log) + 8, "packet layout");
 
 struct Workspace;
+struct ProblemDev;
 
 struct Ctx {
   int device = 0;
@@ -57,6 +59,7 @@ struct Ctx {
   int64_t m_all = -1;    // rows of the whole QP (kkt scaling); -1 = m
   cudaStream_t stream = nullptr;
   bool owns_stream = true;
+  void* prob = nullptr;  // ProblemDev (builder.cu): the structured problem behind a device-built QP
 
   int64_t n = 0, m = 0;
   double h0 = 0.0;
@@ -203,6 +206,13 @@ void launch_recover(Ctx& c, double tau);
 // alpha_from_device the step is alpha_max = min(1, packet tau-ratio minimum)
 // linear: J v_t from the current point's and the direction's prototype values (yv + alpha y,
 // valid inside the host loop after launch_residuals and launch_recover) instead of a P pass
+// builder.cu
+void prob_build(Ctx& c, const cmpc_lq_problem& in, double** H, double** h, double* h0, double** J,
+                double** d, int64_t* m);
+void prob_refresh(Ctx& c, const double* x_bar);
+void prob_recover(Ctx& c, const double* v_dev, double* x, double* u, double* obj);
+void prob_free(Ctx& c);
+
 void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear = false);
 // line-search derivative pieces for externally set directions: (Hv+h).pv, sum ps/s
 void launch_ls_pieces(Ctx& c);

@@ -10,6 +10,7 @@ are the host-side scalar rules (identical to the C++ loop's).
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import enum
 import time
 from dataclasses import dataclass, field
@@ -139,6 +140,71 @@ class DeviceQp:
         else:
             check(L.cmpc_load_qp(self.h, qp.n, qp.m, ptr(qp.H), ptr(qp.h), qp.h0, ptr(qp.J),
                                  ptr(qp.d), 0))
+
+    @classmethod
+    def from_problem(cls, data, device: int | None = None) -> "DeviceQp":
+        """build_dense_qp (reduction.cpp:255-268) on the device: only the
+        structured data crosses PCIe; the dense J is formed and analysed in HBM."""
+        from . import problem as P
+        dm = P.dims(data)
+        L = _lib.lib()
+        device = _linalg.DEVICE if device is None else device
+        out = cls.__new__(cls)
+        h = C.c_void_p()
+        check(L.cmpc_ctx_create(C.byref(h), device))
+        out.h = h
+        keep = {}
+
+        def arr(name, a, order="F"):
+            a = np.asarray(a, dtype=np.float64)
+            a = np.asfortranarray(a) if order == "F" else np.ascontiguousarray(a)
+            keep[name] = a
+            return a.ctypes.data_as(_lib.D) if a.size else None
+
+        pr = _lib.LqProblem(nx=dm.n_x, nu=dm.n_u, nc=dm.n_c, T=dm.T)
+        for f in ("A", "B", "Q", "Qf", "R", "S", "E", "F", "K"):
+            setattr(pr, f, arr(f, getattr(data, f)))
+        for f in ("gl", "gu", "xl", "xu", "ul", "uu", "x_bar"):
+            setattr(pr, f, arr(f, getattr(data, f), "C"))
+        pr.w = arr("w", data.w, "C")
+        check(L.cmpc_build_qp(out.h, C.byref(pr)))
+        info = (C.c_int64 * 8)()
+        L.cmpc_qp_info(out.h, info)
+        out.n, out.m = int(info[0]), int(info[1])
+        out.source = data
+        return out
+
+    def get_qp(self):
+        """(H, h, h0, d) of the loaded QP, read back from the device."""
+        H = np.zeros((self.n, self.n), order="F")
+        h, d, h0 = np.zeros(self.n), np.zeros(self.m), np.zeros(1)
+        check(_lib.lib().cmpc_get_qp(self.h, ptr(H), ptr(h), ptr(h0), ptr(d)))
+        return H, h, float(h0[0]), d
+
+    def refresh_initial_state(self, x_bar):
+        """refresh_initial_state (reduction.cpp:270-280) on the device."""
+        xb = np.ascontiguousarray(np.asarray(x_bar, dtype=np.float64))
+        check(_lib.lib().cmpc_refresh_initial_state(self.h, ptr(xb)))
+        self.source = dataclasses.replace(self.source, x_bar=xb.copy())
+
+    def recover_trajectory(self, v=None) -> "Trajectory":
+        """recover_trajectory (reduction.cpp:282-314) on the device (v None: the last solve's)."""
+        from . import problem as P
+        dm = P.dims(self.source)
+        x = np.zeros((dm.T + 1, dm.n_x))
+        u = np.zeros((dm.T, dm.n_u))
+        obj = np.zeros(1)
+        vv = None if v is None else np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+        check(_lib.lib().cmpc_recover_trajectory(self.h, ptr(vv), ptr(x), ptr(u), ptr(obj)))
+        return P.Trajectory(x=x, u=u, v=None if v is None else vv.reshape(dm.T, dm.n_u).copy(),
+                            objective=float(obj[0]))
+
+    def solve(self, opts: "IpmOptions" = None) -> "IpmResult":
+        """ipm::solve on the loaded QP; the trajectory is recovered on the device when the
+        QP was built there."""
+        opts = opts or IpmOptions()
+        _check_options(opts)
+        return solve_loaded(self, None, opts)
 
     def close(self):
         if getattr(self, "h", None):
@@ -340,6 +406,16 @@ def check_termination(res: Residuals, state: IpmState, opts: IpmOptions) -> Term
 
 
 # ------------------------------------------------------------------ solve
+def solve_problem(data, opts: IpmOptions = None) -> IpmResult:
+    """build_dense_qp + ipm::solve + recover_trajectory, all on the device (SURVEY §8(f)
+    rows 1 and 3): the structured problem in, the trajectory out."""
+    dq = DeviceQp.from_problem(data)
+    try:
+        return dq.solve(opts)
+    finally:
+        dq.close()
+
+
 def solve(qp: DenseQp, opts: IpmOptions = None) -> IpmResult:
     """ipm.cpp:160-268: the whole solve on the device, host loop in C++."""
     opts = opts or IpmOptions()
@@ -355,9 +431,9 @@ def solve(qp: DenseQp, opts: IpmOptions = None) -> IpmResult:
     return solve_loaded(dq, qp, opts, t0)
 
 
-def solve_loaded(dq: DeviceQp, qp: DenseQp, opts: IpmOptions, t0=None) -> IpmResult:
+def solve_loaded(dq: DeviceQp, qp: DenseQp | None, opts: IpmOptions, t0=None) -> IpmResult:
     t0 = time.perf_counter() if t0 is None else t0
-    n, m = qp.n, qp.m
+    n, m = (qp.n, qp.m) if qp is not None else (dq.n, dq.m)
     v, s, l, z = np.zeros(n), np.zeros(m), np.zeros(m), np.zeros(m)
     out = np.zeros(13)
     L = _lib.lib()
@@ -383,7 +459,10 @@ def solve_loaded(dq: DeviceQp, qp: DenseQp, opts: IpmOptions, t0=None) -> IpmRes
                     device_seconds=float(out[6]), launches=int(out[7]), syncs=int(out[8]),
                     trials=int(out[9]), syrk_seconds=float(out[10]), chol_seconds=float(out[11]),
                     condensations=int(out[12]))
-    if qp.source is not None:
+    if qp is None and getattr(dq, "source", None) is not None:
+        res.solution = dq.recover_trajectory()
+        res.solution.v = v.reshape(res.solution.u.shape).copy()
+    elif qp is not None and qp.source is not None:
         res.solution = recover_trajectory(qp, v)
     else:
         res.solution = Trajectory(objective=res.objective)
