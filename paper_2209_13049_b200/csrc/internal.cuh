@@ -96,6 +96,7 @@ struct Ctx {
   int32_t* tile_ptr = nullptr;    // ntiles+1 into tile_units
   int32_t* tile_units = nullptr;  // segment ids per tile in k order (| 1 << 31: thin, rows 0..31 only)
   double* partial = nullptr;      // nunits x 64 x 64
+  double* rhs_part = nullptr;     // nunits x 128: fused P' q half-sums of the diagonal segments
   long long* syrk_prof = nullptr; // debug timeline: {start ns, end ns, smid} per piece (null: off)
   std::vector<double> syrk_cta_cost;  // per piece: segments, k steps per shape (debug timeline)
   void* tmap_P = nullptr;         // CUtensorMap (128 B), host copy passed by value: box {16, 64}
@@ -153,7 +154,7 @@ void free_structure(Ctx& c);
 // ---- syrk.cu
 void syrk_plan(Ctx& c);
 // M(lower) = H + P' diag(omega) P + diag(dsing); writes full symmetric M when mirror
-void launch_condense(Ctx& c, bool mirror);
+void launch_condense(Ctx& c, bool mirror, bool with_rhs = false);
 void syrk_free(Ctx& c);
 
 // ---- chol.cu
@@ -213,6 +214,7 @@ void prob_refresh(Ctx& c, const double* x_bar);
 void prob_recover(Ctx& c, const double* v_dev, double* x, double* u, double* obj);
 void prob_free(Ctx& c);
 
+void launch_debug_sum(Ctx& c, const double* x, int64_t n, int slot);
 void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear = false);
 // line-search derivative pieces for externally set directions: (Hv+h).pv, sum ps/s
 void launch_ls_pieces(Ctx& c);

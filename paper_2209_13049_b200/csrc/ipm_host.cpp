@@ -73,38 +73,33 @@ void rec(cudaEvent_t e, cudaStream_t s) {
     CMPC_CUDA(cudaEventRecord(e, s));
 }
 
-// segment A: sigma/omega/q, condensation with the right-hand side J'(r2 - sigma r3) on a
-// parallel branch, Cholesky (delta = 0) fused with the solve, recovery + fraction to
-// boundary, trial 0
+// segment A: sigma/omega/q, condensation with the right-hand side J'(r2 - sigma r3) fused
+// into the SYRK (its diagonal jobs stream every nonzero row of P), Cholesky (delta = 0)
+// fused with the solve, recovery + fraction to boundary, trial 0
 void seg_step(Ctx& c, double tau) {
   rec(c.ev0, c.stream);
   launch_prepare_step(c, nullptr);
-  CMPC_CUDA(cudaEventRecord(c.fork, c.stream));
-  CMPC_CUDA(cudaStreamWaitEvent(c.stream2, c.fork, 0));
-  {
-    cudaStream_t s0 = c.stream;
-    c.stream = c.stream2;
-    // memory-bound pass, overlaps the tensor-core SYRK (sharded: the partial only; the
-    // collectives stay on the main stream, one communicator, one issue order)
-    if (c.comm) launch_rhs_partial(c);
-    else launch_rhs(c);
-    c.stream = s0;
-  }
-  CMPC_CUDA(cudaEventRecord(c.join, c.stream2));
+  const bool fused = c.ps > 0 && c.npieces > 0;
+  if (!fused) launch_rhs_partial(c);  // no SYRK rows: the singleton part only
   rec(c.ev2, c.stream);
-  launch_condense(c, false);
+  launch_condense(c, false, fused);
   rec(c.ev3, c.stream);
-  CMPC_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
   if (c.comm) {  // M = H + sum_g J_g' Sigma_g J_g and J' (r2 - sigma r3) over all ranks
     comm_group(true);
     comm_allreduce(c, c.M, (size_t)(c.n * c.n), CommType::f64, CommOp::sum);
     comm_allreduce(c, c.rhs, (size_t)c.n, CommType::f64, CommOp::sum);
     comm_group(false);
-    launch_rhs_final(c);
   }
+  launch_rhs_final(c);
+  launch_debug_sum(c, c.M, c.n * c.n, 0);
+  launch_debug_sum(c, c.rhs, c.n, 1);
+  launch_debug_sum(c, c.omega, c.ldp + c.pz, 4);
   launch_cholesky(c, c.M, c.L, 0.0, c.rhs, c.pv);  // factor + both triangular solves
+  launch_debug_sum(c, c.pv, c.n, 2);
+  launch_debug_sum(c, c.L, c.n * c.n, 5);
   rec(c.ev1, c.stream);
   launch_recover(c, tau);
+  launch_debug_sum(c, c.ps_, c.m, 3);
   launch_trial(c, 0.0, true, /*linear=*/true);
   launch_publish(c);
 }
@@ -317,6 +312,11 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
       linalg += ms * 1e-3;
     }
     const Packet B = *c.pk_host;
+    static const bool debug_sums = getenv("CMPC_DEBUG_SUMS") != nullptr;
+    if (debug_sums) {  // per-iteration checksums of the step's buffers (tools/race_sums.py)
+      const unsigned long long* u = reinterpret_cast<const unsigned long long*>(B.pad);
+      fprintf(stderr, "[sums] %p %d M %016llx rhs %016llx pv %016llx ps %016llx omega %016llx L %016llx\n", (void*)&c, (int)iter, u[0], u[1], u[2], u[3], u[4], u[5]);
+    }
     A.kkt = B.kkt;  // kkt at the (possibly new) barrier value, as the reference's res
     A.max_comp = B.max_comp;
     if (shift == kShifts.size()) {

@@ -52,7 +52,10 @@ struct SyrkArgs {
   int npieces;
   unsigned* ctl;             // [0] next piece, [1] retired CTAs (both 0 between launches)
   double* partial;           // per segment: 64 x 64 column-major partial tile
+  const double* q;           // fused right-hand side: P' q over the diagonal jobs (null: off)
+  double* rhs_part;          // per segment: 2 x 64 half-sums of P' q (diagonal segments)
   long long* prof;           // debug: per piece {start ns, end ns, smid}
+  int static_sched;          // debug: CTA b takes pieces b, b + grid, ... (no counter)
 };
 
 // byte offset of element (col c, k) inside a 32 x 64 operand tile (two swizzled boxes)
@@ -121,6 +124,10 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
     for (int b = 0; b < 2; ++b)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[f][b][c] = 0.0;
+  // fused right-hand side: a diagonal job streams every nonzero row of its column block, so
+  // thread (kh, cc) also sums P(k, cc) q(k) over its half of each stage's 32 rows
+  double rq = 0.0;
+  const bool do_rq = DIAG && a.q != nullptr && (!THIN || (threadIdx.x & 63) < 32);
 
   for (int it = it0; it < it0 + nsteps; ++it) {
     const int s = it % kStages;
@@ -130,6 +137,12 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
     const uint32_t sA = smem_u32(smem + s * kStageBytes);
     const uint32_t sB = DIAG ? sA : sA + kOpBytes;
     const uint32_t sW = sA + 2 * kOpBytes;
+    if (DIAG && do_rq) {
+      const int cc = threadIdx.x & 63, k0 = 16 * (threadIdx.x >> 6);
+      const uint32_t sQ = sW + 256;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) rq = fma(lds64(sA + op_off(cc, k0 + kk)), lds64(sQ + 8 * (k0 + kk)), rq);
+    }
 #pragma unroll
     for (int ks = 0; ks < kBK; ks += 16) {
       double af[2][8], ax[2][8];  // A fragments of half r0 (ax: half 0 for the mixed warp)
@@ -163,6 +176,7 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   store_partial<NF>(a, sg, acc, fr, fn, lane);
+  if (DIAG && a.q) a.rhs_part[(size_t)sg * 128 + threadIdx.x] = rq;
 }
 
 // 2 CTAs per SM: 168 registers (each SM sub-partition holds 3 warps of 168 x 32; the few
@@ -200,7 +214,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
       for (int i = 0;; ++i) {
         const int slot = i & 1;
         if (i >= 2) mbar_wait(&pempty[slot], ((i >> 1) & 1) ^ 1);
-        int p = (int)atomicAdd(a.ctl, 1u);
+        int p = a.static_sched ? (int)(blockIdx.x + (unsigned)i * gridDim.x) : (int)atomicAdd(a.ctl, 1u);
         if (p >= a.npieces) p = -1;
         ring[slot] = p;
         mbar_arrive(&pfull[slot]);
@@ -210,11 +224,19 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
           const int ti = u.x & 1023, tj = (u.x >> 10) & 1023;
           const bool thin = (u.x >> 20) & 1, diag = ti == tj;
           const uint32_t abytes = thin ? kOpBytes / 2 : kOpBytes;
-          const uint32_t bytes = abytes + (diag ? 0u : (uint32_t)kOpBytes) + kBK * 8;
+          const bool with_q = diag && a.q != nullptr;
+          const uint32_t bytes = abytes + (diag ? 0u : (uint32_t)kOpBytes) + kBK * 8 + (with_q ? kBK * 8 : 0u);
           const void* tmA = thin ? (const void*)&tmP32 : (const void*)&tmP;
           for (int kk = u.y; kk < u.z; kk += kBK, ++it) {
             const int s = it % kStages;
-            if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+            if (it >= kStages) {
+              mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+              // the consumers' generic-proxy reads of this stage (ordered before us by the
+              // barrier) must also precede our async-proxy (TMA) rewrite of it: without this
+              // fence a slow lane could still read the stage as the next tile lands (seen
+              // under SM contention, tests/test_gpu_concurrency.py)
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
             unsigned char* st = smem + s * kStageBytes;
             mbar_expect_tx(&full[s], bytes);
             // a 32-column box lands exactly where the first 32 columns of a 64-column box would
@@ -225,6 +247,7 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
               tma_load_2d(st + kOpBytes + kBoxBytes, &tmP, kk + 16, 64 * tj, &full[s]);
             }
             bulk_load(st + 2 * kOpBytes, a.omega + kk, kBK * 8, &full[s]);
+            if (with_q) bulk_load(st + 2 * kOpBytes + 256, a.q + kk, kBK * 8, &full[s]);
           }
         }
       }
@@ -285,9 +308,25 @@ __global__ void __launch_bounds__(256)
     k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
                   const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ tile_segs,
                   const double* __restrict__ H, const double* __restrict__ dsing, int64_t n,
-                  double* __restrict__ M, int mirror) {
+                  double* __restrict__ M, int mirror, const double* __restrict__ rp,
+                  const double* __restrict__ qs, const int32_t* __restrict__ sing_ptr,
+                  const double* __restrict__ sing_val, double* __restrict__ rhs) {
   const int2 tl = tiles[blockIdx.x];
   const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
+  if (rp && tl.x == tl.y && blockIdx.y == 0 && threadIdx.x < kTile) {
+    // fused right-hand side of the block: P' q from the diagonal segments' half-sums (in
+    // k order) + the singleton rows of its columns
+    const int64_t col = (int64_t)kTile * tl.x + threadIdx.x;
+    if (col < n) {
+      double s = 0.0;
+      for (int q = u0; q < u1; ++q) {
+        const int32_t id = tile_segs[q] & 0x7fffffff;
+        s += __ldcg(rp + (size_t)id * 128 + threadIdx.x) + __ldcg(rp + (size_t)id * 128 + 64 + threadIdx.x);
+      }
+      for (int32_t k = sing_ptr[col]; k < sing_ptr[col + 1]; ++k) s += sing_val[k] * qs[k];
+      rhs[col] = s;
+    }
+  }
   const int e = blockIdx.y * blockDim.x + threadIdx.x;
   const int rl = e & (kTile - 1), cl = e >> 6;
   const int64_t i = (int64_t)kTile * tl.x + rl, j = (int64_t)kTile * tl.y + cl;
@@ -334,7 +373,7 @@ PFN_encodeTiled get_encode() {
 
 void syrk_free(Ctx& c) {
   for (void* p : {(void*)c.units, (void*)c.cta_ptr, (void*)c.syrk_ctl, (void*)c.tiles,
-                  (void*)c.tile_ptr, (void*)c.tile_units, (void*)c.partial})
+                  (void*)c.tile_ptr, (void*)c.tile_units, (void*)c.partial, (void*)c.rhs_part})
     dev_free(p, c.stream);
   c.units = nullptr;
   c.cta_ptr = nullptr;
@@ -342,6 +381,7 @@ void syrk_free(Ctx& c) {
   c.tiles = nullptr;
   c.tile_ptr = c.tile_units = nullptr;
   c.partial = nullptr;
+  c.rhs_part = nullptr;
   delete[] reinterpret_cast<unsigned char*>(c.tmap_P);
   delete[] reinterpret_cast<unsigned char*>(c.tmap_P32);
   c.tmap_P = c.tmap_P32 = nullptr;
@@ -496,6 +536,7 @@ void syrk_plan(Ctx& c) {
   c.tile_ptr = dev_alloc<int32_t>(tptr.size(), st);
   c.tile_units = dev_alloc<int32_t>(std::max<size_t>(1, tsegs.size()), st);
   c.partial = dev_alloc<double>((size_t)kTile * kTile * std::max<size_t>(1, segs.size()), st);
+  c.rhs_part = dev_zeros<double>((size_t)128 * std::max<size_t>(1, segs.size()), st);
   if (!segs.empty())
     CMPC_CUDA(cudaMemcpyAsync(c.units, segs.data(), sizeof(int4) * segs.size(), cudaMemcpyHostToDevice, st));
   CMPC_CUDA(cudaMemcpyAsync(c.cta_ptr, pptr.data(), sizeof(int32_t) * pptr.size(), cudaMemcpyHostToDevice, st));
@@ -533,15 +574,20 @@ void syrk_plan(Ctx& c) {
   }
 }
 
-void launch_condense(Ctx& c, bool mirror) {
+void launch_condense(Ctx& c, bool mirror, bool with_rhs) {
+  with_rhs = with_rhs && c.ps > 0 && c.npieces > 0;
   SyrkArgs a;
   a.omega = c.omega;
+  a.q = with_rhs ? c.q : nullptr;
+  a.rhs_part = c.rhs_part;
   a.segs = c.units;
   a.piece_ptr = c.cta_ptr;
   a.npieces = c.npieces;
   a.ctl = c.syrk_ctl;
   a.partial = c.partial;
   a.prof = c.syrk_prof;
+  static const int stat = getenv("CMPC_SYRK_STATIC") ? atoi(getenv("CMPC_SYRK_STATIC")) : 0;
+  a.static_sched = stat;
   if (c.npieces > 0) {
     const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(c.tmap_P);
     const CUtensorMap* tm32 = reinterpret_cast<const CUtensorMap*>(c.tmap_P32);
@@ -551,7 +597,7 @@ void launch_condense(Ctx& c, bool mirror) {
   // sharded: every rank's partial J_g' Sigma_g J_g, H added by rank 0; the caller allreduces
   k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 256), 256, 0, c.stream>>>(
       c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr, c.dsing, c.n, c.M,
-      mirror ? 1 : 0);
+      mirror ? 1 : 0, with_rhs ? c.rhs_part : nullptr, c.q + c.ldp, c.sing_ptr, c.sing_val, c.rhs);
   CMPC_LAUNCHED();
 }
 

@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, i
                                                      const double* __restrict__ Jtl,
                                                      const double* __restrict__ v,
                                                      double* __restrict__ r1,
-                                                     const double* __restrict__ part, double h0,
+                                                     const double* __restrict__ part,
                                                      const double* __restrict__ hmax, Packet* pk,
                                                      int mode) {
   __shared__ double sh[32];
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, i
     pk->sum_abs_r3 = m_all > 0 ? sabs : 0.0;
     pk->sum_log_s = m_all > 0 ? slog : 0.0;
     pk->max_h = *hmax;
-    pk->objective = 0.5 * vhv + hv + h0;
+    pk->objective = 0.5 * vhv + hv + hmax[1];  // h0 on the device: graphs outlive an h0 change
     const double ds = fmax(1.0, fmax(*hmax, pk->max_lam) / (double)(n + m_all));
     double kkt = a / ds;
     if (m_all > 0) {
@@ -741,7 +741,7 @@ void vec_alloc(Ctx& c) {
   const int rc = 2048;
   c.colchunks = (int)std::max<int64_t>(1, ceil_div(c.ps, rc));
   c.colpart = dev_zeros<double>((size_t)c.colchunks * n, c.stream);
-  c.hmax = dev_zeros<double>(1, c.stream);
+  c.hmax = dev_zeros<double>(2, c.stream);  // max|h|, h0
   c.d_mu = dev_zeros<double>(1, c.stream);
   c.d_alpha = dev_zeros<double>(2, c.stream);
   c.pk = dev_zeros<Packet>(1, c.stream);
@@ -755,10 +755,7 @@ void vec_alloc(Ctx& c) {
   c.pub_dev = dev_zeros<unsigned long long>(1, c.stream);
   c.pub_expect = 0;
   chol_alloc(c);
-  if (c.n > 0) {
-    k_absmax<<<(unsigned)std::min<int64_t>(64, ceil_div(c.n, 256)), 256, 0, c.stream>>>(c.h, c.n, c.hmax);
-    CMPC_LAUNCHED();
-  }
+  launch_hmax(c);  // max|h| and h0 on the device
   {  // prototypes with many member rows (duplicates of symmetric segments): warp path
     std::vector<int32_t> mp(size_t(c.p + 1), 0), big;
     if (c.p > 0) {
@@ -851,6 +848,22 @@ void launch_proto_reduce(Ctx& c, const double* x1, const double* x2, double* out
   CMPC_LAUNCHED();
 }
 
+// debug (CMPC_DEBUG_SUMS): order-free XOR checksum of a buffer's bit patterns into pk->pad[slot]
+__global__ void k_xorsum(const double* __restrict__ x, int64_t n, Packet* pk, int slot) {
+  unsigned long long v = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v ^= (unsigned long long)__double_as_longlong(x[i]) * (unsigned long long)(2 * i + 1);
+  for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicXor(reinterpret_cast<unsigned long long*>(&pk->pad[slot]), v);
+}
+void launch_debug_sum(Ctx& c, const double* x, int64_t n, int slot) {
+  static const bool on = getenv("CMPC_DEBUG_SUMS") != nullptr;
+  if (!on || n <= 0) return;
+  CMPC_CUDA(cudaMemsetAsync(&c.pk->pad[slot], 0, sizeof(double), c.stream));
+  k_xorsum<<<64, 256, 0, c.stream>>>(x, n, c.pk, slot);
+  CMPC_LAUNCHED();
+}
+
 void launch_zero_packet(Ctx& c) {
   CMPC_CUDA(cudaMemsetAsync(c.pk, 0, sizeof(Packet), c.stream));
 }
@@ -922,7 +935,7 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
   if (c.comm) {
     // this rank's rows: J_g' lambda_g, the row sums and maxima -> allreduce -> finalize
     k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part,
-                                           c.h0, c.hmax, c.pk, 1);
+                                           c.hmax, c.pk, 1);
     CMPC_LAUNCHED();
     comm_group(true);
     comm_allreduce(c, c.Jtl, (size_t)c.n, CommType::f64, CommOp::sum);
@@ -930,7 +943,7 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
     comm_allreduce(c, &c.pk->max_r3, 5, CommType::f64, CommOp::max);     // max_r3 .. max_z
     comm_group(false);
   }
-  k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part, c.h0,
+  k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part,
                                          c.hmax, c.pk, c.comm ? 2 : 0);
   CMPC_LAUNCHED();
 }
@@ -982,20 +995,23 @@ void launch_rhs(Ctx& c) {
   launch_rhs_final(c);
 }
 
-void launch_hmax(Ctx& c) {
-  CMPC_CUDA(cudaMemsetAsync(c.hmax, 0, sizeof(double), c.stream));
-  if (c.n > 0) {
-    k_absmax<<<(unsigned)std::min<int64_t>(64, ceil_div(c.n, 256)), 256, 0, c.stream>>>(c.h, c.n, c.hmax);
-    CMPC_LAUNCHED();
-  }
-}
-
 // a slot of the pinned staging ring (64 doubles, 2 per slot): the host loop synchronises
 // with the stream between segments, so a slot is never reused while its copy is pending
 double* stage_slot(Ctx& c, int) {
   double* p = c.stage + 2 * (c.stage_i & 31);
   ++c.stage_i;
   return p;
+}
+
+void launch_hmax(Ctx& c) {
+  CMPC_CUDA(cudaMemsetAsync(c.hmax, 0, sizeof(double), c.stream));
+  double* st = stage_slot(c, 1);
+  st[0] = c.h0;
+  CMPC_CUDA(cudaMemcpyAsync(c.hmax + 1, st, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  if (c.n > 0) {
+    k_absmax<<<(unsigned)std::min<int64_t>(64, ceil_div(c.n, 256)), 256, 0, c.stream>>>(c.h, c.n, c.hmax);
+    CMPC_LAUNCHED();
+  }
 }
 
 void set_mu(Ctx& c, double mu) {
