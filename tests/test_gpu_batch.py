@@ -43,11 +43,13 @@ def test_config5_batch_slice():
     bs = ipm.BatchSolver(base, len(insts))
     for i, q in enumerate(insts):
         bs.set_instance(i, q.h, q.h0, q.d)
-    res = bs.solve()
+    res = bs.solve(threads=2)  # two workers: each solves several instances in turn
     assert all(s == "converged" for s in res.status)
-    for i in (0, 7):
+    for i in (0, 3, 7):
         single = ipm.solve(insts[i])
         assert res.iter[i] == single.iter and rel(res.v[i], single.v) <= 1e-14
+        # h0 differs per instance; a worker context replays graphs captured for an earlier one
+        assert abs(res.objective[i] - single.objective) <= 1e-12 * (1 + abs(single.objective))
 
 
 def test_batch_solvers_can_be_created_again_on_the_same_base():
