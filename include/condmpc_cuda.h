@@ -70,7 +70,7 @@ int cmpc_recover_trajectory(cmpc_ctx* ctx, const double* v, double* x, double* u
 int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out);
 /* Solve `count` loaded contexts concurrently: a pool of `threads` host threads, each driving
  * its contexts' own streams (the GPU overlaps the instances). v_out: count x n (nullable),
- * scal_out: count x 13 (cmpc_solve's out_scalars per instance). */
+ * scal_out: count x 14 (cmpc_solve's out_scalars per instance). */
 int cmpc_solve_batch(cmpc_ctx** ctxs, int64_t count, const double* opts, int64_t max_iter,
                      double* v_out, double* scal_out, int threads);
 /* Solve `count` instances sharing H and J (config 5): h_all count x n, h0_all count,
@@ -124,10 +124,11 @@ int cmpc_dense_objective(cmpc_ctx* ctx, double* obj);
 
 /* ipm::solve (ipm.cpp:160-268) on the loaded QP.
  * opts[5] = tol, mu_init, kappa_mu, tau, armijo_eta.
- * out_scalars[13] = status (0 converged, 1 max_iter, 2 factorization_failure,
+ * out_scalars[14] = status (0 converged, 1 max_iter, 2 factorization_failure,
  *   3 line_search_failure), iter, kkt_error, objective, total_seconds, linalg_seconds,
- *   device_seconds, launches, syncs, trials, condensation (SYRK) seconds, Cholesky seconds,
- *   condensations; the per-phase times are CUDA events on the solve's stream.
+ *   device_seconds, launches, syncs, trials, condensation (SYRK + reduce) seconds, Cholesky
+ *   seconds, condensations, SYRK kernel seconds; the per-phase times are CUDA events on the
+ *   solve's stream.
  * log(user, rec[8]) per accepted step: iter, mu, alpha, alpha_z, kkt_error, objective,
  *   delta, trial (IterationRecord, ipm.hpp:41-49, plus the shift and trial index).
  * inspect(...) per iteration before the line search (IterationInspection, ipm.hpp:53-58);

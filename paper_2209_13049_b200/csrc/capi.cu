@@ -189,6 +189,7 @@ int cmpc_ctx_create(cmpc_ctx** out, int device) {
     CMPC_CUDA(cudaEventCreate(&x->c.ev1));
     CMPC_CUDA(cudaEventCreate(&x->c.ev2));
     CMPC_CUDA(cudaEventCreate(&x->c.ev3));
+    CMPC_CUDA(cudaEventCreate(&x->c.ev4));
     CMPC_CUDA(cudaStreamCreateWithFlags(&x->c.stream2, cudaStreamNonBlocking));
     CMPC_CUDA(cudaEventCreateWithFlags(&x->c.fork, cudaEventDisableTiming));
     CMPC_CUDA(cudaEventCreateWithFlags(&x->c.join, cudaEventDisableTiming));
@@ -213,6 +214,7 @@ void cmpc_ctx_destroy(cmpc_ctx* x) {
   cudaEventDestroy(x->c.ev1);
   cudaEventDestroy(x->c.ev2);
   cudaEventDestroy(x->c.ev3);
+  cudaEventDestroy(x->c.ev4);
   cudaEventDestroy(x->c.fork);
   cudaEventDestroy(x->c.join);
   cudaStreamDestroy(x->c.stream2);
@@ -364,7 +366,7 @@ int cmpc_solve_batch(cmpc_ctx** ctxs, int64_t count, const double* opts, int64_t
         CMPC_CUDA(cudaSetDevice(c.device));
         require_loaded(c);
         return solve_loop(c, opts, max_iter, v_out ? v_out + i * c.n : nullptr, nullptr, nullptr,
-                          nullptr, scal_out + i * 13, nullptr, nullptr, nullptr);
+                          nullptr, scal_out + i * 14, nullptr, nullptr, nullptr);
       });
       if (rc < 0 && !have_error.exchange(true)) {
         first_error = g_error;
@@ -409,7 +411,7 @@ int cmpc_solve_batch_affine(cmpc_ctx** ctxs, int nctx, int64_t count, const doub
         c.h0 = h0_all[i];
         launch_hmax(c);
         return solve_loop(c, opts, max_iter, v_out ? v_out + i * c.n : nullptr, nullptr, nullptr,
-                          nullptr, scal_out + i * 13, nullptr, nullptr, nullptr);
+                          nullptr, scal_out + i * 14, nullptr, nullptr, nullptr);
       });
       if (rc < 0 && !have_error.exchange(true)) {
         first_error = g_error;

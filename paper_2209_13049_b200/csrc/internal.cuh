@@ -142,7 +142,7 @@ struct Ctx {
   double mu = 0.0;
 
   // events for per-phase timing
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev4 = nullptr;  // ev4: after k_syrk
   double syrk_flops = 0.0;   // algorithmic: sum over prototypes of hi (hi + 1)
   double syrk_bytes = 0.0;   // algorithmic: 8 x nonzeros of P (one read)
 };
@@ -154,7 +154,7 @@ void free_structure(Ctx& c);
 // ---- syrk.cu
 void syrk_plan(Ctx& c);
 // M(lower) = H + P' diag(omega) P + diag(dsing); writes full symmetric M when mirror
-void launch_condense(Ctx& c, bool mirror, bool with_rhs = false);
+void launch_condense(Ctx& c, bool mirror, bool with_rhs = false, cudaEvent_t after_syrk = nullptr);
 void syrk_free(Ctx& c);
 
 // ---- chol.cu

@@ -82,7 +82,7 @@ void seg_step(Ctx& c, double tau) {
   const bool fused = c.ps > 0 && c.npieces > 0;
   if (!fused) launch_rhs_partial(c);  // no SYRK rows: the singleton part only
   rec(c.ev2, c.stream);
-  launch_condense(c, false, fused);
+  launch_condense(c, false, fused, c.ev4);
   rec(c.ev3, c.stream);
   if (c.comm) {  // M = H + sum_g J_g' Sigma_g J_g and J' (r2 - sigma r3) over all ranks
     comm_group(true);
@@ -222,7 +222,7 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   long long syncs = 0, trials = 0;
   const int64_t n = c.n, m = c.m;
   const double start = now_seconds();
-  double linalg = 0.0, device_s = 0.0, syrk_s = 0.0, chol_s = 0.0;
+  double linalg = 0.0, device_s = 0.0, syrk_s = 0.0, chol_s = 0.0, syrk_k = 0.0;
   long long syrk_launches = 0;
   cudaEvent_t e_start, e_end;
   CMPC_CUDA(cudaEventCreate(&e_start));
@@ -297,6 +297,8 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     linalg += ms * 1e-3;
     CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev2, c.ev3));
     syrk_s += ms * 1e-3;
+    CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev2, c.ev4));
+    syrk_k += ms * 1e-3;
     ++syrk_launches;
     CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev3, c.ev1));
     chol_s += ms * 1e-3;
@@ -398,6 +400,7 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   out[10] = syrk_s;
   out[11] = chol_s;
   out[12] = double(syrk_launches);
+  out[13] = syrk_k;
   return CMPC_OK;
 }
 

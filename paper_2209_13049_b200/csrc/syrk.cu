@@ -574,7 +574,7 @@ void syrk_plan(Ctx& c) {
   }
 }
 
-void launch_condense(Ctx& c, bool mirror, bool with_rhs) {
+void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk) {
   with_rhs = with_rhs && c.ps > 0 && c.npieces > 0;
   SyrkArgs a;
   a.omega = c.omega;
@@ -593,6 +593,12 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs) {
     const CUtensorMap* tm32 = reinterpret_cast<const CUtensorMap*>(c.tmap_P32);
     k_syrk<<<c.nctas, kSyrkThreads, kSyrkSmem, c.stream>>>(*tm, *tm32, a);
     CMPC_LAUNCHED();
+  }
+  if (after_syrk) {  // the SYRK kernel's own time (roofline); an event node when capturing
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CMPC_CUDA(cudaStreamIsCapturing(c.stream, &cs));
+    if (cs == cudaStreamCaptureStatusActive) CMPC_CUDA(cudaEventRecordWithFlags(after_syrk, c.stream, cudaEventRecordExternal));
+    else CMPC_CUDA(cudaEventRecord(after_syrk, c.stream));
   }
   // sharded: every rank's partial J_g' Sigma_g J_g, H added by rank 0; the caller allreduces
   k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 256), 256, 0, c.stream>>>(

@@ -121,6 +121,7 @@ class IpmResult:
     syrk_seconds: float = 0.0     # device time of the condensation (SYRK + reduce)
     chol_seconds: float = 0.0     # device time of the first factorization attempts
     condensations: int = 0
+    syrk_kernel_seconds: float = 0.0  # device time of the SYRK kernel alone (k_syrk)
 
 
 class DeviceQp:
@@ -435,7 +436,7 @@ def solve_loaded(dq: DeviceQp, qp: DenseQp | None, opts: IpmOptions, t0=None) ->
     t0 = time.perf_counter() if t0 is None else t0
     n, m = (qp.n, qp.m) if qp is not None else (dq.n, dq.m)
     v, s, l, z = np.zeros(n), np.zeros(m), np.zeros(m), np.zeros(m)
-    out = np.zeros(13)
+    out = np.zeros(14)
     L = _lib.lib()
 
     def _log(user, rec):
@@ -458,7 +459,7 @@ def solve_loaded(dq: DeviceQp, qp: DenseQp | None, opts: IpmOptions, t0=None) ->
                     kkt_error=float(out[2]), objective=float(out[3]), linalg_seconds=float(out[5]),
                     device_seconds=float(out[6]), launches=int(out[7]), syncs=int(out[8]),
                     trials=int(out[9]), syrk_seconds=float(out[10]), chol_seconds=float(out[11]),
-                    condensations=int(out[12]))
+                    condensations=int(out[12]), syrk_kernel_seconds=float(out[13]))
     if qp is None and getattr(dq, "source", None) is not None:
         res.solution = dq.recover_trajectory()
         res.solution.v = v.reshape(res.solution.u.shape).copy()
@@ -517,7 +518,7 @@ class BatchSolver:
         n, cnt = self.base.n, self.count
         nw = max(1, min(self.workers, threads or self.workers))
         v = np.zeros((cnt, n))
-        scal = np.zeros((cnt, 13))
+        scal = np.zeros((cnt, 14))
         arr = (C.c_void_p * nw)(*[c.h.value if isinstance(c.h, C.c_void_p) else c.h for c in self.ctxs[:nw]])
         od = (C.c_double * 5)(opts.tol, opts.mu_init, opts.kappa_mu, opts.tau, opts.armijo_eta)
         t0 = time.perf_counter()
