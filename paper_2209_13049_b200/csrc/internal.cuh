@@ -60,6 +60,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   bool owns_stream = true;
   void* prob = nullptr;  // ProblemDev (builder.cu): the structured problem behind a device-built QP
+  bool pk_autoreset = false;  // inside the host loop: k_publish resets the packet's accumulators
 
   int64_t n = 0, m = 0;
   double h0 = 0.0;
@@ -214,6 +215,7 @@ void prob_refresh(Ctx& c, const double* x_bar);
 void prob_recover(Ctx& c, const double* v_dev, double* x, double* u, double* obj);
 void prob_free(Ctx& c);
 
+void launch_reset_packet_all(Ctx& c);
 void launch_debug_sum(Ctx& c, const double* x, int64_t n, int slot);
 void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear = false);
 // line-search derivative pieces for externally set directions: (Hv+h).pv, sum ps/s

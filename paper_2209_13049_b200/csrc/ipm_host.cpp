@@ -90,7 +90,7 @@ void seg_step(Ctx& c, double tau) {
     comm_allreduce(c, c.rhs, (size_t)c.n, CommType::f64, CommOp::sum);
     comm_group(false);
   }
-  launch_rhs_final(c);
+  if (c.comm || !fused) launch_rhs_final(c);  // (unsharded + fused: done by k_syrk_reduce)
   launch_debug_sum(c, c.M, c.n * c.n, 0);
   launch_debug_sum(c, c.rhs, c.n, 1);
   launch_debug_sum(c, c.omega, c.ldp + c.pz, 4);
@@ -234,6 +234,14 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   launch_init_state(c, c.mu);
   if (c.g_tau != tau) drop_graphs(c);
   c.g_tau = tau;
+  // from here every segment ends in k_publish, which also resets the packet's accumulated
+  // maxima / minima: the per-phase reset kernels drop out of the iteration graphs
+  launch_reset_packet_all(c);
+  struct AutoReset {
+    Ctx& c;
+    explicit AutoReset(Ctx& cc) : c(cc) { c.pk_autoreset = true; }
+    ~AutoReset() { c.pk_autoreset = false; }
+  } auto_reset(c);
   launch_residuals(c);
   sync_packet(c, &syncs);
   Packet A = *c.pk_host;

@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(256)
                   const double* __restrict__ H, const double* __restrict__ dsing, int64_t n,
                   double* __restrict__ M, int mirror, const double* __restrict__ rp,
                   const double* __restrict__ qs, const int32_t* __restrict__ sing_ptr,
-                  const double* __restrict__ sing_val, double* __restrict__ rhs) {
+                  const double* __restrict__ sing_val, double* __restrict__ rhs,
+                  const double* __restrict__ r1) {
   const int2 tl = tiles[blockIdx.x];
   const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
   if (rp && tl.x == tl.y && blockIdx.y == 0 && threadIdx.x < kTile) {
@@ -324,7 +325,8 @@ __global__ void __launch_bounds__(256)
         s += __ldcg(rp + (size_t)id * 128 + threadIdx.x) + __ldcg(rp + (size_t)id * 128 + 64 + threadIdx.x);
       }
       for (int32_t k = sing_ptr[col]; k < sing_ptr[col + 1]; ++k) s += sing_val[k] * qs[k];
-      rhs[col] = s;
+      // unsharded: the final -r1 + J'(r2 - sigma r3) here (k_rhs's rounding, no extra launch)
+      rhs[col] = r1 ? __dadd_rn(-r1[col], s) : s;
     }
   }
   const int e = blockIdx.y * blockDim.x + threadIdx.x;
@@ -603,7 +605,8 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
   // sharded: every rank's partial J_g' Sigma_g J_g, H added by rank 0; the caller allreduces
   k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 256), 256, 0, c.stream>>>(
       c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr, c.dsing, c.n, c.M,
-      mirror ? 1 : 0, with_rhs ? c.rhs_part : nullptr, c.q + c.ldp, c.sing_ptr, c.sing_val, c.rhs);
+      mirror ? 1 : 0, with_rhs ? c.rhs_part : nullptr, c.q + c.ldp, c.sing_ptr, c.sing_val, c.rhs,
+      with_rhs && !c.comm ? c.r1 : nullptr);
   CMPC_LAUNCHED();
 }
 

@@ -703,26 +703,44 @@ __global__ void k_sym_check(const double* __restrict__ H, int64_t n, unsigned* b
 
 // y = H x for a symmetric H as column dots (H' x): one warp per column, contiguous 16-byte
 // loads when n is even, fixed-order warp sum
+// x = v + alpha p when v is given (the line-search trial point, k_axpy_n's rounding; warp j
+// also stores x_j), else x as passed
 __global__ void __launch_bounds__(256) k_hcol_gemv(const double* __restrict__ H, int64_t n,
-                                                   const double* __restrict__ x, double* __restrict__ y) {
+                                                   const double* __restrict__ x, double* __restrict__ y,
+                                                   const double* __restrict__ v, const double* __restrict__ p,
+                                                   double alpha_h, const Packet* apk, double* __restrict__ xt) {
   const int lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x * 8ll + (threadIdx.x >> 5);
   if (j >= n) return;
+  const double al = v ? trial_alpha(alpha_h, apk) : 0.0;
   const double* col = H + j * n;
   double s0 = 0.0, s1 = 0.0;
   if ((n & 1) == 0) {
     const double2* c2 = reinterpret_cast<const double2*>(col);
-    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const double2* x2 = reinterpret_cast<const double2*>(v ? v : x);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
     for (int64_t i = lane; i < n / 2; i += 32) {
-      const double2 a = c2[i], b = x2[i];
+      const double2 a = c2[i];
+      double2 b = x2[i];
+      if (v) {
+        const double2 q = p2[i];
+        b.x = add(b.x, mul(al, q.x));
+        b.y = add(b.y, mul(al, q.y));
+      }
       s0 = fma(a.x, b.x, s0);
       s1 = fma(a.y, b.y, s1);
     }
   } else {
-    for (int64_t i = lane; i < n; i += 32) s0 = fma(col[i], x[i], s0);
+    for (int64_t i = lane; i < n; i += 32) {
+      const double b = v ? add(v[i], mul(al, p[i])) : x[i];
+      s0 = fma(col[i], b, s0);
+    }
   }
   const double s = warp_sum(s0 + s1);
-  if (lane == 0) y[j] = s;
+  if (lane == 0) {
+    y[j] = s;
+    if (v) xt[j] = add(v[j], mul(al, p[j]));
+  }
 }
 
 }  // namespace
@@ -817,14 +835,20 @@ void vec_free(Ctx& c) {
 
 // one warp: packet -> mapped host memory, then the sequence number (system-scope fence
 // between them, so a host that sees the new sequence sees the packet)
-__global__ void k_publish(const Packet* __restrict__ pk, Packet* out, unsigned long long* dev_seq,
-                          unsigned long long* host_seq) {
+__global__ void k_publish(const Packet* pk, Packet* out, unsigned long long* dev_seq,
+                          unsigned long long* host_seq, int reset) {
   constexpr int kWords = sizeof(Packet) / 8;
   const unsigned long long* src = reinterpret_cast<const unsigned long long*>(pk);
   volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(out);
   for (int i = threadIdx.x; i < kWords; i += 32) dst[i] = src[i];
   __threadfence_system();
   __syncwarp();
+  if (threadIdx.x == 0 && reset) {  // the accumulated maxima / minima start over (host loop)
+    Packet* p = const_cast<Packet*>(pk);
+    p->max_r1 = p->max_r3 = p->max_comp = p->max_lam = p->max_s = p->max_z = 0.0;
+    p->alpha_s_min = p->alpha_z_min = __longlong_as_double(0x7ff0000000000000ll);
+    p->any_nonpos = 0;
+  }
   if (threadIdx.x == 0) {
     const unsigned long long q = *dev_seq + 1;
     *dev_seq = q;
@@ -833,7 +857,7 @@ __global__ void k_publish(const Packet* __restrict__ pk, Packet* out, unsigned l
 }
 
 unsigned long long launch_publish(Ctx& c) {
-  k_publish<<<1, 32, 0, c.stream>>>(c.pk, c.pk_map, c.pub_dev, c.pub_map);
+  k_publish<<<1, 32, 0, c.stream>>>(c.pk, c.pk_map, c.pub_dev, c.pub_map, c.pk_autoreset ? 1 : 0);
   CMPC_LAUNCHED();
   return ++c.pub_expect;
 }
@@ -864,6 +888,13 @@ void launch_debug_sum(Ctx& c, const double* x, int64_t n, int slot) {
   CMPC_LAUNCHED();
 }
 
+void launch_reset_packet_all(Ctx& c) {
+  for (int w = 0; w < 3; ++w) {
+    k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, w);
+    CMPC_LAUNCHED();
+  }
+}
+
 void launch_zero_packet(Ctx& c) {
   CMPC_CUDA(cudaMemsetAsync(c.pk, 0, sizeof(Packet), c.stream));
 }
@@ -871,7 +902,8 @@ void launch_zero_packet(Ctx& c) {
 void launch_Hx(Ctx& c, const double* x, double* out) {
   if (c.n == 0) return;
   if (c.h_symmetric) {
-    k_hcol_gemv<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(c.H, c.n, x, out);
+    k_hcol_gemv<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(c.H, c.n, x, out, nullptr, nullptr,
+                                                                     0.0, nullptr, nullptr);
   } else {
     k_rows_gemv<<<(unsigned)ceil_div(c.n, 32), 256, 0, c.stream>>>(c.H, c.n, c.n, c.n, nullptr, x, out);
   }
@@ -911,8 +943,10 @@ void launch_Jtq(Ctx& c, const double* q, double* out) {
 void launch_residuals(Ctx& c, bool reuse_trial) {
   const unsigned pb = part_blocks(c.m);
   const int64_t m_all = rows_all(c);
-  k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 0);
-  CMPC_LAUNCHED();
+  if (!c.pk_autoreset) {  // (in the host loop, k_publish starts every segment clean)
+    k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 0);
+    CMPC_LAUNCHED();
+  }
   if (reuse_trial) {
     // v was just set to the accepted trial point v + alpha pv: H v is the trial's (same
     // kernel, same inputs, bit for bit) and k_update carried P v along as yv + alpha P pv,
@@ -1022,8 +1056,10 @@ void set_mu(Ctx& c, double mu) {
 }
 
 void launch_recover(Ctx& c, double tau) {
-  k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 1);
-  CMPC_LAUNCHED();
+  if (!c.pk_autoreset) {  // (in the host loop, k_publish starts every segment clean)
+    k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 1);
+    CMPC_LAUNCHED();
+  }
   const unsigned pb = part_blocks(c.m);
   if (c.m > 0) {
     launch_Jx(c, c.pv, c.y, nullptr);
@@ -1044,13 +1080,19 @@ void launch_recover(Ctx& c, double tau) {
 
 void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear) {
   const Packet* apk = alpha_from_device ? c.pk : nullptr;
-  k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 2);
-  CMPC_LAUNCHED();
-  if (c.n > 0) {
-    k_axpy_n<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.v, alpha, apk, c.pv, c.vt);
+  if (!c.pk_autoreset) {  // (in the host loop, k_publish starts every segment clean)
+    k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 2);
     CMPC_LAUNCHED();
   }
-  launch_Hx(c, c.vt, c.Hvt);
+  if (c.n > 0 && c.h_symmetric) {  // v_t = v + alpha pv formed inside H v_t's column dots
+    k_hcol_gemv<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(c.H, c.n, nullptr, c.Hvt, c.v, c.pv,
+                                                                     alpha, apk, c.vt);
+    CMPC_LAUNCHED();
+  } else if (c.n > 0) {
+    k_axpy_n<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.v, alpha, apk, c.pv, c.vt);
+    CMPC_LAUNCHED();
+    launch_Hx(c, c.vt, c.Hvt);
+  }
   const unsigned pb = part_blocks(c.m);
   if (c.m > 0) {
     if (!linear) launch_Jx(c, c.vt, c.yt, nullptr);
