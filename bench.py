@@ -423,7 +423,12 @@ def main():
     ms_per_step = ms_total / args.steps
     value = ms_total / (args.steps * world)  # whole job: ms per solve over all ranks
 
-    # end to end through the public API with host (pinned) buffers
+    # end to end through the public API with host (pinned) buffers. The resident context of
+    # the device-timed loop is released first: a second loaded 1.5 GB context in the process
+    # made the pinned 1 GB H2D and the pool allocations of each fresh context erratic
+    # (21-35 ms instead of 18 ms, occasional 0.6 s stalls; tools/e2e_probe2.py)
+    dq.close()
+    qp._device = None
     e2e = None
     if not args.no_e2e:
         pin = dict(H=pinned_like(qp.H), h=pinned_like(qp.h), J=pinned_like(qp.J), d=pinned_like(qp.d))

@@ -209,7 +209,10 @@ class DeviceQp:
 
     def close(self):
         if getattr(self, "h", None):
-            _lib.lib().cmpc_ctx_destroy(self.h)
+            try:
+                _lib.lib().cmpc_ctx_destroy(self.h)
+            except (AttributeError, TypeError):  # interpreter shutdown: the module is gone
+                pass
             self.h = None
 
     __del__ = close
@@ -535,7 +538,10 @@ class BatchSolver:
             c.close()
         self.ctxs = []
         for a in getattr(self, "_pinned", []):
-            _lib.lib().cmpc_host_unregister(a.ctypes.data)
+            try:
+                _lib.lib().cmpc_host_unregister(a.ctypes.data)
+            except (AttributeError, TypeError):  # interpreter shutdown
+                pass
         self._pinned = []
 
     __del__ = close

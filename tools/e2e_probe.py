@@ -6,7 +6,7 @@ from paper_2209_13049_b200 import ipm, problem as P
 import bench
 qp = P.build_dense_qp(P.heat2d_problem(50, 50, T=50))
 pin = dict(H=bench.pinned_like(qp.H), h=bench.pinned_like(qp.h), J=bench.pinned_like(qp.J), d=bench.pinned_like(qp.d))
-for k in range(4):
+for k in range(8):
     fresh = P.DenseQp(H=pin["H"], h=pin["h"], h0=qp.h0, J=pin["J"], d=pin["d"], source=qp.source, gk=qp.gk, x0=qp.x0)
     t0 = time.perf_counter()
     dq = ipm.device_qp(fresh)
