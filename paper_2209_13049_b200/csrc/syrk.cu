@@ -320,9 +320,18 @@ __global__ void __launch_bounds__(256)
     const int64_t col = (int64_t)kTile * tl.x + threadIdx.x;
     if (col < n) {
       double s = 0.0;
-      for (int q = u0; q < u1; ++q) {
-        const int32_t id = tile_segs[q] & 0x7fffffff;
-        s += __ldcg(rp + (size_t)id * 128 + threadIdx.x) + __ldcg(rp + (size_t)id * 128 + 64 + threadIdx.x);
+      for (int q = u0; q < u1; q += 8) {  // eight segments' loads in flight, summed in order
+        double x[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          x[b] = 0.0;
+          if (q + b < u1) {
+            const int32_t id = tile_segs[q + b] & 0x7fffffff;
+            x[b] = __ldcg(rp + (size_t)id * 128 + threadIdx.x) + __ldcg(rp + (size_t)id * 128 + 64 + threadIdx.x);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) s += x[b];
       }
       for (int32_t k = sing_ptr[col]; k < sing_ptr[col + 1]; ++k) s += sing_val[k] * qs[k];
       // unsharded: the final -r1 + J'(r2 - sigma r3) here (k_rhs's rounding, no extra launch)
