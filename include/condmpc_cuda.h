@@ -42,7 +42,8 @@ int cmpc_load_qp(cmpc_ctx* ctx, int64_t n, int64_t m, const double* H, const dou
                  const double* J, const double* d, int on_device);
 
 /* The structured LQ-MPC problem (LqProblemData, proj/include/condmpc/problem.hpp:22-45).
- * Matrices column-major (Eigen's layout); w is T x n_x stage-major (w[t * n_x + i]); bounds
+ * Matrices column-major (Eigen's layout, layout = 0) or row-major (layout = 1, e.g. C-ordered
+ * numpy arrays: transposed on the device instead of on the host); w is T x n_x stage-major (w[t * n_x + i]); bounds
  * may hold +-inf (rows of infinite bounds are skipped, as in reduction.cpp:191-251); S, K,
  * E, F, w may be NULL when zero / n_c == 0. */
 typedef struct cmpc_lq_problem {
@@ -50,6 +51,7 @@ typedef struct cmpc_lq_problem {
   const double *A, *B, *Q, *Qf, *R, *S, *E, *F;
   const double *gl, *gu, *xl, *xu, *ul, *uu;
   const double *w, *x_bar, *K;
+  int64_t layout;
 } cmpc_lq_problem;
 /* build_dense_qp (proj/src/reduction.cpp:255-268) on the device, then load it like
  * cmpc_load_qp without the dense J ever crossing PCIe; the problem stays resident for the

@@ -21,7 +21,7 @@ class LqProblem(C.Structure):
     """cmpc_lq_problem (include/condmpc_cuda.h): LqProblemData for the device builder."""
     _fields_ = [("nx", C.c_int64), ("nu", C.c_int64), ("nc", C.c_int64), ("T", C.c_int64)] + [
         (f, D) for f in ("A", "B", "Q", "Qf", "R", "S", "E", "F", "gl", "gu", "xl", "xu", "ul", "uu",
-                         "w", "x_bar", "K")]
+                         "w", "x_bar", "K")] + [("layout", C.c_int64)]
 
 
 INSPECT_FN = C.CFUNCTYPE(None, C.c_void_p, D, D, D, D, C.c_double, D, D, D, C.c_double, D, D, D,

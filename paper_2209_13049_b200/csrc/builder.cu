@@ -17,6 +17,9 @@
 // x0 and the row table stay resident for refresh_initial_state and recover_trajectory, so a
 // receding-horizon step uploads n_x numbers and never re-analyses J.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -29,46 +32,56 @@ namespace {
 // ---------------------------------------------------------------- plain tiled DGEMM
 // C(M x N) = alpha op(A) op(B) + beta C, column-major; 64 x 64 tiles, 256 threads, 4 x 4
 // outputs per thread. Setup-time GEMMs only (the solve's products are the tuned kernels).
-constexpr int kGT = 64, kGK = 16;
-__global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, double alpha, const double* __restrict__ A,
-                                              int64_t lda, int ta, const double* __restrict__ B, int64_t ldb,
-                                              int tb, double beta, double* __restrict__ C, int64_t ldc) {
-  __shared__ double As[kGK][kGT + 1], Bs[kGK][kGT + 1];
+constexpr int kGK = 16;
+// 256 threads as 16 x 16, each RU x RV outputs: tile (16 RU) x (16 RV); <4,4> for square
+// products, <16,1> for skinny ones (N <= 16). blockIdx.z = split of K (kc columns each); a
+// split's raw product goes to C + z * zs.
+template <int RU, int RV>
+__global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, int kc, double alpha,
+                                              const double* __restrict__ A, int64_t lda, int ta,
+                                              const double* __restrict__ B, int64_t ldb, int tb, double beta,
+                                              double* __restrict__ C, int64_t ldc, int64_t zs) {
+  constexpr int TM = 16 * RU, TN = 16 * RV;
+  __shared__ double As[kGK][TM + 1], Bs[kGK][TN + 1];
   const int tid = threadIdx.x, tr = tid & 15, tc = tid >> 4;
-  const int i0 = blockIdx.x * kGT, j0 = blockIdx.y * kGT;
-  double acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += kGK) {
-    for (int e = tid; e < kGK * kGT; e += 256) {
-      const int kk = e / kGT, ii = e % kGT;  // consecutive threads: consecutive rows
+  const int i0 = blockIdx.x * TM, j0 = blockIdx.y * TN;
+  const int kb = blockIdx.z * kc, ke = min(K, kb + kc);
+  C += blockIdx.z * zs;
+  double acc[RU][RV] = {};
+  for (int k0 = kb; k0 < ke; k0 += kGK) {
+    for (int e = tid; e < kGK * TM; e += 256) {
+      const int kk = e / TM, ii = e % TM;  // consecutive threads: consecutive rows
       const int gi = i0 + ii, gk = k0 + kk;
       double av = 0.0;
-      if (gi < M && gk < K) av = ta ? A[gk + (int64_t)gi * lda] : A[gi + (int64_t)gk * lda];
+      if (gi < M && gk < ke) av = ta ? A[gk + (int64_t)gi * lda] : A[gi + (int64_t)gk * lda];
       As[kk][ii] = av;
-      const int gj = j0 + ii;
+    }
+    for (int e = tid; e < kGK * TN; e += 256) {
+      const int kk = e / TN, jj = e % TN;
+      const int gj = j0 + jj, gk = k0 + kk;
       double bv = 0.0;
-      if (gj < N && gk < K) bv = tb ? B[gj + (int64_t)gk * ldb] : B[gk + (int64_t)gj * ldb];
-      Bs[kk][ii] = bv;
+      if (gj < N && gk < ke) bv = tb ? B[gj + (int64_t)gk * ldb] : B[gk + (int64_t)gj * ldb];
+      Bs[kk][jj] = bv;
     }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < kGK; ++kk) {
-      double a[4], b[4];
+      double a[RU], b[RV];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = As[kk][tr + 16 * u];
-        b[u] = Bs[kk][tc + 16 * u];
-      }
+      for (int u = 0; u < RU; ++u) a[u] = As[kk][tr + 16 * u];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int v = 0; v < RV; ++v) b[v] = Bs[kk][tc + 16 * v];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+      for (int u = 0; u < RU; ++u)
+#pragma unroll
+        for (int v = 0; v < RV; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < RU; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < RV; ++v) {
       const int gi = i0 + tr + 16 * u, gj = j0 + tc + 16 * v;
       if (gi < M && gj < N) {
         double* p = C + gi + (int64_t)gj * ldc;
@@ -77,18 +90,143 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, double alpha,
     }
 }
 
+// C = alpha sum_z W[z] + beta C, splits summed in order (deterministic)
+__global__ void k_gemm_splits(int M, int N, int S, const double* __restrict__ W, double alpha, double beta,
+                              double* __restrict__ C, int64_t ldc) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t MN = (int64_t)M * N;
+  if (e >= MN) return;
+  double s = 0.0;
+  for (int z = 0; z < S; ++z) s += W[z * MN + e];
+  double* p = C + e % M + (e / M) * ldc;
+  *p = alpha * s + (beta == 0.0 ? 0.0 : beta * *p);
+}
+
+// Y = A X for a skinny X (N <= NC columns, A not transposed): a thread owns one row of A and
+// streams its K-chunk (eight loads in flight), the chunk of X staged in shared memory and read
+// as broadcasts. blockIdx.y = split of K; the split's partial goes to W + y * M * N.
+constexpr int kSkRows = 128, kSkK = 128;
+template <int NC>
+__global__ void __launch_bounds__(kSkRows) k_skinny(int M, int N, int K, const double* __restrict__ A, int64_t lda,
+                                                    const double* __restrict__ X, int64_t ldx, int tb,
+                                                    double* __restrict__ W) {
+  __shared__ __align__(16) double Xs[kSkK][NC];
+  const int kb = blockIdx.y * kSkK, ke = min(K, kb + kSkK);
+  for (int e = threadIdx.x; e < kSkK * NC; e += kSkRows) {
+    const int kk = e / NC, j = e % NC, gk = kb + kk;
+    Xs[kk][j] = (gk < ke && j < N) ? (tb ? X[j + (int64_t)gk * ldx] : X[gk + (int64_t)j * ldx]) : 0.0;
+  }
+  __syncthreads();
+  const int i = blockIdx.x * kSkRows + threadIdx.x;
+  if (i >= M) return;
+  double acc[NC] = {};
+  const double* a = A + i;
+  int k = kb;
+  for (; k + 8 <= ke; k += 8) {
+    double av[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) av[u] = __ldg(a + (int64_t)(k + u) * lda);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int j = 0; j < NC; ++j) acc[j] = fma(av[u], Xs[k - kb + u][j], acc[j]);
+  }
+  for (; k < ke; ++k) {
+    const double av = __ldg(a + (int64_t)k * lda);
+#pragma unroll
+    for (int j = 0; j < NC; ++j) acc[j] = fma(av, Xs[k - kb][j], acc[j]);
+  }
+  W += (int64_t)blockIdx.y * M * N;
+#pragma unroll
+  for (int j = 0; j < NC; ++j)
+    if (j < N) W[i + (int64_t)j * M] = acc[j];
+}
+
+// Setup products. Skinny ones (G_k = A_K G_{k-1}: 2500 x 10 x 2500; the free response's
+// 2500 x 1 x 2500) go to k_skinny; the rest to the tiled kernel, K split until about four CTAs
+// per SM are busy. Splits are summed in a fixed order.
 void gemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
           int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
   if (M <= 0 || N <= 0) return;
-  dim3 g((unsigned)ceil_div(M, kGT), (unsigned)ceil_div(N, kGT));
-  k_gemm<<<g, 256, 0, st>>>((int)M, (int)N, (int)K, alpha, A, lda, ta ? 1 : 0, B, ldb, tb ? 1 : 0, beta, C, ldc);
+  if (!ta && N <= 16 && K >= kSkK) {
+    const int64_t S = ceil_div(K, kSkK);
+    double* W = dev_alloc<double>(size_t(S * M * N), st);
+    dim3 g((unsigned)ceil_div(M, kSkRows), (unsigned)S);
+    if (N == 1)
+      k_skinny<1><<<g, kSkRows, 0, st>>>((int)M, (int)N, (int)K, A, lda, B, ldb, tb ? 1 : 0, W);
+    else
+      k_skinny<16><<<g, kSkRows, 0, st>>>((int)M, (int)N, (int)K, A, lda, B, ldb, tb ? 1 : 0, W);
+    CMPC_LAUNCHED();
+    k_gemm_splits<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>((int)M, (int)N, (int)S, W, alpha, beta, C, ldc);
+    CMPC_LAUNCHED();
+    dev_free(W, st);
+    return;
+  }
+  const int64_t tiles = ceil_div(M, 64) * ceil_div(N, 64);
+  int64_t S = std::min<int64_t>(std::max<int64_t>(1, ceil_div(592, tiles)), std::max<int64_t>(1, K / 128));
+  const int64_t kc = ceil_div(ceil_div(std::max<int64_t>(K, 1), S), kGK) * kGK;
+  S = std::max<int64_t>(1, ceil_div(K, kc));
+  dim3 g((unsigned)ceil_div(M, 64), (unsigned)ceil_div(N, 64), (unsigned)S);
+  if (S == 1) {
+    k_gemm<4, 4><<<g, 256, 0, st>>>((int)M, (int)N, (int)K, (int)std::max<int64_t>(K, 1), alpha, A, lda, ta ? 1 : 0,
+                                    B, ldb, tb ? 1 : 0, beta, C, ldc, 0);
+    CMPC_LAUNCHED();
+    return;
+  }
+  double* W = dev_alloc<double>(size_t(S * M * N), st);
+  k_gemm<4, 4><<<g, 256, 0, st>>>((int)M, (int)N, (int)K, (int)kc, 1.0, A, lda, ta ? 1 : 0, B, ldb, tb ? 1 : 0, 0.0,
+                                  W, M, M * N);
   CMPC_LAUNCHED();
+  k_gemm_splits<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>((int)M, (int)N, (int)S, W, alpha, beta, C, ldc);
+  CMPC_LAUNCHED();
+  dev_free(W, st);
+}
+
+// dst (r x c, column-major) from src holding it row-major (= the c x r column-major transpose)
+__global__ void k_transpose(int64_t r, int64_t c, const double* __restrict__ src, double* __restrict__ dst) {
+  __shared__ double t[32][33];
+  const int64_t i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  for (int y = threadIdx.y; y < 32; y += 8) {  // read rows i of src along j (contiguous)
+    const int64_t i = i0 + y, j = j0 + threadIdx.x;
+    if (i < r && j < c) t[y][threadIdx.x] = src[i * c + j];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {  // write columns j of dst along i (contiguous)
+    const int64_t j = j0 + y, i = i0 + threadIdx.x;
+    if (i < r && j < c) dst[i + j * r] = t[threadIdx.x][y];
+  }
 }
 
 // one row of J: kind 0 mixed (E + F K), 1 state, 2 input; upper bound or lower; stage t; index i
 struct RowDesc {
   int kind, upper, t, i;
 };
+
+// the six (kind, side) groups of rows in the reference's order: group g holds rows
+// first .. first + nt * len - 1, stage t0 + r / len, index list[r % len]
+struct RowGroup {
+  int kind, upper, t0, list, len;
+  int64_t first;
+};
+struct RowGroups {
+  RowGroup g[6];
+  int count;
+  int64_t m;
+};
+
+__global__ void k_row_table(RowGroups gr, const int32_t* __restrict__ idx, const double* __restrict__ bvals,
+                            RowDesc* __restrict__ rows, double* __restrict__ bound) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= gr.m) return;
+  int k = 0;
+  while (k + 1 < gr.count && r >= gr.g[k + 1].first) ++k;
+  const RowGroup g = gr.g[k];
+  const int64_t loc = r - g.first;
+  const int64_t tt = loc / g.len;
+  const int j = (int)(loc - tt * g.len);
+  rows[r] = RowDesc{g.kind, g.upper, g.t0 + (int)tt, idx[g.list + j]};
+  bound[r] = bvals[g.list + j];
+}
 
 __global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -155,17 +293,19 @@ __global__ void k_rows_d(int64_t m, const RowDesc* __restrict__ rd, const double
   d[r] = q.upper ? bound[r] - off : off - bound[r];
 }
 
-// J (m x n, column-major), row-fastest so the writes coalesce
+// J (m x n, column-major): a thread owns one row and a chunk of 32 columns (its descriptor
+// read once); consecutive threads write consecutive rows of a column, so the stores coalesce
+constexpr int kJCols = 32;
 __global__ void k_rows_J(int64_t m, int64_t n, const RowDesc* __restrict__ rd, const double* __restrict__ G,
                          const double* __restrict__ KG, const double* __restrict__ EG,
                          const double* __restrict__ F, int nx, int nu, int nc, double* __restrict__ J) {
-  const int64_t total = m * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e % m, col = e / m;
-    const RowDesc q = rd[r];
-    const int j = (int)(col / nu), cc = (int)(col % nu);
-    const double sg = q.upper ? 1.0 : -1.0;
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const RowDesc q = rd[r];
+  const double sg = q.upper ? 1.0 : -1.0;
+  const int64_t c0 = (int64_t)blockIdx.y * kJCols, c1 = min(n, c0 + kJCols);
+  for (int64_t col = c0; col < c1; ++col) {
+    const int j = (int)(col / nu), cc = (int)(col - (int64_t)j * nu);
     double v = 0.0;
     if (j < q.t) {
       const int64_t gc = (int64_t)(q.t - 1 - j) * nu + cc;  // column of G_{t-1-j}
@@ -176,7 +316,7 @@ __global__ void k_rows_J(int64_t m, int64_t n, const RowDesc* __restrict__ rd, c
     }
     if (q.kind == 2 && col == (int64_t)q.t * nu + q.i) v += sg;
     if (q.kind == 0 && j == q.t) v += sg * F[q.i + (int64_t)cc * nc];
-    J[e] = v;
+    __stcs(J + r + col * m, v);
   }
 }
 
@@ -295,9 +435,29 @@ void prob_build(Ctx& c, const cmpc_lq_problem& in, double** H_out, double** h_ou
   p.n = T * nu;
   const int64_t n = p.n;
   cudaStream_t st = c.stream;
+  const bool verbose = getenv("CMPC_VERBOSE") != nullptr;
+  auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double last = wall();
+  auto tick = [&](const char* what) {
+    if (!verbose) return;
+    CMPC_CUDA(cudaStreamSynchronize(st));
+    const double now = wall();
+    fprintf(stderr, "[cmpc build] %-10s %8.2f ms\n", what, (now - last) * 1e3);
+    last = now;
+  };
   auto up = [&](const double* src, int64_t count) {
     double* dst = dev_alloc<double>(size_t(std::max<int64_t>(count, 1)), st);
-    if (count > 0) CMPC_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * count, cudaMemcpyHostToDevice, st));
+    if (count > 0) upload_h2d(dst, src, sizeof(double) * count, st);
+    return dst;
+  };
+  // a matrix argument: column-major as given, or row-major (layout 1) transposed on the device
+  auto upm = [&](const double* src, int64_t r, int64_t cc) {
+    if (!in.layout || r * cc == 0) return up(src, r * cc);
+    double* tmp = up(src, r * cc);
+    double* dst = dev_alloc<double>(size_t(r * cc), st);
+    k_transpose<<<dim3((unsigned)ceil_div(cc, 32), (unsigned)ceil_div(r, 32)), dim3(32, 8), 0, st>>>(r, cc, tmp, dst);
+    CMPC_LAUNCHED();
+    dev_free(tmp, st);
     return dst;
   };
   auto any_nz = [](const double* a, int64_t k) {
@@ -307,16 +467,17 @@ void prob_build(Ctx& c, const cmpc_lq_problem& in, double** H_out, double** h_ou
   };
   p.has_K = in.K && any_nz(in.K, nu * nx);
   p.has_S = in.S && any_nz(in.S, nx * nu);
-  double* A = up(in.A, nx * nx);
-  double* B = up(in.B, nx * nu);
-  p.Q = up(in.Q, nx * nx);
-  p.Qf = up(in.Qf, nx * nx);
-  p.R = up(in.R, nu * nu);
-  p.S = p.has_S ? up(in.S, nx * nu) : dev_zeros<double>(size_t(nx * nu), st);
-  p.K = p.has_K ? up(in.K, nu * nx) : dev_zeros<double>(size_t(nu * nx), st);
-  p.F = up(in.F, nc * nu);
+  double* A = upm(in.A, nx, nx);
+  double* B = upm(in.B, nx, nu);
+  p.Q = upm(in.Q, nx, nx);
+  p.Qf = upm(in.Qf, nx, nx);
+  p.R = upm(in.R, nu, nu);
+  p.S = p.has_S ? upm(in.S, nx, nu) : dev_zeros<double>(size_t(nx * nu), st);
+  p.K = p.has_K ? upm(in.K, nu, nx) : dev_zeros<double>(size_t(nu * nx), st);
+  p.F = upm(in.F, nc, nu);
   p.W = dev_zeros<double>(size_t(nx * T), st);
   if (in.w) CMPC_CUDA(cudaMemcpyAsync(p.W, in.w, sizeof(double) * nx * T, cudaMemcpyHostToDevice, st));
+  tick("h2d");
   // A_K = A + B K; S_K = S + K' R; Q_K = Q + S K + (S K)' + K' R K
   p.AK = A;
   p.SK = dev_alloc<double>(size_t(nx * nu), st);
@@ -339,6 +500,7 @@ void prob_build(Ctx& c, const cmpc_lq_problem& in, double** H_out, double** h_ou
   for (int64_t k = 1; k < T; ++k)
     gemm(st, false, false, nx, nu, nx, 1.0, p.AK, nx, p.G + (k - 1) * nu * nx, nx, 0.0, p.G + k * nu * nx, nx);
   dev_free(B, st);
+  tick("G");
   // Hessian
   double* QG = dev_alloc<double>(size_t(nx * n), st);
   double* Cm = dev_alloc<double>(size_t(n * n), st);
@@ -356,63 +518,66 @@ void prob_build(Ctx& c, const cmpc_lq_problem& in, double** H_out, double** h_ou
   k_hess<<<(unsigned)ceil_div(n * n, 256), 256, 0, st>>>(n, (int)nu, (int)T, Cm, Cf, p.R, CS, H);
   CMPC_LAUNCHED();
   for (void* q : {(void*)QG, (void*)Cm, (void*)Cf, (void*)CS}) dev_free(q, st);
-  // rows of J in the reference's order, one per finite bound
-  std::vector<RowDesc> rows;
-  std::vector<double> bnd;
-  auto fin = [](const double* b, int64_t i) { return b && std::isfinite(b[i]); };
-  for (int upper = 1; upper >= 0; --upper) {
-    const double* b = upper ? in.gu : in.gl;
-    for (int64_t t = 0; t < (nc > 0 ? T : 0); ++t)
-      for (int64_t i = 0; i < nc; ++i)
-        if (fin(b, i)) {
-          rows.push_back({0, upper, (int)t, (int)i});
-          bnd.push_back(b[i]);
-        }
-  }
-  for (int upper = 1; upper >= 0; --upper) {
-    const double* b = upper ? in.xu : in.xl;
-    for (int64_t t = 1; t <= T; ++t)
-      for (int64_t i = 0; i < nx; ++i)
-        if (fin(b, i)) {
-          rows.push_back({1, upper, (int)t, (int)i});
-          bnd.push_back(b[i]);
-        }
-  }
-  for (int upper = 1; upper >= 0; --upper) {
-    const double* b = upper ? in.uu : in.ul;
-    for (int64_t t = 0; t < T; ++t)
-      for (int64_t i = 0; i < nu; ++i)
-        if (fin(b, i)) {
-          rows.push_back({2, upper, (int)t, (int)i});
-          bnd.push_back(b[i]);
-        }
-  }
-  const int64_t m = (int64_t)rows.size();
+  tick("H");
+  // rows of J in the reference's order, one per finite bound. A bound vector is the same at
+  // every stage, so each (kind, side) group is T copies of its list of finite indices: the
+  // lists go to the device and k_row_table expands them.
+  RowGroups gr{};
+  std::vector<int32_t> idx;
+  std::vector<double> bvals;
+  int64_t m = 0;
+  auto group = [&](int kind, int upper, int t0, int64_t nt, const double* b, int64_t len) {
+    RowGroup& g = gr.g[gr.count++];
+    g.kind = kind;
+    g.upper = upper;
+    g.t0 = t0;
+    g.list = (int)idx.size();
+    for (int64_t i = 0; i < len; ++i)
+      if (b && std::isfinite(b[i])) {
+        idx.push_back((int32_t)i);
+        bvals.push_back(b[i]);
+      }
+    g.len = (int)idx.size() - g.list;
+    g.first = m;
+    m += (g.len > 0 ? nt : 0) * g.len;
+  };
+  for (int upper = 1; upper >= 0; --upper) group(0, upper, 0, nc > 0 ? T : 0, upper ? in.gu : in.gl, nc);
+  for (int upper = 1; upper >= 0; --upper) group(1, upper, 1, T, upper ? in.xu : in.xl, nx);
+  for (int upper = 1; upper >= 0; --upper) group(2, upper, 0, T, upper ? in.uu : in.ul, nu);
+  gr.m = m;
   p.m = m;
   p.rows = dev_alloc<RowDesc>(size_t(std::max<int64_t>(m, 1)), st);
   p.bound = dev_alloc<double>(size_t(std::max<int64_t>(m, 1)), st);
   if (m > 0) {
-    CMPC_CUDA(cudaMemcpyAsync(p.rows, rows.data(), sizeof(RowDesc) * m, cudaMemcpyHostToDevice, st));
-    CMPC_CUDA(cudaMemcpyAsync(p.bound, bnd.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
+    int32_t* di = dev_alloc<int32_t>(idx.size(), st);
+    double* db = dev_alloc<double>(bvals.size(), st);
+    CMPC_CUDA(cudaMemcpyAsync(di, idx.data(), sizeof(int32_t) * idx.size(), cudaMemcpyHostToDevice, st));
+    CMPC_CUDA(cudaMemcpyAsync(db, bvals.data(), sizeof(double) * bvals.size(), cudaMemcpyHostToDevice, st));
+    k_row_table<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(gr, di, db, p.rows, p.bound);
+    CMPC_LAUNCHED();
+    dev_free(di, st);
+    dev_free(db, st);
   }
+  tick("rows");
   double *KG = nullptr, *EG = nullptr;
   if (p.has_K) {
     KG = dev_alloc<double>(size_t(nu * n), st);
     gemm(st, false, false, nu, n, nx, 1.0, p.K, nu, p.G, nx, 0.0, KG, nu);
   }
   if (nc > 0) {  // E + F K
-    p.EFK = up(in.E, nc * nx);
+    p.EFK = upm(in.E, nc, nx);
     if (p.has_K) gemm(st, false, false, nc, nx, nu, 1.0, p.F, nc, p.K, nu, 1.0, p.EFK, nc);
     EG = dev_alloc<double>(size_t(nc * n), st);
     gemm(st, false, false, nc, n, nx, 1.0, p.EFK, nc, p.G, nx, 0.0, EG, nc);
   }
   double* J = dev_alloc<double>(size_t(std::max<int64_t>(m * n, 1)), st);
   if (m > 0) {
-    k_rows_J<<<4096, 256, 0, st>>>(m, n, p.rows, p.G, KG, EG, p.F, (int)nx, (int)nu, (int)nc, J);
+    k_rows_J<<<dim3((unsigned)ceil_div(m, 256), (unsigned)ceil_div(n, kJCols)), 256, 0, st>>>(m, n, p.rows, p.G, KG, EG, p.F, (int)nx, (int)nu, (int)nc, J);
     CMPC_LAUNCHED();
   }
   dev_free(KG, st);
   dev_free(EG, st);
+  tick("J");
   // affine terms from the free response
   p.X0 = dev_alloc<double>(size_t(nx * (T + 1)), st);
   CMPC_CUDA(cudaMemcpyAsync(p.X0, in.x_bar, sizeof(double) * nx, cudaMemcpyHostToDevice, st));
@@ -423,6 +588,7 @@ void prob_build(Ctx& c, const cmpc_lq_problem& in, double** H_out, double** h_ou
   affine(c, p, h, h0d, d);
   CMPC_CUDA(cudaMemcpyAsync(h0_out, h0d, sizeof(double), cudaMemcpyDeviceToHost, st));
   CMPC_CUDA(cudaStreamSynchronize(st));
+  tick("affine");
   dev_free(h0d, st);
   *H_out = H;
   *h_out = h;

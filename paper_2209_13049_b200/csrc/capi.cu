@@ -70,8 +70,7 @@ void d2h(Ctx& c, double* dst, const double* src, int64_t count) {
     CMPC_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * count, cudaMemcpyDeviceToHost, c.stream));
 }
 void h2d(Ctx& c, double* dst, const double* src, int64_t count) {
-  if (src && count > 0)
-    CMPC_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * count, cudaMemcpyHostToDevice, c.stream));
+  if (src && count > 0) upload_h2d(dst, src, sizeof(double) * count, c.stream);
 }
 
 void read_packet(Ctx& c) {
@@ -141,10 +140,15 @@ int load_impl(Ctx& c, int64_t n, int64_t m, const double* H, const double* h, do
       c.h = dev_alloc<double>((size_t)n, c.stream);
       c.J = dev_alloc<double>((size_t)(m * n), c.stream);
       c.d = dev_alloc<double>((size_t)m, c.stream);
-      if (n * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.H, H, sizeof(double) * n * n, kind, c.stream));
-      if (n > 0) CMPC_CUDA(cudaMemcpyAsync(c.h, h, sizeof(double) * n, kind, c.stream));
-      if (m * n > 0) CMPC_CUDA(cudaMemcpyAsync(c.J, J, sizeof(double) * m * n, kind, c.stream));
-      if (m > 0) CMPC_CUDA(cudaMemcpyAsync(c.d, d, sizeof(double) * m, kind, c.stream));
+      auto copy = [&](double* dst, const double* src, int64_t count) {
+        if (count <= 0) return;
+        if (on_device) CMPC_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * count, kind, c.stream));
+        else upload_h2d(dst, src, sizeof(double) * count, c.stream);
+      };
+      copy(c.H, H, n * n);
+      copy(c.h, h, n);
+      copy(c.J, J, m * n);
+      copy(c.d, d, m);
     }
     const bool verbose = getenv("CMPC_VERBOSE") != nullptr;
     double last = t_in;

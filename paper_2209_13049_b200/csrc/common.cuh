@@ -36,6 +36,9 @@ extern thread_local long long g_launches;
 // Stream-ordered device allocations from the device's memory pool (kept cached: a
 // reloaded QP of similar size reuses the pages instead of re-mapping gigabytes).
 void pool_init(int device);
+// host -> device copy; large pageable sources are staged through pinned slots by a few host
+// threads (upload.cpp). Returns once enqueued on st; the source may then be reused.
+void upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
 template <typename T>
 inline T* dev_alloc(size_t count, cudaStream_t st) {
   void* p = nullptr;

@@ -8,6 +8,11 @@
 // every sum is a fixed-order two-stage reduction, every max/min an order-free atomic,
 // so two runs are bitwise identical (proj/tests/test_ipm.cpp:432-457).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -745,9 +750,47 @@ __global__ void __launch_bounds__(256) k_hcol_gemv(const double* __restrict__ H,
 
 }  // namespace
 
+// Mapped pinned blocks (packet, sequence word, 64-double staging ring) are recycled across
+// loads and contexts: cudaHostAlloc costs milliseconds, a load should not.
+namespace {
+constexpr size_t kStageOff = (sizeof(Packet) + 64 + 127) / 128 * 128;
+constexpr size_t kPinnedBytes = kStageOff + 64 * sizeof(double);
+std::mutex g_pinned_mu;
+std::vector<void*> g_pinned_free;
+
+void* pinned_take() {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      void* p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  CMPC_CUDA(cudaHostAlloc(&p, kPinnedBytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  return p;
+}
+
+void pinned_give(void* p) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
+}  // namespace
+
 void vec_alloc(Ctx& c) {
   const size_t n = (size_t)c.n, m = (size_t)c.m;
   const size_t py = (size_t)(c.ldp + c.pz);  // prototype-indexed arrays
+  const bool verbose = getenv("CMPC_VERBOSE") != nullptr;
+  auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double last = wall();
+  auto tick = [&](const char* what) {
+    if (!verbose) return;
+    CMPC_CUDA(cudaStreamSynchronize(c.stream));
+    const double now = wall();
+    fprintf(stderr, "[cmpc alloc] %-10s %8.2f ms\n", what, (now - last) * 1e3);
+    last = now;
+  };
   c.v = dev_zeros<double>(n, c.stream); c.s = dev_zeros<double>(m, c.stream); c.lam = dev_zeros<double>(m, c.stream); c.z = dev_zeros<double>(m, c.stream);
   c.r1 = dev_zeros<double>(n, c.stream); c.r2 = dev_zeros<double>(m, c.stream); c.r3 = dev_zeros<double>(m, c.stream);
   c.Hv = dev_zeros<double>(n, c.stream); c.Jtl = dev_zeros<double>(n, c.stream); c.y = dev_zeros<double>(py, c.stream); c.sigma = dev_zeros<double>(m, c.stream);
@@ -763,8 +806,12 @@ void vec_alloc(Ctx& c) {
   c.d_mu = dev_zeros<double>(1, c.stream);
   c.d_alpha = dev_zeros<double>(2, c.stream);
   c.pk = dev_zeros<Packet>(1, c.stream);
-  CMPC_CUDA(cudaHostAlloc(&c.pk_host, sizeof(Packet) + 64, cudaHostAllocMapped));
-  CMPC_CUDA(cudaMallocHost(&c.stage, 64 * sizeof(double)));
+  tick("vectors");
+  {  // packet + sequence word + staging ring: one mapped pinned block from the process pool
+    void* blk = pinned_take();
+    c.pk_host = static_cast<Packet*>(blk);
+    c.stage = reinterpret_cast<double*>(static_cast<char*>(blk) + kStageOff);
+  }
   c.stage_i = 0;
   CMPC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.pk_map), c.pk_host, 0));
   c.pub_host = reinterpret_cast<volatile unsigned long long*>(reinterpret_cast<char*>(c.pk_host) + sizeof(Packet));
@@ -772,7 +819,9 @@ void vec_alloc(Ctx& c) {
   *c.pub_host = 0;
   c.pub_dev = dev_zeros<unsigned long long>(1, c.stream);
   c.pub_expect = 0;
+  tick("pinned");
   chol_alloc(c);
+  tick("chol");
   launch_hmax(c);  // max|h| and h0 on the device
   {  // prototypes with many member rows (duplicates of symmetric segments): warp path
     std::vector<int32_t> mp(size_t(c.p + 1), 0), big;
@@ -788,6 +837,7 @@ void vec_alloc(Ctx& c) {
       CMPC_CUDA(cudaMemcpyAsync(c.proto_big, big.data(), sizeof(int32_t) * big.size(), cudaMemcpyHostToDevice, c.stream));
     CMPC_CUDA(cudaStreamSynchronize(c.stream));
   }
+  tick("big");
   c.sing_ptr = dev_alloc<int32_t>((size_t)n + 1, c.stream);
   k_sing_ptr<<<(unsigned)ceil_div((int64_t)n + 1, 256), 256, 0, c.stream>>>(c.sing_col, c.pz, c.n, c.sing_ptr);
   CMPC_LAUNCHED();
@@ -802,6 +852,7 @@ void vec_alloc(Ctx& c) {
     dev_free(bad, c.stream);
     c.h_symmetric = hb == 0;
   }
+  tick("sym");
 }
 
 void vec_free(Ctx& c) {
@@ -812,8 +863,10 @@ void vec_free(Ctx& c) {
                   (void*)c.vt, (void*)c.yt, (void*)c.yv, (void*)c.Hvt, (void*)c.part, (void*)c.colpart,
                   (void*)c.hmax, (void*)c.pk, (void*)c.d_mu, (void*)c.d_alpha})
     dev_free(p, c.stream);
-  if (c.pk_host) cudaFreeHost(c.pk_host);
-  if (c.stage) cudaFreeHost(c.stage);
+  if (c.pk_host) {
+    CMPC_CUDA(cudaStreamSynchronize(c.stream));  // no staged upload still reading the ring
+    pinned_give(c.pk_host);
+  }
   c.stage = nullptr;
   dev_free(c.sing_ptr, c.stream);
   c.sing_ptr = nullptr;

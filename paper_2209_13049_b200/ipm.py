@@ -156,18 +156,16 @@ class DeviceQp:
         out.h = h
         keep = {}
 
-        def arr(name, a, order="F"):
-            a = np.asarray(a, dtype=np.float64)
-            a = np.asfortranarray(a) if order == "F" else np.ascontiguousarray(a)
+        def arr(name, a):
+            a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))  # no copy for C-ordered input
             keep[name] = a
             return a.ctypes.data_as(_lib.D) if a.size else None
 
-        pr = _lib.LqProblem(nx=dm.n_x, nu=dm.n_u, nc=dm.n_c, T=dm.T)
-        for f in ("A", "B", "Q", "Qf", "R", "S", "E", "F", "K"):
+        # matrices go across row-major (layout 1) and are transposed on the device
+        pr = _lib.LqProblem(nx=dm.n_x, nu=dm.n_u, nc=dm.n_c, T=dm.T, layout=1)
+        for f in ("A", "B", "Q", "Qf", "R", "S", "E", "F", "K", "gl", "gu", "xl", "xu", "ul", "uu", "x_bar"):
             setattr(pr, f, arr(f, getattr(data, f)))
-        for f in ("gl", "gu", "xl", "xu", "ul", "uu", "x_bar"):
-            setattr(pr, f, arr(f, getattr(data, f), "C"))
-        pr.w = arr("w", data.w, "C")
+        pr.w = arr("w", data.w)
         check(L.cmpc_build_qp(out.h, C.byref(pr)))
         info = (C.c_int64 * 8)()
         L.cmpc_qp_info(out.h, info)
