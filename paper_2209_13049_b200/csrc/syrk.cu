@@ -300,10 +300,14 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
   }
 }
 
-// M(i,j) = H(i,j) + (sum of the tile's partials in k order [+ singleton diagonal]), lower
-// (+ mirrored upper); grid (tiles, 16): 256 elements of one tile per block. Thin partials
-// hold rows 0..31 only (flag bit 31 of their id); a warp's 32 elements share one row half,
-// so the skip is warp-uniform. Eight loads in flight, summed in order (deterministic).
+// M(i,j) = H(i,j) + (sum of the tile's partials [+ singleton diagonal]), lower (+ mirrored
+// upper); grid (tiles, 64): 64 elements of one tile per block, four threads per element
+// ("ways"), way w summing the chunks of eight segments w, w + 4, ... (eight loads in flight)
+// and way 0 adding the four in order (deterministic). The first tile column's tiles collect
+// partials from nearly every segment; four ways cut that critical chain by four. Thin
+// partials hold rows 0..31 only (flag bit 31 of their id); a warp's 32 elements share one
+// row half, so the skip is warp-uniform.
+constexpr int kRedWays = 4;
 __global__ void __launch_bounds__(256)
     k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
                   const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ tile_segs,
@@ -312,51 +316,65 @@ __global__ void __launch_bounds__(256)
                   const double* __restrict__ qs, const int32_t* __restrict__ sing_ptr,
                   const double* __restrict__ sing_val, double* __restrict__ rhs,
                   const double* __restrict__ r1) {
+  __shared__ double red[kRedWays][64];
   const int2 tl = tiles[blockIdx.x];
   const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
-  if (rp && tl.x == tl.y && blockIdx.y == 0 && threadIdx.x < kTile) {
-    // fused right-hand side of the block: P' q from the diagonal segments' half-sums (in
-    // k order) + the singleton rows of its columns
-    const int64_t col = (int64_t)kTile * tl.x + threadIdx.x;
+  const int t64 = threadIdx.x & 63, way = threadIdx.x >> 6;
+  if (rp && tl.x == tl.y && blockIdx.y == 0) {
+    // fused right-hand side of the block: P' q from the diagonal segments' half-sums + the
+    // singleton rows of its columns
+    const int64_t col = (int64_t)kTile * tl.x + t64;
+    double s = 0.0;
     if (col < n) {
-      double s = 0.0;
-      for (int q = u0; q < u1; q += 8) {  // eight segments' loads in flight, summed in order
+      for (int q = u0 + 8 * way; q < u1; q += 8 * kRedWays) {
         double x[8];
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
           x[b] = 0.0;
           if (q + b < u1) {
             const int32_t id = tile_segs[q + b] & 0x7fffffff;
-            x[b] = __ldcg(rp + (size_t)id * 128 + threadIdx.x) + __ldcg(rp + (size_t)id * 128 + 64 + threadIdx.x);
+            x[b] = __ldcg(rp + (size_t)id * 128 + t64) + __ldcg(rp + (size_t)id * 128 + 64 + t64);
           }
         }
 #pragma unroll
         for (int b = 0; b < 8; ++b) s += x[b];
       }
+    }
+    red[way][t64] = s;
+    __syncthreads();
+    if (way == 0 && col < n) {
+      s = ((red[0][t64] + red[1][t64]) + red[2][t64]) + red[3][t64];
       for (int32_t k = sing_ptr[col]; k < sing_ptr[col + 1]; ++k) s += sing_val[k] * qs[k];
       // unsharded: the final -r1 + J'(r2 - sigma r3) here (k_rhs's rounding, no extra launch)
       rhs[col] = r1 ? __dadd_rn(-r1[col], s) : s;
     }
+    __syncthreads();
   }
-  const int e = blockIdx.y * blockDim.x + threadIdx.x;
+  const int e = blockIdx.y * 64 + t64;
   const int rl = e & (kTile - 1), cl = e >> 6;
   const int64_t i = (int64_t)kTile * tl.x + rl, j = (int64_t)kTile * tl.y + cl;
-  if (i >= n || j >= n || i < j) return;
+  const bool live = i < n && j < n && i >= j;  // (no early exit: every thread reaches the barrier)
   const bool lower_half = rl >= 32;
   double s = 0.0;
-  for (int q = u0; q < u1; q += 8) {
-    double x[8];
+  if (live) {
+    for (int q = u0 + 8 * way; q < u1; q += 8 * kRedWays) {
+      double x[8];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      x[b] = 0.0;
-      if (q + b < u1) {
-        const int32_t id = __ldg(tile_segs + q + b);
-        if (!(id < 0 && lower_half)) x[b] = __ldcg(partial + (size_t)(id & 0x7fffffff) * (kTile * kTile) + e);
+      for (int b = 0; b < 8; ++b) {
+        x[b] = 0.0;
+        if (q + b < u1) {
+          const int32_t id = __ldg(tile_segs + q + b);
+          if (!(id < 0 && lower_half)) x[b] = __ldcg(partial + (size_t)(id & 0x7fffffff) * (kTile * kTile) + e);
+        }
       }
-    }
 #pragma unroll
-    for (int b = 0; b < 8; ++b) s += x[b];
+      for (int b = 0; b < 8; ++b) s += x[b];
+    }
   }
+  red[way][t64] = s;
+  __syncthreads();
+  if (way != 0 || !live) return;
+  s = ((red[0][t64] + red[1][t64]) + red[2][t64]) + red[3][t64];
   if (i == j) s += dsing[i];
   const double v = H ? H[i + j * n] + s : s;  // H on one rank only when sharded
   M[i + j * n] = v;
@@ -612,7 +630,7 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
     else CMPC_CUDA(cudaEventRecord(after_syrk, c.stream));
   }
   // sharded: every rank's partial J_g' Sigma_g J_g, H added by rank 0; the caller allreduces
-  k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 256), 256, 0, c.stream>>>(
+  k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 64), 64 * kRedWays, 0, c.stream>>>(
       c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr, c.dsing, c.n, c.M,
       mirror ? 1 : 0, with_rhs ? c.rhs_part : nullptr, c.q + c.ldp, c.sing_ptr, c.sing_val, c.rhs,
       with_rhs && !c.comm ? c.r1 : nullptr);

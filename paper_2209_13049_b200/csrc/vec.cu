@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(256) k_rows_gemv(const double* __restrict__ A,
 // per lane, 16-byte loads), the eight warps take interleaved column slices with four loads
 // in flight each, then a fixed-order reduction of the slices. ldp is even (a multiple of
 // kBK), so every row pair is 16-byte aligned. HBM-bound: P is read once.
+template <int D>
 __global__ void __launch_bounds__(256) k_proto_gemv(const double* __restrict__ P, int64_t ldp, int64_t rows,
                                                     const int32_t* __restrict__ hi,
                                                     const double* __restrict__ x, double* __restrict__ y) {
@@ -78,16 +79,16 @@ __global__ void __launch_bounds__(256) k_proto_gemv(const double* __restrict__ P
   const double2* col = reinterpret_cast<const double2*>(P + r);
   const int64_t ld2 = ldp / 2;
   int j = w;
-  for (; j + 24 < wmax; j += 32) {
-    double2 v[4];
-    double xv[4];
+  for (; j + 8 * (D - 1) < wmax; j += 8 * D) {
+    double2 v[D];
+    double xv[D];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < D; ++u) {
       v[u] = r < rows ? __ldcs(col + (j + 8 * u) * ld2) : make_double2(0.0, 0.0);
       xv[u] = x[j + 8 * u];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < D; ++u) {
       const int jj = j + 8 * u;
       const double p0 = jj < w0 ? v[u].x : 0.0, p1 = jj < w1 ? v[u].y : 0.0;
       if (u & 1) {
@@ -132,7 +133,8 @@ __device__ __forceinline__ double jrow(const double* y, int32_t rm) {
 // out[j] partial over a chunk of rc P rows: colpart[chunk*n + j]; one warp per (chunk,
 // column), 16-byte loads (two rows per lane) with four in flight. Column j's nonzeros are
 // the rows >= start_col[j]; the pair containing start_col[j] is read whole and masked.
-__global__ void __launch_bounds__(256) k_ptq_partial(const double* __restrict__ P, int64_t ldp,
+template <int MINB, int D>
+__global__ void __launch_bounds__(256, MINB) k_ptq_partial(const double* __restrict__ P, int64_t ldp,
                                                      int64_t ps, int64_t n,
                                                      const int32_t* __restrict__ start_col,
                                                      const double* __restrict__ q, int rc,
@@ -146,15 +148,15 @@ __global__ void __launch_bounds__(256) k_ptq_partial(const double* __restrict__ 
   const double* col = P + j * ldp;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int64_t k = ka + 2 * lane;
-  for (; k + 192 < k1; k += 256) {
-    double2 v[4], qq[4];
+  for (; k + 64 * (D - 1) < k1; k += 64 * D) {
+    double2 v[D], qq[D];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < D; ++u) {
       v[u] = __ldcs(reinterpret_cast<const double2*>(col + k + 64 * u));
       qq[u] = *reinterpret_cast<const double2*>(q + k + 64 * u);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < D; ++u) {
       const int64_t kk = k + 64 * u;
       const double e0 = kk >= kb ? v[u].x * qq[u].x : 0.0;
       const double e1 = (kk + 1 >= kb && kk + 1 < k1) ? v[u].y * qq[u].y : 0.0;
@@ -965,7 +967,8 @@ void launch_Hx(Ctx& c, const double* x, double* out) {
 
 void launch_Jx(Ctx& c, const double* x, double* y, double* Jx) {
   if (c.ps > 0) {
-    k_proto_gemv<<<(unsigned)ceil_div(c.ps, 64), 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.hi, x, y);
+    // eight 16-byte loads in flight per lane (79% of HBM at config 3; four: 67%)
+    k_proto_gemv<8><<<(unsigned)ceil_div(c.ps, 64), 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.hi, x, y);
     CMPC_LAUNCHED();
   }
   if (c.pz > 0) {
@@ -985,7 +988,8 @@ void launch_Jtq(Ctx& c, const double* q, double* out) {
   if (c.ps > 0) {
     const int rc = 2048;
     dim3 g((unsigned)c.colchunks, (unsigned)ceil_div(c.n, 8));
-    k_ptq_partial<<<g, 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.n, c.start_col, q, rc, c.colpart);
+    // <= 64 registers: four CTAs per SM (74% of HBM at config 3; 102 registers: 61%)
+    k_ptq_partial<4, 4><<<g, 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.n, c.start_col, q, rc, c.colpart);
     CMPC_LAUNCHED();
   }
   k_ptq_final<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(
