@@ -693,7 +693,7 @@ int cmpc_step_directions(cmpc_ctx* x, double tau, double* pv, double* ps, double
     if (!(tau > 0.0 && tau < 1.0)) throw DimError("tau must lie in (0,1)");
     launch_prepare_step(c, nullptr);
     launch_rhs_partial(c);
-    comm_allreduce(c, c.rhs, (size_t)c.n, CommType::f64, CommOp::sum);  // sharded
+    comm_allreduce(c, c.tq, (size_t)c.n, CommType::f64, CommOp::sum);  // sharded
     launch_rhs_final(c);
     launch_chol_solve(c, c.L, c.rhs, c.pv);
     launch_recover(c, tau);

@@ -107,7 +107,12 @@ struct Ctx {
   double *v = nullptr, *s = nullptr, *lam = nullptr, *z = nullptr, *r1 = nullptr, *r2 = nullptr,
          *r3 = nullptr;
   double *Hv = nullptr, *Jtl = nullptr, *y = nullptr, *sigma = nullptr, *omega = nullptr,
-         *q = nullptr, *dsing = nullptr, *rhs = nullptr, *M = nullptr, *L = nullptr;
+         *q = nullptr, *rhs = nullptr, *M = nullptr, *L = nullptr;
+  double* tq = nullptr;  // J'(r2 - sigma r3) of the step (the SYRK's fused right-hand side part)
+  // J'lambda carried along: the recovery forms J' p_lambda = (M - H) pv - tq,
+  // the accepted step adds alpha J' p_lambda to Jtl, and the residual pass skips its J pass
+  double* JtPl = nullptr;
+  bool jtl_recur = false;  // unsharded with rows: the residual after a step reuses Jtl
   double *pv = nullptr, *ps_ = nullptr, *pl = nullptr, *pzd = nullptr, *Jpv = nullptr,
          *vt = nullptr, *yt = nullptr, *Hvt = nullptr;
   double* yv = nullptr;  // P v of the current point (prototype-indexed, like y = P pv)

@@ -87,7 +87,7 @@ void seg_step(Ctx& c, double tau) {
   if (c.comm) {  // M = H + sum_g J_g' Sigma_g J_g and J' (r2 - sigma r3) over all ranks
     comm_group(true);
     comm_allreduce(c, c.M, (size_t)(c.n * c.n), CommType::f64, CommOp::sum);
-    comm_allreduce(c, c.rhs, (size_t)c.n, CommType::f64, CommOp::sum);
+    comm_allreduce(c, c.tq, (size_t)c.n, CommType::f64, CommOp::sum);
     comm_group(false);
   }
   if (c.comm || !fused) launch_rhs_final(c);  // (unsharded + fused: done by k_syrk_reduce)

@@ -311,11 +311,11 @@ constexpr int kRedWays = 4;
 __global__ void __launch_bounds__(256)
     k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
                   const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ tile_segs,
-                  const double* __restrict__ H, const double* __restrict__ dsing, int64_t n,
+                  const double* __restrict__ H, const double* __restrict__ omega_s, int64_t n,
                   double* __restrict__ M, int mirror, const double* __restrict__ rp,
                   const double* __restrict__ qs, const int32_t* __restrict__ sing_ptr,
-                  const double* __restrict__ sing_val, double* __restrict__ rhs,
-                  const double* __restrict__ r1) {
+                  const double* __restrict__ sing_val, double* __restrict__ tq,
+                  double* __restrict__ rhs, const double* __restrict__ r1) {
   __shared__ double red[kRedWays][64];
   const int2 tl = tiles[blockIdx.x];
   const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
@@ -346,7 +346,8 @@ __global__ void __launch_bounds__(256)
       s = ((red[0][t64] + red[1][t64]) + red[2][t64]) + red[3][t64];
       for (int32_t k = sing_ptr[col]; k < sing_ptr[col + 1]; ++k) s += sing_val[k] * qs[k];
       // unsharded: the final -r1 + J'(r2 - sigma r3) here (k_rhs's rounding, no extra launch)
-      rhs[col] = r1 ? __dadd_rn(-r1[col], s) : s;
+      tq[col] = s;
+      if (r1) rhs[col] = __dadd_rn(-r1[col], s);
     }
     __syncthreads();
   }
@@ -375,7 +376,11 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (way != 0 || !live) return;
   s = ((red[0][t64] + red[1][t64]) + red[2][t64]) + red[3][t64];
-  if (i == j) s += dsing[i];
+  if (i == j) {  // + sum over the singleton rows at column i of omega a^2
+    double ds = 0.0;
+    for (int32_t k = sing_ptr[i]; k < sing_ptr[i + 1]; ++k) ds += omega_s[k] * (sing_val[k] * sing_val[k]);
+    s += ds;
+  }
   const double v = H ? H[i + j * n] + s : s;  // H on one rank only when sharded
   M[i + j * n] = v;
   if (mirror && i != j) M[j + i * n] = v;
@@ -631,9 +636,9 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
   }
   // sharded: every rank's partial J_g' Sigma_g J_g, H added by rank 0; the caller allreduces
   k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 64), 64 * kRedWays, 0, c.stream>>>(
-      c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr, c.dsing, c.n, c.M,
-      mirror ? 1 : 0, with_rhs ? c.rhs_part : nullptr, c.q + c.ldp, c.sing_ptr, c.sing_val, c.rhs,
-      with_rhs && !c.comm ? c.r1 : nullptr);
+      c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr, c.omega + c.ldp, c.n, c.M,
+      mirror ? 1 : 0, with_rhs ? c.rhs_part : nullptr, c.q + c.ldp, c.sing_ptr, c.sing_val, c.tq,
+      c.rhs, with_rhs && !c.comm ? c.r1 : nullptr);
   CMPC_LAUNCHED();
 }
 

@@ -119,6 +119,28 @@ __global__ void __launch_bounds__(256) k_proto_gemv(const double* __restrict__ P
   }
 }
 
+// J' p_lambda without a pass over J (J'lambda carried along). With
+// p_lambda = -w + sigma o (J pv) (w = r2 - sigma r3),
+//     J' p_lambda = (J' Sigma J) pv - J' w = (M - H) pv - tq,
+// M the condensed matrix of this step (lower triangle, k_syrk_reduce) and tq = J' w its fused
+// right-hand side part. (M - H) pv has the rounding of the direct P'(omega o P pv) in the
+// worst case (both are bounded by eps |P|' Omega |P| |pv|). One warp per output i: lanes
+// stride j, the lower-triangle element of (i, j) is read from M and H alike.
+__global__ void __launch_bounds__(256) k_jtpl_symv(const double* __restrict__ M, const double* __restrict__ H,
+                                                   int64_t n, const double* __restrict__ pv,
+                                                   const double* __restrict__ tq, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = blockIdx.x * 8ll + (threadIdx.x >> 5);
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t j = lane; j < n; j += 32) {
+    const int64_t e = j >= i ? j + i * n : i + j * n;
+    s += sub(M[e], H[e]) * pv[j];
+  }
+  s = warp_sum(s);
+  if (lane == 0) out[i] = sub(s, tq[i]);
+}
+
 __global__ void k_sing_x(const int32_t* __restrict__ col, const double* __restrict__ val, int64_t pz,
                          const double* __restrict__ x, double* __restrict__ y) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -454,17 +476,6 @@ __global__ void k_sigma_rows(int64_t m, const double* __restrict__ s, const doub
   if (w) w[r] = sub(r2[r], mul(sg, r3[r]));
 }
 
-// dsing[c] = sum over singleton prototypes at column c of omega * a^2
-__global__ void k_dsing(int64_t n, const int32_t* __restrict__ sing_ptr,
-                        const double* __restrict__ sing_val, const double* __restrict__ omega_s,
-                        double* __restrict__ dsing) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  double s = 0.0;
-  for (int32_t k = sing_ptr[j]; k < sing_ptr[j + 1]; ++k) s += omega_s[k] * (sing_val[k] * sing_val[k]);
-  dsing[j] = s;
-}
-
 __global__ void k_rhs(int64_t n, const double* __restrict__ r1, const double* __restrict__ t,
                       int64_t m, double* __restrict__ rhs) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -637,10 +648,12 @@ __global__ void k_update(int64_t n, int64_t m, const double* __restrict__ ap, do
                          const double* __restrict__ ps, double* __restrict__ lam,
                          const double* __restrict__ pl, double* __restrict__ z,
                          const double* __restrict__ pz, int64_t py, double* __restrict__ yv,
-                         const double* __restrict__ y) {
+                         const double* __restrict__ y, double* __restrict__ Jtl,
+                         const double* __restrict__ JtPl) {
   const double alpha = ap[0], alpha_z = ap[1];
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) v[i] = add(v[i], mul(alpha, pv[i]));
+  if (Jtl && i < n) Jtl[i] = add(Jtl[i], mul(alpha, JtPl[i]));  // J'(lambda + alpha p_lambda)
   if (i < py) yv[i] = add(yv[i], mul(alpha, y[i]));  // P v of the new point (see k_trial_rows)
   if (i < m) {
     s[i] = add(s[i], mul(alpha, ps[i]));
@@ -796,7 +809,7 @@ void vec_alloc(Ctx& c) {
   c.v = dev_zeros<double>(n, c.stream); c.s = dev_zeros<double>(m, c.stream); c.lam = dev_zeros<double>(m, c.stream); c.z = dev_zeros<double>(m, c.stream);
   c.r1 = dev_zeros<double>(n, c.stream); c.r2 = dev_zeros<double>(m, c.stream); c.r3 = dev_zeros<double>(m, c.stream);
   c.Hv = dev_zeros<double>(n, c.stream); c.Jtl = dev_zeros<double>(n, c.stream); c.y = dev_zeros<double>(py, c.stream); c.sigma = dev_zeros<double>(m, c.stream);
-  c.omega = dev_zeros<double>(py, c.stream); c.q = dev_zeros<double>(py, c.stream); c.dsing = dev_zeros<double>(n, c.stream); c.rhs = dev_zeros<double>(n, c.stream);
+  c.omega = dev_zeros<double>(py, c.stream); c.q = dev_zeros<double>(py, c.stream); c.tq = dev_zeros<double>(n, c.stream); c.JtPl = dev_zeros<double>(n, c.stream); c.rhs = dev_zeros<double>(n, c.stream);
   c.M = dev_zeros<double>(n * n, c.stream); c.L = dev_zeros<double>(n * n, c.stream);
   c.pv = dev_zeros<double>(n, c.stream); c.ps_ = dev_zeros<double>(m, c.stream); c.pl = dev_zeros<double>(m, c.stream); c.pzd = dev_zeros<double>(m, c.stream);
   c.Jpv = dev_zeros<double>(m, c.stream); c.vt = dev_zeros<double>(n, c.stream); c.yt = dev_zeros<double>(py, c.stream); c.yv = dev_zeros<double>(py, c.stream); c.Hvt = dev_zeros<double>(n, c.stream);
@@ -804,6 +817,7 @@ void vec_alloc(Ctx& c) {
   const int rc = 2048;
   c.colchunks = (int)std::max<int64_t>(1, ceil_div(c.ps, rc));
   c.colpart = dev_zeros<double>((size_t)c.colchunks * n, c.stream);
+  c.jtl_recur = c.m > 0;  // (and no communicator: checked at use, attach comes later)
   c.hmax = dev_zeros<double>(2, c.stream);  // max|h|, h0
   c.d_mu = dev_zeros<double>(1, c.stream);
   c.d_alpha = dev_zeros<double>(2, c.stream);
@@ -860,7 +874,7 @@ void vec_alloc(Ctx& c) {
 void vec_free(Ctx& c) {
   for (void* p : {(void*)c.v, (void*)c.s, (void*)c.lam, (void*)c.z, (void*)c.r1, (void*)c.r2,
                   (void*)c.r3, (void*)c.Hv, (void*)c.Jtl, (void*)c.y, (void*)c.sigma,
-                  (void*)c.omega, (void*)c.q, (void*)c.dsing, (void*)c.rhs, (void*)c.M,
+                  (void*)c.omega, (void*)c.q, (void*)c.tq, (void*)c.JtPl, (void*)c.rhs, (void*)c.M,
                   (void*)c.L, (void*)c.pv, (void*)c.ps_, (void*)c.pl, (void*)c.pzd, (void*)c.Jpv,
                   (void*)c.vt, (void*)c.yt, (void*)c.yv, (void*)c.Hvt, (void*)c.part, (void*)c.colpart,
                   (void*)c.hmax, (void*)c.pk, (void*)c.d_mu, (void*)c.d_alpha})
@@ -882,7 +896,7 @@ void vec_free(Ctx& c) {
   c.pub_map = nullptr;
   chol_free(c);
   c.v = c.s = c.lam = c.z = c.r1 = c.r2 = c.r3 = c.Hv = c.Jtl = c.y = c.sigma = nullptr;
-  c.omega = c.q = c.dsing = c.rhs = c.M = c.L = c.pv = c.ps_ = c.pl = c.pzd = nullptr;
+  c.omega = c.q = c.tq = c.JtPl = c.rhs = c.M = c.L = c.pv = c.ps_ = c.pl = c.pzd = nullptr;
   c.Jpv = c.vt = c.yt = c.yv = c.Hvt = c.part = c.colpart = c.hmax = c.d_mu = c.d_alpha = nullptr;
   c.pk = nullptr;
   c.pk_host = nullptr;
@@ -1017,8 +1031,10 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
     k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.yv, c.d, c.s, c.lam, c.z, c.d_mu, c.r2,
                                            c.r3, c.part, c.pk);
     CMPC_LAUNCHED();
-    launch_proto_reduce<true, false>(c, c.lam, nullptr, c.q, nullptr);
-    launch_Jtq(c, c.q, c.Jtl);
+    if (!(reuse_trial && c.jtl_recur && !c.comm)) {  // (after a step: Jtl was advanced by k_update)
+      launch_proto_reduce<true, false>(c, c.lam, nullptr, c.q, nullptr);
+      launch_Jtq(c, c.q, c.Jtl);
+    }
   } else if (c.comm && c.n > 0) {
     CMPC_CUDA(cudaMemsetAsync(c.Jtl, 0, sizeof(double) * c.n, c.stream));
   }
@@ -1054,10 +1070,7 @@ void launch_residuals_mu(Ctx& c) {
 }
 
 void launch_prepare_step(Ctx& c, const double* sigma_override) {
-  if (c.m == 0) {
-    CMPC_CUDA(cudaMemsetAsync(c.dsing, 0, sizeof(double) * std::max<int64_t>(c.n, 1), c.stream));
-    return;
-  }
+  if (c.m == 0) return;
   k_sigma_rows<<<(unsigned)ceil_div(c.m, 256), 256, 0, c.stream>>>(
       c.m, c.s, c.z, c.r2, c.r3, sigma_override, c.sigma, sigma_override ? nullptr : c.Jpv);
   CMPC_LAUNCHED();
@@ -1065,19 +1078,16 @@ void launch_prepare_step(Ctx& c, const double* sigma_override) {
     launch_proto_reduce<false, false>(c, c.sigma, nullptr, c.omega, nullptr);
   else
     launch_proto_reduce<false, true>(c, c.sigma, c.Jpv, c.omega, c.q);
-  k_dsing<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.sing_ptr, c.sing_val,
-                                                              c.omega + c.ldp, c.dsing);
-  CMPC_LAUNCHED();
 }
 
 void launch_rhs_partial(Ctx& c) {
-  if (c.m > 0) launch_Jtq(c, c.q, c.rhs);
-  else if (c.n > 0) CMPC_CUDA(cudaMemsetAsync(c.rhs, 0, sizeof(double) * c.n, c.stream));
+  if (c.m > 0) launch_Jtq(c, c.q, c.tq);
+  else if (c.n > 0) CMPC_CUDA(cudaMemsetAsync(c.tq, 0, sizeof(double) * c.n, c.stream));
 }
 
 void launch_rhs_final(Ctx& c) {
   if (c.n == 0) return;
-  k_rhs<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.r1, c.rhs, rows_all(c), c.rhs);
+  k_rhs<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.r1, c.tq, rows_all(c), c.rhs);
   CMPC_LAUNCHED();
 }
 
@@ -1118,8 +1128,12 @@ void launch_recover(Ctx& c, double tau) {
     CMPC_LAUNCHED();
   }
   const unsigned pb = part_blocks(c.m);
+  if (c.m > 0) launch_Jx(c, c.pv, c.y, nullptr);
+  if (c.m > 0 && c.jtl_recur && !c.comm && c.n > 0) {  // J' p_lambda for the accepted step
+    k_jtpl_symv<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(c.M, c.H, c.n, c.pv, c.tq, c.JtPl);
+    CMPC_LAUNCHED();
+  }
   if (c.m > 0) {
-    launch_Jx(c, c.pv, c.y, nullptr);
     k_recover_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.s, c.z, c.sigma, c.r2, c.r3,
                                                c.d_mu, tau, c.Jpv, c.ps_, c.pl, c.pzd, c.part, c.pk);
     CMPC_LAUNCHED();
@@ -1212,7 +1226,8 @@ void launch_update_dev(Ctx& c) {
   if (k == 0) return;
   k_update<<<(unsigned)ceil_div(k, 256), 256, 0, c.stream>>>(c.n, c.m, c.d_alpha, c.v, c.pv,
                                                              c.s, c.ps_, c.lam, c.pl, c.z, c.pzd,
-                                                             py, c.yv, c.y);
+                                                             py, c.yv, c.y, c.jtl_recur && !c.comm ? c.Jtl : nullptr,
+                                                             c.JtPl);
   CMPC_LAUNCHED();
 }
 
