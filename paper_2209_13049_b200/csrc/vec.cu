@@ -126,19 +126,58 @@ __global__ void __launch_bounds__(256) k_proto_gemv(const double* __restrict__ P
 // right-hand side part. (M - H) pv has the rounding of the direct P'(omega o P pv) in the
 // worst case (both are bounded by eps |P|' Omega |P| |pv|). One warp per output i: lanes
 // stride j, the lower-triangle element of (i, j) is read from M and H alike.
-__global__ void __launch_bounds__(256) k_jtpl_symv(const double* __restrict__ M, const double* __restrict__ H,
-                                                   int64_t n, const double* __restrict__ pv,
-                                                   const double* __restrict__ tq, double* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = blockIdx.x * 8ll + (threadIdx.x >> 5);
-  if (i >= n) return;
-  double s = 0.0;
-  for (int64_t j = lane; j < n; j += 32) {
-    const int64_t e = j >= i ? j + i * n : i + j * n;
-    s += sub(M[e], H[e]) * pv[j];
+__global__ void __launch_bounds__(1024) k_jtpl_symv(const double* __restrict__ M, const double* __restrict__ H,
+                                                    int64_t n, const double* __restrict__ pv,
+                                                    const double* __restrict__ tq, double* __restrict__ out) {
+  // a CTA owns 32 outputs i0 .. i0 + 31. Part A (j <= i: row i of the lower triangle): lane =
+  // output, the 32 warps stride j, so each load is 32 consecutive rows of one column. Part B
+  // (j > i: column i below the diagonal): warp w takes output i0 + w, lanes stride j along
+  // the column. Loads four at a time; the pieces are added in a fixed order.
+  __shared__ double ra[32][33], rb[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i0 = blockIdx.x * 32ll, ia = i0 + lane, ib = i0 + w;
+  double sa = 0.0, sb = 0.0;
+  if (ia < n) {
+    int64_t j = w;
+    for (; j + 96 <= ia; j += 128) {
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = ia + (j + 32 * u) * n;
+        x[u] = sub(M[e], H[e]) * pv[j + 32 * u];
+      }
+      sa += (x[0] + x[1]) + (x[2] + x[3]);
+    }
+    for (; j <= ia; j += 32) {
+      const int64_t e = ia + j * n;
+      sa += sub(M[e], H[e]) * pv[j];
+    }
   }
-  s = warp_sum(s);
-  if (lane == 0) out[i] = sub(s, tq[i]);
+  if (ib < n) {
+    int64_t j = ib + 1 + lane;
+    for (; j + 96 < n; j += 128) {
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = j + 32 * u + ib * n;
+        x[u] = sub(M[e], H[e]) * pv[j + 32 * u];
+      }
+      sb += (x[0] + x[1]) + (x[2] + x[3]);
+    }
+    for (; j < n; j += 32) {
+      const int64_t e = j + ib * n;
+      sb += sub(M[e], H[e]) * pv[j];
+    }
+  }
+  ra[w][lane] = sa;
+  sb = warp_sum(sb);
+  if (lane == 0) rb[w] = sb;
+  __syncthreads();
+  if (w != 0 || ia >= n) return;
+  double s = 0.0;
+#pragma unroll 8
+  for (int q = 0; q < 32; ++q) s += ra[q][lane];
+  out[ia] = sub(s + rb[lane], tq[ia]);
 }
 
 __global__ void k_sing_x(const int32_t* __restrict__ col, const double* __restrict__ val, int64_t pz,
@@ -1130,7 +1169,7 @@ void launch_recover(Ctx& c, double tau) {
   const unsigned pb = part_blocks(c.m);
   if (c.m > 0) launch_Jx(c, c.pv, c.y, nullptr);
   if (c.m > 0 && c.jtl_recur && !c.comm && c.n > 0) {  // J' p_lambda for the accepted step
-    k_jtpl_symv<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(c.M, c.H, c.n, c.pv, c.tq, c.JtPl);
+    k_jtpl_symv<<<(unsigned)ceil_div(c.n, 32), 1024, 0, c.stream>>>(c.M, c.H, c.n, c.pv, c.tq, c.JtPl);
     CMPC_LAUNCHED();
   }
   if (c.m > 0) {
