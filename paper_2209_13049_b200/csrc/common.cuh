@@ -113,6 +113,31 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
   if (threadIdx.x < 32) r = warp_max((l < NT / 32) ? sh[l] : v);
   return r;
 }
+// NS block sums and NX block maxima with one barrier pair (results valid in warp 0); the same
+// operations in the same order as NS block_sum and NX block_max calls, so bitwise equal.
+// sh: (NS + NX) * 32 doubles.
+template <int NT, int NS, int NX>
+__device__ __forceinline__ void block_sums_maxs(double (&s)[NS], double (&x)[NX], double* sh) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) s[k] = warp_sum(s[k]);
+#pragma unroll
+  for (int k = 0; k < NX; ++k) x[k] = warp_max(x[k]);
+  __syncthreads();
+  if (l == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) sh[k * 32 + w] = s[k];
+#pragma unroll
+    for (int k = 0; k < NX; ++k) sh[(NS + k) * 32 + w] = x[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = warp_sum((l < NT / 32) ? sh[k * 32 + l] : 0.0);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) x[k] = warp_max((l < NT / 32) ? sh[(NS + k) * 32 + l] : x[k]);
+  }
+}
 template <int NT>
 __device__ __forceinline__ double block_min(double v, double* sh) {
 #pragma unroll

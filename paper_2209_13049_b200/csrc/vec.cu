@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kRowT) k_res_rows(int64_t m, const int32_t* __
                                                     const double* __restrict__ mu_p,
                                                     double* __restrict__ r2, double* __restrict__ r3,
                                                     double* __restrict__ part, Packet* pk) {
-  __shared__ double sh[32];
+  __shared__ double sh[7 * 32];
   const double mu = *mu_p;
   double sabs = 0.0, slog = 0.0, ml = 0.0, mss = 0.0, mz = 0.0, mr3 = 0.0, mc = 0.0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
@@ -286,21 +286,16 @@ __global__ void __launch_bounds__(kRowT) k_res_rows(int64_t m, const int32_t* __
     mr3 = fmax(mr3, fabs(t3));
     mc = fmax(mc, fabs(sub(mul(sr, zr), mu)));
   }
-  double t = block_sum<kRowT>(sabs, sh);
-  if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumAbs] = t;
-  t = block_sum<kRowT>(slog, sh);
-  if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumLog] = t;
-  ml = block_max<kRowT>(ml, sh);
-  mss = block_max<kRowT>(mss, sh);
-  mz = block_max<kRowT>(mz, sh);
-  mr3 = block_max<kRowT>(mr3, sh);
-  mc = block_max<kRowT>(mc, sh);
+  double su[2] = {sabs, slog}, mx[5] = {ml, mss, mz, mr3, mc};
+  block_sums_maxs<kRowT>(su, mx, sh);
   if (threadIdx.x == 0) {
-    atomic_max_nonneg(&pk->max_lam, ml);
-    atomic_max_nonneg(&pk->max_s, mss);
-    atomic_max_nonneg(&pk->max_z, mz);
-    atomic_max_nonneg(&pk->max_r3, mr3);
-    atomic_max_nonneg(&pk->max_comp, mc);
+    part[blockIdx.x * kSlots + kSumAbs] = su[0];
+    part[blockIdx.x * kSlots + kSumLog] = su[1];
+    atomic_max_nonneg(&pk->max_lam, mx[0]);
+    atomic_max_nonneg(&pk->max_s, mx[1]);
+    atomic_max_nonneg(&pk->max_z, mx[2]);
+    atomic_max_nonneg(&pk->max_r3, mx[3]);
+    atomic_max_nonneg(&pk->max_comp, mx[4]);
   }
 }
 
@@ -422,50 +417,42 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, i
                                                      const double* __restrict__ part,
                                                      const double* __restrict__ hmax, Packet* pk,
                                                      int mode) {
-  __shared__ double sh[32];
+  __shared__ double sh[5 * 32];
   double sabs = 0.0, slog = 0.0;
-  if (mode != 2) {
+  if (mode != 2)
     for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
       sabs += part[b * kSlots + kSumAbs];
       slog += part[b * kSlots + kSumLog];
     }
-    sabs = block_sum<kFinT>(sabs, sh);
-    __syncthreads();
-    slog = block_sum<kFinT>(slog, sh);
-    __syncthreads();
-    if (mode == 1) {
-      if (threadIdx.x == 0) {
-        pk->sum_abs_r3 = sabs;
-        pk->sum_log_s = slog;
-      }
-      return;
-    }
-  }
   double mr1 = 0.0, vhv = 0.0, hv = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const double g = add(Hv[i], h[i]);
-    const double r = m_all > 0 ? add(g, Jtl[i]) : g;
-    r1[i] = r;
-    mr1 = fmax(mr1, fabs(r));
-    vhv += v[i] * Hv[i];
-    hv += h[i] * v[i];
+  if (mode != 1)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const double g = add(Hv[i], h[i]);
+      const double r = m_all > 0 ? add(g, Jtl[i]) : g;
+      r1[i] = r;
+      mr1 = fmax(mr1, fabs(r));
+      vhv += v[i] * Hv[i];
+      hv += h[i] * v[i];
+    }
+  double su[4] = {sabs, slog, vhv, hv}, mx[1] = {mr1};
+  block_sums_maxs<kFinT>(su, mx, sh);
+  sabs = su[0];
+  slog = su[1];
+  vhv = su[2];
+  hv = su[3];
+  if (mode == 1) {
+    if (threadIdx.x == 0) {
+      pk->sum_abs_r3 = sabs;
+      pk->sum_log_s = slog;
+    }
+    return;
   }
-  vhv = block_sum<kFinT>(vhv, sh);
-  __syncthreads();
-  hv = block_sum<kFinT>(hv, sh);
-  __syncthreads();
-  mr1 = warp_max(mr1);
-  __shared__ double mx[32];
-  if ((threadIdx.x & 31) == 0) mx[threadIdx.x >> 5] = mr1;
-  __syncthreads();
   if (threadIdx.x == 0) {
     if (mode == 2) {
       sabs = pk->sum_abs_r3;
       slog = pk->sum_log_s;
     }
-    double a = 0.0;
-    for (int q = 0; q < kFinT / 32; ++q) a = fmax(a, mx[q]);
-    pk->max_r1 = a;
+    pk->max_r1 = mx[0];
     pk->obj_vHv = vhv;
     pk->obj_hv = hv;
     pk->sum_abs_r3 = m_all > 0 ? sabs : 0.0;
@@ -473,7 +460,7 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, i
     pk->max_h = *hmax;
     pk->objective = 0.5 * vhv + hv + hmax[1];  // h0 on the device: graphs outlive an h0 change
     const double ds = fmax(1.0, fmax(*hmax, pk->max_lam) / (double)(n + m_all));
-    double kkt = a / ds;
+    double kkt = mx[0] / ds;
     if (m_all > 0) {
       const double cs = fmax(1.0, fmax(pk->max_s, pk->max_z) / (double)(2 * m_all));
       kkt = fmax(kkt, pk->max_r3);
@@ -529,7 +516,7 @@ __global__ void __launch_bounds__(kRowT) k_recover_rows(
     const double* __restrict__ r2, const double* __restrict__ r3, const double* __restrict__ mu_p,
     double tau, double* __restrict__ Jpv, double* __restrict__ ps, double* __restrict__ pl,
     double* __restrict__ pz, double* __restrict__ part, Packet* pk) {
-  __shared__ double sh[32];
+  __shared__ double sh[3 * 32];
   const double mu = *mu_p;
   double q = 0.0, as = 1e308, az = 1e308;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
@@ -547,11 +534,12 @@ __global__ void __launch_bounds__(kRowT) k_recover_rows(
     if (p_s < 0.0) as = fmin(as, mul(tau, dv(-sr, p_s)));
     if (p_z < 0.0) az = fmin(az, mul(tau, dv(-zr, p_z)));
   }
-  const double t = block_sum<kRowT>(q, sh);
-  if (threadIdx.x == 0) part[blockIdx.x * kSlots + kSumPsS] = t;
-  as = block_min<kRowT>(as, sh);
-  az = block_min<kRowT>(az, sh);
+  double su[1] = {q}, mx[2] = {-as, -az};  // minima as maxima of the negations (exact)
+  block_sums_maxs<kRowT>(su, mx, sh);
   if (threadIdx.x == 0) {
+    part[blockIdx.x * kSlots + kSumPsS] = su[0];
+    as = -mx[0];
+    az = -mx[1];
     if (as < 1e308) atomic_min_nonneg(&pk->alpha_s_min, as);
     if (az < 1e308) atomic_min_nonneg(&pk->alpha_z_min, az);
   }
@@ -656,29 +644,24 @@ __global__ void __launch_bounds__(kFinT) k_trial_final(int64_t n, int64_t m, int
                                                        const double* __restrict__ Hvt,
                                                        const double* __restrict__ h,
                                                        const double* __restrict__ part, Packet* pk) {
-  __shared__ double sh[32];
+  __shared__ double sh[5 * 32];
   double a = 0.0, b = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     a += vt[i] * Hvt[i];
     b += h[i] * vt[i];
   }
-  a = block_sum<kFinT>(a, sh);
-  __syncthreads();
-  b = block_sum<kFinT>(b, sh);
-  __syncthreads();
   double sabs = 0.0, slog = 0.0;
   for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
     sabs += part[q * kSlots + kSumAbs];
     slog += part[q * kSlots + kSumLog];
   }
-  sabs = block_sum<kFinT>(sabs, sh);
-  __syncthreads();
-  slog = block_sum<kFinT>(slog, sh);
+  double su[4] = {a, b, sabs, slog}, dummy[1] = {0.0};
+  block_sums_maxs<kFinT>(su, dummy, sh);
   if (threadIdx.x == 0) {
-    pk->t_vHv = a;
-    pk->t_hv = b;
-    pk->t_sum_abs = m > 0 ? sabs : 0.0;
-    pk->t_sum_log = m > 0 ? slog : 0.0;
+    pk->t_vHv = su[0];
+    pk->t_hv = su[1];
+    pk->t_sum_abs = m > 0 ? su[2] : 0.0;
+    pk->t_sum_log = m > 0 ? su[3] : 0.0;
   }
 }
 
