@@ -66,11 +66,19 @@ __global__ void __launch_bounds__(256) k_rows_gemv(const double* __restrict__ A,
 template <int D>
 __global__ void __launch_bounds__(256) k_proto_gemv(const double* __restrict__ P, int64_t ldp, int64_t rows,
                                                     const int32_t* __restrict__ hi,
-                                                    const double* __restrict__ x, double* __restrict__ y) {
+                                                    const double* __restrict__ x, double* __restrict__ y,
+                                                    int gblocks, const int32_t* __restrict__ sing_col,
+                                                    const double* __restrict__ sing_val, int64_t pz,
+                                                    double* __restrict__ ys) {
   __shared__ double2 red[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if ((int)blockIdx.x >= gblocks) {  // the singleton prototypes: y_k = a_k x[col_k]
+    const int64_t k = ((int64_t)blockIdx.x - gblocks) * 256 + threadIdx.x;
+    if (k < pz) ys[k] = sing_val[k] * x[sing_col[k]];
+    return;
+  }
   // widest rows first (rows are sorted by width): the heavy blocks start in the first wave
-  const int64_t r = (int64_t)(gridDim.x - 1 - blockIdx.x) * 64 + 2 * lane;
+  const int64_t r = (int64_t)(gblocks - 1 - blockIdx.x) * 64 + 2 * lane;
   const int w0 = r < rows ? hi[r] : 0, w1 = r + 1 < rows ? hi[r + 1] : 0;
   int wmax = max(w0, w1);
 #pragma unroll
@@ -671,10 +679,14 @@ __global__ void k_update(int64_t n, int64_t m, const double* __restrict__ ap, do
                          const double* __restrict__ pl, double* __restrict__ z,
                          const double* __restrict__ pz, int64_t py, double* __restrict__ yv,
                          const double* __restrict__ y, double* __restrict__ Jtl,
-                         const double* __restrict__ JtPl) {
+                         const double* __restrict__ JtPl, double* __restrict__ Hv,
+                         const double* __restrict__ Hvt) {
   const double alpha = ap[0], alpha_z = ap[1];
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) v[i] = add(v[i], mul(alpha, pv[i]));
+  // H v of the new point: the accepted (= last) trial's H v_t, same kernel and inputs, bit for
+  // bit (a residual pass that recomputes H v overwrites it)
+  if (i < n) Hv[i] = Hvt[i];
   if (Jtl && i < n) Jtl[i] = add(Jtl[i], mul(alpha, JtPl[i]));  // J'(lambda + alpha p_lambda)
   if (i < py) yv[i] = add(yv[i], mul(alpha, y[i]));  // P v of the new point (see k_trial_rows)
   if (i < m) {
@@ -1002,14 +1014,13 @@ void launch_Hx(Ctx& c, const double* x, double* out) {
 }
 
 void launch_Jx(Ctx& c, const double* x, double* y, double* Jx) {
-  if (c.ps > 0) {
-    // eight 16-byte loads in flight per lane (79% of HBM at config 3; four: 67%)
-    k_proto_gemv<8><<<(unsigned)ceil_div(c.ps, 64), 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.hi, x, y);
-    CMPC_LAUNCHED();
-  }
-  if (c.pz > 0) {
-    k_sing_x<<<(unsigned)ceil_div(c.pz, 256), 256, 0, c.stream>>>(c.sing_col, c.sing_val, c.pz, x,
-                                                                  y + c.ldp);
+  // eight 16-byte loads in flight per lane (79% of HBM at config 3; four: 67%); the singleton
+  // prototypes ride along as extra CTAs
+  const int gblocks = (int)ceil_div(c.ps, 64);
+  const int sblocks = (int)ceil_div(c.pz, 256);
+  if (gblocks + sblocks > 0) {
+    k_proto_gemv<8><<<(unsigned)(gblocks + sblocks), 256, 0, c.stream>>>(c.P, c.ldp, c.ps, c.hi, x, y, gblocks,
+                                                                        c.sing_col, c.sing_val, c.pz, y + c.ldp);
     CMPC_LAUNCHED();
   }
   (void)Jx;
@@ -1040,14 +1051,10 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
     k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 0);
     CMPC_LAUNCHED();
   }
-  if (reuse_trial) {
-    // v was just set to the accepted trial point v + alpha pv: H v is the trial's (same
-    // kernel, same inputs, bit for bit) and k_update carried P v along as yv + alpha P pv,
-    // the values the trial's merit used
-    if (c.n > 0) CMPC_CUDA(cudaMemcpyAsync(c.Hv, c.Hvt, sizeof(double) * c.n, cudaMemcpyDeviceToDevice, c.stream));
-  } else {
-    launch_Hx(c, c.v, c.Hv);
-  }
+  // reuse_trial: v was just set to the accepted trial point v + alpha pv; k_update copied the
+  // trial's H v_t into H v and carried P v along as yv + alpha P pv, the values the trial's
+  // merit used
+  if (!reuse_trial) launch_Hx(c, c.v, c.Hv);
   if (c.m > 0) {
     if (!reuse_trial) launch_Jx(c, c.v, c.yv, nullptr);
     k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.yv, c.d, c.s, c.lam, c.z, c.d_mu, c.r2,
@@ -1150,11 +1157,15 @@ void launch_recover(Ctx& c, double tau) {
     CMPC_LAUNCHED();
   }
   const unsigned pb = part_blocks(c.m);
-  if (c.m > 0) launch_Jx(c, c.pv, c.y, nullptr);
-  if (c.m > 0 && c.jtl_recur && !c.comm && c.n > 0) {  // J' p_lambda for the accepted step
-    k_jtpl_symv<<<(unsigned)ceil_div(c.n, 32), 1024, 0, c.stream>>>(c.M, c.H, c.n, c.pv, c.tq, c.JtPl);
+  const bool side = c.m > 0 && c.jtl_recur && !c.comm && c.n > 0;
+  if (side) {  // J' p_lambda for the step, beside the recovery pass (joined below)
+    CMPC_CUDA(cudaEventRecord(c.fork, c.stream));
+    CMPC_CUDA(cudaStreamWaitEvent(c.stream2, c.fork, 0));
+    k_jtpl_symv<<<(unsigned)ceil_div(c.n, 32), 1024, 0, c.stream2>>>(c.M, c.H, c.n, c.pv, c.tq, c.JtPl);
     CMPC_LAUNCHED();
+    CMPC_CUDA(cudaEventRecord(c.join, c.stream2));
   }
+  if (c.m > 0) launch_Jx(c, c.pv, c.y, nullptr);
   if (c.m > 0) {
     k_recover_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.s, c.z, c.sigma, c.r2, c.r3,
                                                c.d_mu, tau, c.Jpv, c.ps_, c.pl, c.pzd, c.part, c.pk);
@@ -1163,6 +1174,7 @@ void launch_recover(Ctx& c, double tau) {
   k_recover_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m > 0 ? (int)pb : 0, c.Hv, c.h, c.pv, c.part,
                                              c.pk);
   CMPC_LAUNCHED();
+  if (side) CMPC_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
   if (c.comm) {  // step-length minima and sum ps/s over every rank's rows
     comm_group(true);
     comm_allreduce(c, &c.pk->alpha_s_min, 2, CommType::f64, CommOp::min);
@@ -1249,7 +1261,7 @@ void launch_update_dev(Ctx& c) {
   k_update<<<(unsigned)ceil_div(k, 256), 256, 0, c.stream>>>(c.n, c.m, c.d_alpha, c.v, c.pv,
                                                              c.s, c.ps_, c.lam, c.pl, c.z, c.pzd,
                                                              py, c.yv, c.y, c.jtl_recur && !c.comm ? c.Jtl : nullptr,
-                                                             c.JtPl);
+                                                             c.JtPl, c.Hv, c.Hvt);
   CMPC_LAUNCHED();
 }
 
