@@ -85,6 +85,7 @@ struct Ctx {
   int32_t* sing_ptr = nullptr;   // n+1: singleton prototypes of column j are [sing_ptr[j], sing_ptr[j+1])
   int32_t* proto_big = nullptr;  // prototypes with more than 8 member rows (k_proto_reduce warp path)
   int nbig = 0;
+  int64_t nzero = 0;  // member rows of the zero prototype (zero_k)
   bool h_symmetric = false;      // H == H' bitwise: H x as column dots
   std::vector<int32_t> h_start_col;
 

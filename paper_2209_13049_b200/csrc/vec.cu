@@ -329,7 +329,31 @@ __global__ void __launch_bounds__(kRowT) k_mu_rows(int64_t m, const double* __re
 // (signed when SIGNED1), out2[k] = signed sum of x2; members in ascending row order.
 // One lane per prototype, members in fixed (ascending) order; the all-zero row group
 // (if any) contributes nothing and is skipped.
-template <bool SIGNED1, bool HAS2>
+// SIGMA: the member values are formed here from the rows' state (k_sigma_rows folded in):
+// x1 = sigma = z / s (also stored per row), x2 = w = r2 - sigma r3; the zero prototype's rows
+// get their sigma from the extra CTAs after the warp path (they add nothing to the sums).
+struct SigmaRows {
+  const double *s, *z, *r2, *r3;
+  double* sigma;
+  int zero_blocks;
+  int big_blocks;
+};
+
+template <bool SIGMA>
+__device__ __forceinline__ void member_values(const SigmaRows& sr, const double* x1, const double* x2, int32_t r,
+                                              double& a, double& b) {
+  if (SIGMA) {
+    const double sg = dv(sr.z[r], sr.s[r]);
+    sr.sigma[r] = sg;
+    a = sg;
+    b = sub(sr.r2[r], mul(sg, sr.r3[r]));
+  } else {
+    a = x1[r];
+    b = x2 ? x2[r] : 0.0;
+  }
+}
+
+template <bool SIGNED1, bool HAS2, bool SIGMA = false>
 __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* __restrict__ mem_ptr,
                                                       const int32_t* __restrict__ mem_rows,
                                                       const double* __restrict__ x1,
@@ -338,8 +362,16 @@ __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* 
                                                       double* __restrict__ out2, int64_t ps,
                                                       int64_t ldp, int64_t zero_k,
                                                       const int32_t* __restrict__ big, int nbig,
-                                                      int lane_blocks) {
+                                                      int lane_blocks, SigmaRows sr) {
   const int lane = threadIdx.x & 31;
+  if (SIGMA && (int)blockIdx.x >= lane_blocks + sr.big_blocks) {  // the zero prototype's rows
+    const int64_t e = (int64_t)mem_ptr[zero_k] + ((int64_t)blockIdx.x - lane_blocks - sr.big_blocks) * 256 + threadIdx.x;
+    if (e < mem_ptr[zero_k + 1]) {
+      const int32_t r = mem_rows[e] >> 1;
+      sr.sigma[r] = dv(sr.z[r], sr.s[r]);
+    }
+    return;
+  }
   if ((int)blockIdx.x >= lane_blocks) {
     // a prototype with more than kLaneMembers members: one warp, lanes stride the members
     // (ascending per lane), fixed butterfly sum across the lanes
@@ -351,12 +383,10 @@ __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* 
     for (int32_t e = b0 + lane; e < b1; e += 32) {
       const int32_t rm = mem_rows[e];
       const int32_t r = rm >> 1;
-      const double a = x1[r];
+      double a, bb;
+      member_values<SIGMA>(sr, x1, HAS2 ? x2 : nullptr, r, a, bb);
       s1 += (SIGNED1 && (rm & 1)) ? -a : a;
-      if (HAS2) {
-        const double bb = x2[r];
-        s2 += (rm & 1) ? -bb : bb;
-      }
+      if (HAS2) s2 += (rm & 1) ? -bb : bb;
     }
     s1 = warp_sum(s1);
     if (HAS2) s2 = warp_sum(s2);
@@ -387,12 +417,10 @@ __global__ void __launch_bounds__(256) k_proto_reduce(int64_t p, const int32_t* 
       if (b0 + u < b1) {
         const int32_t rm = mem_rows[b0 + u];
         const int32_t r = rm >> 1;
-        const double a = x1[r];
+        double a, bb;
+        member_values<SIGMA>(sr, x1, HAS2 ? x2 : nullptr, r, a, bb);
         v1[u] = (SIGNED1 && (rm & 1)) ? -a : a;
-        if (HAS2) {
-          const double bb = x2[r];
-          v2[u] = (rm & 1) ? -bb : bb;
-        }
+        if (HAS2) v2[u] = (rm & 1) ? -bb : bb;
       }
     }
 #pragma unroll
@@ -882,6 +910,7 @@ void vec_alloc(Ctx& c) {
     for (int64_t k = 0; k < c.p; ++k)
       if (k != c.zero_k && mp[size_t(k + 1)] - mp[size_t(k)] > kLaneMembers) big.push_back((int32_t)k);
     c.nbig = (int)big.size();
+    c.nzero = c.zero_k >= 0 ? mp[size_t(c.zero_k + 1)] - mp[size_t(c.zero_k)] : 0;
     c.proto_big = dev_alloc<int32_t>(std::max<size_t>(1, big.size()), c.stream);
     if (!big.empty())
       CMPC_CUDA(cudaMemcpyAsync(c.proto_big, big.data(), sizeof(int32_t) * big.size(), cudaMemcpyHostToDevice, c.stream));
@@ -971,7 +1000,20 @@ void launch_proto_reduce(Ctx& c, const double* x1, const double* x2, double* out
   const int grid = lane_blocks + (int)ceil_div(c.nbig, 8);
   k_proto_reduce<SIGNED1, HAS2><<<(unsigned)grid, 256, 0, c.stream>>>(
       c.p, c.mem_ptr, c.mem_rows, x1, x2, out1, out2, c.ps, c.ldp, c.zero_k, c.proto_big, c.nbig,
-      lane_blocks);
+      lane_blocks, SigmaRows{});
+  CMPC_LAUNCHED();
+}
+
+// sigma = z / s per row, then omega (prototype sums of sigma) and q (signed prototype sums of
+// r2 - sigma r3) in one launch (k_sigma_rows + k_proto_reduce<false, true>)
+void launch_sigma_reduce(Ctx& c) {
+  const int lane_blocks = (int)ceil_div(c.p, 256);
+  const int big_blocks = (int)ceil_div(c.nbig, 8);
+  const int zero_blocks = c.zero_k >= 0 ? (int)ceil_div(c.nzero, 256) : 0;
+  const SigmaRows sr{c.s, c.z, c.r2, c.r3, c.sigma, zero_blocks, big_blocks};
+  k_proto_reduce<false, true, true><<<(unsigned)(lane_blocks + big_blocks + zero_blocks), 256, 0, c.stream>>>(
+      c.p, c.mem_ptr, c.mem_rows, nullptr, nullptr, c.omega, c.q, c.ps, c.ldp, c.zero_k, c.proto_big, c.nbig,
+      lane_blocks, sr);
   CMPC_LAUNCHED();
 }
 
@@ -1100,13 +1142,14 @@ void launch_residuals_mu(Ctx& c) {
 
 void launch_prepare_step(Ctx& c, const double* sigma_override) {
   if (c.m == 0) return;
-  k_sigma_rows<<<(unsigned)ceil_div(c.m, 256), 256, 0, c.stream>>>(
-      c.m, c.s, c.z, c.r2, c.r3, sigma_override, c.sigma, sigma_override ? nullptr : c.Jpv);
-  CMPC_LAUNCHED();
-  if (sigma_override)
+  if (sigma_override) {
+    k_sigma_rows<<<(unsigned)ceil_div(c.m, 256), 256, 0, c.stream>>>(c.m, c.s, c.z, c.r2, c.r3, sigma_override,
+                                                                    c.sigma, nullptr);
+    CMPC_LAUNCHED();
     launch_proto_reduce<false, false>(c, c.sigma, nullptr, c.omega, nullptr);
-  else
-    launch_proto_reduce<false, true>(c, c.sigma, c.Jpv, c.omega, c.q);
+  } else {
+    launch_sigma_reduce(c);
+  }
 }
 
 void launch_rhs_partial(Ctx& c) {
