@@ -879,7 +879,8 @@ void vec_alloc(Ctx& c) {
   const int rc = 2048;
   c.colchunks = (int)std::max<int64_t>(1, ceil_div(c.ps, rc));
   c.colpart = dev_zeros<double>((size_t)c.colchunks * n, c.stream);
-  c.jtl_recur = c.m > 0;  // (and no communicator: checked at use, attach comes later)
+  // (and no communicator: checked at use); CMPC_NO_RECUR (debug): the residual's own J'lambda pass
+  c.jtl_recur = c.m > 0 && !getenv("CMPC_NO_RECUR");
   c.hmax = dev_zeros<double>(2, c.stream);  // max|h|, h0
   c.d_mu = dev_zeros<double>(1, c.stream);
   c.d_alpha = dev_zeros<double>(2, c.stream);
@@ -1200,13 +1201,11 @@ void launch_recover(Ctx& c, double tau) {
     CMPC_LAUNCHED();
   }
   const unsigned pb = part_blocks(c.m);
-  const bool side = c.m > 0 && c.jtl_recur && !c.comm && c.n > 0;
-  if (side) {  // J' p_lambda for the step, beside the recovery pass (joined below)
-    CMPC_CUDA(cudaEventRecord(c.fork, c.stream));
-    CMPC_CUDA(cudaStreamWaitEvent(c.stream2, c.fork, 0));
-    k_jtpl_symv<<<(unsigned)ceil_div(c.n, 32), 1024, 0, c.stream2>>>(c.M, c.H, c.n, c.pv, c.tq, c.JtPl);
+  // J' p_lambda for the step (in line: a side-stream branch was no faster alone and cost 45%
+  // in batch mode, where 15 contexts share the GPU)
+  if (c.m > 0 && c.jtl_recur && !c.comm && c.n > 0) {
+    k_jtpl_symv<<<(unsigned)ceil_div(c.n, 32), 1024, 0, c.stream>>>(c.M, c.H, c.n, c.pv, c.tq, c.JtPl);
     CMPC_LAUNCHED();
-    CMPC_CUDA(cudaEventRecord(c.join, c.stream2));
   }
   if (c.m > 0) launch_Jx(c, c.pv, c.y, nullptr);
   if (c.m > 0) {
@@ -1217,7 +1216,6 @@ void launch_recover(Ctx& c, double tau) {
   k_recover_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m > 0 ? (int)pb : 0, c.Hv, c.h, c.pv, c.part,
                                              c.pk);
   CMPC_LAUNCHED();
-  if (side) CMPC_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
   if (c.comm) {  // step-length minima and sum ps/s over every rank's rows
     comm_group(true);
     comm_allreduce(c, &c.pk->alpha_s_min, 2, CommType::f64, CommOp::min);
