@@ -511,6 +511,7 @@ int cmpc_time_phase(cmpc_ctx* x, int what, int reps, double* ms_per_rep) {
         case 8: launch_Jtq(c, c.q, c.Jtl); break;
         case 9: launch_prepare_step(c, nullptr); break;
         case 10: launch_cholesky(c, c.M, c.L, 0.0, c.rhs, c.pv); break;
+        case 11: launch_condense(c, false, c.ps > 0 && c.npieces > 0); break;  // + fused P'q
         default: throw DimError("unknown phase");
       }
     };

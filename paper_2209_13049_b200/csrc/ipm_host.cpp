@@ -79,8 +79,11 @@ void rec(cudaEvent_t e, cudaStream_t s) {
 void seg_step(Ctx& c, double tau) {
   rec(c.ev0, c.stream);
   launch_prepare_step(c, nullptr);
-  const bool fused = c.ps > 0 && c.npieces > 0;
-  if (!fused) launch_rhs_partial(c);  // no SYRK rows: the singleton part only
+  // right-hand side P'q fused into the SYRK's diagonal jobs, or a separate pass over P: the
+  // fused form costs ~9% of the SYRK at n = 500 (the pass: 14%) but ~6% at n = 2000 (the pass:
+  // 3%), so large n takes the pass (tools/phases.py: condense vs condense_rhs vs Jty)
+  const bool fused = c.ps > 0 && c.npieces > 0 && c.n <= 1024;
+  if (!fused) launch_rhs_partial(c);  // J'(r2 - sigma r3) by its own pass over P
   rec(c.ev2, c.stream);
   launch_condense(c, false, fused, c.ev4);
   rec(c.ev3, c.stream);

@@ -63,6 +63,11 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
 
 // D(16x8) += A(16x16, row) B(16x8, col), FP64 (lowers to DMMA.8x8x4 on sm_100a)
 __device__ __forceinline__ void dmma16816(double* d, const double* a, const double* b) {

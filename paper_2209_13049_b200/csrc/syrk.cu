@@ -125,8 +125,10 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[f][b][c] = 0.0;
   // fused right-hand side: a diagonal job streams every nonzero row of its column block, so
-  // thread (kh, cc) also sums P(k, cc) q(k) over its half of each stage's 32 rows
-  double rq = 0.0;
+  // thread (kh, cc) also sums P(k, cc) q(k) over its half of each stage's 32 rows: after the
+  // stage's MMAs are issued (the FMAs overlap the tensor pipe), 16-byte loads of row pairs into
+  // two accumulators (even and odd rows, added at the end)
+  double rq[2] = {0.0, 0.0};
   const bool do_rq = DIAG && a.q != nullptr && (!THIN || (threadIdx.x & 63) < 32);
 
   for (int it = it0; it < it0 + nsteps; ++it) {
@@ -137,12 +139,6 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
     const uint32_t sA = smem_u32(smem + s * kStageBytes);
     const uint32_t sB = DIAG ? sA : sA + kOpBytes;
     const uint32_t sW = sA + 2 * kOpBytes;
-    if (DIAG && do_rq) {
-      const int cc = threadIdx.x & 63, k0 = 16 * (threadIdx.x >> 6);
-      const uint32_t sQ = sW + 256;
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) rq = fma(lds64(sA + op_off(cc, k0 + kk)), lds64(sQ + 8 * (k0 + kk)), rq);
-    }
 #pragma unroll
     for (int ks = 0; ks < kBK; ks += 16) {
       double af[2][8], ax[2][8];  // A fragments of half r0 (ax: half 0 for the mixed warp)
@@ -172,11 +168,22 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
         }
       }
     }
+    if (DIAG && do_rq) {
+      const int cc = threadIdx.x & 63, k0 = 16 * (threadIdx.x >> 6);
+      const uint32_t sQ = sW + 256;
+#pragma unroll
+      for (int kk = 0; kk < 16; kk += 2) {  // rows k, k+1 of column cc share one 16-byte chunk
+        const double2 pa = lds128(sA + op_off(cc, k0 + kk));
+        const double2 qq = lds128(sQ + 8 * (k0 + kk));
+        rq[0] = fma(pa.x, qq.x, rq[0]);
+        rq[1] = fma(pa.y, qq.y, rq[1]);
+      }
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   store_partial<NF>(a, sg, acc, fr, fn, lane);
-  if (DIAG && a.q) a.rhs_part[(size_t)sg * 128 + threadIdx.x] = rq;
+  if (DIAG && a.q) a.rhs_part[(size_t)sg * 128 + threadIdx.x] = rq[0] + rq[1];
 }
 
 // 2 CTAs per SM: 168 registers (each SM sub-partition holds 3 warps of 168 x 32; the few

@@ -222,7 +222,7 @@ class DeviceQp:
                     singletons=out[4], syrk_units=out[5], syrk_flops=out[6], p_bytes=out[7])
 
     PHASES = dict(condense_all=0, condense=1, cholesky=2, chol_solve=3, residuals=4, recover=5,
-                  trial=6, Jx=7, Jty=8, prepare=9, chol_fused=10)
+                  trial=6, Jx=7, Jty=8, prepare=9, chol_fused=10, condense_rhs=11)
 
     def time_phase(self, name: str, reps: int = 10) -> float:
         """Device milliseconds of one phase (CUDA events, back-to-back launches)."""

@@ -24,11 +24,11 @@ for cfg in cfgs:
     print(f"   solve: {r.status.name} iter={r.iter} total={r.total_seconds*1e3:.2f}ms device={r.device_seconds*1e3:.2f}ms "
           f"syrk={r.syrk_seconds*1e3:.2f}ms chol={r.chol_seconds*1e3:.2f}ms launches={r.launches} syncs={r.syncs}")
     per = {}
-    for ph in ["prepare", "condense", "cholesky", "chol_solve", "chol_fused", "residuals", "recover", "trial", "Jx", "Jty"]:
+    for ph in ["prepare", "condense", "condense_rhs", "cholesky", "chol_solve", "chol_fused", "residuals", "recover", "trial", "Jx", "Jty"]:
         per[ph] = dq.time_phase(ph, 20)
     for k, v in per.items():
         extra = ""
-        if k == "condense":
+        if k in ("condense", "condense_rhs"):
             extra = f"  {info['syrk_flops'] / (v * 1e-3) / 1e12:.2f} TF/s ({100 * info['syrk_flops'] / (v * 1e-3) / 37.1e12:.1f}% of 37.1)"
         if k in ("Jx", "Jty"):
             extra = f"  {info['p_bytes'] / (v * 1e-3) / 1e9:.0f} GB/s of P"
