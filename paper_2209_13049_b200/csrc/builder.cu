@@ -11,10 +11,12 @@
 //   H_jk = 2 (sum_{s < T-1-max(j,k)} C[a0+s, b0+s] + Cf[T-1-j, T-1-k] + R_jk + cross)
 //          (a0, b0) = (max - j, max - k): the block-Toeplitz sums of bigB' Q bigB
 //   h_j  = 2 sum_{t > j} (Gall' Q_t x0_t)[block t-1-j] + 2 S_K' x0_j,   h0 = sum x0' Q_t x0
-//   J, d: one row per finite bound in the reference's row order, filled from Gall (state
-//         rows), K Gall (input rows) and (E + F K) Gall (mixed rows).
-// The built H, h, h0, J, d are then loaded like a host QP (structure analysis, plan); Gall,
-// x0 and the row table stay resident for refresh_initial_state and recover_trajectory, so a
+//   J, d: one row per finite bound in the reference's row order, from Gall (state rows),
+//         K Gall (input rows) and (E + F K) Gall (mixed rows). J is never stored (SURVEY
+//         §8(f) row 2): the structure analysis reads it row by row (jrows.cuh, BuiltJ) and
+//         keeps only the distinct rows P.
+// The built H, h, h0, d are then loaded like a host QP (structure analysis, plan); Gall, x0 and
+// the row table stay resident for refresh_initial_state and recover_trajectory, so a
 // receding-horizon step uploads n_x numbers and never re-analyses J.
 #include <algorithm>
 #include <chrono>
@@ -24,6 +26,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "jrows.cuh"
 
 namespace cmpc {
 
@@ -197,10 +200,6 @@ __global__ void k_transpose(int64_t r, int64_t c, const double* __restrict__ src
   }
 }
 
-// one row of J: kind 0 mixed (E + F K), 1 state, 2 input; upper bound or lower; stage t; index i
-struct RowDesc {
-  int kind, upper, t, i;
-};
 
 // the six (kind, side) groups of rows in the reference's order: group g holds rows
 // first .. first + nt * len - 1, stage t0 + r / len, index list[r % len]
@@ -293,33 +292,6 @@ __global__ void k_rows_d(int64_t m, const RowDesc* __restrict__ rd, const double
   d[r] = q.upper ? bound[r] - off : off - bound[r];
 }
 
-// J (m x n, column-major): a thread owns one row and a chunk of 32 columns (its descriptor
-// read once); consecutive threads write consecutive rows of a column, so the stores coalesce
-constexpr int kJCols = 32;
-__global__ void k_rows_J(int64_t m, int64_t n, const RowDesc* __restrict__ rd, const double* __restrict__ G,
-                         const double* __restrict__ KG, const double* __restrict__ EG,
-                         const double* __restrict__ F, int nx, int nu, int nc, double* __restrict__ J) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  const RowDesc q = rd[r];
-  const double sg = q.upper ? 1.0 : -1.0;
-  const int64_t c0 = (int64_t)blockIdx.y * kJCols, c1 = min(n, c0 + kJCols);
-  for (int64_t col = c0; col < c1; ++col) {
-    const int j = (int)(col / nu), cc = (int)(col - (int64_t)j * nu);
-    double v = 0.0;
-    if (j < q.t) {
-      const int64_t gc = (int64_t)(q.t - 1 - j) * nu + cc;  // column of G_{t-1-j}
-      if (q.kind == 1) v = G[q.i + gc * nx];
-      else if (q.kind == 2) v = KG ? KG[q.i + gc * nu] : 0.0;
-      else v = EG[q.i + gc * nc];
-      v *= sg;
-    }
-    if (q.kind == 2 && col == (int64_t)q.t * nu + q.i) v += sg;
-    if (q.kind == 0 && j == q.t) v += sg * F[q.i + (int64_t)cc * nc];
-    __stcs(J + r + col * m, v);
-  }
-}
-
 // x_t = x0_t + sum_{j<t} G_{t-1-j} v_j (X: n_x x (T+1))
 __global__ void k_traj(int nx, int nu, int T, const double* __restrict__ X0, const double* __restrict__ G,
                        const double* __restrict__ v, double* __restrict__ X) {
@@ -356,6 +328,8 @@ struct ProblemDev {
          *S = nullptr, *K = nullptr, *EFK = nullptr, *F = nullptr, *W = nullptr, *X0 = nullptr,
          *bound = nullptr, *Q = nullptr;
   RowDesc* rows = nullptr;
+  double *KG = nullptr, *EG = nullptr;  // K Gall, (E + F K) Gall: the input and mixed rows
+  BuiltJ J{};                           // J, row by row, for the structure analysis
 };
 
 void prob_free(Ctx& c) {
@@ -363,7 +337,7 @@ void prob_free(Ctx& c) {
   if (!p) return;
   for (void* q : {(void*)p->AK, (void*)p->G, (void*)p->QK, (void*)p->Qf, (void*)p->R, (void*)p->SK,
                   (void*)p->S, (void*)p->K, (void*)p->EFK, (void*)p->F, (void*)p->W, (void*)p->X0,
-                  (void*)p->bound, (void*)p->Q, (void*)p->rows})
+                  (void*)p->bound, (void*)p->Q, (void*)p->rows, (void*)p->KG, (void*)p->EG})
     dev_free(q, c.stream);
   delete p;
   c.prob = nullptr;
@@ -570,14 +544,10 @@ void prob_build(Ctx& c, const cmpc_lq_problem& in, double** H_out, double** h_ou
     EG = dev_alloc<double>(size_t(nc * n), st);
     gemm(st, false, false, nc, n, nx, 1.0, p.EFK, nc, p.G, nx, 0.0, EG, nc);
   }
-  double* J = dev_alloc<double>(size_t(std::max<int64_t>(m * n, 1)), st);
-  if (m > 0) {
-    k_rows_J<<<dim3((unsigned)ceil_div(m, 256), (unsigned)ceil_div(n, kJCols)), 256, 0, st>>>(m, n, p.rows, p.G, KG, EG, p.F, (int)nx, (int)nu, (int)nc, J);
-    CMPC_LAUNCHED();
-  }
-  dev_free(KG, st);
-  dev_free(EG, st);
-  tick("J");
+  // J itself is never stored: the structure analysis reads it row by row through BuiltJ
+  p.KG = KG;
+  p.EG = EG;
+  p.J = BuiltJ{p.rows, p.G, KG, EG, p.F, (int)nx, (int)nu, (int)nc};
   // affine terms from the free response
   p.X0 = dev_alloc<double>(size_t(nx * (T + 1)), st);
   CMPC_CUDA(cudaMemcpyAsync(p.X0, in.x_bar, sizeof(double) * nx, cudaMemcpyHostToDevice, st));
@@ -592,9 +562,14 @@ void prob_build(Ctx& c, const cmpc_lq_problem& in, double** H_out, double** h_ou
   dev_free(h0d, st);
   *H_out = H;
   *h_out = h;
-  *J_out = J;
+  *J_out = nullptr;
   *d_out = d;
   *m_out = m;
+}
+
+const BuiltJ* prob_rows(Ctx& c) {
+  auto* p = static_cast<ProblemDev*>(c.prob);
+  return p ? &p->J : nullptr;
 }
 
 void prob_refresh(Ctx& c, const double* x_bar) {

@@ -160,7 +160,8 @@ int load_impl(Ctx& c, int64_t n, int64_t m, const double* H, const double* h, do
       last = now;
     };
     tick("h2d");
-    analyze_structure(c);
+    if (!c.J && prob_rows(c)) analyze_structure_built(c, *prob_rows(c));  // built: J never stored
+    else analyze_structure(c);
     tick("analyze");
     // the dense J is not read again: every product goes through P
     dev_free(c.J, c.stream);

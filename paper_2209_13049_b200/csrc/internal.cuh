@@ -156,6 +156,11 @@ struct Ctx {
 
 // ---- structure.cu
 void analyze_structure(Ctx& c);
+struct BuiltJ;  // jrows.cuh
+// the analysis over the device-built QP's J, generated row by row (never stored)
+void analyze_structure_built(Ctx& c, const BuiltJ& J);
+// the built problem's J (null: the QP was loaded, not built)
+const BuiltJ* prob_rows(Ctx& c);
 void free_structure(Ctx& c);
 
 // ---- syrk.cu

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "jrows.cuh"
 
 namespace cmpc {
 
@@ -32,16 +33,17 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 
 // per row: first/last nonzero, count, sign of the first nonzero, hash of the
 // sign-normalised row
-__global__ void k_row_summary(const double* __restrict__ J, int64_t m, int64_t n, int64_t ldj,
-                              unsigned long long* key, int32_t* lo, int32_t* hi, int32_t* nnz,
-                              int8_t* sg, int32_t* idx) {
+template <class JA>
+__global__ void k_row_summary(JA J, int64_t m, int64_t n, unsigned long long* key, int32_t* lo, int32_t* hi,
+                              int32_t* nnz, int8_t* sg, int32_t* idx) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= m) return;
+  const auto row = J.row(r);
   unsigned long long h = 0x84222325cbf29ce4ull;
   int first = -1, last = -1, cnt = 0;
   double sign = 0.0;
   for (int64_t j = 0; j < n; ++j) {
-    const double a = J[r + j * ldj];
+    const double a = row(j);
     if (a != 0.0) {
       if (first < 0) {
         first = (int)j;
@@ -77,16 +79,17 @@ __global__ void k_leader_of_row(const int32_t* srow, const int32_t* lead_pos, in
   run_of_row[r] = lead_pos[i];
 }
 
-__global__ void k_verify(const double* __restrict__ J, int64_t m, int64_t n, int64_t ldj,
-                         const int32_t* leader_row, const int32_t* run_of_row, const int8_t* sg,
-                         int32_t* collide) {
+template <class JA>
+__global__ void k_verify(JA J, int64_t m, int64_t n, const int32_t* leader_row, const int32_t* run_of_row,
+                         const int8_t* sg, int32_t* collide) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= m) return;
   const int32_t l = leader_row[r];
   if (l == r) return;
   const double s = (sg[r] == sg[l]) ? 1.0 : -1.0;
   bool eq = true;
-  for (int64_t j = 0; j < n && eq; ++j) eq = (J[r + j * ldj] == s * J[l + j * ldj]);
+  const auto rr = J.row(r), rl = J.row(l);
+  for (int64_t j = 0; j < n && eq; ++j) eq = (rr(j) == s * rl(j));
   if (!eq) collide[run_of_row[r]] = 1;
 }
 
@@ -154,27 +157,28 @@ __global__ void k_proto_leader(const int32_t* gorder, const int32_t* first_pos,
 }
 
 // P[k, j] = J[leader_k, j] for j < hi_k (P pre-zeroed); singletons separately
-__global__ void k_gather_P(const double* __restrict__ J, int64_t ldj, const int32_t* leader,
-                           const int32_t* hi_row, int64_t ps, int64_t n, int64_t ldp,
-                           double* P, int32_t* hi) {
+template <class JA>
+__global__ void k_gather_P(JA J, const int32_t* leader, const int32_t* hi_row, int64_t ps, int64_t n,
+                           int64_t ldp, double* P, int32_t* hi) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= ps) return;
   const int32_t l = leader[k];
   const int32_t w = hi_row[l];
   hi[k] = w;
   const int64_t j0 = blockIdx.y;
-  for (int64_t j = j0; j < w; j += gridDim.y) P[k + j * ldp] = J[l + j * ldj];
+  const auto row = J.row(l);
+  for (int64_t j = j0; j < w; j += gridDim.y) P[k + j * ldp] = row(j);
 }
 
-__global__ void k_singletons(const double* __restrict__ J, int64_t ldj, const int32_t* leader,
-                             const int32_t* lo_row, int64_t ps, int64_t pz, int32_t* sing_col,
-                             double* sing_val) {
+template <class JA>
+__global__ void k_singletons(JA J, const int32_t* leader, const int32_t* lo_row, int64_t ps, int64_t pz,
+                             int32_t* sing_col, double* sing_val) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= pz) return;
   const int32_t l = leader[ps + k];
   const int32_t c = lo_row[l];
   sing_col[k] = c < 0 ? 0 : c;
-  sing_val[k] = c < 0 ? 0.0 : J[l + (int64_t)c * ldj];
+  sing_val[k] = c < 0 ? 0.0 : J.row(l)(c);
 }
 
 __global__ void k_start_col(const int32_t* hi, int64_t ps, int64_t n, int32_t* start_col) {
@@ -201,7 +205,8 @@ void free_structure(Ctx& c) {
   c.sing_val = nullptr;
 }
 
-void analyze_structure(Ctx& c) {
+template <class JA>
+void analyze_impl(Ctx& c, const JA& J) {
   free_structure(c);
   const int64_t m = c.m, n = c.n;
   cudaStream_t st = c.stream;
@@ -237,7 +242,7 @@ void analyze_structure(Ctx& c) {
   auto* head = dev_alloc<int32_t>(m, st);
   auto* gid = dev_alloc<int32_t>(m, st);
 
-  k_row_summary<<<gm, T, 0, st>>>(c.J, m, n, m, key, lo, hi_row, nnz, sg, idx);
+  k_row_summary<<<gm, T, 0, st>>>(J, m, n, key, lo, hi_row, nnz, sg, idx);
   CMPC_LAUNCHED();
 
   size_t tmp_bytes = 0, need = 0;
@@ -259,7 +264,7 @@ void analyze_structure(Ctx& c) {
   k_leader_of_row<<<gm, T, 0, st>>>(srow, lead_pos, m, leader_row, run_of_row);
   CMPC_LAUNCHED();
   CMPC_CUDA(cudaMemsetAsync(collide, 0, sizeof(int32_t) * m, st));
-  k_verify<<<gm, T, 0, st>>>(c.J, m, n, m, leader_row, run_of_row, sg, collide);
+  k_verify<<<gm, T, 0, st>>>(J, m, n, leader_row, run_of_row, sg, collide);
   CMPC_LAUNCHED();
   k_heads<<<gm, T, 0, st>>>(lead_pos, collide, m, head);
   CMPC_LAUNCHED();
@@ -311,14 +316,14 @@ void analyze_structure(Ctx& c) {
   c.hi = dev_alloc<int32_t>(ps, st);
   if (ps > 0) {
     dim3 grid(unsigned((ps + T - 1) / T), unsigned(std::min<int64_t>(n, 64)));
-    k_gather_P<<<grid, T, 0, st>>>(c.J, m, leader, hi_row, ps, n, c.ldp, c.P, c.hi);
+    k_gather_P<<<grid, T, 0, st>>>(J, leader, hi_row, ps, n, c.ldp, c.P, c.hi);
     CMPC_LAUNCHED();
   }
   c.sing_col = dev_alloc<int32_t>(c.pz, st);
   c.sing_val = dev_alloc<double>(c.pz, st);
   if (c.pz > 0) {
-    k_singletons<<<unsigned((c.pz + T - 1) / T), T, 0, st>>>(c.J, m, leader, lo, ps, c.pz,
-                                                             c.sing_col, c.sing_val);
+    k_singletons<<<unsigned((c.pz + T - 1) / T), T, 0, st>>>(J, leader, lo, ps, c.pz, c.sing_col,
+                                                             c.sing_val);
     CMPC_LAUNCHED();
   }
   // all-zero rows sort first among the singletons (prefix width 0, value 0)
@@ -343,5 +348,8 @@ void analyze_structure(Ctx& c) {
                   (void*)proto_of_group, (void*)size_by_proto, (void*)leader})
     dev_free(p, st);
 }
+
+void analyze_structure(Ctx& c) { analyze_impl(c, DenseJ{c.J, c.m}); }
+void analyze_structure_built(Ctx& c, const BuiltJ& J) { analyze_impl(c, J); }
 
 }  // namespace cmpc
