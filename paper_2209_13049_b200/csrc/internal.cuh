@@ -165,7 +165,7 @@ void free_structure(Ctx& c);
 
 // ---- syrk.cu
 void syrk_plan(Ctx& c);
-// M(lower) = H + P' diag(omega) P + diag(dsing); writes full symmetric M when mirror
+// M(lower) = H + P' diag(omega) P + (singleton diagonal); writes full symmetric M when mirror
 void launch_condense(Ctx& c, bool mirror, bool with_rhs = false, cudaEvent_t after_syrk = nullptr);
 void syrk_free(Ctx& c);
 
@@ -206,7 +206,7 @@ void set_mu(Ctx& c, double mu);
 void launch_residuals(Ctx& c, bool reuse_trial = false);
 // r2 and complementarity only (after a barrier change) -> packet A kkt updated
 void launch_residuals_mu(Ctx& c);
-// sigma = z/s, omega, dsing, q = Pi'(r2 - sigma r3)
+// sigma = z/s, omega, q = Pi'(r2 - sigma r3) (one launch; the singleton diagonal is added by k_syrk_reduce)
 void launch_prepare_step(Ctx& c, const double* sigma_override);
 // rhs = -r1 + (P' q + singletons): the partial product (this context's rows) and the final
 // combination; launch_rhs does both (unsharded)
