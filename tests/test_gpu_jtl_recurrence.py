@@ -47,3 +47,27 @@ def test_carried_jtl_matches_the_direct_pass(shape):
     finally:
         dq_a.close()
         dq_b.close()
+
+
+def test_separate_rhs_pass_matches_the_fused_one():
+    """n > 1024 takes a separate P'q pass instead of the SYRK-fused right-hand side (DESIGN §5);
+    run both forms at a small size (one process each: the switch is read once) and compare."""
+    import json
+    import subprocess
+    import sys
+    code = (
+        "import json, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "from paper_2209_13049_b200 import ipm, problem as P;"
+        "qp = P.build_dense_qp(P.heat2d_problem(12, 10, T=14));"
+        "r = ipm.solve(qp);"
+        "print(json.dumps({'iter': r.iter, 'status': r.status.name, 'v': r.v.tolist(), 'obj': r.objective}))")
+    out = {}
+    for mode in ("fused", "separate"):
+        env = dict(os.environ, CMPC_RHS_PASS=mode)
+        res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert res.returncode == 0, res.stderr[-2000:]
+        out[mode] = json.loads(res.stdout.strip().splitlines()[-1])
+    a, b = out["fused"], out["separate"]
+    assert a["status"] == b["status"] == "converged" and a["iter"] == b["iter"]
+    assert rel(np.array(a["v"]), np.array(b["v"])) <= 1e-9
+    assert abs(a["obj"] - b["obj"]) <= 1e-10 * (1 + abs(b["obj"]))
