@@ -161,10 +161,18 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
         double bf[4];
 #pragma unroll
         for (int x = 0; x < 4; ++x) bf[x] = w[x] * lds64(sB + op_off(8 * fn[i] + g, ks + t + 4 * x));
+        // as four k4 steps with the two row halves interleaved: four independent DMMA chains
+        // between dependent steps instead of the two inside one m16n8k16 (same k order)
+        if (DIAG && !THIN && i == 0 && mixed) {
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-          if (DIAG && !THIN && i == 0 && mixed) dmma16816(acc[i][mi], ax[mi], bf);
-          else dmma16816(acc[i][mi], af[mi], bf);
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi) dmma1684(acc[i][mi], ax[mi] + 2 * q, bf[q]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi) dmma1684(acc[i][mi], af[mi] + 2 * q, bf[q]);
         }
       }
     }
