@@ -234,6 +234,8 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   CMPC_CUDA(cudaEventCreate(&e_start));
   CMPC_CUDA(cudaEventCreate(&e_end));
   CMPC_CUDA(cudaEventRecord(e_start, c.stream));
+  static const bool tverb = getenv("CMPC_SOLVE_TIMES") != nullptr;
+  const double t_es = now_seconds();
 
   // init (ipm.cpp:170-177)
   set_mu(c, mu_init);
@@ -388,14 +390,19 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     cudaEventDestroy(g_end);
     cudaEventDestroy(g_beg);
   }
+  const double t_loop = now_seconds();
   if (v_out && n > 0) CMPC_CUDA(cudaMemcpyAsync(v_out, c.v, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
   if (m > 0) {
     if (s_out) CMPC_CUDA(cudaMemcpyAsync(s_out, c.s, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
     if (lam_out) CMPC_CUDA(cudaMemcpyAsync(lam_out, c.lam, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
     if (z_out) CMPC_CUDA(cudaMemcpyAsync(z_out, c.z, sizeof(double) * m, cudaMemcpyDeviceToHost, c.stream));
   }
+  const double t_copy = now_seconds();
   CMPC_CUDA(cudaEventRecord(e_end, c.stream));
   CMPC_CUDA(cudaStreamSynchronize(c.stream));
+  if (tverb)
+    fprintf(stderr, "[cmpc solve] to e_start %.3f ms, loop %.3f, copies %.3f, sync %.3f\n",
+            (t_es - start) * 1e3, (t_loop - t_es) * 1e3, (t_copy - t_loop) * 1e3, (now_seconds() - t_copy) * 1e3);
   float dms = 0.f;
   CMPC_CUDA(cudaEventElapsedTime(&dms, e_start, e_end));
   device_s = dms * 1e-3;

@@ -395,9 +395,20 @@ def recover_trajectory(qp: DenseQp, v) -> Trajectory:
             qp.gk[k] = A_K @ qp.gk[k - 1]
         qp.x0 = free_response(A_K, data.x_bar, data.w)
     x = qp.x0.copy()
-    # x_t += sum_{j<t} G_{t-1-j} v_j, one GEMM per lag k = t-1-j
-    for k in range(dm.T):
-        x[k + 1:] += vt[:dm.T - k] @ qp.gk[k].T
+    # x_t = x0_t + sum_{k<t} G_k v_{t-1-k}: one GEMM of the block-Toeplitz arrangement of v
+    # (row t-1 holds v_{t-1}, .., v_0) with [G_0' ; .. ; G_{T-1}'] (a GEMM per lag costs ~3x
+    # more at config 3)
+    T, nu = dm.T, dm.n_u
+    gc = data.__dict__.setdefault("_gcat_cache", {})  # shared by every DenseQp of this data
+    if gc.get("key") is not qp.gk:
+        gc.clear()
+        gc["key"] = qp.gk
+        gc["gcat"] = np.ascontiguousarray(qp.gk.transpose(0, 2, 1).reshape(T * nu, dm.n_x))
+    gcat = gc["gcat"]
+    W = np.zeros((T, T * nu))
+    for r in range(T):
+        W[r, :(r + 1) * nu] = vt[r::-1].reshape(-1)
+    x[1:] += W @ gcat
     u = x[:-1] @ data.K.T + vt
     # the diagonal-weight check scans n_x^2 entries: cache it on the problem data, which
     # every DenseQp built from it (e.g. a fresh upload per solve) shares
