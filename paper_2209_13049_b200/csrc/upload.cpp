@@ -30,6 +30,7 @@ struct Stager {
   char* slot[kSlots] = {};
   cudaEvent_t done[kSlots] = {};
   bool ready = false;
+  int device = -1;  // the events belong to this device (recreated when the caller's differs)
 };
 
 Stager& stager() {
@@ -57,11 +58,20 @@ void upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   Stager& S = stager();
   std::lock_guard<std::mutex> lk(S.mu);
   if (!S.ready) {
-    for (int k = 0; k < kSlots; ++k) {
+    for (int k = 0; k < kSlots; ++k)
       CMPC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&S.slot[k]), kSlotBytes, cudaHostAllocPortable));
-      CMPC_CUDA(cudaEventCreateWithFlags(&S.done[k], cudaEventDisableTiming));
-    }
     S.ready = true;
+  }
+  int dev = 0;
+  CMPC_CUDA(cudaGetDevice(&dev));
+  if (dev != S.device) {
+    for (int k = 0; k < kSlots; ++k)
+      if (S.done[k]) {
+        CMPC_CUDA(cudaEventSynchronize(S.done[k]));
+        cudaEventDestroy(S.done[k]);
+      }
+    for (int k = 0; k < kSlots; ++k) CMPC_CUDA(cudaEventCreateWithFlags(&S.done[k], cudaEventDisableTiming));
+    S.device = dev;
   }
   const size_t nchunks = (bytes + kSlotBytes - 1) / kSlotBytes;
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());

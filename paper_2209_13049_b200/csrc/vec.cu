@@ -134,16 +134,17 @@ __global__ void __launch_bounds__(256) k_proto_gemv(const double* __restrict__ P
 // right-hand side part. (M - H) pv has the rounding of the direct P'(omega o P pv) in the
 // worst case (both are bounded by eps |P|' Omega |P| |pv|). One warp per output i: lanes
 // stride j, the lower-triangle element of (i, j) is read from M and H alike.
-__global__ void __launch_bounds__(1024) k_jtpl_symv(const double* __restrict__ M, const double* __restrict__ H,
-                                                    int64_t n, const double* __restrict__ pv,
-                                                    const double* __restrict__ tq, double* __restrict__ out) {
+__device__ __forceinline__ void jtpl_symv_body(int64_t blk, const double* __restrict__ M,
+                                               const double* __restrict__ H, int64_t n,
+                                               const double* __restrict__ pv, const double* __restrict__ tq,
+                                               double* __restrict__ out) {
   // a CTA owns 32 outputs i0 .. i0 + 31. Part A (j <= i: row i of the lower triangle): lane =
   // output, the 32 warps stride j, so each load is 32 consecutive rows of one column. Part B
   // (j > i: column i below the diagonal): warp w takes output i0 + w, lanes stride j along
   // the column. Loads four at a time; the pieces are added in a fixed order.
   __shared__ double ra[32][33], rb[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t i0 = blockIdx.x * 32ll, ia = i0 + lane, ib = i0 + w;
+  const int64_t i0 = blk * 32, ia = i0 + lane, ib = i0 + w;
   double sa = 0.0, sb = 0.0;
   if (ia < n) {
     int64_t j = w;
@@ -186,6 +187,12 @@ __global__ void __launch_bounds__(1024) k_jtpl_symv(const double* __restrict__ M
 #pragma unroll 8
   for (int q = 0; q < 32; ++q) s += ra[q][lane];
   out[ia] = sub(s + rb[lane], tq[ia]);
+}
+
+__global__ void __launch_bounds__(1024) k_jtpl_symv(const double* __restrict__ M, const double* __restrict__ H,
+                                                    int64_t n, const double* __restrict__ pv,
+                                                    const double* __restrict__ tq, double* __restrict__ out) {
+  jtpl_symv_body(blockIdx.x, M, H, n, pv, tq, out);
 }
 
 __global__ void k_sing_x(const int32_t* __restrict__ col, const double* __restrict__ val, int64_t pz,
@@ -787,12 +794,11 @@ __global__ void k_sym_check(const double* __restrict__ H, int64_t n, unsigned* b
 // loads when n is even, fixed-order warp sum
 // x = v + alpha p when v is given (the line-search trial point, k_axpy_n's rounding; warp j
 // also stores x_j), else x as passed
-__global__ void __launch_bounds__(256) k_hcol_gemv(const double* __restrict__ H, int64_t n,
-                                                   const double* __restrict__ x, double* __restrict__ y,
-                                                   const double* __restrict__ v, const double* __restrict__ p,
-                                                   double alpha_h, const Packet* apk, double* __restrict__ xt) {
+__device__ __forceinline__ void hcol_body(int64_t j, const double* __restrict__ H, int64_t n,
+                                          const double* __restrict__ x, double* __restrict__ y,
+                                          const double* __restrict__ v, const double* __restrict__ p,
+                                          double alpha_h, const Packet* apk, double* __restrict__ xt) {
   const int lane = threadIdx.x & 31;
-  const int64_t j = blockIdx.x * 8ll + (threadIdx.x >> 5);
   if (j >= n) return;
   const double al = v ? trial_alpha(alpha_h, apk) : 0.0;
   const double* col = H + j * n;
@@ -823,6 +829,28 @@ __global__ void __launch_bounds__(256) k_hcol_gemv(const double* __restrict__ H,
     y[j] = s;
     if (v) xt[j] = add(v[j], mul(al, p[j]));
   }
+}
+
+__global__ void __launch_bounds__(256) k_hcol_gemv(const double* __restrict__ H, int64_t n,
+                                                   const double* __restrict__ x, double* __restrict__ y,
+                                                   const double* __restrict__ v, const double* __restrict__ p,
+                                                   double alpha_h, const Packet* apk, double* __restrict__ xt) {
+  hcol_body(blockIdx.x * 8ll + (threadIdx.x >> 5), H, n, x, y, v, p, alpha_h, apk, xt);
+}
+
+// the trial's H v_t (CTAs below hblocks, a warp per column) and, beside it, J' p_lambda
+// (k_jtpl_symv's CTAs; JtPl null: none) in one launch
+__global__ void __launch_bounds__(1024) k_trial_hv(const double* __restrict__ H, int64_t n,
+                                                   double* __restrict__ Hvt, const double* __restrict__ v,
+                                                   const double* __restrict__ pv, double alpha_h,
+                                                   const Packet* apk, double* __restrict__ vt, int hblocks,
+                                                   const double* __restrict__ M, const double* __restrict__ tq,
+                                                   double* __restrict__ JtPl) {
+  if ((int)blockIdx.x < hblocks) {
+    hcol_body(blockIdx.x * 32ll + (threadIdx.x >> 5), H, n, nullptr, Hvt, v, pv, alpha_h, apk, vt);
+    return;
+  }
+  jtpl_symv_body((int64_t)blockIdx.x - hblocks, M, H, n, pv, tq, JtPl);
 }
 
 }  // namespace
@@ -1201,12 +1229,6 @@ void launch_recover(Ctx& c, double tau) {
     CMPC_LAUNCHED();
   }
   const unsigned pb = part_blocks(c.m);
-  // J' p_lambda for the step (in line: a side-stream branch was no faster alone and cost 45%
-  // in batch mode, where 15 contexts share the GPU)
-  if (c.m > 0 && c.jtl_recur && !c.comm && c.n > 0) {
-    k_jtpl_symv<<<(unsigned)ceil_div(c.n, 32), 1024, 0, c.stream>>>(c.M, c.H, c.n, c.pv, c.tq, c.JtPl);
-    CMPC_LAUNCHED();
-  }
   if (c.m > 0) launch_Jx(c, c.pv, c.y, nullptr);
   if (c.m > 0) {
     k_recover_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.y, c.s, c.z, c.sigma, c.r2, c.r3,
@@ -1230,14 +1252,22 @@ void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear) {
     k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 2);
     CMPC_LAUNCHED();
   }
+  // J' p_lambda of the direction (for the step's J'lambda, k_update), formed here beside H v_t
+  // (a side-stream branch was no faster alone and cost 45% in batch mode)
+  const bool jtpl = c.m > 0 && c.jtl_recur && !c.comm && c.n > 0;
   if (c.n > 0 && c.h_symmetric) {  // v_t = v + alpha pv formed inside H v_t's column dots
-    k_hcol_gemv<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(c.H, c.n, nullptr, c.Hvt, c.v, c.pv,
-                                                                     alpha, apk, c.vt);
+    const int hblocks = (int)ceil_div(c.n, 32), sblocks = jtpl ? (int)ceil_div(c.n, 32) : 0;
+    k_trial_hv<<<(unsigned)(hblocks + sblocks), 1024, 0, c.stream>>>(c.H, c.n, c.Hvt, c.v, c.pv, alpha, apk, c.vt,
+                                                                     hblocks, c.M, c.tq, c.JtPl);
     CMPC_LAUNCHED();
   } else if (c.n > 0) {
     k_axpy_n<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(c.n, c.v, alpha, apk, c.pv, c.vt);
     CMPC_LAUNCHED();
     launch_Hx(c, c.vt, c.Hvt);
+    if (jtpl) {
+      k_jtpl_symv<<<(unsigned)ceil_div(c.n, 32), 1024, 0, c.stream>>>(c.M, c.H, c.n, c.pv, c.tq, c.JtPl);
+      CMPC_LAUNCHED();
+    }
   }
   const unsigned pb = part_blocks(c.m);
   if (c.m > 0) {
