@@ -129,3 +129,43 @@ def test_loading_a_bare_qp_drops_the_problem():
     with pytest.raises(ipm.DimensionError):
         dq.refresh_initial_state(data.x_bar)
     dq.close()
+
+
+def test_column_major_and_row_major_inputs_build_the_same_qp(O):
+    """cmpc_lq_problem.layout: 0 = Eigen column-major (the reference's storage, the C++ binding
+    of INTEGRATION.md), 1 = row-major (numpy C order, transposed on the device)."""
+    import ctypes as C
+    from paper_2209_13049_b200 import _lib
+    arrs = random_arrays(31, 6, 3, 2, 7)
+    data = lq_from_oracle(O.problem_from_arrays(**arrs))
+    dm = P.dims(data)
+    L = _lib.lib()
+    got = []
+    for layout in (0, 1):
+        keep = []
+
+        def arr(a, order):
+            a = np.asarray(a, dtype=np.float64)
+            a = np.asfortranarray(a) if order == "F" else np.ascontiguousarray(a)
+            keep.append(a)
+            return a.ctypes.data_as(_lib.D) if a.size else None
+
+        pr = _lib.LqProblem(nx=dm.n_x, nu=dm.n_u, nc=dm.n_c, T=dm.T, layout=layout)
+        for f in ("A", "B", "Q", "Qf", "R", "S", "E", "F", "K"):
+            setattr(pr, f, arr(getattr(data, f), "F" if layout == 0 else "C"))
+        for f in ("gl", "gu", "xl", "xu", "ul", "uu", "x_bar", "w"):
+            setattr(pr, f, arr(getattr(data, f), "C"))
+        h = C.c_void_p()
+        _lib.check(L.cmpc_ctx_create(C.byref(h), 0))
+        try:
+            _lib.check(L.cmpc_build_qp(h, C.byref(pr)))
+            info = (C.c_int64 * 8)()
+            L.cmpc_qp_info(h, info)
+            n, m = int(info[0]), int(info[1])
+            H, hv, d, h0 = np.zeros((n, n), order="F"), np.zeros(n), np.zeros(m), np.zeros(1)
+            _lib.check(L.cmpc_get_qp(h, _lib.ptr(H), _lib.ptr(hv), _lib.ptr(h0), _lib.ptr(d)))
+            got.append((H, hv, d, h0[0]))
+        finally:
+            L.cmpc_ctx_destroy(h)
+    (H0, h0v, d0, c0), (H1, h1v, d1, c1) = got
+    assert np.array_equal(H0, H1) and np.array_equal(h0v, h1v) and np.array_equal(d0, d1) and c0 == c1
