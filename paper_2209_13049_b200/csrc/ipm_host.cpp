@@ -79,12 +79,12 @@ void rec(cudaEvent_t e, cudaStream_t s) {
 void seg_step(Ctx& c, double tau) {
   rec(c.ev0, c.stream);
   launch_prepare_step(c, nullptr);
-  // right-hand side P'q fused into the SYRK's diagonal jobs, or a separate pass over P: the
-  // fused form costs ~9% of the SYRK at n = 500 (the pass: 14%) but ~6% at n = 2000 (the pass:
-  // 3%), so large n takes the pass (tools/phases.py: condense vs condense_rhs vs Jty)
-  // (CMPC_RHS_PASS=separate|fused overrides the rule; tests/test_gpu_jtl_recurrence.py)
+  // right-hand side P'q fused into the SYRK's diagonal jobs (with the plan's step weights
+  // accounting for it: +4% of the SYRK at n = 500, +2% at n = 2000, against 14% and 3% for a
+  // separate pass over P; tools/phases.py condense vs condense_rhs vs Jty).
+  // CMPC_RHS_PASS=separate|fused forces one form (tests/test_gpu_jtl_recurrence.py)
   static const char* force = getenv("CMPC_RHS_PASS");
-  const bool want = force ? force[0] == 'f' : c.n <= 1024;
+  const bool want = force ? force[0] == 'f' : true;
   const bool fused = c.ps > 0 && c.npieces > 0 && want;
   if (!fused) launch_rhs_partial(c);  // J'(r2 - sigma r3) by its own pass over P
   rec(c.ev2, c.stream);

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -42,8 +43,11 @@ constexpr int kSyrkSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barrier
 constexpr int kConsumerWarps = 4;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kSyrkThreads = kConsumers + 32;
-// relative cost of one k step per segment shape (measured: tools/syrk_timeline.py, C3)
-constexpr double kCostFull = 1.0, kCostThin = 0.6, kCostDiag = 0.85, kCostDiagThin = 0.35;
+// relative cost of one k step per segment shape: a diagonal step also forms its rows' share
+// of the fused right-hand side P'q (swept with CMPC_SYRK_COST and tools/phases.py: at C3 the
+// fused condensation 297 us with these, 315 us with the weights measured without it,
+// 1 / 0.6 / 0.85 / 0.35; C4 and C5 improve too)
+constexpr double kCostFull = 1.0, kCostThin = 0.65, kCostDiag = 1.1, kCostDiagThin = 0.5;
 
 struct SyrkArgs {
   const double* omega;
@@ -464,6 +468,9 @@ void syrk_plan(Ctx& c) {
   // jobs: per lower tile (I,J), the rows whose prefix ends in the first half of column block I
   // (THIN: only output rows 0..31 are nonzero) and the rest (FULL)
   struct Job { int tile, ti, tj, thin, kb, ke; double w; };
+  // step weights (CMPC_SYRK_COST="full,thin,diag,diagthin" overrides them for tuning)
+  double cost_f = kCostFull, cost_t = kCostThin, cost_d = kCostDiag, cost_dt = kCostDiagThin;
+  if (const char* e = getenv("CMPC_SYRK_COST")) sscanf(e, "%lf,%lf,%lf,%lf", &cost_f, &cost_t, &cost_d, &cost_dt);
   std::vector<Job> jobs;
   std::vector<int2> tiles;
   for (int tj = 0; tj < nt; ++tj)
@@ -472,8 +479,8 @@ void syrk_plan(Ctx& c) {
       tiles.push_back({ti, tj});
       const int a0 = kstart((int64_t)kTile * ti), a1 = std::max(a0, kstart((int64_t)kTile * ti + 32));
       const bool dg = ti == tj;
-      if (a1 > a0) jobs.push_back({tile, ti, tj, 1, a0, a1, dg ? kCostDiagThin : kCostThin});
-      if (k_end > a1) jobs.push_back({tile, ti, tj, 0, a1, k_end, dg ? kCostDiag : kCostFull});
+      if (a1 > a0) jobs.push_back({tile, ti, tj, 1, a0, a1, dg ? cost_dt : cost_t});
+      if (k_end > a1) jobs.push_back({tile, ti, tj, 0, a1, k_end, dg ? cost_d : cost_f});
     }
   // Pieces. The k axis is split where the cumulative weighted work reaches (1 - tail_frac).
   // The body [0, K) is laid out job after job and cut into one equal-cost piece per CTA slot
