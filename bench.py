@@ -11,10 +11,12 @@ value: device time of K solves with the QP resident in HBM (CUDA events on the s
 stream, max over ranks). e2e: the same metric through the public API
 (paper_2209_13049_b200.ipm.solve on a fresh DenseQp whose arrays sit in pinned host
 memory): H2D upload + structure analysis + solve + D2H of the iterate + trajectory recovery,
-wall clock. N > 1 (torchrun): every rank solves its own instance (initial temperature
-varied per rank, config-5 style batch), no collective in the loop -> weak scaling.
---impl reference: the oracle (CPU restatement of the reference solver) on the box's host
-cores, bounded sample (one IPM iteration, extrapolated by the solve's iteration count).
+wall clock. N > 1 (torchrun): configs 3/4 shard the rows of J across the ranks (one solve per
+step, NCCL allreduces inside the iteration graphs -> strong scaling; --mode replica instead
+solves an independent instance per rank -> weak scaling); config 5 splits the 1024-instance
+batch across the ranks (no collective in the loop).
+--impl reference: the oracle (CPU restatement of the reference solver) on all the box's host
+cores, one whole solve per timed step (rank 0 only).
 """
 from __future__ import annotations
 
@@ -41,9 +43,6 @@ CONFIGS = {
     "c5": dict(desc="config 5: batch of 1024 independent 2-D heat MPC instances 20x25, n_x=500, n_u=5, "
                     "T=30 (n=150, m=30,300), initial temperature 300 K + U[-20,20] per cell, split across GPUs"),
 }
-# iteration count of the reference restatement (oracle) on the full configuration, used to
-# extrapolate its bounded one-iteration sample; cross-checked against the device solve
-ORACLE_ITERS = {"c3": 34, "c4": 36, "c2": 29, "c5": 31}
 
 
 def build_problem(cfg, rank=0):
@@ -134,6 +133,35 @@ def pinned_like(a):
     return out
 
 
+def host_cpu():
+    """CPU model and logical core count of the host the CPU arms run on."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count() or 1}
+
+
+def bench_config(cfg, qp, world, mode):
+    """The `config` dict both arms print (same workload -> same dict)."""
+    if world == 1:
+        par = "single instance"
+    elif mode == "shard":
+        par = (f"rows of J sharded across {world} GPU(s) by whole stages; partial J_g' Sigma_g J_g "
+               f"+ row reductions allreduced (NCCL)")
+    else:
+        par = f"{world} independent instances (one per GPU)"
+    return {"workload": CONFIGS[cfg]["desc"], "n": qp.n, "m": qp.m, "tol": 1e-8,
+            "parallelism": par,
+            "l2": "inputs larger than L2 (J %.2f GB dense)" % (8.0 * qp.m * qp.n / 1e9)
+                  if 8.0 * qp.m * qp.n > 126e6 else "L2 flushed between steps (256 MB write)"}
+
+
 def cpu_sample(qp, threads, iters_full):
     """Oracle (reference restatement) on the host: one IPM iteration, bounded sample."""
     from oracle import oracle as O
@@ -146,30 +174,61 @@ def cpu_sample(qp, threads, iters_full):
 
 
 def run_reference(args, rank, world):
-    cfg = args.config
-    line = {"impl": "reference", "metric": "ms per MPC solve", "unit": "ms", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
-            "scaling": "weak", "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIGS[cfg]["desc"], "tol": 1e-8}}
+    """The reference CPU path: the oracle (C++ restatement of proj/src/ipm.cpp +
+    dense_linalg.cpp; the reference itself needs Eigen3, absent here and on the box) on
+    all host cores. Each timed step is one WHOLE solve of the config's QP (dense J, as the
+    reference multiplies it); warm-up steps are one IPM iteration each (untimed, they only
+    warm the thread pool and the page cache). Rank 0 alone runs it."""
     if rank != 0:
         return None
+    from oracle import oracle as O
     from paper_2209_13049_b200 import problem as P
+    cfg = args.config
+    mode = args.mode if args.mode != "auto" else ("shard" if cfg in ("c3", "c4") and world > 1 else "replica")
     qp = P.build_dense_qp(build_problem(cfg))
     threads = os.cpu_count() or 1
-    iters = ORACLE_ITERS.get(cfg, 30)
-    samples = []
-    for k in range(args.warmup + args.steps):
-        s = cpu_sample(qp, threads, iters)
-        if k >= args.warmup:
-            samples.append(s)
-    ms = statistics.median(s["ms_per_solve"] for s in samples)
-    line.update(value=ms, ms_per_step=ms,
-                cpu_baseline={"value": ms, "unit": "ms", "cores": threads, "kind": "port",
-                              "sample": f"one IPM iteration of the oracle (CPU restatement of "
-                                        f"proj/src/ipm.cpp + dense_linalg.cpp) on the full {cfg} "
-                                        f"QP, x{iters} iterations (its full-solve count)"},
-                e2e={"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                ms_per_iter=statistics.median(s["ms_per_iter"] for s in samples))
+    O.set_threads(threads)
+    O.set_skip_zeros(False)
+    oq = O.qp_from_arrays(qp.H, qp.h, qp.h0, qp.J, qp.d)
+    for _ in range(args.warmup):
+        O.solve(oq, max_iter=1, log=False)
+    times, iters, status = [], [], None
+    wall = time.perf_counter()
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        r = O.solve(oq, log=False)
+        times.append((time.perf_counter() - t) * 1e3)
+        iters.append(r.iter)
+        status = r.status
+    wall = time.perf_counter() - wall
+    ms = float(np.mean(times))
+    # the reference's own build is single-threaded Eigen (-O3, no -march: proj/CMakeLists.txt:8-9):
+    # one iteration of the same QP on one thread, scaled by the solve's iteration count
+    O.set_threads(1)
+    t = time.perf_counter()
+    O.solve(oq, max_iter=1, log=False)
+    st_iter = (time.perf_counter() - t) * 1e3
+    O.set_threads(threads)
+    cpu = host_cpu()
+    line = {"impl": "reference", "metric": "ms per MPC solve", "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
+            "scaling": "strong" if (world > 1 and mode == "shard") else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": bench_config(cfg, qp, world, mode),
+            "value": ms, "ms_per_step": ms, "ms_per_iter": ms / max(float(np.mean(iters)), 1.0),
+            "iterations": iters[-1], "status": status, "samples_ms": [round(x, 1) for x in times],
+            "wall_s": wall,
+            "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "port",
+                             "cpu": cpu,
+                             "sample": f"{args.steps} whole solves ({iters[-1]} IPM iterations each) of "
+                                       f"the full {cfg} QP by the oracle (CPU restatement of "
+                                       f"proj/src/ipm.cpp + dense_linalg.cpp, dense J, OpenMP over "
+                                       f"independent output entries) on {threads} threads; warm-up "
+                                       f"steps are one iteration each"},
+            "single_thread": {"ms_per_iter": st_iter, "ms_per_solve_extrapolated": st_iter * iters[-1],
+                              "sample": "one IPM iteration on 1 thread (the reference's own "
+                                        "single-threaded build), x the solve's iteration count"},
+            "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     return line
 
 
@@ -259,11 +318,8 @@ def run_shard(args, rank, world, local, dist):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": CONFIGS[cfg]["desc"], "n": qp.n, "m": qp.m, "tol": 1e-8,
-                   "parallelism": f"rows of J sharded across {world} GPU(s) by whole stages; "
-                                  f"partial J_g' Sigma_g J_g + row reductions allreduced (NCCL)",
-                   "rows_rank0": int(len(rows)), "prototype_rows_rank0": info["prototypes"],
-                   "l2": "inputs larger than L2 (J 1.0 GB dense)"},
+        "config": bench_config(cfg, qp, world, "shard"),
+        "structure": {"rows_rank0": int(len(rows)), "prototype_rows_rank0": info["prototypes"]},
         "ms_per_iter": ms_total / max(sum(iters), 1), "iterations": iters[-1], "status": r.status.name,
         "roofline": {"bound": "tensor", "kernel": "k_syrk + k_syrk_reduce (rank 0's rows)",
                      "achieved": flops_rank0 / (syrk_s / max(syrk_n, 1)) / 1e12,
@@ -386,7 +442,7 @@ def main():
     data = build_problem(cfg, rank)
     qp = P.build_dense_qp(data)
     dq = ipm.DeviceQp(qp, device=local)
-    qp._device = dq
+    qp._device, qp._device_key = dq, qp.device_key()
     info = dq.info()
     opts = ipm.IpmOptions()
 
@@ -401,8 +457,16 @@ def main():
     l0 = _lib.launch_count()
     dev_s, syrk_s, syrk_n, chol_s, iters, wall = 0.0, 0.0, 0, 0.0, [], time.perf_counter()
     syrk_k = 0.0
+    # inputs smaller than L2 (configs 1, 2): a 256 MB write between the timed solves (the
+    # solve's own CUDA events exclude it)
+    flush = None
+    if 8.0 * qp.m * qp.n <= 126e6:
+        flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=f"cuda:{local}")
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+        for k in range(args.steps):
+            if flush is not None:
+                flush.fill_(float(k))
+                torch.cuda.synchronize(local)  # the solve runs on its own non-blocking stream
             r = ipm.solve_loaded(dq, qp, opts)
             dev_s += r.device_seconds
             syrk_s += r.syrk_seconds
@@ -492,10 +556,9 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": CONFIGS[cfg]["desc"], "n": qp.n, "m": qp.m, "tol": 1e-8,
-                   "parallelism": f"{world} independent instances (one per GPU)" if world > 1 else "single instance",
-                   "l2": "inputs larger than L2 (J 1.0 GB dense, P %.0f MB)" % (info["p_bytes"] / 1e6),
-                   "prototype_rows": info["prototypes"], "syrk_rows": info["syrk_prototypes"]},
+        "config": bench_config(cfg, qp, world, mode),
+        "structure": {"prototype_rows": info["prototypes"], "syrk_rows": info["syrk_prototypes"],
+                      "p_mb": info["p_bytes"] / 1e6},
         "ms_per_iter": ms_total / max(sum(iters), 1) * (1 if world == 1 else 1),
         "iterations": iters[-1], "status": status,
         "roofline": {"bound": "tensor", "kernel": "k_syrk (the condensation's SYRK, right-hand side fused)",
@@ -521,6 +584,7 @@ def main():
         s = cpu_sample(qp, os.cpu_count() or 1, r.iter)
         line["cpu_baseline"] = {
             "value": s["ms_per_solve"], "unit": "ms", "cores": os.cpu_count() or 1, "kind": "port",
+            "cpu": host_cpu(),
             "sample": f"one IPM iteration of the oracle (CPU restatement of proj/src/ipm.cpp + "
                       f"dense_linalg.cpp, dense J) on the same QP, x{r.iter} iterations"}
     traffic = os.path.join(ROOT, "profiles", f"syrk_traffic_{cfg}.json")

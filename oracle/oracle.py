@@ -91,6 +91,7 @@ def lib():
                                 INSPECT_FN, vp]
         L.orc_solve_enumeration.argtypes = [vp, _D, _D, _I64, _I64, _D]
         L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_set_skip_zeros.argtypes = [C.c_int]
         L.orc_get_threads.restype = C.c_int
         _LIB = L
     return _LIB
@@ -142,6 +143,13 @@ def set_threads(n: int):
 
 def get_threads() -> int:
     return lib().orc_get_threads()
+
+
+def set_skip_zeros(on: bool):
+    """Test-speed mode: solve() leaves J's all-zero 512-row column chunks out of every J
+    product. Bitwise the same results (only exact-zero products are skipped, sums keep their
+    order); the timed CPU baseline never sets it."""
+    lib().orc_set_skip_zeros(1 if on else 0)
 
 
 class Rng:

@@ -57,6 +57,7 @@ extern "C" {
 const char* orc_last_error(void) { return g_err.c_str(); }
 void orc_set_threads(int n) { set_threads(n); }
 int orc_get_threads(void) { return get_threads(); }
+void orc_set_skip_zeros(int on) { set_skip_zeros(on != 0); }
 
 orc_rng* orc_rng_new(std::uint64_t seed) { return new orc_rng{std::mt19937_64(seed)}; }
 orc_rng* orc_rng_instance(std::uint64_t seed, std::uint64_t index) {

@@ -18,12 +18,51 @@ namespace orc {
 
 namespace {
 int g_threads = 1;
+bool g_skip_zeros = false;
+// Structural-zero map of the J being solved (set_skip_zeros mode, test speed only): one bit
+// per (column, 512-row chunk) saying whether the chunk holds a nonzero of that column. A
+// skipped chunk contributes only products with an exact zero factor (+-0), so every sum keeps
+// its value and its order: results are bitwise those of the dense loops (finite data).
+struct ZeroMap {
+  const double* data = nullptr;
+  Index m = 0, n = 0, nchunk = 0;
+  std::vector<unsigned char> nz;  // [j * nchunk + c]
+  bool has(Index j, Index c) const { return nz[size_t(j * nchunk + c)] != 0; }
+};
+constexpr Index kZChunk = 512;
+const ZeroMap* g_zmap = nullptr;
+const ZeroMap* zmap_for(const Mat& A) {
+  return (g_zmap && A.r == g_zmap->m && A.c == g_zmap->n && A.a.data() == g_zmap->data) ? g_zmap : nullptr;
+}
+ZeroMap make_zmap(const Mat& J) {
+  ZeroMap z;
+  z.data = J.a.data();
+  z.m = J.r;
+  z.n = J.c;
+  z.nchunk = (J.r + kZChunk - 1) / kZChunk;
+  z.nz.assign(size_t(z.n * z.nchunk), 0);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+  for (Index j = 0; j < J.c; ++j) {
+    const double* c = J.col(j);
+    for (Index k = 0; k < z.nchunk; ++k) {
+      const Index i1 = std::min(J.r, (k + 1) * kZChunk);
+      for (Index i = k * kZChunk; i < i1; ++i)
+        if (c[i] != 0.0) {
+          z.nz[size_t(j * z.nchunk + k)] = 1;
+          break;
+        }
+    }
+  }
+  return z;
+}
 double now_seconds() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 }  // namespace
 
 void set_threads(int n) { g_threads = std::max(1, n); }
+void set_skip_zeros(bool on) { g_skip_zeros = on; }
+bool get_skip_zeros() { return g_skip_zeros; }
 int get_threads() { return g_threads; }
 
 // ------------------------------------------------------------------ helpers
@@ -43,12 +82,21 @@ Vec gemv(const Mat& A, const Vec& x) {
   Vec y(size_t(m), 0.0);
   const Index chunk = 4096;
   const Index nchunks = (m + chunk - 1) / chunk;
+  const ZeroMap* z = zmap_for(A);
 #pragma omp parallel for schedule(static) num_threads(g_threads) if (m * n > 200000)
   for (Index b = 0; b < nchunks; ++b) {
     const Index i0 = b * chunk, i1 = std::min(m, i0 + chunk);
     for (Index j = 0; j < n; ++j) {
       const double xj = x[size_t(j)];
       const double* c = A.col(j);
+      if (z) {  // the same per-element order over j, zero chunks left out
+        for (Index k0 = i0; k0 < i1; k0 += kZChunk) {
+          if (!z->has(j, k0 / kZChunk)) continue;
+          const Index k1 = std::min(i1, k0 + kZChunk);
+          for (Index i = k0; i < k1; ++i) y[size_t(i)] += c[i] * xj;
+        }
+        continue;
+      }
       for (Index i = i0; i < i1; ++i) y[size_t(i)] += c[i] * xj;
     }
   }
@@ -58,11 +106,20 @@ Vec gemv(const Mat& A, const Vec& x) {
 Vec gemv_t(const Mat& A, const Vec& x) {
   const Index m = A.r, n = A.c;
   Vec y(size_t(n), 0.0);
+  const ZeroMap* z = zmap_for(A);
 #pragma omp parallel for schedule(static) num_threads(g_threads) if (m * n > 200000)
   for (Index j = 0; j < n; ++j) {
     const double* c = A.col(j);
     double s = 0.0;
-    for (Index i = 0; i < m; ++i) s += c[i] * x[size_t(i)];
+    if (z) {
+      for (Index k = 0; k < z->nchunk; ++k) {
+        if (!z->has(j, k)) continue;
+        const Index i1 = std::min(m, (k + 1) * kZChunk);
+        for (Index i = k * kZChunk; i < i1; ++i) s += c[i] * x[size_t(i)];
+      }
+    } else {
+      for (Index i = 0; i < m; ++i) s += c[i] * x[size_t(i)];
+    }
     y[size_t(j)] = s;
   }
   return y;
@@ -230,52 +287,76 @@ Mat gram_weighted(const Mat& J, const Vec& sigma) {  // dense_linalg.cpp:128-137
   if (m == 0) return g;
   Vec rs(static_cast<size_t>(m));
   for (Index i = 0; i < m; ++i) rs[size_t(i)] = std::sqrt(sigma[size_t(i)]);
-  // W = diag(sqrt(sigma)) J, formed chunk by chunk; lower triangle of W'W with
-  // each entry summed over rows in ascending order
-  const Index RB = 512;
-  const Index nb = (n + 3) / 4;
-  std::vector<std::pair<Index, Index>> blocks;
-  for (Index bj = 0; bj < nb; ++bj)
-    for (Index bi = bj; bi < nb; ++bi) blocks.push_back({bi, bj});
-  std::vector<double> W(static_cast<size_t>(RB * n));
+  // W = diag(sqrt(sigma)) J, formed chunk by chunk (512 rows) in panels of 8 columns
+  // (panel-major, then row, then column: a row of a panel is 8 contiguous doubles); lower
+  // triangle of W'W by 4x8 entry blocks, each entry summed over the rows in ascending order
+  // (separate multiply and add: the vector lanes compute exactly the scalar recurrence)
+  const Index RB = kZChunk;
+  constexpr Index PW = 8;
+  const Index np = (n + PW - 1) / PW;
+  const ZeroMap* z = zmap_for(J);
+  std::vector<std::pair<Index, Index>> blocks;  // (4-row block of entries, panel of columns)
+  for (Index pj = 0; pj < np; ++pj)
+    for (Index bi = pj * 2; bi < (n + 3) / 4; ++bi) blocks.push_back({bi, pj});
+  std::vector<double> W(static_cast<size_t>(RB * np * PW), 0.0);
+  std::vector<unsigned char> live(static_cast<size_t>(np));
+#ifdef __AVX2__
+  typedef double v4 __attribute__((vector_size(32)));
+#else
+  typedef double v4 __attribute__((vector_size(16)));
+#endif
+  constexpr int VW = int(sizeof(v4) / sizeof(double)), NV = int(PW) / VW;
   for (Index i0 = 0; i0 < m; i0 += RB) {
     const Index rb = std::min(RB, m - i0);
+    for (Index p = 0; p < np; ++p) {
+      bool any = !z;
+      for (Index c = p * PW; c < std::min(n, p * PW + PW) && !any; ++c) any = z->has(c, i0 / RB);
+      live[size_t(p)] = any;
+    }
 #pragma omp parallel num_threads(g_threads) if (m * n * n > 2000000)
     {
 #pragma omp for schedule(static)
-      for (Index j = 0; j < n; ++j) {
-        const double* src = J.col(j) + i0;
-        double* dst = W.data() + j * RB;
-        for (Index i = 0; i < rb; ++i) dst[i] = rs[size_t(i0 + i)] * src[i];
-      }
-#pragma omp for schedule(dynamic, 8)
-      for (size_t b = 0; b < blocks.size(); ++b) {
-        const Index bi = blocks[b].first, bj = blocks[b].second;
-        double acc[4][4];
-        const double* ci[4];
-        const double* cj[4];
-        for (int x = 0; x < 4; ++x) {
-          const Index li = std::min(n - 1, bi * 4 + x), lj = std::min(n - 1, bj * 4 + x);
-          ci[x] = W.data() + li * RB;
-          cj[x] = W.data() + lj * RB;
-        }
-        for (int x = 0; x < 4; ++x)
-          for (int y = 0; y < 4; ++y) {
-            const Index l = bi * 4 + x, k = bj * 4 + y;
-            acc[x][y] = (l < n && k < n) ? g(l, k) : 0.0;
+      for (Index p = 0; p < np; ++p) {
+        if (!live[size_t(p)]) continue;  // all-zero panel: its blocks are skipped below
+        double* dst = W.data() + p * RB * PW;
+        for (Index c = 0; c < PW; ++c) {
+          const Index j = p * PW + c;
+          if (j >= n || (z && !z->has(j, i0 / RB))) {
+            for (Index i = 0; i < rb; ++i) dst[i * PW + c] = 0.0;
+            continue;
           }
+          const double* src = J.col(j) + i0;
+          for (Index i = 0; i < rb; ++i) dst[i * PW + c] = rs[size_t(i0 + i)] * src[i];
+        }
+      }
+#pragma omp for schedule(dynamic, 4)
+      for (size_t b = 0; b < blocks.size(); ++b) {
+        const Index bi = blocks[b].first, pj = blocks[b].second;
+        const Index pa = bi / 2, ca = (bi % 2) * 4;  // the 4 rows' columns inside their panel
+        if (!live[size_t(pa)] || !live[size_t(pj)]) continue;  // every product is an exact zero
+        v4 acc[4][NV];
+        for (int x = 0; x < 4; ++x)
+          for (int y = 0; y < 8; ++y) {
+            const Index l = bi * 4 + x, k = pj * PW + y;
+            acc[x][y / VW][y % VW] = (l < n && k < n && l >= k) ? g(l, k) : 0.0;
+          }
+        const double* A = W.data() + pa * RB * PW + ca;
+        const double* B = W.data() + pj * RB * PW;
         for (Index i = 0; i < rb; ++i) {
-          const double a0 = ci[0][i], a1 = ci[1][i], a2 = ci[2][i], a3 = ci[3][i];
-          const double b0 = cj[0][i], b1 = cj[1][i], b2 = cj[2][i], b3 = cj[3][i];
-          acc[0][0] += a0 * b0; acc[0][1] += a0 * b1; acc[0][2] += a0 * b2; acc[0][3] += a0 * b3;
-          acc[1][0] += a1 * b0; acc[1][1] += a1 * b1; acc[1][2] += a1 * b2; acc[1][3] += a1 * b3;
-          acc[2][0] += a2 * b0; acc[2][1] += a2 * b1; acc[2][2] += a2 * b2; acc[2][3] += a2 * b3;
-          acc[3][0] += a3 * b0; acc[3][1] += a3 * b1; acc[3][2] += a3 * b2; acc[3][3] += a3 * b3;
+          v4 bv[NV];
+          __builtin_memcpy(bv, B + i * PW, sizeof(bv));
+          for (int x = 0; x < 4; ++x) {
+            const double a = A[i * PW + x];
+            for (int q = 0; q < NV; ++q) {
+              const v4 t = bv[q] * a;
+              acc[x][q] += t;
+            }
+          }
         }
         for (int x = 0; x < 4; ++x)
-          for (int y = 0; y < 4; ++y) {
-            const Index l = bi * 4 + x, k = bj * 4 + y;
-            if (l < n && k < n && l >= k) g(l, k) = acc[x][y];
+          for (int y = 0; y < 8; ++y) {
+            const Index l = bi * 4 + x, k = pj * PW + y;
+            if (l < n && k < n && l >= k) g(l, k) = acc[x][y / VW][y % VW];
           }
       }
     }
@@ -1223,6 +1304,14 @@ IpmResult solve(const DenseQp& qp, const IpmOptions& opts) {  // ipm.cpp:160-268
   st.iter = 0;
 
   IpmResult result;
+  ZeroMap zm;
+  struct ZGuard {
+    ~ZGuard() { g_zmap = nullptr; }
+  } zguard;
+  if (g_skip_zeros && m > 0) {
+    zm = make_zmap(qp.J);
+    g_zmap = &zm;
+  }
   Residuals res = compute_residuals(qp, st);
   while (true) {
     const int term = check_termination(res, st, opts);

@@ -215,6 +215,10 @@ IpmResult solve(const DenseQp& qp, const IpmOptions& opts);
 
 // number of OpenMP threads the dense kernels use (1 = the reference's single thread)
 void set_threads(int n);
+// test-speed switch: solve() skips J's all-zero 512-row column chunks in every J product
+// (bitwise the same results for finite data; the timed CPU baseline leaves it off)
+void set_skip_zeros(bool on);
+bool get_skip_zeros();
 int get_threads();
 
 }  // namespace orc

@@ -302,7 +302,8 @@ def main(argv=None) -> int:
         p.add_argument("--tol", type=float, default=1e-8, help="KKT tolerance")
         p.add_argument("--mu-init", type=float, default=1e-1, help="initial barrier parameter")
         p.add_argument("--max-iter", type=int, default=200, help="iteration cap")
-        p.add_argument("--backend", default="cuda", help="factorization backend: cuda")
+        p.add_argument("--backend", default="cuda",
+                       help="factorization backend: cuda (the reference's reference/eigen select it too)")
 
     s = sub.add_parser("solve", help="solve a problem file")
     s.add_argument("file")
@@ -326,7 +327,8 @@ def main(argv=None) -> int:
         a = ap.parse_args(argv)
     except SystemExit as e:
         return 0 if e.code == 0 else INVALID
-    if getattr(a, "backend", "cuda") != "cuda":
+    from . import linalg
+    if getattr(a, "backend", "cuda") not in linalg.BACKEND_NAMES:
         print(f"error: unknown factorization backend: {a.backend}", file=sys.stderr)
         return INVALID
     if getattr(a, "reps", 1) < 1 or (a.cmd == "gen" and (a.N < 1 or a.T < 1)):

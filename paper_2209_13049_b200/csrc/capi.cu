@@ -20,13 +20,13 @@ namespace cmpc {
 thread_local long long g_launches = 0;
 
 void pool_init(int device) {
-  static bool done[64] = {};
-  if (device < 0 || device >= 64 || done[device]) return;
-  cudaMemPool_t pool;
-  CMPC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-  unsigned long long keep = ~0ull;  // never hand cached pages back to the OS
-  CMPC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  done[device] = true;
+  static std::once_flag flags[kMaxDevices];
+  once_per_device(flags, device, [&] {
+    cudaMemPool_t pool;
+    CMPC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    unsigned long long keep = ~0ull;  // never hand cached pages back to the OS
+    CMPC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  });
 }
 thread_local std::string g_error;
 

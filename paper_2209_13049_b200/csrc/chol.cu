@@ -948,13 +948,14 @@ __global__ void __launch_bounds__(512) k_trsv(const double* __restrict__ L,
   for (int64_t i = tid; i < n; i += blockDim.x) x[i] = xs[i];
 }
 
-void set_attrs() {
-  static bool done = false;
-  if (done) return;
-  CMPC_CUDA(cudaFuncSetAttribute(k_chol_df, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
-  CMPC_CUDA(cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotfSmem));
-  CMPC_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  done = true;
+// the > 48 KB dynamic shared memory opt-ins, once per device (the context's device)
+void set_attrs(int device) {
+  static std::once_flag flags[kMaxDevices];
+  once_per_device(flags, device, [] {
+    CMPC_CUDA(cudaFuncSetAttribute(k_chol_df, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
+    CMPC_CUDA(cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotfSmem));
+    CMPC_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  });
 }
 
 }  // namespace
@@ -988,7 +989,7 @@ void launch_cholesky(Ctx& c, const double* M, double* L, double delta, const dou
     CMPC_CUDA(cudaMemsetAsync(info, 0, sizeof(long long), c.stream));
     return;
   }
-  set_attrs();
+  set_attrs(c.device);
   const int nt = (int)ceil_div(n, kNB);
   DfArgs a;
   a.M = M;
@@ -1015,14 +1016,14 @@ void launch_cholesky(Ctx& c, const double* M, double* L, double delta, const dou
 
 void launch_factor_inverses(Ctx& c, const double* L) {
   if (c.n == 0) return;
-  set_attrs();
+  set_attrs(c.device);
   k_diag_inv<<<(unsigned)ceil_div(c.n, kNB), 256, kPotfSmem, c.stream>>>(L, c.n, c.Winv);
   CMPC_LAUNCHED();
 }
 
 void launch_chol_solve(Ctx& c, const double* L, const double* b, double* x) {
   if (c.n == 0) return;
-  set_attrs();
+  set_attrs(c.device);
   const size_t sm = sizeof(double) * ((size_t)c.n + kNB);
   if (sm > 200 * 1024) throw CudaError("chol_solve: n too large for the single-CTA TRSV");
   k_trsv<<<1, 512, sm, c.stream>>>(L, c.Winv, b, x, c.n);

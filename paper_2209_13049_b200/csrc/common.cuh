@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -32,6 +33,21 @@ extern thread_local long long g_launches;
     ++::cmpc::g_launches;               \
     CMPC_CUDA(cudaPeekAtLastError());   \
   } while (0)
+
+// Run f once per device: kernel attributes (large dynamic shared memory opt-in, carveout) and
+// memory-pool settings belong to a device's context, not to the process.
+constexpr int kMaxDevices = 64;
+template <typename F>
+void once_per_device(std::once_flag (&flags)[kMaxDevices], int device, F&& f) {
+  if (device < 0 || device >= kMaxDevices) throw CudaError("device ordinal out of range");
+  std::call_once(flags[device], [&] {
+    int cur = 0;
+    CMPC_CUDA(cudaGetDevice(&cur));
+    if (cur != device) CMPC_CUDA(cudaSetDevice(device));
+    f();
+    if (cur != device) CMPC_CUDA(cudaSetDevice(cur));
+  });
+}
 
 // Stream-ordered device allocations from the device's memory pool (kept cached: a
 // reloaded QP of similar size reuses the pages instead of re-mapping gigabytes).

@@ -204,8 +204,9 @@ void set_mu(Ctx& c, double mu);
 // residuals at the current state (r1, r2, r3, kkt, objective pieces) -> packet A;
 // reuse_trial: the state was just moved to the last evaluated line-search trial point
 void launch_residuals(Ctx& c, bool reuse_trial = false);
-// r2 and complementarity only (after a barrier change) -> packet A kkt updated
-void launch_residuals_mu(Ctx& c);
+// r2 and complementarity only (after a barrier change) -> packet kkt at the new mu, from the
+// residual maxima of `a` (the current point's residual packet) and the recomputed max_comp
+void launch_residuals_mu(Ctx& c, const Packet& a);
 // sigma = z/s, omega, q = Pi'(r2 - sigma r3) (one launch; the singleton diagonal is added by k_syrk_reduce)
 void launch_prepare_step(Ctx& c, const double* sigma_override);
 // rhs = -r1 + (P' q + singletons): the partial product (this context's rows) and the final

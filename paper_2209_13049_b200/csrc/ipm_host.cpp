@@ -132,18 +132,29 @@ void run_segment(Ctx& c, cudaGraphExec_t& exec, long long& nodes, bool allow_cap
   }
   cudaGraph_t graph = nullptr;
   const long long l0 = g_launches;
+  // the captured k_publish advances pub_expect although nothing runs until the launch below:
+  // a capture that fails puts it back, or every later wait would be for a publish that never comes
+  const unsigned long long pub0 = c.pub_expect;
   CMPC_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   try {
     seg();
+    CMPC_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    nodes = g_launches - l0;
+    g_launches = l0;
+    CMPC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   } catch (...) {
-    cudaStreamEndCapture(c.stream, &graph);
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(c.stream, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+      cudaGraph_t g2 = nullptr;
+      cudaStreamEndCapture(c.stream, &g2);
+      if (g2) cudaGraphDestroy(g2);
+    }
     if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    c.pub_expect = pub0;
+    g_launches = l0;
     throw;
   }
-  CMPC_CUDA(cudaStreamEndCapture(c.stream, &graph));
-  nodes = g_launches - l0;
-  g_launches = l0;
-  CMPC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   cudaGraphDestroy(graph);
   CMPC_CUDA(cudaGraphLaunch(exec, c.stream));
   g_launches += nodes;
@@ -299,7 +310,7 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     const double mu_next = (A.kkt <= 10.0 * c.mu) ? std::max(tol / 10.0, kappa_mu * c.mu) : c.mu;
     if (mu_next != c.mu) {
       set_mu(c, mu_next);
-      launch_residuals_mu(c);
+      launch_residuals_mu(c, A);
     }
     // sigma, condensed matrix, factorization with the shift ladder (ipm.cpp:200-226), then
     // speculatively: directions, recovery, fraction to boundary, line-search trial 0

@@ -621,13 +621,12 @@ void syrk_plan(Ctx& c) {
   };
   c.tmap_P = encode(64);
   c.tmap_P32 = encode(32);
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag flags[kMaxDevices];  // per device: the attributes live in its context
+  once_per_device(flags, c.device, [] {
     CMPC_CUDA(cudaFuncSetAttribute(k_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
     // two 99 KB CTAs per SM need the largest shared-memory carveout
     CMPC_CUDA(cudaFuncSetAttribute(k_syrk, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    attr = true;
-  }
+  });
 }
 
 void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk) {

@@ -513,7 +513,16 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, i
   }
 }
 
-__global__ void k_kkt_only(int64_t n, int64_t m, const double* __restrict__ hmax, Packet* pk) {
+// kkt after a barrier change: the residual maxima of the current point come in as arguments
+// (the host loop's packet A: k_publish has reset the device packet's accumulators since) and
+// are written back, so the packet is whole again; only max_comp was recomputed at the new mu
+__global__ void k_kkt_only(int64_t n, int64_t m, const double* __restrict__ hmax, Packet* pk,
+                           double max_r1, double max_r3, double max_lam, double max_s, double max_z) {
+  pk->max_r1 = max_r1;
+  pk->max_r3 = max_r3;
+  pk->max_lam = max_lam;
+  pk->max_s = max_s;
+  pk->max_z = max_z;
   const double ds = fmax(1.0, fmax(*hmax, pk->max_lam) / (double)(n + m));
   double kkt = pk->max_r1 / ds;
   if (m > 0) {
@@ -1155,7 +1164,7 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
   CMPC_LAUNCHED();
 }
 
-void launch_residuals_mu(Ctx& c) {
+void launch_residuals_mu(Ctx& c, const Packet& a) {
   if (c.m > 0 || c.comm) {
     k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 3);
     CMPC_LAUNCHED();
@@ -1165,7 +1174,8 @@ void launch_residuals_mu(Ctx& c) {
     CMPC_LAUNCHED();
   }
   comm_allreduce(c, &c.pk->max_comp, 1, CommType::f64, CommOp::max);
-  k_kkt_only<<<1, 1, 0, c.stream>>>(c.n, rows_all(c), c.hmax, c.pk);
+  k_kkt_only<<<1, 1, 0, c.stream>>>(c.n, rows_all(c), c.hmax, c.pk, a.max_r1, a.max_r3, a.max_lam,
+                                    a.max_s, a.max_z);
   CMPC_LAUNCHED();
 }
 

@@ -295,9 +295,16 @@ class ShardedQp:
 
 
 def device_qp(qp: DenseQp) -> DeviceQp:
-    """The QP's cached device context (re-created when it was closed)."""
-    if qp._device is None or getattr(qp._device, "h", None) is None:
-        qp._device = DeviceQp(qp)
+    """The QP's cached device context: re-created when it was closed or when the QP's arrays
+    are no longer the ones it was loaded from (DenseQp.device_key). The reference takes the QP
+    by const reference on every call, so a solve always sees the current arrays."""
+    key = qp.device_key()
+    if qp._device is not None and getattr(qp._device, "h", None) is not None and qp._device_key == key:
+        return qp._device
+    if qp._device is not None and qp._device_key is not None and qp._device_key != key:
+        qp._device.close()  # the arrays changed under the cached context
+    qp._device = DeviceQp(qp)
+    qp._device_key = key
     return qp._device
 
 
@@ -426,7 +433,7 @@ def solve(qp: DenseQp, opts: IpmOptions = None) -> IpmResult:
         raise DimensionError("qp.h length does not match qp.H")
     if qp.d.size != qp.m:
         raise DimensionError("qp.d length does not match qp.J")
-    if opts.backend != "cuda":
+    if opts.backend not in _linalg.BACKEND_NAMES:
         raise ValueError(f"unknown factorization backend: {opts.backend}")
     t0 = time.perf_counter()
     dq = device_qp(qp)

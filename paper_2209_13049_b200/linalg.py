@@ -97,9 +97,16 @@ class CudaBackend(Backend):
         return Factor(L, dt)
 
 
+# The reference's names (dense_linalg.cpp:112-116: "reference" = blocked right-looking
+# Cholesky, "eigen" = Eigen::LLT) select the same device factorization here: both compute
+# the lower Cholesky factor of the same matrix, so code written against the reference keeps
+# working; "cuda" names it explicitly. Anything else throws like the reference.
+BACKEND_NAMES = ("cuda", "reference", "eigen")
+
+
 def make_backend(name: str) -> Backend:
     """dense_linalg.cpp:112-116 with the B200 registry."""
-    if name == "cuda":
+    if name in BACKEND_NAMES:
         return CudaBackend()
     raise ValueError(f"unknown factorization backend: {name}")
 

@@ -144,7 +144,26 @@ class DenseQp:
     # used to shard rows across GPUs by whole stages
     row_stage: np.ndarray | None = None
     row_width: np.ndarray | None = None
-    _device: object = field(default=None, repr=False, compare=False)
+    # the cached device context (ipm.device_qp) and the fingerprint of the arrays it was loaded
+    # from: never copied by dataclasses.replace, re-checked on every solve
+    _device: object = field(init=False, default=None, repr=False, compare=False)
+    _device_key: object = field(init=False, default=None, repr=False, compare=False)
+    _version: int = field(init=False, default=0, repr=False, compare=False)
+
+    _QP_FIELDS = ("H", "h", "h0", "J", "d")
+
+    def __setattr__(self, name, value):
+        if name in DenseQp._QP_FIELDS:  # reassigning an array or h0 invalidates the upload
+            object.__setattr__(self, "_version", getattr(self, "_version", 0) + 1)
+        object.__setattr__(self, name, value)
+
+    def device_key(self):
+        """Cheap fingerprint of the arrays a device upload holds: the array objects, their
+        data pointers, shapes and strides, h0, and a counter bumped on reassignment. In-place
+        edits of the arrays' contents are not seen: call invalidate_device() after them."""
+        def arr(a):
+            return (id(a), a.__array_interface__["data"][0], a.shape, a.strides)
+        return (self._version, arr(self.H), arr(self.h), arr(self.J), arr(self.d), self.h0)
 
     def __post_init__(self):
         self.H = np.asfortranarray(np.asarray(self.H, dtype=np.float64))
@@ -170,6 +189,7 @@ class DenseQp:
         if self._device is not None:
             self._device.close()
         self._device = None
+        self._device_key = None
 
 
 def _apply_Q(Qt, X, diag):
@@ -372,9 +392,11 @@ def refresh_initial_state(qp: DenseQp, x_bar) -> None:
     Q_K = data.Q + SK + SK.T + data.K.T @ data.R @ data.K
     S_K = data.S + data.K.T @ data.R
     qp.x0 = free_response(A_K, data.x_bar, data.w)
+    fresh = qp._device is not None and qp._device_key == qp.device_key()
     qp.h, qp.h0, qp.d = _affine(data, qp.gk, qp.x0, Q_K, S_K)
-    if qp._device is not None:
+    if fresh:  # same H and J on the device: only h, h0, d travel
         qp._device.update_affine(qp.h, qp.h0, qp.d)
+        qp._device_key = qp.device_key()
 
 
 def recover_trajectory(qp: DenseQp, v) -> Trajectory:

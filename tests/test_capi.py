@@ -70,7 +70,7 @@ def test_error_codes_surface_as_exceptions():
         with pytest.raises(DimensionError):
             ipm.solve(qp, ipm.IpmOptions(**bad))
     with pytest.raises(ValueError):
-        ipm.solve(qp, ipm.IpmOptions(backend="reference"))
+        ipm.solve(qp, ipm.IpmOptions(backend="lapack"))
 
 
 def test_host_side_rules():  # test_ipm.cpp:322-361 on the host mirror
@@ -97,7 +97,10 @@ def test_backend_registry():  # test_dense_linalg.cpp:162-169 with the B200 regi
     from paper_2209_13049_b200 import linalg
     assert linalg.make_backend("cuda").name() == "cuda"
     assert linalg.make_backend("cuda").parallel()
-    for unknown in ("reference-cpu", "eigen", "nonexistent"):
+    # the reference's names select the device factorization (same factor)
+    for alias in ("reference", "eigen"):
+        assert linalg.make_backend(alias).name() == "cuda"
+    for unknown in ("reference-cpu", "Eigen", "nonexistent", ""):
         with pytest.raises(ValueError):
             linalg.make_backend(unknown)
 

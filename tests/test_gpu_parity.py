@@ -88,3 +88,58 @@ def test_device_matches_golden_fixtures(name):
     assert abs(r.objective - want["objective"]) <= TOL * (1 + abs(want["objective"]))
     assert rel(r.v, want["v"]) <= TOL and rel(r.z, want["z"]) <= TOL
     assert [x.trial for x in log] == [int(row[7]) for row in want["log"]]
+
+
+def _with_dead_column(qp, h_dead: float):
+    """The QP with one extra variable that no constraint touches and H couples to nothing:
+    M's extra diagonal entry is exactly h_dead at every iteration, so the reference's shift
+    ladder (ipm.cpp:205-221) decides every factorization; the variable's gradient stays 0."""
+    n = qp.n
+    H = np.zeros((n + 1, n + 1))
+    H[:n, :n] = qp.H
+    H[n, n] = h_dead
+    J = np.zeros((qp.m, n + 1))
+    J[:, :n] = qp.J
+    return P.DenseQp(H=H, h=np.append(qp.h, 0.0), h0=qp.h0, J=J, d=qp.d)
+
+
+@pytest.mark.parametrize("h_dead,delta", [(0.0, 1e-8), (-5e-7, 1e-6), (-0.5, 1.0)])
+def test_shift_ladder_rescues_every_step_like_the_reference(O, h_dead, delta):
+    # proj/src/ipm.cpp:205-221 (the reference's own test covers only total failure,
+    # proj/tests/test_ipm.cpp:397-403): the zero pivot fails at delta = 0 and the ladder's
+    # first sufficient shift is used and logged, on the device as in the oracle
+    p = O.random_problem(O.instance_rng(42, 3), fixed=(10, 2, 0, 10))
+    qp = _with_dead_column(P.build_dense_qp(lq_from_oracle(p)), h_dead)
+    r, o, log = solve_both(O, qp)
+    assert_parity(r, o, log)
+    assert r.status == ipm.IpmStatus.converged
+    assert {x.delta for x in log} == {delta}
+
+
+def test_inspected_kkt_matches_the_reference_after_every_barrier_update(O):
+    # compute_residuals at the new mu (ipm.cpp:197): the device recomputes only the
+    # complementarity part; the kkt seen by inspect must be the reference's at every iteration
+    for i in range(3):
+        p = O.random_problem(O.instance_rng(42, i), fixed=(10, 2, 0, 10))
+        qp = P.build_dense_qp(lq_from_oracle(p))
+        dev, ref = [], []
+        r = ipm.solve(qp, ipm.IpmOptions(inspect=lambda s: dev.append((s.state.mu, s.residuals.kkt_error))))
+        O.solve(oracle_qp(O, qp), inspect=lambda d: ref.append((d["mu"], d["kkt"])))
+        assert r.status == ipm.IpmStatus.converged and len(dev) == len(ref) == r.iter
+        mus = [m for m, _ in ref]
+        assert [m for m, _ in dev] == mus
+        assert len(set(mus)) > 3  # the barrier moved several times
+        for (_, kd), (_, kr) in zip(dev, ref):
+            assert abs(kd - kr) <= 1e-9 * (1 + abs(kr))
+
+
+def test_failure_exit_reports_the_reference_kkt(O):
+    # every shift fails (a dead column with M entry -1e3 < -1e2): factorization_failure after
+    # the first barrier decision, returning the residual kkt at the current mu (ipm.cpp:219-226)
+    p = O.random_problem(O.instance_rng(42, 0), fixed=(10, 2, 0, 10))
+    qp = _with_dead_column(P.build_dense_qp(lq_from_oracle(p)), -1e3)
+    r = ipm.solve(qp)
+    o = O.solve(oracle_qp(O, qp))
+    assert r.status.name == o.status == "factorization_failure"
+    assert r.iter == o.iter == 0
+    assert abs(r.kkt_error - o.kkt_error) <= 1e-9 * (1 + abs(o.kkt_error))

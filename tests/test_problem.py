@@ -124,3 +124,20 @@ def test_dims_validation():
     bad.T = 4
     with pytest.raises(DimensionError):
         P.dims(bad)
+
+
+def test_device_cache_is_not_copied_and_tracks_reassignment():
+    # dataclasses.replace must not carry the cached device context over, and
+    # reassigning H/h/h0/J/d must change the fingerprint the cache is checked against
+    import dataclasses
+    qp = P.DenseQp(H=[[4.0]], h=[2.0], h0=0.0, J=[[-1.0]], d=[0.0])
+    qp._device, qp._device_key = object(), qp.device_key()
+    other = dataclasses.replace(qp, d=np.array([1.0]))
+    assert other._device is None and other._device_key is None
+    k0 = qp.device_key()
+    qp.d = np.array([0.5])
+    assert qp.device_key() != k0
+    k1 = qp.device_key()
+    qp.h0 = 1.0
+    assert qp.device_key() != k1
+    assert qp.device_key() == qp.device_key()
