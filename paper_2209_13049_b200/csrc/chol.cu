@@ -1,23 +1,33 @@
 // K2/K3/K4: Cholesky of the condensed matrix with the reference's failure rule, and
 // the two triangular solves.
 //
-// Reference: ReferenceBackend::factorize (proj/src/dense_linalg.cpp:59-77, block 64:
-// potf2 :24-40, trsm :43-51, trailing rankUpdate), failure "!(diag > 0) || !isfinite"
-// at the first pivot; Factor::solve (:102-110). The shift ladder (proj/src/ipm.cpp:
-// 205-221) re-factors M + delta I; here M is kept intact and L written separately, so a
-// retry never repeats the SYRK. info = failing pivot + 1 (0 = success).
+// Reference: ReferenceBackend::factorize (proj/src/dense_linalg.cpp:59-77: potf2 :24-40,
+// trsm :43-51, trailing rankUpdate), failure "!(diag > 0) || !isfinite" at the first
+// pivot; Factor::solve (:102-110). The shift ladder (proj/src/ipm.cpp:205-221) re-factors
+// M + delta I; here M is kept intact and L written separately, so a retry never repeats the
+// SYRK. info = failing pivot + 1 (0 = success).
 //
-// One persistent dataflow kernel (k_chol_df) factors the whole matrix, tile by tile
-// (64 x 64, lower tiles only), left-looking:
-//   tile (i, j):  A_ij <- M_ij - sum_{k<j} L_ik L_jk^T        (DMMA, accumulator in registers)
-//                 i == j: L_jj = potf2(A_jj) and W_j = L_jj^{-1} (register-blocked, in smem)
-//                 i >  j: L_ij = A_ij W_j^T                   (DMMA, no sequential TRSM)
+// One persistent dataflow kernel (k_chol_df) factors the matrix in 32 x 32 tiles (lower
+// tiles only), left-looking, and fuses both triangular solves:
+//   diagonal task d   A_{d,d-1} <- M_{d,d-1} - sum_{k<d-1} L_dk L_{d-1,k}^T   (DMMA, registers)
+//                     A_dd      <- M_dd + delta I - sum_{k<d-1} L_dk L_dk^T
+//                     then, once diagonal d-1 is published: the sub-diagonal panel
+//                     L_{d,d-1} = A_{d,d-1} W_{d-1}^T (published at once), A_dd -= L L^T,
+//                     and the 32 x 32 factor: warp 0 runs the pivot chain (row i of the
+//                     tile in lane i's registers; the next pivot travels by one shuffle,
+//                     each finished column through shared memory) while warp 1 forms
+//                     W_d = L_dd^{-1} column by column right behind it; forward solve
+//                     y_d = W_d (b_d - sum_k L_dk y_k) rides along.
+//   panel task (i, j), i >= j + 2:   L_ij = (M_ij - sum_{k<j} L_ik L_jk^T) W_j^T
+//   backward task i:  x_i = W_i^T (y_i - sum_{j>i} L_ji^T x_j)
+// So each column of the factor costs one inter-CTA hop on the critical path (diagonal d-1
+// -> diagonal d), not two: the sub-diagonal panel is formed by the CTA that needs it next.
 // Every finished tile publishes a per-tile flag (release/acquire at GPU scope) stamped with
-// the launch's generation number, so flags never need resetting. CTAs grab tiles from an
-// atomic counter in column-major (topological) order, and a tile only waits for tiles
-// earlier in that order, which were grabbed by CTAs that are already running: the kernel
-// cannot deadlock whatever the residency. The last CTA out publishes info and advances the
-// generation. The W blocks are kept, so the triangular solves (k_trsv) are block GEMVs.
+// the launch's generation number, so flags never need resetting. CTAs grab tasks from an
+// atomic counter in an order where a task only waits for tasks earlier in that order,
+// which were grabbed by CTAs that are already running: the kernel cannot deadlock whatever
+// the residency. The last CTA out publishes info and advances the generation. The W blocks
+// are kept, so a later stand-alone solve (k_trsv) is block GEMVs.
 #include <algorithm>
 
 #include "internal.cuh"
@@ -27,480 +37,70 @@ namespace cmpc {
 
 namespace {
 
-#ifdef CMPC_TRACE
-__device__ unsigned long long g_trace[256];
-#define TRACE(i)                                                   \
-  do {                                                             \
-    if (blockIdx.x == 0 && threadIdx.x == 0) g_trace[(i)] = clock64(); \
-  } while (0)
-#define TRACEW(i)                                                   \
-  do {                                                              \
-    if (blockIdx.x == 0 && threadIdx.x == 32) g_trace[(i)] = clock64(); \
-  } while (0)
+#ifdef CMPC_CHOL_TRACE
+// tools/exp/chol_trace.cu: per task, clock64 stamps kept in shared memory while the task runs
+// (no global traffic inside the timed region) and flushed with a %globaltimer stamp at its end
+__device__ unsigned long long g_ctrace[4096 * 10];
+__shared__ unsigned long long s_ctrace[8];
+__device__ __forceinline__ void ctrace(int slot) {
+  if (threadIdx.x == 0) s_ctrace[slot] = clock64();
+}
+__device__ __forceinline__ void ctrace_flush(int task) {
+  if (threadIdx.x == 0 && task < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long c = clock64();
+    for (int k = 0; k < 8; ++k) g_ctrace[task * 10 + k] = s_ctrace[k] ? c - s_ctrace[k] : 0ull;
+    g_ctrace[task * 10 + 8] = t;
+    for (int k = 0; k < 8; ++k) s_ctrace[k] = 0;
+  }
+}
+#define CTRACE(task, slot) ctrace(slot)
+#define CTRACE_FLUSH(task) ctrace_flush(task)
 #else
-#define TRACE(i) \
-  do {           \
+#define CTRACE(task, slot) \
+  do {                     \
   } while (0)
-#define TRACEW(i) \
-  do {            \
+#define CTRACE_FLUSH(task) \
+  do {                     \
   } while (0)
 #endif
 
-constexpr int kNB = 64;
-constexpr int kLD = kNB + 1;
-constexpr int kGemmLD = 68;
-constexpr int kPotfSmem = (2 * kNB * kLD + 8 * 64) * 8;
-constexpr int kDfThreads = 256;
-
-// W = L^{-1} for the factored 64 x 64 lower block in a (identity padding beyond b),
-// right-looking substitution on L W = I: step p scales row p of W, then rows i > p
-// subtract l_ip W_p. 256 threads, 2 barriers per step.
-__device__ void inv64(const double* a, double* w) {
-  const int tid = threadIdx.x;
-  for (int e = tid; e < kNB * kNB; e += blockDim.x) w[(e & 63) + (e >> 6) * kLD] = ((e & 63) == (e >> 6)) ? 1.0 : 0.0;
-  __syncthreads();
-  const int i = tid & 63, kg = tid >> 6;
-  for (int p = 0; p < kNB; ++p) {
-    const double l = a[p + p * kLD];
-    if (tid >= 64 && tid - 64 <= p) w[p + (tid - 64) * kLD] = dv(w[p + (tid - 64) * kLD], l);
-    __syncthreads();
-    if (i > p) {
-      const double lip = a[i + p * kLD];
-      for (int k = kg; k <= p; k += 4) w[i + k * kLD] = fma(-lip, w[p + k * kLD], w[i + k * kLD]);
-    }
-    __syncthreads();
-  }
-}
-
-// load the b x b diagonal block at (k0, k0); identity padding beyond b. All 16 loads of a
-// thread are issued before any shared store (generic pointers would otherwise serialise them).
-__device__ void load_diag(const double* L, int64_t n, int64_t k0, int b, double* a) {
-  double v[16];
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int e = threadIdx.x + 256 * u, i = e & 63, j = e >> 6;
-    double x = 0.0;
-    if (i < b && j < b) {
-      if (i >= j) x = L[(k0 + i) + (k0 + j) * n];
-    } else if (i == j) {
-      x = 1.0;
-    }
-    v[u] = x;
-  }
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int e = threadIdx.x + 256 * u;
-    a[(e & 63) + (e >> 6) * kLD] = v[u];
-  }
-}
-
-// write the lower b x b part of a to L and the full (zero-upper) 64 x 64 W
-__device__ void store_diag(double* L, int64_t n, int64_t k0, int b, const double* a, const double* w,
-                           double* Wout, bool write_l) {
-  double va[16], vw[16];
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int e = threadIdx.x + 256 * u, i = e & 63, j = e >> 6;
-    va[u] = a[i + j * kLD];
-    vw[u] = (i >= j) ? w[i + j * kLD] : 0.0;
-  }
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int e = threadIdx.x + 256 * u, i = e & 63, j = e >> 6;
-    if (write_l && i < b && j < b && i >= j) L[(k0 + i) + (k0 + j) * n] = va[u];
-    Wout[e] = vw[u];
-  }
-}
-
-// 1/sqrt(x) from a float seed and two Newton steps in FP64 (the FP64 sqrt and divide
-// sequences cost several hundred cycles each on the pivot's critical path); exact
-// fallback outside the float range
-__device__ __forceinline__ double rsqrt_fast(double x) {
-  if (x > 1e-30 && x < 1e30) {
-    double y = (double)rsqrtf((float)x);
-    const double hx = 0.5 * x;
-    y = y * fma(-hx * y, y, 1.5);
-    y = y * fma(-hx * y, y, 1.5);
-    return y;
-  }
-  return 1.0 / sqrt(x);
-}
-
+constexpr int kB = 32;           // tile edge
+constexpr int kLD = 36;          // staged-tile leading dimension (conflict-free DMMA fragments)
+constexpr int kTS = kB * kLD;    // doubles per staged tile
+constexpr int kT = 128;          // threads per CTA (4 warps)
 constexpr unsigned kFull = 0xffffffffu;
 
-// 1/x for x > 0 from a float seed and two Newton steps (exact fallback outside float range)
-__device__ __forceinline__ double rcp_fast(double x) {
-  if (x > 1e-30 && x < 1e30) {
-    double y = (double)__frcp_rn((float)x);
-    y = y * fma(-x, y, 2.0);
-    y = y * fma(-x, y, 2.0);
-    return y;
-  }
-  return 1.0 / x;
-}
-
-__device__ __forceinline__ void bar_sync_n(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive_n(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// 1/sqrt(x): MUFU.RSQ64H seed + two Newton steps (~1/3 the latency of the float-seed
-// path with its range branch, measured in tools/exp/p1_bench.cu); flushes subnormals, so
-// the caller re-factors exactly when a pivot leaves [1e-300, 1e300]
-__device__ __forceinline__ double rsqrt_mufu(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
-  return y;
-}
-
-// 8 x 8 Cholesky + inverse in registers (every lane redundantly) from the lower block at
-// a + o * (kLD + 1). Returns the first failing pivot (< bv) or -1; *odd flags a pivot out of
-// the fast reciprocal square root's range.
-template <bool EXACT>
-__device__ __forceinline__ int factor8(const double* a, int o, int bv, double (&l)[8][8], double (&wi)[8][8],
-                                       bool* odd) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j <= i; ++j) l[i][j] = a[(o + i) + (o + j) * kLD];
-  int fail = -1;
-  bool bad = false;
-  double rl[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const double d = l[j][j];
-    if (fail < 0 && j < bv && (!(d > 0.0) || !isfinite(d))) fail = j;
-    bad |= !(d >= 1e-300 && d <= 1e300);
-    const double y = EXACT ? 1.0 / sqrt(d) : rsqrt_mufu(d);
-    rl[j] = y;
-    l[j][j] = d * y;
-#pragma unroll
-    for (int i = j + 1; i < 8; ++i) l[i][j] *= y;
-#pragma unroll
-    for (int k = j + 1; k < 8; ++k)
-#pragma unroll
-      for (int i = k; i < 8; ++i) l[i][k] = fma(-l[i][j], l[k][j], l[i][k]);
-  }
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    wi[p][p] = rl[p];
-#pragma unroll
-    for (int k = 0; k < p; ++k) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = k; q < p; ++q) s = fma(l[p][q], wi[q][k], s);
-      wi[p][k] = -rl[p] * s;
-    }
-  }
-  *odd = bad;
-  return fail;
-}
-
-
-
-// Factor the 64 x 64 block a (LD kLD; lower, zero upper part, identity padding beyond b)
-// in place and build W = L^{-1} in w (LD kLD, lower). Right-looking over eight 8-wide
-// column blocks with one block of lookahead:
-//   warp 0 (pivot warp)  P1 factor the 8 x 8 diagonal block kb and its inverse W8 in
-//                        registers (the pivot chain), then, once the workers have finished
-//                        step kb-1, P3 the panel rows X of block kb+1 (W8 from registers)
-//                        and P4 the update of diagonal block kb+1, so P1(kb+1) starts
-//                        without waiting for the rest of step kb;
-//   warps 1-3, 5-7       every other product of the step, as DMMA m16n8k4 fragments
-//   (workers)            (K = 8) spread warp-uniformly over the six warps: W2 the W rows of
-//                        block kb, W(o+i, :o) = -W8(i,:) B(o:o+8, :o) (B = sum L W
-//                        accumulates in w), the panel rows X(r,:) = A(r, o:o+8) W8' below
-//                        block kb+1, then S3 A(r, c) -= X(r,:) X(c,:)' below block kb+1 and
-//                        B(r, c) += X(r,:) W(o:o+8, c);
-//   warp 4               parked, so the pivot warp owns its scheduler's instruction cache.
-// X and the block's W rows are stored p-major with stride kXLD (conflict-free fragments).
-// Named barriers: 1 = step published (pivot -> workers), 3 = workers done with a step
-// (workers -> pivot), 4 = worker-only. The loops stay rolled: a fully unrolled body
-// overflows the instruction cache. Returns the first failing pivot (uniform) or -1.
-constexpr int kXLD = 68;
-__device__ int diag_factor(double* __restrict__ a, double* __restrict__ w, double* __restrict__ sc, int b) {
-  constexpr int kW = 192, kWarps = 6;  // worker threads / warps
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  double* xs = sc;                  // 2 x [8 x kXLD]: X(r, p) at xs[buf][p * kXLD + r]
-  double* wsb = xs + 2 * 8 * kXLD;  // [8 x kXLD]: W(o + p, c) at wsb[p * kXLD + c]
-  double* l8s = wsb + 8 * kXLD;     // 2 x [8 x 8] factor (row-major)
-  double* w8s = l8s + 128;          // 2 x [8 x 8] inverse
-  volatile int* fls = reinterpret_cast<volatile int*>(w8s + 128);
-  for (int e = tid; e < kNB * kLD; e += kDfThreads) w[e] = 0.0;
-  l8s[tid] = 0.0;  // l8s and w8s (256 doubles): strictly upper parts stay zero
-  if (tid == 0) *fls = -1;
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll 1
-    for (int kb = 0; kb < 8; ++kb) {
-      const int o = 8 * kb, buf = kb & 1;
-      TRACE(10 + 4 * kb);
-      const int bv = b - o < 0 ? 0 : (b - o > 8 ? 8 : b - o);
-      double l[8][8], wi[8][8];
-      bool odd;
-      int fail = factor8<false>(a, o, bv, l, wi, &odd);
-      if (odd) fail = factor8<true>(a, o, bv, l, wi, &odd);
-      double* l8 = l8s + 64 * buf;
-      double* w8 = w8s + 64 * buf;
-      if (lane == 0) {  // straight-line stores (a lane-indexed store compiles to a jump table)
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j <= i; ++j) {
-            l8[i * 8 + j] = l[i][j];
-            w8[i * 8 + j] = wi[i][j];
-          }
-        if (fail >= 0) *fls = o + fail;
-      }
-      TRACE(11 + 4 * kb);
-      if (kb < 7) {
-        bar_sync_n(3, 224);  // workers are done with step kb-1
-#ifdef CMPC_TRACE
-        if (*fls > 1000) break;  // never: a shared read that waits for the barrier (trace)
-#endif
-        TRACE(12 + 4 * kb);
-        if (fail < 0) {
-          double* x = xs + 8 * kXLD * buf;
-          // P3: X rows of block kb+1, lane i < 8 takes row o+8+i: X(r, p) = sum_{q<=p} A(r, o+q) W8(p, q)
-          if (lane < 8) {
-            const int r = o + 8 + lane;
-            double ar[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) ar[q] = a[r + (o + q) * kLD];
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-              double s = 0.0;
-#pragma unroll
-              for (int q = 0; q <= p; ++q) s = fma(ar[q], wi[p][q], s);
-              x[p * kXLD + r] = s;
-              a[r + (o + p) * kLD] = s;
-            }
-          }
-          __syncwarp();
-          TRACE(60 + kb);
-          // P4: diagonal block kb+1 -= X X', lane (i, j0) takes entries (i, j0) and (i, j0 + 4)
-          {
-            const int ri = o + 8 + g, r0 = o + 8 + t, r1 = r0 + 4;
-            double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-              const double xi = x[p * kXLD + ri];
-              s0 = fma(xi, x[p * kXLD + r0], s0);
-              s1 = fma(xi, x[p * kXLD + r1], s1);
-            }
-            if (t <= g) a[ri + r0 * kLD] -= s0;
-            if (t + 4 <= g) a[ri + r1 * kLD] -= s1;
-          }
-          __syncwarp();
-        }
-      }
-      TRACE(13 + 4 * kb);
-      bar_arrive_n(1, 224);  // step kb published
-      if (fail >= 0) break;
-    }
-  } else if (warp != 4) {
-    const int wid = warp < 4 ? warp - 1 : warp - 2;  // 0..5
-    const int wt = wid * 32 + lane;                   // 0..191
-    bar_arrive_n(3, 224);
-#pragma unroll 1
-    for (int kb = 0; kb < 8; ++kb) {
-      const int o = 8 * kb, buf = kb & 1;
-      bar_sync_n(1, 224);
-      if (*fls >= 0) break;
-      TRACEW(100 + 4 * kb);
-      const double* l8 = l8s + 64 * buf;
-      const double* w8 = w8s + 64 * buf;
-      double* x = xs + 8 * kXLD * buf;
-      // the block's L entries and its diagonal W entries
-      if (wt < 64) {
-        const int i = wt >> 3, j = wt & 7;
-        wsb[i * kXLD + o + j] = w8[i * 8 + j];
-        a[(o + i) + (o + j) * kLD] = l8[i * 8 + j];
-      }
-      // W2: D(c, i) = sum_p B(o+p, c) W8(i, p), c < o; W(o+i, c) = -D
-      for (int f = wid; f < (o + 15) / 16; f += kWarps) {
-        const int m0 = 16 * f;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k0 = 0; k0 < 8; k0 += 4) {
-          const int p = k0 + t;
-          double af[2];
-          af[0] = m0 + g < o ? w[(o + p) + (m0 + g) * kLD] : 0.0;
-          af[1] = m0 + g + 8 < o ? w[(o + p) + (m0 + g + 8) * kLD] : 0.0;
-          dmma1684(acc, af, w8[g * 8 + p]);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int c = m0 + g + 8 * (e >> 1), i = 2 * t + (e & 1);
-          if (c < o) wsb[i * kXLD + c] = -acc[e];
-        }
-      }
-      // X rows below block kb+1: D(r, p) = sum_q A(r, o+q) W8(p, q), r >= o+16
-      for (int f = wid; f < (kNB - 1 - o) / 16; f += kWarps) {
-        const int m0 = o + 16 + 16 * f;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k0 = 0; k0 < 8; k0 += 4) {
-          const int q = k0 + t;
-          double af[2];
-          af[0] = m0 + g < kNB ? a[(m0 + g) + (o + q) * kLD] : 0.0;
-          af[1] = m0 + g + 8 < kNB ? a[(m0 + g + 8) + (o + q) * kLD] : 0.0;
-          dmma1684(acc, af, w8[g * 8 + q]);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = m0 + g + 8 * (e >> 1), p = 2 * t + (e & 1);
-          if (r < kNB) x[p * kXLD + r] = acc[e];
-        }
-      }
-      TRACEW(101 + 4 * kb);
-      bar_sync_n(4, kW);
-#ifdef CMPC_TRACE
-      if (*fls > 1000) break;  // never: waits for the barrier (trace)
-#endif
-      TRACEW(102 + 4 * kb);
-      // S3a: A(r, c) -= X(r,:) X(c,:)' for r >= o+16, o+8 <= c <= r, in 16 x 8 fragments
-      // (row group rg holds min(2 rg + 3, ncg) of them); two fragments in flight per warp
-      {
-        const int nrg = (kNB - 1 - o) / 16, ncg = (kNB - 8 - o) / 8;
-        int total = 0;
-        for (int rg = 0; rg < nrg; ++rg) total += min(2 * rg + 3, ncg);
-        for (int f = wid; f < total; f += 2 * kWarps) {
-          const bool two = f + kWarps < total;
-          int m0[2], n0[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            int ff = (u == 0 || !two) ? f : f + kWarps, rg = 0, cnt = min(3, ncg);
-            while (ff >= cnt) {
-              ff -= cnt;
-              ++rg;
-              cnt = min(2 * rg + 3, ncg);
-            }
-            m0[u] = o + 16 + 16 * rg;
-            n0[u] = o + 8 + 8 * ff;
-          }
-          double acc[2][4], af[2][2][2], bf[2][2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-#pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2) {
-              const int r = m0[u] + g + 8 * (e2 >> 1), c = n0[u] + 2 * t + (e2 & 1);
-              acc[u][e2] = (r < kNB && c <= r) ? a[r + c * kLD] : 0.0;
-            }
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int p = 4 * k + t;
-              af[u][k][0] = m0[u] + g < kNB ? -x[p * kXLD + m0[u] + g] : 0.0;
-              af[u][k][1] = m0[u] + g + 8 < kNB ? -x[p * kXLD + m0[u] + g + 8] : 0.0;
-              bf[u][k] = x[p * kXLD + n0[u] + g];
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) dmma1684(acc[u], af[u][k], bf[u][k]);
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (u == 1 && !two) break;
-#pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2) {
-              const int r = m0[u] + g + 8 * (e2 >> 1), c = n0[u] + 2 * t + (e2 & 1);
-              if (r < kNB && c <= r) a[r + c * kLD] = acc[u][e2];
-            }
-          }
-        }
-      }
-      TRACEW(140 + 2 * kb);
-      // S3b: B(r, c) += X(r,:) W(o:o+8, c) for r >= o+8, c < o+8; two fragments in flight
-      {
-        const int nrg = (kNB - 8 - o + 15) / 16, ncg = kb + 1, total = nrg * ncg;
-        for (int f = wid; f < total; f += 2 * kWarps) {
-          const bool two = f + kWarps < total;
-          int m0[2], n0[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int ff = (u == 0 || !two) ? f : f + kWarps;
-            const int rg = ff / ncg;
-            m0[u] = o + 8 + 16 * rg;
-            n0[u] = 8 * (ff - rg * ncg);
-          }
-          double acc[2][4], af[2][2][2], bf[2][2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-#pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2) {
-              const int r = m0[u] + g + 8 * (e2 >> 1), c = n0[u] + 2 * t + (e2 & 1);
-              acc[u][e2] = r < kNB ? w[r + c * kLD] : 0.0;
-            }
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int p = 4 * k + t;
-              af[u][k][0] = m0[u] + g < kNB ? x[p * kXLD + m0[u] + g] : 0.0;
-              af[u][k][1] = m0[u] + g + 8 < kNB ? x[p * kXLD + m0[u] + g + 8] : 0.0;
-              bf[u][k] = wsb[p * kXLD + n0[u] + g];
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) dmma1684(acc[u], af[u][k], bf[u][k]);
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (u == 1 && !two) break;
-#pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2) {
-              const int r = m0[u] + g + 8 * (e2 >> 1), c = n0[u] + 2 * t + (e2 & 1);
-              if (r < kNB) w[r + c * kLD] = acc[u][e2];
-            }
-          }
-        }
-      }
-      TRACEW(141 + 2 * kb);
-      // finished W rows of block kb; the panel L(r, o:o+8) = X below block kb+1
-      for (int e = wt; e < 8 * (o + 8); e += kW) {
-        const int i = e & 7, c = e >> 3;
-        w[(o + i) + c * kLD] = wsb[i * kXLD + c];
-      }
-      for (int e = wt; e < 8 * (kNB - 16 - o); e += kW) {
-        const int r = o + 16 + (e >> 3), p = e & 7;
-        a[r + (o + p) * kLD] = x[p * kXLD + r];
-      }
-      TRACEW(103 + 4 * kb);
-      if (kb < 6) bar_arrive_n(3, 224);
-    }
-  }
-  __syncthreads();
-  return *fls;
-}
-
-// inverse of every 64 x 64 diagonal block of an existing factor (one CTA per block)
-__global__ void __launch_bounds__(256) k_diag_inv(const double* __restrict__ L, int64_t n,
-                                                  double* __restrict__ Winv) {
-  extern __shared__ double sm[];
-  double* a = sm;
-  double* w = sm + kNB * kLD;
-  const int64_t k0 = (int64_t)blockIdx.x * kNB;
-  const int b = (int)(n - k0 < kNB ? n - k0 : kNB);
-  load_diag(L, n, k0, b, a);
-  __syncthreads();
-  inv64(a, w);
-  store_diag(nullptr, n, k0, b, a, w, Winv + (size_t)blockIdx.x * kNB * kNB, false);
-}
-
-constexpr int kTB = kNB * kGemmLD;    // doubles per staged 64 x 64 tile
-constexpr int kDfExt = 512;           // solve scratch after the staging buffers (doubles)
-constexpr int kDfSmem = (4 * kTB + kDfExt) * 8;  // two stages of (X, Y); the potf2 scratch aliases stage 0
+// shared memory (doubles)
+constexpr int kOffStage = 0;              // 2 stages x {X, Y}
+constexpr int kOffA = 4 * kTS;            // -acc of a panel / the factor's input and L
+constexpr int kOffW = 5 * kTS;            // a staged W / the new W of a diagonal tile
+constexpr int kOffP = 6 * kTS;            // the panel product
+constexpr int kOffCol = 7 * kTS;          // 32 x 32 finished factor columns (pivot chain)
+constexpr int kOffRR = kOffCol + kB * kB; // 1 / l_pp
+constexpr int kOffYs = kOffRR + kB;       // 2 staged y_k
+constexpr int kOffYp = kOffYs + 2 * kB;   // y_{d-1}
+constexpr int kOffTv = kOffYp + kB;       // b_d - sum_k L_dk y_k
+constexpr int kOffRed = kOffTv + kB;      // 4 x 32 quarter partial sums
+constexpr int kSmemDoubles = kOffRed + 4 * kB;
+constexpr int kDfSmem = kSmemDoubles * 8;
+static_assert((kOffCol * 8) % 16 == 0, "16-byte aligned factor columns");
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// polling load: relaxed (an acquire load compiles to LDG.STRONG + CCTL.IVALL, and a spinning
+// CTA's stream of L1 invalidations slows the shared-memory pipe of its SM neighbour, e.g. a
+// diagonal tile's pivot chain); the acquire fence follows once the flag is seen
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -510,353 +110,530 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
-// stage a packed 64 x 64 tile (column-major, 64 contiguous doubles per column) into
-// x[k * kGemmLD + i] with 16-byte cp.async (L2 only: tiles written by other CTAs)
+// 1/sqrt(x): MUFU.RSQ64H seed + two Newton steps (~1/3 the latency of the exact sequence);
+// flushes subnormals, so the caller re-factors exactly when a pivot leaves [1e-300, 1e300]
+__device__ __forceinline__ double rsqrt_mufu(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
+// stage a packed 32 x 32 tile (column-major, 32 contiguous doubles per column) into
+// x[k * kLD + i] with 16-byte cp.async (L2 only: tiles written by other CTAs)
 __device__ __forceinline__ void stage_tile(double* x, const double* src) {
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int ch = threadIdx.x + kDfThreads * u;
-    const int k = ch >> 5, i2 = (ch & 31) * 2;
-    cp_async16(x + k * kGemmLD + i2, src + k * kNB + i2);
+  for (int u = 0; u < 4; ++u) {
+    const int ch = threadIdx.x + kT * u;
+    const int k = ch >> 4, i2 = (ch & 15) * 2;
+    cp_async16(x + k * kLD + i2, src + k * kB + i2);
+  }
+}
+__device__ __forceinline__ void stage_vec(double* x, const double* src) {
+  if (threadIdx.x < 16) cp_async16(x + 2 * threadIdx.x, src + 2 * threadIdx.x);
+}
+
+// Warp w owns the 16 x 16 block (rows 16 (w & 1) + [0,16), columns 16 (w >> 1) + [0,16)) of a
+// 32 x 32 tile as two m16n8 fragments: acc[ni][e] is element
+// (16 (w & 1) + g + 8 (e >> 1), 16 (w >> 1) + 8 ni + 2 t + (e & 1)).
+struct Frag {
+  int m0, n0, g, t;
+  __device__ Frag() {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    m0 = 16 * (warp & 1);
+    n0 = 16 * (warp >> 1);
+    g = lane >> 2;
+    t = lane & 3;
+  }
+  __device__ int row(int e) const { return m0 + g + 8 * (e >> 1); }
+  __device__ int col(int ni, int e) const { return n0 + 8 * ni + 2 * t + (e & 1); }
+};
+
+// acc += X Y^T (k = 0..31) for this warp's block; X, Y staged as x[k * kLD + row]
+__device__ __forceinline__ void gemm_xyt(const Frag& f, const double* x, const double* y, double (&acc)[2][4]) {
+  const double* xa = x + f.t * kLD + f.m0 + f.g;
+  const double* yb = y + f.t * kLD + f.n0 + f.g;
+#pragma unroll
+  for (int ks = 0; ks < kB; ks += 4) {
+    const int o = ks * kLD;
+    const double af[2] = {xa[o], xa[o + 8]};
+    dmma1684(acc[0], af, yb[o]);
+    dmma1684(acc[1], af, yb[o + 8]);
   }
 }
 
-// acc += X Y^T (k = 0..63) for this warp's 32 x 16 block; 8 warps cover the 64 x 64 tile.
-// acc[mi][ni][e] holds element (32 wm + 16 mi + g + 8 (e >> 1), 16 wn + 8 ni + 2 t + (e & 1)).
-__device__ __forceinline__ void gemm_xyt(const double* x, const double* y, double (&acc)[2][2][4]) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const double* xa = x + t * kGemmLD + 32 * (warp & 1) + g;
-  const double* yb = y + t * kGemmLD + 16 * (warp >> 1) + g;
-#pragma unroll 4
-  for (int ks = 0; ks < kNB; ks += 4) {
-    const int o = ks * kGemmLD;
-    double af[2][2], bf[2];
-    af[0][0] = xa[o];
-    af[0][1] = xa[o + 8];
-    af[1][0] = xa[o + 16];
-    af[1][1] = xa[o + 24];
-    bf[0] = yb[o];
-    bf[1] = yb[o + 8];
+__device__ __forceinline__ void frag_store(const Frag& f, double* x, const double (&acc)[2][4], double sign) {
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+  for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) dmma1684(acc[mi][ni], af[mi], bf[ni]);
-  }
+    for (int e = 0; e < 4; ++e) x[f.col(ni, e) * kLD + f.row(e)] = sign * acc[ni][e];
 }
 
 struct DfArgs {
   const double* M;  // n x n, lower part read
   double* L;        // n x n column-major factor (lower tiles and diagonal tiles written)
-  double* Lt;       // nt x nt packed 64 x 64 tiles of L (off-diagonal tiles), read by other CTAs
-  double* W;        // nt packed 64 x 64 inverses of the diagonal tiles
+  double* Lt;       // nt x nt packed 32 x 32 tiles of L (off-diagonal tiles), read by other CTAs
+  double* W;        // nt packed 32 x 32 inverses of the diagonal tiles
   int64_t n;
   double delta;
-  int nt, ntiles;
+  int nt, ntasks;
   unsigned* flags;  // nt x nt per-tile done flags (== generation when done)
-  unsigned* ctl;    // [0] generation, [1] exit count, [2] failure generation, [3] pivot + 1, [4] tile counter
+  unsigned* ctl;    // [0] generation, [1] exit count, [2] failure generation, [3] pivot + 1, [4] task counter
   long long* info;
-  // fused triangular solves (rhs == nullptr: factor only). The diagonal tile i also forms
-  // y_i = W_i (b_i - sum_k L_ik y_k) while it streams L_ik; nt backward tasks follow the
-  // tiles: x_i = W_i' (y_i - sum_{j>i} L_ji' x_j), published through xflags.
-  const double* rhs;  // n
-  double* x;          // n (may alias rhs only if rhs is not read after the forward pass: it is not)
-  double* ybuf;       // nt * 64
-  double* xbuf;       // nt * 64
+  const double* rhs;  // n (nullptr: factor only)
+  double* x;          // n (may alias rhs: rhs is read before any block of x is written)
+  double* ybuf;       // nt * 32
+  double* xbuf;       // nt * 32
   unsigned* xflags;   // nt
   int nback;          // nt when solving, else 0
 };
 
-// thread 0: spin until both tile flags carry the generation; false on a published failure
+// thread 0: spin until both flags carry the generation; false on a published failure
 __device__ __forceinline__ bool wait_flags(const unsigned* f1, const unsigned* f2, const unsigned* fail,
                                            unsigned target) {
   while (true) {
-    if (ld_acquire(f1) == target && ld_acquire(f2) == target) return true;
-    if (ld_acquire(fail) == target) return false;
+    if (ld_relaxed(f1) == target && ld_relaxed(f2) == target) {
+      fence_acquire();
+      return true;
+    }
+    if (ld_relaxed(fail) == target) {
+      fence_acquire();
+      return false;
+    }
+  }
+}
+__device__ __forceinline__ unsigned* tile_flag(const DfArgs& A, int i, int j) { return A.flags + i * A.nt + j; }
+__device__ __forceinline__ const double* tile_src(const DfArgs& A, int i, int j) {
+  return A.Lt + ((size_t)i * A.nt + j) * (kB * kB);
+}
+__device__ __forceinline__ void publish(unsigned* flag, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flag, target);
   }
 }
 
-// one lower tile (i, j): left-looking updates, then potf2 + inverse (i == j) or the panel
-// product with W_j (i > j). Returns false when the factorization failed somewhere.
-__device__ bool df_tile(const DfArgs& A, int i, int j, unsigned target, double* sm, volatile unsigned* s_flag) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
-  const int nt = A.nt;
-  const int64_t n = A.n, r0 = (int64_t)kNB * i, c0 = (int64_t)kNB * j;
-  const bool diag = i == j;
-  const bool idle = diag && wm == 0 && wn >= 2;  // strictly upper 32 x 16 blocks of a diagonal tile
-  const unsigned* fl = A.flags;
+// acc = -(M block at (r0, c0)) (+ -delta on the diagonal); lower part only when diag
+__device__ __forceinline__ void load_neg_m(const Frag& f, const DfArgs& A, int64_t r0, int64_t c0, bool diag,
+                                           double (&acc)[2][4]) {
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = f.row(e), c = f.col(ni, e);
+      double v = 0.0;
+      if (r0 + r < A.n && c0 + c < A.n && (!diag || r >= c)) {
+        v = A.M[(r0 + r) + (c0 + c) * A.n];
+        if (diag && r == c && A.delta != 0.0) v = add(v, A.delta);
+      }
+      acc[ni][e] = -v;
+    }
+}
+
+// left-looking updates acc1 += L_{i,k} L_{j1,k}^T and (two) acc2 += L_{i,k} L_{j2,k}^T for
+// k < K, double-buffered (tile k+1 prefetched when already published); with fwd also the
+// forward-solve partial sum_k L_{i,k} y_k (thread: row tid & 31, columns of quarter tid >> 5).
+// Returns false on a published failure.
+template <bool TWO>
+__device__ bool left_updates(const DfArgs& A, const Frag& f, int i, int j1, int K, bool skip2, unsigned target,
+                             double* sm, volatile unsigned* s_flag, double (&acc1)[2][4], double (&acc2)[2][4],
+                             bool fwd, double& fpart) {
+  if (K <= 0) return true;
+  const int tid = threadIdx.x;
   const unsigned* failw = A.ctl + 2;
-  const bool fwd = diag && A.rhs != nullptr;
-  double* ext = sm + 4 * kTB;  // [0,128) y_k stages, [128,192) t_i, [192,448) quarter partials
-  const int fr = tid & 63, qd = tid >> 6;
-  double fpart = 0.0;
-
-  // acc = -(M_ij) (+ -delta on the diagonal), so the updates accumulate with DMMA's "+"
-  double acc[2][2][4];
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = 32 * wm + 16 * mi + g + 8 * (e >> 1), cl = 16 * wn + 8 * ni + 2 * t + (e & 1);
-        double v = 0.0;
-        if (r0 + r < n && c0 + cl < n && (!diag || r >= cl)) {
-          v = A.M[(r0 + r) + (c0 + cl) * n];
-          if (diag && r == cl && A.delta != 0.0) v = add(v, A.delta);
-        }
-        acc[mi][ni][e] = -v;
-      }
-
-  // A_ij -= sum_k L_ik L_jk^T, double-buffered: tile k+1 is prefetched when already published
-  if (j > 0) {
-    if (tid == 0) *s_flag = wait_flags(fl + i * nt, fl + j * nt, failw, target) ? 1u : 2u;
-    __syncthreads();
-    if (*s_flag == 2u) return false;
-    stage_tile(sm, A.Lt + ((size_t)i * nt) * (kNB * kNB));
-    if (!diag) stage_tile(sm + kTB, A.Lt + ((size_t)j * nt) * (kNB * kNB));
-    if (fwd && tid < 32) cp_async16(ext + 2 * tid, A.ybuf + 2 * tid);
+  // stage s: X at sm + 2 s kTS (rows i), Y at + kTS (rows j1)
+  if (tid == 0) *s_flag = wait_flags(tile_flag(A, i, 0), tile_flag(A, j1, 0), failw, target) ? 1u : 2u;
+  __syncthreads();
+  if (*s_flag == 2u) return false;
+  double* ys = sm + kOffYs;
+  stage_tile(sm, tile_src(A, i, 0));
+  stage_tile(sm + kTS, tile_src(A, j1, 0));
+  if (fwd) stage_vec(ys, A.ybuf);
+  cp_commit();
+  const int fr = tid & 31, qd = tid >> 5;
+  for (int k = 0; k < K; ++k) {
+    const int s = k & 1;
+    double* xs = sm + 2 * s * kTS;
+    double* xo = sm + 2 * (s ^ 1) * kTS;
+    const bool more = k + 1 < K;
+    if (tid == 0) {
+      const bool ready =
+          more && ld_relaxed(tile_flag(A, i, k + 1)) == target && ld_relaxed(tile_flag(A, j1, k + 1)) == target;
+      if (ready) fence_acquire();
+      *s_flag = ready ? 1u : 0u;
+    }
+    __syncthreads();  // buffer s^1 is free (gemm k-1 done); s_flag visible
+    const bool pre = *s_flag == 1u;
+    if (pre) {
+      stage_tile(xo, tile_src(A, i, k + 1));
+      stage_tile(xo + kTS, tile_src(A, j1, k + 1));
+      if (fwd) stage_vec(ys + kB * (s ^ 1), A.ybuf + kB * (k + 1));
+    }
     cp_commit();
-    for (int k = 0; k < j; ++k) {
-      const int s = k & 1;
-      double* xs = sm + 2 * s * kTB;
-      double* xo = sm + 2 * (s ^ 1) * kTB;
-      const bool more = k + 1 < j;
-      if (tid == 0)
-        *s_flag = (more && ld_acquire(fl + i * nt + k + 1) == target && ld_acquire(fl + j * nt + k + 1) == target)
-                      ? 1u : 0u;
-      __syncthreads();  // buffer s^1 is free (gemm k-1 done); s_flag visible
-      const bool pre = *s_flag == 1u;
-      if (pre) {
-        stage_tile(xo, A.Lt + ((size_t)i * nt + k + 1) * (kNB * kNB));
-        if (!diag) stage_tile(xo + kTB, A.Lt + ((size_t)j * nt + k + 1) * (kNB * kNB));
-        if (fwd && tid < 32) cp_async16(ext + 64 * (s ^ 1) + 2 * tid, A.ybuf + 64 * (k + 1) + 2 * tid);
-      }
-      cp_commit();
-      cp_wait1();
-      __syncthreads();  // tile k visible to every warp
-      if (!idle) gemm_xyt(xs, diag ? xs : xs + kTB, acc);
-      if (fwd) {  // forward substitution partial: sum_k L_ik y_k, quarter qd of the columns
-        const double* yk = ext + 64 * s;
+    cp_wait1();
+    __syncthreads();  // tile k visible to every warp
+    if (TWO) {
+      if (!skip2) gemm_xyt(f, xs, xs, acc2);   // the diagonal block's own update
+      gemm_xyt(f, xs, xs + kTS, acc1);
+    } else {
+      gemm_xyt(f, xs, xs + kTS, acc1);
+    }
+    if (fwd) {
+      const double* yk = ys + kB * s;
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) fpart = fma(xs[(16 * qd + kk) * kGemmLD + fr], yk[16 * qd + kk], fpart);
-      }
-      if (more && !pre) {
-        if (tid == 0) *s_flag = wait_flags(fl + i * nt + k + 1, fl + j * nt + k + 1, failw, target) ? 1u : 2u;
-        __syncthreads();
-        if (*s_flag == 2u) return false;
-        stage_tile(xo, A.Lt + ((size_t)i * nt + k + 1) * (kNB * kNB));
-        if (!diag) stage_tile(xo + kTB, A.Lt + ((size_t)j * nt + k + 1) * (kNB * kNB));
-        if (fwd && tid < 32) cp_async16(ext + 64 * (s ^ 1) + 2 * tid, A.ybuf + 64 * (k + 1) + 2 * tid);
-        cp_commit();
-      }
+      for (int kk = 0; kk < 8; ++kk) fpart = fma(xs[(8 * qd + kk) * kLD + fr], yk[8 * qd + kk], fpart);
+    }
+    if (more && !pre) {
+      if (tid == 0)
+        *s_flag = wait_flags(tile_flag(A, i, k + 1), tile_flag(A, j1, k + 1), failw, target) ? 1u : 2u;
+      __syncthreads();
+      if (*s_flag == 2u) return false;
+      stage_tile(xo, tile_src(A, i, k + 1));
+      stage_tile(xo + kTS, tile_src(A, j1, k + 1));
+      if (fwd) stage_vec(ys + kB * (s ^ 1), A.ybuf + kB * (k + 1));
+      cp_commit();
     }
   }
   __syncthreads();  // staging buffers free
-  if (fwd) {  // t_i = b_i - sum_k L_ik y_k (fixed-order quarter sums)
-    double* red = ext + 192;
-    red[qd * 64 + fr] = fpart;
-    __syncthreads();
-    if (tid < 64) {
-      const double bi = c0 + tid < n ? A.rhs[c0 + tid] : 0.0;
-      ext[128 + tid] = bi - ((red[tid] + red[64 + tid]) + (red[128 + tid] + red[192 + tid]));
-    }
-  }
+  return true;
+}
 
-  if (diag) {
-    double* a = sm;
-    const int b = (int)(n - c0 < kNB ? n - c0 : kNB);
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = 32 * wm + 16 * mi + g + 8 * (e >> 1), cl = 16 * wn + 8 * ni + 2 * t + (e & 1);
-          double v;
-          if (r >= b || cl >= b) v = (r == cl) ? 1.0 : 0.0;
-          else v = (r >= cl) ? -acc[mi][ni][e] : 0.0;
-          a[r + cl * kLD] = v;
-        }
-    __syncthreads();
-    TRACE(2);
-    double* w = sm + kNB * kLD;
-    const int f = diag_factor(a, w, w + kNB * kLD, b);
-    if (f >= 0) {
-      if (tid == 0) {
-        A.ctl[3] = (unsigned)(c0 + f + 1);
-        __threadfence();
-        st_release(A.ctl + 2, target);
-      }
-      return false;
-    }
-    double* Wj = A.W + (size_t)j * (kNB * kNB);
-    for (int e = tid; e < kNB * kNB; e += kDfThreads) {
-      const int r = e & 63, cl = e >> 6;
-      if (r < b && cl < b) A.L[(c0 + r) + (c0 + cl) * n] = (r >= cl) ? a[r + cl * kLD] : 0.0;
-      Wj[e] = (r >= cl) ? w[r + cl * kLD] : 0.0;
-    }
-    if (fwd) {  // y_i = W_i t_i (W lower), published with the tile flag
-      double* red = ext + 192;
-      const double* tv = ext + 128;
-      double s = 0.0;
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        const int c = 16 * qd + cc;
-        if (c <= fr) s = fma(w[fr + c * kLD], tv[c], s);
-      }
-      red[qd * 64 + fr] = s;
-      __syncthreads();
-      if (tid < 64) A.ybuf[c0 + tid] = (red[tid] + red[64 + tid]) + (red[128 + tid] + red[192 + tid]);
-    }
-  } else {
-    double* x = sm;
-    double* y = sm + kTB;
-    if (tid == 0) *s_flag = wait_flags(fl + j * nt + j, fl + j * nt + j, failw, target) ? 1u : 2u;
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = 32 * wm + 16 * mi + g + 8 * (e >> 1), cl = 16 * wn + 8 * ni + 2 * t + (e & 1);
-          x[cl * kGemmLD + r] = -acc[mi][ni][e];
-        }
-    __syncthreads();
-    if (*s_flag == 2u) return false;
-    stage_tile(y, A.W + (size_t)j * (kNB * kNB));
-    cp_commit();
-    cp_wait0();
-    __syncthreads();
-    double out[2][2][4];
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) out[mi][ni][e] = 0.0;
-    gemm_xyt(x, y, out);  // L_ij = A_ij W_j^T
-    __syncthreads();
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = 32 * wm + 16 * mi + g + 8 * (e >> 1), cl = 16 * wn + 8 * ni + 2 * t + (e & 1);
-          x[cl * kGemmLD + r] = out[mi][ni][e];
-        }
-    __syncthreads();
-    double* Lt = A.Lt + ((size_t)i * nt + j) * (kNB * kNB);
-    for (int e = tid; e < kNB * kNB; e += kDfThreads) {
-      const int r = e & 63, cl = e >> 6;
-      const double v = x[cl * kGemmLD + r];
-      Lt[e] = v;
-      if (r0 + r < n) A.L[(r0 + r) + (c0 + cl) * n] = v;
-    }
-  }
+// L_ij = (-acc) W_j^T: waits for diagonal j, stages W_j (and y_j into yprev when fwd), leaves
+// the product in the P region and writes it to Lt and L. Returns false on a failure.
+__device__ bool panel(const DfArgs& A, const Frag& f, int i, int j, unsigned target, double* sm,
+                      volatile unsigned* s_flag, const double (&acc)[2][4], bool fwd) {
+  const int tid = threadIdx.x;
+  if (tid == 0) *s_flag = wait_flags(tile_flag(A, j, j), tile_flag(A, j, j), A.ctl + 2, target) ? 1u : 2u;
+  frag_store(f, sm + kOffA, acc, -1.0);
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    st_release(A.flags + i * nt + j, target);
+  CTRACE(0, 7);
+  if (*s_flag == 2u) return false;
+  stage_tile(sm + kOffW, A.W + (size_t)j * (kB * kB));
+  if (fwd) stage_vec(sm + kOffYp, A.ybuf + kB * j);
+  cp_commit();
+  cp_wait0();
+  __syncthreads();
+  double out[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+  gemm_xyt(f, sm + kOffA, sm + kOffW, out);
+  frag_store(f, sm + kOffP, out, 1.0);
+  __syncthreads();
+  double* Lt = A.Lt + ((size_t)i * A.nt + j) * (kB * kB);
+  const int64_t r0 = (int64_t)kB * i, c0 = (int64_t)kB * j;
+  for (int e = tid; e < kB * kB; e += kT) {
+    const int r = e & 31, c = e >> 5;
+    const double v = sm[kOffP + c * kLD + r];
+    Lt[e] = v;
+    if (r0 + r < A.n) A.L[(r0 + r) + (c0 + c) * A.n] = v;
   }
   return true;
 }
 
-// backward block i: x_i = W_i' (y_i - sum_{j>i} L_ji' x_j), j from the last block down (the
-// tile L_ji is staged before x_j is awaited). Warp w owns columns 8w..8w+7; lanes split the
-// 64 rows, fixed-order warp sums.
+// warp 0: the 32 x 32 factor of a (column-major lower input, kLD) in place, row i in lane i's
+// registers. Pivot p: l_ip = a_ip / sqrt(a_pp); the next pivot a_{p+1,p+1} - l^2 is formed in
+// lane p+1 and shuffled to all lanes (the critical chain); column p goes to shared memory
+// (col) for the rank-1 update of every row and for warp 1's inverse. Returns the first
+// failing pivot (< b) or -1; *odd when a pivot left the fast rsqrt's range.
+#ifdef CMPC_CHOL_NOINLINE
+#define CHOL_FACTOR_INLINE __noinline__
+#else
+#define CHOL_FACTOR_INLINE
+#endif
+template <bool EXACT>
+__device__ CHOL_FACTOR_INLINE int factor_rows(double* a_sm, double* col, double* rr, volatile int* cnt, int b, bool* odd) {
+  const int lane = threadIdx.x & 31;
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = (c <= lane) ? a_sm[c * kLD + lane] : 0.0;
+  double dcur = __shfl_sync(kFull, a[0], 0);
+  int fail = -1;
+  bool bad = false;
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    if (fail < 0 && p < b && (!(dcur > 0.0) || !isfinite(dcur))) fail = p;
+    bad |= !(dcur >= 1e-300 && dcur <= 1e300);
+    const double r = EXACT ? 1.0 / sqrt(dcur) : rsqrt_mufu(dcur);
+    const double l = (lane >= p) ? a[p] * r : 0.0;
+    a[p] = l;
+    if (p < 31) {
+      const double dn = fma(-l, l, a[p + 1]);  // lane p+1: its next pivot
+      dcur = __shfl_sync(kFull, dn, p + 1);
+    }
+    col[p * kB + lane] = l;
+    if (lane == 0) rr[p] = r;
+    __syncwarp();
+    if (lane == 0) {
+#ifndef CMPC_CHOL_NOFENCE
+      __threadfence_block();
+#endif
+      *cnt = p + 1;
+    }
+#pragma unroll
+    for (int c = (p + 1) & ~1; c < 32; c += 2) {
+      const double2 lc = ld2(col + p * kB + c);
+      if (c > p) a[c] = fma(-l, lc.x, a[c]);
+      if (c + 1 > p) a[c + 1] = fma(-l, lc.y, a[c + 1]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a_sm[c * kLD + lane] = (c <= lane) ? a[c] : 0.0;
+  *odd = bad;
+  return fail;
+}
+
+// warp 1: W = L^{-1} column by column (lane c = column c), one pivot behind warp 0:
+// w_p = s_p / l_pp, s_i -= l_ip w_p (i > p). Column-major into w_sm.
+__device__ CHOL_FACTOR_INLINE void inverse_cols(double* w_sm, const double* col, const double* rr, volatile int* cnt) {
+  const int lane = threadIdx.x & 31;
+  double s[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    while (*cnt <= p) __nanosleep(20);
+#ifndef CMPC_CHOL_NOFENCE
+    __threadfence_block();
+#endif
+    const double wp = s[p] * rr[p];
+    s[p] = wp;
+#pragma unroll
+    for (int i = (p + 1) & ~1; i < 32; i += 2) {
+      const double2 lc = ld2(col + p * kB + i);
+      if (i > p) s[i] = fma(-lc.x, wp, s[i]);
+      if (i + 1 > p) s[i + 1] = fma(-lc.y, wp, s[i + 1]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) w_sm[lane * kLD + i] = (i >= lane) ? s[i] : 0.0;
+}
+
+// diagonal task d: the sub-diagonal panel L_{d,d-1} and the diagonal tile (see the header)
+__device__ bool df_diag(const DfArgs& A, int d, unsigned target, double* sm, volatile unsigned* s_flag,
+                        volatile int* cnt, volatile int* s_res) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Frag f;
+  const int64_t r0 = (int64_t)kB * d;
+  const bool fwd = A.rhs != nullptr;
+  const bool has_p = d >= 1;
+  const bool upper = warp == 2;  // rows 0..15 x columns 16..31: strictly upper in a diagonal tile
+  double accP[2][4], accD[2][4];
+  if (has_p) load_neg_m(f, A, r0, r0 - kB, false, accP);
+  load_neg_m(f, A, r0, r0, true, accD);
+  double fpart = 0.0;
+  CTRACE(d, 0);
+  if (!left_updates<true>(A, f, d, d - 1, d - 1, upper, target, sm, s_flag, accP, accD, fwd, fpart)) return false;
+  CTRACE(d, 1);
+  const int fr = tid & 31, qd = tid >> 5;
+  if (has_p) {
+    if (!panel(A, f, d, d - 1, target, sm, s_flag, accP, fwd)) return false;
+    publish(tile_flag(A, d, d - 1), target);
+    CTRACE(d, 2);
+    if (!upper) gemm_xyt(f, sm + kOffP, sm + kOffP, accD);
+    if (fwd) {
+      const double* yp = sm + kOffYp;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) fpart = fma(sm[kOffP + (8 * qd + kk) * kLD + fr], yp[8 * qd + kk], fpart);
+    }
+  }
+  double* red = sm + kOffRed;
+  double* tv = sm + kOffTv;
+  if (fwd) red[qd * kB + fr] = fpart;
+  const int b = (int)(A.n - r0 < kB ? A.n - r0 : kB);
+  // factor input: -accD, lower, identity padding beyond b
+  double* a_sm = sm + kOffA;
+  auto store_input = [&] {
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = f.row(e), c = f.col(ni, e);
+        double v;
+        if (r >= b || c >= b) v = (r == c) ? 1.0 : 0.0;
+        else v = (r >= c) ? -accD[ni][e] : 0.0;
+        a_sm[c * kLD + r] = v;
+      }
+  };
+  store_input();
+  if (tid == 0) *cnt = 0;
+  __syncthreads();
+  if (fwd && tid < kB) {
+    const double bi = r0 + tid < A.n ? A.rhs[r0 + tid] : 0.0;
+    tv[tid] = bi - ((red[tid] + red[kB + tid]) + (red[2 * kB + tid] + red[3 * kB + tid]));
+  }
+  double* col = sm + kOffCol;
+  double* rr = sm + kOffRR;
+  bool odd = false;
+  CTRACE(d, 3);
+  if (warp == 0) {
+    const int fl = factor_rows<false>(a_sm, col, rr, cnt, b, &odd);
+    if (lane == 0) {
+      s_res[0] = fl;
+      s_res[1] = odd ? 1 : 0;
+    }
+  } else if (warp == 1) {
+    inverse_cols(sm + kOffW, col, rr, cnt);
+  }
+  __syncthreads();
+  CTRACE(d, 6);
+  if (s_res[1]) {  // a pivot outside [1e-300, 1e300]: redo the tile with the exact square root
+    store_input();
+    if (tid == 0) *cnt = 0;
+    __syncthreads();
+    if (warp == 0) {
+      const int fl = factor_rows<true>(a_sm, col, rr, cnt, b, &odd);
+      if (lane == 0) s_res[0] = fl;
+    } else if (warp == 1) {
+      inverse_cols(sm + kOffW, col, rr, cnt);
+    }
+    __syncthreads();
+  }
+  CTRACE(d, 4);
+  const int fl = s_res[0];
+  if (fl >= 0) {
+    if (tid == 0) {
+      A.ctl[3] = (unsigned)(r0 + fl + 1);
+      __threadfence();
+      st_release(A.ctl + 2, target);
+    }
+    return false;
+  }
+  const double* w_sm = sm + kOffW;
+  if (fwd) {  // y_d = W_d t (W lower): quarter sums in a fixed order
+    double s = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const int c = 8 * qd + cc;
+      if (c <= fr) s = fma(w_sm[c * kLD + fr], tv[c], s);
+    }
+    __syncthreads();  // red reused
+    red[qd * kB + fr] = s;
+    __syncthreads();
+    if (tid < kB) A.ybuf[r0 + tid] = (red[tid] + red[kB + tid]) + (red[2 * kB + tid] + red[3 * kB + tid]);
+  }
+  double* Wd = A.W + (size_t)d * (kB * kB);
+  for (int e = tid; e < kB * kB; e += kT) {
+    const int r = e & 31, c = e >> 5;
+    if (r < b && c < b) A.L[(r0 + r) + (r0 + c) * A.n] = a_sm[c * kLD + r];
+    Wd[e] = w_sm[c * kLD + r];
+  }
+  publish(tile_flag(A, d, d), target);
+  CTRACE(d, 5);
+  CTRACE_FLUSH(d);
+  return true;
+}
+
+// panel task (i, j), i >= j + 2
+__device__ bool df_panel(const DfArgs& A, int i, int j, unsigned target, double* sm, volatile unsigned* s_flag) {
+  const Frag f;
+  double acc[2][4], unused[2][4];
+  CTRACE(64 + i * 64 + j, 0);
+  load_neg_m(f, A, (int64_t)kB * i, (int64_t)kB * j, false, acc);
+  double fpart = 0.0;
+  if (!left_updates<false>(A, f, i, j, j, true, target, sm, s_flag, acc, unused, false, fpart)) return false;
+  CTRACE(64 + i * 64 + j, 1);
+  if (!panel(A, f, i, j, target, sm, s_flag, acc, false)) return false;
+  publish(tile_flag(A, i, j), target);
+  CTRACE(64 + i * 64 + j, 2);
+  CTRACE_FLUSH(64 + i * 64 + j);
+  return true;
+}
+
+// backward block i: x_i = W_i^T (y_i - sum_{j>i} L_ji^T x_j), j from the last block down (the
+// tile L_ji is staged before x_j is awaited). Warp w owns columns 8w..8w+7; lane = row;
+// fixed-order warp sums.
 __device__ bool df_back(const DfArgs& A, int i, unsigned target, double* sm, volatile unsigned* s_flag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt = A.nt;
-  const unsigned* fl = A.flags;
   const unsigned* failw = A.ctl + 2;
-  // W_i and y_i are final once the diagonal tile is
-  if (tid == 0) *s_flag = wait_flags(fl + i * nt + i, fl + i * nt + i, failw, target) ? 1u : 2u;
+  CTRACE(2048 + i, 0);
+  if (tid == 0) *s_flag = wait_flags(tile_flag(A, i, i), tile_flag(A, i, i), failw, target) ? 1u : 2u;
   __syncthreads();
   if (*s_flag == 2u) return false;
-  const double* Wi = A.W + (size_t)i * (kNB * kNB);
-  double wv0[8], wv1[8];
+  const double* Wi = A.W + (size_t)i * (kB * kB);
+  double wv[8], part[8];
 #pragma unroll
   for (int cl = 0; cl < 8; ++cl) {
-    wv0[cl] = __ldcg(Wi + (8 * warp + cl) * kNB + lane);
-    wv1[cl] = __ldcg(Wi + (8 * warp + cl) * kNB + lane + 32);
+    wv[cl] = __ldcg(Wi + (8 * warp + cl) * kB + lane);
+    part[cl] = 0.0;
   }
-  double part[8];
-#pragma unroll
-  for (int cl = 0; cl < 8; ++cl) part[cl] = 0.0;
   for (int j = nt - 1; j > i; --j) {
-    if (tid == 0) *s_flag = wait_flags(fl + j * nt + i, fl + j * nt + i, failw, target) ? 1u : 2u;
+    double* xs = sm + (j & 1) * kTS;
+    if (tid == 0) *s_flag = wait_flags(tile_flag(A, j, i), tile_flag(A, j, i), failw, target) ? 1u : 2u;
     __syncthreads();
     if (*s_flag == 2u) return false;
-    stage_tile(sm, A.Lt + ((size_t)j * nt + i) * (kNB * kNB));
+    stage_tile(xs, tile_src(A, j, i));
     cp_commit();
     if (tid == 0) *s_flag = wait_flags(A.xflags + j, A.xflags + j, failw, target) ? 1u : 2u;
     cp_wait0();
     __syncthreads();
     if (*s_flag == 2u) return false;
-    const double x0 = __ldcg(A.xbuf + 64 * j + lane), x1 = __ldcg(A.xbuf + 64 * j + lane + 32);
+    const double xj = __ldcg(A.xbuf + kB * j + lane);
 #pragma unroll
-    for (int cl = 0; cl < 8; ++cl) {
-      const int c = 8 * warp + cl;
-      part[cl] = fma(sm[c * kGemmLD + lane], x0, part[cl]);
-      part[cl] = fma(sm[c * kGemmLD + lane + 32], x1, part[cl]);
-    }
-    __syncthreads();  // staging buffer reused by the next j
+    for (int cl = 0; cl < 8; ++cl) part[cl] = fma(xs[(8 * warp + cl) * kLD + lane], xj, part[cl]);
   }
-  double* accv = sm + 4 * kTB;  // 64
-  const double* yi = A.ybuf + 64 * i;
+  double* accv = sm + kOffTv;
+  const double* yi = A.ybuf + kB * i;
 #pragma unroll
   for (int cl = 0; cl < 8; ++cl) {
     const double s = warp_sum(part[cl]);
     if (lane == 0) accv[8 * warp + cl] = __ldcg(yi + 8 * warp + cl) - s;
   }
   __syncthreads();
-  const double a0 = accv[lane], a1 = accv[lane + 32];
-  const int64_t r0 = (int64_t)kNB * i;
+  const double a0 = accv[lane];
+  const int64_t r0 = (int64_t)kB * i;
 #pragma unroll
   for (int cl = 0; cl < 8; ++cl) {
     const int c = 8 * warp + cl;  // x(c) = sum_{r >= c} W(r, c) acc(r)
-    const double s = warp_sum(fma(wv0[cl], a0, wv1[cl] * a1));
+    const double s = warp_sum(wv[cl] * a0);
     if (lane == 0) {
-      A.xbuf[64 * i + c] = s;
+      A.xbuf[kB * i + c] = s;
       if (r0 + c < A.n) A.x[r0 + c] = s;
     }
   }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    st_release(A.xflags + i, target);
-  }
+  publish(A.xflags + i, target);
+  CTRACE(2048 + i, 1);
+  CTRACE_FLUSH(2048 + i);
   return true;
 }
 
-__global__ void __launch_bounds__(kDfThreads, 1) k_chol_df(const DfArgs A) {
+__global__ void __launch_bounds__(kT) k_chol_df(const DfArgs A) {
   extern __shared__ __align__(16) double sm_df[];
   __shared__ unsigned s_target, s_q, s_flag;
+  __shared__ int s_cnt, s_res[2];
   const int tid = threadIdx.x;
   if (tid == 0) s_target = *reinterpret_cast<volatile unsigned*>(A.ctl) + 1u;
   __syncthreads();
   const unsigned target = s_target;
-  TRACE(0);
+  CTRACE(4095, 0);
+  CTRACE_FLUSH(4095);
   while (true) {
     if (tid == 0) s_q = atomicAdd(A.ctl + 4, 1u);
     __syncthreads();
     const int q = (int)s_q;
-    if (q >= A.ntiles + A.nback) break;
-    if (q >= A.ntiles) {  // backward solve tasks, last block first
-      if (!df_back(A, A.nt - 1 - (q - A.ntiles), target, sm_df, &s_flag)) break;
-      continue;
+    if (q >= A.ntasks + A.nback) break;
+    bool ok;
+    if (q >= A.ntasks) {  // backward solve tasks, last block first
+      ok = df_back(A, A.nt - 1 - (q - A.ntasks), target, sm_df, &s_flag);
+    } else {
+      // column by column: the diagonal task of column j (it also forms L_{j,j-1}), then the
+      // panels (i, j), i >= j + 2
+      int j = 0, rem = q;
+      while (true) {
+        const int cnt = 1 + max(0, A.nt - j - 2);
+        if (rem < cnt) break;
+        rem -= cnt;
+        ++j;
+      }
+      if (rem == 0) ok = df_diag(A, j, target, sm_df, &s_flag, &s_cnt, s_res);
+      else ok = df_panel(A, j + 1 + rem, j, target, sm_df, &s_flag);
     }
-    int j = 0, rem = q;  // column-major enumeration of the lower tiles
-    while (rem >= A.nt - j) {
-      rem -= A.nt - j;
-      ++j;
-    }
-    if (!df_tile(A, j + rem, j, target, sm_df, &s_flag)) break;
+    if (!ok) break;
+    __syncthreads();
   }
-  TRACE(3);
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -873,30 +650,62 @@ __global__ void __launch_bounds__(kDfThreads, 1) k_chol_df(const DfArgs A) {
   }
 }
 
-// x = L^{-T} L^{-1} b with the 64 x 64 diagonal-block inverses W; one CTA of 512
-// threads; x may alias b. Forward: y_k = W_k (b_k - sum_{j<k} L_kj y_j); backward:
+// inverse of every 32 x 32 diagonal block of an existing factor (one warp per block)
+__global__ void __launch_bounds__(32) k_diag_inv(const double* __restrict__ L, int64_t n,
+                                                 double* __restrict__ Winv) {
+  __shared__ double a[kB][kB + 1];  // a[c][r] = L(k0 + r, k0 + c)
+  const int lane = threadIdx.x;
+  const int64_t k0 = (int64_t)blockIdx.x * kB;
+  const int b = (int)(n - k0 < kB ? n - k0 : kB);
+  for (int e = lane; e < kB * kB; e += 32) {
+    const int r = e & 31, c = e >> 5;
+    a[c][r] = (r < b && c < b) ? (r >= c ? L[(k0 + r) + (k0 + c) * n] : 0.0) : (r == c ? 1.0 : 0.0);
+  }
+  __syncwarp();
+  double s[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int p = 0; p < 32; ++p) {
+    const double wp = s[p] / a[p][p];
+    s[p] = wp;
+#pragma unroll
+    for (int i = p + 1; i < 32; ++i) s[i] = fma(-a[p][i], wp, s[i]);
+  }
+  double* W = Winv + (size_t)blockIdx.x * kB * kB + lane * kB;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) W[i] = (i >= lane) ? s[i] : 0.0;
+}
+
+// x = L^{-T} L^{-1} b with the 32 x 32 diagonal-block inverses W; one CTA of 512 threads;
+// x may alias b. Forward: y_k = W_k (b_k - sum_{j<k} L_kj y_j); backward:
 // x_k = W_k^T (y_k - sum_{i>k} L_ik^T x_i).
 __global__ void __launch_bounds__(512) k_trsv(const double* __restrict__ L,
                                               const double* __restrict__ W, const double* b,
                                               double* x, int64_t n) {
   extern __shared__ double xs[];
-  double* t = xs + n;  // 64 scratch
+  double* t = xs + n;  // 32 scratch
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int64_t i = tid; i < n; i += blockDim.x) xs[i] = b[i];
   __syncthreads();
-  const int64_t nb = (n + kNB - 1) / kNB;
-  const int row = tid >> 3, part = tid & 7;  // 64 rows x 8 parts
+  const int64_t nb = (n + kB - 1) / kB;
+  const int row = tid >> 4, part = tid & 15;  // 32 rows x 16 parts
+  auto sum16 = [](double s) {
+    s += __shfl_xor_sync(kFull, s, 1);
+    s += __shfl_xor_sync(kFull, s, 2);
+    s += __shfl_xor_sync(kFull, s, 4);
+    s += __shfl_xor_sync(kFull, s, 8);
+    return s;
+  };
   for (int64_t kb = 0; kb < nb; ++kb) {
-    const int64_t r0 = kb * kNB;
-    const int bs = (int)(n - r0 < kNB ? n - r0 : kNB);
-    const double* Wk = W + kb * kNB * kNB;
+    const int64_t r0 = kb * kB;
+    const int bs = (int)(n - r0 < kB ? n - r0 : kB);
+    const double* Wk = W + kb * kB * kB;
     // y_k = W_k b'_k (W lower: row i uses columns j <= i)
     double s = 0.0;
     if (row < bs)
-      for (int j = part; j <= row; j += 8) s += Wk[row + j * kNB] * xs[r0 + j];
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
+      for (int j = part; j <= row; j += 16) s += Wk[row + j * kB] * xs[r0 + j];
+    s = sum16(s);
     __syncthreads();
     if (part == 0 && row < bs) xs[r0 + row] = s;
     __syncthreads();
@@ -915,10 +724,10 @@ __global__ void __launch_bounds__(512) k_trsv(const double* __restrict__ L,
     __syncthreads();
   }
   for (int64_t kb = nb - 1; kb >= 0; --kb) {
-    const int64_t r0 = kb * kNB;
-    const int bs = (int)(n - r0 < kNB ? n - r0 : kNB);
+    const int64_t r0 = kb * kB;
+    const int bs = (int)(n - r0 < kB ? n - r0 : kB);
     const int64_t tail = r0 + bs;
-    const double* Wk = W + kb * kNB * kNB;
+    const double* Wk = W + kb * kB * kB;
     // t_i = y_i - sum_{p >= tail} L[p, i] x_p (column dots, one warp per column)
     for (int i = warp; i < bs; i += 16) {
       double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
@@ -938,10 +747,8 @@ __global__ void __launch_bounds__(512) k_trsv(const double* __restrict__ L,
     // x_k = W_k^T t: x_i = sum_{j >= i} W[j][i] t_j
     double s = 0.0;
     if (row < bs)
-      for (int j = row + part; j < bs; j += 8) s += Wk[j + row * kNB] * t[j];
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
+      for (int j = row + part; j < bs; j += 16) s += Wk[j + row * kB] * t[j];
+    s = sum16(s);
     if (part == 0 && row < bs) xs[r0 + row] = s;
     __syncthreads();
   }
@@ -953,7 +760,6 @@ void set_attrs(int device) {
   static std::once_flag flags[kMaxDevices];
   once_per_device(flags, device, [] {
     CMPC_CUDA(cudaFuncSetAttribute(k_chol_df, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
-    CMPC_CUDA(cudaFuncSetAttribute(k_diag_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotfSmem));
     CMPC_CUDA(cudaFuncSetAttribute(k_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   });
 }
@@ -961,17 +767,17 @@ void set_attrs(int device) {
 }  // namespace
 
 void chol_alloc(Ctx& c) {
-  const int64_t nb = ceil_div(std::max<int64_t>(c.n, 1), kNB);
-  c.Winv = dev_zeros<double>((size_t)nb * kNB * kNB, c.stream);
-  c.Lt = dev_zeros<double>((size_t)nb * nb * kNB * kNB, c.stream);
+  const int64_t nb = ceil_div(std::max<int64_t>(c.n, 1), kB);
+  c.Winv = dev_zeros<double>((size_t)nb * kB * kB, c.stream);
+  c.Lt = dev_zeros<double>((size_t)nb * nb * kB * kB, c.stream);
   c.df_flags = dev_zeros<unsigned>((size_t)nb * nb, c.stream);
   c.df_ctl = dev_zeros<unsigned>(8, c.stream);
-  c.df_y = dev_zeros<double>((size_t)nb * kNB, c.stream);
-  c.df_x = dev_zeros<double>((size_t)nb * kNB, c.stream);
+  c.df_y = dev_zeros<double>((size_t)nb * kB, c.stream);
+  c.df_x = dev_zeros<double>((size_t)nb * kB, c.stream);
   c.df_xflags = dev_zeros<unsigned>((size_t)nb, c.stream);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-  c.df_grid = sms;
+  c.df_grid = 2 * sms;  // two 74 KB CTAs per SM
 }
 
 void chol_free(Ctx& c) {
@@ -990,7 +796,7 @@ void launch_cholesky(Ctx& c, const double* M, double* L, double delta, const dou
     return;
   }
   set_attrs(c.device);
-  const int nt = (int)ceil_div(n, kNB);
+  const int nt = (int)ceil_div(n, kB);
   DfArgs a;
   a.M = M;
   a.L = L;
@@ -999,7 +805,7 @@ void launch_cholesky(Ctx& c, const double* M, double* L, double delta, const dou
   a.n = n;
   a.delta = delta;
   a.nt = nt;
-  a.ntiles = nt * (nt + 1) / 2;
+  a.ntasks = nt + (nt >= 2 ? (nt - 1) * (nt - 2) / 2 : 0);
   a.flags = c.df_flags;
   a.ctl = c.df_ctl;
   a.info = info;
@@ -1009,22 +815,21 @@ void launch_cholesky(Ctx& c, const double* M, double* L, double delta, const dou
   a.xbuf = c.df_x;
   a.xflags = c.df_xflags;
   a.nback = rhs ? nt : 0;
-  const int grid = std::min(a.ntiles + a.nback, c.df_grid);
-  k_chol_df<<<grid, kDfThreads, kDfSmem, c.stream>>>(a);
+  const int grid = std::min(a.ntasks + a.nback, c.df_grid);
+  k_chol_df<<<grid, kT, kDfSmem, c.stream>>>(a);
   CMPC_LAUNCHED();
 }
 
 void launch_factor_inverses(Ctx& c, const double* L) {
   if (c.n == 0) return;
-  set_attrs(c.device);
-  k_diag_inv<<<(unsigned)ceil_div(c.n, kNB), 256, kPotfSmem, c.stream>>>(L, c.n, c.Winv);
+  k_diag_inv<<<(unsigned)ceil_div(c.n, kB), 32, 0, c.stream>>>(L, c.n, c.Winv);
   CMPC_LAUNCHED();
 }
 
 void launch_chol_solve(Ctx& c, const double* L, const double* b, double* x) {
   if (c.n == 0) return;
   set_attrs(c.device);
-  const size_t sm = sizeof(double) * ((size_t)c.n + kNB);
+  const size_t sm = sizeof(double) * ((size_t)c.n + kB);
   if (sm > 200 * 1024) throw CudaError("chol_solve: n too large for the single-CTA TRSV");
   k_trsv<<<1, 512, sm, c.stream>>>(L, c.Winv, b, x, c.n);
   CMPC_LAUNCHED();
