@@ -131,13 +131,15 @@ struct Ctx {
   cudaGraphExec_t g_step = nullptr, g_next = nullptr;
   long long g_step_nodes = 0, g_next_nodes = 0;
   double g_tau = 0.0;
-  double* Winv = nullptr;    // inverses of the 64 x 64 diagonal blocks of L
-  double* Lt = nullptr;      // packed 64 x 64 off-diagonal tiles of L (dataflow Cholesky)
+  double* Winv = nullptr;    // inverses of the 32 x 32 diagonal blocks of L
+  double* Lt = nullptr;      // packed 32 x 32 off-diagonal tiles of L (dataflow Cholesky)
   unsigned* df_flags = nullptr;  // per-tile done flags (generation stamped)
-  unsigned* df_ctl = nullptr;    // generation, exit count, failure, pivot, tile counter
-  double* df_y = nullptr;        // fused forward-solve blocks (nt x 64)
-  double* df_x = nullptr;        // fused backward-solve blocks (nt x 64)
-  unsigned* df_xflags = nullptr; // backward block done flags
+  unsigned* df_ctl = nullptr;    // generation, exit count, failure, pivot, task counter
+  double* df_y = nullptr;        // fused forward-solve blocks (nt x 32)
+  double* df_part = nullptr;     // per diagonal block: the pre-accumulated A_{d,d-1}, A_dd and b_d - sum L y
+  unsigned* df_pflags = nullptr; // their done flags
+  double* df_x = nullptr;        // distributed backward solve (large n): solved blocks (nt x 32)
+  unsigned* df_xflags = nullptr; // their done flags
   int df_grid = 148;
   Packet* pk = nullptr;      // device packet
   Packet* pk_host = nullptr; // pinned, device-mapped mirror

@@ -11,28 +11,15 @@
 namespace cmpc {
 thread_local long long g_launches = 0;
 namespace {
-// the diagonal factor + inverse alone (one CTA), clock64 around it
-__global__ void __launch_bounds__(kT) k_factor_only(const double* M, int64_t n, double* out, long long* cyc) {
-  extern __shared__ __align__(16) double sm_fo[];
-  __shared__ int s_cnt;
-  double* a_sm = sm_fo + kOffA;
-  for (int rep = 0; rep < 3; ++rep) {
-    for (int e = threadIdx.x; e < kB * kB; e += kT) {
-      const int r = e & 31, c = e >> 5;
-      a_sm[c * kLD + r] = (r >= c) ? M[r + c * n] : 0.0;
-    }
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    const long long t0 = clock64();
-    bool odd = false;
-    int f = 0;
-    if (threadIdx.x < 32) f = factor_rows<false>(a_sm, sm_fo + kOffCol, sm_fo + kOffRR, &s_cnt, 32, &odd);
-    else if (threadIdx.x < 64) inverse_cols(sm_fo + kOffW, sm_fo + kOffCol, sm_fo + kOffRR, &s_cnt);
-    __syncthreads();
-    const long long t1 = clock64();
-    if (threadIdx.x == 0) cyc[rep] = t1 - t0 + 0 * f;
-  }
-  for (int e = threadIdx.x; e < kB * kB; e += kT) out[e] = a_sm[(e >> 5) * kLD + (e & 31)] + sm_fo[kOffW + e];
+// spine_back alone, one CTA, on the factor a previous launch left in Lt / W / ybuf
+__global__ void __launch_bounds__(256, 1) k_back_only(const DfArgs A, long long* cyc) {
+  extern __shared__ __align__(16) double sm_bo[];
+  __shared__ __align__(8) uint64_t full[kBSlots], empty[kBSlots];
+  __syncthreads();
+  const long long t0 = clock64();
+  spine_back(A, sm_bo, full, empty);
+  __syncthreads();
+  if (threadIdx.x == 0) *cyc = clock64() - t0;
 }
 }  // namespace
 }
@@ -73,14 +60,18 @@ int main(int argc, char** argv) {
   cudaEventElapsedTime(&ms, e0, e1);
   printf("n=%lld fused factor+solve: %.1f us per launch\n", (long long)n, ms * 1e3 / reps);
   {
-    long long* dcyc = dev_zeros<long long>(4, c.stream);
-    double* dout = dev_zeros<double>(1024, c.stream);
-    CMPC_CUDA(cudaFuncSetAttribute(k_factor_only, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
-    k_factor_only<<<1, kT, kDfSmem, c.stream>>>(dM, n, dout, dcyc);
-    CMPC_CUDA(cudaStreamSynchronize(c.stream));
-    long long cyc[3];
-    CMPC_CUDA(cudaMemcpy(cyc, dcyc, sizeof(cyc), cudaMemcpyDeviceToHost));
-    printf("factor_rows + inverse_cols alone: %lld %lld %lld cycles\n", cyc[0], cyc[1], cyc[2]);
+    const int nt = (int)((n + 31) / 32);
+    DfArgs a{};
+    a.M = dM; a.L = dL; a.Lt = c.Lt; a.W = c.Winv; a.n = n; a.nt = nt; a.ybuf = c.df_y; a.x = dx; a.rhs = db;
+    long long* dcyc = dev_zeros<long long>(1, c.stream);
+    CMPC_CUDA(cudaFuncSetAttribute(k_back_only, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
+    for (int r = 0; r < 3; ++r) {
+      k_back_only<<<1, 256, kDfSmem, c.stream>>>(a, dcyc);
+      long long cyc = 0;
+      CMPC_CUDA(cudaMemcpyAsync(&cyc, dcyc, 8, cudaMemcpyDeviceToHost, c.stream));
+      CMPC_CUDA(cudaStreamSynchronize(c.stream));
+      printf("spine_back alone: %.2f us\n", cyc / 1965.0);
+    }
   }
   std::vector<unsigned long long> tr(4096 * 10);
 #ifdef CMPC_CHOL_TRACE
@@ -88,20 +79,16 @@ int main(int argc, char** argv) {
 #else
   return 0;
 #endif
-  // slots: cycles from the stamp to the task's end; [8] = globaltimer at the end
-  const unsigned long long t0 = tr[4095 * 10 + 8];
+  // spine: clock64 per step (compute stamps 0-5 on SMSP of warp 0; I/O stamps 6, 7 on warp 4)
   const int nt = (int)((n + 31) / 32);
-  auto cyc_us = [](unsigned long long c) { return c / 1965.0; };
-  printf("diag d: end(us)  [us before the end:] start  updates-done  flag(d-1)-seen  panel-published  factor-start  factor-done(pass 1)  published\n");
-  for (int d = 0; d < nt; ++d) {
-    const unsigned long long* r = &tr[d * 10];
-    printf("%2d end %7.2f | start %6.2f upd %6.2f flag %6.2f panel %6.2f fstart %6.2f fdone %6.2f pub %6.2f\n", d,
-           (double)(r[8] - t0) * 1e-3, cyc_us(r[0]), cyc_us(r[1]), cyc_us(r[7]), cyc_us(r[2]), cyc_us(r[3]), cyc_us(r[6]), cyc_us(r[5]));
-  }
-  printf("backward i: end(us) duration\n");
-  for (int i = nt - 1; i >= 0; --i) {
-    const unsigned long long* r = &tr[(2048 + i) * 10];
-    printf("%2d %7.2f %6.2f\n", i, (double)(r[8] - t0) * 1e-3, cyc_us(r[0]));
-  }
+  const unsigned long long* sp = &tr[3000 * 10];
+  auto cy = [&](int k, int e) { return (double)((long long)sp[k * 8 + e] - (long long)sp[0]) / 1965.0; };
+  printf("spine (us from step 0 start): wait-in  in-ready  panel-done  factor-start  factor-done  step-done | io: k-2 gemm done | diag-published\n");
+  for (int k = 0; k < nt && k < 63; ++k)
+    printf("%2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f | %7.2f %7.2f\n", k, cy(k, 0), cy(k, 1), cy(k, 2), cy(k, 3), cy(k, 4),
+           cy(k, 5), cy(k, 6), cy(k, 7));
+  printf("backward: %.2f -> %.2f us\n", cy(63, 0), cy(63, 1));
+  printf("io: k  inputs-staged  pready-passed  sdone-passed\n");
+  for (int k = 0; k < nt && k < 31; ++k) printf("%2d %7.2f %7.2f %7.2f\n", k, cy(k + 32, 0), cy(k + 32, 1), cy(k + 32, 2));
   return 0;
 }
