@@ -81,6 +81,20 @@ int cmpc_solve_batch(cmpc_ctx** ctxs, int64_t count, const double* opts, int64_t
 int cmpc_solve_batch_affine(cmpc_ctx** ctxs, int nctx, int64_t count, const double* h_all,
                             const double* h0_all, const double* d_all, const double* opts,
                             int64_t max_iter, double* v_out, double* scal_out);
+/* Lockstep batch (config 5, refresh_initial_state semantics): `count` instances sharing the
+ * loaded H and J of `base` (kept alive by the caller) and differing in (h, h0, d), solved by
+ * ONE host loop whose kernels each cover every active instance (the reference solves them one
+ * by one: proj/src/verify.cpp:104-111 over proj/src/ipm.cpp:160-268 per instance). n <= 160.
+ * set_affine: h_all count x n, h0_all count, d_all count x m (host, row per instance).
+ * solve: v_out count x n (nullable), scal_out count x 14 (cmpc_solve's out_scalars: status,
+ * iterations, kkt, objective), stats (nullable) 6: batch iterations, device seconds, wall
+ * seconds, kernel launches, host syncs, device rounds. */
+typedef struct cmpc_batch cmpc_batch;
+int cmpc_batch_create(cmpc_ctx* base, int64_t count, cmpc_batch** out);
+int cmpc_batch_set_affine(cmpc_batch* b, const double* h_all, const double* h0_all, const double* d_all);
+int cmpc_batch_solve(cmpc_batch* b, const double* opts, int64_t max_iter, double* v_out, double* scal_out,
+                     double* stats);
+void cmpc_batch_destroy(cmpc_batch* b);
 /* Page-lock / release a host buffer (cudaHostRegister) used for repeated uploads */
 int cmpc_host_register(void* p, int64_t bytes);
 int cmpc_host_unregister(void* p);

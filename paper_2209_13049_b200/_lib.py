@@ -73,6 +73,10 @@ SIGNATURES = {
     "cmpc_host_unregister": (C.c_int, [C.c_void_p]),
     "cmpc_solve_batch_affine": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, D, D, D, D,
                                           C.c_int64, D, D]),
+    "cmpc_batch_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    "cmpc_batch_set_affine": (C.c_int, [C.c_void_p, D, D, D]),
+    "cmpc_batch_solve": (C.c_int, [C.c_void_p, D, C.c_int64, D, D, D]),
+    "cmpc_batch_destroy": (None, [C.c_void_p]),
     "cmpc_comm_unique_id": (C.c_int, [C.c_void_p]),
     "cmpc_ctx_attach_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int64]),
     "cmpc_ctx_detach_comm": (C.c_int, [C.c_void_p]),

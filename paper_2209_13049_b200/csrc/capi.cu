@@ -432,6 +432,59 @@ int cmpc_solve_batch_affine(cmpc_ctx** ctxs, int nctx, int64_t count, const doub
   return err.load();
 }
 
+struct cmpc_batch {
+  cmpc::BatchCtx* b = nullptr;
+  int device = 0;
+};
+
+int cmpc_batch_create(cmpc_ctx* base, int64_t count, cmpc_batch** out) {
+  return guard([&] {
+    if (!base || !out) throw DimError("null argument");
+    Ctx& c = base->c;
+    require_loaded(c);
+    CMPC_CUDA(cudaSetDevice(c.device));
+    auto* x = new cmpc_batch;
+    x->device = c.device;
+    try {
+      x->b = batch_create(c, count);
+    } catch (...) {
+      delete x;
+      throw;
+    }
+    *out = x;
+    return CMPC_OK;
+  });
+}
+
+int cmpc_batch_set_affine(cmpc_batch* b, const double* h_all, const double* h0_all, const double* d_all) {
+  return guard([&] {
+    if (!b || !b->b) throw DimError("null batch (closed?)");
+    CMPC_CUDA(cudaSetDevice(b->device));
+    batch_set_affine(*b->b, h_all, h0_all, d_all);
+    return CMPC_OK;
+  });
+}
+
+int cmpc_batch_solve(cmpc_batch* b, const double* opts, int64_t max_iter, double* v_out, double* scal_out,
+                     double* stats) {
+  return guard([&] {
+    if (!b || !b->b) throw DimError("null batch (closed?)");
+    CMPC_CUDA(cudaSetDevice(b->device));
+    batch_solve(*b->b, opts, max_iter, v_out, scal_out, stats);
+    return CMPC_OK;
+  });
+}
+
+void cmpc_batch_destroy(cmpc_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  try {
+    batch_destroy(b->b);
+  } catch (...) {
+  }
+  delete b;
+}
+
 // Page-lock a host buffer for the batch uploads (plain DMA instead of staged copies)
 int cmpc_host_register(void* p, int64_t bytes) {
   return guard([&] {

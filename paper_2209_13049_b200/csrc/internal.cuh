@@ -170,6 +170,24 @@ void syrk_plan(Ctx& c);
 // M(lower) = H + P' diag(omega) P + (singleton diagonal); writes full symmetric M when mirror
 void launch_condense(Ctx& c, bool mirror, bool with_rhs = false, cudaEvent_t after_syrk = nullptr);
 void syrk_free(Ctx& c);
+// lockstep batch (batch.cu): B instances sharing H and P, per-instance omega/q in prototype
+// space at stride s_proto, M (n x n lower), tq, rhs and r1 (n) at their natural strides
+struct BatchSyrk {
+  int4* units = nullptr;
+  int32_t* piece_ptr = nullptr;
+  int npieces = 0, nunits = 0, ntiles = 0;
+  int2* tiles = nullptr;
+  int32_t* tile_ptr = nullptr;
+  int32_t* tile_units = nullptr;
+  unsigned* ctl = nullptr;
+  double* partial = nullptr;
+  double* rhs_part = nullptr;
+  int64_t B = 0;
+};
+void syrk_plan_batch(Ctx& c, int64_t B, BatchSyrk& out, cudaStream_t st);
+void syrk_free_batch(BatchSyrk& b, cudaStream_t st);
+void launch_condense_batch(Ctx& c, BatchSyrk& bs, cudaStream_t st, const double* omega, const double* q,
+                           int64_t s_proto, double* M, double* tq, double* rhs, const double* r1);
 
 // ---- chol.cu
 // L = chol(M + delta I) (lower, upper zeroed); failing pivot+1 in c.pk->info; with rhs,
@@ -182,6 +200,13 @@ void chol_free(Ctx& c);
 void launch_factor_inverses(Ctx& c, const double* L);
 // x = L^{-T} L^{-1} b (in place on x allowed); uses the diagonal-block inverses
 void launch_chol_solve(Ctx& c, const double* L, const double* b, double* x);
+
+// ---- batch.cu (lockstep batch of instances sharing H and J)
+struct BatchCtx;
+BatchCtx* batch_create(Ctx& base, int64_t B);
+void batch_destroy(BatchCtx* b);
+void batch_set_affine(BatchCtx& b, const double* h, const double* h0, const double* d);
+void batch_solve(BatchCtx& b, const double* opts, int64_t max_iter, double* v_out, double* scal, double* stats);
 
 // ---- comm.cpp (NCCL, opened at run time)
 enum class CommType { f64, i64 };

@@ -60,6 +60,10 @@ struct SyrkArgs {
   double* rhs_part;          // per segment: 2 x 64 half-sums of P' q (diagonal segments)
   long long* prof;           // debug: per piece {start ns, end ns, smid}
   int static_sched;          // debug: CTA b takes pieces b, b + grid, ... (no counter)
+  // lockstep batch (batch.cu): piece g is piece g % ppi of instance g / ppi; per-instance
+  // omega, q, partial and rhs_part live at these strides (0, ppi = npieces: one instance)
+  int ppi;
+  int64_t s_omega, s_q, s_partial, s_rhs;
 };
 
 // byte offset of element (col c, k) inside a 32 x 64 operand tile (two swizzled boxes)
@@ -70,10 +74,10 @@ __device__ __forceinline__ uint32_t op_off(int c, int k) {
 
 // Segment epilogue: store the accumulators as the segment's partial tile.
 template <int NF>
-__device__ __forceinline__ void store_partial(const SyrkArgs& a, int sg,
+__device__ __forceinline__ void store_partial(const SyrkArgs& a, int inst, int sg,
                                               const double (&acc)[NF][2][4], const int* fr,
                                               const int* fn, int lane) {
-  double* out = a.partial + (size_t)sg * (kTile * kTile);
+  double* out = a.partial + inst * a.s_partial + (size_t)sg * (kTile * kTile);
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int f = 0; f < NF; ++f)
@@ -96,7 +100,7 @@ __device__ __forceinline__ void store_partial(const SyrkArgs& a, int sg,
 //   THIN (diagonal):     the lower-left 32x32 block           -> 1 per warp
 template <int NF, bool DIAG, bool THIN>
 __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* smem, uint64_t* full,
-                                             uint64_t* empty, int it0, int sg, const int4 u,
+                                             uint64_t* empty, int it0, int inst, int sg, const int4 u,
                                              int warp, int lane) {
   const int nsteps = (u.z - u.y) / kBK;
   const int g = lane >> 2, t = lane & 3;
@@ -194,8 +198,8 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  store_partial<NF>(a, sg, acc, fr, fn, lane);
-  if (DIAG && a.q) a.rhs_part[(size_t)sg * 128 + threadIdx.x] = rq[0] + rq[1];
+  store_partial<NF>(a, inst, sg, acc, fr, fn, lane);
+  if (DIAG && a.q) a.rhs_part[inst * a.s_rhs + (size_t)sg * 128 + threadIdx.x] = rq[0] + rq[1];
 }
 
 // 2 CTAs per SM: 168 registers (each SM sub-partition holds 3 warps of 168 x 32; the few
@@ -233,11 +237,14 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
       for (int i = 0;; ++i) {
         const int slot = i & 1;
         if (i >= 2) mbar_wait(&pempty[slot], ((i >> 1) & 1) ^ 1);
-        int p = a.static_sched ? (int)(blockIdx.x + (unsigned)i * gridDim.x) : (int)atomicAdd(a.ctl, 1u);
-        if (p >= a.npieces) p = -1;
-        ring[slot] = p;
+        int pg = a.static_sched ? (int)(blockIdx.x + (unsigned)i * gridDim.x) : (int)atomicAdd(a.ctl, 1u);
+        if (pg >= a.npieces) pg = -1;
+        ring[slot] = pg;
         mbar_arrive(&pfull[slot]);
-        if (p < 0) break;
+        if (pg < 0) break;
+        const int inst = pg / a.ppi, p = pg - inst * a.ppi;
+        const double* omega = a.omega + inst * a.s_omega;
+        const double* qv = a.q ? a.q + inst * a.s_q : nullptr;
         for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
           const int4 u = a.segs[sg];
           const int ti = u.x & 1023, tj = (u.x >> 10) & 1023;
@@ -265,8 +272,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
               tma_load_2d(st + kOpBytes, &tmP, kk, 64 * tj, &full[s]);
               tma_load_2d(st + kOpBytes + kBoxBytes, &tmP, kk + 16, 64 * tj, &full[s]);
             }
-            bulk_load(st + 2 * kOpBytes, a.omega + kk, kBK * 8, &full[s]);
-            if (with_q) bulk_load(st + 2 * kOpBytes + 256, a.q + kk, kBK * 8, &full[s]);
+            bulk_load(st + 2 * kOpBytes, omega + kk, kBK * 8, &full[s]);
+            if (with_q) bulk_load(st + 2 * kOpBytes + 256, qv + kk, kBK * 8, &full[s]);
           }
         }
       }
@@ -279,21 +286,22 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
   for (int i = 0;; ++i) {
     const int slot = i & 1;
     mbar_wait(&pfull[slot], (i >> 1) & 1);
-    const int p = ring[slot];
+    const int pg = ring[slot];
     __syncwarp();
     if (lane == 0) mbar_arrive(&pempty[slot]);
-    if (p < 0) break;
+    if (pg < 0) break;
+    const int inst = pg / a.ppi, p = pg - inst * a.ppi;
     long long t_start = 0;
     if (a.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
       const int4 u = a.segs[sg];
       const bool thin = (u.x >> 20) & 1, diag = (u.x & 1023) == ((u.x >> 10) & 1023);
       if (diag) {
-        if (thin) syrk_segment<1, true, true>(a, smem, full, empty, it0, sg, u, warp, lane);
-        else syrk_segment<3, true, false>(a, smem, full, empty, it0, sg, u, warp, lane);
+        if (thin) syrk_segment<1, true, true>(a, smem, full, empty, it0, inst, sg, u, warp, lane);
+        else syrk_segment<3, true, false>(a, smem, full, empty, it0, inst, sg, u, warp, lane);
       } else {
-        if (thin) syrk_segment<2, false, true>(a, smem, full, empty, it0, sg, u, warp, lane);
-        else syrk_segment<4, false, false>(a, smem, full, empty, it0, sg, u, warp, lane);
+        if (thin) syrk_segment<2, false, true>(a, smem, full, empty, it0, inst, sg, u, warp, lane);
+        else syrk_segment<4, false, false>(a, smem, full, empty, it0, inst, sg, u, warp, lane);
       }
       it0 += (u.z - u.y) / kBK;
     }
@@ -302,9 +310,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
       unsigned smid;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      a.prof[3 * p] = t_start;
-      a.prof[3 * p + 1] = t_end;
-      a.prof[3 * p + 2] = smid;
+      a.prof[3 * pg] = t_start;
+      a.prof[3 * pg + 1] = t_end;
+      a.prof[3 * pg + 2] = smid;
     }
   }
   // the last CTA out resets the piece counter for the next launch (every producer has made
@@ -327,6 +335,10 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
 // partials hold rows 0..31 only (flag bit 31 of their id); a warp's 32 elements share one
 // row half, so the skip is warp-uniform.
 constexpr int kRedWays = 4;
+// lockstep batch: instance blockIdx.z at these strides (all 0 for one instance)
+struct RedStrides {
+  int64_t partial, proto, rp, M, vec;
+};
 __global__ void __launch_bounds__(256)
     k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
                   const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ tile_segs,
@@ -334,8 +346,19 @@ __global__ void __launch_bounds__(256)
                   double* __restrict__ M, int mirror, const double* __restrict__ rp,
                   const double* __restrict__ qs, const int32_t* __restrict__ sing_ptr,
                   const double* __restrict__ sing_val, double* __restrict__ tq,
-                  double* __restrict__ rhs, const double* __restrict__ r1) {
+                  double* __restrict__ rhs, const double* __restrict__ r1, RedStrides bs) {
   __shared__ double red[kRedWays][64];
+  {
+    const int64_t b = blockIdx.z;
+    partial += b * bs.partial;
+    omega_s += b * bs.proto;
+    M += b * bs.M;
+    if (rp) rp += b * bs.rp;
+    qs += b * bs.proto;
+    tq += b * bs.vec;
+    rhs += b * bs.vec;
+    if (r1) r1 += b * bs.vec;
+  }
   const int2 tl = tiles[blockIdx.x];
   const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
   const int t64 = threadIdx.x & 63, way = threadIdx.x >> 6;
@@ -643,6 +666,8 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
   a.prof = c.syrk_prof;
   static const int stat = getenv("CMPC_SYRK_STATIC") ? atoi(getenv("CMPC_SYRK_STATIC")) : 0;
   a.static_sched = stat;
+  a.ppi = std::max(1, c.npieces);
+  a.s_omega = a.s_q = a.s_partial = a.s_rhs = 0;
   if (c.npieces > 0) {
     const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(c.tmap_P);
     const CUtensorMap* tm32 = reinterpret_cast<const CUtensorMap*>(c.tmap_P32);
@@ -659,7 +684,115 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
   k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 64), 64 * kRedWays, 0, c.stream>>>(
       c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr, c.omega + c.ldp, c.n, c.M,
       mirror ? 1 : 0, with_rhs ? c.rhs_part : nullptr, c.q + c.ldp, c.sing_ptr, c.sing_val, c.tq,
-      c.rhs, with_rhs && !c.comm ? c.r1 : nullptr);
+      c.rhs, with_rhs && !c.comm ? c.r1 : nullptr, RedStrides{0, 0, 0, 0, 0});
+  CMPC_LAUNCHED();
+}
+
+// ---------------------------------------------------------------- lockstep batch
+// The batch (batch.cu) shares P and its structure; with B instances there is parallelism
+// enough without splitting k, so every job (tile, shape) is one segment over its whole k
+// range and one piece, the pieces ordered by decreasing cost (largest first); partials per
+// instance: one per job.
+void syrk_plan_batch(Ctx& c, int64_t B, BatchSyrk& out, cudaStream_t st) {
+  syrk_free_batch(out, st);
+  const int64_t n = c.n;
+  const int nt = (int)ceil_div(n, kTile);
+  const int k_end = (int)c.ldp;
+  auto kstart = [&](int64_t col) {
+    if (c.ps == 0) return k_end;
+    return c.h_start_col[size_t(std::min<int64_t>(n, col))] / kBK * kBK;
+  };
+  struct Job { int tile, ti, tj, thin, kb, ke; double cost; };
+  std::vector<Job> jobs;
+  std::vector<int2> tiles;
+  for (int tj = 0; tj < nt; ++tj)
+    for (int ti = tj; ti < nt; ++ti) {
+      const int tile = (int)tiles.size();
+      tiles.push_back({ti, tj});
+      const int a0 = kstart((int64_t)kTile * ti), a1 = std::max(a0, kstart((int64_t)kTile * ti + 32));
+      const bool dg = ti == tj;
+      if (a1 > a0) jobs.push_back({tile, ti, tj, 1, a0, a1, (a1 - a0) * (dg ? kCostDiagThin : kCostThin)});
+      if (k_end > a1) jobs.push_back({tile, ti, tj, 0, a1, k_end, (k_end - a1) * (dg ? kCostDiag : kCostFull)});
+    }
+  std::vector<int> order(jobs.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return jobs[size_t(x)].cost > jobs[size_t(y)].cost; });
+  std::vector<int4> segs;
+  std::vector<int32_t> pptr{0};
+  std::vector<std::vector<int32_t>> per_tile(tiles.size());
+  for (int o : order) {
+    const Job& jb = jobs[size_t(o)];
+    const int id = (int)segs.size();
+    per_tile[size_t(jb.tile)].push_back(jb.thin ? (id | int(0x80000000u)) : id);
+    segs.push_back({jb.ti | jb.tj << 10 | jb.thin << 20, jb.kb, jb.ke, jb.tile});
+    pptr.push_back((int32_t)segs.size());
+  }
+  std::vector<int32_t> tptr(tiles.size() + 1, 0), tsegs;
+  for (size_t t = 0; t < tiles.size(); ++t) {
+    tptr[t + 1] = tptr[t] + (int32_t)per_tile[t].size();
+    for (int32_t u : per_tile[t]) tsegs.push_back(u);
+  }
+  out.B = B;
+  out.nunits = (int)segs.size();
+  out.npieces = (int)segs.size();
+  out.ntiles = (int)tiles.size();
+  out.units = dev_alloc<int4>(std::max<size_t>(1, segs.size()), st);
+  out.piece_ptr = dev_alloc<int32_t>(pptr.size(), st);
+  out.ctl = dev_zeros<unsigned>(2, st);
+  out.tiles = dev_alloc<int2>(tiles.size(), st);
+  out.tile_ptr = dev_alloc<int32_t>(tptr.size(), st);
+  out.tile_units = dev_alloc<int32_t>(std::max<size_t>(1, tsegs.size()), st);
+  out.partial = dev_alloc<double>((size_t)kTile * kTile * std::max<size_t>(1, segs.size()) * B, st);
+  out.rhs_part = dev_zeros<double>((size_t)128 * std::max<size_t>(1, segs.size()) * B, st);
+  if (!segs.empty())
+    CMPC_CUDA(cudaMemcpyAsync(out.units, segs.data(), sizeof(int4) * segs.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaMemcpyAsync(out.piece_ptr, pptr.data(), sizeof(int32_t) * pptr.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaMemcpyAsync(out.tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaMemcpyAsync(out.tile_ptr, tptr.data(), sizeof(int32_t) * tptr.size(), cudaMemcpyHostToDevice, st));
+  if (!tsegs.empty())
+    CMPC_CUDA(cudaMemcpyAsync(out.tile_units, tsegs.data(), sizeof(int32_t) * tsegs.size(), cudaMemcpyHostToDevice, st));
+  CMPC_CUDA(cudaStreamSynchronize(st));
+}
+
+void syrk_free_batch(BatchSyrk& b, cudaStream_t st) {
+  for (void* p : {(void*)b.units, (void*)b.piece_ptr, (void*)b.ctl, (void*)b.tiles, (void*)b.tile_ptr,
+                  (void*)b.tile_units, (void*)b.partial, (void*)b.rhs_part})
+    dev_free(p, st);
+  b = BatchSyrk{};
+}
+
+void launch_condense_batch(Ctx& c, BatchSyrk& bs, cudaStream_t st, const double* omega, const double* q,
+                           int64_t s_proto, double* M, double* tq, double* rhs, const double* r1) {
+  const int64_t B = bs.B;
+  if (bs.npieces > 0 && c.ps > 0) {
+    SyrkArgs a;
+    a.omega = omega;
+    a.q = q;
+    a.rhs_part = bs.rhs_part;
+    a.segs = bs.units;
+    a.piece_ptr = bs.piece_ptr;
+    a.npieces = (int)(bs.npieces * B);
+    a.ctl = bs.ctl;
+    a.partial = bs.partial;
+    a.prof = nullptr;
+    a.static_sched = 0;
+    a.ppi = bs.npieces;
+    a.s_omega = s_proto;
+    a.s_q = s_proto;
+    a.s_partial = (int64_t)bs.nunits * kTile * kTile;
+    a.s_rhs = (int64_t)bs.nunits * 128;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    const int grid = (int)std::min<int64_t>(a.npieces, 2 * sms);
+    const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(c.tmap_P);
+    const CUtensorMap* tm32 = reinterpret_cast<const CUtensorMap*>(c.tmap_P32);
+    k_syrk<<<grid, kSyrkThreads, kSyrkSmem, st>>>(*tm, *tm32, a);
+    CMPC_LAUNCHED();
+  }
+  const RedStrides rs{(int64_t)bs.nunits * kTile * kTile, s_proto, (int64_t)bs.nunits * 128, c.n * c.n, c.n};
+  k_syrk_reduce<<<dim3(bs.ntiles, kTile * kTile / 64, (unsigned)B), 64 * kRedWays, 0, st>>>(
+      bs.partial, bs.tiles, bs.tile_ptr, bs.tile_units, c.H, omega + c.ldp, c.n, M, 0,
+      c.ps > 0 ? bs.rhs_part : nullptr, q + c.ldp, c.sing_ptr, c.sing_val, tq, rhs, r1, rs);
   CMPC_LAUNCHED();
 }
 

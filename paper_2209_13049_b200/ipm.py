@@ -491,26 +491,58 @@ class BatchResult:
     wall_seconds: float
 
 
+LOCKSTEP_MAX_N = 160  # csrc/batch.cu keeps each instance's condensed matrix in shared memory
+
+
 class BatchSolver:
     """Independent instances that share H and J and differ in (h, h0, d) — the
     receding-horizon / config-5 case (refresh_initial_state, reduction.cpp:270-280).
-    A few worker device contexts (cloned from the base QP's analysed structure, one host
-    thread and one CUDA stream each) take the instances in turn inside the library; each
-    instance's (h, h0, d) is uploaded into the worker's context before its solve."""
 
-    def __init__(self, base: DenseQp, count: int, workers: int | None = None):
+    mode "lockstep" (the default when n <= 160 and J has rows): ONE host loop drives every
+    instance, each kernel covering all active instances in one launch (csrc/batch.cu: the
+    condensation's SYRK with an instance dimension over the shared P, one CTA per instance
+    for the Cholesky, DGEMMs for the products with P and H); every instance still takes the
+    reference's decisions (ipm.cpp:160-268) on its own scalars.
+    mode "workers": a few worker device contexts (cloned from the base QP's analysed
+    structure, one host thread and one CUDA stream each) take the instances in turn, each
+    running the single-instance loop."""
+
+    def __init__(self, base: DenseQp, count: int, workers: int | None = None, mode: str = "auto"):
         import os
         self.base = base
         self.count = count
-        # one core stays free for the driver and the interpreter
-        self.workers = max(1, min(count, workers or max(1, (os.cpu_count() or 2) - 1)))
-        root = device_qp(base)
-        self.ctxs = [root.clone() for _ in range(self.workers)]
-        root.close()
+        if mode == "auto":
+            mode = "lockstep" if (0 < base.m and base.n <= LOCKSTEP_MAX_N) else "workers"
+        if mode not in ("lockstep", "workers"):
+            raise ValueError(f"unknown batch mode: {mode}")
+        self.mode = mode
         self.h_all = np.repeat(f64(base.h).reshape(1, -1), count, axis=0)
         self.h0_all = np.full(count, float(base.h0))
         self.d_all = np.repeat(f64(base.d).reshape(1, -1), count, axis=0)
         self._pinned = []
+        self.ctxs = []
+        self._batch = None
+        self._root = None
+        if mode == "lockstep":
+            self.workers = 1
+            self._root = DeviceQp(base)
+            h = C.c_void_p()
+            check(_lib.lib().cmpc_batch_create(self._root.h, int(count), C.byref(h)))
+            self._batch = h
+            self._dirty = True
+        else:
+            # workers per process: the cores this process may use (under torchrun every rank
+            # gets its share of the host, not all of it), one left for the interpreter
+            try:
+                cores = len(os.sched_getaffinity(0))
+            except AttributeError:
+                cores = os.cpu_count() or 2
+            local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+            cores = max(1, cores // max(1, local))
+            self.workers = max(1, min(count, workers or max(1, cores - 1)))
+            root = device_qp(base)
+            self.ctxs = [root.clone() for _ in range(self.workers)]
+            root.close()
         for a in (self.h_all, self.d_all):  # page-locked: the per-instance uploads are plain DMA
             if a.nbytes and _lib.lib().cmpc_host_register(a.ctypes.data, a.nbytes) == 0:
                 self._pinned.append(a)
@@ -519,11 +551,31 @@ class BatchSolver:
         self.h_all[i] = np.asarray(h, dtype=np.float64)
         self.h0_all[i] = float(h0)
         self.d_all[i] = np.asarray(d, dtype=np.float64)
+        self._dirty = True
 
     def solve(self, opts: IpmOptions = None, threads: int | None = None) -> BatchResult:
         opts = opts or IpmOptions()
         _check_options(opts)
         n, cnt = self.base.n, self.count
+        if self.mode == "lockstep":
+            L = _lib.lib()
+            if self._dirty:
+                check(L.cmpc_batch_set_affine(self._batch, ptr(self.h_all), ptr(self.h0_all), ptr(self.d_all)))
+                self._dirty = False
+            v = np.zeros((cnt, n))
+            scal = np.zeros((cnt, 14))
+            stats = np.zeros(6)
+            od = (C.c_double * 5)(opts.tol, opts.mu_init, opts.kappa_mu, opts.tau, opts.armijo_eta)
+            t0 = time.perf_counter()
+            check(L.cmpc_batch_solve(self._batch, od, int(opts.max_iter), ptr(v), ptr(scal), ptr(stats)))
+            wall = time.perf_counter() - t0
+            self.last_stats = dict(batch_iterations=int(stats[0]), device_seconds=float(stats[1]),
+                                   wall_seconds=float(stats[2]), launches=int(stats[3]),
+                                   syncs=int(stats[4]), rounds=int(stats[5]))
+            return BatchResult(status=[IpmStatus(int(x)).name for x in scal[:, 0]], iter=scal[:, 1].astype(int),
+                               objective=scal[:, 3].copy(), kkt_error=scal[:, 2].copy(), v=v,
+                               device_seconds=np.full(cnt, float(stats[1]) / cnt), launches=int(stats[3]),
+                               wall_seconds=wall)
         nw = max(1, min(self.workers, threads or self.workers))
         v = np.zeros((cnt, n))
         scal = np.zeros((cnt, 14))
@@ -539,7 +591,16 @@ class BatchSolver:
                            wall_seconds=wall)
 
     def close(self):
-        for c in self.ctxs:
+        if getattr(self, "_batch", None) is not None:
+            try:
+                _lib.lib().cmpc_batch_destroy(self._batch)
+            except (AttributeError, TypeError):  # interpreter shutdown
+                pass
+            self._batch = None
+        if getattr(self, "_root", None) is not None:
+            self._root.close()
+            self._root = None
+        for c in getattr(self, "ctxs", []):
             c.close()
         self.ctxs = []
         for a in getattr(self, "_pinned", []):

@@ -20,10 +20,10 @@ def instances(data, count, seed=5):
     return base, out
 
 
-def test_batch_matches_single_solves_and_oracle(O):
+def test_worker_batch_matches_single_solves_bitwise(O):
     data = P.heat2d_problem(10, 8, T=12, splits=([5], [5], [4], [4]))
     base, insts = instances(data, 12)
-    bs = ipm.BatchSolver(base, len(insts))
+    bs = ipm.BatchSolver(base, len(insts), mode="workers")
     for i, q in enumerate(insts):
         bs.set_instance(i, q.h, q.h0, q.d)
     res = bs.solve(threads=4)
@@ -37,19 +37,50 @@ def test_batch_matches_single_solves_and_oracle(O):
     bs.close()
 
 
+def test_lockstep_batch_matches_single_solves_and_oracle(O):
+    # the lockstep batch (csrc/batch.cu) takes every decision of ipm.cpp:160-268 per instance:
+    # same iterations and barrier sequence as the oracle, iterates within the north-star 1e-8
+    data = P.heat2d_problem(10, 8, T=12, splits=([5], [5], [4], [4]))
+    base, insts = instances(data, 12)
+    bs = ipm.BatchSolver(base, len(insts))
+    assert bs.mode == "lockstep"
+    for i, q in enumerate(insts):
+        bs.set_instance(i, q.h, q.h0, q.d)
+    res = bs.solve()
+    assert all(s == "converged" for s in res.status)
+    for i, q in enumerate(insts):
+        single = ipm.solve(q)
+        assert res.iter[i] == single.iter and rel(res.v[i], single.v) <= 1e-10
+        assert abs(res.objective[i] - single.objective) <= 1e-10 * (1 + abs(single.objective))
+        o = O.solve(oracle_qp(O, q))
+        assert res.iter[i] == o.iter and rel(res.v[i], o.v) <= 1e-8
+        assert abs(res.objective[i] - o.objective) <= 1e-8 * (1 + abs(o.objective))
+        assert abs(res.kkt_error[i] - o.kkt_error) <= 1e-9 * (1 + abs(o.kkt_error))
+    # a second solve after new instance data reuses the batch context
+    for i, q in enumerate(insts[:3]):
+        bs.set_instance(i, insts[-1 - i].h, insts[-1 - i].h0, insts[-1 - i].d)
+    res2 = bs.solve()
+    for i in range(3):
+        assert res2.iter[i] == res.iter[len(insts) - 1 - i]
+        assert rel(res2.v[i], res.v[len(insts) - 1 - i]) <= 1e-12
+    bs.close()
+
+
 def test_config5_batch_slice():
     data = P.heat2d_problem(20, 25, T=30)
     base, insts = instances(data, 8, seed=11)
-    bs = ipm.BatchSolver(base, len(insts))
-    for i, q in enumerate(insts):
-        bs.set_instance(i, q.h, q.h0, q.d)
-    res = bs.solve(threads=2)  # two workers: each solves several instances in turn
-    assert all(s == "converged" for s in res.status)
-    for i in (0, 3, 7):
-        single = ipm.solve(insts[i])
-        assert res.iter[i] == single.iter and rel(res.v[i], single.v) <= 1e-14
-        # h0 differs per instance; a worker context replays graphs captured for an earlier one
-        assert abs(res.objective[i] - single.objective) <= 1e-12 * (1 + abs(single.objective))
+    for mode in ("lockstep", "workers"):
+        bs = ipm.BatchSolver(base, len(insts), mode=mode)
+        for i, q in enumerate(insts):
+            bs.set_instance(i, q.h, q.h0, q.d)
+        res = bs.solve(threads=2)
+        assert all(s == "converged" for s in res.status)
+        for i in (0, 3, 7):
+            single = ipm.solve(insts[i])
+            tol = 1e-14 if mode == "workers" else 1e-10
+            assert res.iter[i] == single.iter and rel(res.v[i], single.v) <= tol
+            assert abs(res.objective[i] - single.objective) <= 1e-10 * (1 + abs(single.objective))
+        bs.close()
 
 
 def test_batch_solvers_can_be_created_again_on_the_same_base():
@@ -60,7 +91,7 @@ def test_batch_solvers_can_be_created_again_on_the_same_base():
     base, insts = instances(data, 6)
     iters = []
     for _ in range(3):
-        bs = ipm.BatchSolver(base, len(insts), workers=3)
+        bs = ipm.BatchSolver(base, len(insts), workers=3, mode="workers")
         for i, q in enumerate(insts):
             bs.set_instance(i, q.h, q.h0, q.d)
         res = bs.solve()
