@@ -331,43 +331,48 @@ __global__ void k_b_sing_t(int64_t n, int64_t py, int64_t ldp, const int32_t* __
 
 // Cholesky of M_b + delta_b I in shared memory (one CTA per instance; the reference's pivot
 // rule "!(d > 0) || !isfinite(d)", proj/src/dense_linalg.cpp:24-40, first failure reported as
-// info = pivot + 1) and, when it succeeds, x = L^{-T} L^{-1} rhs_b.
-__global__ void __launch_bounds__(kBT) k_b_chol(int n, const double* __restrict__ M, const double* __restrict__ delta,
+// info = pivot + 1) and, when it succeeds, x = L^{-T} L^{-1} rhs_b. The right-hand side rides
+// along as an extra matrix row (row n of every column), so the forward solve is the rank-one
+// updates' own by-product; one barrier per pivot: step j updates the trailing matrix with the
+// raw column j scaled by 1/d_j, and scales column j (to l_ij = a_ij / sqrt(d_j)) in step j+1,
+// when nothing reads it any more.
+constexpr int kCholT = 1024;  // the matrix fills the SM's shared memory (one CTA per SM): all the warps it can hold
+__global__ void __launch_bounds__(kCholT) k_b_chol(int n, const double* __restrict__ M, const double* __restrict__ delta,
                                                 const double* __restrict__ rhs, double* __restrict__ x, Packet* pk,
                                                 const int* __restrict__ act) {
   extern __shared__ double bsm[];
-  const int ld = n + 1;
-  double* a = bsm;            // a[j * ld + i], i >= j
-  double* y = bsm + n * ld;   // n: rhs -> y -> x
+  const int ld = n + 2;       // rows 0..n-1: the matrix, row n: the right-hand side
+  double* a = bsm;            // a[j * ld + i], i >= j (and i = n)
+  double* xs = bsm + n * ld;  // n
   __shared__ int s_fail;
   const int64_t b = blockIdx.x;
   if (!act[b]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double dl = delta[b];
   const double* Mb = M + b * (int64_t)n * n;
-  for (int e = tid; e < n * n; e += kBT) {
+  for (int e = tid; e < n * n; e += kCholT) {
     const int i = e % n, j = e / n;
     if (i >= j) a[j * ld + i] = (i == j && dl != 0.0) ? add(Mb[i + (int64_t)j * n], dl) : Mb[i + (int64_t)j * n];
   }
-  for (int i = tid; i < n; i += kBT) y[i] = rhs[b * n + i];
+  for (int j = tid; j < n; j += kCholT) a[j * ld + n] = rhs[b * n + j];
   if (tid == 0) s_fail = -1;
   __syncthreads();
-  const int cc = tid >> 4, rr = tid & 15;  // half-warps run down one column: conflict-free rows
+  const int cc = tid >> 5, rr = lane;  // one warp per column, lanes down 32 consecutive rows
   for (int j = 0; j < n; ++j) {
     const double d = a[j * ld + j];
     if (!(d > 0.0) || !isfinite(d)) {  // uniform: every thread reads the same pivot
       if (tid == 0) s_fail = j;
       break;
     }
-    const double ljj = sqrt(d);
-    __syncthreads();  // every thread has read the pivot
-    if (tid == 0) a[j * ld + j] = ljj;
-    for (int i = j + 1 + tid; i < n; i += kBT) a[j * ld + i] = dv(a[j * ld + i], ljj);
-    __syncthreads();
-    // trailing update a(i, k) -= l_ij l_kj, j < k <= i
-    for (int k = j + 1 + cc; k < n; k += 16) {
-      const double lkj = a[j * ld + k];
-      for (int i = k + rr; i < n; i += 16) a[k * ld + i] = fma(-a[j * ld + i], lkj, a[k * ld + i]);
+    const double ri = dv(1.0, d);
+    if (j > 0) {  // column j-1 is final: scale it (nothing reads it in this step)
+      const double lp = sqrt(a[(j - 1) * ld + (j - 1)]);
+      for (int i = j + tid; i <= n; i += kCholT) a[(j - 1) * ld + i] = dv(a[(j - 1) * ld + i], lp);
+    }
+    // a(i, k) -= a_ij a_kj / d_j, j < k <= i (i = n: the right-hand side row)
+    for (int k = j + 1 + cc; k < n; k += kCholT / 32) {
+      const double lkj = mul(a[j * ld + k], ri);
+      for (int i = k + rr; i <= n; i += 32) a[k * ld + i] = fma(-a[j * ld + i], lkj, a[k * ld + i]);
     }
     __syncthreads();
   }
@@ -376,26 +381,25 @@ __global__ void __launch_bounds__(kBT) k_b_chol(int n, const double* __restrict_
     if (tid == 0) pk[b].info = s_fail + 1;
     return;
   }
-  // forward: y_j = y_j / l_jj, y_i -= l_ij y_j (i > j)
-  for (int j = 0; j < n; ++j) {
-    if (tid == 0) y[j] = dv(y[j], a[j * ld + j]);
+  {  // the last column, then the diagonal: l_jj = sqrt(d_j) (the columns were scaled by it)
+    const double lp = sqrt(a[(n - 1) * ld + (n - 1)]);
+    if (tid == 0) a[(n - 1) * ld + n] = dv(a[(n - 1) * ld + n], lp);
     __syncthreads();
-    const double yj = y[j];
-    for (int i = j + 1 + tid; i < n; i += kBT) y[i] = fma(-a[j * ld + i], yj, y[i]);
+    for (int j = tid; j < n; j += kCholT) a[j * ld + j] = sqrt(a[j * ld + j]);
     __syncthreads();
   }
-  // backward: x_j = (y_j - sum_{i>j} l_ij x_i) / l_jj, one warp
+  // y_j = a[j][n] (= (L^{-1} rhs)_j); backward: x_j = (y_j - sum_{i>j} l_ij x_i) / l_jj, one warp
   if (warp == 0) {
     for (int j = n - 1; j >= 0; --j) {
       double s = 0.0;
-      for (int i = j + 1 + lane; i < n; i += 32) s = fma(a[j * ld + i], y[i], s);
+      for (int i = j + 1 + lane; i < n; i += 32) s = fma(a[j * ld + i], xs[i], s);
       s = warp_sum(s);
-      if (lane == 0) y[j] = dv(sub(y[j], s), a[j * ld + j]);
+      if (lane == 0) xs[j] = dv(sub(a[j * ld + n], s), a[j * ld + j]);
       __syncwarp();
     }
   }
   __syncthreads();
-  for (int i = tid; i < n; i += kBT) x[b * n + i] = y[i];
+  for (int i = tid; i < n; i += kCholT) x[b * n + i] = xs[i];
   if (tid == 0) pk[b].info = 0;
 }
 
@@ -613,7 +617,7 @@ BatchCtx* batch_create(Ctx& base, int64_t B) {
     CMPC_CUDA(cudaMallocHost(&b->hstage, sizeof(double) * 4 * B));
     CMPC_CUDA(cudaMallocHost(&b->istage, sizeof(int) * B));
     CMPC_CUDA(cudaFuncSetAttribute(k_b_chol, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(double) * (kBatchMaxN * (kBatchMaxN + 1) + kBatchMaxN))));
+                                   (int)(sizeof(double) * (kBatchMaxN * (kBatchMaxN + 2) + kBatchMaxN))));
     syrk_plan_batch(base, B, b->syrk, b->st);
     if (cublas().create(&b->blas) != 0) throw CudaError("batch: cublasCreate failed");
     cublas().set_stream(b->blas, b->st);
@@ -762,8 +766,8 @@ struct Host {
   }
   void cholesky() {
     phase("chol", [&] {
-      const size_t sm = sizeof(double) * ((size_t)b.n * (b.n + 1) + b.n);
-      k_b_chol<<<(unsigned)b.B, kBT, sm, b.st>>>((int)b.n, b.M, b.delta, b.rhs, b.pv, b.pk, b.act);
+      const size_t sm = sizeof(double) * ((size_t)b.n * (b.n + 2) + b.n);
+      k_b_chol<<<(unsigned)b.B, kCholT, sm, b.st>>>((int)b.n, b.M, b.delta, b.rhs, b.pv, b.pk, b.act);
       CMPC_LAUNCHED();
     });
   }
