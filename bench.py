@@ -444,6 +444,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
     if world > 1 and args.impl != "reference":
+        from paper_2209_13049_b200.ipm import NCCL_DETERMINISM
+        for k, v in NCCL_DETERMINISM.items():  # before any communicator exists
+            os.environ.setdefault(k, v)
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)

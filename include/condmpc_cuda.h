@@ -90,6 +90,12 @@ int cmpc_solve_batch_affine(cmpc_ctx** ctxs, int nctx, int64_t count, const doub
  * iterations, kkt, objective), stats (nullable) 6: batch iterations, device seconds, wall
  * seconds, kernel launches, host syncs, device rounds. */
 typedef struct cmpc_batch cmpc_batch;
+/* In-process loopback communicator (tests): `nranks` contexts on one device, each driven by
+ * its own host thread, behave like the ranks of an NCCL communicator in the row-sharded solve
+ * (every allreduce is reduced in rank order on the device). attach: as cmpc_ctx_attach_comm. */
+int cmpc_loop_create(int nranks, int device, void** group);
+void cmpc_loop_destroy(void* group);
+int cmpc_ctx_attach_loop(cmpc_ctx* ctx, void* group, int rank, int64_t m_total);
 int cmpc_batch_create(cmpc_ctx* base, int64_t count, cmpc_batch** out);
 int cmpc_batch_set_affine(cmpc_batch* b, const double* h_all, const double* h0_all, const double* d_all);
 int cmpc_batch_solve(cmpc_batch* b, const double* opts, int64_t max_iter, double* v_out, double* scal_out,

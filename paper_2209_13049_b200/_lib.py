@@ -77,6 +77,9 @@ SIGNATURES = {
     "cmpc_batch_set_affine": (C.c_int, [C.c_void_p, D, D, D]),
     "cmpc_batch_solve": (C.c_int, [C.c_void_p, D, C.c_int64, D, D, D]),
     "cmpc_batch_destroy": (None, [C.c_void_p]),
+    "cmpc_loop_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "cmpc_loop_destroy": (None, [C.c_void_p]),
+    "cmpc_ctx_attach_loop": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64]),
     "cmpc_comm_unique_id": (C.c_int, [C.c_void_p]),
     "cmpc_ctx_attach_comm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int64]),
     "cmpc_ctx_detach_comm": (C.c_int, [C.c_void_p]),

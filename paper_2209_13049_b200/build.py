@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libcondmpc_cuda.so")
 ROOT = os.path.dirname(HERE)
 
 SOURCES = ["structure.cu", "syrk.cu", "chol.cu", "vec.cu", "batch.cu", "builder.cu", "capi.cu", "ipm_host.cpp", "comm.cpp",
-           "upload.cpp"]
+           "comm_loop.cu", "upload.cpp"]
 HEADERS = ["common.cuh", "internal.cuh", "ptx.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",

@@ -535,6 +535,35 @@ int cmpc_ctx_attach_comm(cmpc_ctx* x, const void* id128, int nranks, int rank, i
   });
 }
 
+int cmpc_loop_create(int nranks, int device, void** group) {
+  return guard([&] {
+    if (!group) throw DimError("null argument");
+    *group = comm_loop_create(nranks, device);
+    return CMPC_OK;
+  });
+}
+
+void cmpc_loop_destroy(void* group) {
+  try {
+    comm_loop_destroy(group);
+  } catch (...) {
+  }
+}
+
+int cmpc_ctx_attach_loop(cmpc_ctx* x, void* group, int rank, int64_t m_total) {
+  return guard([&] {
+    if (!x || !group) throw DimError("null argument");
+    Ctx& c = x->c;
+    require_loaded(c);
+    if (m_total < c.m) throw DimError("m_total is smaller than this shard's rows");
+    CMPC_CUDA(cudaStreamSynchronize(c.stream));
+    drop_graphs(c);
+    comm_loop_attach(c, group, rank);
+    c.m_all = m_total;
+    return CMPC_OK;
+  });
+}
+
 int cmpc_ctx_detach_comm(cmpc_ctx* x) {
   return guard([&] {
     if (!x) throw DimError("null context (closed?)");

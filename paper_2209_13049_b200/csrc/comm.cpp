@@ -8,12 +8,15 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstring>
 #include <mutex>
 #include <string>
 
 #include "internal.cuh"
 
 namespace cmpc {
+
+
 
 namespace {
 
@@ -76,26 +79,38 @@ void comm_attach(Ctx& c, const void* id128, int nranks, int rank) {
   c.comm = comm;
   c.nranks = nranks;
   c.rank = rank;
+  comm_buffers(c);
+}
+
+void comm_buffers(Ctx& c) {
+  if (c.n > 0 && !c.Mpack) c.Mpack = dev_alloc<double>((size_t)(c.n * (c.n + 1) / 2), c.stream);
 }
 
 void comm_detach(Ctx& c) {
-  if (c.comm) {
+  if (c.comm && !c.comm_loop) {
     cudaStreamSynchronize(c.stream);
     api().CommDestroy(static_cast<ncclComm_t>(c.comm));
   }
+  if (c.comm_loop) cudaStreamSynchronize(c.stream);  // the group outlives its ranks
   c.comm = nullptr;
+  c.comm_loop = false;
   c.nranks = 1;
   c.rank = 0;
 }
 
 void comm_allreduce(Ctx& c, void* buf, size_t count, CommType type, CommOp op) {
   if (!c.comm || count == 0) return;
+  if (c.comm_loop) {
+    comm_loop_allreduce(c, buf, count, type, op);
+    return;
+  }
   const ncclDataType_t dt = type == CommType::f64 ? ncclFloat64 : ncclInt64;
   const ncclRedOp_t ro = op == CommOp::sum ? ncclSum : (op == CommOp::max ? ncclMax : ncclMin);
   check(api().AllReduce(buf, buf, count, dt, ro, static_cast<ncclComm_t>(c.comm), c.stream), "AllReduce");
 }
 
-void comm_group(bool start) {
+void comm_group(Ctx& c, bool start) {
+  if (!c.comm || c.comm_loop) return;
   check(start ? api().GroupStart() : api().GroupEnd(), start ? "GroupStart" : "GroupEnd");
 }
 

@@ -54,7 +54,8 @@ struct ProblemDev;
 struct Ctx {
   int device = 0;
   // row-sharded solve (comm.cpp): this context holds rows of J; partial sums are allreduced
-  void* comm = nullptr;  // ncclComm_t
+  void* comm = nullptr;  // ncclComm_t, or the LoopGroup when comm_loop
+  bool comm_loop = false;  // in-process loopback communicator (tests: N ranks on one GPU)
   int nranks = 1, rank = 0;
   int64_t m_all = -1;    // rows of the whole QP (kkt scaling); -1 = m
   cudaStream_t stream = nullptr;
@@ -110,6 +111,7 @@ struct Ctx {
   double *Hv = nullptr, *Jtl = nullptr, *y = nullptr, *sigma = nullptr, *omega = nullptr,
          *q = nullptr, *rhs = nullptr, *M = nullptr, *L = nullptr;
   double* tq = nullptr;  // J'(r2 - sigma r3) of the step (the SYRK's fused right-hand side part)
+  double* Mpack = nullptr;  // sharded: the lower triangle of M packed for the allreduce
   // J'lambda carried along: the recovery forms J' p_lambda = (M - H) pv - tq,
   // the accepted step adds alpha J' p_lambda to Jtl, and the residual pass skips its J pass
   double* JtPl = nullptr;
@@ -216,7 +218,14 @@ void comm_attach(Ctx& c, const void* id128, int nranks, int rank);
 void comm_detach(Ctx& c);
 // in-place allreduce on c.stream (no-op without a communicator)
 void comm_allreduce(Ctx& c, void* buf, size_t count, CommType type, CommOp op);
-void comm_group(bool start);
+void comm_group(Ctx& c, bool start);
+// loopback communicator: N contexts on one device, one host thread each (comm.cpp)
+void* comm_loop_create(int nranks, int device);
+void comm_loop_destroy(void* group);
+void comm_loop_attach(Ctx& c, void* group, int rank);
+void comm_loop_allreduce(Ctx& c, void* buf, size_t count, CommType type, CommOp op);
+// the sharded solve's packed-M buffer (allocated when a communicator attaches)
+void comm_buffers(Ctx& c);
 inline int64_t rows_all(const Ctx& c) { return c.m_all >= 0 ? c.m_all : c.m; }
 
 // ---- vec.cu
@@ -275,6 +284,8 @@ void launch_Hx(Ctx& c, const double* x, double* out);
 // stand-alone fraction_to_boundary minima into out[2] (device)
 void launch_fraction_to_boundary(cudaStream_t st, int64_t m, const double* s, const double* ps,
                                  const double* z, const double* pz, double tau, double* out);
+// pack (to_packed) / unpack the lower triangle of the n x n column-major M
+void launch_pack_lower(Ctx& c, double* M, double* packed, bool to_packed);
 void vec_alloc(Ctx& c);
 void vec_free(Ctx& c);
 

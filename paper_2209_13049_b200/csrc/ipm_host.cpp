@@ -91,10 +91,13 @@ void seg_step(Ctx& c, double tau) {
   launch_condense(c, false, fused, c.ev4);
   rec(c.ev3, c.stream);
   if (c.comm) {  // M = H + sum_g J_g' Sigma_g J_g and J' (r2 - sigma r3) over all ranks
-    comm_group(true);
-    comm_allreduce(c, c.M, (size_t)(c.n * c.n), CommType::f64, CommOp::sum);
+    // only the lower triangle is formed (and factored): it travels packed, n (n + 1) / 2
+    launch_pack_lower(c, c.M, c.Mpack, true);
+    comm_group(c, true);
+    comm_allreduce(c, c.Mpack, (size_t)(c.n * (c.n + 1) / 2), CommType::f64, CommOp::sum);
     comm_allreduce(c, c.tq, (size_t)c.n, CommType::f64, CommOp::sum);
-    comm_group(false);
+    comm_group(c, false);
+    launch_pack_lower(c, c.M, c.Mpack, false);
   }
   if (c.comm || !fused) launch_rhs_final(c);  // (unsharded + fused: done by k_syrk_reduce)
   launch_debug_sum(c, c.M, c.n * c.n, 0);
@@ -126,7 +129,9 @@ void run_segment(Ctx& c, cudaGraphExec_t& exec, long long& nodes, bool allow_cap
     ++c.pub_expect;  // every segment graph ends with one k_publish
     return;
   }
-  if (!allow_capture || getenv("CMPC_NO_GRAPHS")) {
+  // (a loopback communicator synchronizes the ranks' streams with events across contexts,
+  // which a per-context capture cannot hold)
+  if (!allow_capture || c.comm_loop || getenv("CMPC_NO_GRAPHS")) {
     seg();
     return;
   }

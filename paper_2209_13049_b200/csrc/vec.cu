@@ -892,7 +892,26 @@ void pinned_give(void* p) {
 }
 }  // namespace
 
+// column j of the lower triangle at packed offset j n - j (j - 1) / 2
+__global__ void k_pack_lower(int64_t n, double* __restrict__ M, double* __restrict__ pk, int to_packed) {
+  const int64_t j = blockIdx.y;
+  const int64_t base = j * n - j * (j - 1) / 2;
+  for (int64_t i = j + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (to_packed) pk[base + (i - j)] = M[i + j * n];
+    else M[i + j * n] = pk[base + (i - j)];
+  }
+}
+
+void launch_pack_lower(Ctx& c, double* M, double* packed, bool to_packed) {
+  if (c.n == 0) return;
+  if (!packed) throw CudaError("pack_lower: no packed buffer (allocated when a communicator attaches)");
+  k_pack_lower<<<dim3((unsigned)std::min<int64_t>(8, ceil_div(c.n, 256)), (unsigned)c.n), 256, 0, c.stream>>>(
+      c.n, M, packed, to_packed ? 1 : 0);
+  CMPC_LAUNCHED();
+}
+
 void vec_alloc(Ctx& c) {
+  if (c.comm) comm_buffers(c);  // a sharded context reloaded with its communicator attached
   const size_t n = (size_t)c.n, m = (size_t)c.m;
   const size_t py = (size_t)(c.ldp + c.pz);  // prototype-indexed arrays
   const bool verbose = getenv("CMPC_VERBOSE") != nullptr;
@@ -978,7 +997,7 @@ void vec_free(Ctx& c) {
                   (void*)c.omega, (void*)c.q, (void*)c.tq, (void*)c.JtPl, (void*)c.rhs, (void*)c.M,
                   (void*)c.L, (void*)c.pv, (void*)c.ps_, (void*)c.pl, (void*)c.pzd, (void*)c.Jpv,
                   (void*)c.vt, (void*)c.yt, (void*)c.yv, (void*)c.Hvt, (void*)c.part, (void*)c.colpart,
-                  (void*)c.hmax, (void*)c.pk, (void*)c.d_mu, (void*)c.d_alpha})
+                  (void*)c.hmax, (void*)c.pk, (void*)c.d_mu, (void*)c.d_alpha, (void*)c.Mpack})
     dev_free(p, c.stream);
   if (c.pk_host) {
     CMPC_CUDA(cudaStreamSynchronize(c.stream));  // no staged upload still reading the ring
@@ -1001,6 +1020,7 @@ void vec_free(Ctx& c) {
   c.Jpv = c.vt = c.yt = c.yv = c.Hvt = c.part = c.colpart = c.hmax = c.d_mu = c.d_alpha = nullptr;
   c.pk = nullptr;
   c.pk_host = nullptr;
+  c.Mpack = nullptr;
 }
 
 // one warp: packet -> mapped host memory, then the sequence number (system-scope fence
@@ -1153,11 +1173,11 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
     k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part,
                                            c.hmax, c.pk, 1);
     CMPC_LAUNCHED();
-    comm_group(true);
+    comm_group(c, true);
     comm_allreduce(c, c.Jtl, (size_t)c.n, CommType::f64, CommOp::sum);
     comm_allreduce(c, &c.pk->sum_log_s, 2, CommType::f64, CommOp::sum);  // sum_log_s, sum_abs_r3
     comm_allreduce(c, &c.pk->max_r3, 5, CommType::f64, CommOp::max);     // max_r3 .. max_z
-    comm_group(false);
+    comm_group(c, false);
   }
   k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part,
                                          c.hmax, c.pk, c.comm ? 2 : 0);
@@ -1249,10 +1269,10 @@ void launch_recover(Ctx& c, double tau) {
                                              c.pk);
   CMPC_LAUNCHED();
   if (c.comm) {  // step-length minima and sum ps/s over every rank's rows
-    comm_group(true);
+    comm_group(c, true);
     comm_allreduce(c, &c.pk->alpha_s_min, 2, CommType::f64, CommOp::min);
     comm_allreduce(c, &c.pk->d_ps_s, 1, CommType::f64, CommOp::sum);
-    comm_group(false);
+    comm_group(c, false);
   }
 }
 
@@ -1290,10 +1310,10 @@ void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear) {
                                            c.part, c.pk);
   CMPC_LAUNCHED();
   if (c.comm) {  // merit row sums and the slack-positivity flag over every rank's rows
-    comm_group(true);
+    comm_group(c, true);
     comm_allreduce(c, &c.pk->t_sum_log, 2, CommType::f64, CommOp::sum);
     comm_allreduce(c, &c.pk->any_nonpos, 1, CommType::i64, CommOp::max);
-    comm_group(false);
+    comm_group(c, false);
   }
 }
 

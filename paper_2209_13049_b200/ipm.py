@@ -255,6 +255,9 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+NCCL_DETERMINISM = {"NCCL_ALGO": "Ring", "NCCL_PROTO": "Simple"}
+
+
 class ShardedQp:
     """This rank's part of a row-sharded QP: rows `rows` of J and d (from
     problem.shard_rows) on this process's GPU, attached to an NCCL communicator over all
@@ -263,7 +266,13 @@ class ShardedQp:
     rank, with s, lambda, z for this rank's rows."""
 
     def __init__(self, qp: DenseQp, rows, uid: bytes, nranks: int, rank: int):
+        import os
         from .problem import shard_qp
+        # a fixed reduction algorithm and protocol: NCCL's choice may change with the message
+        # size or topology, and with it the summation order (bitwise reproducible solves,
+        # proj/tests/test_ipm.cpp:432-457); must be set before the communicator exists
+        for k, v in NCCL_DETERMINISM.items():
+            os.environ.setdefault(k, v)
         self.rows = np.asarray(rows, dtype=np.int64)
         self.m_total = qp.m
         self.local = shard_qp(qp, self.rows)
@@ -292,6 +301,58 @@ class ShardedQp:
         if getattr(self, "dq", None) is not None:
             self.dq.close()
             self.dq = None
+
+
+class LoopbackShards:
+    """The row-sharded solve (ShardedQp's C++ loop and kernels) with `nranks` ranks inside one
+    process on one GPU: the shards (problem.shard_rows) are attached to an in-process loopback
+    communicator instead of NCCL, and solve() drives every rank from its own host thread, as
+    torchrun would drive one process per GPU. Tests of the multi-rank path without a multi-GPU
+    node; the results of every rank are returned."""
+
+    def __init__(self, qp: DenseQp, nranks: int, device: int | None = None):
+        from .problem import shard_qp, shard_rows
+        device = _linalg.DEVICE if device is None else device
+        L = _lib.lib()
+        g = C.c_void_p()
+        check(L.cmpc_loop_create(int(nranks), int(device), C.byref(g)))
+        self.group = g
+        self.rows = shard_rows(qp, nranks)
+        self.locals = [shard_qp(qp, r) for r in self.rows]
+        self.dqs = [DeviceQp(loc, device=device) for loc in self.locals]
+        for r, dq in enumerate(self.dqs):
+            check(L.cmpc_ctx_attach_loop(dq.h, self.group, r, int(qp.m)))
+        self.nranks = nranks
+
+    def solve(self, opts: IpmOptions = None) -> list:
+        import threading
+        opts = opts or IpmOptions()
+        _check_options(opts)
+        out = [None] * self.nranks
+        errs = []
+
+        def run(r):
+            try:
+                out[r] = solve_loaded(self.dqs[r], self.locals[r], opts)
+            except Exception as e:  # re-raised in the caller
+                errs.append(e)
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(self.nranks)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+        return out
+
+    def close(self):
+        for dq in getattr(self, "dqs", []):
+            dq.close()
+        self.dqs = []
+        if getattr(self, "group", None) is not None:
+            _lib.lib().cmpc_loop_destroy(self.group)
+            self.group = None
 
 
 def device_qp(qp: DenseQp) -> DeviceQp:

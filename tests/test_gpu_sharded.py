@@ -79,3 +79,49 @@ def test_shard_residuals_partition_the_rows():
         np.testing.assert_array_equal(part.r3, whole.r3[rows])
         r1_jtl += part.r1 - (qp.H @ st.v + qp.h)  # J_g' lambda_g
     assert np.abs(qp.H @ st.v + qp.h + r1_jtl - whole.r1).max() <= 1e-10 * (1 + np.abs(whole.r1).max())
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_sharded_loop_at_several_ranks_matches_the_unsharded_solve_and_oracle(O, nranks):
+    # the real sharded C++ loop (ipm_host.cpp) and kernels with N ranks: an in-process
+    # loopback communicator stands in for NCCL over N contexts on the one GPU, one host
+    # thread per rank (ipm.cpp:183-251 on every rank, the row sums combined in rank order)
+    from _cmpc_helpers import oracle_qp
+    qp = heat_qp(T=14)
+    ref_log = []
+    ref = ipm.solve(qp, ipm.IpmOptions(log=ref_log.append))
+    sh = ipm.LoopbackShards(qp, nranks)
+    try:
+        assert sum(len(r) for r in sh.rows) == qp.m and len(sh.rows) == nranks
+        outs = sh.solve()
+    finally:
+        sh.close()
+    o = O.solve(oracle_qp(O, qp))
+    for r in outs:  # identical decisions on every rank: same iterations, same iterate v
+        assert r.status.name == ref.status.name == o.status == "converged"
+        assert r.iter == ref.iter == o.iter
+        assert np.array_equal(r.v, outs[0].v)
+        assert r.objective == outs[0].objective and r.kkt_error == outs[0].kkt_error
+        assert rel(r.v, ref.v) <= 1e-10 and rel(r.v, o.v) <= 1e-8
+        assert abs(r.objective - o.objective) <= 1e-8 * (1 + abs(o.objective))
+        assert abs(r.kkt_error - o.kkt_error) <= 1e-9 * (1 + abs(o.kkt_error))
+    # each rank holds its rows' slacks and duals: together the unsharded ones
+    s_all = np.zeros(qp.m)
+    for rows, r in zip(sh.rows, outs):
+        s_all[rows] = r.s
+    assert rel(s_all, o.s) <= 1e-8
+
+
+@pytest.mark.timeout(600)
+def test_sharded_loop_on_config2_shape_at_two_ranks():
+    qp = P.build_dense_qp(P.heat1d_problem(200, 50))
+    ref = ipm.solve(qp)
+    sh = ipm.LoopbackShards(qp, 2)
+    try:
+        outs = sh.solve()
+    finally:
+        sh.close()
+    for r in outs:
+        assert r.iter == ref.iter and r.status.name == ref.status.name
+        assert rel(r.v, ref.v) <= 1e-10
