@@ -60,3 +60,49 @@ def test_concurrent_condensations_are_bitwise_identical():
         assert np.array_equal(o, ref)
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("shape", [(20, 25, 30), (12, 10, 40)])
+def test_concurrent_cholesky_paths_are_bitwise_identical(shape):
+    # the dataflow Cholesky (chol.cu) under SM contention: the spine's named barriers and
+    # mbarrier signals, the pre-diagonal / panel tasks' flags, the spine backward solve
+    # (n = 150) and the per-block backward tasks (n = 320) must give bitwise the same factor
+    # and solve whatever the interleaving (compute-sanitizer is not available on this pool;
+    # this is the race check)
+    nx, ny, T = shape
+    qp = P.build_dense_qp(P.heat2d_problem(nx, ny, T=T))
+    ref = ipm.solve(qp)
+    root = ipm.device_qp(qp)
+    K = 10
+    ctxs = [root.clone() for _ in range(K)]
+    for _ in range(2):
+        outs = [None] * K
+
+        def run(i):
+            outs[i] = ipm.solve_loaded(ctxs[i], qp, ipm.IpmOptions())
+
+        ths = [threading.Thread(target=run, args=(i,)) for i in range(K)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        for r in outs:
+            assert r.iter == ref.iter
+            assert np.array_equal(r.v, ref.v) and np.array_equal(r.s, ref.s) and np.array_equal(r.z, ref.z)
+    for c in ctxs:
+        c.close()
+
+
+def test_lockstep_batch_is_bitwise_reproducible():
+    from paper_2209_13049_b200 import batch
+    data = P.heat2d_problem(20, 25, T=30)
+    base = P.build_dense_qp(data)
+    xbs = P.batch_initial_states(500, 64, seed=9)
+    bs = ipm.BatchSolver(base, 64)
+    for i, xb in enumerate(xbs):
+        bs.set_instance(i, *batch.instance_affine(base, xb))
+    a = bs.solve()
+    b = bs.solve()
+    bs.close()
+    assert np.array_equal(a.iter, b.iter) and np.array_equal(a.v, b.v)
+    assert all(s == "converged" for s in a.status)
