@@ -45,6 +45,9 @@ CONFIGS = {
 }
 
 
+C4_T = 200  # config 4's horizon (--T: the sweep 50, 100, 150, 200)
+
+
 def build_problem(cfg, rank=0):
     from paper_2209_13049_b200 import problem as P
     if cfg == "c1":
@@ -58,7 +61,7 @@ def build_problem(cfg, rank=0):
     elif cfg == "c3":
         data = P.heat2d_problem(50, 50, T=50)
     elif cfg == "c4":
-        data = P.heat2d_problem(40, 25, T=200)
+        data = P.heat2d_problem(40, 25, T=C4_T)
     elif cfg == "c5":
         data = P.heat2d_problem(20, 25, T=30)
     else:
@@ -422,6 +425,14 @@ def run_batch(args, rank, world, local, dist):
         "ms_per_batch_iteration": ms / args.steps / max(1, biters[-1]),
         "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
     }
+    if not args.no_cpu_baseline and world == 1:
+        one = P.build_dense_qp(data)
+        s_ = cpu_sample(one, os.cpu_count() or 1, int(round(float(np.mean(iters)))))
+        line["cpu_baseline"] = {
+            "value": s_["ms_per_solve"], "unit": "ms", "cores": os.cpu_count() or 1, "kind": "port",
+            "cpu": host_cpu(),
+            "sample": "one IPM iteration of the oracle on one config-5 instance (dense J), x the batch's "
+                      "mean iteration count: ms per instance solve"}
     print(json.dumps(line), flush=True)
     bs.close()
 
@@ -434,11 +445,17 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--T", type=int, default=200, help="config 4's horizon (50, 100, 150, 200)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="auto", choices=["auto", "shard", "replica"],
                     help="N > 1: shard = rows of J split across the GPUs, one solve (configs 3/4, "
                          "the default there); replica = an independent instance per GPU")
     args = ap.parse_args()
+    global C4_T
+    C4_T = args.T
+    if args.config == "c4" and args.T != 200:
+        CONFIGS["c4"] = dict(desc=f"config 4: long-horizon 2-D heat 40x25, n_x=1000, n_u=10, T={args.T} "
+                                  f"(n={10 * args.T}, m={2020 * args.T:,})")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
