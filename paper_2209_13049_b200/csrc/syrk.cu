@@ -689,6 +689,60 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
 }
 
 // ---------------------------------------------------------------- lockstep batch
+namespace {
+// M_b(i, j) = H(i, j) + the tile's partials in plan order (+ the singleton diagonal); the
+// fused right-hand side of the diagonal tiles: tq = P'q + singletons, rhs = -r1 + tq. One
+// block per (tile, instance): a job has one or two partials per tile, so the one-block-per-64-
+// elements shape of k_syrk_reduce (built for tens of split-k partials) would be mostly launch
+// overhead across a batch.
+__global__ void __launch_bounds__(256)
+    k_syrk_reduce_batch(const double* __restrict__ partial, const int2* __restrict__ tiles,
+                        const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ tile_segs,
+                        const double* __restrict__ H, const double* __restrict__ omega_s, int64_t n,
+                        double* __restrict__ M, const double* __restrict__ rp, const double* __restrict__ qs,
+                        const int32_t* __restrict__ sing_ptr, const double* __restrict__ sing_val,
+                        double* __restrict__ tq, double* __restrict__ rhs, const double* __restrict__ r1,
+                        RedStrides bs) {
+  const int64_t b = blockIdx.y;
+  partial += b * bs.partial;
+  omega_s += b * bs.proto;
+  M += b * bs.M;
+  const int2 tl = tiles[blockIdx.x];
+  const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
+  if (rp && tl.x == tl.y && threadIdx.x < 64) {
+    const int64_t col = (int64_t)kTile * tl.x + threadIdx.x;
+    if (col < n) {
+      const double* rpb = rp + b * bs.rp;
+      double s = 0.0;
+      for (int q = u0; q < u1; ++q) {
+        const int32_t id = tile_segs[q] & 0x7fffffff;
+        s += __ldcg(rpb + (size_t)id * 128 + threadIdx.x) + __ldcg(rpb + (size_t)id * 128 + 64 + threadIdx.x);
+      }
+      const double* qb = qs + b * bs.proto;
+      for (int32_t k = sing_ptr[col]; k < sing_ptr[col + 1]; ++k) s += sing_val[k] * qb[k];
+      tq[b * bs.vec + col] = s;
+      if (r1) rhs[b * bs.vec + col] = __dadd_rn(-r1[b * bs.vec + col], s);
+    }
+  }
+  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+    const int rl = e & (kTile - 1), cl = e >> 6;
+    const int64_t i = (int64_t)kTile * tl.x + rl, j = (int64_t)kTile * tl.y + cl;
+    if (!(i < n && j < n && i >= j)) continue;
+    double s = 0.0;
+    for (int q = u0; q < u1; ++q) {
+      const int32_t id = tile_segs[q];
+      if (!(id < 0 && rl >= 32)) s += __ldcg(partial + (size_t)(id & 0x7fffffff) * (kTile * kTile) + e);
+    }
+    if (i == j) {
+      double ds = 0.0;
+      for (int32_t k = sing_ptr[i]; k < sing_ptr[i + 1]; ++k) ds += omega_s[k] * (sing_val[k] * sing_val[k]);
+      s += ds;
+    }
+    M[i + j * n] = H[i + j * n] + s;
+  }
+}
+}  // namespace
+
 // The batch (batch.cu) shares P and its structure; with B instances there is parallelism
 // enough without splitting k, so every job (tile, shape) is one segment over its whole k
 // range and one piece, the pieces ordered by decreasing cost (largest first); partials per
@@ -790,8 +844,8 @@ void launch_condense_batch(Ctx& c, BatchSyrk& bs, cudaStream_t st, const double*
     CMPC_LAUNCHED();
   }
   const RedStrides rs{(int64_t)bs.nunits * kTile * kTile, s_proto, (int64_t)bs.nunits * 128, c.n * c.n, c.n};
-  k_syrk_reduce<<<dim3(bs.ntiles, kTile * kTile / 64, (unsigned)B), 64 * kRedWays, 0, st>>>(
-      bs.partial, bs.tiles, bs.tile_ptr, bs.tile_units, c.H, omega + c.ldp, c.n, M, 0,
+  k_syrk_reduce_batch<<<dim3(bs.ntiles, (unsigned)B), 256, 0, st>>>(
+      bs.partial, bs.tiles, bs.tile_ptr, bs.tile_units, c.H, omega + c.ldp, c.n, M,
       c.ps > 0 ? bs.rhs_part : nullptr, q + c.ldp, c.sing_ptr, c.sing_val, tq, rhs, r1, rs);
   CMPC_LAUNCHED();
 }

@@ -291,6 +291,93 @@ __global__ void k_v4(const double* A, double* L, double* W, Out* out, int reps) 
   }
 }
 
+
+// V5: two pivots per round (2x2 blocked pivot chain): column pair (p, p+1) formed with two
+// rsqrt, one shared-memory broadcast round and one mbarrier-free counter signal per pair
+template <bool WARP1>
+__global__ void k_v5(const double* A, double* L, double* W, Out* out, int reps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ __align__(16) double col[32 * 32];
+  __shared__ double rr[32];
+  __shared__ volatile int cnt;
+  long long t0 = 0, t1 = 0, t2 = 0;
+  for (int it = 0; it < reps; ++it) {
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    if (warp == 0) {
+      double a[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) a[c] = (c <= lane) ? A[lane + 32 * c] : 0.0;
+      __syncwarp();
+      t0 = clock64();
+      double d1 = __shfl_sync(kFull, a[0], 0);
+#pragma unroll
+      for (int p = 0; p < 32; p += 2) {
+        const double r1 = rsqrt_mufu(d1);
+        const double l1 = (lane >= p) ? a[p] * r1 : 0.0;
+        const double l21 = __shfl_sync(kFull, l1, p + 1);
+        const double d2 = __shfl_sync(kFull, fma(-l1, l1, a[p + 1]), p + 1);
+        const double r2 = rsqrt_mufu(d2);
+        const double l2 = (lane >= p + 1) ? fma(-l1, l21, a[p + 1]) * r2 : 0.0;
+        if (p + 2 < 32) d1 = __shfl_sync(kFull, fma(-l2, l2, fma(-l1, l1, a[p + 2])), p + 2);
+        a[p] = l1;
+        a[p + 1] = l2;
+        col[p * 32 + lane] = l1;
+        col[(p + 1) * 32 + lane] = l2;
+        if (lane == 0) {
+          rr[p] = r1;
+          rr[p + 1] = r2;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = (p + 2); c < 32; c += 2) {
+          const double2 c1 = ld2(col + p * 32 + c);
+          const double2 c2 = ld2(col + (p + 1) * 32 + c);
+          a[c] = fma(-l2, c2.x, fma(-l1, c1.x, a[c]));
+          a[c + 1] = fma(-l2, c2.y, fma(-l1, c1.y, a[c + 1]));
+        }
+        if (WARP1 && lane == 0) {
+          __threadfence_block();
+          cnt = p + 2;
+        }
+      }
+      t1 = clock64();
+#pragma unroll
+      for (int c = 0; c < 32; ++c) L[lane + 32 * c] = a[c];
+    } else if (warp == 1 && WARP1) {
+      double s[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int p = 0; p < 32; ++p) {
+        if ((p & 1) == 0)
+          while (cnt <= p) __nanosleep(20);
+        __threadfence_block();
+        const double wp = s[p] * rr[p];
+        s[p] = wp;
+#pragma unroll
+        for (int i = (p + 1) & ~1; i < 32; i += 2) {
+          const double2 lc = ld2(col + p * 32 + i);
+          if (i > p) s[i] = fma(-lc.x, wp, s[i]);
+          if (i + 1 > p) s[i + 1] = fma(-lc.y, wp, s[i + 1]);
+        }
+      }
+      t2 = clock64();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) W[i + 32 * lane] = (i >= lane) ? s[i] : 0.0;
+    }
+    __syncthreads();
+  }
+  __shared__ long long st[2];
+  if (threadIdx.x == 0) { st[0] = t0; st[1] = t1; }
+  __syncthreads();
+  if (threadIdx.x == (WARP1 ? 32 : 0)) {
+    out->t0 = st[0];
+    out->t1 = WARP1 ? t2 : st[1];
+    out->fail = (int)(st[1] - st[0]);
+  }
+}
+
 int main(int argc, char** argv) {
   const int reps = argc > 1 ? atoi(argv[1]) : 3;
   const int n = 32;
@@ -368,5 +455,11 @@ int main(int argc, char** argv) {
   k_v4<true, false, true, true><<<1, 128>>>(dA, dL, dW, dO, reps);
   CK(cudaDeviceSynchronize());
   check("V4e = V4d with the rcp pivot chain", true);
+  k_v5<false><<<1, 128>>>(dA, dL, dW, dO, reps);
+  CK(cudaDeviceSynchronize());
+  check("V5 two pivots per round, factor only", false);
+  k_v5<true><<<1, 128>>>(dA, dL, dW, dO, reps);
+  CK(cudaDeviceSynchronize());
+  check("V5 two pivots per round + W warp (fail = factor cycles)", true);
   return 0;
 }
