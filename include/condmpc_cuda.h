@@ -100,6 +100,12 @@ int cmpc_batch_create(cmpc_ctx* base, int64_t count, cmpc_batch** out);
 int cmpc_batch_set_affine(cmpc_batch* b, const double* h_all, const double* h0_all, const double* d_all);
 int cmpc_batch_solve(cmpc_batch* b, const double* opts, int64_t max_iter, double* v_out, double* scal_out,
                      double* stats);
+/* The batch's condensation step alone (assemble_condensed + the right-hand side's J'w,
+ * proj/src/ipm.cpp:72-103, for every instance): sigma_all, w_all count x m (host); M_out
+ * count x n x n (lower triangle of H + J' diag(sigma_b) J, column-major), tq_out count x n
+ * (J' w_b). Leaves the batch's iterates untouched. */
+int cmpc_batch_condense(cmpc_batch* b, const double* sigma_all, const double* w_all, double* M_out,
+                        double* tq_out);
 void cmpc_batch_destroy(cmpc_batch* b);
 /* Page-lock / release a host buffer (cudaHostRegister) used for repeated uploads */
 int cmpc_host_register(void* p, int64_t bytes);

@@ -762,7 +762,7 @@ struct Host {
                                                    b.sigma, b.w, b.omega, b.qw, b.act);
       CMPC_LAUNCHED();
     });
-    phase("syrk", [&] { launch_condense_batch(c, b.syrk, b.st, b.omega, b.qw, b.py, b.M, b.tq, b.rhs, b.r1); });
+    phase("syrk", [&] { launch_condense_batch(c, b.syrk, b.st, b.omega, b.qw, b.py, b.M, b.tq, b.rhs, b.r1, b.act); });
   }
   void cholesky() {
     phase("chol", [&] {
@@ -808,6 +808,23 @@ double now_s() {
 }
 
 }  // namespace
+
+void batch_condense(BatchCtx& b, const double* sigma, const double* w, double* M_out, double* tq_out) {
+  Ctx& c = *b.base;
+  const int64_t B = b.B, n = b.n, m = b.m;
+  upload_h2d(b.sigma, sigma, sizeof(double) * B * m, b.st);
+  upload_h2d(b.w, w, sizeof(double) * B * m, b.st);
+  std::vector<int> all(size_t(B), 1);
+  std::memcpy(b.istage, all.data(), sizeof(int) * B);
+  CMPC_CUDA(cudaMemcpyAsync(b.act, b.istage, sizeof(int) * B, cudaMemcpyHostToDevice, b.st));
+  k_b_proto<false><<<dim3(bgrid(c.p), (unsigned)B), kBT, 0, b.st>>>(c.p, c.ps, c.ldp, m, b.py, c.zero_k, c.mem_ptr,
+                                                                    c.mem_rows, b.sigma, b.w, b.omega, b.qw, b.act);
+  CMPC_LAUNCHED();
+  launch_condense_batch(c, b.syrk, b.st, b.omega, b.qw, b.py, b.M, b.tq, b.rhs, nullptr, b.act);
+  CMPC_CUDA(cudaMemcpyAsync(M_out, b.M, sizeof(double) * B * n * n, cudaMemcpyDeviceToHost, b.st));
+  CMPC_CUDA(cudaMemcpyAsync(tq_out, b.tq, sizeof(double) * B * n, cudaMemcpyDeviceToHost, b.st));
+  CMPC_CUDA(cudaStreamSynchronize(b.st));
+}
 
 // the lockstep host loop: ipm::solve (ipm.cpp:160-268) for every instance, decision for decision
 void batch_solve(BatchCtx& b, const double* opts, int64_t max_iter, double* v_out, double* scal, double* stats) {

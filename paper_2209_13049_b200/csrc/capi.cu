@@ -475,6 +475,16 @@ int cmpc_batch_solve(cmpc_batch* b, const double* opts, int64_t max_iter, double
   });
 }
 
+int cmpc_batch_condense(cmpc_batch* b, const double* sigma_all, const double* w_all, double* M_out,
+                        double* tq_out) {
+  return guard([&] {
+    if (!b || !b->b || !sigma_all || !w_all || !M_out || !tq_out) throw DimError("null argument");
+    CMPC_CUDA(cudaSetDevice(b->device));
+    batch_condense(*b->b, sigma_all, w_all, M_out, tq_out);
+    return CMPC_OK;
+  });
+}
+
 void cmpc_batch_destroy(cmpc_batch* b) {
   if (!b) return;
   cudaSetDevice(b->device);

@@ -172,24 +172,21 @@ void syrk_plan(Ctx& c);
 // M(lower) = H + P' diag(omega) P + (singleton diagonal); writes full symmetric M when mirror
 void launch_condense(Ctx& c, bool mirror, bool with_rhs = false, cudaEvent_t after_syrk = nullptr);
 void syrk_free(Ctx& c);
-// lockstep batch (batch.cu): B instances sharing H and P, per-instance omega/q in prototype
-// space at stride s_proto, M (n x n lower), tq, rhs and r1 (n) at their natural strides
+// ---- bsyrk.cu: lockstep-batch condensation (batch.cu): B instances sharing H and P, one CTA
+// per instance; per-instance omega/q in prototype space at stride s_proto, M (n x n lower),
+// tq, rhs and r1 (n) at their natural strides; inactive instances (act = 0) are skipped
 struct BatchSyrk {
-  int4* units = nullptr;
-  int32_t* piece_ptr = nullptr;
-  int npieces = 0, nunits = 0, ntiles = 0;
-  int2* tiles = nullptr;
-  int32_t* tile_ptr = nullptr;
-  int32_t* tile_units = nullptr;
-  unsigned* ctl = nullptr;
-  double* partial = nullptr;
-  double* rhs_part = nullptr;
+  int2* chunks = nullptr;            // 32-row chunks of P in processing order: {first row, width}
+  int nchunks = 0;
+  unsigned char reg[15][4] = {};     // each consumer warp's 16 x 16 output regions
+  double flops_per_instance = 0.0;   // algorithmic: sum over SYRK rows of hi (hi + 1)
   int64_t B = 0;
 };
 void syrk_plan_batch(Ctx& c, int64_t B, BatchSyrk& out, cudaStream_t st);
 void syrk_free_batch(BatchSyrk& b, cudaStream_t st);
 void launch_condense_batch(Ctx& c, BatchSyrk& bs, cudaStream_t st, const double* omega, const double* q,
-                           int64_t s_proto, double* M, double* tq, double* rhs, const double* r1);
+                           int64_t s_proto, double* M, double* tq, double* rhs, const double* r1,
+                           const int* act);
 
 // ---- chol.cu
 // L = chol(M + delta I) (lower, upper zeroed); failing pivot+1 in c.pk->info; with rhs,
@@ -208,6 +205,7 @@ struct BatchCtx;
 BatchCtx* batch_create(Ctx& base, int64_t B);
 void batch_destroy(BatchCtx* b);
 void batch_set_affine(BatchCtx& b, const double* h, const double* h0, const double* d);
+void batch_condense(BatchCtx& b, const double* sigma, const double* w, double* M_out, double* tq_out);
 void batch_solve(BatchCtx& b, const double* opts, int64_t max_iter, double* v_out, double* scal, double* stats);
 
 // ---- comm.cpp (NCCL, opened at run time)

@@ -688,166 +688,4 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
   CMPC_LAUNCHED();
 }
 
-// ---------------------------------------------------------------- lockstep batch
-namespace {
-// M_b(i, j) = H(i, j) + the tile's partials in plan order (+ the singleton diagonal); the
-// fused right-hand side of the diagonal tiles: tq = P'q + singletons, rhs = -r1 + tq. One
-// block per (tile, instance): a job has one or two partials per tile, so the one-block-per-64-
-// elements shape of k_syrk_reduce (built for tens of split-k partials) would be mostly launch
-// overhead across a batch.
-__global__ void __launch_bounds__(256)
-    k_syrk_reduce_batch(const double* __restrict__ partial, const int2* __restrict__ tiles,
-                        const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ tile_segs,
-                        const double* __restrict__ H, const double* __restrict__ omega_s, int64_t n,
-                        double* __restrict__ M, const double* __restrict__ rp, const double* __restrict__ qs,
-                        const int32_t* __restrict__ sing_ptr, const double* __restrict__ sing_val,
-                        double* __restrict__ tq, double* __restrict__ rhs, const double* __restrict__ r1,
-                        RedStrides bs) {
-  const int64_t b = blockIdx.y;
-  partial += b * bs.partial;
-  omega_s += b * bs.proto;
-  M += b * bs.M;
-  const int2 tl = tiles[blockIdx.x];
-  const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
-  if (rp && tl.x == tl.y && threadIdx.x < 64) {
-    const int64_t col = (int64_t)kTile * tl.x + threadIdx.x;
-    if (col < n) {
-      const double* rpb = rp + b * bs.rp;
-      double s = 0.0;
-      for (int q = u0; q < u1; ++q) {
-        const int32_t id = tile_segs[q] & 0x7fffffff;
-        s += __ldcg(rpb + (size_t)id * 128 + threadIdx.x) + __ldcg(rpb + (size_t)id * 128 + 64 + threadIdx.x);
-      }
-      const double* qb = qs + b * bs.proto;
-      for (int32_t k = sing_ptr[col]; k < sing_ptr[col + 1]; ++k) s += sing_val[k] * qb[k];
-      tq[b * bs.vec + col] = s;
-      if (r1) rhs[b * bs.vec + col] = __dadd_rn(-r1[b * bs.vec + col], s);
-    }
-  }
-  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
-    const int rl = e & (kTile - 1), cl = e >> 6;
-    const int64_t i = (int64_t)kTile * tl.x + rl, j = (int64_t)kTile * tl.y + cl;
-    if (!(i < n && j < n && i >= j)) continue;
-    double s = 0.0;
-    for (int q = u0; q < u1; ++q) {
-      const int32_t id = tile_segs[q];
-      if (!(id < 0 && rl >= 32)) s += __ldcg(partial + (size_t)(id & 0x7fffffff) * (kTile * kTile) + e);
-    }
-    if (i == j) {
-      double ds = 0.0;
-      for (int32_t k = sing_ptr[i]; k < sing_ptr[i + 1]; ++k) ds += omega_s[k] * (sing_val[k] * sing_val[k]);
-      s += ds;
-    }
-    M[i + j * n] = H[i + j * n] + s;
-  }
-}
-}  // namespace
-
-// The batch (batch.cu) shares P and its structure; with B instances there is parallelism
-// enough without splitting k, so every job (tile, shape) is one segment over its whole k
-// range and one piece, the pieces ordered by decreasing cost (largest first); partials per
-// instance: one per job.
-void syrk_plan_batch(Ctx& c, int64_t B, BatchSyrk& out, cudaStream_t st) {
-  syrk_free_batch(out, st);
-  const int64_t n = c.n;
-  const int nt = (int)ceil_div(n, kTile);
-  const int k_end = (int)c.ldp;
-  auto kstart = [&](int64_t col) {
-    if (c.ps == 0) return k_end;
-    return c.h_start_col[size_t(std::min<int64_t>(n, col))] / kBK * kBK;
-  };
-  struct Job { int tile, ti, tj, thin, kb, ke; double cost; };
-  std::vector<Job> jobs;
-  std::vector<int2> tiles;
-  for (int tj = 0; tj < nt; ++tj)
-    for (int ti = tj; ti < nt; ++ti) {
-      const int tile = (int)tiles.size();
-      tiles.push_back({ti, tj});
-      const int a0 = kstart((int64_t)kTile * ti), a1 = std::max(a0, kstart((int64_t)kTile * ti + 32));
-      const bool dg = ti == tj;
-      if (a1 > a0) jobs.push_back({tile, ti, tj, 1, a0, a1, (a1 - a0) * (dg ? kCostDiagThin : kCostThin)});
-      if (k_end > a1) jobs.push_back({tile, ti, tj, 0, a1, k_end, (k_end - a1) * (dg ? kCostDiag : kCostFull)});
-    }
-  std::vector<int> order(jobs.size());
-  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return jobs[size_t(x)].cost > jobs[size_t(y)].cost; });
-  std::vector<int4> segs;
-  std::vector<int32_t> pptr{0};
-  std::vector<std::vector<int32_t>> per_tile(tiles.size());
-  for (int o : order) {
-    const Job& jb = jobs[size_t(o)];
-    const int id = (int)segs.size();
-    per_tile[size_t(jb.tile)].push_back(jb.thin ? (id | int(0x80000000u)) : id);
-    segs.push_back({jb.ti | jb.tj << 10 | jb.thin << 20, jb.kb, jb.ke, jb.tile});
-    pptr.push_back((int32_t)segs.size());
-  }
-  std::vector<int32_t> tptr(tiles.size() + 1, 0), tsegs;
-  for (size_t t = 0; t < tiles.size(); ++t) {
-    tptr[t + 1] = tptr[t] + (int32_t)per_tile[t].size();
-    for (int32_t u : per_tile[t]) tsegs.push_back(u);
-  }
-  out.B = B;
-  out.nunits = (int)segs.size();
-  out.npieces = (int)segs.size();
-  out.ntiles = (int)tiles.size();
-  out.units = dev_alloc<int4>(std::max<size_t>(1, segs.size()), st);
-  out.piece_ptr = dev_alloc<int32_t>(pptr.size(), st);
-  out.ctl = dev_zeros<unsigned>(2, st);
-  out.tiles = dev_alloc<int2>(tiles.size(), st);
-  out.tile_ptr = dev_alloc<int32_t>(tptr.size(), st);
-  out.tile_units = dev_alloc<int32_t>(std::max<size_t>(1, tsegs.size()), st);
-  out.partial = dev_alloc<double>((size_t)kTile * kTile * std::max<size_t>(1, segs.size()) * B, st);
-  out.rhs_part = dev_zeros<double>((size_t)128 * std::max<size_t>(1, segs.size()) * B, st);
-  if (!segs.empty())
-    CMPC_CUDA(cudaMemcpyAsync(out.units, segs.data(), sizeof(int4) * segs.size(), cudaMemcpyHostToDevice, st));
-  CMPC_CUDA(cudaMemcpyAsync(out.piece_ptr, pptr.data(), sizeof(int32_t) * pptr.size(), cudaMemcpyHostToDevice, st));
-  CMPC_CUDA(cudaMemcpyAsync(out.tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, st));
-  CMPC_CUDA(cudaMemcpyAsync(out.tile_ptr, tptr.data(), sizeof(int32_t) * tptr.size(), cudaMemcpyHostToDevice, st));
-  if (!tsegs.empty())
-    CMPC_CUDA(cudaMemcpyAsync(out.tile_units, tsegs.data(), sizeof(int32_t) * tsegs.size(), cudaMemcpyHostToDevice, st));
-  CMPC_CUDA(cudaStreamSynchronize(st));
-}
-
-void syrk_free_batch(BatchSyrk& b, cudaStream_t st) {
-  for (void* p : {(void*)b.units, (void*)b.piece_ptr, (void*)b.ctl, (void*)b.tiles, (void*)b.tile_ptr,
-                  (void*)b.tile_units, (void*)b.partial, (void*)b.rhs_part})
-    dev_free(p, st);
-  b = BatchSyrk{};
-}
-
-void launch_condense_batch(Ctx& c, BatchSyrk& bs, cudaStream_t st, const double* omega, const double* q,
-                           int64_t s_proto, double* M, double* tq, double* rhs, const double* r1) {
-  const int64_t B = bs.B;
-  if (bs.npieces > 0 && c.ps > 0) {
-    SyrkArgs a;
-    a.omega = omega;
-    a.q = q;
-    a.rhs_part = bs.rhs_part;
-    a.segs = bs.units;
-    a.piece_ptr = bs.piece_ptr;
-    a.npieces = (int)(bs.npieces * B);
-    a.ctl = bs.ctl;
-    a.partial = bs.partial;
-    a.prof = nullptr;
-    a.static_sched = 0;
-    a.ppi = bs.npieces;
-    a.s_omega = s_proto;
-    a.s_q = s_proto;
-    a.s_partial = (int64_t)bs.nunits * kTile * kTile;
-    a.s_rhs = (int64_t)bs.nunits * 128;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
-    const int grid = (int)std::min<int64_t>(a.npieces, 2 * sms);
-    const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(c.tmap_P);
-    const CUtensorMap* tm32 = reinterpret_cast<const CUtensorMap*>(c.tmap_P32);
-    k_syrk<<<grid, kSyrkThreads, kSyrkSmem, st>>>(*tm, *tm32, a);
-    CMPC_LAUNCHED();
-  }
-  const RedStrides rs{(int64_t)bs.nunits * kTile * kTile, s_proto, (int64_t)bs.nunits * 128, c.n * c.n, c.n};
-  k_syrk_reduce_batch<<<dim3(bs.ntiles, (unsigned)B), 256, 0, st>>>(
-      bs.partial, bs.tiles, bs.tile_ptr, bs.tile_units, c.H, omega + c.ldp, c.n, M,
-      c.ps > 0 ? bs.rhs_part : nullptr, q + c.ldp, c.sing_ptr, c.sing_val, tq, rhs, r1, rs);
-  CMPC_LAUNCHED();
-}
-
 }  // namespace cmpc

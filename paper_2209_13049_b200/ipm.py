@@ -614,6 +614,20 @@ class BatchSolver:
         self.d_all[i] = np.asarray(d, dtype=np.float64)
         self._dirty = True
 
+    def condense(self, sigma, w):
+        """Lockstep mode: the condensation step alone for every instance (assemble_condensed +
+        the right-hand side's J'w, ipm.cpp:72-103): sigma, w count x m -> (M count x n x n with
+        the lower triangle of H + J' diag(sigma_b) J, tq count x n = J' w_b)."""
+        if self.mode != "lockstep":
+            raise ValueError("condense needs the lockstep batch")
+        n, m, cnt = self.base.n, self.base.m, self.count
+        sg = np.ascontiguousarray(sigma, dtype=np.float64).reshape(cnt, m)
+        ww = np.ascontiguousarray(w, dtype=np.float64).reshape(cnt, m)
+        M = np.zeros((cnt, n, n))
+        tq = np.zeros((cnt, n))
+        check(_lib.lib().cmpc_batch_condense(self._batch, ptr(sg), ptr(ww), ptr(M), ptr(tq)))
+        return M.transpose(0, 2, 1), tq  # column-major per instance
+
     def solve(self, opts: IpmOptions = None, threads: int | None = None) -> BatchResult:
         opts = opts or IpmOptions()
         _check_options(opts)

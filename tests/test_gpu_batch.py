@@ -99,3 +99,34 @@ def test_batch_solvers_can_be_created_again_on_the_same_base():
         iters.append(list(res.iter))
         bs.close()
     assert iters[0] == iters[1] == iters[2]
+
+
+@pytest.mark.parametrize("shape", ["heat_small", "config5"])
+def test_batch_condensation_matches_fp64(shape):
+    # the lockstep condensation kernel (csrc/bsyrk.cu) alone: M_b = H + J' diag(sigma_b) J
+    # (lower triangle) and tq_b = J' w_b for every instance, against an fp64 numpy product
+    # (assemble_condensed, ipm.cpp:72-77; the right-hand side's J'w, ipm.cpp:79-103)
+    if shape == "heat_small":
+        data = P.heat2d_problem(10, 8, T=12, splits=([5], [5], [4], [4]))
+    else:
+        import bench
+        data = bench.build_problem("c5")
+    base = P.build_dense_qp(data)
+    cnt = 7
+    rng = np.random.default_rng(3)
+    m, n = base.m, base.n
+    sigma = np.exp(rng.uniform(-6, 6, size=(cnt, m)))
+    w = rng.standard_normal((cnt, m))
+    bs = ipm.BatchSolver(base, cnt, mode="lockstep")
+    M, tq = bs.condense(sigma, w)
+    bs.close()
+    J, H = base.J, base.H
+    for b in range(cnt):
+        ref = H + J.T @ (sigma[b][:, None] * J)
+        scale = np.abs(H).max() + (np.abs(J).T @ (sigma[b][:, None] * np.abs(J))).max()
+        lo = np.tril_indices(n)
+        err = np.abs(M[b][lo] - ref[lo]).max() / scale
+        assert err <= 1e-13, (b, err)
+        tref = J.T @ w[b]
+        terr = np.abs(tq[b] - tref).max() / (np.abs(J).T @ np.abs(w[b])).max()
+        assert terr <= 1e-13, (b, terr)
