@@ -253,10 +253,10 @@ __global__ void __launch_bounds__(kBT) k_b_mu_rows(int64_t m, const double* __re
   mc = block_max<kBT>(mc, sh);
   if (threadIdx.x == 0) part[((int64_t)b * kBBlk + blockIdx.x) * kBSlots + kBComp] = mc;
 }
-__global__ void k_b_kkt_mu(int64_t n, int64_t m, const double* __restrict__ part, Packet* pk,
+__global__ void k_b_kkt_mu(int64_t B, int64_t n, int64_t m, const double* __restrict__ part, Packet* pk,
                            const int* __restrict__ act) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (!act[b]) return;
+  if (b >= B || !act[b]) return;
   double mc = 0.0;
   for (int k = 0; k < kBBlk; ++k) mc = fmax(mc, part[(b * kBBlk + k) * kBSlots + kBComp]);
   Packet* p = pk + b;
@@ -336,65 +336,116 @@ __global__ void k_b_sing_t(int64_t n, int64_t py, int64_t ldp, const int32_t* __
 // updates' own by-product; one barrier per pivot: step j updates the trailing matrix with the
 // raw column j scaled by 1/d_j, and scales column j (to l_ij = a_ij / sqrt(d_j)) in step j+1,
 // when nothing reads it any more.
-constexpr int kCholT = 1024;  // the matrix fills the SM's shared memory (one CTA per SM): all the warps it can hold
-__global__ void __launch_bounds__(kCholT) k_b_chol(int n, const double* __restrict__ M, const double* __restrict__ delta,
-                                                const double* __restrict__ rhs, double* __restrict__ x, Packet* pk,
-                                                const int* __restrict__ act) {
+constexpr int kCholT = 1024;  // 32 warps: warp w owns the columns w + 32 c, lane l the rows l + 32 a
+constexpr int kCholS = 5;     // 32-row / 32-column slots: n <= 160
+__device__ __forceinline__ constexpr int cslot(int a, int c) { return a * (a + 1) / 2 + c; }
+
+// Per-instance Cholesky of M_b + delta_b I and both triangular solves with rhs_b (the
+// ReferenceBackend factorize + Factor::solve, proj/src/dense_linalg.cpp:59-77 and :102-110),
+// one CTA per instance. Right-looking with the trailing matrix in REGISTERS: thread (lane,
+// warp) holds the elements (lane + 32 a, warp + 32 c), a >= c, of the lower triangle (15
+// doubles); per pivot j one barrier: every thread applies column j of L (read from shared
+// memory, where its owner warp wrote it) to its elements, then the warp owning column j+1
+// forms it (pivot by shuffle, l = a / l_jj), stores it to shared memory and advances the
+// forward solve. The backward solve reads L from shared memory.
+__global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __restrict__ M,
+                                                   const double* __restrict__ delta, const double* __restrict__ rhs,
+                                                   double* __restrict__ x, Packet* pk, const int* __restrict__ act) {
   extern __shared__ double bsm[];
-  const int ld = n + 2;       // rows 0..n-1: the matrix, row n: the right-hand side
-  double* a = bsm;            // a[j * ld + i], i >= j (and i = n)
-  double* xs = bsm + n * ld;  // n
+  double* L = bsm;            // L[i + j * n], i >= j
+  double* y = bsm + n * n;    // forward-solve vector (rhs, then L^{-1} rhs)
+  double* xs = y + n;         // n
   __shared__ int s_fail;
   const int64_t b = blockIdx.x;
   if (!act[b]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double dl = delta[b];
   const double* Mb = M + b * (int64_t)n * n;
-  for (int e = tid; e < n * n; e += kCholT) {
-    const int i = e % n, j = e / n;
-    if (i >= j) a[j * ld + i] = (i == j && dl != 0.0) ? add(Mb[i + (int64_t)j * n], dl) : Mb[i + (int64_t)j * n];
-  }
-  for (int j = tid; j < n; j += kCholT) a[j * ld + n] = rhs[b * n + j];
+  double r[cslot(kCholS, 0)];
+#pragma unroll
+  for (int a = 0; a < kCholS; ++a)
+#pragma unroll
+    for (int c = 0; c <= a; ++c) {
+      const int i = lane + 32 * a, k = warp + 32 * c;
+      double v = 0.0;
+      if (i < n && k < n && i >= k) {
+        v = Mb[i + (int64_t)k * n];
+        if (i == k && dl != 0.0) v = add(v, dl);
+      }
+      r[cslot(a, c)] = v;
+    }
+  for (int j = tid; j < n; j += kCholT) y[j] = rhs[b * n + j];
   if (tid == 0) s_fail = -1;
   __syncthreads();
-  const int cc = tid >> 5, rr = lane;  // one warp per column, lanes down 32 consecutive rows
-  for (int j = 0; j < n; ++j) {
-    const double d = a[j * ld + j];
-    if (!(d > 0.0) || !isfinite(d)) {  // uniform: every thread reads the same pivot
-      if (tid == 0) s_fail = j;
-      break;
+
+  // column j (owner warp j % 32): l_jj = sqrt(a_jj), l_ij = a_ij / l_jj; forward solve step
+  auto finalize = [&](int j) {
+    const int cj = j >> 5;
+    double d = 0.0;
+#pragma unroll
+    for (int c = 0; c < kCholS; ++c)
+      if (c == cj) d = r[cslot(c, c)];
+    d = __shfl_sync(0xffffffffu, d, j & 31);
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (lane == 0) s_fail = j;
+      return;
     }
-    const double ri = dv(1.0, d);
-    if (j > 0) {  // column j-1 is final: scale it (nothing reads it in this step)
-      const double lp = sqrt(a[(j - 1) * ld + (j - 1)]);
-      for (int i = j + tid; i <= n; i += kCholT) a[(j - 1) * ld + i] = dv(a[(j - 1) * ld + i], lp);
+    const double ljj = sqrt(d);
+    const double yj = dv(y[j], ljj);
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < kCholS; ++c) {
+      if (c != cj) continue;
+#pragma unroll
+      for (int a = c; a < kCholS; ++a) {
+        const int i = lane + 32 * a;
+        if (i > j && i < n) {
+          const double l = dv(r[cslot(a, c)], ljj);
+          r[cslot(a, c)] = l;
+          L[i + j * n] = l;
+          y[i] = fma(-l, yj, y[i]);
+        }
+      }
     }
-    // a(i, k) -= a_ij a_kj / d_j, j < k <= i (i = n: the right-hand side row)
-    for (int k = j + 1 + cc; k < n; k += kCholT / 32) {
-      const double lkj = mul(a[j * ld + k], ri);
-      for (int i = k + rr; i <= n; i += 32) a[k * ld + i] = fma(-a[j * ld + i], lkj, a[k * ld + i]);
+    if (lane == 0) {
+      L[j + j * n] = ljj;
+      y[j] = yj;
     }
+  };
+
+  if (warp == 0) finalize(0);
+  __syncthreads();
+  for (int j = 0; j + 1 < n; ++j) {
+    if (s_fail >= 0) break;
+    double li[kCholS];
+#pragma unroll
+    for (int a = 0; a < kCholS; ++a) {
+      const int i = lane + 32 * a;
+      li[a] = i > j && i < n ? L[i + j * n] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < kCholS; ++c) {
+      const int k = warp + 32 * c;
+      if (k <= j || k >= n) continue;  // warp-uniform
+      const double lk = L[k + j * n];
+#pragma unroll
+      for (int a = c; a < kCholS; ++a)
+        if (lane + 32 * a >= k) r[cslot(a, c)] = fma(-li[a], lk, r[cslot(a, c)]);
+    }
+    if (warp == ((j + 1) & 31)) finalize(j + 1);
     __syncthreads();
   }
-  __syncthreads();
   if (s_fail >= 0) {
     if (tid == 0) pk[b].info = s_fail + 1;
     return;
   }
-  {  // the last column, then the diagonal: l_jj = sqrt(d_j) (the columns were scaled by it)
-    const double lp = sqrt(a[(n - 1) * ld + (n - 1)]);
-    if (tid == 0) a[(n - 1) * ld + n] = dv(a[(n - 1) * ld + n], lp);
-    __syncthreads();
-    for (int j = tid; j < n; j += kCholT) a[j * ld + j] = sqrt(a[j * ld + j]);
-    __syncthreads();
-  }
-  // y_j = a[j][n] (= (L^{-1} rhs)_j); backward: x_j = (y_j - sum_{i>j} l_ij x_i) / l_jj, one warp
+  // backward: x_j = (y_j - sum_{i>j} l_ij x_i) / l_jj, one warp
   if (warp == 0) {
     for (int j = n - 1; j >= 0; --j) {
       double s = 0.0;
-      for (int i = j + 1 + lane; i < n; i += 32) s = fma(a[j * ld + i], xs[i], s);
+      for (int i = j + 1 + lane; i < n; i += 32) s = fma(L[i + j * n], xs[i], s);
       s = warp_sum(s);
-      if (lane == 0) xs[j] = dv(sub(a[j * ld + n], s), a[j * ld + j]);
+      if (lane == 0) xs[j] = dv(sub(y[j], s), L[j + j * n]);
       __syncwarp();
     }
   }
@@ -617,7 +668,7 @@ BatchCtx* batch_create(Ctx& base, int64_t B) {
     CMPC_CUDA(cudaMallocHost(&b->hstage, sizeof(double) * 4 * B));
     CMPC_CUDA(cudaMallocHost(&b->istage, sizeof(int) * B));
     CMPC_CUDA(cudaFuncSetAttribute(k_b_chol, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(double) * (kBatchMaxN * (kBatchMaxN + 2) + kBatchMaxN))));
+                                   (int)(sizeof(double) * (kBatchMaxN * kBatchMaxN + 2 * kBatchMaxN))));
     syrk_plan_batch(base, B, b->syrk, b->st);
     if (cublas().create(&b->blas) != 0) throw CudaError("batch: cublasCreate failed");
     cublas().set_stream(b->blas, b->st);
@@ -748,7 +799,7 @@ struct Host {
   void residuals_mu() {
     k_b_mu_rows<<<rows(), kBT, 0, b.st>>>(b.m, b.s, b.lam, b.z, b.mu, b.r2, b.part, b.act);
     CMPC_LAUNCHED();
-    k_b_kkt_mu<<<(unsigned)ceil_div(b.B, 128), 128, 0, b.st>>>(b.n, b.m, b.part, b.pk, b.act);
+    k_b_kkt_mu<<<(unsigned)ceil_div(b.B, 128), 128, 0, b.st>>>(b.B, b.n, b.m, b.part, b.pk, b.act);
     CMPC_LAUNCHED();
   }
   // sigma, omega, q, condensation with the right-hand side -r1 + J'(r2 - sigma r3)
@@ -766,7 +817,7 @@ struct Host {
   }
   void cholesky() {
     phase("chol", [&] {
-      const size_t sm = sizeof(double) * ((size_t)b.n * (b.n + 2) + b.n);
+      const size_t sm = sizeof(double) * ((size_t)b.n * b.n + 2 * b.n);
       k_b_chol<<<(unsigned)b.B, kCholT, sm, b.st>>>((int)b.n, b.M, b.delta, b.rhs, b.pv, b.pk, b.act);
       CMPC_LAUNCHED();
     });

@@ -42,7 +42,7 @@ constexpr int kBsColBoxes = 5;                     // 5 x 32 columns = 160 = kBa
 constexpr int kBsBox = 16 * 32 * 8;                // one {16 k, 32 cols} FP64 box (4 KB)
 constexpr int kBsStageP = 2 * kBsColBoxes * kBsBox;  // 32 k x 160 cols
 constexpr int kBsStageBytes = kBsStageP + 1024;      // + omega, q (256 B each), 1 KB aligned
-constexpr int kBsStages = 4;
+constexpr int kBsStages = 5;
 constexpr int kBsSmem = kBsStages * kBsStageBytes + 1024 /*align*/ + 2 * 8 * kBsStages /*barriers*/;
 static_assert(kBsStageP % 1024 == 0, "128B-swizzled boxes need 1 KB alignment");
 static_assert(kBsKC == kBK, "chunks must tile ldp");
@@ -342,6 +342,10 @@ void launch_condense_batch(Ctx& c, BatchSyrk& bs, cudaStream_t st, const double*
   a.r1 = r1;
   a.act = act;
   std::memcpy(a.reg, bs.reg, sizeof(a.reg));
+  if ((reinterpret_cast<uintptr_t>(omega) | reinterpret_cast<uintptr_t>(q) | (uintptr_t)(s_proto * 8)) & 15)
+    throw CudaError("batch condensation: omega/q not 16-byte aligned for the bulk copies (" +
+                    std::to_string(reinterpret_cast<uintptr_t>(omega) & 255) + ", " +
+                    std::to_string(reinterpret_cast<uintptr_t>(q) & 255) + ")");
   const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(c.tmap_P32);
   k_bsyrk<<<(unsigned)bs.B, kBsThreads, kBsSmem, st>>>(*tm, a);
   CMPC_LAUNCHED();
