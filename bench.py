@@ -380,13 +380,15 @@ def run_batch(args, rank, world, local, dist):
     barrier()
     l0 = _lib.launch_count()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters, biters = [], []
+    iters, biters, cstats = [], [], []
     with ClockSampler(local) as clk:
         st.record()
         for _ in range(args.steps):
             res = bs.solve(opts)
             iters.append(float(np.mean(res.iter)))
-            biters.append(getattr(bs, "last_stats", {}).get("batch_iterations", int(np.max(res.iter))))
+            ls = getattr(bs, "last_stats", {})
+            biters.append(ls.get("batch_iterations", int(np.max(res.iter))))
+            cstats.append(ls)
         torch.cuda.synchronize(local)
         en.record()
         en.synchronize()
@@ -435,6 +437,19 @@ def run_batch(args, rank, world, local, dist):
         "ms_per_batch_iteration": ms / args.steps / max(1, biters[-1]),
         "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e,
     }
+    if cstats and "condense_seconds" in cstats[-1]:
+        # the lockstep condensation kernel (csrc/bsyrk.cu): its algorithmic FLOPs (sum over the
+        # SYRK rows of hi (hi + 1) per instance it covered) over its CUDA-event time in the solves
+        sec = sum(c["condense_seconds"] for c in cstats)
+        nl = sum(c["condense_launches"] for c in cstats)
+        flops = sum(c["condense_instances"] * c["condense_flops_per_instance"] for c in cstats)
+        achieved = flops / sec / 1e12 if sec > 0 else 0.0
+        line["roofline"] = {
+            "bound": "tensor", "kernel": "k_bsyrk (lockstep condensation, one CTA per instance)",
+            "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+            "peak_source": "measured FP64 DMMA peak (profiles/r01_fp64_peak_probe.txt)",
+            "algorithmic_flops_per_launch": flops / max(1, nl), "avg_launch_ms": sec * 1e3 / max(1, nl),
+            "share_of_step": sec * 1e3 / ms if ms > 0 else None, "traffic": None}
     if not args.no_cpu_baseline and world == 1:
         one = P.build_dense_qp(data)
         s_ = cpu_sample(one, os.cpu_count() or 1, int(round(float(np.mean(iters)))))

@@ -87,8 +87,10 @@ int cmpc_solve_batch_affine(cmpc_ctx** ctxs, int nctx, int64_t count, const doub
  * by one: proj/src/verify.cpp:104-111 over proj/src/ipm.cpp:160-268 per instance). n <= 160.
  * set_affine: h_all count x n, h0_all count, d_all count x m (host, row per instance).
  * solve: v_out count x n (nullable), scal_out count x 14 (cmpc_solve's out_scalars: status,
- * iterations, kkt, objective), stats (nullable) 6: batch iterations, device seconds, wall
- * seconds, kernel launches, host syncs, device rounds. */
+ * iterations, kkt, objective), stats (nullable) 10: batch iterations, device seconds, wall
+ * seconds, kernel launches, host syncs, device rounds, the condensation kernel's device seconds,
+ * its launches, the instances it covered (summed over launches), its algorithmic FLOPs per
+ * instance (sum over the SYRK rows of hi (hi + 1)). */
 typedef struct cmpc_batch cmpc_batch;
 /* In-process loopback communicator (tests): `nranks` contexts on one device, each driven by
  * its own host thread, behave like the ranks of an NCCL communicator in the row-sharded solve

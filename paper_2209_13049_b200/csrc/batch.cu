@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
   double* L = bsm;            // L[i + j * n], i >= j
   double* y = bsm + n * n;    // forward-solve vector (rhs, then L^{-1} rhs)
   double* xs = y + n;         // n
+  double* rd = xs + n;        // 1 / l_jj
   __shared__ int s_fail;
   const int64_t b = blockIdx.x;
   if (!act[b]) return;
@@ -378,7 +379,9 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
   if (tid == 0) s_fail = -1;
   __syncthreads();
 
-  // column j (owner warp j % 32): l_jj = sqrt(a_jj), l_ij = a_ij / l_jj; forward solve step
+  // column j (owner warp j % 32): l_jj = sqrt(a_jj), l_ij = a_ij / l_jj (as a_ij * rsqrt(a_jj):
+  // the pivot chain is the kernel's critical path, one IEEE division per element would double
+  // it); forward solve step y_j = y_j / l_jj, y_i -= l_ij y_j
   auto finalize = [&](int j) {
     const int cj = j >> 5;
     double d = 0.0;
@@ -390,8 +393,8 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
       if (lane == 0) s_fail = j;
       return;
     }
-    const double ljj = sqrt(d);
-    const double yj = dv(y[j], ljj);
+    const double rl = rsqrt(d);
+    const double yj = mul(y[j], rl);
     __syncwarp();
 #pragma unroll
     for (int c = 0; c < kCholS; ++c) {
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
       for (int a = c; a < kCholS; ++a) {
         const int i = lane + 32 * a;
         if (i > j && i < n) {
-          const double l = dv(r[cslot(a, c)], ljj);
+          const double l = mul(r[cslot(a, c)], rl);
           r[cslot(a, c)] = l;
           L[i + j * n] = l;
           y[i] = fma(-l, yj, y[i]);
@@ -408,7 +411,8 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
       }
     }
     if (lane == 0) {
-      L[j + j * n] = ljj;
+      L[j + j * n] = sqrt(d);
+      rd[j] = rl;
       y[j] = yj;
     }
   };
@@ -423,6 +427,9 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
       const int i = lane + 32 * a;
       li[a] = i > j && i < n ? L[i + j * n] : 0.0;
     }
+    const bool owner = warp == ((j + 1) & 31);
+    // columns in increasing order: the owner's first live column is j + 1, finalized before
+    // its other columns are updated (they are off the critical path)
 #pragma unroll
     for (int c = 0; c < kCholS; ++c) {
       const int k = warp + 32 * c;
@@ -431,22 +438,33 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
 #pragma unroll
       for (int a = c; a < kCholS; ++a)
         if (lane + 32 * a >= k) r[cslot(a, c)] = fma(-li[a], lk, r[cslot(a, c)]);
+      if (owner && k == j + 1) finalize(j + 1);
     }
-    if (warp == ((j + 1) & 31)) finalize(j + 1);
     __syncthreads();
   }
   if (s_fail >= 0) {
     if (tid == 0) pk[b].info = s_fail + 1;
     return;
   }
-  // backward: x_j = (y_j - sum_{i>j} l_ij x_i) / l_jj, one warp
+  // backward (one warp, right-looking): x_j = y_j / l_jj, then y_i -= l_ji x_j for i < j; lane
+  // l keeps y_i for i = l + 32 a in registers and x_j reaches every lane by one shuffle
   if (warp == 0) {
+    double yr[kCholS];
+#pragma unroll
+    for (int a = 0; a < kCholS; ++a) yr[a] = lane + 32 * a < n ? y[lane + 32 * a] : 0.0;
     for (int j = n - 1; j >= 0; --j) {
-      double s = 0.0;
-      for (int i = j + 1 + lane; i < n; i += 32) s = fma(L[i + j * n], xs[i], s);
-      s = warp_sum(s);
-      if (lane == 0) xs[j] = dv(sub(y[j], s), L[j + j * n]);
-      __syncwarp();
+      double yj = 0.0;
+#pragma unroll
+      for (int a = 0; a < kCholS; ++a)
+        if (a == (j >> 5)) yj = yr[a];
+      yj = __shfl_sync(0xffffffffu, yj, j & 31);
+      const double xj = mul(yj, rd[j]);
+      if (lane == 0) xs[j] = xj;
+#pragma unroll
+      for (int a = 0; a < kCholS; ++a) {
+        const int i = lane + 32 * a;
+        if (i < j) yr[a] = fma(-L[j + i * n], xj, yr[a]);
+      }
     }
   }
   __syncthreads();
@@ -668,7 +686,7 @@ BatchCtx* batch_create(Ctx& base, int64_t B) {
     CMPC_CUDA(cudaMallocHost(&b->hstage, sizeof(double) * 4 * B));
     CMPC_CUDA(cudaMallocHost(&b->istage, sizeof(int) * B));
     CMPC_CUDA(cudaFuncSetAttribute(k_b_chol, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(double) * (kBatchMaxN * kBatchMaxN + 2 * kBatchMaxN))));
+                                   (int)(sizeof(double) * (kBatchMaxN * kBatchMaxN + 3 * kBatchMaxN))));
     syrk_plan_batch(base, B, b->syrk, b->st);
     if (cublas().create(&b->blas) != 0) throw CudaError("batch: cublasCreate failed");
     cublas().set_stream(b->blas, b->st);
@@ -711,13 +729,28 @@ struct Host {
   bool timed = getenv("CMPC_BATCH_TIMES") != nullptr;
   std::vector<std::pair<const char*, double>> acc;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
+  // device time of the condensation kernel (the bench's roofline), read after each sync
+  cudaEvent_t sy0 = nullptr, sy1 = nullptr;
+  double syrk_ms = 0.0, syrk_inst = 0.0;
+  long long syrk_launches = 0;
   explicit Host(BatchCtx& bb) : b(bb), c(*bb.base) {
+    CMPC_CUDA(cudaEventCreate(&sy0));
+    CMPC_CUDA(cudaEventCreate(&sy1));
     if (timed) {
       cudaEventCreate(&t0);
       cudaEventCreate(&t1);
     }
   }
+  void syrk_account(int64_t active) {  // after a sync: the iteration's condensation has run
+    float ms = 0.f;
+    CMPC_CUDA(cudaEventElapsedTime(&ms, sy0, sy1));
+    syrk_ms += ms;
+    syrk_inst += (double)active;
+    ++syrk_launches;
+  }
   ~Host() {
+    cudaEventDestroy(sy0);
+    cudaEventDestroy(sy1);
     if (timed) {
       for (auto& a : acc) fprintf(stderr, "[batch phase] %-10s %9.3f ms\n", a.first, a.second);
       cudaEventDestroy(t0);
@@ -813,11 +846,15 @@ struct Host {
                                                    b.sigma, b.w, b.omega, b.qw, b.act);
       CMPC_LAUNCHED();
     });
-    phase("syrk", [&] { launch_condense_batch(c, b.syrk, b.st, b.omega, b.qw, b.py, b.M, b.tq, b.rhs, b.r1, b.act); });
+    phase("syrk", [&] {
+      CMPC_CUDA(cudaEventRecord(sy0, b.st));
+      launch_condense_batch(c, b.syrk, b.st, b.omega, b.qw, b.py, b.M, b.tq, b.rhs, b.r1, b.act);
+      CMPC_CUDA(cudaEventRecord(sy1, b.st));
+    });
   }
   void cholesky() {
     phase("chol", [&] {
-      const size_t sm = sizeof(double) * ((size_t)b.n * b.n + 2 * b.n);
+      const size_t sm = sizeof(double) * ((size_t)b.n * b.n + 3 * b.n);
       k_b_chol<<<(unsigned)b.B, kCholT, sm, b.st>>>((int)b.n, b.M, b.delta, b.rhs, b.pv, b.pk, b.act);
       CMPC_LAUNCHED();
     });
@@ -949,6 +986,7 @@ void batch_solve(BatchCtx& b, const double* opts, int64_t max_iter, double* v_ou
     H.trial(true);
     H.read_packets(&syncs);
     ++rounds;
+    H.syrk_account(std::count(run.begin(), run.end(), 1));
     std::vector<Packet> Bp(b.pk_host, b.pk_host + B);
     // shift ladder (ipm.cpp:205-221): re-factor the failed instances with the next shift
     for (int64_t i = 0; i < B; ++i) shift[i] = 0;
@@ -1084,6 +1122,10 @@ void batch_solve(BatchCtx& b, const double* opts, int64_t max_iter, double* v_ou
     stats[3] = double(g_launches - launches0);
     stats[4] = double(syncs);
     stats[5] = double(rounds);
+    stats[6] = H.syrk_ms * 1e-3;
+    stats[7] = double(H.syrk_launches);
+    stats[8] = H.syrk_inst;
+    stats[9] = b.syrk.flops_per_instance;
   }
 }
 

@@ -639,14 +639,17 @@ class BatchSolver:
                 self._dirty = False
             v = np.zeros((cnt, n))
             scal = np.zeros((cnt, 14))
-            stats = np.zeros(6)
+            stats = np.zeros(10)
             od = (C.c_double * 5)(opts.tol, opts.mu_init, opts.kappa_mu, opts.tau, opts.armijo_eta)
             t0 = time.perf_counter()
             check(L.cmpc_batch_solve(self._batch, od, int(opts.max_iter), ptr(v), ptr(scal), ptr(stats)))
             wall = time.perf_counter() - t0
             self.last_stats = dict(batch_iterations=int(stats[0]), device_seconds=float(stats[1]),
                                    wall_seconds=float(stats[2]), launches=int(stats[3]),
-                                   syncs=int(stats[4]), rounds=int(stats[5]))
+                                   syncs=int(stats[4]), rounds=int(stats[5]),
+                                   condense_seconds=float(stats[6]), condense_launches=int(stats[7]),
+                                   condense_instances=float(stats[8]),
+                                   condense_flops_per_instance=float(stats[9]))
             return BatchResult(status=[IpmStatus(int(x)).name for x in scal[:, 0]], iter=scal[:, 1].astype(int),
                                objective=scal[:, 3].copy(), kkt_error=scal[:, 2].copy(), v=v,
                                device_seconds=np.full(cnt, float(stats[1]) / cnt), launches=int(stats[3]),
