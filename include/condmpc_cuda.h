@@ -34,6 +34,12 @@ long long cmpc_launch_count(void);
 /* context = the device-resident DenseQp + IpmState of one solve */
 int cmpc_ctx_create(cmpc_ctx** out, int device);
 void cmpc_ctx_destroy(cmpc_ctx* ctx);
+/* Per-context options (no process-wide switches): "jtl_recurrence" 1 (default) carries J'lambda
+ * across a step, 0 recomputes it by a pass over J as compute_residuals does (ipm.cpp:46-70);
+ * "rhs_pass" 0/1 (default) fuses J'(r2 - sigma r3) into the condensation, 2 runs it as its own
+ * pass; "graphs" 1 (default) replays the per-iteration segments as CUDA graphs, 0 launches them
+ * eagerly. Unknown keys or values: CMPC_ERR_DIM. Takes effect at the next solve. */
+int cmpc_ctx_set_option(cmpc_ctx* ctx, const char* key, int64_t value);
 
 /* Load DenseQp{H, h, h0, J, d} (proj/include/condmpc/reduction.hpp:25-33).
  * on_device = 0: host pointers (copied H2D); 1: device pointers (copied D2D).

@@ -76,6 +76,7 @@ SIGNATURES = {
     "cmpc_batch_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
     "cmpc_batch_set_affine": (C.c_int, [C.c_void_p, D, D, D]),
     "cmpc_batch_solve": (C.c_int, [C.c_void_p, D, C.c_int64, D, D, D]),
+    "cmpc_ctx_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "cmpc_batch_condense": (C.c_int, [C.c_void_p, D, D, D, D]),
     "cmpc_batch_destroy": (None, [C.c_void_p]),
     "cmpc_loop_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),

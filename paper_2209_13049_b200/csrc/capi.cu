@@ -298,6 +298,30 @@ int cmpc_recover_trajectory(cmpc_ctx* x, const double* v, double* xs, double* us
   });
 }
 
+int cmpc_ctx_set_option(cmpc_ctx* x, const char* key, int64_t value) {
+  return guard([&] {
+    if (!x || !key) throw DimError("null argument");
+    Ctx& c = x->c;
+    CMPC_CUDA(cudaSetDevice(c.device));
+    const std::string k(key);
+    if (k == "jtl_recurrence") {
+      if (value != 0 && value != 1) throw DimError("jtl_recurrence must be 0 or 1");
+      c.opt_jtl_recur = value == 1;
+      c.jtl_recur = c.m > 0 && c.opt_jtl_recur;
+    } else if (k == "rhs_pass") {
+      if (value < 0 || value > 2) throw DimError("rhs_pass must be 0, 1 or 2");
+      c.opt_rhs_pass = (int)value;
+    } else if (k == "graphs") {
+      if (value != 0 && value != 1) throw DimError("graphs must be 0 or 1");
+      c.opt_graphs = value == 1;
+    } else {
+      throw DimError("unknown option: " + k);
+    }
+    drop_graphs(c);  // captured segments hold the previous form
+    return CMPC_OK;
+  });
+}
+
 int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
   if (!src || !out) {
     g_error = "cmpc_ctx_clone: null context";
@@ -311,6 +335,9 @@ int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
     Ctx& c = x->c;
     require_loaded(const_cast<Ctx&>(s));
     CMPC_CUDA(cudaStreamSynchronize(s.stream));
+    c.opt_jtl_recur = s.opt_jtl_recur;
+    c.opt_rhs_pass = s.opt_rhs_pass;
+    c.opt_graphs = s.opt_graphs;
     c.n = s.n;
     c.m = s.m;
     c.h0 = s.h0;

@@ -116,6 +116,10 @@ struct Ctx {
   // the accepted step adds alpha J' p_lambda to Jtl, and the residual pass skips its J pass
   double* JtPl = nullptr;
   bool jtl_recur = false;  // unsharded with rows: the residual after a step reuses Jtl
+  // per-context options (cmpc_ctx_set_option; defaults = the measured best forms)
+  bool opt_jtl_recur = true;  // "jtl_recurrence": carry J'lambda (else the direct pass)
+  int opt_rhs_pass = 0;       // "rhs_pass": 0/1 = fused into the SYRK, 2 = its own pass over P
+  bool opt_graphs = true;     // "graphs": capture the per-iteration segments as CUDA graphs
   double *pv = nullptr, *ps_ = nullptr, *pl = nullptr, *pzd = nullptr, *Jpv = nullptr,
          *vt = nullptr, *yt = nullptr, *Hvt = nullptr;
   double* yv = nullptr;  // P v of the current point (prototype-indexed, like y = P pv)

@@ -82,10 +82,8 @@ void seg_step(Ctx& c, double tau) {
   // right-hand side P'q fused into the SYRK's diagonal jobs (with the plan's step weights
   // accounting for it: +4% of the SYRK at n = 500, +2% at n = 2000, against 14% and 3% for a
   // separate pass over P; tools/phases.py condense vs condense_rhs vs Jty).
-  // CMPC_RHS_PASS=separate|fused forces one form (tests/test_gpu_jtl_recurrence.py)
-  static const char* force = getenv("CMPC_RHS_PASS");
-  const bool want = force ? force[0] == 'f' : true;
-  const bool fused = c.ps > 0 && c.npieces > 0 && want;
+  // option "rhs_pass" = 2 forces the separate pass (tests/test_gpu_jtl_recurrence.py)
+  const bool fused = c.ps > 0 && c.npieces > 0 && c.opt_rhs_pass != 2;
   if (!fused) launch_rhs_partial(c);  // J'(r2 - sigma r3) by its own pass over P
   rec(c.ev2, c.stream);
   launch_condense(c, false, fused, c.ev4);
@@ -131,7 +129,7 @@ void run_segment(Ctx& c, cudaGraphExec_t& exec, long long& nodes, bool allow_cap
   }
   // (a loopback communicator synchronizes the ranks' streams with events across contexts,
   // which a per-context capture cannot hold)
-  if (!allow_capture || c.comm_loop || getenv("CMPC_NO_GRAPHS")) {
+  if (!allow_capture || c.comm_loop || !c.opt_graphs) {
     seg();
     return;
   }

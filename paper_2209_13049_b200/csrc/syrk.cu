@@ -491,9 +491,8 @@ void syrk_plan(Ctx& c) {
   // jobs: per lower tile (I,J), the rows whose prefix ends in the first half of column block I
   // (THIN: only output rows 0..31 are nonzero) and the rest (FULL)
   struct Job { int tile, ti, tj, thin, kb, ke; double w; };
-  // step weights (CMPC_SYRK_COST="full,thin,diag,diagthin" overrides them for tuning)
-  double cost_f = kCostFull, cost_t = kCostThin, cost_d = kCostDiag, cost_dt = kCostDiagThin;
-  if (const char* e = getenv("CMPC_SYRK_COST")) sscanf(e, "%lf,%lf,%lf,%lf", &cost_f, &cost_t, &cost_d, &cost_dt);
+  // step weights per segment shape (measured with tools/syrk_timeline.py)
+  const double cost_f = kCostFull, cost_t = kCostThin, cost_d = kCostDiag, cost_dt = kCostDiagThin;
   std::vector<Job> jobs;
   std::vector<int2> tiles;
   for (int tj = 0; tj < nt; ++tj)
@@ -522,10 +521,7 @@ void syrk_plan(Ctx& c) {
   for (double x : dens) work += x;
   // small problems (C2, C5: ~2 steps per slot) run fewer, longer pieces: fewer partial tiles
   // to reduce, and no dynamic tail
-  double tail_frac = work >= 16.0 * slots ? 0.1 : 0.0, min_piece = 3.0, min_body = 8.0;
-  if (const char* e = getenv("CMPC_SYRK_TAILFRAC")) tail_frac = std::min(1.0, std::max(0.0, atof(e)));
-  if (const char* e = getenv("CMPC_SYRK_MINBODY")) min_body = std::max(1.0, atof(e));
-  if (const char* e = getenv("CMPC_SYRK_MINPIECE")) min_piece = std::max(0.5, atof(e));
+  const double tail_frac = work >= 16.0 * slots ? 0.1 : 0.0, min_piece = 3.0, min_body = 8.0;
   int ksplit = nsteps_all;  // body = steps [0, ksplit)
   {
     double acc = 0.0;
@@ -664,8 +660,7 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
   a.ctl = c.syrk_ctl;
   a.partial = c.partial;
   a.prof = c.syrk_prof;
-  static const int stat = getenv("CMPC_SYRK_STATIC") ? atoi(getenv("CMPC_SYRK_STATIC")) : 0;
-  a.static_sched = stat;
+  a.static_sched = 0;
   a.ppi = std::max(1, c.npieces);
   a.s_omega = a.s_q = a.s_partial = a.s_rhs = 0;
   if (c.npieces > 0) {

@@ -935,8 +935,8 @@ void vec_alloc(Ctx& c) {
   const int rc = 2048;
   c.colchunks = (int)std::max<int64_t>(1, ceil_div(c.ps, rc));
   c.colpart = dev_zeros<double>((size_t)c.colchunks * n, c.stream);
-  // (and no communicator: checked at use); CMPC_NO_RECUR (debug): the residual's own J'lambda pass
-  c.jtl_recur = c.m > 0 && !getenv("CMPC_NO_RECUR");
+  // (and no communicator: checked at use); option "jtl_recurrence" = 0: the direct pass
+  c.jtl_recur = c.m > 0 && c.opt_jtl_recur;
   c.hmax = dev_zeros<double>(2, c.stream);  // max|h|, h0
   c.d_mu = dev_zeros<double>(1, c.stream);
   c.d_alpha = dev_zeros<double>(2, c.stream);

@@ -242,6 +242,13 @@ class DeviceQp:
         h, d = f64(h), f64(d)
         check(_lib.lib().cmpc_update_qp_affine(self.h, ptr(h), float(h0), ptr(d), 0))
 
+    def set_option(self, key: str, value: int):
+        """Per-context switches (no process-wide environment): "jtl_recurrence" (1: carry
+        J'lambda across a step, 0: recompute it by a pass over J as compute_residuals does),
+        "rhs_pass" (0/1: fused into the condensation, 2: its own pass over P), "graphs" (1:
+        CUDA-graph replay of the per-iteration segments, 0: eager launches)."""
+        check(_lib.lib().cmpc_ctx_set_option(self.h, key.encode(), int(value)))
+
     def set_state(self, st: IpmState):
         v, s, l, z = _state_arrays(st, self.n, self.m)
         check(_lib.lib().cmpc_set_state(self.h, ptr(v), ptr(s), ptr(l), ptr(z), float(st.mu)))

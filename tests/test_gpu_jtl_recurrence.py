@@ -3,8 +3,6 @@ J'lambda + alpha J'p_lambda with J'p_lambda = (M - H) pv - J'(r2 - sigma r3) ins
 over J. The reference recomputes J'lambda from lambda (ipm.cpp:46-70); the two must give the
 same solve: same iterations, iterates within the parity tolerance, and a final kkt that the
 direct residual pass confirms."""
-import os
-
 import numpy as np
 import pytest
 
@@ -15,15 +13,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _solve(qp, recur: bool):
-    if recur:
-        os.environ.pop("CMPC_NO_RECUR", None)
-    else:
-        os.environ["CMPC_NO_RECUR"] = "1"
-    try:
-        dq = ipm.DeviceQp(qp)  # the switch is read when the context loads the QP
-        return dq, dq.solve()
-    finally:
-        os.environ.pop("CMPC_NO_RECUR", None)
+    dq = ipm.DeviceQp(qp)
+    dq.set_option("jtl_recurrence", 1 if recur else 0)  # per context: no process-wide switch
+    return dq, dq.solve()
 
 
 @pytest.mark.parametrize("shape", [(12, 10, 14), (20, 25, 30)])
@@ -50,24 +42,29 @@ def test_carried_jtl_matches_the_direct_pass(shape):
 
 
 def test_separate_rhs_pass_matches_the_fused_one():
-    """n > 1024 takes a separate P'q pass instead of the SYRK-fused right-hand side (DESIGN §5);
-    run both forms at a small size (one process each: the switch is read once) and compare."""
-    import json
-    import subprocess
-    import sys
-    code = (
-        "import json, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
-        "from paper_2209_13049_b200 import ipm, problem as P;"
-        "qp = P.build_dense_qp(P.heat2d_problem(12, 10, T=14));"
-        "r = ipm.solve(qp);"
-        "print(json.dumps({'iter': r.iter, 'status': r.status.name, 'v': r.v.tolist(), 'obj': r.objective}))")
+    """the separate P'q pass (option rhs_pass = 2) against the SYRK-fused right-hand side, on
+    two contexts of one process (the options are per context)"""
+    qp = P.build_dense_qp(P.heat2d_problem(12, 10, T=14))
     out = {}
-    for mode in ("fused", "separate"):
-        env = dict(os.environ, CMPC_RHS_PASS=mode)
-        res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
-        assert res.returncode == 0, res.stderr[-2000:]
-        out[mode] = json.loads(res.stdout.strip().splitlines()[-1])
-    a, b = out["fused"], out["separate"]
-    assert a["status"] == b["status"] == "converged" and a["iter"] == b["iter"]
-    assert rel(np.array(a["v"]), np.array(b["v"])) <= 1e-9
-    assert abs(a["obj"] - b["obj"]) <= 1e-10 * (1 + abs(b["obj"]))
+    for mode in (1, 2):
+        dq = ipm.DeviceQp(qp)
+        dq.set_option("rhs_pass", mode)
+        out[mode] = dq.solve()
+        dq.close()
+    a, b = out[1], out[2]
+    assert a.status == b.status == ipm.IpmStatus.converged and a.iter == b.iter
+    assert rel(a.v, b.v) <= 1e-9
+    assert abs(a.objective - b.objective) <= 1e-10 * (1 + abs(b.objective))
+
+
+def test_options_are_per_context_and_checked():
+    qp = P.build_dense_qp(P.heat2d_problem(8, 6, T=8))
+    a, b = ipm.DeviceQp(qp), ipm.DeviceQp(qp)
+    a.set_option("graphs", 0)  # eager launches on a only
+    ra, rb = a.solve(), b.solve()
+    assert ra.iter == rb.iter and np.array_equal(ra.v, rb.v)  # same kernels, same order
+    for key, val in (("graphs", 2), ("rhs_pass", 3), ("no_such_option", 1)):
+        with pytest.raises(Exception):
+            a.set_option(key, val)
+    a.close()
+    b.close()
