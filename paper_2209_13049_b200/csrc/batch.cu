@@ -329,31 +329,42 @@ __global__ void k_b_sing_t(int64_t n, int64_t py, int64_t ldp, const int32_t* __
   }
 }
 
-// Cholesky of M_b + delta_b I in shared memory (one CTA per instance; the reference's pivot
-// rule "!(d > 0) || !isfinite(d)", proj/src/dense_linalg.cpp:24-40, first failure reported as
-// info = pivot + 1) and, when it succeeds, x = L^{-T} L^{-1} rhs_b. The right-hand side rides
-// along as an extra matrix row (row n of every column), so the forward solve is the rank-one
-// updates' own by-product; one barrier per pivot: step j updates the trailing matrix with the
-// raw column j scaled by 1/d_j, and scales column j (to l_ij = a_ij / sqrt(d_j)) in step j+1,
-// when nothing reads it any more.
-constexpr int kCholT = 1024;  // 32 warps: warp w owns the columns w + 32 c, lane l the rows l + 32 a
-constexpr int kCholS = 5;     // 32-row / 32-column slots: n <= 160
-__device__ __forceinline__ constexpr int cslot(int a, int c) { return a * (a + 1) / 2 + c; }
+constexpr int kCholT = 256;   // 8 warps: warp w owns the columns w + 8 c, lane l the rows l + 32 a
+constexpr int kCholW = kCholT / 32;
+constexpr int kCholA = 5;     // row slots: n <= 160
+constexpr int kCholC = 20;    // column slots
+// slot (a, c) exists when row block a can reach column w + 8 c (32 a + 31 >= 8 c)
+__device__ __forceinline__ constexpr int cslot(int a, int c) { return 2 * a * a + 2 * a + c; }
+constexpr int kCholSlots = cslot(kCholA, 0);
+
+__device__ __forceinline__ double b_rsqrt(double x) {  // MUFU seed + two Newton steps
+  if (!(x >= 1e-300 && x <= 1e300)) return 1.0 / sqrt(x);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
 
 // Per-instance Cholesky of M_b + delta_b I and both triangular solves with rhs_b (the
-// ReferenceBackend factorize + Factor::solve, proj/src/dense_linalg.cpp:59-77 and :102-110),
-// one CTA per instance. Right-looking with the trailing matrix in REGISTERS: thread (lane,
-// warp) holds the elements (lane + 32 a, warp + 32 c), a >= c, of the lower triangle (15
-// doubles); per pivot j one barrier: every thread applies column j of L (read from shared
-// memory, where its owner warp wrote it) to its elements, then the warp owning column j+1
-// forms it (pivot by shuffle, l = a / l_jj), stores it to shared memory and advances the
-// forward solve. The backward solve reads L from shared memory.
+// ReferenceBackend factorize + Factor::solve, proj/src/dense_linalg.cpp:59-77 and :102-110,
+// pivot rule "!(d > 0) || !isfinite(d)" with info = first failing pivot + 1), one CTA per
+// instance. Right-looking with the trailing matrix in REGISTERS: thread (lane, warp) holds the
+// elements (lane + 32 a, warp + 8 c) of its slots (60 doubles). Pivots run in blocks of 8
+// columns (one per warp) inside a loop unrolled over the column slot c, so the pivot column's
+// slot is a compile-time index. Per pivot j one barrier: the owner warp forms column j (pivot
+// by shuffle, l = a * rsqrt(a_jj)), stores it to shared memory and advances the forward solve;
+// after the barrier every thread applies it to all its slots — no per-element or per-column
+// predicates: entries above the diagonal and of finished columns are updated too and never
+// read. L lives in shared memory with an odd leading dimension (n + 1), so the backward solve's
+// row reads are conflict-free; it runs right-looking in one warp's registers.
 __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __restrict__ M,
                                                    const double* __restrict__ delta, const double* __restrict__ rhs,
                                                    double* __restrict__ x, Packet* pk, const int* __restrict__ act) {
   extern __shared__ double bsm[];
-  double* L = bsm;            // L[i + j * n], i >= j
-  double* y = bsm + n * n;    // forward-solve vector (rhs, then L^{-1} rhs)
+  const int ld = n + 1;
+  double* L = bsm;            // L[i + j * ld], i >= j
+  double* y = bsm + n * ld;   // forward-solve vector (rhs, then L^{-1} rhs)
   double* xs = y + n;         // n
   double* rd = xs + n;        // 1 / l_jj
   __shared__ int s_fail;
@@ -362,12 +373,12 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double dl = delta[b];
   const double* Mb = M + b * (int64_t)n * n;
-  double r[cslot(kCholS, 0)];
+  double r[kCholSlots];
 #pragma unroll
-  for (int a = 0; a < kCholS; ++a)
+  for (int a = 0; a < kCholA; ++a)
 #pragma unroll
-    for (int c = 0; c <= a; ++c) {
-      const int i = lane + 32 * a, k = warp + 32 * c;
+    for (int c = 0; c <= 4 * a + 3; ++c) {
+      const int i = lane + 32 * a, k = warp + kCholW * c;
       double v = 0.0;
       if (i < n && k < n && i >= k) {
         v = Mb[i + (int64_t)k * n];
@@ -379,68 +390,63 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
   if (tid == 0) s_fail = -1;
   __syncthreads();
 
-  // column j (owner warp j % 32): l_jj = sqrt(a_jj), l_ij = a_ij / l_jj (as a_ij * rsqrt(a_jj):
-  // the pivot chain is the kernel's critical path, one IEEE division per element would double
-  // it); forward solve step y_j = y_j / l_jj, y_i -= l_ij y_j
-  auto finalize = [&](int j) {
-    const int cj = j >> 5;
-    double d = 0.0;
+  bool failed = false;
 #pragma unroll
-    for (int c = 0; c < kCholS; ++c)
-      if (c == cj) d = r[cslot(c, c)];
-    d = __shfl_sync(0xffffffffu, d, j & 31);
-    if (!(d > 0.0) || !isfinite(d)) {
-      if (lane == 0) s_fail = j;
-      return;
-    }
-    const double rl = rsqrt(d);
-    const double yj = mul(y[j], rl);
-    __syncwarp();
+  for (int cb = 0; cb < kCholC; ++cb) {
+    if (failed || kCholW * cb >= n) break;
+    for (int jj = 0; jj < kCholW; ++jj) {
+      const int j = kCholW * cb + jj;
+      if (j >= n) break;
+      if (warp == jj) {  // column j: its slot index cb is a constant here
+        const int aj = j >> 5;
+        double d = 0.0;
 #pragma unroll
-    for (int c = 0; c < kCholS; ++c) {
-      if (c != cj) continue;
+        for (int a = 0; a < kCholA; ++a)
+          if (cb <= 4 * a + 3 && a == aj) d = r[cslot(a, cb)];
+        d = __shfl_sync(0xffffffffu, d, j & 31);
+        if (!(d > 0.0) || !isfinite(d)) {
+          if (lane == 0) s_fail = j;
+        } else {
+          const double rl = b_rsqrt(d);
+          const double yj = mul(y[j], rl);
+          __syncwarp();
 #pragma unroll
-      for (int a = c; a < kCholS; ++a) {
-        const int i = lane + 32 * a;
-        if (i > j && i < n) {
-          const double l = mul(r[cslot(a, c)], rl);
-          r[cslot(a, c)] = l;
-          L[i + j * n] = l;
-          y[i] = fma(-l, yj, y[i]);
+          for (int a = 0; a < kCholA; ++a) {
+            if (cb > 4 * a + 3) continue;
+            const int i = lane + 32 * a;
+            if (i > j && i < n) {
+              const double l = mul(r[cslot(a, cb)], rl);
+              L[i + j * ld] = l;
+              y[i] = fma(-l, yj, y[i]);
+            }
+          }
+          if (lane == 0) {
+            L[j + j * ld] = mul(d, rl);
+            rd[j] = rl;
+            y[j] = yj;
+          }
         }
       }
-    }
-    if (lane == 0) {
-      L[j + j * n] = sqrt(d);
-      rd[j] = rl;
-      y[j] = yj;
-    }
-  };
-
-  if (warp == 0) finalize(0);
-  __syncthreads();
-  for (int j = 0; j + 1 < n; ++j) {
-    if (s_fail >= 0) break;
-    double li[kCholS];
+      __syncthreads();
+      if (s_fail >= 0) {
+        failed = true;
+        break;
+      }
+      if (j + 1 >= n) break;
+      double li[kCholA];
 #pragma unroll
-    for (int a = 0; a < kCholS; ++a) {
-      const int i = lane + 32 * a;
-      li[a] = i > j && i < n ? L[i + j * n] : 0.0;
-    }
-    const bool owner = warp == ((j + 1) & 31);
-    // columns in increasing order: the owner's first live column is j + 1, finalized before
-    // its other columns are updated (they are off the critical path)
+      for (int a = 0; a < kCholA; ++a) {
+        const int i = lane + 32 * a;
+        li[a] = i > j && i < n ? L[i + j * ld] : 0.0;  // finished rows: no update
+      }
 #pragma unroll
-    for (int c = 0; c < kCholS; ++c) {
-      const int k = warp + 32 * c;
-      if (k <= j || k >= n) continue;  // warp-uniform
-      const double lk = L[k + j * n];
+      for (int c = 0; c < kCholC; ++c) {
+        const double lk = L[min(warp + kCholW * c, n - 1) + j * ld];
 #pragma unroll
-      for (int a = c; a < kCholS; ++a)
-        if (lane + 32 * a >= k) r[cslot(a, c)] = fma(-li[a], lk, r[cslot(a, c)]);
-      if (owner && k == j + 1) finalize(j + 1);
+        for (int a = 0; a < kCholA; ++a)
+          if (c <= 4 * a + 3) r[cslot(a, c)] = fma(-li[a], lk, r[cslot(a, c)]);
+      }
     }
-    __syncthreads();
   }
   if (s_fail >= 0) {
     if (tid == 0) pk[b].info = s_fail + 1;
@@ -449,21 +455,21 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
   // backward (one warp, right-looking): x_j = y_j / l_jj, then y_i -= l_ji x_j for i < j; lane
   // l keeps y_i for i = l + 32 a in registers and x_j reaches every lane by one shuffle
   if (warp == 0) {
-    double yr[kCholS];
+    double yr[kCholA];
 #pragma unroll
-    for (int a = 0; a < kCholS; ++a) yr[a] = lane + 32 * a < n ? y[lane + 32 * a] : 0.0;
+    for (int a = 0; a < kCholA; ++a) yr[a] = lane + 32 * a < n ? y[lane + 32 * a] : 0.0;
     for (int j = n - 1; j >= 0; --j) {
       double yj = 0.0;
 #pragma unroll
-      for (int a = 0; a < kCholS; ++a)
+      for (int a = 0; a < kCholA; ++a)
         if (a == (j >> 5)) yj = yr[a];
       yj = __shfl_sync(0xffffffffu, yj, j & 31);
       const double xj = mul(yj, rd[j]);
       if (lane == 0) xs[j] = xj;
 #pragma unroll
-      for (int a = 0; a < kCholS; ++a) {
+      for (int a = 0; a < kCholA; ++a) {
         const int i = lane + 32 * a;
-        if (i < j) yr[a] = fma(-L[j + i * n], xj, yr[a]);
+        if (i < j) yr[a] = fma(-L[j + i * ld], xj, yr[a]);
       }
     }
   }
@@ -686,7 +692,7 @@ BatchCtx* batch_create(Ctx& base, int64_t B) {
     CMPC_CUDA(cudaMallocHost(&b->hstage, sizeof(double) * 4 * B));
     CMPC_CUDA(cudaMallocHost(&b->istage, sizeof(int) * B));
     CMPC_CUDA(cudaFuncSetAttribute(k_b_chol, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(sizeof(double) * (kBatchMaxN * kBatchMaxN + 3 * kBatchMaxN))));
+                                   (int)(sizeof(double) * (kBatchMaxN * (kBatchMaxN + 1) + 3 * kBatchMaxN))));
     syrk_plan_batch(base, B, b->syrk, b->st);
     if (cublas().create(&b->blas) != 0) throw CudaError("batch: cublasCreate failed");
     cublas().set_stream(b->blas, b->st);
@@ -854,7 +860,7 @@ struct Host {
   }
   void cholesky() {
     phase("chol", [&] {
-      const size_t sm = sizeof(double) * ((size_t)b.n * b.n + 3 * b.n);
+      const size_t sm = sizeof(double) * ((size_t)b.n * (b.n + 1) + 3 * b.n);
       k_b_chol<<<(unsigned)b.B, kCholT, sm, b.st>>>((int)b.n, b.M, b.delta, b.rhs, b.pv, b.pk, b.act);
       CMPC_LAUNCHED();
     });
