@@ -97,8 +97,9 @@ constexpr int kLD = 36;          // staged-tile leading dimension (conflict-free
 constexpr int kTS = kB * kLD;    // doubles per staged tile
 constexpr int kT = 256;          // threads per CTA: warps 0-3 compute, 4-7 I/O (spine) / staging
 constexpr int kCT = 128;         // compute threads
-constexpr int kMaxFusedN = 288;  // the spine runs the backward solve up to this n (beyond it one
-                                 // SM's L2 bandwidth, ~22 GB/s, loses to per-block tasks)
+constexpr int kMaxFusedN = 768;  // the spine runs the backward solve up to this n (bundled bulk
+                                 // copies: n = 500 156 us vs 170 with per-block tasks; n = 1000
+                                 // 330 vs 321: beyond, the per-block tasks win)
 constexpr int kPartLen = 2 * 1024 + kB;  // pre-diagonal results: A_{d,d-1}, A_dd (fragment order), t_d
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -277,9 +278,12 @@ __device__ __forceinline__ bool wait_flags(const unsigned* f1, const unsigned* f
   }
 }
 __device__ __forceinline__ unsigned* tile_flag(const DfArgs& A, int i, int j) { return A.flags + i * A.nt + j; }
-__device__ __forceinline__ const double* tile_src(const DfArgs& A, int i, int j) {
-  return A.Lt + ((size_t)i * A.nt + j) * (kB * kB);
+// packed tiles column-major over the tile grid: tile (i, j) at (j nt + i), so the tiles below a
+// diagonal block (one block column) are contiguous for the backward solve's bulk copies
+__device__ __forceinline__ double* tile_ptr(const DfArgs& A, int i, int j) {
+  return A.Lt + ((size_t)j * A.nt + i) * (kB * kB);
 }
+__device__ __forceinline__ const double* tile_src(const DfArgs& A, int i, int j) { return tile_ptr(A, i, j); }
 // all threads of the CTA: the global writes before it become visible with the flag. The
 // barrier orders every thread's writes before thread 0's release store, which is cumulative;
 // no sequentially-consistent fence (MEMBAR.SC.GPU drains the SM's memory pipe and stalls the
@@ -404,7 +408,7 @@ __device__ bool df_panel(const DfArgs& A, int i, int j, unsigned target, double*
     frag_store(f, sm + kTP, out, 1.0);
   }
   __syncthreads();
-  double* Lt = A.Lt + ((size_t)i * A.nt + j) * (kB * kB);
+  double* Lt = tile_ptr(A, i, j);
   const int64_t r0 = (int64_t)kB * i, c0 = (int64_t)kB * j;
   for (int e = tid; e < kB * kB; e += kT) {
     const int r = e & 31, c = e >> 5;
@@ -707,7 +711,7 @@ __device__ bool spine_publish(const DfArgs& A, unsigned target, double* sm, vola
       nbar_sync(kBarPready + p, kPairCount);
       STRACE(k + 32, 1);
       const double* pk = sm + kSP + p * kTS;
-      double* Lt = A.Lt + ((size_t)k * A.nt + (k - 1)) * (kB * kB);
+      double* Lt = tile_ptr(A, k, k - 1);
       for (int e = t; e < kB * kB; e += kIOT) {
         const int r = e & 31, c = e >> 5;
         const double v = pk[c * kLD + r];
@@ -743,20 +747,23 @@ __device__ bool spine_publish(const DfArgs& A, unsigned target, double* sm, vola
 
 // backward solve on the spine: x_i = W_i^T (y_i - sum_{j>i} L_ji^T x_j), block i from the last
 // down, from the packed tiles of L. Per block the stream holds W_i (with y_i) and then the tiles
-// (j, i), j = nt-1 .. i+1; the items (independent of x) flow through a ring of kBSlots 8 KB
-// slots filled by 1-D bulk copies (one elected thread, full/empty mbarriers), so neither the L2
-// latency nor CTA-wide barriers are paid per tile. The loop issues no global load of its own:
-// the empty barrier's arrive is a release, and its fence would wait for any global load in
-// flight. Per tile, warp w sums columns 4w..4w+3 over the 32 rows (lane = row); per block,
-// fixed-order warp sums, then x_i = W_i^T t.
+// (j, i), j = nt-1 .. i+1, in BUNDLES of up to kBG tiles (one block column is contiguous, so a
+// bundle is one 1-D bulk copy): the items (independent of x) flow through a ring of kBSlots
+// slots (one elected thread, full/empty mbarriers), so neither the L2 latency nor CTA-wide
+// barriers are paid per tile, and the per-item cost (~0.2 us: wait, release, refill) is paid
+// per bundle (tools/exp/l2_stream.cu: one SM streams 1 MB in 10 us from 16 KB copies, 41 us
+// from 4 KB ones). The loop issues no global load of its own: the empty barrier's arrive is a
+// release, and its fence would wait for any global load in flight. Per tile, warp w sums
+// columns 4w..4w+3 over the 32 rows (lane = row), tiles in decreasing j; per block, fixed-order
+// warp sums, then x_i = W_i^T t.
 #ifndef CMPC_DIAG_BACK
 #define CMPC_DIAG_BACK 0
 #endif
-// the tiles come from the L2 at ~1-2 us effective latency (half from the other die's L2): the
-// ring keeps 18 items (144 KB) in flight
-constexpr int kBSlots = 24;
-constexpr int kBLag = 6;     // a slot is refilled kBLag items after it was read (no wait)
-constexpr int kBYs = kBSlots * kB * kB;   // y_i beside its W item: one 32-vector per slot
+constexpr int kBG = 4;        // tiles per bundle (32 KB)
+constexpr int kBSlots = 6;
+constexpr int kBLag = 2;      // a slot is refilled kBLag items after it was read (no wait)
+constexpr int kBSlot = kBG * kB * kB;     // doubles per slot
+constexpr int kBYs = kBSlots * kBSlot;    // y_i beside its W item: one 32-vector per slot
 constexpr int kBRed = kBYs + kBSlots * kB;
 constexpr int kBTv = kBRed + 8 * kB;
 constexpr int kBXs = kBTv + kB;
@@ -770,18 +777,20 @@ __device__ void spine_back(const DfArgs& A, double* sm, uint64_t* full, uint64_t
   double* tv = sm + kBTv;
   const int64_t n = A.n;
   const int nt = A.nt;
-  const int total = nt * (nt - 1) / 2 + nt;  // tiles + one W item per block
-  int pi = nt - 1, pj = nt;  // producer cursor: block pi, row pj (pj == nt: the W item)
+  int total = 0;  // one W item per block + its bundles
+  for (int i = 0; i < nt; ++i) total += 1 + (nt - 1 - i + kBG - 1) / kBG;
+  int pi = nt - 1, pj = nt;  // producer cursor: block pi, next tile row pj (pj == nt: the W item)
   auto issue = [&](int sl) {
     if (pj == nt) {
       mbar_expect_tx(full + sl, kB * kB * 8 + kB * 8);
-      bulk_load(sm + sl * (kB * kB), A.W + (size_t)pi * (kB * kB), kB * kB * 8, full + sl);
+      bulk_load(sm + sl * kBSlot, A.W + (size_t)pi * (kB * kB), kB * kB * 8, full + sl);
       bulk_load(sm + kBYs + sl * kB, A.ybuf + (size_t)kB * pi, kB * 8, full + sl);
       pj = nt - 1;
-    } else {
-      mbar_expect_tx(full + sl, kB * kB * 8);
-      bulk_load(sm + sl * (kB * kB), tile_src(A, pj, pi), kB * kB * 8, full + sl);
-      --pj;
+    } else {  // tiles (lo .. pj, pi): contiguous
+      const int lo = max(pi + 1, pj - kBG + 1), cnt = pj - lo + 1;
+      mbar_expect_tx(full + sl, (uint32_t)(cnt * kB * kB * 8));
+      bulk_load(sm + sl * kBSlot, tile_src(A, lo, pi), (uint32_t)(cnt * kB * kB * 8), full + sl);
+      pj = lo - 1;
     }
     if (pj == pi) {  // block pi done: the next block's W item
       --pi;
@@ -820,20 +829,23 @@ __device__ void spine_back(const DfArgs& A, double* sm, uint64_t* full, uint64_t
     {  // the W item: W_i (column-major) and y_i
       const int sl = q % kBSlots;
       mbar_wait(full + sl, (uint32_t)((q / kBSlots) & 1));
-      const double* X = sm + sl * (kB * kB);
+      const double* X = sm + sl * kBSlot;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) wv[cc] = X[(4 * warp + cc) * kB + lane];
       yv = sm[kBYs + sl * kB + lane];
       consumed();
     }
     double s4[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int j = nt - 1; j > i; --j) {
+    for (int hi = nt - 1; hi > i; hi -= kBG) {
+      const int lo = max(i + 1, hi - kBG + 1);
       const int sl = q % kBSlots;
       mbar_wait(full + sl, (uint32_t)((q / kBSlots) & 1));
-      const double* X = sm + sl * (kB * kB);  // column-major 32 x 32
-      const double xr = xs[(int64_t)kB * j + lane];
+      for (int j = hi; j >= lo; --j) {
+        const double* X = sm + sl * kBSlot + (j - lo) * (kB * kB);  // column-major 32 x 32
+        const double xr = xs[(int64_t)kB * j + lane];
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) s4[cc] = fma(X[(4 * warp + cc) * kB + lane], xr, s4[cc]);
+        for (int cc = 0; cc < 4; ++cc) s4[cc] = fma(X[(4 * warp + cc) * kB + lane], xr, s4[cc]);
+      }
       consumed();
     }
 #pragma unroll

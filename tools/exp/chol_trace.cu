@@ -65,7 +65,7 @@ int main(int argc, char** argv) {
     a.M = dM; a.L = dL; a.Lt = c.Lt; a.W = c.Winv; a.n = n; a.nt = nt; a.ybuf = c.df_y; a.x = dx; a.rhs = db;
     long long* dcyc = dev_zeros<long long>(1, c.stream);
     CMPC_CUDA(cudaFuncSetAttribute(k_back_only, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
-    for (int r = 0; r < 3; ++r) {
+    for (int r = 0; r < (n <= kMaxFusedN ? 3 : 0); ++r) {
       k_back_only<<<1, 256, kDfSmem, c.stream>>>(a, dcyc);
       long long cyc = 0;
       CMPC_CUDA(cudaMemcpyAsync(&cyc, dcyc, 8, cudaMemcpyDeviceToHost, c.stream));
