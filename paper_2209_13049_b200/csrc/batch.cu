@@ -478,14 +478,15 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
   if (tid == 0) pk[b].info = 0;
 }
 
-// recovery rows: Jpv, ps = -r3 - Jpv, plambda = -r2 + sigma (r3 + Jpv), pz = mu/s - z - sigma ps,
+// recovery rows: ps = -r3 - Jpv, plambda = -r2 + sigma (r3 + Jpv), pz = mu/s - z - sigma ps (J pv
+// itself is not stored: nothing downstream reads it),
 // fraction-to-boundary ratios and sum ps/s
 __global__ void __launch_bounds__(kBT) k_b_recover_rows(int64_t m, int64_t py, const int32_t* __restrict__ row_map,
                                                         const double* __restrict__ y, const double* __restrict__ s,
                                                         const double* __restrict__ z, const double* __restrict__ sigma,
                                                         const double* __restrict__ r2, const double* __restrict__ r3,
                                                         const double* __restrict__ mu_p, double tau,
-                                                        double* __restrict__ Jpv, double* __restrict__ ps,
+                                                        double* __restrict__ ps,
                                                         double* __restrict__ pl, double* __restrict__ pz,
                                                         double* __restrict__ part, const int* __restrict__ act) {
   __shared__ double sh[3 * 32];
@@ -498,7 +499,6 @@ __global__ void __launch_bounds__(kBT) k_b_recover_rows(int64_t m, int64_t py, c
     const int64_t o = b * m + r;
     const double jp = jrow_b(yb, row_map[r]);
     const double sr = s[o], zr = z[o], sg = sigma[o], t3 = r3[o];
-    Jpv[o] = jp;
     const double p_s = sub(-t3, jp);
     const double p_l = add(-r2[o], mul(sg, add(t3, jp)));
     const double p_z = sub(sub(mul(mu, dv(1.0, sr)), zr), mul(sg, p_s));
@@ -639,7 +639,7 @@ struct BatchCtx {
   double *h = nullptr, *h0 = nullptr, *d = nullptr, *hmax = nullptr;
   double *v = nullptr, *s = nullptr, *lam = nullptr, *z = nullptr, *r1 = nullptr, *r2 = nullptr, *r3 = nullptr;
   double *sigma = nullptr, *w = nullptr, *omega = nullptr, *qw = nullptr, *lp = nullptr, *tq = nullptr;
-  double *rhs = nullptr, *M = nullptr, *pv = nullptr, *ps = nullptr, *pl = nullptr, *pz = nullptr, *Jpv = nullptr;
+  double *rhs = nullptr, *M = nullptr, *pv = nullptr, *ps = nullptr, *pl = nullptr, *pz = nullptr;
   double *yv = nullptr, *y = nullptr, *Hv = nullptr, *Hvt = nullptr, *vt = nullptr, *Jtl = nullptr;
   double *part = nullptr, *mu = nullptr, *alpha = nullptr, *alpha_z = nullptr, *delta = nullptr;
   int* act = nullptr;
@@ -680,7 +680,7 @@ BatchCtx* batch_create(Ctx& base, int64_t B) {
     b->hmax = balloc<double>(*b, B);
     for (double** p : {&b->v, &b->r1, &b->rhs, &b->pv, &b->Hv, &b->Hvt, &b->vt, &b->Jtl, &b->tq})
       *p = balloc<double>(*b, B * n, true);
-    for (double** p : {&b->s, &b->lam, &b->z, &b->r2, &b->r3, &b->sigma, &b->w, &b->ps, &b->pl, &b->pz, &b->Jpv})
+    for (double** p : {&b->s, &b->lam, &b->z, &b->r2, &b->r3, &b->sigma, &b->w, &b->ps, &b->pl, &b->pz})
       *p = balloc<double>(*b, B * m, true);
     for (double** p : {&b->omega, &b->qw, &b->lp, &b->yv, &b->y}) *p = balloc<double>(*b, B * py, true);
     b->M = balloc<double>(*b, B * n * n, true);
@@ -872,7 +872,7 @@ struct Host {
   }
   void recover_rows(double tau) {
     k_b_recover_rows<<<rows(), kBT, 0, b.st>>>(b.m, b.py, c.row_map, b.y, b.s, b.z, b.sigma, b.r2, b.r3, b.mu, tau,
-                                               b.Jpv, b.ps, b.pl, b.pz, b.part, b.act);
+                                               b.ps, b.pl, b.pz, b.part, b.act);
     CMPC_LAUNCHED();
     k_b_recover_final<<<(unsigned)b.B, kBT, 0, b.st>>>(b.n, b.Hv, b.h, b.pv, b.part, b.pk, b.act);
     CMPC_LAUNCHED();
