@@ -82,7 +82,13 @@ __device__ __forceinline__ void bs_chunk(const unsigned char* st, const int (&of
   const double* sq = sw + 32;
 #pragma unroll
   for (int k4 = 0; k4 < kBsKC / 4; ++k4) {
-    const int k = 4 * k4 + t, kk = k & 15;
+    // the k rows of this step: 16-byte chunks c and c ^ 4 of the 128-byte row (c = k4 & 3), so
+    // that the lanes of each half-warp (g = 0..3 or 4..7, t = 0..3) hit 16 distinct 8-byte bank
+    // pairs through the 128B swizzle (chunk ^ g); rows 4 k4 .. 4 k4 + 3 would give chunks
+    // {c', c'+1} ^ g, shared by g and g ^ 1: two-way conflicts on every fragment load (ncu: 44%
+    // of the shared wavefronts; removing them did not move the kernel's time). Any assignment of
+    // the 32 rows to (k4, t) is valid as long as A, B, omega and q share it.
+    const int kk = 2 * (k4 & 3) + (t & 1) + 8 * (t >> 1), k = 16 * (k4 >> 2) + kk;
     // this lane's element (col, k) of an 8-column group: the 128B swizzle XORs the 16-byte
     // chunk index with col & 7 = g
     const unsigned char* base = st + (k4 >> 2) * (kBsColBoxes * kBsBox) + g * 128 +
@@ -170,9 +176,11 @@ __global__ void __launch_bounds__(kBsThreads, 1)
         for (int x = 0; x < 4; ++x) acc[r][h][x] = 0.0;
     double rq[2] = {0.0, 0.0};
 
+    int h_next = a.nchunks > 0 ? __ldg(&a.chunks[0].y) : 0;  // read one chunk ahead
     for (int c = 0; c < a.nchunks; ++c) {
       const int s = c % kBsStages;
-      const int h = __ldg(&a.chunks[c].y);
+      const int h = h_next;
+      if (c + 1 < a.nchunks) h_next = __ldg(&a.chunks[c + 1].y);
       int na = 0;
 #pragma unroll
       for (int r = 0; r < kBsRegs; ++r) na += 16 * rI[r] < h;
@@ -269,6 +277,8 @@ void syrk_plan_batch(Ctx& c, int64_t B, BatchSyrk& out, cudaStream_t st) {
   }
   out.nchunks = nch;
   // regions in activation order, dealt to the SM sub-partitions (warp % 4) by least load so far
+  // (balancing per warp instead — longest-processing-time over the 15 warps, then the warps
+  // over the sub-partitions — left the sub-partitions 8% apart and ran 6% slower)
   const int nr = (n + 15) / 16;
   std::vector<std::pair<int, int>> regs;
   for (int I = 0; I < nr; ++I)
