@@ -60,10 +60,6 @@ struct SyrkArgs {
   double* rhs_part;          // per segment: 2 x 64 half-sums of P' q (diagonal segments)
   long long* prof;           // debug: per piece {start ns, end ns, smid}
   int static_sched;          // debug: CTA b takes pieces b, b + grid, ... (no counter)
-  // lockstep batch (batch.cu): piece g is piece g % ppi of instance g / ppi; per-instance
-  // omega, q, partial and rhs_part live at these strides (0, ppi = npieces: one instance)
-  int ppi;
-  int64_t s_omega, s_q, s_partial, s_rhs;
 };
 
 // byte offset of element (col c, k) inside a 32 x 64 operand tile (two swizzled boxes)
@@ -74,10 +70,10 @@ __device__ __forceinline__ uint32_t op_off(int c, int k) {
 
 // Segment epilogue: store the accumulators as the segment's partial tile.
 template <int NF>
-__device__ __forceinline__ void store_partial(const SyrkArgs& a, int inst, int sg,
+__device__ __forceinline__ void store_partial(const SyrkArgs& a, int sg,
                                               const double (&acc)[NF][2][4], const int* fr,
                                               const int* fn, int lane) {
-  double* out = a.partial + inst * a.s_partial + (size_t)sg * (kTile * kTile);
+  double* out = a.partial + (size_t)sg * (kTile * kTile);
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int f = 0; f < NF; ++f)
@@ -100,7 +96,7 @@ __device__ __forceinline__ void store_partial(const SyrkArgs& a, int inst, int s
 //   THIN (diagonal):     the lower-left 32x32 block           -> 1 per warp
 template <int NF, bool DIAG, bool THIN>
 __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* smem, uint64_t* full,
-                                             uint64_t* empty, int it0, int inst, int sg, const int4 u,
+                                             uint64_t* empty, int it0, int sg, const int4 u,
                                              int warp, int lane) {
   const int nsteps = (u.z - u.y) / kBK;
   const int g = lane >> 2, t = lane & 3;
@@ -198,8 +194,8 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  store_partial<NF>(a, inst, sg, acc, fr, fn, lane);
-  if (DIAG && a.q) a.rhs_part[inst * a.s_rhs + (size_t)sg * 128 + threadIdx.x] = rq[0] + rq[1];
+  store_partial<NF>(a, sg, acc, fr, fn, lane);
+  if (DIAG && a.q) a.rhs_part[(size_t)sg * 128 + threadIdx.x] = rq[0] + rq[1];
 }
 
 // 2 CTAs per SM: 168 registers (each SM sub-partition holds 3 warps of 168 x 32; the few
@@ -242,9 +238,9 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
         ring[slot] = pg;
         mbar_arrive(&pfull[slot]);
         if (pg < 0) break;
-        const int inst = pg / a.ppi, p = pg - inst * a.ppi;
-        const double* omega = a.omega + inst * a.s_omega;
-        const double* qv = a.q ? a.q + inst * a.s_q : nullptr;
+        const int p = pg;
+        const double* omega = a.omega;
+        const double* qv = a.q;
         for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
           const int4 u = a.segs[sg];
           const int ti = u.x & 1023, tj = (u.x >> 10) & 1023;
@@ -290,18 +286,18 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&pempty[slot]);
     if (pg < 0) break;
-    const int inst = pg / a.ppi, p = pg - inst * a.ppi;
+    const int p = pg;
     long long t_start = 0;
     if (a.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
       const int4 u = a.segs[sg];
       const bool thin = (u.x >> 20) & 1, diag = (u.x & 1023) == ((u.x >> 10) & 1023);
       if (diag) {
-        if (thin) syrk_segment<1, true, true>(a, smem, full, empty, it0, inst, sg, u, warp, lane);
-        else syrk_segment<3, true, false>(a, smem, full, empty, it0, inst, sg, u, warp, lane);
+        if (thin) syrk_segment<1, true, true>(a, smem, full, empty, it0, sg, u, warp, lane);
+        else syrk_segment<3, true, false>(a, smem, full, empty, it0, sg, u, warp, lane);
       } else {
-        if (thin) syrk_segment<2, false, true>(a, smem, full, empty, it0, inst, sg, u, warp, lane);
-        else syrk_segment<4, false, false>(a, smem, full, empty, it0, inst, sg, u, warp, lane);
+        if (thin) syrk_segment<2, false, true>(a, smem, full, empty, it0, sg, u, warp, lane);
+        else syrk_segment<4, false, false>(a, smem, full, empty, it0, sg, u, warp, lane);
       }
       it0 += (u.z - u.y) / kBK;
     }
@@ -335,10 +331,6 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
 // partials hold rows 0..31 only (flag bit 31 of their id); a warp's 32 elements share one
 // row half, so the skip is warp-uniform.
 constexpr int kRedWays = 4;
-// lockstep batch: instance blockIdx.z at these strides (all 0 for one instance)
-struct RedStrides {
-  int64_t partial, proto, rp, M, vec;
-};
 __global__ void __launch_bounds__(256)
     k_syrk_reduce(const double* __restrict__ partial, const int2* __restrict__ tiles,
                   const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ tile_segs,
@@ -346,19 +338,8 @@ __global__ void __launch_bounds__(256)
                   double* __restrict__ M, int mirror, const double* __restrict__ rp,
                   const double* __restrict__ qs, const int32_t* __restrict__ sing_ptr,
                   const double* __restrict__ sing_val, double* __restrict__ tq,
-                  double* __restrict__ rhs, const double* __restrict__ r1, RedStrides bs) {
+                  double* __restrict__ rhs, const double* __restrict__ r1) {
   __shared__ double red[kRedWays][64];
-  {
-    const int64_t b = blockIdx.z;
-    partial += b * bs.partial;
-    omega_s += b * bs.proto;
-    M += b * bs.M;
-    if (rp) rp += b * bs.rp;
-    qs += b * bs.proto;
-    tq += b * bs.vec;
-    rhs += b * bs.vec;
-    if (r1) r1 += b * bs.vec;
-  }
   const int2 tl = tiles[blockIdx.x];
   const int u0 = tile_ptr[blockIdx.x], u1 = tile_ptr[blockIdx.x + 1];
   const int t64 = threadIdx.x & 63, way = threadIdx.x >> 6;
@@ -661,8 +642,6 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
   a.partial = c.partial;
   a.prof = c.syrk_prof;
   a.static_sched = 0;
-  a.ppi = std::max(1, c.npieces);
-  a.s_omega = a.s_q = a.s_partial = a.s_rhs = 0;
   if (c.npieces > 0) {
     const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(c.tmap_P);
     const CUtensorMap* tm32 = reinterpret_cast<const CUtensorMap*>(c.tmap_P32);
@@ -679,7 +658,7 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
   k_syrk_reduce<<<dim3(c.ntiles, kTile * kTile / 64), 64 * kRedWays, 0, c.stream>>>(
       c.partial, c.tiles, c.tile_ptr, c.tile_units, c.rank == 0 ? c.H : nullptr, c.omega + c.ldp, c.n, c.M,
       mirror ? 1 : 0, with_rhs ? c.rhs_part : nullptr, c.q + c.ldp, c.sing_ptr, c.sing_val, c.tq,
-      c.rhs, with_rhs && !c.comm ? c.r1 : nullptr, RedStrides{0, 0, 0, 0, 0});
+      c.rhs, with_rhs && !c.comm ? c.r1 : nullptr);
   CMPC_LAUNCHED();
 }
 
