@@ -3,13 +3,13 @@
 // BASELINE.json config 5 (1024 instances). The reference solves them one by one
 // (proj/src/verify.cpp:104-111 runs its thread pool over instances); here ONE host loop
 // drives all of them, every kernel covering every active instance in one launch:
-//   * the condensation is the SYRK kernel of syrk.cu with an instance dimension: P and its
-//     structure are shared (L2-resident at config 5, 7 MB), omega_b and q_b per instance,
-//     one segment per (tile, shape) job over its whole k range;
+//   * the condensation (bsyrk.cu) runs one CTA per instance holding its whole lower triangle
+//     in registers while P (shared, L2-resident at config 5, 14 MB) streams through TMA;
+//     H, the singleton terms and the right-hand side J'w are fused in;
 //   * the products with P and H are plain DGEMMs over the B right-hand sides (cuBLAS, loaded
 //     at run time): P X, P' Lambda, H V;
 //   * the Cholesky of each n x n matrix (n <= kBatchMaxN) and both triangular solves run in
-//     one CTA per instance with the matrix in shared memory;
+//     one CTA per instance with the trailing matrix in registers (k_b_chol);
 //   * the row passes (residuals, sigma, recovery, fraction to boundary, trials, update) are
 //     the single-instance formulas with blockIdx.y = instance and per-instance block sums
 //     reduced in a fixed order.

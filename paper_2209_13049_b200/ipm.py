@@ -567,9 +567,9 @@ class BatchSolver:
     receding-horizon / config-5 case (refresh_initial_state, reduction.cpp:270-280).
 
     mode "lockstep" (the default when n <= 160 and J has rows): ONE host loop drives every
-    instance, each kernel covering all active instances in one launch (csrc/batch.cu: the
-    condensation's SYRK with an instance dimension over the shared P, one CTA per instance
-    for the Cholesky, DGEMMs for the products with P and H); every instance still takes the
+    instance, each kernel covering all active instances in one launch (csrc/batch.cu,
+    csrc/bsyrk.cu: one CTA per instance for the condensation over the shared P and for the
+    Cholesky, DGEMMs for the products with P and H); every instance still takes the
     reference's decisions (ipm.cpp:160-268) on its own scalars.
     mode "workers": a few worker device contexts (cloned from the base QP's analysed
     structure, one host thread and one CUDA stream each) take the instances in turn, each
