@@ -130,3 +130,56 @@ def test_batch_condensation_matches_fp64(shape):
         tref = J.T @ w[b]
         terr = np.abs(tq[b] - tref).max() / (np.abs(J).T @ np.abs(w[b])).max()
         assert terr <= 1e-13, (b, terr)
+
+
+def _ragged_qp(n, m, seed):
+    """A random strictly convex QP whose constraint rows have ragged nonzero prefixes (widths
+    1..n, some repeated up to sign, some all-zero): exercises the batch kernels' region plan and
+    chunk widths away from the MPC layout."""
+    rng = np.random.default_rng(seed)
+    G = rng.standard_normal((n, n))
+    H = G @ G.T + n * np.eye(n)
+    J = rng.standard_normal((m, n))
+    widths = rng.integers(0, n + 1, size=m)
+    for r, w in enumerate(widths):
+        J[r, w:] = 0.0
+    J[m // 2: m // 2 + 10] = -J[:10]  # exact negations merge into one prototype
+    x0 = rng.standard_normal(n) * 0.1
+    d = J @ x0 + rng.uniform(0.5, 2.0, size=m)  # strictly feasible at x0
+    return P.DenseQp(H=H, h=rng.standard_normal(n), h0=0.0, J=J, d=d)
+
+
+@pytest.mark.parametrize("n", [2, 17, 37, 100, 160])
+def test_batch_kernels_ragged_shapes(n, O):
+    # the condensation and the Cholesky of the lockstep batch at n not a multiple of 16 / 32,
+    # up to the n = 160 limit: condensation vs fp64, every instance's solve vs its single
+    # solve and the oracle
+    base = _ragged_qp(n, 3 * n + 20, seed=n)
+    cnt = 5
+    rng = np.random.default_rng(7)
+    m = base.m
+    sigma = np.exp(rng.uniform(-4, 4, size=(cnt, m)))
+    w = rng.standard_normal((cnt, m))
+    bs = ipm.BatchSolver(base, cnt, mode="lockstep")
+    M, tq = bs.condense(sigma, w)
+    J, H = base.J, base.H
+    for b in range(cnt):
+        ref = H + J.T @ (sigma[b][:, None] * J)
+        lo = np.tril_indices(n)
+        scale = np.abs(H).max() + (np.abs(J).T @ (sigma[b][:, None] * np.abs(J))).max()
+        assert np.abs(M[b][lo] - ref[lo]).max() <= 1e-13 * scale
+        assert np.abs(tq[b] - J.T @ w[b]).max() <= 1e-13 * (np.abs(J).T @ np.abs(w[b])).max()
+    qps = []
+    for i in range(cnt):
+        q = P.DenseQp(H=base.H, h=base.h + 0.1 * rng.standard_normal(n), h0=0.0, J=base.J,
+                      d=base.d + 0.05 * rng.uniform(0, 1, size=m))
+        qps.append(q)
+        bs.set_instance(i, q.h, q.h0, q.d)
+    res = bs.solve()
+    bs.close()
+    for i, q in enumerate(qps):
+        single = ipm.solve(q)
+        o = O.solve(oracle_qp(O, q))
+        assert res.status[i] == single.status.name == o.status
+        assert res.iter[i] == single.iter == o.iter
+        assert rel(res.v[i], o.v) <= 1e-8
