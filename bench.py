@@ -638,7 +638,14 @@ def main():
 
     avg_syrk_s = syrk_s / max(syrk_n, 1)
     avg_syrk_k = syrk_k / max(syrk_n, 1)
-    achieved = info["syrk_flops"] / avg_syrk_k / 1e12
+    small = syrk_n == 0  # the one-CTA solver (csrc/small.cu): the whole solve is one kernel
+    if small:
+        # its condensation FLOPs per solve over the kernel's whole (latency-bound) duration
+        avg_syrk_k = avg_syrk_s = ms_total * 1e-3 / max(args.steps, 1)
+        flops_launch = info["syrk_flops"] * iters[-1]
+    else:
+        flops_launch = info["syrk_flops"]
+    achieved = flops_launch / avg_syrk_k / 1e12
     line = {
         "metric": "ms per MPC solve", "value": value, "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -649,15 +656,18 @@ def main():
                       "p_mb": info["p_bytes"] / 1e6},
         "ms_per_iter": ms_total / max(sum(iters), 1) * (1 if world == 1 else 1),
         "iterations": iters[-1], "status": status,
-        "roofline": {"bound": "tensor", "kernel": "k_syrk (the condensation's SYRK, right-hand side fused)",
+        "roofline": {"bound": "tensor",
+                     "kernel": ("k_small_ipm (the whole solve in one CTA: latency-bound; its condensation "
+                                "FLOPs over its duration)") if small else
+                               "k_syrk (the condensation's SYRK, right-hand side fused)",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS,
                      "peak_source": "measured FP64 DMMA peak (mma.sync m16n8k16.f64, "
                                     "profiles/r01_fp64_peak_probe.txt); MEASURED_PEAKS.json has no FP64 entry",
-                     "algorithmic_flops_per_launch": info["syrk_flops"],
+                     "algorithmic_flops_per_launch": flops_launch,
                      "avg_launch_ms": avg_syrk_k * 1e3,
                      "condensation_ms": avg_syrk_s * 1e3,
-                     "condensation_frac": info["syrk_flops"] / avg_syrk_s / 1e12 / FP64_PEAK_TFLOPS,
+                     "condensation_frac": flops_launch / avg_syrk_s / 1e12 / FP64_PEAK_TFLOPS,
                      "share_of_step": syrk_k / max(t_local, 1e-30),
                      "traffic": None},
         "phase_ms_per_iter": {"condense": syrk_s * 1e3 / max(sum(iters), 1),

@@ -83,9 +83,10 @@ void release_qp(Ctx& c) {
   vec_free(c);
   syrk_free(c);
   free_structure(c);
-  for (double* p : {c.H, c.h, c.d}) dev_free(p, c.stream);
+  for (double* p : {c.H, c.h, c.d, c.Jsmall, c.small_log, c.small_res}) dev_free(p, c.stream);
   if (c.J && c.owns_J) dev_free(c.J, c.stream);
-  c.H = c.h = c.J = c.d = nullptr;
+  c.H = c.h = c.J = c.d = c.Jsmall = c.small_log = c.small_res = nullptr;
+  c.small_log_cap = 0;
   c.n = c.m = 0;
 }
 
@@ -163,8 +164,18 @@ int load_impl(Ctx& c, int64_t n, int64_t m, const double* H, const double* h, do
     if (!c.J && prob_rows(c)) analyze_structure_built(c, *prob_rows(c));  // built: J never stored
     else analyze_structure(c);
     tick("analyze");
-    // the dense J is not read again: every product goes through P
-    dev_free(c.J, c.stream);
+    // the dense J is not read again by the general path (every product goes through P); a
+    // QP small enough for the one-CTA solver keeps it (small.cu)
+    if (c.J && small_fits(n, m)) {
+      if (c.owns_J) {
+        c.Jsmall = c.J;
+      } else {
+        c.Jsmall = dev_alloc<double>((size_t)std::max<int64_t>(1, m * n), c.stream);
+        CMPC_CUDA(cudaMemcpyAsync(c.Jsmall, c.J, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c.stream));
+      }
+    } else if (c.owns_J) {
+      dev_free(c.J, c.stream);
+    }
     c.J = nullptr;
     syrk_plan(c);
     tick("plan");
@@ -314,6 +325,9 @@ int cmpc_ctx_set_option(cmpc_ctx* x, const char* key, int64_t value) {
     } else if (k == "graphs") {
       if (value != 0 && value != 1) throw DimError("graphs must be 0 or 1");
       c.opt_graphs = value == 1;
+    } else if (k == "small_path") {
+      if (value != 0 && value != 1) throw DimError("small_path must be 0 or 1");
+      c.opt_small = value == 1;
     } else {
       throw DimError("unknown option: " + k);
     }
@@ -338,6 +352,7 @@ int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
     c.opt_jtl_recur = s.opt_jtl_recur;
     c.opt_rhs_pass = s.opt_rhs_pass;
     c.opt_graphs = s.opt_graphs;
+    c.opt_small = s.opt_small;
     c.n = s.n;
     c.m = s.m;
     c.h0 = s.h0;
@@ -360,6 +375,7 @@ int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
     c.d = dup(s.d, size_t(s.m));
     c.J = nullptr;
     c.P = dup(s.P, size_t(s.ldp * s.n));
+    if (s.Jsmall) c.Jsmall = dup(s.Jsmall, size_t(std::max<int64_t>(1, s.m * s.n)));
     c.hi = dup(s.hi, size_t(s.ps));
     c.start_col = dup(s.start_col, size_t(s.n + 1));
     c.row_map = dup(s.row_map, size_t(s.m));

@@ -120,6 +120,12 @@ struct Ctx {
   bool opt_jtl_recur = true;  // "jtl_recurrence": carry J'lambda (else the direct pass)
   int opt_rhs_pass = 0;       // "rhs_pass": 0/1 = fused into the SYRK, 2 = its own pass over P
   bool opt_graphs = true;     // "graphs": capture the per-iteration segments as CUDA graphs
+  bool opt_small = true;      // "small_path": whole solve in one CTA when the QP fits (small.cu)
+  // small.cu: the dense J kept for the one-CTA solver (null when the QP does not fit)
+  double* Jsmall = nullptr;
+  double* small_log = nullptr;
+  int64_t small_log_cap = 0;
+  double* small_res = nullptr;
   double *pv = nullptr, *ps_ = nullptr, *pl = nullptr, *pzd = nullptr, *Jpv = nullptr,
          *vt = nullptr, *yt = nullptr, *Hvt = nullptr;
   double* yv = nullptr;  // P v of the current point (prototype-indexed, like y = P pv)
@@ -176,6 +182,11 @@ void syrk_plan(Ctx& c);
 // M(lower) = H + P' diag(omega) P + (singleton diagonal); writes full symmetric M when mirror
 void launch_condense(Ctx& c, bool mirror, bool with_rhs = false, cudaEvent_t after_syrk = nullptr);
 void syrk_free(Ctx& c);
+// ---- small.cu: the whole IPM loop in one CTA for QPs that fit in shared memory
+bool small_fits(int64_t n, int64_t m);
+int small_solve(Ctx& c, const double* opts, int64_t max_iter, double* v_out, double* s_out, double* lam_out,
+                double* z_out, double* out, cmpc_log_fn log, void* user);
+
 // ---- bsyrk.cu: lockstep-batch condensation (batch.cu): B instances sharing H and P, one CTA
 // per instance; per-instance omega/q in prototype space at stride s_proto, M (n x n lower),
 // tq, rhs and r1 (n) at their natural strides; inactive instances (act = 0) are skipped

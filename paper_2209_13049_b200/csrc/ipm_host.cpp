@@ -238,6 +238,9 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   require(mu_init > 0.0, "mu_init must be positive");
   require(max_iter >= 1, "max_iter must be at least 1");
 
+  // QPs that fit in one CTA's shared memory: the whole loop on the device (small.cu)
+  if (!inspect && c.opt_small && c.Jsmall && !c.comm)
+    return small_solve(c, opts, max_iter, v_out, s_out, lam_out, z_out, out, log, user);
   const long long launches0 = g_launches;
   long long syncs = 0, trials = 0;
   const int64_t n = c.n, m = c.m;
