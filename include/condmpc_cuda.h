@@ -38,7 +38,10 @@ void cmpc_ctx_destroy(cmpc_ctx* ctx);
  * across a step, 0 recomputes it by a pass over J as compute_residuals does (ipm.cpp:46-70);
  * "rhs_pass" 0/1 (default) fuses J'(r2 - sigma r3) into the condensation, 2 runs it as its own
  * pass; "graphs" 1 (default) replays the per-iteration segments as CUDA graphs, 0 launches them
- * eagerly. Unknown keys or values: CMPC_ERR_DIM. Takes effect at the next solve. */
+ * eagerly; "small_path" 1 (default) runs the whole solve in one CTA (every decision on the
+ * device, the log hook replayed afterwards) for QPs with n <= 32 whose J fits in shared memory
+ * when no inspect hook is given, 0 never. Unknown keys or values: CMPC_ERR_DIM. Takes effect at
+ * the next solve. */
 int cmpc_ctx_set_option(cmpc_ctx* ctx, const char* key, int64_t value);
 
 /* Load DenseQp{H, h, h0, J, d} (proj/include/condmpc/reduction.hpp:25-33).
