@@ -765,6 +765,7 @@ struct Host {
   }
   template <typename F>
   void phase(const char* name, F&& f) {
+    NvtxRange nv(name);
     if (!timed) {
       f();
       return;
@@ -928,6 +929,7 @@ void batch_solve(BatchCtx& b, const double* opts, int64_t max_iter, double* v_ou
   if (!(tau > 0.0 && tau < 1.0)) throw DimError("tau must lie in (0,1)");
   if (!(mu_init > 0.0)) throw DimError("mu_init must be positive");
   if (max_iter < 1) throw DimError("max_iter must be at least 1");
+  NvtxRange nv("cmpc_batch_solve");
   Host H(b);
   const int64_t B = b.B, n = b.n, m = b.m;
   const long long launches0 = g_launches;

@@ -121,6 +121,7 @@ int load_impl(Ctx& c, int64_t n, int64_t m, const double* H, const double* h, do
     if (n < 0 || m < 0) throw DimError("negative dimensions");
     if (m > (int64_t(1) << 29) || n > (int64_t(1) << 24)) throw DimError("QP too large");
     CMPC_CUDA(cudaSetDevice(c.device));
+    NvtxRange nv("cmpc_load_qp (upload, structure analysis, SYRK plan)");
     const double t_in = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     release_qp(c);
     if (getenv("CMPC_VERBOSE"))

@@ -18,6 +18,8 @@
 #include <cstdint>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "../../include/condmpc_cuda.h"
 
@@ -47,6 +49,14 @@ static_assert(offsetof(Packet, sum_abs_r3) == offsetof(Packet, sum_log_s) + 8, "
 static_assert(offsetof(Packet, max_z) == offsetof(Packet, max_r3) + 32, "packet layout");
 static_assert(offsetof(Packet, alpha_z_min) == offsetof(Packet, alpha_s_min) + 8, "packet layout");
 static_assert(offsetof(Packet, t_sum_abs) == offsetof(Packet, t_sum_log) + 8, "packet layout");
+
+// NVTX range for profilers (nsys / ncu --nvtx); header-only NVTX 3, free without a tool attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct Workspace;
 struct ProblemDev;

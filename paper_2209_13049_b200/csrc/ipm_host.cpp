@@ -77,6 +77,7 @@ void rec(cudaEvent_t e, cudaStream_t s) {
 // into the SYRK (its diagonal jobs stream every nonzero row of P), Cholesky (delta = 0)
 // fused with the solve, recovery + fraction to boundary, trial 0
 void seg_step(Ctx& c, double tau) {
+  NvtxRange nv("cmpc: condense + factor + step + trial 0");
   rec(c.ev0, c.stream);
   launch_prepare_step(c, nullptr);
   // right-hand side P'q fused into the SYRK's diagonal jobs (with the plan's step weights
@@ -113,6 +114,7 @@ void seg_step(Ctx& c, double tau) {
 
 // segment B: the accepted step (alpha, alpha_z on the device) and the residuals after it
 void seg_next(Ctx& c) {
+  NvtxRange nv("cmpc: update + residuals");
   launch_update_dev(c);
   launch_residuals(c, /*reuse_trial=*/true);
   launch_publish(c);
@@ -238,6 +240,7 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   require(mu_init > 0.0, "mu_init must be positive");
   require(max_iter >= 1, "max_iter must be at least 1");
 
+  NvtxRange nv_solve("cmpc_solve");
   // QPs that fit in one CTA's shared memory: the whole loop on the device (small.cu)
   if (!inspect && c.opt_small && c.Jsmall && !c.comm)
     return small_solve(c, opts, max_iter, v_out, s_out, lam_out, z_out, out, log, user);
@@ -303,6 +306,7 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   };
   gap_mark_end();
   while (true) {
+    NvtxRange nv_iter("cmpc: IPM iteration");
     // check_termination (ipm.cpp:153-158)
     if (A.kkt <= tol && c.mu <= tol) {
       status = 0;

@@ -445,6 +445,7 @@ bool small_fits(int64_t n, int64_t m) {
 
 int small_solve(Ctx& c, const double* opts, int64_t max_iter, double* v_out, double* s_out, double* lam_out,
                 double* z_out, double* out, cmpc_log_fn log, void* user) {
+  NvtxRange nv("cmpc_solve: one-CTA solver");
   const int64_t n = c.n, m = c.m;
   const double t0 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
   if (c.small_log_cap < max_iter) {
