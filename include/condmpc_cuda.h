@@ -40,8 +40,11 @@ void cmpc_ctx_destroy(cmpc_ctx* ctx);
  * pass; "graphs" 1 (default) replays the per-iteration segments as CUDA graphs, 0 launches them
  * eagerly; "small_path" 1 (default) runs the whole solve in one CTA (every decision on the
  * device, the log hook replayed afterwards) for QPs with n <= 32 whose J fits in shared memory
- * when no inspect hook is given, 0 never. Unknown keys or values: CMPC_ERR_DIM. Takes effect at
- * the next solve. */
+ * when no inspect hook is given, 0 never; "speculate" 1 (default) enqueues the step update and
+ * the next residual pass behind the factor/step segment before the host has seen the step,
+ * gated on the device's own evaluation of line-search trial 0 (the host re-checks it and
+ * finishes the line search itself when trial 0 is refused), 0 waits for the host's decision.
+ * Unknown keys or values: CMPC_ERR_DIM. Takes effect at the next solve. */
 int cmpc_ctx_set_option(cmpc_ctx* ctx, const char* key, int64_t value);
 
 /* Load DenseQp{H, h, h0, J, d} (proj/include/condmpc/reduction.hpp:25-33).

@@ -329,6 +329,9 @@ int cmpc_ctx_set_option(cmpc_ctx* x, const char* key, int64_t value) {
     } else if (k == "small_path") {
       if (value != 0 && value != 1) throw DimError("small_path must be 0 or 1");
       c.opt_small = value == 1;
+    } else if (k == "speculate") {
+      if (value != 0 && value != 1) throw DimError("speculate must be 0 or 1");
+      c.opt_spec = value == 1;
     } else {
       throw DimError("unknown option: " + k);
     }
@@ -354,6 +357,7 @@ int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
     c.opt_rhs_pass = s.opt_rhs_pass;
     c.opt_graphs = s.opt_graphs;
     c.opt_small = s.opt_small;
+    c.opt_spec = s.opt_spec;
     c.n = s.n;
     c.m = s.m;
     c.h0 = s.h0;

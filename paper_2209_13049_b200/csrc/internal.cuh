@@ -131,6 +131,7 @@ struct Ctx {
   int opt_rhs_pass = 0;       // "rhs_pass": 0/1 = fused into the SYRK, 2 = its own pass over P
   bool opt_graphs = true;     // "graphs": capture the per-iteration segments as CUDA graphs
   bool opt_small = true;      // "small_path": whole solve in one CTA when the QP fits (small.cu)
+  bool opt_spec = true;       // "speculate": enqueue update + residuals behind the step segment
   // small.cu: the dense J kept for the one-CTA solver (null when the QP does not fit)
   double* Jsmall = nullptr;
   double* small_log = nullptr;
@@ -144,7 +145,9 @@ struct Ctx {
   int colchunks = 0;
   double* hmax = nullptr;
   double* d_mu = nullptr;    // barrier value on the device (kernels read it: graph-safe)
-  double* d_alpha = nullptr; // accepted step lengths {alpha, alpha_z} on the device
+  // accepted step {alpha, alpha_z, go} on the device, then the residual pass's merit snapshot
+  // {max_lam, v'Hv, h'v, sum log s, sum |r3|} (trial0_decide)
+  double* d_alpha = nullptr;
   double* stage = nullptr;   // pinned ring for the host -> device scalars (mu, alpha): a copy from
   int stage_i = 0;           // pageable memory is staged and synchronous, from pinned a plain DMA
   // CUDA graphs of the two per-iteration segments (captured on the second iteration)
@@ -153,6 +156,7 @@ struct Ctx {
   cudaGraphExec_t g_step = nullptr, g_next = nullptr;
   long long g_step_nodes = 0, g_next_nodes = 0;
   double g_tau = 0.0;
+  double g_eta = 0.0;  // eta baked into the captured seg_step (trial0_decide)
   double* Winv = nullptr;    // inverses of the 32 x 32 diagonal blocks of L
   double* Lt = nullptr;      // packed 32 x 32 off-diagonal tiles of L (dataflow Cholesky)
   unsigned* df_flags = nullptr;  // per-tile done flags (generation stamped)
@@ -166,6 +170,8 @@ struct Ctx {
   Packet* pk = nullptr;      // device packet
   Packet* pk_host = nullptr; // pinned, device-mapped mirror
   Packet* pk_map = nullptr;  // device address of pk_host (k_publish writes it directly)
+  Packet* pk_host_b = nullptr;  // second mirror: seg_step's publish (packet B)
+  Packet* pk_map_b = nullptr;
   volatile unsigned long long* pub_host = nullptr;  // mapped publish sequence number
   unsigned long long* pub_map = nullptr;            // its device address
   unsigned long long* pub_dev = nullptr;            // device-side publish counter
@@ -255,14 +261,15 @@ inline int64_t rows_all(const Ctx& c) { return c.m_all >= 0 ? c.m_all : c.m; }
 void launch_zero_packet(Ctx& c);
 // copy the packet into the mapped host mirror and bump the publish sequence (the host spins
 // on it instead of a stream synchronize + D2H copy); returns the sequence value to wait for
-unsigned long long launch_publish(Ctx& c);
+unsigned long long launch_publish(Ctx& c, bool slot_b = false);
 // max |h| (after h changed)
 void launch_hmax(Ctx& c);
 // set the barrier value (host copy and the device scalar the kernels read)
 void set_mu(Ctx& c, double mu);
 // residuals at the current state (r1, r2, r3, kkt, objective pieces) -> packet A;
 // reuse_trial: the state was just moved to the last evaluated line-search trial point
-void launch_residuals(Ctx& c, bool reuse_trial = false);
+// gated: nothing runs unless the step was taken (d_alpha[2] != 0; the speculative seg_next)
+void launch_residuals(Ctx& c, bool reuse_trial = false, bool gated = false);
 // r2 and complementarity only (after a barrier change) -> packet kkt at the new mu, from the
 // residual maxima of `a` (the current point's residual packet) and the recomputed max_comp
 void launch_residuals_mu(Ctx& c, const Packet& a);
@@ -288,7 +295,9 @@ void prob_free(Ctx& c);
 
 void launch_reset_packet_all(Ctx& c);
 void launch_debug_sum(Ctx& c, const double* x, int64_t n, int slot);
-void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear = false);
+// decide: also the speculative trial-0 acceptance into d_alpha (trial0_decide, vec.cu)
+void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear = false,
+                  bool decide = false, double eta = 0.0);
 // line-search derivative pieces for externally set directions: (Hv+h).pv, sum ps/s
 void launch_ls_pieces(Ctx& c);
 // v = 0, s = max(1, d), z = mu / s, lambda = z (ipm.cpp:170-177)

@@ -75,8 +75,9 @@ void rec(cudaEvent_t e, cudaStream_t s) {
 
 // segment A: sigma/omega/q, condensation with the right-hand side J'(r2 - sigma r3) fused
 // into the SYRK (its diagonal jobs stream every nonzero row of P), Cholesky (delta = 0)
-// fused with the solve, recovery + fraction to boundary, trial 0
-void seg_step(Ctx& c, double tau) {
+// fused with the solve, recovery + fraction to boundary, trial 0 and the device's verdict on
+// it (trial0_decide), published into the second packet slot
+void seg_step(Ctx& c, double tau, double eta) {
   NvtxRange nv("cmpc: condense + factor + step + trial 0");
   rec(c.ev0, c.stream);
   launch_prepare_step(c, nullptr);
@@ -108,15 +109,19 @@ void seg_step(Ctx& c, double tau) {
   rec(c.ev1, c.stream);
   launch_recover(c, tau);
   launch_debug_sum(c, c.ps_, c.m, 3);
-  launch_trial(c, 0.0, true, /*linear=*/true);
-  launch_publish(c);
+  launch_trial(c, 0.0, true, /*linear=*/true, /*decide=*/true, eta);
+  launch_publish(c, /*slot_b=*/true);
 }
 
-// segment B: the accepted step (alpha, alpha_z on the device) and the residuals after it
+// seg_next may run gated on the device's trial-0 verdict: every kernel in it then checks it
+bool seg_next_gated(const Ctx& c) { return !c.comm && (c.m == 0 || c.jtl_recur); }
+
+// segment B: the accepted step (alpha, alpha_z on the device) and the residuals after it;
+// nothing runs when d_alpha[2] = 0 (a speculative launch whose trial 0 the device refused)
 void seg_next(Ctx& c) {
   NvtxRange nv("cmpc: update + residuals");
   launch_update_dev(c);
-  launch_residuals(c, /*reuse_trial=*/true);
+  launch_residuals(c, /*reuse_trial=*/true, /*gated=*/seg_next_gated(c));
   launch_publish(c);
 }
 
@@ -260,8 +265,13 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
   // init (ipm.cpp:170-177)
   set_mu(c, mu_init);
   launch_init_state(c, c.mu);
-  if (c.g_tau != tau) drop_graphs(c);
+  if (c.g_tau != tau || c.g_eta != eta) drop_graphs(c);
   c.g_tau = tau;
+  c.g_eta = eta;
+  // speculation: seg_next is enqueued right behind seg_step and applies the step only if the
+  // device accepted trial 0; an inspect hook needs the state before the step, a communicator
+  // allreduces the trial's sums after the verdict would be taken
+  const bool spec = c.opt_spec && !inspect && seg_next_gated(c);
   // from here every segment ends in k_publish, which also resets the packet's accumulated
   // maxima / minima: the per-phase reset kernels drop out of the iteration graphs
   launch_reset_packet_all(c);
@@ -326,7 +336,8 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     // speculatively: directions, recovery, fraction to boundary, line-search trial 0
     size_t shift = 0;
     gap_mark_begin();
-    run_segment(c, c.g_step, c.g_step_nodes, iter >= 1, [&] { seg_step(c, tau); });
+    run_segment(c, c.g_step, c.g_step_nodes, iter >= 1, [&] { seg_step(c, tau, eta); });
+    if (spec) run_segment(c, c.g_next, c.g_next_nodes, iter >= 1, [&] { seg_next(c); });
     gap_mark_end();
     wait_published(c, c.pub_expect, &syncs);
     float ms = 0.f;
@@ -339,7 +350,26 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
     ++syrk_launches;
     CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev3, c.ev1));
     chol_s += ms * 1e-3;
-    while (c.pk_host->info != 0) {
+    Packet B = *c.pk_host_b;
+    if (spec && B.pad[6] != 0.0) {  // the device took trial 0: the step is already applied
+      const double alpha_max = std::min(1.0, B.alpha_s_min);
+      double alpha = 0.0;
+      int nt = 0;
+      // the host's own verdict on the same packet (no launch when it agrees)
+      const int j = run_line_search(c, A, B.d_gpv, B.d_ps_s, alpha_max, eta, &B, &alpha, &nt, &syncs);
+      if (j != 0 || alpha != alpha_max)
+        throw CudaError("speculative step: the device accepted line-search trial 0, the host did not");
+      trials += nt;
+      const double mu_used = c.mu;
+      iter += 1;
+      A = *c.pk_host;
+      if (log) {
+        const double rec[8] = {double(iter), mu_used, alpha, std::min(1.0, B.alpha_z_min), A.kkt, A.objective, 0.0, 0.0};
+        log(user, rec);
+      }
+      continue;
+    }
+    while (B.info != 0) {
       if (++shift == kShifts.size()) break;
       CMPC_CUDA(cudaEventRecord(c.ev0, c.stream));
       launch_cholesky(c, c.M, c.L, kShifts[shift], c.rhs, c.pv);
@@ -347,10 +377,10 @@ int solve_loop(Ctx& c, const double* opts, int64_t max_iter, double* v_out, doub
       launch_recover(c, tau);
       launch_trial(c, 0.0, true, /*linear=*/true);
       sync_packet(c, &syncs);
+      B = *c.pk_host;
       CMPC_CUDA(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
       linalg += ms * 1e-3;
     }
-    const Packet B = *c.pk_host;
     static const bool debug_sums = getenv("CMPC_DEBUG_SUMS") != nullptr;
     if (debug_sums) {  // per-iteration checksums of the step's buffers (tools/race_sums.py)
       const unsigned long long* u = reinterpret_cast<const unsigned long long*>(B.pad);

@@ -282,8 +282,10 @@ __global__ void __launch_bounds__(kRowT) k_res_rows(int64_t m, const int32_t* __
                                                     const double* __restrict__ z,
                                                     const double* __restrict__ mu_p,
                                                     double* __restrict__ r2, double* __restrict__ r3,
-                                                    double* __restrict__ part, Packet* pk) {
+                                                    double* __restrict__ part, Packet* pk,
+                                                    const double* __restrict__ gate) {
   __shared__ double sh[7 * 32];
+  if (gate && gate[2] == 0.0) return;  // (speculative segment whose step was not taken)
   const double mu = *mu_p;
   double sabs = 0.0, slog = 0.0, ml = 0.0, mss = 0.0, mz = 0.0, mr3 = 0.0, mc = 0.0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
@@ -459,8 +461,10 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, i
                                                      double* __restrict__ r1,
                                                      const double* __restrict__ part,
                                                      const double* __restrict__ hmax, Packet* pk,
-                                                     int mode) {
+                                                     int mode, const double* __restrict__ gate,
+                                                     double* __restrict__ snap) {
   __shared__ double sh[5 * 32];
+  if (gate && gate[2] == 0.0) return;
   double sabs = 0.0, slog = 0.0;
   if (mode != 2)
     for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
@@ -510,6 +514,13 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, i
       kkt = fmax(kkt, pk->max_comp / cs);
     }
     pk->kkt = kkt;
+    if (snap) {  // the merit pieces of this point for trial0_decide
+      snap[0] = pk->max_lam;
+      snap[1] = vhv;
+      snap[2] = hv;
+      snap[3] = pk->sum_log_s;
+      snap[4] = pk->sum_abs_r3;
+    }
   }
 }
 
@@ -691,11 +702,48 @@ __global__ void __launch_bounds__(kRowT) k_trial_rows(int64_t m, const int32_t* 
   if (__syncthreads_or(bad) && threadIdx.x == 0) pk->any_nonpos = 1;
 }
 
+// speculative acceptance of trial 0 (host loop, seg_step): the first pass of the reference's
+// accept loop (ipm.cpp:129-143) exactly as run_line_search evaluates it on the host, same
+// operations in the same order, from the step packet and the residual snapshot dec[3..7]
+// that k_res_final left ({max_lam, v'Hv, h'v, sum log s, sum |r3|} of the current point).
+// Writes dec = {alpha, alpha_z, go}: with go != 0 the update + residual segment the host
+// enqueued behind this one applies the step; with go = 0 it does nothing and the host runs
+// the rest of the line search (or the shift ladder) and sets go itself (set_alpha).
+__device__ void trial0_decide(Packet* pk, bool rows, double mu, double eta, double* dec) {
+  const double alpha = fmin(1.0, pk->alpha_s_min), alpha_z = fmin(1.0, pk->alpha_z_min);
+  int go = 0;
+  if (pk->info == 0 && !(rows && pk->any_nonpos)) {
+    const double rho = add(mul(10.0, dec[3]), 1.0);
+    double phi0 = add(mul(0.5, dec[4]), dec[5]);
+    double derivative = pk->d_gpv;
+    double phi = add(mul(0.5, pk->t_vHv), pk->t_hv);
+    if (rows) {
+      phi0 = sub(phi0, mul(mu, dec[6]));
+      phi0 = add(phi0, mul(rho, dec[7]));
+      derivative = sub(derivative, mul(mu, pk->d_ps_s));
+      derivative = sub(derivative, mul(rho, dec[7]));
+      phi = sub(phi, mul(mu, pk->t_sum_log));
+      phi = add(phi, mul(rho, pk->t_sum_abs));
+    }
+    constexpr double band = 10.0 * 2.220446049250313080847e-16;  // 10 DBL_EPSILON
+    if (derivative <= 0.0 && phi <= add(phi0, mul(mul(eta, alpha), derivative)))
+      go = 1;
+    else if (fabs(sub(phi, phi0)) <= mul(band, add(1.0, fabs(phi0))))
+      go = 1;
+  }
+  dec[0] = alpha;
+  dec[1] = alpha_z;
+  dec[2] = go ? 1.0 : 0.0;
+  pk->pad[6] = go ? 1.0 : 0.0;
+}
+
 __global__ void __launch_bounds__(kFinT) k_trial_final(int64_t n, int64_t m, int nparts,
                                                        const double* __restrict__ vt,
                                                        const double* __restrict__ Hvt,
                                                        const double* __restrict__ h,
-                                                       const double* __restrict__ part, Packet* pk) {
+                                                       const double* __restrict__ part, Packet* pk,
+                                                       const double* __restrict__ mu_p,
+                                                       double* dec, double eta) {
   __shared__ double sh[5 * 32];
   double a = 0.0, b = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -714,6 +762,7 @@ __global__ void __launch_bounds__(kFinT) k_trial_final(int64_t n, int64_t m, int
     pk->t_hv = su[1];
     pk->t_sum_abs = m > 0 ? su[2] : 0.0;
     pk->t_sum_log = m > 0 ? su[3] : 0.0;
+    if (dec) trial0_decide(pk, m > 0, *mu_p, eta, dec);
   }
 }
 
@@ -725,6 +774,7 @@ __global__ void k_update(int64_t n, int64_t m, const double* __restrict__ ap, do
                          const double* __restrict__ y, double* __restrict__ Jtl,
                          const double* __restrict__ JtPl, double* __restrict__ Hv,
                          const double* __restrict__ Hvt) {
+  if (ap[2] == 0.0) return;  // trial 0 not accepted: the host finishes the line search first
   const double alpha = ap[0], alpha_z = ap[1];
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) v[i] = add(v[i], mul(alpha, pv[i]));
@@ -867,8 +917,10 @@ __global__ void __launch_bounds__(1024) k_trial_hv(const double* __restrict__ H,
 // Mapped pinned blocks (packet, sequence word, 64-double staging ring) are recycled across
 // loads and contexts: cudaHostAlloc costs milliseconds, a load should not.
 namespace {
-constexpr size_t kStageOff = (sizeof(Packet) + 64 + 127) / 128 * 128;
-constexpr size_t kPinnedBytes = kStageOff + 64 * sizeof(double);
+// [packet A][sequence word][packet B (seg_step's publish)][staging ring]
+constexpr size_t kPkBOff = (sizeof(Packet) + 64 + 127) / 128 * 128;
+constexpr size_t kStageOff = (kPkBOff + sizeof(Packet) + 127) / 128 * 128;
+constexpr size_t kPinnedBytes = kStageOff + 128 * sizeof(double);
 std::mutex g_pinned_mu;
 std::vector<void*> g_pinned_free;
 
@@ -939,7 +991,7 @@ void vec_alloc(Ctx& c) {
   c.jtl_recur = c.m > 0 && c.opt_jtl_recur;
   c.hmax = dev_zeros<double>(2, c.stream);  // max|h|, h0
   c.d_mu = dev_zeros<double>(1, c.stream);
-  c.d_alpha = dev_zeros<double>(2, c.stream);
+  c.d_alpha = dev_zeros<double>(8, c.stream);  // alpha, alpha_z, go, residual snapshot[5]
   c.pk = dev_zeros<Packet>(1, c.stream);
   tick("vectors");
   {  // packet + sequence word + staging ring: one mapped pinned block from the process pool
@@ -951,6 +1003,8 @@ void vec_alloc(Ctx& c) {
   CMPC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.pk_map), c.pk_host, 0));
   c.pub_host = reinterpret_cast<volatile unsigned long long*>(reinterpret_cast<char*>(c.pk_host) + sizeof(Packet));
   c.pub_map = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(c.pk_map) + sizeof(Packet));
+  c.pk_host_b = reinterpret_cast<Packet*>(reinterpret_cast<char*>(c.pk_host) + kPkBOff);
+  c.pk_map_b = reinterpret_cast<Packet*>(reinterpret_cast<char*>(c.pk_map) + kPkBOff);
   *c.pub_host = 0;
   c.pub_dev = dev_zeros<unsigned long long>(1, c.stream);
   c.pub_expect = 0;
@@ -1011,7 +1065,7 @@ void vec_free(Ctx& c) {
   c.nbig = 0;
   dev_free(c.pub_dev, c.stream);
   c.pub_dev = nullptr;
-  c.pk_map = nullptr;
+  c.pk_map = c.pk_map_b = nullptr;
   c.pub_host = nullptr;
   c.pub_map = nullptr;
   chol_free(c);
@@ -1019,7 +1073,7 @@ void vec_free(Ctx& c) {
   c.omega = c.q = c.tq = c.JtPl = c.rhs = c.M = c.L = c.pv = c.ps_ = c.pl = c.pzd = nullptr;
   c.Jpv = c.vt = c.yt = c.yv = c.Hvt = c.part = c.colpart = c.hmax = c.d_mu = c.d_alpha = nullptr;
   c.pk = nullptr;
-  c.pk_host = nullptr;
+  c.pk_host = c.pk_host_b = nullptr;
   c.Mpack = nullptr;
 }
 
@@ -1046,8 +1100,9 @@ __global__ void k_publish(const Packet* pk, Packet* out, unsigned long long* dev
   }
 }
 
-unsigned long long launch_publish(Ctx& c) {
-  k_publish<<<1, 32, 0, c.stream>>>(c.pk, c.pk_map, c.pub_dev, c.pub_map, c.pk_autoreset ? 1 : 0);
+unsigned long long launch_publish(Ctx& c, bool slot_b) {
+  k_publish<<<1, 32, 0, c.stream>>>(c.pk, slot_b ? c.pk_map_b : c.pk_map, c.pub_dev, c.pub_map,
+                                    c.pk_autoreset ? 1 : 0);
   CMPC_LAUNCHED();
   return ++c.pub_expect;
 }
@@ -1144,7 +1199,8 @@ void launch_Jtq(Ctx& c, const double* q, double* out) {
   CMPC_LAUNCHED();
 }
 
-void launch_residuals(Ctx& c, bool reuse_trial) {
+void launch_residuals(Ctx& c, bool reuse_trial, bool gated) {
+  const double* gate = gated ? c.d_alpha : nullptr;
   const unsigned pb = part_blocks(c.m);
   const int64_t m_all = rows_all(c);
   if (!c.pk_autoreset) {  // (in the host loop, k_publish starts every segment clean)
@@ -1158,9 +1214,10 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
   if (c.m > 0) {
     if (!reuse_trial) launch_Jx(c, c.v, c.yv, nullptr);
     k_res_rows<<<pb, kRowT, 0, c.stream>>>(c.m, c.row_map, c.yv, c.d, c.s, c.lam, c.z, c.d_mu, c.r2,
-                                           c.r3, c.part, c.pk);
+                                           c.r3, c.part, c.pk, gate);
     CMPC_LAUNCHED();
-    if (!(reuse_trial && c.jtl_recur && !c.comm)) {  // (after a step: Jtl was advanced by k_update)
+    if (!(reuse_trial && c.jtl_recur && !c.comm)) {
+      if (gated) throw CudaError("gated residual pass needs the J'lambda recurrence");  // (after a step: Jtl was advanced by k_update)
       launch_proto_reduce<true, false>(c, c.lam, nullptr, c.q, nullptr);
       launch_Jtq(c, c.q, c.Jtl);
     }
@@ -1171,7 +1228,7 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
   if (c.comm) {
     // this rank's rows: J_g' lambda_g, the row sums and maxima -> allreduce -> finalize
     k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part,
-                                           c.hmax, c.pk, 1);
+                                           c.hmax, c.pk, 1, gate, nullptr);
     CMPC_LAUNCHED();
     comm_group(c, true);
     comm_allreduce(c, c.Jtl, (size_t)c.n, CommType::f64, CommOp::sum);
@@ -1180,7 +1237,7 @@ void launch_residuals(Ctx& c, bool reuse_trial) {
     comm_group(c, false);
   }
   k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part,
-                                         c.hmax, c.pk, c.comm ? 2 : 0);
+                                         c.hmax, c.pk, c.comm ? 2 : 0, gate, c.d_alpha + 3);
   CMPC_LAUNCHED();
 }
 
@@ -1227,10 +1284,10 @@ void launch_rhs(Ctx& c) {
   launch_rhs_final(c);
 }
 
-// a slot of the pinned staging ring (64 doubles, 2 per slot): the host loop synchronises
+// a slot of the pinned staging ring (128 doubles, 4 per slot): the host loop synchronises
 // with the stream between segments, so a slot is never reused while its copy is pending
 double* stage_slot(Ctx& c, int) {
-  double* p = c.stage + 2 * (c.stage_i & 31);
+  double* p = c.stage + 4 * (c.stage_i & 31);
   ++c.stage_i;
   return p;
 }
@@ -1276,7 +1333,7 @@ void launch_recover(Ctx& c, double tau) {
   }
 }
 
-void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear) {
+void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear, bool decide, double eta) {
   const Packet* apk = alpha_from_device ? c.pk : nullptr;
   if (!c.pk_autoreset) {  // (in the host loop, k_publish starts every segment clean)
     k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 2);
@@ -1307,7 +1364,8 @@ void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear) {
     CMPC_LAUNCHED();
   }
   k_trial_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m, c.m > 0 ? (int)pb : 0, c.vt, c.Hvt, c.h,
-                                           c.part, c.pk);
+                                           c.part, c.pk, c.d_mu,
+                                           decide && !c.comm ? c.d_alpha : nullptr, eta);
   CMPC_LAUNCHED();
   if (c.comm) {  // merit row sums and the slack-positivity flag over every rank's rows
     comm_group(c, true);
@@ -1352,7 +1410,8 @@ void set_alpha(Ctx& c, double alpha, double alpha_z) {
   double* st = stage_slot(c, 2);
   st[0] = alpha;
   st[1] = alpha_z;
-  CMPC_CUDA(cudaMemcpyAsync(c.d_alpha, st, 2 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  st[2] = 1.0;  // the step is taken (k_update's gate)
+  CMPC_CUDA(cudaMemcpyAsync(c.d_alpha, st, 3 * sizeof(double), cudaMemcpyHostToDevice, c.stream));
 }
 
 void launch_update_dev(Ctx& c) {

@@ -247,7 +247,9 @@ class DeviceQp:
         J'lambda across a step, 0: recompute it by a pass over J as compute_residuals does),
         "rhs_pass" (0/1: fused into the condensation, 2: its own pass over P), "graphs" (1:
         CUDA-graph replay of the per-iteration segments, 0: eager launches), "small_path" (1:
-        the whole solve in one CTA when n <= 32 and J fits in shared memory, 0: never)."""
+        the whole solve in one CTA when n <= 32 and J fits in shared memory, 0: never),
+        "speculate" (1: the step update and next residual pass are enqueued before the host
+        has seen the step, gated on the device's evaluation of line-search trial 0; 0: off)."""
         check(_lib.lib().cmpc_ctx_set_option(self.h, key.encode(), int(value)))
 
     def set_state(self, st: IpmState):
