@@ -471,6 +471,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--T", type=int, default=200, help="config 4's horizon (50, 100, 150, 200)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-markov", action="store_true",
+                    help="skip the device-built (Markov table) leg")
     ap.add_argument("--mode", default="auto", choices=["auto", "shard", "replica"],
                     help="N > 1: shard = rows of J split across the GPUs, one solve (configs 3/4, "
                          "the default there); replica = an independent instance per GPU")
@@ -631,6 +633,34 @@ def main():
                        "note": "build_dense_qp + solve + recover_trajectory on the device (median); "
                                "the reference cannot build this QP (bigAtilde alone is 127 GB at config 3)"}
 
+    # the same QP built on the device with the Markov table as the prototype source (SURVEY
+    # §8(f) row 2: P never stored), device-resident solves timed like the main leg
+    markov = None
+    if not args.no_markov and cfg in ("c2", "c3", "c4", "c5"):
+        dqm = ipm.DeviceQp.from_problem(data, device=local, options={"markov": 2})
+        mi = dqm.info()
+        if mi["markov"]:
+            for _ in range(min(args.warmup, 2)):
+                ipm.solve_loaded(dqm, None, opts)
+            md, mk_k, mk_n, mit = 0.0, 0.0, 0, 0
+            for _ in range(args.steps):
+                rm = ipm.solve_loaded(dqm, None, opts)
+                md += rm.device_seconds
+                mk_k += rm.syrk_kernel_seconds
+                mk_n += rm.condensations
+                mit = rm.iter
+            kk = mk_k / max(mk_n, 1)
+            markov = {"ms_per_solve": md * 1e3 / args.steps, "iterations": mit, "status": rm.status.name,
+                      "syrk_avg_launch_ms": kk * 1e3,
+                      "syrk_frac": mi["syrk_flops"] / kk / 1e12 / FP64_PEAK_TFLOPS,
+                      "table_mb": mi["stored_bytes"] / 1e6, "table_rows": mi["markov_rows"],
+                      "table_cols": mi["markov_cols"], "p_mb_not_stored": info["p_bytes"] / 1e6,
+                      "note": "QP built on the device (cmpc_build_qp, option markov = 2); the SYRK and the "
+                              "P products read the Markov table of B-responses, P is never stored "
+                              "(csrc/markov.cu). The default (markov = 1) uses the table when P would "
+                              "exceed 64 MB (configs 3, 4)"}
+        dqm.close()
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -676,6 +706,7 @@ def main():
         "clocks": clk.summary(),
         "e2e": e2e,
         "e2e_from_problem": e2e_problem,
+        "markov": markov,
         "wall_s": wall,
     }
     if not args.no_cpu_baseline and world == 1:

@@ -44,6 +44,10 @@ void cmpc_ctx_destroy(cmpc_ctx* ctx);
  * the next residual pass behind the factor/step segment before the host has seen the step,
  * gated on the device's own evaluation of line-search trial 0 (the host re-checks it and
  * finishes the line search itself when trial 0 is refused), 0 waits for the host's decision.
+ * "markov" 1 (default) reads the SYRK prototypes of a QP built by cmpc_build_qp from the
+ * Markov table (G_k = A_K^k B per state, never materialising P) when every prototype is a
+ * state row and the materialised P would exceed 64 MB, 2 whenever every prototype is a state
+ * row, 0 always materialises P (takes effect at the next cmpc_build_qp).
  * Unknown keys or values: CMPC_ERR_DIM. Takes effect at the next solve. */
 int cmpc_ctx_set_option(cmpc_ctx* ctx, const char* key, int64_t value);
 
@@ -128,6 +132,10 @@ int cmpc_host_unregister(void* p);
  * algorithmic SYRK flops per condensation (sum over prototypes of hi (hi + 1)),
  * algorithmic bytes of one pass over P (8 x nonzeros) */
 int cmpc_qp_info(cmpc_ctx* ctx, int64_t* out);
+/* out[4] = Markov table in use (1: the prototypes of a built QP are read from the table of
+ * B-responses, P is never stored), its rows, its columns, bytes of the stored prototype
+ * source (the table, or P) */
+int cmpc_qp_layout(cmpc_ctx* ctx, int64_t* out);
 /* Diagnostics: run the condensation once and record a per-CTA timeline; out (cap x 4):
  * {start us, end us, SM id, planned weighted k-steps}; *nctas = CTAs of the launch */
 int cmpc_debug_syrk_timeline(cmpc_ctx* ctx, double* out, int64_t cap, int64_t* nctas);

@@ -40,6 +40,7 @@ SIGNATURES = {
     "cmpc_ctx_destroy": (None, [C.c_void_p]),
     "cmpc_load_qp": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, D, D, C.c_double, D, D, C.c_int]),
     "cmpc_qp_info": (C.c_int, [C.c_void_p, I64]),
+    "cmpc_qp_layout": (C.c_int, [C.c_void_p, I64]),
     "cmpc_build_qp": (C.c_int, [C.c_void_p, C.POINTER(LqProblem)]),
     "cmpc_refresh_initial_state": (C.c_int, [C.c_void_p, D]),
     "cmpc_get_qp": (C.c_int, [C.c_void_p, D, D, D, D]),

@@ -18,7 +18,7 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libcondmpc_cuda.so")
 ROOT = os.path.dirname(HERE)
 
-SOURCES = ["structure.cu", "syrk.cu", "chol.cu", "vec.cu", "batch.cu", "bsyrk.cu", "small.cu", "builder.cu", "capi.cu", "ipm_host.cpp", "comm.cpp",
+SOURCES = ["structure.cu", "markov.cu", "syrk.cu", "chol.cu", "vec.cu", "batch.cu", "bsyrk.cu", "small.cu", "builder.cu", "capi.cu", "ipm_host.cpp", "comm.cpp",
            "comm_loop.cu", "upload.cpp"]
 HEADERS = ["common.cuh", "internal.cuh", "ptx.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -661,6 +661,7 @@ unsigned bgrid(int64_t len) { return (unsigned)std::max<int64_t>(1, std::min<int
 }  // namespace
 
 BatchCtx* batch_create(Ctx& base, int64_t B) {
+  if (base.markov) throw DimError("batch mode reads the materialised prototypes: build the base QP with option markov = 0");
   if (B < 1) throw DimError("batch: count must be positive");
   if (base.n > kBatchMaxN) throw DimError("batch: the lockstep batch supports n <= 160");
   if (base.m == 0 || base.ps == 0) throw DimError("batch: the lockstep batch needs inequality rows");

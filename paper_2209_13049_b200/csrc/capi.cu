@@ -83,6 +83,7 @@ void release_qp(Ctx& c) {
   vec_free(c);
   syrk_free(c);
   free_structure(c);
+  markov_free(c);
   for (double* p : {c.H, c.h, c.d, c.Jsmall, c.small_log, c.small_res}) dev_free(p, c.stream);
   if (c.J && c.owns_J) dev_free(c.J, c.stream);
   c.H = c.h = c.J = c.d = c.Jsmall = c.small_log = c.small_res = nullptr;
@@ -329,6 +330,9 @@ int cmpc_ctx_set_option(cmpc_ctx* x, const char* key, int64_t value) {
     } else if (k == "small_path") {
       if (value != 0 && value != 1) throw DimError("small_path must be 0 or 1");
       c.opt_small = value == 1;
+    } else if (k == "markov") {
+      if (value < 0 || value > 2) throw DimError("markov must be 0, 1 or 2");
+      c.opt_markov = (int)value;  // (read when a QP is built: cmpc_build_qp)
     } else if (k == "speculate") {
       if (value != 0 && value != 1) throw DimError("speculate must be 0 or 1");
       c.opt_spec = value == 1;
@@ -358,6 +362,7 @@ int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
     c.opt_graphs = s.opt_graphs;
     c.opt_small = s.opt_small;
     c.opt_spec = s.opt_spec;
+    c.opt_markov = s.opt_markov;
     c.n = s.n;
     c.m = s.m;
     c.h0 = s.h0;
@@ -379,7 +384,7 @@ int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
     c.h = dup(s.h, size_t(s.n));
     c.d = dup(s.d, size_t(s.m));
     c.J = nullptr;
-    c.P = dup(s.P, size_t(s.ldp * s.n));
+    c.P = s.P ? dup(s.P, size_t(s.ldp * s.n)) : nullptr;
     if (s.Jsmall) c.Jsmall = dup(s.Jsmall, size_t(std::max<int64_t>(1, s.m * s.n)));
     c.hi = dup(s.hi, size_t(s.ps));
     c.start_col = dup(s.start_col, size_t(s.n + 1));
@@ -388,6 +393,23 @@ int cmpc_ctx_clone(cmpc_ctx* src, cmpc_ctx** out) {
     c.mem_rows = dup(s.mem_rows, size_t(s.m));
     c.sing_col = dup(s.sing_col, size_t(s.pz));
     c.sing_val = dup(s.sing_val, size_t(s.pz));
+    if (s.markov) {  // the Markov table and its layout (the plan's chunk lists are rebuilt)
+      c.markov = true;
+      c.ldmk = s.ldmk;
+      c.mk_cols = s.mk_cols;
+      c.mk_nq = s.mk_nq;
+      c.mk_T = s.mk_T;
+      c.mk_nu = s.mk_nu;
+      c.mk_nchunks = s.mk_nchunks;
+      c.mk_ps = s.mk_ps;
+      c.h_mk_chunk = s.h_mk_chunk;
+      c.h_mk_width = s.h_mk_width;
+      c.mk = dup(s.mk, size_t(s.ldmk * s.mk_cols));
+      c.mk_base = dup(s.mk_base, size_t(s.mk_T + 2));
+      c.mk_cnt = dup(s.mk_cnt, size_t(s.mk_T + 1));
+      c.mk_rbend = dup(s.mk_rbend, size_t(s.ldmk / 32));
+      c.mk_chunk = dup(s.mk_chunk, size_t(s.mk_nchunks));
+    }
     syrk_plan(c);
     vec_alloc(c);
     sync(c);
@@ -567,6 +589,19 @@ int cmpc_qp_info(cmpc_ctx* x, int64_t* out) {
   out[5] = c.nunits;
   out[6] = (int64_t)c.syrk_flops;
   out[7] = (int64_t)c.syrk_bytes;
+  return CMPC_OK;
+}
+
+int cmpc_qp_layout(cmpc_ctx* x, int64_t* out) {
+  if (!x || !out) {
+    g_error = "null argument";
+    return CMPC_ERR_DIM;
+  }
+  const Ctx& c = x->c;
+  out[0] = c.markov ? 1 : 0;
+  out[1] = c.markov ? c.mk_nq : 0;
+  out[2] = c.markov ? c.mk_cols : 0;
+  out[3] = c.markov ? 8 * c.ldmk * c.mk_cols : (c.P ? 8 * c.ldp * c.n : 0);
   return CMPC_OK;
 }
 

@@ -100,6 +100,33 @@ struct Ctx {
   bool h_symmetric = false;      // H == H' bitwise: H x as column dots
   std::vector<int32_t> h_start_col;
 
+  // Markov-table prototypes (markov.cu): for a device-built QP whose SYRK
+  // prototypes are all state rows, P is never stored. State row (t, i) of J is
+  // [G_{t-1} .. G_0] row i (G_k = A_K^k B), a window of row i of the Markov table
+  //   MK[q, s] = G_{T-1-s/nu}[order(q), s % nu]   (nq x T nu, column-major, ld ldmk)
+  // starting at column (T - t) nu; the table's zero tail ends every row's nonzero prefix.
+  // The prototype space is laid out stage-major in 32-row chunks: stage t holds Q rows
+  // [0, cnt_t) (states ordered by the first stage their B-response is nonzero, so these are
+  // exactly the states whose row at stage t is nonzero), padded to a chunk multiple.
+  // option "markov": 0 never, 1 (default) when the QP allows it and the materialised P would
+  // exceed kMarkovMinBytes (below that P is L2-sized and its plain passes are the faster
+  // ones), 2 whenever the QP allows it
+  int opt_markov = 1;
+  bool markov = false;           // active for the loaded QP
+  double* mk = nullptr;          // the Markov table
+  int64_t ldmk = 0, mk_cols = 0, mk_nq = 0;
+  int mk_T = 0, mk_nu = 0, mk_nchunks = 0;
+  int64_t mk_ps = 0;             // prototype rows of the layout (32 x chunks)
+  int32_t* mk_pos = nullptr;     // nx: state -> table row (-1: response identically zero)
+  int32_t* mk_base = nullptr;    // T + 2: first prototype row of stage t (t = 1..T; [T+1] = ps)
+  int32_t* mk_cnt = nullptr;     // T + 1: padded rows of stage t
+  int2* mk_chunk = nullptr;      // per chunk: {table row, column shift (T - t) nu}
+  int4* mk_clist = nullptr;      // SYRK plan: chunk lists per column block (full, thin), per
+                                 // position {table row, column shift, prototype row}
+  int32_t* mk_rbend = nullptr;   // per 32-row table block: end of its nonzero columns
+  std::vector<int2> h_mk_chunk;
+  std::vector<int32_t> h_mk_width;  // per chunk: its widest row's nonzero prefix (= first row's)
+
   // SYRK work decomposition (syrk.cu): segments (a k range of one tile) grouped in pieces
   int nunits = 0, ntiles = 0, nctas = 0, npieces = 0;
   int4* units = nullptr;          // segments {tile_i | tile_j << 10 | thin << 20, k0, k1, tile}
@@ -192,6 +219,22 @@ void analyze_structure_built(Ctx& c, const BuiltJ& J);
 // the built problem's J (null: the QP was loaded, not built)
 const BuiltJ* prob_rows(Ctx& c);
 void free_structure(Ctx& c);
+
+// ---- markov.cu
+// the Markov table and chunk layout of a built QP (false: not applicable, P is materialised)
+bool markov_prepare(Ctx& c);
+void markov_free(Ctx& c);
+// structure.cu: prototype order -> Markov layout (false: a SYRK prototype is not a state row)
+struct MarkovRemap {
+  const void* rows;  // RowDesc*
+  const int32_t* pos;
+  const int32_t* base;
+  int64_t ps;  // prototype rows of the Markov layout
+  bool force;  // option markov = 2: no size threshold
+};
+constexpr double kMarkovMinBytes = 64e6;
+void launch_markov_gemv(Ctx& c, const double* x, double* y);
+void launch_markov_ptq(Ctx& c, const double* q, double* out);
 
 // ---- syrk.cu
 void syrk_plan(Ctx& c);

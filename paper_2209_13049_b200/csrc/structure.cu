@@ -181,6 +181,37 @@ __global__ void k_singletons(JA J, const int32_t* leader, const int32_t* lo_row,
   sing_val[k] = c < 0 ? 0.0 : J.row(l)(c);
 }
 
+// Markov layout: prototype k (standard order, k < ps) -> its leader's row of the table at
+// its stage; flags a leader that is not a state row (then P is materialised after all)
+__global__ void k_mk_remap(const int32_t* leader, int64_t ps, const RowDesc* rows,
+                           const int32_t* pos, const int32_t* base, int32_t* remap, int32_t* bad) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= ps) return;
+  const RowDesc q = rows[leader[k]];
+  const int32_t p = q.kind == 1 ? pos[q.i] : -1;
+  if (p < 0) {
+    *bad = 1;
+    remap[k] = 0;
+    return;
+  }
+  remap[k] = base[q.t] + p;
+}
+
+__global__ void k_mk_groups(const int32_t* proto_of_group, int64_t G, int64_t ps, int64_t ps_mk,
+                            const int32_t* remap, int32_t* out) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  const int32_t k = proto_of_group[g];
+  out[g] = k < ps ? remap[k] : (int32_t)(ps_mk + (k - ps));
+}
+
+__global__ void k_mk_hi(const int32_t* leader, const int32_t* hi_row, int64_t ps,
+                        const int32_t* remap, int32_t* hi) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= ps) return;
+  hi[remap[k]] = hi_row[leader[k]];
+}
+
 __global__ void k_start_col(const int32_t* hi, int64_t ps, int64_t n, int32_t* start_col) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c > n) return;
@@ -206,7 +237,7 @@ void free_structure(Ctx& c) {
 }
 
 template <class JA>
-void analyze_impl(Ctx& c, const JA& J) {
+void analyze_impl(Ctx& c, const JA& J, const MarkovRemap* mk) {
   free_structure(c);
   const int64_t m = c.m, n = c.n;
   cudaStream_t st = c.stream;
@@ -301,23 +332,81 @@ void analyze_impl(Ctx& c, const JA& J) {
                             cudaMemcpyDeviceToHost, st));
   CMPC_CUDA(cudaStreamSynchronize(st));
   int64_t ps = std::lower_bound(hk.begin(), hk.end(), 1ull << 62) - hk.begin();
-  c.ps = ps;
-  c.p = G;
+  // the Markov layout (markov.cu) replaces the prototype order of the SYRK part: prototype k
+  // moves to its leader's table row at its stage, the layout's other rows are empty
+  // prototypes (no member rows: weight 0, zero rows of the table)
+  int32_t* remap = nullptr;
+  int64_t ps_l = ps;  // prototype rows of the layout
+  if (mk) {
+    remap = dev_alloc<int32_t>(size_t(std::max<int64_t>(ps, 1)), st);
+    int32_t* bad = dev_zeros<int32_t>(1, st);
+    if (ps > 0) {
+      k_mk_remap<<<unsigned((ps + T - 1) / T), T, 0, st>>>(leader, ps, static_cast<const RowDesc*>(mk->rows),
+                                                          mk->pos, mk->base, remap, bad);
+      CMPC_LAUNCHED();
+    }
+    int32_t hb = 0;
+    CMPC_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CMPC_CUDA(cudaStreamSynchronize(st));
+    dev_free(bad, st);
+    // declined: a prototype that is not a state row, a layout mostly made of empty rows
+    // (duplicate-heavy J: the table would multiply rows the analysis merged), or (option 1)
+    // a P small enough to stay in L2
+    const double p_bytes = 8.0 * (double)round_up(std::max<int64_t>(ps, 1), kBK) * (double)n;
+    if (hb || mk->ps > 2 * ps + 4096 || (!mk->force && p_bytes < kMarkovMinBytes)) {
+      dev_free(remap, st);
+      remap = nullptr;
+    } else {
+      ps_l = mk->ps;
+      const int64_t Gl = ps_l + (G - ps);
+      auto* pog = dev_alloc<int32_t>(G, st);
+      k_mk_groups<<<gg, T, 0, st>>>(proto_of_group, G, ps, ps_l, remap, pog);
+      CMPC_LAUNCHED();
+      dev_free(proto_of_group, st);
+      proto_of_group = pog;
+      dev_free(size_by_proto, st);
+      size_by_proto = dev_zeros<int32_t>(size_t(Gl + 1), st);
+      k_group_size<<<gg, T, 0, st>>>(first_pos, G, m, proto_of_group, size_by_proto);
+      CMPC_LAUNCHED();
+      dev_free(c.mem_ptr, st);
+      c.mem_ptr = dev_alloc<int32_t>(size_t(Gl + 1), st);
+      size_t need2 = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, need2, size_by_proto, c.mem_ptr, (int)(Gl + 1), st);
+      if (need2 > tmp_bytes) {
+        dev_free(tmp, st);
+        tmp_bytes = need2;
+        tmp = dev_alloc<unsigned char>(tmp_bytes + 256, st);
+      }
+      CMPC_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, size_by_proto, c.mem_ptr, (int)(Gl + 1), st));
+    }
+  }
+  c.markov = remap != nullptr;
+  c.ps = ps_l;
+  c.p = ps_l + (G - ps);
   c.pz = G - ps;
-  c.ldp = round_up(std::max<int64_t>(ps, 1), kBK);
+  c.ldp = round_up(std::max<int64_t>(ps_l, 1), kBK);
   c.row_map = dev_alloc<int32_t>(m, st);
   c.mem_rows = dev_alloc<int32_t>(m, st);
-  k_row_map<<<gm, T, 0, st>>>(srow, gid, first_pos, proto_of_group, c.mem_ptr, sg, m, ps, c.ldp,
+  k_row_map<<<gm, T, 0, st>>>(srow, gid, first_pos, proto_of_group, c.mem_ptr, sg, m, ps_l, c.ldp,
                               c.row_map, c.mem_rows);
   CMPC_LAUNCHED();
 
-  c.P = dev_alloc<double>(size_t(c.ldp * n), st);
-  CMPC_CUDA(cudaMemsetAsync(c.P, 0, sizeof(double) * c.ldp * n, st));
-  c.hi = dev_alloc<int32_t>(ps, st);
-  if (ps > 0) {
-    dim3 grid(unsigned((ps + T - 1) / T), unsigned(std::min<int64_t>(n, 64)));
-    k_gather_P<<<grid, T, 0, st>>>(J, leader, hi_row, ps, n, c.ldp, c.P, c.hi);
-    CMPC_LAUNCHED();
+  if (c.markov) {  // P stays implicit; prefix widths for the work count
+    c.hi = dev_zeros<int32_t>(size_t(std::max<int64_t>(ps_l, 1)), st);
+    if (ps > 0) {
+      k_mk_hi<<<unsigned((ps + T - 1) / T), T, 0, st>>>(leader, hi_row, ps, remap, c.hi);
+      CMPC_LAUNCHED();
+    }
+    dev_free(remap, st);
+  } else {
+    c.P = dev_alloc<double>(size_t(c.ldp * n), st);
+    CMPC_CUDA(cudaMemsetAsync(c.P, 0, sizeof(double) * c.ldp * n, st));
+    c.hi = dev_alloc<int32_t>(ps, st);
+    if (ps > 0) {
+      dim3 grid(unsigned((ps + T - 1) / T), unsigned(std::min<int64_t>(n, 64)));
+      k_gather_P<<<grid, T, 0, st>>>(J, leader, hi_row, ps, n, c.ldp, c.P, c.hi);
+      CMPC_LAUNCHED();
+    }
   }
   c.sing_col = dev_alloc<int32_t>(c.pz, st);
   c.sing_val = dev_alloc<double>(c.pz, st);
@@ -332,10 +421,14 @@ void analyze_impl(Ctx& c, const JA& J) {
     double v0 = 1.0;
     CMPC_CUDA(cudaMemcpyAsync(&v0, c.sing_val, sizeof(double), cudaMemcpyDeviceToHost, st));
     CMPC_CUDA(cudaStreamSynchronize(st));
-    if (v0 == 0.0) c.zero_k = ps;
+    if (v0 == 0.0) c.zero_k = ps_l;
   }
-  k_start_col<<<unsigned((n + 1 + T - 1) / T), T, 0, st>>>(c.hi, ps, n, c.start_col);
-  CMPC_LAUNCHED();
+  if (c.markov) {  // (rows are stage-major, not sorted by width: the plan uses chunk lists)
+    CMPC_CUDA(cudaMemsetAsync(c.start_col, 0, sizeof(int32_t) * (n + 1), st));
+  } else {
+    k_start_col<<<unsigned((n + 1 + T - 1) / T), T, 0, st>>>(c.hi, ps, n, c.start_col);
+    CMPC_LAUNCHED();
+  }
   c.h_start_col.resize(size_t(n + 1));
   CMPC_CUDA(cudaMemcpyAsync(c.h_start_col.data(), c.start_col, sizeof(int32_t) * (n + 1),
                             cudaMemcpyDeviceToHost, st));
@@ -349,7 +442,16 @@ void analyze_impl(Ctx& c, const JA& J) {
     dev_free(p, st);
 }
 
-void analyze_structure(Ctx& c) { analyze_impl(c, DenseJ{c.J, c.m}); }
-void analyze_structure_built(Ctx& c, const BuiltJ& J) { analyze_impl(c, J); }
+void analyze_structure(Ctx& c) {
+  markov_free(c);
+  analyze_impl(c, DenseJ{c.J, c.m}, nullptr);
+}
+void analyze_structure_built(Ctx& c, const BuiltJ& J) {
+  c.markov = false;
+  const bool mk = markov_prepare(c);  // the table + layout (false: not applicable)
+  const MarkovRemap mr{J.rows, c.mk_pos, c.mk_base, c.mk_ps, c.opt_markov == 2};
+  analyze_impl(c, J, mk ? &mr : nullptr);
+  if (mk && !c.markov) markov_free(c);  // declined by the analysis
+}
 
 }  // namespace cmpc

@@ -60,6 +60,10 @@ struct SyrkArgs {
   double* rhs_part;          // per segment: 2 x 64 half-sums of P' q (diagonal segments)
   long long* prof;           // debug: per piece {start ns, end ns, smid}
   int static_sched;          // debug: CTA b takes pieces b, b + grid, ... (no counter)
+  // Markov layout (markov.cu): a segment's k range indexes the chunk lists; chunk ch covers
+  // prototype rows [32 ch, 32 ch + 32) and reads table rows cinfo.x.. at column shift cinfo.y
+  const int4* clist;         // per position {table row, column shift, prototype row}; null:
+                             // P materialised, k = prototype row
 };
 
 // byte offset of element (col c, k) inside a 32 x 64 operand tile (two swizzled boxes)
@@ -249,8 +253,14 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
           const bool with_q = diag && a.q != nullptr;
           const uint32_t bytes = abytes + (diag ? 0u : (uint32_t)kOpBytes) + kBK * 8 + (with_q ? kBK * 8 : 0u);
           const void* tmA = thin ? (const void*)&tmP32 : (const void*)&tmP;
+          // operand rows / column offset / prototype row of each k step; Markov layout: the
+          // position's entry, loaded one step ahead so its latency overlaps the current step
+          int4 nx4 = make_int4(u.y, 0, u.y, 0);
+          if (a.clist && u.y < u.z) nx4 = __ldg(a.clist + u.y / kBK);
           for (int kk = u.y; kk < u.z; kk += kBK, ++it) {
             const int s = it % kStages;
+            const int ra = a.clist ? nx4.x : kk, cs = a.clist ? nx4.y : 0, pr = a.clist ? nx4.z : kk;
+            if (a.clist && kk + kBK < u.z) nx4 = __ldg(a.clist + (kk + kBK) / kBK);
             if (it >= kStages) {
               mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
               // the consumers' generic-proxy reads of this stage (ordered before us by the
@@ -262,14 +272,14 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
             unsigned char* st = smem + s * kStageBytes;
             mbar_expect_tx(&full[s], bytes);
             // a 32-column box lands exactly where the first 32 columns of a 64-column box would
-            tma_load_2d(st, tmA, kk, 64 * ti, &full[s]);
-            tma_load_2d(st + kBoxBytes, tmA, kk + 16, 64 * ti, &full[s]);
+            tma_load_2d(st, tmA, ra, cs + 64 * ti, &full[s]);
+            tma_load_2d(st + kBoxBytes, tmA, ra + 16, cs + 64 * ti, &full[s]);
             if (!diag) {
-              tma_load_2d(st + kOpBytes, &tmP, kk, 64 * tj, &full[s]);
-              tma_load_2d(st + kOpBytes + kBoxBytes, &tmP, kk + 16, 64 * tj, &full[s]);
+              tma_load_2d(st + kOpBytes, &tmP, ra, cs + 64 * tj, &full[s]);
+              tma_load_2d(st + kOpBytes + kBoxBytes, &tmP, ra + 16, cs + 64 * tj, &full[s]);
             }
-            bulk_load(st + 2 * kOpBytes, omega + kk, kBK * 8, &full[s]);
-            if (with_q) bulk_load(st + 2 * kOpBytes + 256, qv + kk, kBK * 8, &full[s]);
+            bulk_load(st + 2 * kOpBytes, omega + pr, kBK * 8, &full[s]);
+            if (with_q) bulk_load(st + 2 * kOpBytes + 256, qv + pr, kBK * 8, &full[s]);
           }
         }
       }
@@ -471,20 +481,46 @@ void syrk_plan(Ctx& c) {
   };
   // jobs: per lower tile (I,J), the rows whose prefix ends in the first half of column block I
   // (THIN: only output rows 0..31 are nonzero) and the rest (FULL)
-  struct Job { int tile, ti, tj, thin, kb, ke; double w; };
+  struct Job { int tile, ti, tj, thin, kb, ke; double w; int split; };
   // step weights per segment shape (measured with tools/syrk_timeline.py)
   const double cost_f = kCostFull, cost_t = kCostThin, cost_d = kCostDiag, cost_dt = kCostDiagThin;
   std::vector<Job> jobs;
   std::vector<int2> tiles;
+  // Markov layout: the k axis of a job is a list of chunks (stage-major prototype rows are
+  // not sorted by width). Column block ti's lists: the chunks whose widest row passes
+  // 64 ti + 32 (FULL) and those ending in (64 ti, 64 ti + 32] (THIN); kb/ke index clist.
+  std::vector<int32_t> clist;
+  std::vector<int2> mk_full((size_t)nt), mk_thin((size_t)nt);
+  if (c.markov) {
+    for (int ti = 0; ti < nt; ++ti) {
+      const int lo = kTile * ti, mid = kTile * ti + 32;
+      mk_full[size_t(ti)].x = (int)clist.size();
+      for (int ch = 0; ch < c.mk_nchunks; ++ch)
+        if (c.h_mk_width[size_t(ch)] > mid) clist.push_back(ch);
+      mk_full[size_t(ti)].y = (int)clist.size();
+      mk_thin[size_t(ti)].x = (int)clist.size();
+      for (int ch = 0; ch < c.mk_nchunks; ++ch)
+        if (c.h_mk_width[size_t(ch)] > lo && c.h_mk_width[size_t(ch)] <= mid) clist.push_back(ch);
+      mk_thin[size_t(ti)].y = (int)clist.size();
+    }
+  }
   for (int tj = 0; tj < nt; ++tj)
     for (int ti = tj; ti < nt; ++ti) {
       const int tile = (int)tiles.size();
       tiles.push_back({ti, tj});
-      const int a0 = kstart((int64_t)kTile * ti), a1 = std::max(a0, kstart((int64_t)kTile * ti + 32));
       const bool dg = ti == tj;
-      if (a1 > a0) jobs.push_back({tile, ti, tj, 1, a0, a1, dg ? cost_dt : cost_t});
-      if (k_end > a1) jobs.push_back({tile, ti, tj, 0, a1, k_end, dg ? cost_d : cost_f});
+      if (c.markov) {
+        const int2 th = mk_thin[size_t(ti)], fu = mk_full[size_t(ti)];
+        if (th.y > th.x) jobs.push_back({tile, ti, tj, 1, th.x * kBK, th.y * kBK, dg ? cost_dt : cost_t, 0});
+        if (fu.y > fu.x) jobs.push_back({tile, ti, tj, 0, fu.x * kBK, fu.y * kBK, dg ? cost_d : cost_f, 0});
+        continue;
+      }
+      const int a0 = kstart((int64_t)kTile * ti), a1 = std::max(a0, kstart((int64_t)kTile * ti + 32));
+      if (a1 > a0) jobs.push_back({tile, ti, tj, 1, a0, a1, dg ? cost_dt : cost_t, 0});
+      if (k_end > a1) jobs.push_back({tile, ti, tj, 0, a1, k_end, dg ? cost_d : cost_f, 0});
     }
+  // k step of a job position: the prototype row step, or (Markov) the chunk id
+  auto step_of = [&](int pos) { return c.markov ? clist[size_t(pos)] : pos; };
   // Pieces. The k axis is split where the cumulative weighted work reaches (1 - tail_frac).
   // The body [0, K) is laid out job after job and cut into one equal-cost piece per CTA slot
   // (every CTA starts with one; few segments, so few partial tiles). The tail [K, end) is laid
@@ -494,10 +530,10 @@ void syrk_plan(Ctx& c) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
   const int slots = sms * 2;
-  const int nsteps_all = k_end / kBK;
+  const int nsteps_all = c.markov ? c.mk_nchunks : k_end / kBK;
   std::vector<double> dens(size_t(std::max(nsteps_all, 1)), 0.0);  // weighted cost per k step
   for (const Job& jb : jobs)
-    for (int q = jb.kb / kBK; q < jb.ke / kBK; ++q) dens[size_t(q)] += jb.w;
+    for (int q = jb.kb / kBK; q < jb.ke / kBK; ++q) dens[size_t(step_of(q))] += jb.w;
   double work = 0.0;
   for (double x : dens) work += x;
   // small problems (C2, C5: ~2 steps per slot) run fewer, longer pieces: fewer partial tiles
@@ -514,6 +550,16 @@ void syrk_plan(Ctx& c) {
       acc += dens[size_t(q)];
     }
   }
+  // a job's positions before / after the split step (its list is in step order)
+  for (Job& jb : jobs) {
+    int q = jb.kb / kBK;
+    while (q < jb.ke / kBK && step_of(q) < ksplit) ++q;
+    jb.split = q;
+  }
+  auto range = [&](const Job& jb, int region, int& a, int& b) {
+    a = region == 0 ? jb.kb / kBK : jb.split;
+    b = region == 0 ? jb.split : jb.ke / kBK;
+  };
   std::vector<int4> segs;
   std::vector<int32_t> pptr{0};
   std::vector<std::vector<int32_t>> per_tile(tiles.size());
@@ -526,11 +572,11 @@ void syrk_plan(Ctx& c) {
     if (pptr.back() != (int32_t)segs.size()) pptr.push_back((int32_t)segs.size());
   };
   for (int region = 0; region < 2; ++region) {
-    const int q0 = region == 0 ? 0 : ksplit, q1 = region == 0 ? ksplit : nsteps_all;
     double cw = 0.0;
     int64_t steps = 0;
     for (const Job& jb : jobs) {
-      const int a = std::max(q0, jb.kb / kBK), b = std::min(q1, jb.ke / kBK);
+      int a, b;
+      range(jb, region, a, b);
       if (a < b) {
         cw += (b - a) * jb.w;
         steps += b - a;
@@ -545,8 +591,8 @@ void syrk_plan(Ctx& c) {
     double tgt = target();
     for (const Job& jb : jobs) {
       const double w = jb.w;
-      int a = std::max(q0, jb.kb / kBK);
-      const int b = std::min(q1, jb.ke / kBK);
+      int a, b;
+      range(jb, region, a, b);
       while (a < b) {
         const int need = std::max(1, (int)std::ceil((tgt - in_piece) / w - 1e-9));
         const int take = std::min(b - a, need);
@@ -600,17 +646,33 @@ void syrk_plan(Ctx& c) {
   CMPC_CUDA(cudaMemcpyAsync(c.tile_ptr, tptr.data(), sizeof(int32_t) * tptr.size(), cudaMemcpyHostToDevice, st));
   if (!tsegs.empty())
     CMPC_CUDA(cudaMemcpyAsync(c.tile_units, tsegs.data(), sizeof(int32_t) * tsegs.size(), cudaMemcpyHostToDevice, st));
+  dev_free(c.mk_clist, st);
+  c.mk_clist = nullptr;
+  std::vector<int4> cl4;
+  if (c.markov) {
+    cl4.reserve(clist.size());
+    for (int32_t ch : clist) {
+      const int2 ci = c.h_mk_chunk[size_t(ch)];
+      cl4.push_back({ci.x, ci.y, ch * kBK, 0});
+    }
+    c.mk_clist = dev_alloc<int4>(std::max<size_t>(1, cl4.size()), st);
+    if (!cl4.empty())
+      CMPC_CUDA(cudaMemcpyAsync(c.mk_clist, cl4.data(), sizeof(int4) * cl4.size(), cudaMemcpyHostToDevice, st));
+  }
   CMPC_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
 
-  // TMA descriptors over P (ldp rows x n cols, column-major), boxes {16 rows, 64 | 32 cols}
+  // TMA descriptors over P (ldp rows x n cols, column-major) or, Markov layout, over the
+  // table (ldmk rows x T nu cols: a window past the last column reads zeros), boxes
+  // {16 rows, 64 | 32 cols}
   auto encode = [&](int cols) {
     auto* tm = new unsigned char[sizeof(CUtensorMap)];
-    const cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(c.ldp, 1), (cuuint64_t)n};
-    const cuuint64_t strides[1] = {(cuuint64_t)std::max<int64_t>(c.ldp, 1) * sizeof(double)};
+    const int64_t rows = c.markov ? c.ldmk : std::max<int64_t>(c.ldp, 1);
+    const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)(c.markov ? c.mk_cols : n)};
+    const cuuint64_t strides[1] = {(cuuint64_t)rows * sizeof(double)};
     const cuuint32_t box[2] = {16, (cuuint32_t)cols};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = get_encode()(reinterpret_cast<CUtensorMap*>(tm), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
-                              c.P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              c.markov ? (void*)c.mk : (void*)c.P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -642,6 +704,7 @@ void launch_condense(Ctx& c, bool mirror, bool with_rhs, cudaEvent_t after_syrk)
   a.partial = c.partial;
   a.prof = c.syrk_prof;
   a.static_sched = 0;
+  a.clist = c.markov ? c.mk_clist : nullptr;
   if (c.npieces > 0) {
     const CUtensorMap* tm = reinterpret_cast<const CUtensorMap*>(c.tmap_P);
     const CUtensorMap* tm32 = reinterpret_cast<const CUtensorMap*>(c.tmap_P32);

@@ -1169,6 +1169,10 @@ void launch_Hx(Ctx& c, const double* x, double* out) {
 }
 
 void launch_Jx(Ctx& c, const double* x, double* y, double* Jx) {
+  if (c.markov) {  // P x from the Markov table (markov.cu)
+    launch_markov_gemv(c, x, y);
+    return;
+  }
   // eight 16-byte loads in flight per lane (79% of HBM at config 3; four: 67%); the singleton
   // prototypes ride along as extra CTAs
   const int gblocks = (int)ceil_div(c.ps, 64);
@@ -1187,6 +1191,13 @@ void launch_Jx(Ctx& c, const double* x, double* y, double* Jx) {
 
 void launch_Jtq(Ctx& c, const double* q, double* out) {
   if (c.n == 0) return;
+  if (c.markov) {  // P' q from the Markov table into chunk 0 of colpart
+    launch_markov_ptq(c, q, c.colpart);
+    k_ptq_final<<<(unsigned)ceil_div(c.n, 8), 256, 0, c.stream>>>(c.colpart, 1, c.n, c.sing_ptr, c.sing_val,
+                                                                q + c.ldp, out);
+    CMPC_LAUNCHED();
+    return;
+  }
   if (c.ps > 0) {
     const int rc = 2048;
     dim3 g((unsigned)c.colchunks, (unsigned)ceil_div(c.n, 8));

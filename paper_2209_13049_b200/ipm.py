@@ -143,9 +143,13 @@ class DeviceQp:
                                  ptr(qp.d), 0))
 
     @classmethod
-    def from_problem(cls, data, device: int | None = None) -> "DeviceQp":
+    def from_problem(cls, data, device: int | None = None, options: dict | None = None) -> "DeviceQp":
         """build_dense_qp (reduction.cpp:255-268) on the device: only the
-        structured data crosses PCIe; the dense J is formed and analysed in HBM."""
+        structured data crosses PCIe; J is never stored (the analysis generates its rows) and,
+        when every SYRK prototype is a state row, neither is P: the SYRK and the P products
+        read the Markov table of B-responses (option "markov": 1, the
+        default, when P would exceed 64 MB; 2 always; 0 never). ``options``: per-context
+        options applied before the build (set_option)."""
         from . import problem as P
         dm = P.dims(data)
         L = _lib.lib()
@@ -154,6 +158,8 @@ class DeviceQp:
         h = C.c_void_p()
         check(L.cmpc_ctx_create(C.byref(h), device))
         out.h = h
+        for k, v in (options or {}).items():
+            out.set_option(k, v)
         keep = {}
 
         def arr(name, a):
@@ -218,8 +224,12 @@ class DeviceQp:
     def info(self):
         out = (C.c_int64 * 8)()
         _lib.lib().cmpc_qp_info(self.h, out)
+        lay = (C.c_int64 * 4)()
+        _lib.lib().cmpc_qp_layout(self.h, lay)
         return dict(n=out[0], m=out[1], prototypes=out[2], syrk_prototypes=out[3],
-                    singletons=out[4], syrk_units=out[5], syrk_flops=out[6], p_bytes=out[7])
+                    singletons=out[4], syrk_units=out[5], syrk_flops=out[6], p_bytes=out[7],
+                    markov=bool(lay[0]), markov_rows=lay[1], markov_cols=lay[2],
+                    stored_bytes=lay[3])
 
     PHASES = dict(condense_all=0, condense=1, cholesky=2, chol_solve=3, residuals=4, recover=5,
                   trial=6, Jx=7, Jty=8, prepare=9, chol_fused=10, condense_rhs=11)
