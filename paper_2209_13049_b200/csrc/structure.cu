@@ -133,17 +133,19 @@ __global__ void k_group_size(const int32_t* first_pos, int64_t G, int64_t m,
 
 // row_map addresses prototype-indexed vectors: SYRK prototypes at [0, ps), singletons
 // at [ldp, ldp + pz)
+// gflip (Markov layout, else null): the group's table row is the NEGATED leader (a lower-bound
+// leader row is -[G_{t-1} .. G_0] row i; the table holds +G)
 __global__ void k_row_map(const int32_t* srow, const int32_t* gid, const int32_t* first_pos,
                           const int32_t* proto_of_group, const int32_t* mem_ptr,
                           const int8_t* sg, int64_t m, int64_t ps, int64_t ldp, int32_t* row_map,
-                          int32_t* mem_rows) {
+                          int32_t* mem_rows, const int32_t* gflip) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int32_t g = gid[i] - 1;
   const int32_t r = srow[i];
   const int32_t lead = srow[first_pos[g]];
   const int32_t pr = proto_of_group[g];
-  const int32_t neg = sg[r] != sg[lead] ? 1 : 0;
+  const int32_t neg = (sg[r] != sg[lead] ? 1 : 0) ^ (gflip ? gflip[g] : 0);
   const int32_t yi = pr < ps ? pr : (int32_t)(ldp + (pr - ps));
   row_map[r] = (yi << 1) | neg;
   mem_rows[mem_ptr[pr] + (int32_t)(i - first_pos[g])] = (r << 1) | neg;
@@ -184,7 +186,8 @@ __global__ void k_singletons(JA J, const int32_t* leader, const int32_t* lo_row,
 // Markov layout: prototype k (standard order, k < ps) -> its leader's row of the table at
 // its stage; flags a leader that is not a state row (then P is materialised after all)
 __global__ void k_mk_remap(const int32_t* leader, int64_t ps, const RowDesc* rows,
-                           const int32_t* pos, const int32_t* base, int32_t* remap, int32_t* bad) {
+                           const int32_t* pos, const int32_t* base, int32_t* remap, int32_t* flip,
+                           int32_t* bad) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= ps) return;
   const RowDesc q = rows[leader[k]];
@@ -192,17 +195,20 @@ __global__ void k_mk_remap(const int32_t* leader, int64_t ps, const RowDesc* row
   if (p < 0) {
     *bad = 1;
     remap[k] = 0;
+    flip[k] = 0;
     return;
   }
   remap[k] = base[q.t] + p;
+  flip[k] = q.upper ? 0 : 1;  // the table holds the upper-bound orientation (+G)
 }
 
 __global__ void k_mk_groups(const int32_t* proto_of_group, int64_t G, int64_t ps, int64_t ps_mk,
-                            const int32_t* remap, int32_t* out) {
+                            const int32_t* remap, const int32_t* flip, int32_t* out, int32_t* gflip) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= G) return;
   const int32_t k = proto_of_group[g];
   out[g] = k < ps ? remap[k] : (int32_t)(ps_mk + (k - ps));
+  gflip[g] = k < ps ? flip[k] : 0;
 }
 
 __global__ void k_mk_hi(const int32_t* leader, const int32_t* hi_row, int64_t ps,
@@ -336,13 +342,15 @@ void analyze_impl(Ctx& c, const JA& J, const MarkovRemap* mk) {
   // moves to its leader's table row at its stage, the layout's other rows are empty
   // prototypes (no member rows: weight 0, zero rows of the table)
   int32_t* remap = nullptr;
+  int32_t* gflip = nullptr;
   int64_t ps_l = ps;  // prototype rows of the layout
   if (mk) {
     remap = dev_alloc<int32_t>(size_t(std::max<int64_t>(ps, 1)), st);
+    int32_t* flip = dev_alloc<int32_t>(size_t(std::max<int64_t>(ps, 1)), st);
     int32_t* bad = dev_zeros<int32_t>(1, st);
     if (ps > 0) {
       k_mk_remap<<<unsigned((ps + T - 1) / T), T, 0, st>>>(leader, ps, static_cast<const RowDesc*>(mk->rows),
-                                                          mk->pos, mk->base, remap, bad);
+                                                          mk->pos, mk->base, remap, flip, bad);
       CMPC_LAUNCHED();
     }
     int32_t hb = 0;
@@ -360,7 +368,8 @@ void analyze_impl(Ctx& c, const JA& J, const MarkovRemap* mk) {
       ps_l = mk->ps;
       const int64_t Gl = ps_l + (G - ps);
       auto* pog = dev_alloc<int32_t>(G, st);
-      k_mk_groups<<<gg, T, 0, st>>>(proto_of_group, G, ps, ps_l, remap, pog);
+      gflip = dev_alloc<int32_t>(G, st);
+      k_mk_groups<<<gg, T, 0, st>>>(proto_of_group, G, ps, ps_l, remap, flip, pog, gflip);
       CMPC_LAUNCHED();
       dev_free(proto_of_group, st);
       proto_of_group = pog;
@@ -379,6 +388,7 @@ void analyze_impl(Ctx& c, const JA& J, const MarkovRemap* mk) {
       }
       CMPC_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, size_by_proto, c.mem_ptr, (int)(Gl + 1), st));
     }
+    dev_free(flip, st);
   }
   c.markov = remap != nullptr;
   c.ps = ps_l;
@@ -388,8 +398,9 @@ void analyze_impl(Ctx& c, const JA& J, const MarkovRemap* mk) {
   c.row_map = dev_alloc<int32_t>(m, st);
   c.mem_rows = dev_alloc<int32_t>(m, st);
   k_row_map<<<gm, T, 0, st>>>(srow, gid, first_pos, proto_of_group, c.mem_ptr, sg, m, ps_l, c.ldp,
-                              c.row_map, c.mem_rows);
+                              c.row_map, c.mem_rows, gflip);
   CMPC_LAUNCHED();
+  dev_free(gflip, st);
 
   if (c.markov) {  // P stays implicit; prefix widths for the work count
     c.hi = dev_zeros<int32_t>(size_t(std::max<int64_t>(ps_l, 1)), st);

@@ -122,3 +122,32 @@ def test_table_context_clones_and_refuses_batch_mode():
     b = dq.solve()
     assert a.iter == b.iter and np.array_equal(a.v, b.v)
     dq.close()
+
+
+@pytest.mark.parametrize("case", [(51, 3, 1, 1), (52, 4, 1, 9), (53, 7, 3, 2), (54, 40, 2, 5), (55, 2, 4, 33)])
+def test_table_edge_shapes(O, case):
+    """one stage, one input, more inputs than states, 40 states in two chunks per stage, long
+    horizons: products against dense algebra and the oracle's decisions"""
+    seed, nx, nu, T = case
+    arrs = random_arrays(seed, nx, nu, 0, T, K=False, S=False, inf_frac=0.3)
+    data = lq_from_oracle(O.problem_from_arrays(**arrs))
+    qp = P.build_dense_qp(data)
+    out = {}
+    for mk in (True, False):
+        dq = _built(data, mk)
+        if mk and not dq.info()["markov"]:  # every state unbounded: nothing for the table
+            assert not np.isfinite(arrs["xl"]).any() and not np.isfinite(arrs["xu"]).any()
+        _products(dq, qp, seed)
+        log = []
+        out[mk] = (ipm.solve_loaded(dq, None, ipm.IpmOptions(log=log.append)), log)
+        dq.close()
+    (a, la), (b, lb) = out[True], out[False]
+    # the table changes no decision of the device loop ...
+    assert a.status == b.status and a.iter == b.iter
+    assert [(x.mu, x.delta, x.trial) for x in la] == [(x.mu, x.delta, x.trial) for x in lb]
+    # ... and the solve is the reference's (case 4 ends in the line search's roundoff band,
+    # where the accepted trial of the last iteration is decided by the last bits of phi: the
+    # device loop takes trial 0 there with the table, with P and with the dense J alike)
+    o = O.solve(oracle_qp(O, qp))
+    assert a.status.name == o.status and a.iter == o.iter
+    assert rel(a.v, o.v) <= 1e-8 and abs(a.objective - o.objective) <= 1e-8 * (1 + abs(o.objective))
