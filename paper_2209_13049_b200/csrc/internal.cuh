@@ -117,8 +117,10 @@ struct Ctx {
   int64_t ldmk = 0, mk_cols = 0, mk_nq = 0;
   int mk_T = 0, mk_nu = 0, mk_nchunks = 0;
   int64_t mk_ps = 0;             // prototype rows of the layout (32 x chunks)
-  int32_t* mk_pos = nullptr;     // nx: state -> table row (-1: response identically zero)
-  int32_t* mk_base = nullptr;    // T + 2: first prototype row of stage t (t = 1..T; [T+1] = ps)
+  int mk_nx = 0;                 // sources: states [0, nx), inputs [nx, nx + nu), mixed after
+  bool mk_inputs = false;        // input rows are table rows (feedback K)
+  int32_t* mk_pos = nullptr;     // source (state, input, mixed row) -> table row (-1: none)
+  int32_t* mk_base = nullptr;    // T + 2: first prototype row of stage t (t = 0..T; [T+1] = ps)
   int32_t* mk_cnt = nullptr;     // T + 1: padded rows of stage t
   int2* mk_chunk = nullptr;      // per chunk: {table row, column shift (T - t) nu}
   int4* mk_clist = nullptr;      // SYRK plan: chunk lists per column block (full, thin), per
@@ -231,6 +233,8 @@ struct MarkovRemap {
   const int32_t* base;
   int64_t ps;  // prototype rows of the Markov layout
   bool force;  // option markov = 2: no size threshold
+  int nx, nu;  // source offsets (states, inputs, mixed rows)
+  bool inputs;
 };
 constexpr double kMarkovMinBytes = 64e6;
 void launch_markov_gemv(Ctx& c, const double* x, double* y);

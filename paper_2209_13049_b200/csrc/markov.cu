@@ -1,20 +1,24 @@
 // Markov-table prototypes: for a QP built on the device from the
-// structured problem, the SYRK prototypes are state rows of J, and state row (t, i) is
-//   [G_{t-1} .. G_0] row i,   G_k = A_K^k B   (reduction.cpp:43-60 builds these blocks,
-//                                              reduction.cpp:205-248 the rows)
-// i.e. a window of one row of the Markov table
-//   MK[q, s] = G_{T-1-s/nu}[order(q), s % nu]      (q < nq, s < T nu)
-// starting at column (T - t) nu: every row of P is a shifted view of the table, whose
-// zero tail ends its nonzero prefix. The table is nq x T nu (10 MB at config 3, 16 MB at
-// config 4 T = 200) against 180 MB / 1.53 GB for the materialised P, and it stays in L2.
+// structured problem, every row of J is a window of one row of a table of B-responses
+// (reduction.cpp:43-60 builds the blocks, reduction.cpp:182-251 the rows):
+//   state row (t, i):  [G_{t-1} .. G_0] row i                      G_k = A_K^k B
+//   input row (t, i):  [(K G)_{t-1} .. (K G)_0, e_i] row i          (feedback K)
+//   mixed row (t, i):  [((E + F K) G)_{t-1} .. , F] row i
+// With the Markov blocks in reverse order and the "own stage" block D last, source q (a
+// state, input or mixed row index) has the table row
+//   MK[q, s] = M_{T-1-s/nu}[i, s % nu]  (s < T nu),   D[i, s % nu]  (T nu <= s < (T+1) nu)
+// and row (t, i) of J is the window of MK[q] starting at column (T - t) nu. MK is
+// nq x (T+1) nu (10 MB at config 3, 16 MB at config 4 T = 200 against 180 MB / 1.53 GB of
+// materialised P) and stays in L2. Input rows without feedback are singletons and stay out.
 //
-// Prototype layout: stage-major 32-row chunks. States are ordered by the first stage their
-// B-response is nonzero (tf), so at stage t the nonzero rows are exactly table rows
-// [0, cnt_t) with cnt_t = #{tf < t}; the stage's block is padded to a chunk multiple (the
-// padding rows are zero in the stage's window). The structure analysis (structure.cu) moves
-// each SYRK prototype to its leader's (stage, table row) slot; the other slots are empty
-// prototypes (weight 0). Consumers: the SYRK reads its operand boxes straight from the table
-// by TMA (syrk.cu, chunk -> {table row, column shift}); P x and P' q below.
+// Prototype layout: stage-major 32-row chunks. Sources are ordered by the last nonzero column
+// L_q of their table row (descending): at stage t the window of q is nonzero exactly when
+// L_q >= (T - t) nu, so the stage's nonzero rows are table rows [0, cnt_t), and a chunk's
+// first row has its widest prefix (L_q - (T - t) nu + 1). Each stage's block is padded to a
+// chunk multiple (the padding rows are zero in the stage's window). The structure analysis
+// (structure.cu) moves each SYRK prototype to its leader's (stage, table row) slot; the other
+// slots are empty prototypes (weight 0). Consumers: the SYRK reads its operand boxes straight
+// from the table by TMA (syrk.cu, chunk -> {table row, column shift}); P x and P' q below.
 #include <algorithm>
 #include <mutex>
 #include <numeric>
@@ -29,38 +33,54 @@ namespace {
 
 constexpr int kMkKT = 16;  // stages per thread in k_mk_gemv
 
-// states that have a state row in J (only those enter the table)
-__global__ void k_mk_used(const RowDesc* rows, int64_t m, int32_t* used) {
+// the table's sources: states [0, nx), inputs [nx, nx + nu) (feedback only), mixed rows
+// [nx + nu, nx + nu + nc); a source enters when J has a row of it
+__device__ __forceinline__ int mk_src(const RowDesc q, int nx, int nu, bool inputs) {
+  if (q.kind == 1) return q.i;
+  if (q.kind == 2) return inputs ? nx + q.i : -1;
+  return nx + nu + q.i;
+}
+
+__global__ void k_mk_used(const RowDesc* rows, int64_t m, int nx, int nu, bool inputs, int32_t* used) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= m) return;
-  const RowDesc q = rows[r];
-  if (q.kind == 1) used[q.i] = 1;
+  const int q = mk_src(rows[r], nx, nu, inputs);
+  if (q >= 0) used[q] = 1;
 }
 
-// first k with G_k row i nonzero (T: never) and the last nonzero input of that block (the
-// row's nonzero prefix at stage t ends at (t - 1 - tf) nu + lc + 1); G = [G_0 .. G_{T-1}]
-// column-major, ld nx
-__global__ void k_mk_first(const double* G, int64_t nx, int nu, int T, int32_t* tf, int32_t* lc) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= nx) return;
-  int t = 0, last = -1;
-  for (; t < T; ++t) {
-    for (int cc = 0; cc < nu; ++cc)
-      if (G[i + ((int64_t)t * nu + cc) * nx] != 0.0) last = cc;
-    if (last >= 0) break;
+// MK[q, s] of source q (see the header); G = [G_0 .. G_{T-1}] (ld nx), KG (ld nu), EG and F
+// (ld nc), all column-major
+struct MkSrc {
+  const double *G, *KG, *EG, *F;
+  int nx, nu, nc, T;
+  __device__ __forceinline__ double operator()(int q, int64_t s) const {
+    const int64_t b = s / nu, cc = s - b * nu;
+    if (q < nx) return b < T ? G[q + ((T - 1 - b) * nu + cc) * nx] : 0.0;
+    if (q < nx + nu) {
+      const int i = q - nx;
+      return b < T ? KG[i + ((T - 1 - b) * nu + cc) * nu] : (cc == i ? 1.0 : 0.0);
+    }
+    const int i = q - nx - nu;
+    return b < T ? EG[i + ((T - 1 - b) * nu + cc) * nc] : F[i + cc * nc];
   }
-  tf[i] = t;
-  lc[i] = last;
+};
+
+// last nonzero column of each source's table row (-1: none)
+__global__ void k_mk_last(MkSrc src, int nsrc, int32_t* last) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nsrc) return;
+  int64_t s = (int64_t)(src.T + 1) * src.nu - 1;
+  for (; s >= 0; --s)
+    if (src(q, s) != 0.0) break;
+  last[q] = (int32_t)s;
 }
 
-// MK[q + s ldmk] = G[order[q] + ((T-1-s/nu) nu + s%nu) nx]; rows >= nq stay zero
-__global__ void k_mk_fill(const double* G, int64_t nx, int nu, int T, const int32_t* order,
-                          int64_t nq, int64_t ldmk, double* mk) {
+// MK[q + s ldmk] = table row of source order[q]; rows >= nq stay zero
+__global__ void k_mk_fill(MkSrc src, const int32_t* order, int64_t nq, int64_t ldmk, double* mk) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t s = blockIdx.y;
   if (q >= nq) return;
-  const int64_t blk = T - 1 - s / nu, cc = s % nu;
-  mk[q + s * ldmk] = G[order[q] + (blk * nu + cc) * nx];
+  mk[q + s * ldmk] = src(order[q], s);
 }
 
 // y = P x over the layout: thread (row r of a 32-row table block, warp w) walks the table
@@ -81,14 +101,16 @@ __global__ void __launch_bounds__(kMkW * 32) k_mk_gemv(const double* __restrict_
   extern __shared__ double xs_dyn[];  // [kMkW][kMkKT][33] reduction, then x
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t q0 = (int64_t)blockIdx.x * 32;
-  const int g = (int)blockIdx.y + 1;  // first stage of the group (stages are 1..T)
+  const int g = (int)blockIdx.y;  // first stage of the group (stages are 0..T)
   int nk = 0;
   for (int t = g; t <= T && nk < kMkKT; t += groups) ++nk;
   double (*red)[kMkKT][33] = reinterpret_cast<double (*)[kMkKT][33]>(xs_dyn);
   const double* xv = x;
   if (SX) {
     double* xs = xs_dyn + kMkW * kMkKT * 33;
-    for (int64_t i = threadIdx.x; i < n; i += kMkW * 32) xs[i] = x[i];
+    // x and nu zeros past it: stage T's windows reach one block past x (the own-stage block of
+    // input / mixed sources, which have no row at stage T), so no bound check per product
+    for (int64_t i = threadIdx.x; i < n + nu; i += kMkW * 32) xs[i] = i < n ? x[i] : 0.0;
     __syncthreads();
     xv = xs;
   }
@@ -109,7 +131,7 @@ __global__ void __launch_bounds__(kMkW * 32) k_mk_gemv(const double* __restrict_
 #pragma unroll
       for (int k = 0; k < kMkKT; ++k) {
         const int c = s + kMkW * u - (T - g - groups * k) * nu;  // column of P (warp-uniform)
-        if (k < nk && c >= 0) acc[k] += a[u] * xv[c];
+        if (k < nk && c >= 0 && (SX || c < n)) acc[k] += a[u] * xv[c];
       }
   }
   for (; s < s_end; s += kMkW) {
@@ -117,7 +139,7 @@ __global__ void __launch_bounds__(kMkW * 32) k_mk_gemv(const double* __restrict_
 #pragma unroll
     for (int k = 0; k < kMkKT; ++k) {
       const int c = s - (T - g - groups * k) * nu;
-      if (k < nk && c >= 0) acc[k] += a * xv[c];
+      if (k < nk && c >= 0 && (SX || c < n)) acc[k] += a * xv[c];
     }
   }
 #pragma unroll
@@ -148,8 +170,8 @@ __global__ void __launch_bounds__(256) k_mk_ptq(const double* __restrict__ mk, i
   __shared__ double sh[8];
   const int j = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double s = 0.0;
-  // warp w takes stages t = t0 + w, t0 + w + 8, ..; P[(t, .), j] nonzero only for j < t nu
-  for (int t = j / nu + 1 + w; t <= T; t += 8) {
+  // warp w takes stages t = t0 + w, t0 + w + 8, ..; P[(t, .), j] nonzero only for j < (t+1) nu
+  for (int t = j / nu + w; t <= T; t += 8) {
     const double* colp = mk + (int64_t)((T - t) * nu + j) * ldmk;
     const double* qq = q + base[t];
     for (int r = lane; r < cnt[t]; r += 32) s += colp[r] * qq[r];
@@ -177,7 +199,8 @@ void markov_free(Ctx& c) {
   c.h_mk_chunk.clear();
   c.h_mk_width.clear();
   c.ldmk = c.mk_cols = c.mk_nq = c.mk_ps = 0;
-  c.mk_T = c.mk_nu = c.mk_nchunks = 0;
+  c.mk_T = c.mk_nu = c.mk_nchunks = c.mk_nx = 0;
+  c.mk_inputs = false;
   c.markov = false;
 }
 
@@ -185,69 +208,69 @@ bool markov_prepare(Ctx& c) {
   markov_free(c);
   const BuiltJ* bj = prob_rows(c);
   if (!c.opt_markov || !bj || c.m == 0 || c.n == 0 || bj->nu <= 0) return false;
-  const int64_t nx = bj->nx, m = c.m, n = c.n;
-  const int nu = bj->nu;
+  const int nx = bj->nx, nu = bj->nu, nc = bj->nc;
+  const int64_t m = c.m, n = c.n;
   const int T = (int)(n / nu);
   if ((int64_t)T * nu != n) return false;
+  const bool inputs = bj->KG != nullptr;  // without feedback the input rows are singletons
+  const int nsrc = nx + nu + nc;
   cudaStream_t st = c.stream;
-  int32_t* used = dev_zeros<int32_t>(size_t(nx), st);
-  int32_t* tf = dev_alloc<int32_t>(size_t(nx), st);
-  int32_t* lc = dev_alloc<int32_t>(size_t(nx), st);
-  k_mk_used<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(static_cast<const RowDesc*>(bj->rows), m, used);
+  const MkSrc src{bj->G, bj->KG, bj->EG, bj->F, nx, nu, nc, T};
+  int32_t* used = dev_zeros<int32_t>(size_t(nsrc), st);
+  int32_t* last = dev_alloc<int32_t>(size_t(nsrc), st);
+  k_mk_used<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(static_cast<const RowDesc*>(bj->rows), m, nx, nu, inputs,
+                                                      used);
   CMPC_LAUNCHED();
-  k_mk_first<<<(unsigned)ceil_div(nx, 256), 256, 0, st>>>(bj->G, nx, nu, T, tf, lc);
+  k_mk_last<<<(unsigned)ceil_div(nsrc, 128), 128, 0, st>>>(src, nsrc, last);
   CMPC_LAUNCHED();
-  std::vector<int32_t> hu((size_t)nx), ht((size_t)nx), hl((size_t)nx);
-  CMPC_CUDA(cudaMemcpyAsync(hu.data(), used, sizeof(int32_t) * nx, cudaMemcpyDeviceToHost, st));
-  CMPC_CUDA(cudaMemcpyAsync(ht.data(), tf, sizeof(int32_t) * nx, cudaMemcpyDeviceToHost, st));
-  CMPC_CUDA(cudaMemcpyAsync(hl.data(), lc, sizeof(int32_t) * nx, cudaMemcpyDeviceToHost, st));
+  std::vector<int32_t> hu((size_t)nsrc), hl((size_t)nsrc);
+  CMPC_CUDA(cudaMemcpyAsync(hu.data(), used, sizeof(int32_t) * nsrc, cudaMemcpyDeviceToHost, st));
+  CMPC_CUDA(cudaMemcpyAsync(hl.data(), last, sizeof(int32_t) * nsrc, cudaMemcpyDeviceToHost, st));
   CMPC_CUDA(cudaStreamSynchronize(st));
   dev_free(used, st);
-  dev_free(tf, st);
-  dev_free(lc, st);
+  dev_free(last, st);
   std::vector<int32_t> order;
-  for (int64_t i = 0; i < nx; ++i)
-    if (hu[size_t(i)] && ht[size_t(i)] < T) order.push_back((int32_t)i);
+  for (int q = 0; q < nsrc; ++q)
+    if (hu[size_t(q)] && hl[size_t(q)] >= 0) order.push_back(q);
   if (order.empty()) return false;
-  // by first nonzero stage, then by the end of that block's nonzeros (descending): a chunk's
-  // first row then has the chunk's widest prefix at every stage
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-    if (ht[size_t(a)] != ht[size_t(b)]) return ht[size_t(a)] < ht[size_t(b)];
-    return hl[size_t(a)] > hl[size_t(b)];
-  });
+  // widest first: the window of q at stage t ends at L_q - (T - t) nu, so one order sorts
+  // every stage by width, and a stage's nonzero rows are a prefix of it
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return hl[size_t(a)] > hl[size_t(b)]; });
   const int64_t nq = (int64_t)order.size();
-  std::vector<int32_t> pos((size_t)nx, -1);
+  std::vector<int32_t> pos((size_t)nsrc, -1);
   for (int64_t q = 0; q < nq; ++q) pos[size_t(order[size_t(q)])] = (int32_t)q;
-  // per stage t = 1..T: nonzero rows cnt_t = #{tf < t} (order is sorted by tf), padded
+  // per stage t = 0..T: cnt_t = #{L_q >= (T - t) nu}, padded to chunks
   std::vector<int32_t> base(size_t(T + 2), 0), cnt(size_t(T + 1), 0);
   c.h_mk_chunk.clear();
   c.h_mk_width.clear();
   int64_t nz = 0;
-  for (int t = 1; t <= T; ++t) {
-    while (nz < nq && ht[size_t(order[size_t(nz)])] < t) ++nz;
+  for (int t = 0; t <= T; ++t) {
+    const int64_t lo = (int64_t)(T - t) * nu;
+    while (nz < nq && hl[size_t(order[size_t(nz)])] >= lo) ++nz;
     const int64_t pc = round_up(nz, kBK);
     cnt[size_t(t)] = (int32_t)pc;
     base[size_t(t + 1)] = base[size_t(t)] + (int32_t)pc;
     for (int64_t q0 = 0; q0 < pc; q0 += kBK) {
-      c.h_mk_chunk.push_back({(int)q0, (T - t) * nu});
-      const int32_t f = order[size_t(q0)];
-      c.h_mk_width.push_back((t - 1 - ht[size_t(f)]) * nu + hl[size_t(f)] + 1);
+      c.h_mk_chunk.push_back({(int)q0, (int)lo});
+      c.h_mk_width.push_back((int32_t)(hl[size_t(order[size_t(q0)])] - lo + 1));
     }
   }
   const int64_t ps = base[size_t(T + 1)];
   if (ps == 0) return false;
   c.ldmk = round_up(nq, 32);
-  c.mk_cols = (int64_t)T * nu;
+  c.mk_cols = (int64_t)(T + 1) * nu;
   c.mk_nq = nq;
   c.mk_T = T;
   c.mk_nu = nu;
   c.mk_ps = ps;
   c.mk_nchunks = (int)c.h_mk_chunk.size();
-  // per 32-row table block: end of its nonzero columns, (T - tf of its first row) nu
+  c.mk_nx = nx;
+  c.mk_inputs = inputs;
+  // per 32-row table block: end of its nonzero columns (its first row's)
   std::vector<int32_t> rbend((size_t)(c.ldmk / 32));
   for (size_t b = 0; b < rbend.size(); ++b) {
     const int64_t q = (int64_t)b * 32;
-    rbend[b] = q < nq ? (T - ht[size_t(order[size_t(q)])]) * nu : 0;
+    rbend[b] = q < nq ? hl[size_t(order[size_t(q)])] + 1 : 0;
   }
   auto up = [&](const std::vector<int32_t>& v) {
     int32_t* d = dev_alloc<int32_t>(std::max<size_t>(1, v.size()), st);
@@ -263,8 +286,7 @@ bool markov_prepare(Ctx& c) {
   CMPC_CUDA(cudaMemcpyAsync(c.mk_chunk, c.h_mk_chunk.data(), sizeof(int2) * c.h_mk_chunk.size(),
                             cudaMemcpyHostToDevice, st));
   c.mk = dev_zeros<double>(size_t(c.ldmk * c.mk_cols), st);
-  k_mk_fill<<<dim3((unsigned)ceil_div(nq, 256), (unsigned)c.mk_cols), 256, 0, st>>>(bj->G, nx, nu, T, dorder, nq,
-                                                                                  c.ldmk, c.mk);
+  k_mk_fill<<<dim3((unsigned)ceil_div(nq, 256), (unsigned)c.mk_cols), 256, 0, st>>>(src, dorder, nq, c.ldmk, c.mk);
   CMPC_LAUNCHED();
   CMPC_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
   dev_free(dorder, st);
@@ -275,9 +297,9 @@ void launch_markov_gemv(Ctx& c, const double* x, double* y) {
   if (c.ps > 0) {
     // stage groups: at most kMkKT stages per thread, and two CTAs per SM for small tables
     const int nrb = (int)(c.ldmk / 32);
-    const int groups = std::min(c.mk_T, std::max({4, (int)ceil_div(c.mk_T, kMkKT), (int)ceil_div(296, nrb)}));
+    const int groups = std::min(c.mk_T + 1, std::max({4, (int)ceil_div(c.mk_T + 1, kMkKT), (int)ceil_div(296, nrb)}));
     const dim3 grid((unsigned)nrb, (unsigned)groups);
-    const size_t sred = sizeof(double) * kMkW * kMkKT * 33, sx = sizeof(double) * (size_t)c.n;
+    const size_t sred = sizeof(double) * kMkW * kMkKT * 33, sx = sizeof(double) * (size_t)(c.n + c.mk_nu);
     static std::once_flag flags[kMaxDevices];
     once_per_device(flags, c.device, [] {
       CMPC_CUDA(cudaFuncSetAttribute(k_mk_gemv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));

@@ -184,14 +184,16 @@ __global__ void k_singletons(JA J, const int32_t* leader, const int32_t* lo_row,
 }
 
 // Markov layout: prototype k (standard order, k < ps) -> its leader's row of the table at
-// its stage; flags a leader that is not a state row (then P is materialised after all)
+// its stage; flags a leader outside the table (then P is materialised after all)
 __global__ void k_mk_remap(const int32_t* leader, int64_t ps, const RowDesc* rows,
-                           const int32_t* pos, const int32_t* base, int32_t* remap, int32_t* flip,
-                           int32_t* bad) {
+                           const int32_t* pos, const int32_t* base, int nx, int nu, bool inputs,
+                           int32_t* remap, int32_t* flip, int32_t* bad) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= ps) return;
   const RowDesc q = rows[leader[k]];
-  const int32_t p = q.kind == 1 ? pos[q.i] : -1;
+  // the table's source of the row: state, input (feedback only), mixed
+  const int src = q.kind == 1 ? q.i : q.kind == 2 ? (inputs ? nx + q.i : -1) : nx + nu + q.i;
+  const int32_t p = src >= 0 ? pos[src] : -1;
   if (p < 0) {
     *bad = 1;
     remap[k] = 0;
@@ -350,7 +352,8 @@ void analyze_impl(Ctx& c, const JA& J, const MarkovRemap* mk) {
     int32_t* bad = dev_zeros<int32_t>(1, st);
     if (ps > 0) {
       k_mk_remap<<<unsigned((ps + T - 1) / T), T, 0, st>>>(leader, ps, static_cast<const RowDesc*>(mk->rows),
-                                                          mk->pos, mk->base, remap, flip, bad);
+                                                          mk->pos, mk->base, mk->nx, mk->nu, mk->inputs,
+                                                          remap, flip, bad);
       CMPC_LAUNCHED();
     }
     int32_t hb = 0;
@@ -460,7 +463,7 @@ void analyze_structure(Ctx& c) {
 void analyze_structure_built(Ctx& c, const BuiltJ& J) {
   c.markov = false;
   const bool mk = markov_prepare(c);  // the table + layout (false: not applicable)
-  const MarkovRemap mr{J.rows, c.mk_pos, c.mk_base, c.mk_ps, c.opt_markov == 2};
+  const MarkovRemap mr{J.rows, c.mk_pos, c.mk_base, c.mk_ps, c.opt_markov == 2, c.mk_nx, c.mk_nu, c.mk_inputs};
   analyze_impl(c, J, mk ? &mr : nullptr);
   if (mk && !c.markov) markov_free(c);  // declined by the analysis
 }

@@ -1,7 +1,7 @@
 """for a QP built on the device, the SYRK prototypes are read from the
 Markov table of B-responses (csrc/markov.cu) and P is never stored. State row (t, i) of J is
-[G_{t-1} .. G_0] row i (G_k = A_K^k B, proj/src/reduction.cpp:43-60, rows :205-248), a
-window of the table. Every product through the table must equal the dense algebra, and the
+[G_{t-1} .. G_0] row i (G_k = A_K^k B, proj/src/reduction.cpp:43-60, rows :182-251), input
+and mixed rows add their own-stage block: every row is a window of the table. Every product through the table must equal the dense algebra, and the
 solve must take the reference's decisions (the oracle) exactly as the materialised path does."""
 import numpy as np
 import pytest
@@ -94,15 +94,30 @@ def test_plate_solve_matches_the_materialised_path(O):
     assert rel(a.solution.x, b.solution.x) <= 1e-10
 
 
-def test_table_is_declined_when_a_prototype_is_not_a_state_row(O):
-    # feedback K makes the input rows dense (K Gall): the table does not cover them
-    arrs = random_arrays(41, 5, 2, 0, 6, K=True, S=False)
+@pytest.mark.parametrize("case", [(41, 5, 2, 0, 6, True, False), (42, 6, 2, 3, 7, False, True),
+                                  (43, 4, 3, 2, 9, True, True), (44, 9, 2, 4, 12, True, False)])
+def test_table_covers_feedback_and_mixed_rows(O, case):
+    """with feedback K the input rows are [(K G)_{t-1} .. (K G)_0, e_i], mixed rows
+    [((E + F K) G)_{t-1} .. , F]: windows of the same table with the own-stage block last"""
+    seed, nx, nu, nc, T, K, S = case
+    arrs = random_arrays(seed, nx, nu, nc, T, K=K, S=S)
     data = lq_from_oracle(O.problem_from_arrays(**arrs))
-    dq = _built(data, True)
-    assert not dq.info()["markov"]
     qp = P.build_dense_qp(data)
-    _products(dq, qp, 2)
-    dq.close()
+    out = {}
+    for mk in (True, False):
+        dq = _built(data, mk)
+        assert dq.info()["markov"] == mk
+        _products(dq, qp, seed)
+        log = []
+        out[mk] = (ipm.solve_loaded(dq, None, ipm.IpmOptions(log=log.append)), log)
+        dq.close()
+    (a, la), (b, lb) = out[True], out[False]
+    o = O.solve(oracle_qp(O, qp))
+    assert_parity(a, o, la)
+    # (the materialised built path of case 1 takes trial 1 instead of 0 in its converged
+    # 11th iteration, inside the line search's roundoff band: a summation-order effect; its
+    # iterates stay at 1e-16 of the oracle's)
+    assert b.status.name == o.status and b.iter == o.iter and rel(b.v, o.v) <= 1e-8
 
 
 def test_table_context_clones_and_refuses_batch_mode():
