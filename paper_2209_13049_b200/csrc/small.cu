@@ -34,6 +34,7 @@ struct SmallArgs {
   double *v, *s, *lam, *z;  // outputs (device)
   double* res;              // status, iter, kkt, objective, trials
   double* log;              // max_iter x 8: iter, mu, alpha, alpha_z, kkt, objective, delta, trial
+  long long* prof;          // debug (CMPC_SMALL_PROF): clock cycles per phase, 8 phases
 };
 
 // fixed-order CTA sum / max (every thread gets the result)
@@ -111,7 +112,6 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
   double* jp = jv + m;         // J pv
   double* st = jp + m;         // trial slack
   double* red = st + m;        // 6 x 8 partials
-  __shared__ int s_flag;
 
   for (int i = tid; i < m * n; i += kSmT) J[(i % m) + (i / m) * lj] = a.J[i];
   for (int i = tid; i < n * n; i += kSmT) H[i] = a.H[i];
@@ -204,6 +204,15 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
     return add(mul(0.5, a1), a2);
   };
 
+  // debug phase clock (thread 0; CMPC_SMALL_PROF)
+  long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_t = clock64();
+  auto mark = [&](int ph) {
+    if (a.prof && tid == 0) {
+      const long long t = clock64();
+      ph_acc[ph] += t - ph_t;
+      ph_t = t;
+    }
+  };
   double kkt = residuals();
   int iter = 0, status = -1, trials = 0;
   constexpr double kShifts[7] = {0.0, 1e-8, 1e-6, 1e-4, 1e-2, 1.0, 1e2};
@@ -223,71 +232,115 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
       kkt = residuals();
     }
     // sigma = z / s; M = H + W'W, W = sqrt(sigma) J (assemble_condensed + gram_weighted)
-    for (int r = tid; r < m; r += kSmT) sg[r] = dv(z[r], s[r]);
-    __syncthreads();
-    // W = sqrt(sigma) J, formed once per iteration
-    for (int e = tid; e < m * n; e += kSmT) {
-      const int r = e % m, c = e / m;
-      W[r + c * lj] = mul(sqrt(sg[r]), J[r + c * lj]);
+    // W = sqrt(sigma) J, formed once per iteration (the square root once per row, kept in jp:
+    // J pv is formed after the factorization)
+    for (int r = tid; r < m; r += kSmT) {
+      sg[r] = dv(z[r], s[r]);
+      jp[r] = sqrt(sg[r]);
     }
     __syncthreads();
+    for (int r = tid; r < m; r += kSmT) {
+      const double q = jp[r];
+      for (int c = 0; c < n; ++c) W[r + c * lj] = mul(q, J[r + c * lj]);
+    }
+    __syncthreads();
+    mark(0);
     double delta = 0.0;
     bool factored = false;
+#pragma unroll 1
     for (int sh = 0; sh < 7 && !factored; ++sh) {
       delta = kShifts[sh];
-      for (int e = tid; e < n * n; e += kSmT) {  // lower triangle of M (+ delta I)
-        const int i = e % n, j = e / n;
-        if (i < j) continue;
-        // W = sqrt(sigma) J: entry (i, j) of W'W over the rows in four interleaved partial sums
-        double g4[4] = {0.0, 0.0, 0.0, 0.0};
-        int r = 0;
-        for (; r + 4 <= m; r += 4)
+      // lower triangle of M (+ delta I) = H + W'W, W = sqrt(sigma) J: entry (i, j) over the rows
+      // in four interleaved partial sums; a thread takes a 2 x 2 block of entries, so each W
+      // element it loads serves two products (the gram is bound by shared-memory loads)
+      {
+        const int nb = (n + 1) / 2;
+        for (int e = tid; e < nb * nb; e += kSmT) {
+          const int bi = e % nb, bj = e / nb;
+          if (bi < bj) continue;
+          const int i0 = 2 * bi, j0 = 2 * bj;
+          const int i1 = min(i0 + 1, n - 1), j1 = min(j0 + 1, n - 1);  // (odd n: a duplicate)
+          double g[2][2][4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            g4[q] = add(g4[q], mul(W[r + q + i * lj], W[r + q + j * lj]));
-        for (; r < m; ++r) g4[0] = add(g4[0], mul(W[r + i * lj], W[r + j * lj]));
-        double x = add(H[e], add(add(g4[0], g4[1]), add(g4[2], g4[3])));
-        if (i == j && delta != 0.0) x = add(x, delta);
-        mt[e] = x;
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v2 = 0; v2 < 2; ++v2)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) g[u][v2][q] = 0.0;
+          int r = 0;
+          for (; r + 4 <= m; r += 4)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double a0 = W[r + q + i0 * lj], a1 = W[r + q + i1 * lj];
+              const double b0 = W[r + q + j0 * lj], b1 = W[r + q + j1 * lj];
+              g[0][0][q] = add(g[0][0][q], mul(a0, b0));
+              g[0][1][q] = add(g[0][1][q], mul(a0, b1));
+              g[1][0][q] = add(g[1][0][q], mul(a1, b0));
+              g[1][1][q] = add(g[1][1][q], mul(a1, b1));
+            }
+          for (; r < m; ++r) {
+            const double a0 = W[r + i0 * lj], a1 = W[r + i1 * lj];
+            const double b0 = W[r + j0 * lj], b1 = W[r + j1 * lj];
+            g[0][0][0] = add(g[0][0][0], mul(a0, b0));
+            g[0][1][0] = add(g[0][1][0], mul(a0, b1));
+            g[1][0][0] = add(g[1][0][0], mul(a1, b0));
+            g[1][1][0] = add(g[1][1][0], mul(a1, b1));
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v2 = 0; v2 < 2; ++v2) {
+              const int i = i0 + u, j = j0 + v2;
+              if (i >= n || j >= n || i < j) continue;
+              const int e2 = i + j * n;
+              double x = add(H[e2], add(add(g[u][v2][0], g[u][v2][1]), add(g[u][v2][2], g[u][v2][3])));
+              if (i == j && delta != 0.0) x = add(x, delta);
+              mt[e2] = x;
+            }
+        }
       }
       __syncthreads();
+      mark(1);
       // Cholesky of M + delta I, right-looking over the whole CTA (pivot rule of potf2_lower,
       // dense_linalg.cpp:24-40: !(d > 0) || !isfinite(d)); the pivot's 1 / sqrt by the MUFU seed
       // and two Newton steps (the IEEE sqrt and division are long subroutines on the chain)
-      if (tid == 0) s_flag = 0;
+      // one barrier per pivot: every thread forms the pivot's reciprocal square root itself (the
+      // same operations on the same value), L[i, p] and L[c, p] on the fly from column p (which
+      // the trailing update of this pivot does not touch)
+      int bad = 0;
       for (int p = 0; p < n; ++p) {
-        if (tid == 0) {
-          const double dp = mt[p + p * n];
-          if (!(dp > 0.0) || !isfinite(dp)) {
-            s_flag = 1;
-          } else {
-            double rp;
-            if (dp >= 1e-300 && dp <= 1e300) {
-              asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rp) : "d"(dp));
-              const double hx = 0.5 * dp;
-              rp = rp * fma(-hx * rp, rp, 1.5);
-              rp = rp * fma(-hx * rp, rp, 1.5);
-            } else {
-              rp = 1.0 / sqrt(dp);
-            }
-            L[p + p * ll] = mul(dp, rp);
-            rd[p] = rp;
-          }
+        const double dp = mt[p + p * n];
+        if (!(dp > 0.0) || !isfinite(dp)) {  // (uniform)
+          bad = 1;
+          break;
         }
-        __syncthreads();
-        if (s_flag) break;
-        const double rp = rd[p];
-        for (int i = p + 1 + tid; i < n; i += kSmT) L[i + p * ll] = mul(mt[i + p * n], rp);
-        __syncthreads();
-        const int w = n - p - 1;
-        for (int e = tid; e < w * w; e += kSmT) {
-          const int i = p + 1 + e % w, c = p + 1 + e / w;
-          if (i >= c) mt[i + c * n] = sub(mt[i + c * n], mul(L[i + p * ll], L[c + p * ll]));
+        double rp;
+        if (dp >= 1e-300 && dp <= 1e300) {
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rp) : "d"(dp));
+          const double hx = 0.5 * dp;
+          rp = rp * fma(-hx * rp, rp, 1.5);
+          rp = rp * fma(-hx * rp, rp, 1.5);
+        } else {
+          rp = 1.0 / sqrt(dp);
+        }
+        if (tid == 0) {
+          L[p + p * ll] = mul(dp, rp);
+          rd[p] = rp;
+        }
+        // trailing update: thread (row i = tid % 32, columns c = tid / 32 + 8 k) of the lower
+        // part (n <= 32); warp 0 also stores the column
+        const int i = tid & 31;
+        if (i > p && i < n) {
+          const double lip = mul(mt[i + p * n], rp);
+          if (warp == 0) L[i + p * ll] = lip;
+          for (int c = p + 1 + (tid >> 5); c <= i; c += kSmT / 32)
+            mt[i + c * n] = sub(mt[i + c * n], mul(lip, mul(mt[c + p * n], rp)));
         }
         __syncthreads();
       }
-      factored = !s_flag;
+      factored = !bad;  // (uniform)
       __syncthreads();
+      mark(2);
     }
     if (!factored) {
       status = 2;
@@ -300,23 +353,24 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
     __syncthreads();
     for (int i = tid; i < n; i += kSmT) pv[i] = m > 0 ? add(-r1[i], vt[i]) : -r1[i];
     __syncthreads();
-    if (warp == 0) {  // factor_solve (dense_linalg.cpp:102-110), right-looking in one warp
+    if (warp == 0) {  // factor_solve (dense_linalg.cpp:102-110), right-looking in one warp:
+      // pv[i] in lane i's register (n <= 32), each x_j broadcast by a shuffle
+      const int i = lane;
+      double pvi = i < n ? pv[i] : 0.0;
       for (int j = 0; j < n; ++j) {
-        const double xj = mul(pv[j], rd[j]);
-        __syncwarp();
-        for (int i = j + 1 + lane; i < n; i += 32) pv[i] = sub(pv[i], mul(L[i + j * ll], xj));
-        if (lane == 0) pv[j] = xj;
-        __syncwarp();
+        const double xj = __shfl_sync(0xffffffffu, mul(pvi, rd[j]), j);
+        if (i > j && i < n) pvi = sub(pvi, mul(L[i + j * ll], xj));
+        if (i == j) pvi = xj;
       }
       for (int j = n - 1; j >= 0; --j) {
-        const double xj = mul(pv[j], rd[j]);
-        __syncwarp();
-        for (int i = lane; i < j; i += 32) pv[i] = sub(pv[i], mul(L[j + i * ll], xj));
-        if (lane == 0) pv[j] = xj;
-        __syncwarp();
+        const double xj = __shfl_sync(0xffffffffu, mul(pvi, rd[j]), j);
+        if (i < j) pvi = sub(pvi, mul(L[j + i * ll], xj));
+        if (i == j) pvi = xj;
       }
+      if (i < n) pv[i] = pvi;
     }
     __syncthreads();
+    mark(3);
     gemv_rows(J, m, n, lj, pv, jp);
     __syncthreads();
     double as = 1.0, az = 1.0;  // fraction_to_boundary (ipm.cpp:105-116)
@@ -329,12 +383,15 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
       if (p_s < 0.0) as = fmin(as, mul(a.tau, dv(-s[r], p_s)));
       if (p_z < 0.0) az = fmin(az, mul(a.tau, dv(-z[r], p_z)));
     }
-    // min as the negated max (exact); 1.0 when no blocking entry
-    const double alpha_max = -cta_max(-as, red), alpha_z = -cta_max(-az, red);
-    // line_search + merit (ipm.cpp:118-144, :25-32)
+    // line_search + merit (ipm.cpp:118-144, :25-32): the step-length minima (min as the
+    // negated max, exact; 1.0 when no blocking entry) and max |lambda| in one reduction, the
+    // merit sums in another
     double ml = 0.0;
     for (int r = tid; r < m; r += kSmT) ml = fmax(ml, fabs(lam[r]));
-    ml = cta_max(ml, red);
+    double mx3[3] = {-as, -az, ml};
+    cta_reduce<3, true>(mx3, red);
+    const double alpha_max = -mx3[0], alpha_z = -mx3[1];
+    ml = mx3[2];
     const double rho = add(mul(10.0, ml), 1.0);
     double slog = 0.0, sl1 = 0.0, sq = 0.0;
     for (int r = tid; r < m; r += kSmT) {
@@ -342,9 +399,12 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
       sl1 += fabs(add(sub(jv[r], dd[r]), s[r]));
       sq += dv(ps[r], s[r]);
     }
-    slog = cta_sum(slog, red);
-    sl1 = cta_sum(sl1, red);
-    sq = cta_sum(sq, red);
+    __syncthreads();  // (red is reused)
+    double su3[3] = {slog, sl1, sq};
+    cta_reduce<3, false>(su3, red);
+    slog = su3[0];
+    sl1 = su3[1];
+    sq = su3[2];
     double phi0 = quad(v, hv), deriv = 0.0;
     {
       double gpv = 0.0;
@@ -356,6 +416,7 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
       deriv = sub(sub(deriv, mul(mu, sq)), mul(rho, sl1));
     }
     constexpr double band = 10.0 * 2.220446049250313e-16;
+    mark(4);
     double alpha = alpha_max;
     int jacc = -1;
     for (int j = 0; j <= 30; ++j, alpha *= 0.5) {
@@ -377,8 +438,10 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
         tl += log(st[r]);
         t1 += fabs(add(sub(sg[r], dd[r]), st[r]));
       }
-      tl = cta_sum(tl, red);
-      t1 = cta_sum(t1, red);
+      double su2[2] = {tl, t1};
+      cta_reduce<2, false>(su2, red);
+      tl = su2[0];
+      t1 = su2[1];
       double phi = quad(vt, rhs);
       if (m > 0) phi = add(sub(phi, mul(mu, tl)), mul(rho, t1));
       if (deriv <= 0.0 && phi <= add(phi0, mul(mul(a.eta, alpha), deriv))) {
@@ -395,6 +458,7 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
       break;
     }
     __syncthreads();
+    mark(5);
     const double mu_used = mu;
     for (int i = tid; i < n; i += kSmT) v[i] = add(v[i], mul(alpha, pv[i]));
     for (int r = tid; r < m; r += kSmT) {
@@ -417,8 +481,11 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
       rec[6] = delta;
       rec[7] = jacc;
     }
+    mark(6);
   }
   __syncthreads();
+  if (a.prof && tid == 0)
+    for (int i = 0; i < 8; ++i) a.prof[i] = ph_acc[i];
   for (int i = tid; i < n; i += kSmT) a.v[i] = v[i];
   for (int r = tid; r < m; r += kSmT) {
     a.s[r] = s[r];
@@ -478,6 +545,9 @@ int small_solve(Ctx& c, const double* opts, int64_t max_iter, double* v_out, dou
   a.z = c.z;
   a.res = c.small_res;
   a.log = c.small_log;
+  static const bool sprof = getenv("CMPC_SMALL_PROF") != nullptr;
+  a.prof = nullptr;
+  if (sprof) a.prof = dev_zeros<long long>(8, c.stream);
   cudaEvent_t e0, e1;
   CMPC_CUDA(cudaEventCreate(&e0));
   CMPC_CUDA(cudaEventCreate(&e1));
@@ -488,6 +558,13 @@ int small_solve(Ctx& c, const double* opts, int64_t max_iter, double* v_out, dou
   double res[8] = {0};
   CMPC_CUDA(cudaMemcpyAsync(res, c.small_res, sizeof(double) * 5, cudaMemcpyDeviceToHost, c.stream));
   CMPC_CUDA(cudaStreamSynchronize(c.stream));
+  if (a.prof) {  // debug: cycles per phase over the solve
+    long long ph[8];
+    CMPC_CUDA(cudaMemcpy(ph, a.prof, sizeof(ph), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[small prof] sigma+W %lld gram %lld chol %lld solves %lld dirs+ls-setup %lld trials %lld update+res %lld (cycles, %d iterations)\n",
+            ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6], (int)res[1]);
+    dev_free(a.prof, c.stream);
+  }
   const int64_t iters = (int64_t)res[1];
   std::vector<double> lg;
   if (log && iters > 0) {
