@@ -145,12 +145,25 @@ __global__ void __launch_bounds__(kSmT, 1) k_small_ipm(const SmallArgs a) {
   const int warp = tid >> 5, lane = tid & 31;
   // y = J'x: a warp per column, lanes over the rows, fixed-order warp sum (every thread must
   // call it; y is complete after the caller's next barrier)
+  // (a warp's columns c, c + 8, c + 16, c + 24 side by side: four independent chains and warp
+  // sums instead of one after the other; each column's own order is unchanged)
   auto gemv_jt = [&](const double* x, double* y) {
-    for (int c = warp; c < n; c += kSmT / 32) {
-      double acc = 0.0;
-      for (int r = lane; r < m; r += 32) acc = add(acc, mul(J[r + c * lj], x[r]));
-      acc = warp_sum(acc);
-      if (lane == 0) y[c] = acc;
+    constexpr int kW = kSmT / 32;
+    for (int c0 = warp; c0 < n; c0 += 4 * kW) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int r = lane; r < m; r += 32) {
+        const double xr = x[r];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (c0 + kW * k < n) acc[k] = add(acc[k], mul(J[r + (c0 + kW * k) * lj], xr));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (c0 + kW * k < n) {
+          const double t = warp_sum(acc[k]);
+          if (lane == 0) y[c0 + kW * k] = t;
+        }
+      }
     }
   };
   // compute_residuals (ipm.cpp:46-70): r1, r2, r3, jv, hv; returns kkt
