@@ -91,6 +91,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the first line takes nvidia-smi's start-up: wait for it so that the sampling is live
+            # when the timed region starts (a short region would otherwise see no sample at all)
+            t0 = time.perf_counter()
+            while not self.samples and time.perf_counter() - t0 < 3.0:
+                time.sleep(0.01)
+            self.n0 = len(self.samples)
         except (FileNotFoundError, OSError):
             self.proc = None
         return self
@@ -101,6 +107,11 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            # a region shorter than the 200 ms period: the next sample, right at its end
+            t0 = time.perf_counter()
+            while len(self.samples) <= self.n0 and time.perf_counter() - t0 < 1.0:
+                time.sleep(0.005)
+            self.samples = self.samples[self.n0:]  # (taken from the region's start on)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
