@@ -39,6 +39,7 @@ double merit_host(const Packet&, double vhv, double hv, double sum_log, double s
 namespace {
 
 constexpr int kBT = 256;      // threads of the row / final kernels
+constexpr int kStageSlots = 8;  // pinned upload ring (Host::upload_*)
 constexpr int kBBlk = 32;     // row-kernel blocks per instance
 constexpr int kBatchMaxN = 160;  // the per-instance Cholesky keeps M in shared memory
 enum BSlot { kBAbs = 0, kBLog, kBLam, kBS, kBZ, kBR3, kBComp, kBPsS, kBAs, kBAz, kBBad, kBSlots };
@@ -143,26 +144,43 @@ __global__ void k_b_hmax(int64_t n, const double* __restrict__ h, double* __rest
   if (threadIdx.x == 0) hmax[blockIdx.x] = a;
 }
 
-// residual rows: r2 = lambda - mu/s, r3 = Jv - d + s and their sums / maxima
+// residual rows: r2 = lambda - mu/s, r3 = Jv - d + s and their sums / maxima. STEP: the
+// accepted step of the rows first (s += alpha ps, lambda += alpha pl, z += alpha_z pz, the
+// update of ipm.cpp:240-243), so the iterate is read once for both
+template <bool STEP>
 __global__ void __launch_bounds__(kBT) k_b_res_rows(int64_t m, int64_t py, const int32_t* __restrict__ row_map,
                                                     const double* __restrict__ yv, const double* __restrict__ d,
-                                                    const double* __restrict__ s, const double* __restrict__ lam,
-                                                    const double* __restrict__ z, const double* __restrict__ mu_p,
+                                                    double* __restrict__ s, double* __restrict__ lam,
+                                                    double* __restrict__ z, const double* __restrict__ mu_p,
                                                     double* __restrict__ r2, double* __restrict__ r3,
-                                                    double* __restrict__ part, const int* __restrict__ act) {
+                                                    double* __restrict__ part, const int* __restrict__ act,
+                                                    const double* __restrict__ alpha,
+                                                    const double* __restrict__ alpha_z,
+                                                    const double* __restrict__ ps, const double* __restrict__ pl,
+                                                    const double* __restrict__ pz, double* __restrict__ sigma) {
   __shared__ double sh[7 * 32];
   const int64_t b = blockIdx.y;
   if (!act[b]) return;
   const double mu = mu_p[b];
   const double* y = yv + b * py;
+  const double al = STEP ? alpha[b] : 0.0, az = STEP ? alpha_z[b] : 0.0;
   double sabs = 0.0, slog = 0.0, ml = 0.0, mss = 0.0, mz = 0.0, mr3 = 0.0, mc = 0.0;
   B_ROWS_LOOP(m) {
     const int64_t o = b * m + r;
     const double jv = jrow_b(y, row_map[r]);
-    const double sr = s[o], lr = lam[o], zr = z[o];
+    double sr = s[o], lr = lam[o], zr = z[o];
+    if (STEP) {
+      sr = add(sr, mul(al, ps[o]));
+      lr = add(lr, mul(al, pl[o]));
+      zr = add(zr, mul(az, pz[o]));
+      s[o] = sr;
+      lam[o] = lr;
+      z[o] = zr;
+    }
     r2[o] = sub(lr, mul(mu, dv(1.0, sr)));
     const double t3 = add(sub(jv, d[o]), sr);
     r3[o] = t3;
+    sigma[o] = dv(zr, sr);  // the next condensation's sigma (s and z stay until then)
     sabs += fabs(t3);
     slog += log(sr);
     ml = fmax(ml, fabs(lr));
@@ -271,29 +289,18 @@ __global__ void k_b_kkt_mu(int64_t B, int64_t n, int64_t m, const double* __rest
   p->kkt = kkt;
 }
 
-// sigma = z / s and w = r2 - sigma r3 per row (step_directions, ipm.cpp:79-103)
-__global__ void __launch_bounds__(kBT) k_b_sigma_rows(int64_t m, const double* __restrict__ s,
-                                                      const double* __restrict__ z, const double* __restrict__ r2,
-                                                      const double* __restrict__ r3, double* __restrict__ sigma,
-                                                      double* __restrict__ w, const int* __restrict__ act) {
-  const int64_t b = blockIdx.y;
-  if (!act[b]) return;
-  B_ROWS_LOOP(m) {
-    const int64_t o = b * m + r;
-    const double sg = dv(z[o], s[o]);
-    sigma[o] = sg;
-    w[o] = sub(r2[o], mul(sg, r3[o]));
-  }
-}
-
 // per prototype k: out1 = sum over the member rows of x1 (signed when SIGNED1), out2 = signed
 // sum of x2 (when x2); members in ascending row order; the all-zero group gives 0
-template <bool SIGNED1>
+// WR: x2 is not stored but formed per member row as w = r2 - x1 r3 (x1 = sigma; the
+// step_directions right-hand side, ipm.cpp:79-103), so no pass over the rows writes it
+template <bool SIGNED1, bool WR = false>
 __global__ void __launch_bounds__(kBT) k_b_proto(int64_t p, int64_t ps, int64_t ldp, int64_t m, int64_t py,
                                                  int64_t zero_k, const int32_t* __restrict__ mem_ptr,
                                                  const int32_t* __restrict__ mem_rows, const double* __restrict__ x1,
                                                  const double* __restrict__ x2, double* __restrict__ out1,
-                                                 double* __restrict__ out2, const int* __restrict__ act) {
+                                                 double* __restrict__ out2, const int* __restrict__ act,
+                                                 const double* __restrict__ r2 = nullptr,
+                                                 const double* __restrict__ r3 = nullptr) {
   const int64_t b = blockIdx.y;
   if (!act[b]) return;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < p; k += (int64_t)gridDim.x * blockDim.x) {
@@ -304,7 +311,10 @@ __global__ void __launch_bounds__(kBT) k_b_proto(int64_t p, int64_t ps, int64_t 
         const int64_t o = b * m + (rm >> 1);
         const double a = x1[o];
         s1 += (SIGNED1 && (rm & 1)) ? -a : a;
-        if (x2) {
+        if (WR) {
+          const double c = sub(r2[o], mul(a, r3[o]));
+          s2 += (rm & 1) ? -c : c;
+        } else if (x2) {
           const double c = x2[o];
           s2 += (rm & 1) ? -c : c;
         }
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(kBT) k_b_proto(int64_t p, int64_t ps, int64_t 
     }
     const int64_t o = b * py + (k < ps ? k : ldp + (k - ps));
     out1[o] = s1;
-    if (x2) out2[o] = s2;
+    if (WR || x2) out2[o] = s2;
   }
 }
 
@@ -610,6 +620,7 @@ __global__ void __launch_bounds__(kBT) k_b_trial_final(int64_t n, int64_t m, con
 }
 
 // the accepted step (ipm.cpp:240-243)
+template <bool ROWS>
 __global__ void k_b_update(int64_t n, int64_t m, const double* __restrict__ alpha, const double* __restrict__ alpha_z,
                            double* __restrict__ v, const double* __restrict__ pv, double* __restrict__ s,
                            const double* __restrict__ ps, double* __restrict__ lam, const double* __restrict__ pl,
@@ -619,6 +630,7 @@ __global__ void k_b_update(int64_t n, int64_t m, const double* __restrict__ alph
   const double al = alpha[b], az = alpha_z[b];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     v[b * n + i] = add(v[b * n + i], mul(al, pv[b * n + i]));
+  if (!ROWS) return;  // (the rows' step rides on the residual pass: k_b_res_rows<true>)
   B_ROWS_LOOP(m) {
     const int64_t o = b * m + r;
     s[o] = add(s[o], mul(al, ps[o]));
@@ -645,7 +657,7 @@ struct BatchCtx {
   int* act = nullptr;
   Packet* pk = nullptr;
   Packet* pk_host = nullptr;
-  double* hstage = nullptr;  // pinned staging for the per-instance scalars (mu, alpha, delta)
+  double* hstage = nullptr;  // pinned staging ring for the per-instance scalars (mu, alpha, delta)
   int* istage = nullptr;     // pinned staging for the masks
   std::vector<double*> owned;
 };
@@ -690,8 +702,8 @@ BatchCtx* batch_create(Ctx& base, int64_t B) {
     b->act = balloc<int>(*b, B, true);
     b->pk = balloc<Packet>(*b, B, true);
     CMPC_CUDA(cudaMallocHost(&b->pk_host, sizeof(Packet) * B));
-    CMPC_CUDA(cudaMallocHost(&b->hstage, sizeof(double) * 4 * B));
-    CMPC_CUDA(cudaMallocHost(&b->istage, sizeof(int) * B));
+    CMPC_CUDA(cudaMallocHost(&b->hstage, sizeof(double) * kStageSlots * B));
+    CMPC_CUDA(cudaMallocHost(&b->istage, sizeof(int) * kStageSlots * B));
     CMPC_CUDA(cudaFuncSetAttribute(k_b_chol, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sizeof(double) * (kBatchMaxN * (kBatchMaxN + 1) + 3 * kBatchMaxN))));
     syrk_plan_batch(base, B, b->syrk, b->st);
@@ -789,15 +801,19 @@ struct Host {
   dim3 rows() const { return dim3(kBBlk, (unsigned)b.B); }
   dim3 vecs() const { return dim3(bgrid(b.n), (unsigned)b.B); }
   dim3 protos() const { return dim3(bgrid(c.p), (unsigned)b.B); }
+  // uploads go through a ring of kStageSlots pinned slots without a synchronize: at most four
+  // uploads happen between two packet reads (which synchronize the stream), so a slot is never
+  // rewritten while its copy is pending
+  int hslot = 0, islot = 0;
   void upload_scalars(double* dst, const std::vector<double>& x) {
-    std::memcpy(b.hstage, x.data(), sizeof(double) * b.B);
-    CMPC_CUDA(cudaMemcpyAsync(dst, b.hstage, sizeof(double) * b.B, cudaMemcpyHostToDevice, b.st));
-    CMPC_CUDA(cudaStreamSynchronize(b.st));  // the staging buffer is reused
+    double* st = b.hstage + (size_t)(hslot++ % kStageSlots) * b.B;
+    std::memcpy(st, x.data(), sizeof(double) * b.B);
+    CMPC_CUDA(cudaMemcpyAsync(dst, st, sizeof(double) * b.B, cudaMemcpyHostToDevice, b.st));
   }
   void upload_mask(const std::vector<int>& x) {
-    std::memcpy(b.istage, x.data(), sizeof(int) * b.B);
-    CMPC_CUDA(cudaMemcpyAsync(b.act, b.istage, sizeof(int) * b.B, cudaMemcpyHostToDevice, b.st));
-    CMPC_CUDA(cudaStreamSynchronize(b.st));
+    int* st = b.istage + (size_t)(islot++ % kStageSlots) * b.B;
+    std::memcpy(st, x.data(), sizeof(int) * b.B);
+    CMPC_CUDA(cudaMemcpyAsync(b.act, st, sizeof(int) * b.B, cudaMemcpyHostToDevice, b.st));
   }
   void read_packets(long long* syncs) {
     CMPC_CUDA(cudaMemcpyAsync(b.pk_host, b.pk, sizeof(Packet) * b.B, cudaMemcpyDeviceToHost, b.st));
@@ -813,10 +829,23 @@ struct Host {
     }
   }
   // residuals at the current point (ipm.cpp:46-70) -> packets of the active instances
-  void residuals() {
+  // step: the accepted step's rows are applied by the residual row pass (v by k_b_update<false>
+  // before it)
+  void residuals(bool step = false) {
     phase("res:Pv", [&] { px(b.v, b.yv); });
     phase("res:Hv", [&] {
       dgemm(b.blas, false, (int)b.n, (int)b.B, (int)b.n, c.H, (int)b.n, b.v, (int)b.n, b.Hv, (int)b.n);
+    });
+    phase("res:rows", [&] {  // (before lamP: with a step it writes the new lambda)
+      if (step)
+        k_b_res_rows<true><<<rows(), kBT, 0, b.st>>>(b.m, b.py, c.row_map, b.yv, b.d, b.s, b.lam, b.z, b.mu, b.r2,
+                                                     b.r3, b.part, b.act, b.alpha, b.alpha_z, b.ps, b.pl, b.pz,
+                                                     b.sigma);
+      else
+        k_b_res_rows<false><<<rows(), kBT, 0, b.st>>>(b.m, b.py, c.row_map, b.yv, b.d, b.s, b.lam, b.z, b.mu, b.r2,
+                                                      b.r3, b.part, b.act, nullptr, nullptr, nullptr, nullptr,
+                                                      nullptr, b.sigma);
+      CMPC_LAUNCHED();
     });
     phase("res:lamP", [&] {
       k_b_proto<true><<<protos(), kBT, 0, b.st>>>(c.p, c.ps, c.ldp, b.m, b.py, c.zero_k, c.mem_ptr, c.mem_rows,
@@ -828,10 +857,7 @@ struct Host {
       k_b_sing_t<<<vecs(), kBT, 0, b.st>>>(b.n, b.py, c.ldp, c.sing_ptr, c.sing_val, b.lp, b.Jtl, b.act);
       CMPC_LAUNCHED();
     });
-    phase("res:rows", [&] {
-      k_b_res_rows<<<rows(), kBT, 0, b.st>>>(b.m, b.py, c.row_map, b.yv, b.d, b.s, b.lam, b.z, b.mu, b.r2, b.r3,
-                                             b.part, b.act);
-      CMPC_LAUNCHED();
+    phase("res:final", [&] {
       k_b_res_final<<<(unsigned)b.B, kBT, 0, b.st>>>(b.n, b.m, b.Hv, b.h, b.Jtl, b.v, b.r1, b.part, b.hmax, b.h0,
                                                      b.pk, b.act);
       CMPC_LAUNCHED();
@@ -845,13 +871,12 @@ struct Host {
   }
   // sigma, omega, q, condensation with the right-hand side -r1 + J'(r2 - sigma r3)
   void condense() {
-    phase("sigma", [&] {
-      k_b_sigma_rows<<<rows(), kBT, 0, b.st>>>(b.m, b.s, b.z, b.r2, b.r3, b.sigma, b.w, b.act);
-      CMPC_LAUNCHED();
-    });
+    // sigma = z / s came with the last residual pass; w = r2 - sigma r3 is formed inside the
+    // prototype sums (r2 is current: a barrier update recomputes it)
     phase("omegaP", [&] {
-      k_b_proto<false><<<protos(), kBT, 0, b.st>>>(c.p, c.ps, c.ldp, b.m, b.py, c.zero_k, c.mem_ptr, c.mem_rows,
-                                                   b.sigma, b.w, b.omega, b.qw, b.act);
+      k_b_proto<false, true><<<protos(), kBT, 0, b.st>>>(c.p, c.ps, c.ldp, b.m, b.py, c.zero_k, c.mem_ptr,
+                                                         c.mem_rows, b.sigma, nullptr, b.omega, b.qw, b.act, b.r2,
+                                                         b.r3);
       CMPC_LAUNCHED();
     });
     phase("syrk", [&] {
@@ -1094,10 +1119,10 @@ void batch_solve(BatchCtx& b, const double* opts, int64_t max_iter, double* v_ou
     H.upload_scalars(b.alpha, alpha);
     H.upload_scalars(b.alpha_z, alpha_z);
     H.upload_mask(accept);
-    k_b_update<<<H.rows(), kBT, 0, b.st>>>(n, m, b.alpha, b.alpha_z, b.v, b.pv, b.s, b.ps, b.lam, b.pl, b.z, b.pz,
-                                          b.act);
+    k_b_update<false><<<H.vecs(), kBT, 0, b.st>>>(n, m, b.alpha, b.alpha_z, b.v, b.pv, b.s, b.ps, b.lam, b.pl, b.z,
+                                                 b.pz, b.act);
     CMPC_LAUNCHED();
-    H.residuals();
+    H.residuals(/*step=*/true);
     H.read_packets(&syncs);
     for (int64_t i = 0; i < B; ++i)
       if (accept[i]) A[i] = b.pk_host[i];
