@@ -620,22 +620,23 @@ __global__ void __launch_bounds__(kBT) k_b_trial_final(int64_t n, int64_t m, con
 }
 
 // the accepted step (ipm.cpp:240-243)
-template <bool ROWS>
-__global__ void k_b_update(int64_t n, int64_t m, const double* __restrict__ alpha, const double* __restrict__ alpha_z,
-                           double* __restrict__ v, const double* __restrict__ pv, double* __restrict__ s,
-                           const double* __restrict__ ps, double* __restrict__ lam, const double* __restrict__ pl,
-                           double* __restrict__ z, const double* __restrict__ pz, const int* __restrict__ act) {
+// the accepted step of v (ipm.cpp:240-243) and what the accepted trial already formed at the
+// new point: P v + alpha P pv (the trial's J v_t, k_b_trial_rows: the same operations) and
+// H v_t (the trial's product; later trial rounds of other instances recompute it from the same
+// v_t). The rows' step rides on the residual pass (k_b_res_rows<true>).
+__global__ void k_b_step_v(int64_t n, int64_t py, const double* __restrict__ alpha, double* __restrict__ v,
+                           const double* __restrict__ pv, double* __restrict__ yv, const double* __restrict__ y,
+                           double* __restrict__ Hv, const double* __restrict__ Hvt, const int* __restrict__ act) {
   const int64_t b = blockIdx.y;
   if (!act[b]) return;
-  const double al = alpha[b], az = alpha_z[b];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    v[b * n + i] = add(v[b * n + i], mul(al, pv[b * n + i]));
-  if (!ROWS) return;  // (the rows' step rides on the residual pass: k_b_res_rows<true>)
-  B_ROWS_LOOP(m) {
-    const int64_t o = b * m + r;
-    s[o] = add(s[o], mul(al, ps[o]));
-    lam[o] = add(lam[o], mul(al, pl[o]));
-    z[o] = add(z[o], mul(az, pz[o]));
+  const double al = alpha[b];
+  const int64_t k = n > py ? n : py;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) {
+      v[b * n + i] = add(v[b * n + i], mul(al, pv[b * n + i]));
+      Hv[b * n + i] = Hvt[b * n + i];
+    }
+    if (i < py) yv[b * py + i] = add(yv[b * py + i], mul(al, y[b * py + i]));
   }
 }
 
@@ -829,13 +830,15 @@ struct Host {
     }
   }
   // residuals at the current point (ipm.cpp:46-70) -> packets of the active instances
-  // step: the accepted step's rows are applied by the residual row pass (v by k_b_update<false>
-  // before it)
+  // step: the accepted step's rows are applied by the residual row pass (v, P v, H v by
+  // k_b_step_v before it)
   void residuals(bool step = false) {
-    phase("res:Pv", [&] { px(b.v, b.yv); });
-    phase("res:Hv", [&] {
-      dgemm(b.blas, false, (int)b.n, (int)b.B, (int)b.n, c.H, (int)b.n, b.v, (int)b.n, b.Hv, (int)b.n);
-    });
+    if (!step) {  // (after a step, k_b_step_v carried P v and H v)
+      phase("res:Pv", [&] { px(b.v, b.yv); });
+      phase("res:Hv", [&] {
+        dgemm(b.blas, false, (int)b.n, (int)b.B, (int)b.n, c.H, (int)b.n, b.v, (int)b.n, b.Hv, (int)b.n);
+      });
+    }
     phase("res:rows", [&] {  // (before lamP: with a step it writes the new lambda)
       if (step)
         k_b_res_rows<true><<<rows(), kBT, 0, b.st>>>(b.m, b.py, c.row_map, b.yv, b.d, b.s, b.lam, b.z, b.mu, b.r2,
@@ -1119,8 +1122,8 @@ void batch_solve(BatchCtx& b, const double* opts, int64_t max_iter, double* v_ou
     H.upload_scalars(b.alpha, alpha);
     H.upload_scalars(b.alpha_z, alpha_z);
     H.upload_mask(accept);
-    k_b_update<false><<<H.vecs(), kBT, 0, b.st>>>(n, m, b.alpha, b.alpha_z, b.v, b.pv, b.s, b.ps, b.lam, b.pl, b.z,
-                                                 b.pz, b.act);
+    k_b_step_v<<<dim3(bgrid(std::max(n, b.py)), (unsigned)B), kBT, 0, b.st>>>(n, b.py, b.alpha, b.v, b.pv, b.yv, b.y,
+                                                                          b.Hv, b.Hvt, b.act);
     CMPC_LAUNCHED();
     H.residuals(/*step=*/true);
     H.read_packets(&syncs);
