@@ -370,7 +370,9 @@ __device__ __forceinline__ double b_rsqrt(double x) {  // MUFU seed + two Newton
 // row reads are conflict-free; it runs right-looking in one warp's registers.
 __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __restrict__ M,
                                                    const double* __restrict__ delta, const double* __restrict__ rhs,
-                                                   double* __restrict__ x, Packet* pk, const int* __restrict__ act) {
+                                                   double* __restrict__ x, Packet* pk, const int* __restrict__ act,
+                                                   const double* __restrict__ H, const double* __restrict__ tq,
+                                                   double* __restrict__ JtPl) {
   extern __shared__ double bsm[];
   const int ld = n + 1;
   double* L = bsm;            // L[i + j * ld], i >= j
@@ -485,6 +487,16 @@ __global__ void __launch_bounds__(kCholT, 1) k_b_chol(int n, const double* __res
   }
   __syncthreads();
   for (int i = tid; i < n; i += kCholT) x[b * n + i] = xs[i];
+  // J' p_lambda = (M - H) pv - tq: step_directions' p_lambda (ipm.cpp:79-103) through the
+  // condensed matrix, J'(-r2 + Sigma (r3 + J pv)) = J' Sigma J pv - J'(r2 - Sigma r3), so the step
+  // advances J'lambda by alpha J'p_lambda instead of a pass over P (the single-instance path's
+  // recurrence, vec.cu k_jtpl_symv); row i of the lower triangle, then column i, ascending j
+  for (int i = tid; i < n; i += kCholT) {
+    double s = 0.0;
+    for (int j = 0; j <= i; ++j) s = add(s, mul(sub(Mb[i + (int64_t)j * n], H[i + (int64_t)j * n]), xs[j]));
+    for (int j = i + 1; j < n; ++j) s = add(s, mul(sub(Mb[j + (int64_t)i * n], H[j + (int64_t)i * n]), xs[j]));
+    JtPl[b * n + i] = sub(s, tq[b * n + i]);
+  }
   if (tid == 0) pk[b].info = 0;
 }
 
@@ -626,7 +638,8 @@ __global__ void __launch_bounds__(kBT) k_b_trial_final(int64_t n, int64_t m, con
 // v_t). The rows' step rides on the residual pass (k_b_res_rows<true>).
 __global__ void k_b_step_v(int64_t n, int64_t py, const double* __restrict__ alpha, double* __restrict__ v,
                            const double* __restrict__ pv, double* __restrict__ yv, const double* __restrict__ y,
-                           double* __restrict__ Hv, const double* __restrict__ Hvt, const int* __restrict__ act) {
+                           double* __restrict__ Hv, const double* __restrict__ Hvt, double* __restrict__ Jtl,
+                           const double* __restrict__ JtPl, const int* __restrict__ act) {
   const int64_t b = blockIdx.y;
   if (!act[b]) return;
   const double al = alpha[b];
@@ -635,6 +648,7 @@ __global__ void k_b_step_v(int64_t n, int64_t py, const double* __restrict__ alp
     if (i < n) {
       v[b * n + i] = add(v[b * n + i], mul(al, pv[b * n + i]));
       Hv[b * n + i] = Hvt[b * n + i];
+      Jtl[b * n + i] = add(Jtl[b * n + i], mul(al, JtPl[b * n + i]));  // J'(lambda + alpha p_lambda)
     }
     if (i < py) yv[b * py + i] = add(yv[b * py + i], mul(al, y[b * py + i]));
   }
@@ -654,6 +668,7 @@ struct BatchCtx {
   double *sigma = nullptr, *w = nullptr, *omega = nullptr, *qw = nullptr, *lp = nullptr, *tq = nullptr;
   double *rhs = nullptr, *M = nullptr, *pv = nullptr, *ps = nullptr, *pl = nullptr, *pz = nullptr;
   double *yv = nullptr, *y = nullptr, *Hv = nullptr, *Hvt = nullptr, *vt = nullptr, *Jtl = nullptr;
+  double* JtPl = nullptr;  // J' p_lambda of the step (k_b_chol's epilogue)
   double *part = nullptr, *mu = nullptr, *alpha = nullptr, *alpha_z = nullptr, *delta = nullptr;
   int* act = nullptr;
   Packet* pk = nullptr;
@@ -692,7 +707,7 @@ BatchCtx* batch_create(Ctx& base, int64_t B) {
     b->h0 = balloc<double>(*b, B);
     b->d = balloc<double>(*b, B * m);
     b->hmax = balloc<double>(*b, B);
-    for (double** p : {&b->v, &b->r1, &b->rhs, &b->pv, &b->Hv, &b->Hvt, &b->vt, &b->Jtl, &b->tq})
+    for (double** p : {&b->v, &b->r1, &b->rhs, &b->pv, &b->Hv, &b->Hvt, &b->vt, &b->Jtl, &b->tq, &b->JtPl})
       *p = balloc<double>(*b, B * n, true);
     for (double** p : {&b->s, &b->lam, &b->z, &b->r2, &b->r3, &b->sigma, &b->w, &b->ps, &b->pl, &b->pz})
       *p = balloc<double>(*b, B * m, true);
@@ -830,8 +845,8 @@ struct Host {
     }
   }
   // residuals at the current point (ipm.cpp:46-70) -> packets of the active instances
-  // step: the accepted step's rows are applied by the residual row pass (v, P v, H v by
-  // k_b_step_v before it)
+  // step: the accepted step's rows are applied by the residual row pass (v, P v, H v and J'lambda
+  // by k_b_step_v before it)
   void residuals(bool step = false) {
     if (!step) {  // (after a step, k_b_step_v carried P v and H v)
       phase("res:Pv", [&] { px(b.v, b.yv); });
@@ -850,16 +865,18 @@ struct Host {
                                                       nullptr, b.sigma);
       CMPC_LAUNCHED();
     });
-    phase("res:lamP", [&] {
-      k_b_proto<true><<<protos(), kBT, 0, b.st>>>(c.p, c.ps, c.ldp, b.m, b.py, c.zero_k, c.mem_ptr, c.mem_rows,
-                                                  b.lam, nullptr, b.lp, nullptr, b.act);
-      CMPC_LAUNCHED();
-    });
-    phase("res:Jtl", [&] {
-      dgemm(b.blas, true, (int)b.n, (int)b.B, (int)c.ldp, c.P, (int)c.ldp, b.lp, (int)b.py, b.Jtl, (int)b.n);
-      k_b_sing_t<<<vecs(), kBT, 0, b.st>>>(b.n, b.py, c.ldp, c.sing_ptr, c.sing_val, b.lp, b.Jtl, b.act);
-      CMPC_LAUNCHED();
-    });
+    if (!step) {  // (after a step, k_b_step_v advanced J'lambda by alpha J'p_lambda)
+      phase("res:lamP", [&] {
+        k_b_proto<true><<<protos(), kBT, 0, b.st>>>(c.p, c.ps, c.ldp, b.m, b.py, c.zero_k, c.mem_ptr, c.mem_rows,
+                                                    b.lam, nullptr, b.lp, nullptr, b.act);
+        CMPC_LAUNCHED();
+      });
+      phase("res:Jtl", [&] {
+        dgemm(b.blas, true, (int)b.n, (int)b.B, (int)c.ldp, c.P, (int)c.ldp, b.lp, (int)b.py, b.Jtl, (int)b.n);
+        k_b_sing_t<<<vecs(), kBT, 0, b.st>>>(b.n, b.py, c.ldp, c.sing_ptr, c.sing_val, b.lp, b.Jtl, b.act);
+        CMPC_LAUNCHED();
+      });
+    }
     phase("res:final", [&] {
       k_b_res_final<<<(unsigned)b.B, kBT, 0, b.st>>>(b.n, b.m, b.Hv, b.h, b.Jtl, b.v, b.r1, b.part, b.hmax, b.h0,
                                                      b.pk, b.act);
@@ -891,7 +908,8 @@ struct Host {
   void cholesky() {
     phase("chol", [&] {
       const size_t sm = sizeof(double) * ((size_t)b.n * (b.n + 1) + 3 * b.n);
-      k_b_chol<<<(unsigned)b.B, kCholT, sm, b.st>>>((int)b.n, b.M, b.delta, b.rhs, b.pv, b.pk, b.act);
+      k_b_chol<<<(unsigned)b.B, kCholT, sm, b.st>>>((int)b.n, b.M, b.delta, b.rhs, b.pv, b.pk, b.act, c.H, b.tq,
+                                                    b.JtPl);
       CMPC_LAUNCHED();
     });
   }
@@ -1123,7 +1141,7 @@ void batch_solve(BatchCtx& b, const double* opts, int64_t max_iter, double* v_ou
     H.upload_scalars(b.alpha_z, alpha_z);
     H.upload_mask(accept);
     k_b_step_v<<<dim3(bgrid(std::max(n, b.py)), (unsigned)B), kBT, 0, b.st>>>(n, b.py, b.alpha, b.v, b.pv, b.yv, b.y,
-                                                                          b.Hv, b.Hvt, b.act);
+                                                                          b.Hv, b.Hvt, b.Jtl, b.JtPl, b.act);
     CMPC_LAUNCHED();
     H.residuals(/*step=*/true);
     H.read_packets(&syncs);
