@@ -316,7 +316,8 @@ void set_mu(Ctx& c, double mu);
 // residuals at the current state (r1, r2, r3, kkt, objective pieces) -> packet A;
 // reuse_trial: the state was just moved to the last evaluated line-search trial point
 // gated: nothing runs unless the step was taken (d_alpha[2] != 0; the speculative seg_next)
-void launch_residuals(Ctx& c, bool reuse_trial = false, bool gated = false);
+// publish >= 0: the last kernel also publishes the packet into slot A (0) or B (1)
+void launch_residuals(Ctx& c, bool reuse_trial = false, bool gated = false, int publish = -1);
 // r2 and complementarity only (after a barrier change) -> packet kkt at the new mu, from the
 // residual maxima of `a` (the current point's residual packet) and the recomputed max_comp
 void launch_residuals_mu(Ctx& c, const Packet& a);
@@ -344,7 +345,7 @@ void launch_reset_packet_all(Ctx& c);
 void launch_debug_sum(Ctx& c, const double* x, int64_t n, int slot);
 // decide: also the speculative trial-0 acceptance into d_alpha (trial0_decide, vec.cu)
 void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear = false,
-                  bool decide = false, double eta = 0.0);
+                  bool decide = false, double eta = 0.0, int publish = -1);
 // line-search derivative pieces for externally set directions: (Hv+h).pv, sum ps/s
 void launch_ls_pieces(Ctx& c);
 // v = 0, s = max(1, d), z = mu / s, lambda = z (ipm.cpp:170-177)

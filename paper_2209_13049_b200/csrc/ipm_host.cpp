@@ -109,8 +109,7 @@ void seg_step(Ctx& c, double tau, double eta) {
   rec(c.ev1, c.stream);
   launch_recover(c, tau);
   launch_debug_sum(c, c.ps_, c.m, 3);
-  launch_trial(c, 0.0, true, /*linear=*/true, /*decide=*/true, eta);
-  launch_publish(c, /*slot_b=*/true);
+  launch_trial(c, 0.0, true, /*linear=*/true, /*decide=*/true, eta, /*publish into slot B=*/1);
 }
 
 // seg_next may run gated on the device's trial-0 verdict: every kernel in it then checks it
@@ -121,8 +120,7 @@ bool seg_next_gated(const Ctx& c) { return !c.comm && (c.m == 0 || c.jtl_recur);
 void seg_next(Ctx& c) {
   NvtxRange nv("cmpc: update + residuals");
   launch_update_dev(c);
-  launch_residuals(c, /*reuse_trial=*/true, /*gated=*/seg_next_gated(c));
-  launch_publish(c);
+  launch_residuals(c, /*reuse_trial=*/true, /*gated=*/seg_next_gated(c), /*publish into slot A=*/0);
 }
 
 // run a segment eagerly, or capture it once into a CUDA graph and replay it

@@ -24,6 +24,36 @@ constexpr int kRowT = 256;
 constexpr int kLaneMembers = 8;  // prototypes with more member rows take the warp path of k_proto_reduce
 enum Slot { kSumAbs = 0, kSumLog = 1, kSumPsS = 2, kSlots = 16 };
 
+// packet -> mapped host memory, then the sequence number (system-scope fence between them, so a
+// host that sees the new sequence sees the packet); with reset, the accumulated maxima / minima
+// start over (host loop). One warp. k_publish alone, or at the end of a segment's last kernel
+// (PubArgs.out non-null: one launch less per segment)
+struct PubArgs {
+  Packet* out;
+  unsigned long long* dev_seq;
+  unsigned long long* host_seq;
+  int reset;
+};
+__device__ __forceinline__ void publish_warp(Packet* pk, const PubArgs& pa, int lane) {
+  constexpr int kWords = sizeof(Packet) / 8;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(pk);
+  volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(pa.out);
+  for (int i = lane; i < kWords; i += 32) dst[i] = src[i];
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0 && pa.reset) {
+    pk->max_r1 = pk->max_r3 = pk->max_comp = pk->max_lam = pk->max_s = pk->max_z = 0.0;
+    pk->alpha_s_min = pk->alpha_z_min = __longlong_as_double(0x7ff0000000000000ll);
+    pk->any_nonpos = 0;
+  }
+  if (lane == 0) {
+    const unsigned long long q = *pa.dev_seq + 1;
+    *pa.dev_seq = q;
+    *reinterpret_cast<volatile unsigned long long*>(pa.host_seq) = q;
+  }
+}
+
+
 inline unsigned part_blocks(int64_t m) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(kPartBlocks, ceil_div(m, kRowT)));
 }
@@ -462,9 +492,12 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, i
                                                      const double* __restrict__ part,
                                                      const double* __restrict__ hmax, Packet* pk,
                                                      int mode, const double* __restrict__ gate,
-                                                     double* __restrict__ snap) {
+                                                     double* __restrict__ snap, PubArgs pub) {
   __shared__ double sh[5 * 32];
-  if (gate && gate[2] == 0.0) return;
+  if (gate && gate[2] == 0.0) {  // (a refused speculative step: nothing but the publish)
+    if (pub.out && threadIdx.x < 32) publish_warp(pk, pub, threadIdx.x);
+    return;
+  }
   double sabs = 0.0, slog = 0.0;
   if (mode != 2)
     for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
@@ -521,6 +554,10 @@ __global__ void __launch_bounds__(kFinT) k_res_final(int64_t n, int64_t m_all, i
       snap[3] = pk->sum_log_s;
       snap[4] = pk->sum_abs_r3;
     }
+  }
+  if (pub.out) {  // the segment's publish
+    __syncthreads();
+    if (threadIdx.x < 32) publish_warp(pk, pub, threadIdx.x);
   }
 }
 
@@ -743,7 +780,7 @@ __global__ void __launch_bounds__(kFinT) k_trial_final(int64_t n, int64_t m, int
                                                        const double* __restrict__ h,
                                                        const double* __restrict__ part, Packet* pk,
                                                        const double* __restrict__ mu_p,
-                                                       double* dec, double eta) {
+                                                       double* dec, double eta, PubArgs pub) {
   __shared__ double sh[5 * 32];
   double a = 0.0, b = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -763,6 +800,10 @@ __global__ void __launch_bounds__(kFinT) k_trial_final(int64_t n, int64_t m, int
     pk->t_sum_abs = m > 0 ? su[2] : 0.0;
     pk->t_sum_log = m > 0 ? su[3] : 0.0;
     if (dec) trial0_decide(pk, m > 0, *mu_p, eta, dec);
+  }
+  if (pub.out) {  // the segment's publish
+    __syncthreads();
+    if (threadIdx.x < 32) publish_warp(pk, pub, threadIdx.x);
   }
 }
 
@@ -1077,34 +1118,19 @@ void vec_free(Ctx& c) {
   c.Mpack = nullptr;
 }
 
-// one warp: packet -> mapped host memory, then the sequence number (system-scope fence
-// between them, so a host that sees the new sequence sees the packet)
-__global__ void k_publish(const Packet* pk, Packet* out, unsigned long long* dev_seq,
-                          unsigned long long* host_seq, int reset) {
-  constexpr int kWords = sizeof(Packet) / 8;
-  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(pk);
-  volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(out);
-  for (int i = threadIdx.x; i < kWords; i += 32) dst[i] = src[i];
-  __threadfence_system();
-  __syncwarp();
-  if (threadIdx.x == 0 && reset) {  // the accumulated maxima / minima start over (host loop)
-    Packet* p = const_cast<Packet*>(pk);
-    p->max_r1 = p->max_r3 = p->max_comp = p->max_lam = p->max_s = p->max_z = 0.0;
-    p->alpha_s_min = p->alpha_z_min = __longlong_as_double(0x7ff0000000000000ll);
-    p->any_nonpos = 0;
-  }
-  if (threadIdx.x == 0) {
-    const unsigned long long q = *dev_seq + 1;
-    *dev_seq = q;
-    *reinterpret_cast<volatile unsigned long long*>(host_seq) = q;
-  }
+// one warp: the packet published on its own (publish_warp)
+__global__ void k_publish(Packet* pk, PubArgs pa) { publish_warp(pk, pa, threadIdx.x); }
+
+// the publish arguments of slot A (residual packet) or B (seg_step's packet); counts the publish
+PubArgs pub_args(Ctx& c, bool slot_b) {
+  ++c.pub_expect;
+  return PubArgs{slot_b ? c.pk_map_b : c.pk_map, c.pub_dev, c.pub_map, c.pk_autoreset ? 1 : 0};
 }
 
 unsigned long long launch_publish(Ctx& c, bool slot_b) {
-  k_publish<<<1, 32, 0, c.stream>>>(c.pk, slot_b ? c.pk_map_b : c.pk_map, c.pub_dev, c.pub_map,
-                                    c.pk_autoreset ? 1 : 0);
+  k_publish<<<1, 32, 0, c.stream>>>(c.pk, pub_args(c, slot_b));
   CMPC_LAUNCHED();
-  return ++c.pub_expect;
+  return c.pub_expect;
 }
 
 template <bool SIGNED1, bool HAS2>
@@ -1210,7 +1236,7 @@ void launch_Jtq(Ctx& c, const double* q, double* out) {
   CMPC_LAUNCHED();
 }
 
-void launch_residuals(Ctx& c, bool reuse_trial, bool gated) {
+void launch_residuals(Ctx& c, bool reuse_trial, bool gated, int publish) {
   const double* gate = gated ? c.d_alpha : nullptr;
   const unsigned pb = part_blocks(c.m);
   const int64_t m_all = rows_all(c);
@@ -1239,7 +1265,7 @@ void launch_residuals(Ctx& c, bool reuse_trial, bool gated) {
   if (c.comm) {
     // this rank's rows: J_g' lambda_g, the row sums and maxima -> allreduce -> finalize
     k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part,
-                                           c.hmax, c.pk, 1, gate, nullptr);
+                                           c.hmax, c.pk, 1, gate, nullptr, PubArgs{});
     CMPC_LAUNCHED();
     comm_group(c, true);
     comm_allreduce(c, c.Jtl, (size_t)c.n, CommType::f64, CommOp::sum);
@@ -1248,7 +1274,8 @@ void launch_residuals(Ctx& c, bool reuse_trial, bool gated) {
     comm_group(c, false);
   }
   k_res_final<<<1, kFinT, 0, c.stream>>>(c.n, m_all, np, c.Hv, c.h, c.Jtl, c.v, c.r1, c.part,
-                                         c.hmax, c.pk, c.comm ? 2 : 0, gate, c.d_alpha + 3);
+                                         c.hmax, c.pk, c.comm ? 2 : 0, gate, c.d_alpha + 3,
+                                         publish >= 0 ? pub_args(c, publish == 1) : PubArgs{});
   CMPC_LAUNCHED();
 }
 
@@ -1344,7 +1371,8 @@ void launch_recover(Ctx& c, double tau) {
   }
 }
 
-void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear, bool decide, double eta) {
+void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear, bool decide, double eta,
+                  int publish) {
   const Packet* apk = alpha_from_device ? c.pk : nullptr;
   if (!c.pk_autoreset) {  // (in the host loop, k_publish starts every segment clean)
     k_reset_packet<<<1, 1, 0, c.stream>>>(c.pk, 2);
@@ -1376,13 +1404,15 @@ void launch_trial(Ctx& c, double alpha, bool alpha_from_device, bool linear, boo
   }
   k_trial_final<<<1, kFinT, 0, c.stream>>>(c.n, c.m, c.m > 0 ? (int)pb : 0, c.vt, c.Hvt, c.h,
                                            c.part, c.pk, c.d_mu,
-                                           decide && !c.comm ? c.d_alpha : nullptr, eta);
+                                           decide && !c.comm ? c.d_alpha : nullptr, eta,
+                                           publish >= 0 && !c.comm ? pub_args(c, publish == 1) : PubArgs{});
   CMPC_LAUNCHED();
   if (c.comm) {  // merit row sums and the slack-positivity flag over every rank's rows
     comm_group(c, true);
     comm_allreduce(c, &c.pk->t_sum_log, 2, CommType::f64, CommOp::sum);
     comm_allreduce(c, &c.pk->any_nonpos, 1, CommType::i64, CommOp::max);
     comm_group(c, false);
+    if (publish >= 0) launch_publish(c, publish == 1);
   }
 }
 
