@@ -37,17 +37,7 @@ struct SmallArgs {
   long long* prof;          // debug (CMPC_SMALL_PROF): clock cycles per phase, 8 phases
 };
 
-// fixed-order CTA sum / max (every thread gets the result)
-__device__ double cta_sum(double x, double* red) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  x = warp_sum(x);
-  __syncthreads();
-  if (lane == 0) red[w] = x;
-  __syncthreads();
-  double t = 0.0;
-  for (int i = 0; i < kSmT / 32; ++i) t = add(t, red[i]);
-  return t;
-}
+// fixed-order CTA max (every thread gets the result)
 __device__ double cta_max(double x, double* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   x = warp_max(x);
