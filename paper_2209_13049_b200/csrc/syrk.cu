@@ -23,6 +23,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -48,6 +49,7 @@ constexpr int kSyrkThreads = kConsumers + 32;
 // fused condensation 297 us with these, 315 us with the weights measured without it,
 // 1 / 0.6 / 0.85 / 0.35; C4 and C5 improve too)
 constexpr double kCostFull = 1.0, kCostThin = 0.65, kCostDiag = 1.1, kCostDiagThin = 0.5;
+constexpr double kCostQ1 = 0.4, kCostQ3 = 0.85;  // off-diagonal rows 0..15 / 0..47
 
 struct SyrkArgs {
   const double* omega;
@@ -202,6 +204,68 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
   if (DIAG && a.q) a.rhs_part[(size_t)sg * 128 + threadIdx.x] = rq[0] + rq[1];
 }
 
+// Off-diagonal segments whose rows end in the first or third quarter of the tile's block row
+// (Q1: output rows 0..15, Q3: rows 0..47): R16 sixteen-row blocks x 64 columns, warp w owning
+// column groups 2w, 2w + 1 (so the four warps stay balanced); the tile's other rows are zero
+// for these prototype rows and are neither computed nor stored (k_syrk_reduce skips them)
+template <int R16>
+__device__ __forceinline__ void syrk_segment_q(const SyrkArgs& a, unsigned char* smem, uint64_t* full,
+                                               uint64_t* empty, int it0, int sg, const int4 u, int warp,
+                                               int lane) {
+  const int nsteps = (u.z - u.y) / kBK;
+  const int g = lane >> 2, t = lane & 3;
+  const int cg0 = 2 * warp;
+  double acc[R16][2][4];
+#pragma unroll
+  for (int rb = 0; rb < R16; ++rb)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[rb][b][c] = 0.0;
+  for (int it = it0; it < it0 + nsteps; ++it) {
+    const int s = it % kStages;
+    mbar_wait(&full[s], (it / kStages) & 1);
+    const uint32_t sA = smem_u32(smem + s * kStageBytes);
+    const uint32_t sB = sA + kOpBytes;
+    const uint32_t sW = sA + 2 * kOpBytes;
+#pragma unroll
+    for (int ks = 0; ks < kBK; ks += 16) {
+      double af[R16][8];
+#pragma unroll
+      for (int rb = 0; rb < R16; ++rb)
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          af[rb][x] = lds64(sA + op_off(16 * rb + g + 8 * (x & 1), ks + t + 4 * (x >> 1)));
+      double w[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) w[x] = lds64(sW + 8 * (ks + t + 4 * x));
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        double bf[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) bf[x] = w[x] * lds64(sB + op_off(8 * (cg0 + i) + g, ks + t + 4 * x));
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int rb = 0; rb < R16; ++rb) dmma1684(acc[rb][i], af[rb] + 2 * q, bf[q]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  double* out = a.partial + (size_t)sg * (kTile * kTile);
+#pragma unroll
+  for (int rb = 0; rb < R16; ++rb)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = 16 * rb + g, c = 8 * (cg0 + i) + 2 * t;
+      __stcg(out + c * kTile + r, acc[rb][i][0]);
+      __stcg(out + (c + 1) * kTile + r, acc[rb][i][1]);
+      __stcg(out + c * kTile + r + 8, acc[rb][i][2]);
+      __stcg(out + (c + 1) * kTile + r + 8, acc[rb][i][3]);
+    }
+}
+
 // 2 CTAs per SM: 168 registers (each SM sub-partition holds 3 warps of 168 x 32; the few
 // spilled values live outside the k loops)
 __global__ void __launch_bounds__(kSyrkThreads, 2)
@@ -248,7 +312,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
         for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
           const int4 u = a.segs[sg];
           const int ti = u.x & 1023, tj = (u.x >> 10) & 1023;
-          const bool thin = (u.x >> 20) & 1, diag = ti == tj;
+          const int shape = (u.x >> 20) & 3, diag = ti == tj;  // 0 full, 1 thin, 2 Q1, 3 Q3
+          const bool thin = shape == 1 || shape == 2;  // the A operand's first 32 columns suffice
           const uint32_t abytes = thin ? kOpBytes / 2 : kOpBytes;
           const bool with_q = diag && a.q != nullptr;
           const uint32_t bytes = abytes + (diag ? 0u : (uint32_t)kOpBytes) + kBK * 8 + (with_q ? kBK * 8 : 0u);
@@ -301,13 +366,19 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
     if (a.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
       const int4 u = a.segs[sg];
-      const bool thin = (u.x >> 20) & 1, diag = (u.x & 1023) == ((u.x >> 10) & 1023);
+      const int shape = (u.x >> 20) & 3;
+      const bool diag = (u.x & 1023) == ((u.x >> 10) & 1023);
       if (diag) {
-        if (thin) syrk_segment<1, true, true>(a, smem, full, empty, it0, sg, u, warp, lane);
+        if (shape == 1) syrk_segment<1, true, true>(a, smem, full, empty, it0, sg, u, warp, lane);
         else syrk_segment<3, true, false>(a, smem, full, empty, it0, sg, u, warp, lane);
+      } else if (shape == 0) {
+        syrk_segment<4, false, false>(a, smem, full, empty, it0, sg, u, warp, lane);
+      } else if (shape == 1) {
+        syrk_segment<2, false, true>(a, smem, full, empty, it0, sg, u, warp, lane);
+      } else if (shape == 2) {
+        syrk_segment_q<1>(a, smem, full, empty, it0, sg, u, warp, lane);
       } else {
-        if (thin) syrk_segment<2, false, true>(a, smem, full, empty, it0, sg, u, warp, lane);
-        else syrk_segment<4, false, false>(a, smem, full, empty, it0, sg, u, warp, lane);
+        syrk_segment_q<3>(a, smem, full, empty, it0, sg, u, warp, lane);
       }
       it0 += (u.z - u.y) / kBK;
     }
@@ -365,7 +436,7 @@ __global__ void __launch_bounds__(256)
         for (int b = 0; b < 8; ++b) {
           x[b] = 0.0;
           if (q + b < u1) {
-            const int32_t id = tile_segs[q + b] & 0x7fffffff;
+            const int32_t id = tile_segs[q + b] & 0x3fffffff;
             x[b] = __ldcg(rp + (size_t)id * 128 + t64) + __ldcg(rp + (size_t)id * 128 + 64 + t64);
           }
         }
@@ -388,7 +459,7 @@ __global__ void __launch_bounds__(256)
   const int rl = e & (kTile - 1), cl = e >> 6;
   const int64_t i = (int64_t)kTile * tl.x + rl, j = (int64_t)kTile * tl.y + cl;
   const bool live = i < n && j < n && i >= j;  // (no early exit: every thread reaches the barrier)
-  const bool lower_half = rl >= 32;
+  // a partial's valid rows: code (id bits 30-31) 0: 64, else 16 code (Q1 16, thin 32, Q3 48)
   double s = 0.0;
   if (live) {
     for (int q = u0 + 8 * way; q < u1; q += 8 * kRedWays) {
@@ -398,7 +469,8 @@ __global__ void __launch_bounds__(256)
         x[b] = 0.0;
         if (q + b < u1) {
           const int32_t id = __ldg(tile_segs + q + b);
-          if (!(id < 0 && lower_half)) x[b] = __ldcg(partial + (size_t)(id & 0x7fffffff) * (kTile * kTile) + e);
+          const int code = (int)((unsigned)id >> 30);
+          if (code == 0 || rl < 16 * code) x[b] = __ldcg(partial + (size_t)(id & 0x3fffffff) * (kTile * kTile) + e);
         }
       }
 #pragma unroll
@@ -481,27 +553,32 @@ void syrk_plan(Ctx& c) {
   };
   // jobs: per lower tile (I,J), the rows whose prefix ends in the first half of column block I
   // (THIN: only output rows 0..31 are nonzero) and the rest (FULL)
-  struct Job { int tile, ti, tj, thin, kb, ke; double w; int split; };
+  // shape: 0 full, 1 thin (output rows 0..31), 2 Q1 (rows 0..15), 3 Q3 (rows 0..47); diagonal
+  // tiles use full and thin only
+  struct Job { int tile, ti, tj, shape, kb, ke; double w; int split; };
   // step weights per segment shape (measured with tools/syrk_timeline.py)
   const double cost_f = kCostFull, cost_t = kCostThin, cost_d = kCostDiag, cost_dt = kCostDiagThin;
+  const double cost_q1 = kCostQ1, cost_q3 = kCostQ3;
   std::vector<Job> jobs;
   std::vector<int2> tiles;
   // Markov layout: the k axis of a job is a list of chunks (stage-major prototype rows are
-  // not sorted by width). Column block ti's lists: the chunks whose widest row passes
-  // 64 ti + 32 (FULL) and those ending in (64 ti, 64 ti + 32] (THIN); kb/ke index clist.
+  // not sorted by width). Column block ti's lists, in this order: the chunks whose widest row
+  // ends in (64 ti, +16] (Q1), (+16, +32] (THIN), (+32, +48] (Q3), beyond (FULL); a diagonal
+  // tile's thin job spans the first two, its full job the last two. kb/ke index clist.
   std::vector<int32_t> clist;
-  std::vector<int2> mk_full((size_t)nt), mk_thin((size_t)nt);
+  std::vector<std::array<int, 5>> mk_lists((size_t)nt);  // list boundaries per column block
   if (c.markov) {
     for (int ti = 0; ti < nt; ++ti) {
-      const int lo = kTile * ti, mid = kTile * ti + 32;
-      mk_full[size_t(ti)].x = (int)clist.size();
-      for (int ch = 0; ch < c.mk_nchunks; ++ch)
-        if (c.h_mk_width[size_t(ch)] > mid) clist.push_back(ch);
-      mk_full[size_t(ti)].y = (int)clist.size();
-      mk_thin[size_t(ti)].x = (int)clist.size();
-      for (int ch = 0; ch < c.mk_nchunks; ++ch)
-        if (c.h_mk_width[size_t(ch)] > lo && c.h_mk_width[size_t(ch)] <= mid) clist.push_back(ch);
-      mk_thin[size_t(ti)].y = (int)clist.size();
+      const int lo = kTile * ti;
+      const int edge[5] = {lo, lo + 16, lo + 32, lo + 48, 1 << 30};
+      mk_lists[size_t(ti)][0] = (int)clist.size();
+      for (int q = 0; q < 4; ++q) {
+        for (int ch = 0; ch < c.mk_nchunks; ++ch) {
+          const int w = c.h_mk_width[size_t(ch)];
+          if (w > edge[q] && w <= edge[q + 1]) clist.push_back(ch);
+        }
+        mk_lists[size_t(ti)][size_t(q + 1)] = (int)clist.size();
+      }
     }
   }
   for (int tj = 0; tj < nt; ++tj)
@@ -509,15 +586,24 @@ void syrk_plan(Ctx& c) {
       const int tile = (int)tiles.size();
       tiles.push_back({ti, tj});
       const bool dg = ti == tj;
+      // the job boundaries along k: rows ending in (lo, lo+16], (+16, +32], (+32, +48], beyond
+      int b[5];
       if (c.markov) {
-        const int2 th = mk_thin[size_t(ti)], fu = mk_full[size_t(ti)];
-        if (th.y > th.x) jobs.push_back({tile, ti, tj, 1, th.x * kBK, th.y * kBK, dg ? cost_dt : cost_t, 0});
-        if (fu.y > fu.x) jobs.push_back({tile, ti, tj, 0, fu.x * kBK, fu.y * kBK, dg ? cost_d : cost_f, 0});
-        continue;
+        for (int q = 0; q < 5; ++q) b[q] = mk_lists[size_t(ti)][size_t(q)] * kBK;
+      } else {
+        b[0] = kstart((int64_t)kTile * ti);
+        for (int q = 1; q < 4; ++q) b[q] = std::max(b[q - 1], kstart((int64_t)kTile * ti + 16 * q));
+        b[4] = std::max(b[3], k_end);
       }
-      const int a0 = kstart((int64_t)kTile * ti), a1 = std::max(a0, kstart((int64_t)kTile * ti + 32));
-      if (a1 > a0) jobs.push_back({tile, ti, tj, 1, a0, a1, dg ? cost_dt : cost_t, 0});
-      if (k_end > a1) jobs.push_back({tile, ti, tj, 0, a1, k_end, dg ? cost_d : cost_f, 0});
+      if (dg) {
+        if (b[2] > b[0]) jobs.push_back({tile, ti, tj, 1, b[0], b[2], cost_dt, 0});
+        if (b[4] > b[2]) jobs.push_back({tile, ti, tj, 0, b[2], b[4], cost_d, 0});
+      } else {
+        if (b[1] > b[0]) jobs.push_back({tile, ti, tj, 2, b[0], b[1], cost_q1, 0});
+        if (b[2] > b[1]) jobs.push_back({tile, ti, tj, 1, b[1], b[2], cost_t, 0});
+        if (b[3] > b[2]) jobs.push_back({tile, ti, tj, 3, b[2], b[3], cost_q3, 0});
+        if (b[4] > b[3]) jobs.push_back({tile, ti, tj, 0, b[3], b[4], cost_f, 0});
+      }
     }
   // k step of a job position: the prototype row step, or (Markov) the chunk id
   auto step_of = [&](int pos) { return c.markov ? clist[size_t(pos)] : pos; };
@@ -565,8 +651,10 @@ void syrk_plan(Ctx& c) {
   std::vector<std::vector<int32_t>> per_tile(tiles.size());
   auto emit = [&](const Job& jb, int a, int b) {
     const int id = (int)segs.size();
-    per_tile[size_t(jb.tile)].push_back(jb.thin ? (id | int(0x80000000u)) : id);
-    segs.push_back({jb.ti | jb.tj << 10 | jb.thin << 20, a * kBK, b * kBK, jb.tile});
+    // k_syrk_reduce's row code (bits 30-31): valid rows 16 x code, 0 = all 64
+    static constexpr unsigned kCode[4] = {0u, 2u, 1u, 3u};
+    per_tile[size_t(jb.tile)].push_back((int32_t)((unsigned)id | (kCode[jb.shape] << 30)));
+    segs.push_back({jb.ti | jb.tj << 10 | jb.shape << 20, a * kBK, b * kBK, jb.tile});
   };
   auto close_piece = [&]() {
     if (pptr.back() != (int32_t)segs.size()) pptr.push_back((int32_t)segs.size());
@@ -614,7 +702,7 @@ void syrk_plan(Ctx& c) {
   for (int p = 0; p < npieces; ++p)
     for (int q = pptr[size_t(p)]; q < pptr[size_t(p) + 1]; ++q) {
       const int4 u = segs[size_t(q)];
-      const int thin = (u.x >> 20) & 1, dg = (u.x & 1023) == ((u.x >> 10) & 1023);
+      const int thin = ((u.x >> 20) & 3) != 0 ? 1 : 0, dg = (u.x & 1023) == ((u.x >> 10) & 1023);
       c.syrk_cta_cost[size_t(5 * p)] += 1.0;
       c.syrk_cta_cost[size_t(5 * p + 1 + thin + 2 * dg)] += double(u.z - u.y) / kBK;
     }
