@@ -131,12 +131,12 @@ struct Ctx {
 
   // SYRK work decomposition (syrk.cu): segments (a k range of one tile) grouped in pieces
   int nunits = 0, ntiles = 0, nctas = 0, npieces = 0;
-  int4* units = nullptr;          // segments {tile_i | tile_j << 10 | thin << 20, k0, k1, tile}
+  int4* units = nullptr;          // segments {tile_i | tile_j << 10 | shape << 20, k0, k1, tile}
   int32_t* cta_ptr = nullptr;     // npieces+1 into units
   unsigned* syrk_ctl = nullptr;   // piece counter, retired CTAs, reduction item counter, per-tile done counts
   int2* tiles = nullptr;          // ntiles {ti, tj}
   int32_t* tile_ptr = nullptr;    // ntiles+1 into tile_units
-  int32_t* tile_units = nullptr;  // segment ids per tile in k order (| 1 << 31: thin, rows 0..31 only)
+  int32_t* tile_units = nullptr;  // segment ids per tile in k order (bits 30-31: valid rows 16 x code, 0 = 64)
   double* partial = nullptr;      // nunits x 64 x 64
   double* rhs_part = nullptr;     // nunits x 128: fused P' q half-sums of the diagonal segments
   long long* syrk_prof = nullptr; // debug timeline: {start ns, end ns, smid} per piece (null: off)

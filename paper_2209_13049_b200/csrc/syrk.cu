@@ -12,9 +12,10 @@
 // * math: mma.sync m16n8k16 f64 (DMMA.8x8x4), 4 consumer warps per 64x64 tile, each owning
 //   an equal share of the tile's useful 16x8 fragments.
 // * zero-block skipping: rows are sorted by nonzero prefix width; tile (I,J) (I>=J) only
-//   visits the rows whose prefix reaches column 64*I, and the rows whose prefix ends in the
-//   first half of block I run as THIN segments (output rows 0..31 only, A operand 32
-//   columns): the executed DMMA work is 1.22x the algorithmic count at config 3, not 1.35x.
+//   visits the rows whose prefix reaches column 64*I, and the rows whose prefix ends inside
+//   block I only compute the output rows they can reach: off-diagonal segments in 16-row
+//   steps (Q1: rows 0..15, THIN: 0..31, Q3: 0..47, FULL; Q1/THIN need only the A operand's
+//   first 32 columns), diagonal ones THIN or FULL.
 // * scheduling: one persistent CTA pair per SM grabs PIECES from an atomic counter: first one
 //   equal-cost body piece each, then tail pieces of decreasing cost so the CTAs finish
 //   together; a piece holds one or more SEGMENTS (a k range of one tile).
@@ -53,7 +54,7 @@ constexpr double kCostQ1 = 0.4, kCostQ3 = 0.85;  // off-diagonal rows 0..15 / 0.
 
 struct SyrkArgs {
   const double* omega;
-  const int4* segs;          // {ti | tj << 10 | thin << 20, k0, k1, tile index}
+  const int4* segs;          // {ti | tj << 10 | shape << 20, k0, k1, tile index}
   const int32_t* piece_ptr;  // npieces + 1 into segs
   int npieces;
   unsigned* ctl;             // [0] next piece, [1] retired CTAs (both 0 between launches)
