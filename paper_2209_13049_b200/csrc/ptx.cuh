@@ -79,6 +79,12 @@ __device__ __forceinline__ void dmma16816(double* d, const double* a, const doub
         "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 // D(16x8) += A(16x4) B(4x8)
+__device__ __forceinline__ void dmma884(double* d, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ void dmma1684(double* d, const double* a, double b) {
   asm volatile(
       "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "

@@ -13,9 +13,9 @@
 //   an equal share of the tile's useful 16x8 fragments.
 // * zero-block skipping: rows are sorted by nonzero prefix width; tile (I,J) (I>=J) only
 //   visits the rows whose prefix reaches column 64*I, and the rows whose prefix ends inside
-//   block I only compute the output rows they can reach: off-diagonal segments in 16-row
-//   steps (Q1: rows 0..15, THIN: 0..31, Q3: 0..47, FULL; Q1/THIN need only the A operand's
-//   first 32 columns), diagonal ones THIN or FULL.
+//   block I only compute the output rows they can reach: off-diagonal segments in 8-row
+//   steps (rows 0..8q-1, q = 1..8; up to 32 rows only the A operand's first 32 columns are
+//   loaded), diagonal ones THIN (rows 0..31) or FULL.
 // * scheduling: one persistent CTA pair per SM grabs PIECES from an atomic counter: first one
 //   equal-cost body piece each, then tail pieces of decreasing cost so the CTAs finish
 //   together; a piece holds one or more SEGMENTS (a k range of one tile).
@@ -49,8 +49,10 @@ constexpr int kSyrkThreads = kConsumers + 32;
 // of the fused right-hand side P'q (swept with CMPC_SYRK_COST and tools/phases.py: at C3 the
 // fused condensation 297 us with these, 315 us with the weights measured without it,
 // 1 / 0.6 / 0.85 / 0.35; C4 and C5 improve too)
-constexpr double kCostFull = 1.0, kCostThin = 0.65, kCostDiag = 1.1, kCostDiagThin = 0.5;
-constexpr double kCostQ1 = 0.4, kCostQ3 = 0.85;  // off-diagonal rows 0..15 / 0..47
+constexpr double kCostDiag = 1.1, kCostDiagThin = 0.5;
+// off-diagonal segments by output rows / 8 (index 1..8): 16 rows 0.4, 32 rows 0.65 (THIN),
+// 48 rows 0.85, 64 rows 1.0 (FULL) as measured; the 8-row steps interpolated
+constexpr double kCostRows[9] = {0.0, 0.25, 0.4, 0.55, 0.65, 0.75, 0.85, 0.93, 1.0};
 
 struct SyrkArgs {
   const double* omega;
@@ -205,24 +207,27 @@ __device__ __forceinline__ void syrk_segment(const SyrkArgs& a, unsigned char* s
   if (DIAG && a.q) a.rhs_part[(size_t)sg * 128 + threadIdx.x] = rq[0] + rq[1];
 }
 
-// Off-diagonal segments whose rows end in the first or third quarter of the tile's block row
-// (Q1: output rows 0..15, Q3: rows 0..47): R16 sixteen-row blocks x 64 columns, warp w owning
-// column groups 2w, 2w + 1 (so the four warps stay balanced); the tile's other rows are zero
-// for these prototype rows and are neither computed nor stored (k_syrk_reduce skips them)
-template <int R16>
+// Off-diagonal segments whose rows end inside the tile's block row at a row count that is not
+// 32 or 64: 16 R16 (+ 8 with HALF) output rows x 64 columns, warp w owning column groups 2w, 2w + 1
+// (so the four warps stay balanced; the 8-row block runs on m8n8k4); the tile's other rows are
+// zero for these prototype rows and are neither computed nor stored (k_syrk_reduce skips them)
+template <int R16, bool HALF>
 __device__ __forceinline__ void syrk_segment_q(const SyrkArgs& a, unsigned char* smem, uint64_t* full,
                                                uint64_t* empty, int it0, int sg, const int4 u, int warp,
                                                int lane) {
+  constexpr int RA = R16 > 0 ? R16 : 1;  // (array extent; R16 = 0 uses only the 8-row block)
   const int nsteps = (u.z - u.y) / kBK;
   const int g = lane >> 2, t = lane & 3;
   const int cg0 = 2 * warp;
-  double acc[R16][2][4];
+  double acc[RA][2][4], acc8[2][2];
 #pragma unroll
-  for (int rb = 0; rb < R16; ++rb)
+  for (int rb = 0; rb < RA; ++rb)
 #pragma unroll
     for (int b = 0; b < 2; ++b)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[rb][b][c] = 0.0;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) acc8[b][0] = acc8[b][1] = 0.0;
   for (int it = it0; it < it0 + nsteps; ++it) {
     const int s = it % kStages;
     mbar_wait(&full[s], (it / kStages) & 1);
@@ -231,12 +236,15 @@ __device__ __forceinline__ void syrk_segment_q(const SyrkArgs& a, unsigned char*
     const uint32_t sW = sA + 2 * kOpBytes;
 #pragma unroll
     for (int ks = 0; ks < kBK; ks += 16) {
-      double af[R16][8];
+      double af[RA][8], a8[4];
 #pragma unroll
       for (int rb = 0; rb < R16; ++rb)
 #pragma unroll
         for (int x = 0; x < 8; ++x)
           af[rb][x] = lds64(sA + op_off(16 * rb + g + 8 * (x & 1), ks + t + 4 * (x >> 1)));
+      if (HALF)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a8[q] = lds64(sA + op_off(16 * R16 + g, ks + t + 4 * q));
       double w[4];
 #pragma unroll
       for (int x = 0; x < 4; ++x) w[x] = lds64(sW + 8 * (ks + t + 4 * x));
@@ -246,9 +254,11 @@ __device__ __forceinline__ void syrk_segment_q(const SyrkArgs& a, unsigned char*
 #pragma unroll
         for (int x = 0; x < 4; ++x) bf[x] = w[x] * lds64(sB + op_off(8 * (cg0 + i) + g, ks + t + 4 * x));
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < 4; ++q) {
 #pragma unroll
           for (int rb = 0; rb < R16; ++rb) dmma1684(acc[rb][i], af[rb] + 2 * q, bf[q]);
+          if (HALF) dmma884(acc8[i], a8[q], bf[q]);
+        }
       }
     }
     __syncwarp();
@@ -256,15 +266,22 @@ __device__ __forceinline__ void syrk_segment_q(const SyrkArgs& a, unsigned char*
   }
   double* out = a.partial + (size_t)sg * (kTile * kTile);
 #pragma unroll
-  for (int rb = 0; rb < R16; ++rb)
+  for (int i = 0; i < 2; ++i) {
+    const int c = 8 * (cg0 + i) + 2 * t;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int r = 16 * rb + g, c = 8 * (cg0 + i) + 2 * t;
+    for (int rb = 0; rb < R16; ++rb) {
+      const int r = 16 * rb + g;
       __stcg(out + c * kTile + r, acc[rb][i][0]);
       __stcg(out + (c + 1) * kTile + r, acc[rb][i][1]);
       __stcg(out + c * kTile + r + 8, acc[rb][i][2]);
       __stcg(out + (c + 1) * kTile + r + 8, acc[rb][i][3]);
     }
+    if (HALF) {
+      const int r = 16 * R16 + g;
+      __stcg(out + c * kTile + r, acc8[i][0]);
+      __stcg(out + (c + 1) * kTile + r, acc8[i][1]);
+    }
+  }
 }
 
 // 2 CTAs per SM: 168 registers (each SM sub-partition holds 3 warps of 168 x 32; the few
@@ -313,8 +330,8 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
         for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
           const int4 u = a.segs[sg];
           const int ti = u.x & 1023, tj = (u.x >> 10) & 1023;
-          const int shape = (u.x >> 20) & 3, diag = ti == tj;  // 0 full, 1 thin, 2 Q1, 3 Q3
-          const bool thin = shape == 1 || shape == 2;  // the A operand's first 32 columns suffice
+          const int shape = (u.x >> 20) & 15, diag = ti == tj;  // output rows / 8 (1..8)
+          const bool thin = shape <= 4;  // the A operand's first 32 columns suffice
           const uint32_t abytes = thin ? kOpBytes / 2 : kOpBytes;
           const bool with_q = diag && a.q != nullptr;
           const uint32_t bytes = abytes + (diag ? 0u : (uint32_t)kOpBytes) + kBK * 8 + (with_q ? kBK * 8 : 0u);
@@ -367,19 +384,22 @@ __global__ void __launch_bounds__(kSyrkThreads, 2)
     if (a.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     for (int sg = a.piece_ptr[p]; sg < a.piece_ptr[p + 1]; ++sg) {
       const int4 u = a.segs[sg];
-      const int shape = (u.x >> 20) & 3;
+      const int shape = (u.x >> 20) & 15;  // output rows / 8
       const bool diag = (u.x & 1023) == ((u.x >> 10) & 1023);
       if (diag) {
-        if (shape == 1) syrk_segment<1, true, true>(a, smem, full, empty, it0, sg, u, warp, lane);
+        if (shape == 4) syrk_segment<1, true, true>(a, smem, full, empty, it0, sg, u, warp, lane);
         else syrk_segment<3, true, false>(a, smem, full, empty, it0, sg, u, warp, lane);
-      } else if (shape == 0) {
-        syrk_segment<4, false, false>(a, smem, full, empty, it0, sg, u, warp, lane);
-      } else if (shape == 1) {
-        syrk_segment<2, false, true>(a, smem, full, empty, it0, sg, u, warp, lane);
-      } else if (shape == 2) {
-        syrk_segment_q<1>(a, smem, full, empty, it0, sg, u, warp, lane);
       } else {
-        syrk_segment_q<3>(a, smem, full, empty, it0, sg, u, warp, lane);
+        switch (shape) {
+          case 1: syrk_segment_q<0, true>(a, smem, full, empty, it0, sg, u, warp, lane); break;
+          case 2: syrk_segment_q<1, false>(a, smem, full, empty, it0, sg, u, warp, lane); break;
+          case 3: syrk_segment_q<1, true>(a, smem, full, empty, it0, sg, u, warp, lane); break;
+          case 4: syrk_segment<2, false, true>(a, smem, full, empty, it0, sg, u, warp, lane); break;
+          case 5: syrk_segment_q<2, true>(a, smem, full, empty, it0, sg, u, warp, lane); break;
+          case 6: syrk_segment_q<3, false>(a, smem, full, empty, it0, sg, u, warp, lane); break;
+          case 7: syrk_segment_q<3, true>(a, smem, full, empty, it0, sg, u, warp, lane); break;
+          default: syrk_segment<4, false, false>(a, smem, full, empty, it0, sg, u, warp, lane); break;
+        }
       }
       it0 += (u.z - u.y) / kBK;
     }
@@ -437,7 +457,7 @@ __global__ void __launch_bounds__(256)
         for (int b = 0; b < 8; ++b) {
           x[b] = 0.0;
           if (q + b < u1) {
-            const int32_t id = tile_segs[q + b] & 0x3fffffff;
+            const int32_t id = tile_segs[q + b] & 0x0fffffff;
             x[b] = __ldcg(rp + (size_t)id * 128 + t64) + __ldcg(rp + (size_t)id * 128 + 64 + t64);
           }
         }
@@ -460,7 +480,7 @@ __global__ void __launch_bounds__(256)
   const int rl = e & (kTile - 1), cl = e >> 6;
   const int64_t i = (int64_t)kTile * tl.x + rl, j = (int64_t)kTile * tl.y + cl;
   const bool live = i < n && j < n && i >= j;  // (no early exit: every thread reaches the barrier)
-  // a partial's valid rows: code (id bits 30-31) 0: 64, else 16 code (Q1 16, thin 32, Q3 48)
+  // a partial's valid rows: 8 x code (id bits 28-31)
   double s = 0.0;
   if (live) {
     for (int q = u0 + 8 * way; q < u1; q += 8 * kRedWays) {
@@ -470,8 +490,8 @@ __global__ void __launch_bounds__(256)
         x[b] = 0.0;
         if (q + b < u1) {
           const int32_t id = __ldg(tile_segs + q + b);
-          const int code = (int)((unsigned)id >> 30);
-          if (code == 0 || rl < 16 * code) x[b] = __ldcg(partial + (size_t)(id & 0x3fffffff) * (kTile * kTile) + e);
+          const int code = (int)((unsigned)id >> 28);
+          if (rl < 8 * code) x[b] = __ldcg(partial + (size_t)(id & 0x0fffffff) * (kTile * kTile) + e);
         }
       }
 #pragma unroll
@@ -554,31 +574,30 @@ void syrk_plan(Ctx& c) {
   };
   // jobs: per lower tile (I,J), the rows whose prefix ends in the first half of column block I
   // (THIN: only output rows 0..31 are nonzero) and the rest (FULL)
-  // shape: 0 full, 1 thin (output rows 0..31), 2 Q1 (rows 0..15), 3 Q3 (rows 0..47); diagonal
-  // tiles use full and thin only
+  // shape = the output rows a segment computes / 8 (1..8): off-diagonal tiles in 8-row steps,
+  // diagonal tiles 4 (rows 0..31) or 8
   struct Job { int tile, ti, tj, shape, kb, ke; double w; int split; };
-  // step weights per segment shape (measured with tools/syrk_timeline.py)
-  const double cost_f = kCostFull, cost_t = kCostThin, cost_d = kCostDiag, cost_dt = kCostDiagThin;
-  const double cost_q1 = kCostQ1, cost_q3 = kCostQ3;
+  // step weights per segment shape (measured with tools/syrk_timeline.py and the bench)
+  const double cost_d = kCostDiag, cost_dt = kCostDiagThin;
   std::vector<Job> jobs;
   std::vector<int2> tiles;
   // Markov layout: the k axis of a job is a list of chunks (stage-major prototype rows are
-  // not sorted by width). Column block ti's lists, in this order: the chunks whose widest row
-  // ends in (64 ti, +16] (Q1), (+16, +32] (THIN), (+32, +48] (Q3), beyond (FULL); a diagonal
-  // tile's thin job spans the first two, its full job the last two. kb/ke index clist.
+  // not sorted by width). Column block ti's lists, in order: the chunks whose widest row ends
+  // in (64 ti + 8 (q - 1), 64 ti + 8 q], q = 1..8 (the last list: everything beyond); a
+  // diagonal tile's thin job spans the first four, its full job the rest. kb/ke index clist.
   std::vector<int32_t> clist;
-  std::vector<std::array<int, 5>> mk_lists((size_t)nt);  // list boundaries per column block
+  std::vector<std::array<int, 9>> mk_lists((size_t)nt);  // list boundaries per column block
   if (c.markov) {
     for (int ti = 0; ti < nt; ++ti) {
       const int lo = kTile * ti;
-      const int edge[5] = {lo, lo + 16, lo + 32, lo + 48, 1 << 30};
       mk_lists[size_t(ti)][0] = (int)clist.size();
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 1; q <= 8; ++q) {
+        const int e0 = lo + 8 * (q - 1), e1 = q == 8 ? (1 << 30) : lo + 8 * q;
         for (int ch = 0; ch < c.mk_nchunks; ++ch) {
           const int w = c.h_mk_width[size_t(ch)];
-          if (w > edge[q] && w <= edge[q + 1]) clist.push_back(ch);
+          if (w > e0 && w <= e1) clist.push_back(ch);
         }
-        mk_lists[size_t(ti)][size_t(q + 1)] = (int)clist.size();
+        mk_lists[size_t(ti)][size_t(q)] = (int)clist.size();
       }
     }
   }
@@ -587,23 +606,21 @@ void syrk_plan(Ctx& c) {
       const int tile = (int)tiles.size();
       tiles.push_back({ti, tj});
       const bool dg = ti == tj;
-      // the job boundaries along k: rows ending in (lo, lo+16], (+16, +32], (+32, +48], beyond
-      int b[5];
+      // the job boundaries along k: rows ending in (lo + 8 (q-1), lo + 8 q], q = 1..8
+      int b[9];
       if (c.markov) {
-        for (int q = 0; q < 5; ++q) b[q] = mk_lists[size_t(ti)][size_t(q)] * kBK;
+        for (int q = 0; q < 9; ++q) b[q] = mk_lists[size_t(ti)][size_t(q)] * kBK;
       } else {
         b[0] = kstart((int64_t)kTile * ti);
-        for (int q = 1; q < 4; ++q) b[q] = std::max(b[q - 1], kstart((int64_t)kTile * ti + 16 * q));
-        b[4] = std::max(b[3], k_end);
+        for (int q = 1; q < 8; ++q) b[q] = std::max(b[q - 1], kstart((int64_t)kTile * ti + 8 * q));
+        b[8] = std::max(b[7], k_end);
       }
       if (dg) {
-        if (b[2] > b[0]) jobs.push_back({tile, ti, tj, 1, b[0], b[2], cost_dt, 0});
-        if (b[4] > b[2]) jobs.push_back({tile, ti, tj, 0, b[2], b[4], cost_d, 0});
+        if (b[4] > b[0]) jobs.push_back({tile, ti, tj, 4, b[0], b[4], cost_dt, 0});
+        if (b[8] > b[4]) jobs.push_back({tile, ti, tj, 8, b[4], b[8], cost_d, 0});
       } else {
-        if (b[1] > b[0]) jobs.push_back({tile, ti, tj, 2, b[0], b[1], cost_q1, 0});
-        if (b[2] > b[1]) jobs.push_back({tile, ti, tj, 1, b[1], b[2], cost_t, 0});
-        if (b[3] > b[2]) jobs.push_back({tile, ti, tj, 3, b[2], b[3], cost_q3, 0});
-        if (b[4] > b[3]) jobs.push_back({tile, ti, tj, 0, b[3], b[4], cost_f, 0});
+        for (int q = 1; q <= 8; ++q)
+          if (b[q] > b[q - 1]) jobs.push_back({tile, ti, tj, q, b[q - 1], b[q], kCostRows[q], 0});
       }
     }
   // k step of a job position: the prototype row step, or (Markov) the chunk id
@@ -652,9 +669,8 @@ void syrk_plan(Ctx& c) {
   std::vector<std::vector<int32_t>> per_tile(tiles.size());
   auto emit = [&](const Job& jb, int a, int b) {
     const int id = (int)segs.size();
-    // k_syrk_reduce's row code (bits 30-31): valid rows 16 x code, 0 = all 64
-    static constexpr unsigned kCode[4] = {0u, 2u, 1u, 3u};
-    per_tile[size_t(jb.tile)].push_back((int32_t)((unsigned)id | (kCode[jb.shape] << 30)));
+    // k_syrk_reduce's row code (bits 28-31): valid rows 8 x code
+    per_tile[size_t(jb.tile)].push_back((int32_t)((unsigned)id | ((unsigned)jb.shape << 28)));
     segs.push_back({jb.ti | jb.tj << 10 | jb.shape << 20, a * kBK, b * kBK, jb.tile});
   };
   auto close_piece = [&]() {
@@ -703,7 +719,7 @@ void syrk_plan(Ctx& c) {
   for (int p = 0; p < npieces; ++p)
     for (int q = pptr[size_t(p)]; q < pptr[size_t(p) + 1]; ++q) {
       const int4 u = segs[size_t(q)];
-      const int thin = ((u.x >> 20) & 3) != 0 ? 1 : 0, dg = (u.x & 1023) == ((u.x >> 10) & 1023);
+      const int thin = ((u.x >> 20) & 15) < 8 ? 1 : 0, dg = (u.x & 1023) == ((u.x >> 10) & 1023);
       c.syrk_cta_cost[size_t(5 * p)] += 1.0;
       c.syrk_cta_cost[size_t(5 * p + 1 + thin + 2 * dg)] += double(u.z - u.y) / kBK;
     }
